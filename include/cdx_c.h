@@ -1,0 +1,268 @@
+/*
+ * cdx_c.h — C-ABI of the B200-native Certaindex hot path (libcdx.so).
+ *
+ * Plain pointers and sizes only; no C++ or torch types cross this boundary.  Every entry
+ * point is the batched replacement of a scalar routine of the reference library
+ * (proj/include/cdx/*.hpp, CPU, one program at a time); the comment above each one
+ * cites the reference interface it replaces.  The reference has no scheduler code: the
+ * scheduler rows restate SPEC.md:385-486.
+ *
+ * Conventions
+ *   - All array arguments of the compute entry points are DEVICE pointers owned by the
+ *     caller (cudaMalloc / torch tensors).  The cdx_*_host entry points take HOST
+ *     pointers and stream them through the device themselves.
+ *   - Calls are asynchronous on the context stream; cdx_sync() waits and reports
+ *     device-side validation errors (e.g. a reward outside [0,1]).
+ *   - Status codes map 1:1 onto the reference's exception types:
+ *       CDX_EINVAL   <-> std::invalid_argument     CDX_ERUNTIME <-> std::runtime_error
+ *       CDX_ERANGE   <-> std::out_of_range         CDX_ELOGIC   <-> std::logic_error
+ *     cdx_last_error() returns the reference's message text for the failure.
+ *   - There is no CPU fallback: without a usable sm_100 device every call returns
+ *     CDX_ECUDA.
+ */
+#ifndef CDX_C_H
+#define CDX_C_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define CDX_ABI_VERSION 1
+
+typedef enum {
+    CDX_OK = 0,
+    CDX_EINVAL = 1,
+    CDX_ERUNTIME = 2,
+    CDX_ERANGE = 3,
+    CDX_ELOGIC = 4,
+    CDX_ECUDA = 5,
+    CDX_ENCCL = 6
+} cdx_status;
+
+/* metrics.hpp:85 SignalKind (same ordinals) */
+enum { CDX_SIG_ENTROPY = 0, CDX_SIG_REWARD = 1, CDX_SIG_MEAN_LEN = 2, CDX_SIG_LOGPROB = 3 };
+/* metrics.hpp:105 ThresholdDir */
+enum { CDX_DIR_GE = 0, CDX_DIR_LE = 1 };
+/* metrics.hpp:72 RewardAggregation */
+enum { CDX_AGG_MEAN = 0, CDX_AGG_MAX = 1 };
+/* probe.hpp:52 ExitDecision; also the `reason` byte of the batched outputs */
+enum { CDX_EXIT_CONTINUE = 0, CDX_EXIT_CERTAIN = 1, CDX_EXIT_BUDGET = 2 };
+/* runtime.hpp:32 Archetype */
+enum { CDX_ARCH_SC = 0, CDX_ARCH_REBASE = 1, CDX_ARCH_MCTS = 2, CDX_ARCH_COT = 3 };
+/* SPEC.md:391 AllocationPolicy.kind */
+enum {
+    CDX_POL_EVEN = 0,
+    CDX_POL_LENGTH_PROXY = 1,
+    CDX_POL_STATIC_THRESHOLD = 2,
+    CDX_POL_INITIAL_CURVE_FIT = 3,
+    CDX_POL_K_STEP_THRESHOLD = 4,
+    CDX_POL_DYNAMIC_CURVE_FIT = 5
+};
+/* SPEC.md:395 InterSchedPolicy.order */
+enum { CDX_ORDER_FIFO = 0, CDX_ORDER_SJF = 1, CDX_ORDER_LPM = 2 };
+
+/* metrics.hpp:107-112 SignalThreshold */
+typedef struct {
+    uint8_t signal; /* CDX_SIG_* */
+    uint8_t dir;    /* CDX_DIR_* */
+    uint8_t _pad[6];
+    double cutoff;
+} cdx_threshold;
+
+/* SPEC.md:390-393 AllocationPolicy (batched subset: even / static / k-step threshold) */
+typedef struct {
+    uint8_t kind; /* CDX_POL_EVEN | CDX_POL_STATIC_THRESHOLD | CDX_POL_K_STEP_THRESHOLD */
+    uint8_t _pad[3];
+    int32_t detect_at;       /* detect_at_knob, 1-based knob unit (<= resource_cap) */
+    int32_t recheck_every;   /* k_step_threshold: re-test every this many units (>= 1) */
+    int32_t resource_cap;    /* knob units, <= probes per request */
+    int64_t tokens_per_unit; /* token budget of one knob unit (interval_tokens * samples) */
+} cdx_alloc_policy;
+
+/* probe.hpp:25-33 ProbeConfig (markers travel separately, see cdx_canon_intern) */
+typedef struct {
+    int32_t interval_tokens;
+    int32_t window;
+    double threshold;
+    int64_t max_tokens;
+} cdx_probe_cfg;
+
+/* SPEC.md:394-397 InterSchedPolicy */
+typedef struct {
+    uint8_t gang;  /* requests grouped by program (always 1 for the program-level order) */
+    uint8_t order; /* CDX_ORDER_FIFO | CDX_ORDER_SJF */
+    uint8_t _pad[6];
+    double starvation_limit; /* > 0 */
+    double prior_tokens;     /* estimate_iteration_tokens prior */
+} cdx_inter_policy;
+
+/* Per-program scheduler state, structure of arrays (device pointers).
+ * runtime.hpp:123-133 ReasoningProgram + runtime.hpp:191-192 iteration_tokens(). */
+typedef struct {
+    const double* arrival;        /* program arrival time */
+    const double* last_service;   /* last time the program was serviced */
+    const int64_t* iter_tok_sum;  /* sum of completed iteration token counts */
+    const uint32_t* iter_count;   /* number of completed iterations */
+    const uint16_t* knob;         /* units granted so far */
+    const uint16_t* cap;          /* resource cap */
+    const uint8_t* terminated;    /* nonzero: dropped from the order */
+    uint32_t id_base;             /* program id = id_base + index */
+    uint32_t _pad;
+} cdx_prog_soa;
+
+/* Synthetic trace parameters (counter-based restatement of runtime.hpp:45-69 and
+ * runtime.cpp:91-117).  Answer ids: 0 = the stationary
+ * answer "S", 1..M-1 = distractors "D1".."D{M-1}", M+a = the hesitant form "wait, "+name(a). */
+typedef struct {
+    uint64_t seed;
+    uint32_t groups;            /* M >= 2 */
+    uint32_t conv_lo, conv_hi;  /* convergence knob ~ U{lo..hi} */
+    uint32_t _pad;
+    double noise_level;         /* before convergence */
+    double residual_noise;      /* from convergence on */
+    double solvable_fraction;
+    double hesitation_prob;     /* CoT */
+    uint32_t reward_start_k;    /* reward model means in units of 2^-24 */
+    uint32_t reward_final_k;
+    uint32_t reward_unsolvable_k;
+    uint32_t reward_jitter_k;   /* uniform jitter half-width */
+} cdx_gen_params;
+
+typedef struct cdx_ctx cdx_ctx;
+
+/* ---- context ----------------------------------------------------------------------- */
+int cdx_ctx_create(int device, cdx_ctx** out);
+int cdx_ctx_destroy(cdx_ctx* ctx);
+/* Run subsequent calls on this cudaStream_t (NULL = the device's legacy default stream).
+ * A new context runs on its own non-blocking stream; cdx_ctx_use_own_stream restores it. */
+int cdx_ctx_set_stream(cdx_ctx* ctx, void* cuda_stream);
+int cdx_ctx_use_own_stream(cdx_ctx* ctx);
+void* cdx_ctx_stream(cdx_ctx* ctx);
+int cdx_sync(cdx_ctx* ctx);
+const char* cdx_last_error(const cdx_ctx* ctx);
+int cdx_abi_version(void);
+/* Number of kernel launches this context has issued (the bench's gpu_launches count). */
+uint64_t cdx_launch_count(const cdx_ctx* ctx);
+
+/* ---- synthetic trace generation on the device (runtime.cpp:91-117 restated) ------- */
+int cdx_gen_sc(cdx_ctx* ctx, const cdx_gen_params* g, uint64_t r0, uint64_t R, uint32_t P,
+               uint32_t S, uint32_t* ids);
+int cdx_gen_cot(cdx_ctx* ctx, const cdx_gen_params* g, uint64_t r0, uint64_t R, uint32_t P,
+                uint32_t* ids, uint64_t* hes);
+int cdx_gen_reward(cdx_ctx* ctx, const cdx_gen_params* g, uint64_t g0, uint64_t G, uint32_t T,
+                   uint32_t W, float* rewards, uint32_t* ids);
+
+/* ---- K2: Self-Consistency certaindex ------------------------------------------------
+ * Replaces, per (request r, probe p) row of S sampled answers,
+ *   metrics::certaindex_entropy(metrics::cluster_exact(row))        metrics.hpp:44,66
+ *   metrics::combined_meets_thresholds({H~}, thresholds)            metrics.hpp:116
+ * ids: u32[R][P][S] interned answer ids (equal id <=> equal trimmed bytes).
+ * hcert: f32[R][P] (nullable).  meets_bits: u32[R][ceil(P/32)], bit p%32 of word p/32.
+ * Decisions are taken on the FP64 certaindex; hcert is its fp32 rounding.               */
+int cdx_sc_certaindex(cdx_ctx* ctx, const uint32_t* ids, uint64_t R, uint32_t P, uint32_t S,
+                      const cdx_threshold* th, uint32_t n_th, float* hcert, uint32_t* meets_bits);
+
+/* Per-row clusters in first-seen order (the full metrics::Clustering of every row):
+ * n_clusters u32[rows], leader u32[rows][S] (sample index of the cluster's first answer,
+ * first n_clusters entries valid), size u32[rows][S].  metrics.cpp:21-37               */
+int cdx_cluster_rows(cdx_ctx* ctx, const uint32_t* ids, uint64_t rows, uint32_t S,
+                     uint32_t* n_clusters, uint32_t* leader, uint32_t* size);
+
+/* Entropy of explicit clusterings (façade path of semantic_entropy/certaindex_entropy):
+ * sizes u32[rows][max_m] in cluster order, m u32[rows]; every row's total n must be
+ * <= max_n (host bound, sizes the term table); outputs f64 (nullable).  A row with an
+ * empty cluster, m == 0 or n > max_n fails at cdx_sync with "semantic_entropy: invalid
+ * clustering".  metrics.cpp:107-125                                                      */
+int cdx_entropy_from_sizes(cdx_ctx* ctx, const uint32_t* sizes, const uint32_t* m,
+                           uint64_t rows, uint32_t max_m, uint32_t max_n, double* H,
+                           double* Hcert);
+
+/* ---- K5: SPEC allocate + exclusive scan of token budgets + stable compaction --------
+ * Replaces scheduler.allocate for a batch of requests whose certaindex
+ * threshold outcome per knob unit is meets_bits (from K2/K4).  Outputs per request:
+ *   exit_knob  i32  knob unit at which the request terminates (always set: cap at latest)
+ *   reason     u8   CDX_EXIT_CERTAIN (threshold met) | CDX_EXIT_BUDGET (resource cap)
+ *   granted    i32  knob units granted (== exit_knob)
+ *   offsets    i64  base_offset + exclusive prefix sum of granted*tokens_per_unit
+ *   kept       u32  stable list of request indices continuing past detect_at
+ * Device scalars: n_kept (u64), tokens_saved (i64) = sum (cap-granted)*tokens_per_unit,
+ * total_budget (i64, nullable) = sum of budgets.                                         */
+int cdx_allocate_scan(cdx_ctx* ctx, const uint32_t* meets_bits, uint64_t R, uint32_t P,
+                      const cdx_alloc_policy* pol, int64_t base_offset, uint32_t kept_base,
+                      int32_t* exit_knob, uint8_t* reason, int32_t* granted, int64_t* offsets,
+                      uint32_t* kept, uint64_t* n_kept, int64_t* tokens_saved,
+                      int64_t* total_budget);
+
+/* ---- K3: CoT probe-window exit ------------------------------------------------------
+ * Replaces, for every prefix of each request's probe trace,
+ *   probe::should_exit(trace, cfg)        probe.cpp:77-85  (consistency probe.cpp:64-75)
+ *   probe::final_answer(trace)            probe.cpp:87-102
+ * ids u32[R][P]; hes u64[R][ceil(P/64)] hesitation bits; offsets i64[R][P] token offsets
+ * (nullable: offset of probe p = (p+1)*interval_tokens).  Outputs: exit_step i32 (0-based
+ * probe index, -1 = no exit), reason u8, final_id u32, low_conf u8, ck f32[R][P] (nullable:
+ * consistency at every probe, 0.0 while the window is not ready, runtime.cpp:298).        */
+int cdx_cot_exit(cdx_ctx* ctx, const uint32_t* ids, const uint64_t* hes, const int64_t* offsets,
+                 uint64_t R, uint32_t P, const cdx_probe_cfg* cfg, int32_t* exit_step,
+                 uint8_t* reason, uint32_t* final_id, uint8_t* low_conf, float* ck);
+
+/* ---- K4: reward certaindex (MCTS mean / Rebase max), cumulative over steps ----------
+ * Replaces the MCTS/Rebase branch of ProgramDriver::update_certaindex (runtime.cpp:
+ * 279-292): at step t, R = certaindex_reward(all rewards of steps 0..t) (metrics.cpp:
+ * 127-137) and H~ = certaindex_entropy(cluster_exact(all answers of steps 0..t)).
+ * rewards f32[G][T][W]; ids u32[G][T][W] (nullable: no entropy signal); agg u8[G]
+ * (CDX_AGG_MEAN for MCTS, CDX_AGG_MAX for Rebase).  Thresholds are per aggregation kind.
+ * Outputs R f32[G][T], H f32[G][T] (nullable), meets_bits u32[G][ceil(T/32)] (nullable). */
+int cdx_reward_certaindex(cdx_ctx* ctx, const float* rewards, const uint32_t* ids,
+                          const uint8_t* agg, uint64_t G, uint32_t T, uint32_t W,
+                          const cdx_threshold* th_mean, uint32_t n_th_mean,
+                          const cdx_threshold* th_max, uint32_t n_th_max, float* R, float* H,
+                          uint32_t* meets_bits);
+
+/* Scalar-façade reward path: RewardSet of f64 values, rows of variable length.
+ * values f64 concatenated, row_off u64[rows+1], agg u8[rows]; out f64[rows]. */
+int cdx_reward_sets(cdx_ctx* ctx, const double* values, const uint64_t* row_off,
+                    const uint8_t* agg, uint64_t rows, double* out);
+
+/* ---- K1: answer canonicalisation + interning + hesitation ---------------------------
+ * Replaces metrics::trim + the unordered_map key of cluster_exact (metrics.cpp:12-37) and
+ * probe::flag_hesitation (probe.cpp:36-44).  bytes: string arena (device), offsets
+ * u64[n+1].  markers: host array of n_markers NUL-terminated strings.  Outputs: ids u32[n]
+ * dense, in first-seen order of the trimmed bytes; hes u8[n] (nullable); first_index
+ * u64[n_unique] (nullable, arena index of each id's first occurrence); *n_unique (host).  */
+int cdx_canon_intern(cdx_ctx* ctx, const char* bytes, const uint64_t* offsets, uint64_t n,
+                     const char* const* markers, uint32_t n_markers, uint32_t* ids,
+                     uint8_t* hes, uint64_t* first_index, uint64_t* n_unique);
+
+/* ---- K6: gang-scheduling program order ----------------------------------------------
+ * Replaces scheduler.escalate / estimate_iteration_tokens / next_batch program order
+ * (tie-break SPEC.md:470).  Order: escalated programs first (FIFO by
+ * arrival), then the policy key (fifo: arrival; sjf: est_tokens_per_iter * (cap-knob)),
+ * then arrival, then program id.  Terminated programs are dropped.  order u32[N] receives
+ * program ids; *n_out (host) the count; escalated u8[N] (nullable) per input program.
+ * keys (nullable, device u64[N][3]) receives the sortable composite key of each ordered
+ * program, for the multi-GPU merge (cdx_gang_merge).                                     */
+int cdx_gang_priority(cdx_ctx* ctx, const cdx_prog_soa* progs, uint64_t N,
+                      const cdx_inter_policy* pol, double now, uint32_t* order, uint64_t* n_out,
+                      uint8_t* escalated, uint64_t* keys);
+/* Merge `runs` sorted runs (concatenated keys u64[total][3] + ids u32[total], run_off
+ * u64[runs+1]) into one global order (ids out u32[total]).  Used after the NCCL allgather. */
+int cdx_gang_merge(cdx_ctx* ctx, const uint64_t* keys, const uint32_t* ids,
+                   const uint64_t* run_off, uint32_t runs, uint32_t* order_out);
+
+/* ---- end-to-end host entry: SC certaindex + allocate from HOST buffers ---------------
+ * Streams ids (host, ideally pinned) through the device in chunks of whole requests,
+ * overlapping H2D copies with K2+K5, and copies exit_knob/reason/granted/offsets and the
+ * fp32 certaindex (nullable) back to host buffers.  Returns when the results are on host. */
+int cdx_sc_decide_host(cdx_ctx* ctx, const uint32_t* ids_host, uint64_t R, uint32_t P,
+                       uint32_t S, const cdx_threshold* th, uint32_t n_th,
+                       const cdx_alloc_policy* pol, int32_t* exit_knob_host,
+                       uint8_t* reason_host, int64_t* offsets_host, float* hcert_host,
+                       int64_t* tokens_saved_host);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* CDX_C_H */

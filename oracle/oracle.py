@@ -1,0 +1,442 @@
+"""oracle.py — numpy/ctypes access to the CHECKERS (test infrastructure only).
+
+  Oracle   : liboracle.so, the C restatement of the hot path (cdx_oracle.c)
+  Ref      : _ref/libcdxref.so, the reference's own C++ sources + ref_harness.cpp
+
+Only tests/, __graft_entry__.smoke() and bench.py's CPU legs import this module.  The
+product (libcdx.so / paper_2412_20993_b200) never does.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ORACLE_SO = os.path.join(HERE, "liboracle.so")
+REF_SO = os.path.join(HERE, "_ref", "libcdxref.so")
+
+P = C.c_void_p
+
+
+class Threshold(C.Structure):
+    _fields_ = [("signal", C.c_uint8), ("dir", C.c_uint8), ("_pad", C.c_uint8 * 6), ("cutoff", C.c_double)]
+
+
+class AllocPolicy(C.Structure):
+    _fields_ = [("kind", C.c_uint8), ("_pad", C.c_uint8 * 3), ("detect_at", C.c_int32),
+                ("recheck_every", C.c_int32), ("resource_cap", C.c_int32), ("tokens_per_unit", C.c_int64)]
+
+
+class ProbeCfg(C.Structure):
+    _fields_ = [("interval_tokens", C.c_int32), ("window", C.c_int32), ("threshold", C.c_double),
+                ("max_tokens", C.c_int64)]
+
+
+class InterPolicy(C.Structure):
+    _fields_ = [("gang", C.c_uint8), ("order", C.c_uint8), ("_pad", C.c_uint8 * 6),
+                ("starvation_limit", C.c_double), ("prior_tokens", C.c_double)]
+
+
+class ProgSoA(C.Structure):
+    _fields_ = [("arrival", P), ("last_service", P), ("iter_tok_sum", P), ("iter_count", P), ("knob", P),
+                ("cap", P), ("terminated", P), ("id_base", C.c_uint32), ("_pad", C.c_uint32)]
+
+
+class GenParams(C.Structure):
+    _fields_ = [("seed", C.c_uint64), ("groups", C.c_uint32), ("conv_lo", C.c_uint32), ("conv_hi", C.c_uint32),
+                ("_pad", C.c_uint32), ("noise_level", C.c_double), ("residual_noise", C.c_double),
+                ("solvable_fraction", C.c_double), ("hesitation_prob", C.c_double),
+                ("reward_start_k", C.c_uint32), ("reward_final_k", C.c_uint32),
+                ("reward_unsolvable_k", C.c_uint32), ("reward_jitter_k", C.c_uint32)]
+
+
+def build():
+    """Build the checkers (the reference part only where /root/reference exists)."""
+    subprocess.run(["make", "-s", "-C", HERE], check=True)
+
+
+def _load(path):
+    if not os.path.exists(path):
+        build()
+    return C.CDLL(path)
+
+
+_O = None
+_R = None
+
+
+def lib():
+    global _O
+    if _O is None:
+        _O = _load(ORACLE_SO)
+        _O.cdxo_mix64.restype = C.c_uint64
+        _O.cdxo_mix64.argtypes = [C.c_uint64]
+        _O.cdxo_derive_seed.restype = C.c_uint64
+        _O.cdxo_derive_seed.argtypes = [C.c_uint64] * 3
+        _O.cdxo_semantic_entropy.restype = C.c_double
+        _O.cdxo_certaindex_entropy.restype = C.c_double
+        _O.cdxo_estimate_iteration_tokens.restype = C.c_double
+        _O.cdxo_estimate_iteration_tokens.argtypes = [C.c_int64, C.c_uint32, C.c_double]
+        _O.cdxo_answer.restype = C.c_uint32
+        _O.cdxo_answer.argtypes = [P, C.c_uint64, C.c_uint64, C.c_uint32]
+        _O.cdxo_cot_amin.argtypes = [C.c_int, C.c_double]
+        _O.cdxo_trim.restype = C.c_size_t
+        _O.cdxo_trim.argtypes = [C.c_char_p, C.c_size_t, C.POINTER(C.c_size_t)]
+        for name in ("cdxo_gen_sc", "cdxo_gen_cot", "cdxo_gen_reward"):
+            getattr(_O, name).restype = None
+    return _O
+
+
+def ref_available() -> bool:
+    if os.path.exists(REF_SO):
+        return True
+    if os.path.isdir("/root/reference/proj/src"):
+        build()
+    return os.path.exists(REF_SO)
+
+
+def ref():
+    global _R
+    if _R is None:
+        if not ref_available():
+            raise RuntimeError("oracle/_ref/libcdxref.so unavailable (reference not built)")
+        _R = C.CDLL(REF_SO)
+        _R.ref_last_error.restype = C.c_char_p
+        _R.ref_mix64.restype = C.c_uint64
+        _R.ref_mix64.argtypes = [C.c_uint64]
+        _R.ref_derive_seed.restype = C.c_uint64
+        _R.ref_derive_seed.argtypes = [C.c_uint64] * 3
+    return _R
+
+
+def _p(a):
+    return None if a is None else a.ctypes.data_as(C.c_void_p)
+
+
+def gen_params(seed=20993, groups=5, conv_lo=1, conv_hi=64, noise_level=0.5, residual_noise=0.0,
+               solvable_fraction=0.9, hesitation_prob=0.0, reward_start_k=5033165, reward_final_k=15099494,
+               reward_unsolvable_k=4194304, reward_jitter_k=1677722) -> GenParams:
+    g = GenParams()
+    g.seed, g.groups, g.conv_lo, g.conv_hi = seed, groups, conv_lo, conv_hi
+    g.noise_level, g.residual_noise, g.solvable_fraction = noise_level, residual_noise, solvable_fraction
+    g.hesitation_prob = hesitation_prob
+    g.reward_start_k, g.reward_final_k = reward_start_k, reward_final_k
+    g.reward_unsolvable_k, g.reward_jitter_k = reward_unsolvable_k, reward_jitter_k
+    return g
+
+
+def vocab(groups):
+    names = ["S"] + [f"D{i}" for i in range(1, groups)]
+    return names + ["wait, " + n for n in names]
+
+
+def _vocab_c(v):
+    arr = (C.c_char_p * len(v))(*[s.encode() for s in v])
+    return arr, len(v)
+
+
+def thresholds(ths):
+    """ths: list of (signal, cutoff, dir)."""
+    arr = (Threshold * max(1, len(ths)))()
+    for i, (sig, cut, d) in enumerate(ths):
+        arr[i].signal, arr[i].cutoff, arr[i].dir = sig, cut, d
+    return arr, len(ths)
+
+
+# ---------------------------------------------------------------- generators (restated)
+def gen_sc(g, R, P_, S, r0=0):
+    ids = np.empty((R, P_, S), np.uint32)
+    lib().cdxo_gen_sc(C.byref(g), C.c_uint64(r0), C.c_uint64(R), C.c_uint32(P_), C.c_uint32(S), _p(ids))
+    return ids
+
+
+def gen_cot(g, R, P_, r0=0):
+    ids = np.empty((R, P_), np.uint32)
+    hes = np.empty((R, (P_ + 63) // 64), np.uint64)
+    lib().cdxo_gen_cot(C.byref(g), C.c_uint64(r0), C.c_uint64(R), C.c_uint32(P_), _p(ids), _p(hes))
+    return ids, hes
+
+
+def gen_reward(g, G, T, W, g0=0):
+    rw = np.empty((G, T, W), np.float32)
+    ids = np.empty((G, T, W), np.uint32)
+    lib().cdxo_gen_reward(C.byref(g), C.c_uint64(g0), C.c_uint64(G), C.c_uint32(T), C.c_uint32(W), _p(rw), _p(ids))
+    return rw, ids
+
+
+# ---------------------------------------------------------------- restated hot path
+def sc_certaindex(ids, ths):
+    R, P_, S = ids.shape
+    h64 = np.empty((R, P_), np.float64)
+    h32 = np.empty((R, P_), np.float32)
+    meets = np.empty((R, (P_ + 31) // 32), np.uint32)
+    arr, n = thresholds(ths)
+    st = lib().cdxo_sc_certaindex(_p(np.ascontiguousarray(ids)), C.c_uint64(R), C.c_uint32(P_), C.c_uint32(S), arr,
+                                  C.c_uint32(n), _p(h64), _p(h32), _p(meets))
+    if st:
+        raise ValueError(f"oracle sc_certaindex status {st}")
+    return h64, h32, meets
+
+
+def allocate_scan(meets, R, P_, kind, detect_at, cap, recheck_every=1, tokens_per_unit=64, base_offset=0):
+    pol = AllocPolicy()
+    pol.kind, pol.detect_at, pol.resource_cap = kind, detect_at, cap
+    pol.recheck_every, pol.tokens_per_unit = recheck_every, tokens_per_unit
+    ek = np.empty(R, np.int32)
+    why = np.empty(R, np.uint8)
+    gr = np.empty(R, np.int32)
+    off = np.empty(R, np.int64)
+    kept = np.empty(max(R, 1), np.uint32)
+    nk = C.c_uint64(0)
+    saved = C.c_int64(0)
+    mb = np.ascontiguousarray(meets, dtype=np.uint32) if meets is not None else np.zeros((R, (P_ + 31) // 32),
+                                                                                          np.uint32)
+    st = lib().cdxo_allocate_scan(_p(mb), C.c_uint64(R), C.c_uint32(P_), C.byref(pol), C.c_int64(base_offset),
+                                  _p(ek), _p(why), _p(gr), _p(off), _p(kept), C.byref(nk), C.byref(saved))
+    if st:
+        raise ValueError(f"oracle allocate status {st}")
+    return dict(exit_knob=ek, reason=why, granted=gr, offsets=off, kept=kept[:nk.value], n_kept=nk.value,
+                tokens_saved=saved.value)
+
+
+def probe_cfg(interval_tokens=64, window=3, threshold=0.9, max_tokens=1 << 20):
+    c = ProbeCfg()
+    c.interval_tokens, c.window, c.threshold, c.max_tokens = interval_tokens, window, threshold, max_tokens
+    return c
+
+
+def cot_exit(ids, hes, cfg, offsets=None, replay=False, want_ck=False):
+    R, P_ = ids.shape
+    ex = np.empty(R, np.int32)
+    why = np.empty(R, np.uint8)
+    fid = np.empty(R, np.uint32)
+    low = np.empty(R, np.uint8)
+    ck = np.empty((R, P_), np.float32) if want_ck else None
+    fn = lib().cdxo_cot_exit_replay if replay else lib().cdxo_cot_exit_batched
+    st = fn(_p(np.ascontiguousarray(ids)), _p(np.ascontiguousarray(hes)),
+            _p(None if offsets is None else np.ascontiguousarray(offsets, dtype=np.int64)), C.c_uint64(R),
+            C.c_uint32(P_), C.byref(cfg), _p(ex), _p(why), _p(fid), _p(low), _p(ck))
+    if st:
+        raise ValueError(f"oracle cot status {st}")
+    return dict(exit_step=ex, reason=why, final_id=fid, low_conf=low, ck=ck)
+
+
+def reward_certaindex(rw, ids, agg):
+    G, T, W = rw.shape
+    R64 = np.empty((G, T), np.float64)
+    R32 = np.empty((G, T), np.float32)
+    H = np.empty((G, T), np.float32) if ids is not None else None
+    st = lib().cdxo_reward_certaindex(_p(np.ascontiguousarray(rw)), _p(None if ids is None else np.ascontiguousarray(ids)),
+                                      _p(np.ascontiguousarray(agg, dtype=np.uint8)), C.c_uint64(G), C.c_uint32(T),
+                                      C.c_uint32(W), _p(R64), _p(R32), _p(H))
+    if st:
+        raise ValueError(f"oracle reward status {st}")
+    return R64, R32, H
+
+
+def gang_order(soa, order_kind, starvation_limit, prior, now, id_base=0):
+    N = soa["arrival"].shape[0]
+    s = ProgSoA()
+    keep = {}
+    for k, dt in (("arrival", np.float64), ("last_service", np.float64), ("iter_tok_sum", np.int64),
+                  ("iter_count", np.uint32), ("knob", np.uint16), ("cap", np.uint16), ("terminated", np.uint8)):
+        keep[k] = np.ascontiguousarray(soa[k], dtype=dt)
+        setattr(s, k, keep[k].ctypes.data)
+    s.id_base = id_base
+    pol = InterPolicy()
+    pol.gang, pol.order, pol.starvation_limit, pol.prior_tokens = 1, order_kind, starvation_limit, prior
+    order = np.empty(max(N, 1), np.uint32)
+    esc = np.empty(max(N, 1), np.uint8)
+    n = C.c_uint64(0)
+    lib().cdxo_gang_order.argtypes = [P, C.c_uint64, P, C.c_double, P, P, P]
+    st = lib().cdxo_gang_order(C.byref(s), C.c_uint64(N), C.byref(pol), C.c_double(now), _p(order), C.byref(n),
+                               _p(esc))
+    if st:
+        raise ValueError(f"oracle gang status {st}")
+    return order[:n.value], esc[:N]
+
+
+def canon_intern(strings, markers=("wait", "hmm")):
+    bs = [s.encode() if isinstance(s, str) else s for s in strings]
+    arena = b"".join(bs)
+    offs = np.zeros(len(bs) + 1, np.uint64)
+    np.cumsum([len(b) for b in bs], out=offs[1:]) if bs else None
+    mk = b"".join(m.encode() for m in markers)
+    moff = np.zeros(len(markers) + 1, np.uint32)
+    if markers:
+        np.cumsum([len(m.encode()) for m in markers], out=moff[1:])
+    ids = np.empty(max(len(bs), 1), np.uint32)
+    hes = np.empty(max(len(bs), 1), np.uint8)
+    nu = C.c_uint64(0)
+    ab = C.create_string_buffer(arena, len(arena) + 1)
+    mb = C.create_string_buffer(mk, len(mk) + 1)
+    st = lib().cdxo_canon_intern(ab, _p(offs), C.c_uint64(len(bs)), mb, _p(moff), C.c_uint32(len(markers)), _p(ids),
+                                 _p(hes), C.byref(nu))
+    if st:
+        raise ValueError("oracle intern failed")
+    return ids[:len(bs)], hes[:len(bs)], nu.value
+
+
+# ---------------------------------------------------------------- the reference itself
+class RefError(Exception):
+    pass
+
+
+def _ref_err():
+    return ref().ref_last_error().decode()
+
+
+def ref_cluster_exact(answers):
+    n = len(answers)
+    arr = (C.c_char_p * max(n, 1))(*[a.encode() if isinstance(a, str) else a for a in answers])
+    sizes = (C.c_int32 * max(n, 1))()
+    labels = C.create_string_buffer(64 * max(n, 1))
+    m = ref().ref_cluster_exact(arr, C.c_uint32(n), sizes, labels, C.c_uint32(64))
+    if m < 0:
+        raise RefError(_ref_err())
+    return [(labels.raw[k * 64:(k + 1) * 64].split(b"\0")[0].decode(), sizes[k]) for k in range(m)]
+
+
+def ref_entropy(sizes):
+    arr = (C.c_int32 * max(1, len(sizes)))(*sizes)
+    H, Hc = C.c_double(), C.c_double()
+    if ref().ref_entropy(arr, C.c_uint32(len(sizes)), C.c_int32(sum(sizes)), C.byref(H), C.byref(Hc)) < 0:
+        raise RefError(_ref_err())
+    return H.value, Hc.value
+
+
+def ref_certaindex_reward(values, agg_max):
+    arr = (C.c_double * max(1, len(values)))(*values)
+    out = C.c_double()
+    if ref().ref_certaindex_reward(arr, C.c_uint32(len(values)), C.c_int(agg_max), C.byref(out)) < 0:
+        raise RefError(_ref_err())
+    return out.value
+
+
+def ref_meets(signals: dict, ths):
+    sig = (C.c_double * 4)()
+    pres = (C.c_int32 * 4)()
+    for k, v in signals.items():
+        sig[k] = v
+        pres[k] = 1
+    arr, n = thresholds(ths)
+    r = ref().ref_meets(sig, pres, arr, C.c_uint32(n))
+    if r < 0:
+        raise RefError(_ref_err())
+    return bool(r)
+
+
+def ref_flag_hesitation(answer, markers):
+    arr = (C.c_char_p * max(1, len(markers)))(*[m.encode() for m in markers])
+    return bool(ref().ref_flag_hesitation(answer.encode() if isinstance(answer, str) else answer, arr,
+                                          C.c_uint32(len(markers))))
+
+
+def _records(records):
+    n = len(records)
+    step = (C.c_int32 * max(n, 1))(*[r[0] for r in records])
+    off = (C.c_int64 * max(n, 1))(*[r[1] for r in records])
+    ans = (C.c_char_p * max(n, 1))(*[r[2].encode() for r in records])
+    hes = (C.c_uint8 * max(n, 1))(*[1 if r[3] else 0 for r in records])
+    return step, off, ans, hes, n
+
+
+def ref_should_exit(records, interval_tokens=64, window=3, threshold=0.9, max_tokens=1 << 20):
+    """records: list of (step_index, token_offset, answer, hesitant)."""
+    step, off, ans, hes, n = _records(records)
+    cfg = probe_cfg(interval_tokens, window, threshold, max_tokens)
+    r = ref().ref_should_exit(step, off, ans, hes, C.c_uint32(n), C.byref(cfg))
+    if r < 0:
+        raise RefError(_ref_err())
+    return r
+
+
+def ref_consistency(records, k, w):
+    step, off, ans, hes, n = _records(records)
+    out = C.c_double()
+    r = ref().ref_consistency(step, ans, hes, C.c_uint32(n), C.c_int32(k), C.c_int32(w), C.byref(out))
+    if r < 0:
+        raise RefError(_ref_err())
+    return out.value if r == 1 else None
+
+
+def ref_final_answer(records, terminated_at=None, reason=1):
+    step, off, ans, hes, n = _records(records)
+    buf = C.create_string_buffer(256)
+    low = C.c_uint8()
+    r = ref().ref_final_answer(step, ans, hes, C.c_uint32(n), C.c_int32(-1 if terminated_at is None else terminated_at),
+                               C.c_int32(reason), buf, C.c_uint32(256), C.byref(low))
+    if r < 0:
+        raise RefError(_ref_err())
+    return buf.value.decode(), bool(low.value)
+
+
+def ref_read_trace_jsonl(text):
+    r = ref().ref_read_trace_jsonl(text.encode())
+    if r < 0:
+        raise RefError(_ref_err())
+    return r
+
+
+def ref_driver_signals(archetype, seed, cap, conv, solvable, units):
+    ent = (C.c_double * units)()
+    rew = (C.c_double * units)()
+    ln = (C.c_double * units)()
+    r = ref().ref_driver_signals(archetype, C.c_uint64(seed), cap, conv, solvable, units, ent, rew, ln)
+    if r < 0:
+        raise RefError(_ref_err())
+    return list(ent), list(rew), list(ln)
+
+
+def ref_sc_batch(ids, groups, ths, nthreads=1, mode=0, want=True):
+    R, P_, S = ids.shape
+    v, nv = _vocab_c(vocab(groups))
+    h = np.empty((R, P_), np.float64) if want else None
+    meets = np.empty((R, (P_ + 31) // 32), np.uint32) if want else None
+    arr, n = thresholds(ths)
+    r = ref().ref_sc_batch(_p(np.ascontiguousarray(ids)), C.c_uint64(R), C.c_uint32(P_), C.c_uint32(S), v,
+                           C.c_uint32(nv), arr, C.c_uint32(n), _p(h), _p(meets), C.c_int(nthreads), C.c_int(mode))
+    if r < 0:
+        raise RefError(_ref_err())
+    return h, meets
+
+
+def ref_cot_batch(ids, hes, groups, interval_tokens=64, window=3, threshold=0.9, max_tokens=1 << 20, nthreads=1,
+                  want_ck=True):
+    R, P_ = ids.shape
+    v, nv = _vocab_c(vocab(groups))
+    cfg = probe_cfg(interval_tokens, window, threshold, max_tokens)
+    ex = np.empty(R, np.int32)
+    why = np.empty(R, np.uint8)
+    fid = np.empty(R, np.uint32)
+    low = np.empty(R, np.uint8)
+    ck = np.empty((R, P_), np.float32) if want_ck else None
+    r = ref().ref_cot_batch(_p(np.ascontiguousarray(ids)), _p(np.ascontiguousarray(hes)), C.c_uint64(R),
+                            C.c_uint32(P_), v, C.c_uint32(nv), C.byref(cfg), _p(ex), _p(why), _p(fid), _p(low), _p(ck),
+                            C.c_int(nthreads))
+    if r < 0:
+        raise RefError(_ref_err())
+    return dict(exit_step=ex, reason=why, final_id=fid, low_conf=low, ck=ck)
+
+
+def ref_reward_batch(rw, ids, agg, groups=5, nthreads=1):
+    G, T, W = rw.shape
+    v, nv = _vocab_c(vocab(groups))
+    R = np.empty((G, T), np.float64)
+    H = np.empty((G, T), np.float64) if ids is not None else None
+    r = ref().ref_reward_batch(_p(np.ascontiguousarray(rw)), _p(None if ids is None else np.ascontiguousarray(ids)),
+                               _p(np.ascontiguousarray(agg, dtype=np.uint8)), C.c_uint64(G), C.c_uint32(T),
+                               C.c_uint32(W), v, C.c_uint32(nv), _p(R), _p(H), C.c_int(nthreads))
+    if r < 0:
+        raise RefError(_ref_err())
+    return R, H
+
+
+def hardware_threads():
+    try:
+        return int(ref().ref_hardware_threads())
+    except Exception:
+        return os.cpu_count() or 1

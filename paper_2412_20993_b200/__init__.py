@@ -1,0 +1,370 @@
+"""paper_2412_20993_b200 — B200-native Certaindex (Dynasor, arXiv 2412.20993) hot path.
+
+The product is libcdx.so: hand-written sm_100a kernels behind the C-ABI declared in
+include/cdx_c.h, with the reference's C++ API (include/cdx/*.hpp) layered above it.  This
+Python module is plumbing for tests and the bench: it binds the C-ABI with ctypes and
+moves torch CUDA tensors (device memory + the current stream) in and out.  It never
+computes a certaindex itself and has no CPU fallback.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+from typing import Optional, Sequence
+
+from . import _abi
+from ._abi import (AGG_MAX, AGG_MEAN, ARCH_COT, ARCH_MCTS, ARCH_REBASE, ARCH_SC, DIR_GE, DIR_LE,  # noqa: F401
+                   EXIT_BUDGET, EXIT_CERTAIN, EXIT_CONTINUE, ORDER_FIFO, ORDER_SJF, POL_EVEN,
+                   POL_K_STEP_THRESHOLD, POL_STATIC_THRESHOLD, SIG_ENTROPY, SIG_LOGPROB, SIG_MEAN_LEN,
+                   SIG_REWARD)
+
+__all__ = ["Context", "CdxError", "Threshold", "AllocPolicy", "ProbeConfig", "InterPolicy", "GenParams",
+           "load_library"]
+
+
+class CdxError(Exception):
+    code = -1
+
+
+class CdxInvalidArgument(CdxError, ValueError):
+    """std::invalid_argument in the reference."""
+    code = _abi.CDX_EINVAL
+
+
+class CdxRuntimeError(CdxError, RuntimeError):
+    """std::runtime_error in the reference."""
+    code = _abi.CDX_ERUNTIME
+
+
+class CdxOutOfRange(CdxError, IndexError):
+    code = _abi.CDX_ERANGE
+
+
+class CdxLogicError(CdxError):
+    code = _abi.CDX_ELOGIC
+
+
+class CdxCudaError(CdxError, RuntimeError):
+    code = _abi.CDX_ECUDA
+
+
+class CdxNcclError(CdxError, RuntimeError):
+    code = _abi.CDX_ENCCL
+
+
+_ERR = {c.code: c for c in (CdxInvalidArgument, CdxRuntimeError, CdxOutOfRange, CdxLogicError, CdxCudaError,
+                             CdxNcclError)}
+
+
+def load_library():
+    return _abi.load()
+
+
+@dataclass
+class Threshold:
+    """metrics.hpp:107-112 SignalThreshold."""
+    signal: int = SIG_ENTROPY
+    cutoff: float = 0.0
+    dir: int = DIR_GE
+
+
+@dataclass
+class AllocPolicy:
+    """SPEC.md:390-393 AllocationPolicy (batched subset)."""
+    kind: int = POL_STATIC_THRESHOLD
+    detect_at: int = 5
+    resource_cap: int = 64
+    recheck_every: int = 1
+    tokens_per_unit: int = 64
+
+
+@dataclass
+class ProbeConfig:
+    """probe.hpp:25-33 ProbeConfig."""
+    interval_tokens: int = 64
+    window: int = 3
+    threshold: float = 0.9
+    max_tokens: int = 1 << 20
+
+
+@dataclass
+class InterPolicy:
+    """SPEC.md:394-397 InterSchedPolicy."""
+    order: int = ORDER_SJF
+    starvation_limit: float = 1.0
+    prior_tokens: float = 128.0
+    gang: bool = True
+
+
+@dataclass
+class GenParams:
+    """Synthetic trace parameters (runtime.hpp:45-69 restated counter-based)."""
+    seed: int = 20993
+    groups: int = 5
+    conv_lo: int = 1
+    conv_hi: int = 64
+    noise_level: float = 0.5
+    residual_noise: float = 0.0
+    solvable_fraction: float = 0.9
+    hesitation_prob: float = 0.0
+    reward_start_k: int = 5033165      # 0.3 * 2^24
+    reward_final_k: int = 15099494     # 0.9 * 2^24
+    reward_unsolvable_k: int = 4194304  # 0.25 * 2^24
+    reward_jitter_k: int = 1677722     # 0.1 * 2^24
+
+    def c(self) -> _abi.GenParams:
+        g = _abi.GenParams()
+        for k in ("seed", "groups", "conv_lo", "conv_hi", "noise_level", "residual_noise", "solvable_fraction",
+                  "hesitation_prob", "reward_start_k", "reward_final_k", "reward_unsolvable_k", "reward_jitter_k"):
+            setattr(g, k, getattr(self, k))
+        return g
+
+
+def vocab(groups: int) -> list:
+    """Answer strings behind the synthetic ids (cdx_c.h cdx_gen_params)."""
+    names = ["S"] + [f"D{i}" for i in range(1, groups)]
+    return names + ["wait, " + n for n in names]
+
+
+def c_thresholds(ths: Sequence[Threshold]):
+    arr = (_abi.Threshold * max(1, len(ths)))()
+    for i, t in enumerate(ths):
+        arr[i].signal, arr[i].dir, arr[i].cutoff = t.signal, t.dir, float(t.cutoff)
+    return arr, len(ths)
+
+
+def c_policy(p: AllocPolicy) -> _abi.AllocPolicy:
+    a = _abi.AllocPolicy()
+    a.kind, a.detect_at, a.recheck_every = p.kind, p.detect_at, p.recheck_every
+    a.resource_cap, a.tokens_per_unit = p.resource_cap, p.tokens_per_unit
+    return a
+
+
+def c_probe(c: ProbeConfig) -> _abi.ProbeCfg:
+    a = _abi.ProbeCfg()
+    a.interval_tokens, a.window, a.threshold, a.max_tokens = c.interval_tokens, c.window, float(c.threshold), \
+        c.max_tokens
+    return a
+
+
+def c_inter(p: InterPolicy) -> _abi.InterPolicy:
+    a = _abi.InterPolicy()
+    a.gang, a.order, a.starvation_limit, a.prior_tokens = int(p.gang), p.order, float(p.starvation_limit), \
+        float(p.prior_tokens)
+    return a
+
+
+def _ptr(t) -> Optional[int]:
+    return None if t is None else t.data_ptr()
+
+
+class Context:
+    """One cdx_ctx bound to a CUDA device; calls run on torch's current stream."""
+
+    def __init__(self, device: int = 0):
+        import torch
+        self.torch = torch
+        self.lib = _abi.load()
+        self.device = device
+        h = C.c_void_p()
+        st = self.lib.cdx_ctx_create(device, C.byref(h))
+        if st != _abi.CDX_OK:
+            raise _ERR.get(st, CdxError)(f"cdx_ctx_create(device={device}) failed with status {st}"
+                                         " (a B200 / sm_100 device is required; there is no CPU fallback)")
+        self.h = h
+        self.dev = torch.device("cuda", device)
+
+    def close(self):
+        if getattr(self, "h", None):
+            self.lib.cdx_ctx_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # -- plumbing --
+    def _bind_stream(self):
+        s = self.torch.cuda.current_stream(self.dev).cuda_stream
+        self.lib.cdx_ctx_set_stream(self.h, C.c_void_p(s))
+
+    def _check(self, st: int):
+        if st != _abi.CDX_OK:
+            msg = self.lib.cdx_last_error(self.h).decode()
+            raise _ERR.get(st, CdxError)(msg)
+
+    def sync(self):
+        self._check(self.lib.cdx_sync(self.h))
+
+    @property
+    def launches(self) -> int:
+        return int(self.lib.cdx_launch_count(self.h))
+
+    def empty(self, shape, dtype):
+        return self.torch.empty(shape, dtype=dtype, device=self.dev)
+
+    # -- synthetic traces --
+    def gen_sc(self, g: GenParams, R: int, P: int, S: int, r0: int = 0, out=None):
+        t = self.torch
+        ids = out if out is not None else self.empty((R, P, S), t.int32)
+        self._bind_stream()
+        gp = g.c()
+        self._check(self.lib.cdx_gen_sc(self.h, C.byref(gp), r0, R, P, S, _ptr(ids)))
+        return ids
+
+    def gen_cot(self, g: GenParams, R: int, P: int, r0: int = 0):
+        t = self.torch
+        ids = self.empty((R, P), t.int32)
+        hes = self.empty((R, (P + 63) // 64), t.int64)
+        self._bind_stream()
+        gp = g.c()
+        self._check(self.lib.cdx_gen_cot(self.h, C.byref(gp), r0, R, P, _ptr(ids), _ptr(hes)))
+        return ids, hes
+
+    def gen_reward(self, g: GenParams, G: int, T: int, W: int, g0: int = 0, with_ids: bool = True):
+        t = self.torch
+        rw = self.empty((G, T, W), t.float32)
+        ids = self.empty((G, T, W), t.int32) if with_ids else None
+        self._bind_stream()
+        gp = g.c()
+        self._check(self.lib.cdx_gen_reward(self.h, C.byref(gp), g0, G, T, W, _ptr(rw), _ptr(ids)))
+        return rw, ids
+
+    # -- K2 --
+    def sc_certaindex(self, ids, thresholds: Sequence[Threshold] = (), want_hcert: bool = True,
+                      hcert=None, meets=None):
+        t = self.torch
+        R, P, S = ids.shape
+        if want_hcert and hcert is None:
+            hcert = self.empty((R, P), t.float32)
+        if meets is None:
+            meets = self.empty((R, (P + 31) // 32), t.int32)
+        arr, n = c_thresholds(thresholds)
+        self._bind_stream()
+        self._check(self.lib.cdx_sc_certaindex(self.h, _ptr(ids), R, P, S, arr, n,
+                                               _ptr(hcert) if want_hcert else None, _ptr(meets)))
+        return hcert, meets
+
+    def cluster_rows(self, ids2d):
+        t = self.torch
+        rows, S = ids2d.shape
+        ncl = self.empty((rows,), t.int32)
+        leader = self.torch.zeros((rows, S), dtype=t.int32, device=self.dev)
+        size = self.torch.zeros((rows, S), dtype=t.int32, device=self.dev)
+        self._bind_stream()
+        self._check(self.lib.cdx_cluster_rows(self.h, _ptr(ids2d), rows, S, _ptr(ncl), _ptr(leader), _ptr(size)))
+        return ncl, leader, size
+
+    def entropy_from_sizes(self, sizes, m, max_n: int):
+        t = self.torch
+        rows, max_m = sizes.shape
+        H = self.empty((rows,), t.float64)
+        Hc = self.empty((rows,), t.float64)
+        self._bind_stream()
+        self._check(self.lib.cdx_entropy_from_sizes(self.h, _ptr(sizes), _ptr(m), rows, max_m, max_n, _ptr(H),
+                                                    _ptr(Hc)))
+        return H, Hc
+
+    # -- K5 --
+    def allocate_scan(self, meets, R: int, P: int, policy: AllocPolicy, base_offset: int = 0, kept_base: int = 0,
+                      out=None):
+        t = self.torch
+        o = out or {}
+        exit_knob = o.get("exit_knob", self.empty((R,), t.int32))
+        reason = o.get("reason", self.empty((R,), t.uint8))
+        granted = o.get("granted", self.empty((R,), t.int32))
+        offsets = o.get("offsets", self.empty((R,), t.int64))
+        kept = o.get("kept", self.empty((max(R, 1),), t.int32))
+        scal = o.get("scalars", self.torch.zeros((3,), dtype=t.int64, device=self.dev))
+        pol = c_policy(policy)
+        self._bind_stream()
+        self._check(self.lib.cdx_allocate_scan(self.h, _ptr(meets), R, P, C.byref(pol), base_offset, kept_base,
+                                               _ptr(exit_knob), _ptr(reason), _ptr(granted), _ptr(offsets),
+                                               _ptr(kept), scal.data_ptr(), scal.data_ptr() + 8,
+                                               scal.data_ptr() + 16))
+        return dict(exit_knob=exit_knob, reason=reason, granted=granted, offsets=offsets, kept=kept,
+                    scalars=scal)
+
+    # -- K3 --
+    def cot_exit(self, ids, hes, cfg: ProbeConfig, offsets=None, want_ck: bool = False, out=None):
+        t = self.torch
+        R, P = ids.shape
+        o = out or {}
+        ex = o.get("exit_step", self.empty((R,), t.int32))
+        reason = o.get("reason", self.empty((R,), t.uint8))
+        fid = o.get("final_id", self.empty((R,), t.int32))
+        low = o.get("low_conf", self.empty((R,), t.uint8))
+        ck = self.empty((R, P), t.float32) if want_ck else None
+        c = c_probe(cfg)
+        self._bind_stream()
+        self._check(self.lib.cdx_cot_exit(self.h, _ptr(ids), _ptr(hes), _ptr(offsets), R, P, C.byref(c), _ptr(ex),
+                                          _ptr(reason), _ptr(fid), _ptr(low), _ptr(ck)))
+        return dict(exit_step=ex, reason=reason, final_id=fid, low_conf=low, ck=ck)
+
+    # -- K4 --
+    def reward_certaindex(self, rewards, ids, agg, th_mean: Sequence[Threshold] = (),
+                          th_max: Sequence[Threshold] = (), want_H: bool = True, want_meets: bool = True):
+        t = self.torch
+        G, T, W = rewards.shape
+        R = self.empty((G, T), t.float32)
+        H = self.empty((G, T), t.float32) if (want_H and ids is not None) else None
+        meets = self.empty((G, (T + 31) // 32), t.int32) if want_meets else None
+        a1, n1 = c_thresholds(th_mean)
+        a2, n2 = c_thresholds(th_max)
+        self._bind_stream()
+        self._check(self.lib.cdx_reward_certaindex(self.h, _ptr(rewards), _ptr(ids), _ptr(agg), G, T, W, a1, n1, a2,
+                                                   n2, _ptr(R), _ptr(H), _ptr(meets)))
+        return R, H, meets
+
+    def reward_sets(self, values, row_off, agg):
+        t = self.torch
+        rows = agg.shape[0]
+        out = self.empty((rows,), t.float64)
+        self._bind_stream()
+        self._check(self.lib.cdx_reward_sets(self.h, _ptr(values), _ptr(row_off), _ptr(agg), rows, _ptr(out)))
+        return out
+
+    # -- K1 --
+    def canon_intern(self, arena, offsets, markers: Sequence[str] = ("wait", "hmm"), want_hes: bool = True):
+        t = self.torch
+        n = offsets.shape[0] - 1
+        ids = self.empty((max(n, 1),), t.int32)
+        hes = self.empty((max(n, 1),), t.uint8) if want_hes else None
+        first = self.empty((max(n, 1),), t.int64)
+        mk = (C.c_char_p * max(1, len(markers)))(*[m.encode() for m in markers])
+        nu = C.c_uint64(0)
+        self._bind_stream()
+        self._check(self.lib.cdx_canon_intern(self.h, _ptr(arena), _ptr(offsets), n, mk, len(markers), _ptr(ids),
+                                              _ptr(hes), _ptr(first), C.byref(nu)))
+        return ids[:n], (hes[:n] if hes is not None else None), first[:nu.value], nu.value
+
+    # -- K6 --
+    def gang_priority(self, soa: dict, policy: InterPolicy, now: float, id_base: int = 0, want_keys: bool = False,
+                      want_escalated: bool = False):
+        t = self.torch
+        N = soa["arrival"].shape[0]
+        s = _abi.ProgSoA()
+        for k in ("arrival", "last_service", "iter_tok_sum", "iter_count", "knob", "cap", "terminated"):
+            setattr(s, k, soa[k].data_ptr())
+        s.id_base = id_base
+        order = self.empty((max(N, 1),), t.int32)
+        esc = self.empty((max(N, 1),), t.uint8) if want_escalated else None
+        keys = self.empty((max(N, 1), 3), t.int64) if want_keys else None
+        n_out = C.c_uint64(0)
+        pol = c_inter(policy)
+        self._bind_stream()
+        self._check(self.lib.cdx_gang_priority(self.h, C.byref(s), N, C.byref(pol), float(now), _ptr(order),
+                                               C.byref(n_out), _ptr(esc), _ptr(keys)))
+        n = n_out.value
+        return order[:n], (esc[:N] if esc is not None else None), (keys[:n] if keys is not None else None)
+
+    def gang_merge(self, keys, ids, run_off):
+        t = self.torch
+        total = ids.shape[0]
+        out = self.empty((max(total, 1),), t.int32)
+        self._bind_stream()
+        self._check(self.lib.cdx_gang_merge(self.h, _ptr(keys), _ptr(ids), _ptr(run_off), run_off.shape[0] - 1,
+                                            _ptr(out)))
+        return out[:total]

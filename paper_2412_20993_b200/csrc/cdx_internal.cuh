@@ -1,0 +1,174 @@
+// cdx_internal.cuh — context, error plumbing and the sm_100a async-copy primitives
+// (TMA tensor loads, 1-D bulk copies, mbarriers) shared by the Certaindex kernels.
+#pragma once
+
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <cudaTypedefs.h>
+
+#include <cstdint>
+#include <string>
+
+#include "../../include/cdx_c.h"
+
+#define CDX_SMS 148
+
+struct cdx_ctx {
+    int device = 0;
+    int sm_count = CDX_SMS;
+    cudaStream_t own_stream = nullptr;
+    cudaStream_t stream = nullptr;
+    std::string err;
+    uint64_t launches = 0;
+    // device error word: 0 ok, else a CDX_E* code set by a kernel (validated on sync)
+    int* d_err = nullptr;
+    int* h_err = nullptr;  // pinned mirror
+    std::string pending_err_msg[8];
+    // growable scratch (look-back tile state, counters, tables)
+    void* scratch = nullptr;
+    size_t scratch_bytes = 0;
+    void* scratch2 = nullptr;
+    size_t scratch2_bytes = 0;
+    // host-entry pipeline buffers
+    void* pipe_buf = nullptr;
+    size_t pipe_bytes = 0;
+    cudaStream_t copy_stream = nullptr;
+    // term-table cache (device): keyed by the list of n values it was built for
+    double* tt_dev = nullptr;
+    size_t tt_bytes = 0;
+    std::string tt_key;
+};
+
+namespace cdx {
+
+int set_error(cdx_ctx* ctx, int code, const std::string& msg);
+int cuda_fail(cdx_ctx* ctx, cudaError_t e, const char* what);
+void* scratch(cdx_ctx* ctx, size_t bytes);
+void* scratch2(cdx_ctx* ctx, size_t bytes);
+// device-side validation error codes (set via atomicCAS on ctx->d_err)
+enum DevErr : int {
+    DEV_OK = 0,
+    DEV_REWARD_RANGE = 1,   // "certaindex_reward: reward outside [0,1]"
+    DEV_INTERN_COLLISION = 2,
+    DEV_INTERN_FULL = 3,
+    DEV_BAD_CLUSTERING = 4,  // "semantic_entropy: invalid clustering"
+};
+const char* dev_err_message(int code);
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda needed)
+bool encode_tmap_2d(CUtensorMap* map, const void* base, uint64_t inner, uint64_t outer,
+                    uint64_t row_stride_bytes, uint32_t box_inner, uint32_t box_outer,
+                    CUtensorMapDataType dtype, CUtensorMapSwizzle swz);
+// rank-N tiled tensor map: dims/box innermost first, strides_bytes has rank-1 entries
+bool encode_tmap(CUtensorMap* map, const void* base, uint32_t rank, const uint64_t* dims,
+                 const uint64_t* strides_bytes, const uint32_t* box, CUtensorMapDataType dtype,
+                 CUtensorMapSwizzle swz);
+// Host-built entropy term tables: for each n in ns, T_n[c] = (c/n)*log(c/n), c = 0..n
+// (metrics.cpp:113-116 with the host libm), uploaded to device scratch.  Returns device
+// pointers: tab (rows concatenated), row_off[i] = offset of n_i's row, logs[i] = log(n_i).
+struct TermTables {
+    const double* tab = nullptr;
+    const uint64_t* row_off = nullptr;
+    const double* logs = nullptr;
+};
+int build_term_tables(cdx_ctx* ctx, const uint32_t* ns, uint32_t count, TermTables* out);
+double host_term(uint32_t c, uint32_t n);
+
+#define CDX_LAUNCHED(ctx) ((ctx)->launches++)
+
+__device__ __forceinline__ void set_dev_err(int* d_err, int code) { atomicCAS(d_err, 0, code); }
+
+// ---------------------------------------------------------------------------------------
+// mbarrier / bulk-copy / TMA (PTX for sm_90+/sm_100a; SASS: SYNCS.*, UBLKCP, UTMALDG)
+// ---------------------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+
+__device__ __forceinline__ void fence_mbar_init() {
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+
+__device__ __forceinline__ void fence_proxy_async() {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+                 "r"(bytes)
+                 : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred P1;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+        "@!P1 bra WAIT_%=;\n"
+        "}\n" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+
+// 1-D bulk global->shared copy, completion counted on `bar` (bytes % 16 == 0, 16B aligned)
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar,
+                                         uint64_t policy) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint "
+        "[%0], [%1], %2, [%3], %4;" ::"r"(smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(policy)
+        : "memory");
+}
+
+// 2-D TMA tile load at (c0 = inner coordinate, c1 = outer coordinate)
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int32_t c0, int32_t c1,
+                                            uint64_t* bar, uint64_t policy) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.L2::cache_hint "
+        "[%0], [%1, {%2, %3}], [%4], %5;" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar)), "l"(policy)
+        : "memory");
+}
+
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, int32_t c0, int32_t c1,
+                                            int32_t c2, uint64_t* bar, uint64_t policy) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.L2::cache_hint "
+        "[%0], [%1, {%2, %3, %4}], [%5], %6;" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar)), "l"(policy)
+        : "memory");
+}
+
+__device__ __forceinline__ void tma_prefetch_desc(const CUtensorMap* map) {
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
+}
+
+__device__ __forceinline__ uint64_t policy_evict_first() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+
+// streaming stores that do not allocate in L1
+__device__ __forceinline__ void st_na_f32(float* p, float v) {
+    asm volatile("st.global.L1::no_allocate.f32 [%0], %1;" ::"l"(p), "f"(v) : "memory");
+}
+
+// 128B-swizzle: 16-byte chunk c of smem row r lives at chunk c ^ (r & 7)
+__device__ __forceinline__ uint32_t swz128(uint32_t row, uint32_t chunk) {
+    return row * 128u + ((chunk ^ (row & 7u)) << 4);
+}
+
+}  // namespace cdx
+
+// kernel-launch helper: records the launch and surfaces launch errors
+#define CDX_CHECK_LAUNCH(ctx, name)                                         \
+    do {                                                                    \
+        (ctx)->launches++;                                                  \
+        cudaError_t _e = cudaGetLastError();                                \
+        if (_e != cudaSuccess) return cdx::cuda_fail((ctx), _e, name);      \
+    } while (0)

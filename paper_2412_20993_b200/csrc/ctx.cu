@@ -1,0 +1,228 @@
+// ctx.cu — C-ABI context: device selection, stream, scratch, error reporting.
+#include <cmath>
+#include <cstring>
+#include <mutex>
+#include <vector>
+
+#include "cdx_internal.cuh"
+
+namespace cdx {
+
+int set_error(cdx_ctx* ctx, int code, const std::string& msg) {
+    if (ctx) ctx->err = msg;
+    return code;
+}
+
+int cuda_fail(cdx_ctx* ctx, cudaError_t e, const char* what) {
+    return set_error(ctx, CDX_ECUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+static void* grow(cdx_ctx* ctx, void** buf, size_t* have, size_t bytes) {
+    if (bytes <= *have) return *buf;
+    if (*buf) {
+        cudaStreamSynchronize(ctx->stream);
+        cudaFree(*buf);
+        *buf = nullptr;
+        *have = 0;
+    }
+    size_t want = bytes < (1u << 20) ? (1u << 20) : bytes + bytes / 4;
+    if (cudaMalloc(buf, want) != cudaSuccess) {
+        *buf = nullptr;
+        return nullptr;
+    }
+    *have = want;
+    return *buf;
+}
+
+void* scratch(cdx_ctx* ctx, size_t bytes) { return grow(ctx, &ctx->scratch, &ctx->scratch_bytes, bytes); }
+void* scratch2(cdx_ctx* ctx, size_t bytes) {
+    return grow(ctx, &ctx->scratch2, &ctx->scratch2_bytes, bytes);
+}
+
+const char* dev_err_message(int code) {
+    switch (code) {
+        case DEV_REWARD_RANGE: return "certaindex_reward: reward outside [0,1]";
+        case DEV_INTERN_COLLISION: return "canon_intern: 64-bit hash collision between distinct answers";
+        case DEV_INTERN_FULL: return "canon_intern: intern table full";
+        case DEV_BAD_CLUSTERING: return "semantic_entropy: invalid clustering";
+    }
+    return "device error";
+}
+
+static PFN_cuTensorMapEncodeTiled_v12000 tmap_fn() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+    });
+    return fn;
+}
+
+bool encode_tmap(CUtensorMap* map, const void* base, uint32_t rank, const uint64_t* dims,
+                 const uint64_t* strides_bytes, const uint32_t* box, CUtensorMapDataType dtype,
+                 CUtensorMapSwizzle swz) {
+    auto fn = tmap_fn();
+    if (!fn || rank < 1 || rank > 5) return false;
+    cuuint64_t d[5], st[4];
+    cuuint32_t b[5], es[5];
+    for (uint32_t i = 0; i < rank; ++i) {
+        d[i] = dims[i];
+        b[i] = box[i];
+        es[i] = 1;
+    }
+    for (uint32_t i = 0; i + 1 < rank; ++i) st[i] = strides_bytes[i];
+    CUresult r = fn(map, dtype, rank, const_cast<void*>(base), d, st, b, es, CU_TENSOR_MAP_INTERLEAVE_NONE, swz,
+                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS;
+}
+
+double host_term(uint32_t c, uint32_t n) {
+    // p * log(p) with p = c/n, exactly as metrics.cpp:113-116 rounds it (no contraction)
+    volatile double p = static_cast<double>(c) / static_cast<double>(n);
+    volatile double lg = std::log(p);
+    return p * lg;
+}
+
+int build_term_tables(cdx_ctx* ctx, const uint32_t* ns, uint32_t count, TermTables* out) {
+    std::string key(reinterpret_cast<const char*>(ns), count * sizeof(uint32_t));
+    if (ctx->tt_dev && key == ctx->tt_key) {
+        out->row_off = reinterpret_cast<const uint64_t*>(ctx->tt_dev);
+        out->logs = ctx->tt_dev + count;
+        out->tab = ctx->tt_dev + 2 * count;
+        return CDX_OK;
+    }
+    std::vector<double> host(2 * count);
+    uint64_t off = 0;
+    for (uint32_t i = 0; i < count; ++i) {
+        std::memcpy(&host[i], &off, 8);
+        off += static_cast<uint64_t>(ns[i]) + 1;
+    }
+    for (uint32_t i = 0; i < count; ++i) host[count + i] = std::log(static_cast<double>(ns[i]));
+    host.reserve(2 * count + off);
+    for (uint32_t i = 0; i < count; ++i) {
+        host.push_back(0.0);
+        for (uint32_t c = 1; c <= ns[i]; ++c) host.push_back(host_term(c, ns[i]));
+    }
+    const size_t bytes = host.size() * sizeof(double);
+    cudaStreamSynchronize(ctx->stream);
+    if (bytes > ctx->tt_bytes) {
+        if (ctx->tt_dev) cudaFree(ctx->tt_dev);
+        ctx->tt_dev = nullptr;
+        ctx->tt_bytes = 0;
+        if (cudaMalloc(&ctx->tt_dev, bytes) != cudaSuccess) return set_error(ctx, CDX_ECUDA, "term table alloc");
+        ctx->tt_bytes = bytes;
+    }
+    cudaError_t e = cudaMemcpy(ctx->tt_dev, host.data(), bytes, cudaMemcpyHostToDevice);
+    if (e != cudaSuccess) return cuda_fail(ctx, e, "term table upload");
+    ctx->tt_key = key;
+    out->row_off = reinterpret_cast<const uint64_t*>(ctx->tt_dev);
+    out->logs = ctx->tt_dev + count;
+    out->tab = ctx->tt_dev + 2 * count;
+    return CDX_OK;
+}
+
+bool encode_tmap_2d(CUtensorMap* map, const void* base, uint64_t inner, uint64_t outer,
+                    uint64_t row_stride_bytes, uint32_t box_inner, uint32_t box_outer,
+                    CUtensorMapDataType dtype, CUtensorMapSwizzle swz) {
+    auto fn = tmap_fn();
+    if (!fn) return false;
+    cuuint64_t dims[2] = {inner, outer};
+    cuuint64_t strides[1] = {row_stride_bytes};
+    cuuint32_t box[2] = {box_inner, box_outer};
+    cuuint32_t estr[2] = {1, 1};
+    CUresult r = fn(map, dtype, 2, const_cast<void*>(base), dims, strides, box, estr,
+                    CU_TENSOR_MAP_INTERLEAVE_NONE, swz, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS;
+}
+
+}  // namespace cdx
+
+extern "C" {
+
+int cdx_abi_version(void) { return CDX_ABI_VERSION; }
+
+int cdx_ctx_create(int device, cdx_ctx** out) {
+    if (!out) return CDX_EINVAL;
+    *out = nullptr;
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0) return CDX_ECUDA;
+    if (device < 0 || device >= n) return CDX_EINVAL;
+    cudaDeviceProp prop;
+    if (cudaGetDeviceProperties(&prop, device) != cudaSuccess) return CDX_ECUDA;
+    if (prop.major != 10) return CDX_ECUDA;  // sm_100a kernels only
+    if (cudaSetDevice(device) != cudaSuccess) return CDX_ECUDA;
+    auto* c = new cdx_ctx();
+    c->device = device;
+    c->sm_count = prop.multiProcessorCount;
+    if (cudaStreamCreateWithFlags(&c->own_stream, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaMalloc(&c->d_err, sizeof(int)) != cudaSuccess ||
+        cudaMallocHost(&c->h_err, sizeof(int)) != cudaSuccess) {
+        delete c;
+        return CDX_ECUDA;
+    }
+    cudaMemset(c->d_err, 0, sizeof(int));
+    cudaDeviceSynchronize();
+    c->stream = c->own_stream;
+    *out = c;
+    return CDX_OK;
+}
+
+int cdx_ctx_destroy(cdx_ctx* ctx) {
+    if (!ctx) return CDX_OK;
+    cudaSetDevice(ctx->device);
+    cudaStreamSynchronize(ctx->stream);
+    if (ctx->scratch) cudaFree(ctx->scratch);
+    if (ctx->scratch2) cudaFree(ctx->scratch2);
+    if (ctx->pipe_buf) cudaFree(ctx->pipe_buf);
+    if (ctx->tt_dev) cudaFree(ctx->tt_dev);
+    if (ctx->d_err) cudaFree(ctx->d_err);
+    if (ctx->h_err) cudaFreeHost(ctx->h_err);
+    if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
+    if (ctx->copy_stream) cudaStreamDestroy(ctx->copy_stream);
+    delete ctx;
+    return CDX_OK;
+}
+
+int cdx_ctx_set_stream(cdx_ctx* ctx, void* s) {
+    if (!ctx) return CDX_EINVAL;
+    // NULL is the (legacy) default stream of the device, shared with every runtime in the
+    // process (e.g. torch's default stream); cdx_ctx_use_own_stream() restores the private one
+    ctx->stream = static_cast<cudaStream_t>(s);
+    return CDX_OK;
+}
+
+int cdx_ctx_use_own_stream(cdx_ctx* ctx) {
+    if (!ctx) return CDX_EINVAL;
+    ctx->stream = ctx->own_stream;
+    return CDX_OK;
+}
+
+void* cdx_ctx_stream(cdx_ctx* ctx) { return ctx ? ctx->stream : nullptr; }
+
+uint64_t cdx_launch_count(const cdx_ctx* ctx) { return ctx ? ctx->launches : 0; }
+
+const char* cdx_last_error(const cdx_ctx* ctx) { return ctx ? ctx->err.c_str() : "null context"; }
+
+int cdx_sync(cdx_ctx* ctx) {
+    if (!ctx) return CDX_EINVAL;
+    cudaSetDevice(ctx->device);
+    cudaError_t e = cudaStreamSynchronize(ctx->stream);
+    if (e != cudaSuccess) return cdx::cuda_fail(ctx, e, "cdx_sync");
+    e = cudaMemcpy(ctx->h_err, ctx->d_err, sizeof(int), cudaMemcpyDeviceToHost);
+    if (e != cudaSuccess) return cdx::cuda_fail(ctx, e, "cdx_sync");
+    const int code = *ctx->h_err;
+    if (code != 0) {
+        cudaMemset(ctx->d_err, 0, sizeof(int));
+        const int st = (code == cdx::DEV_REWARD_RANGE || code == cdx::DEV_BAD_CLUSTERING) ? CDX_EINVAL : CDX_ERUNTIME;
+        return cdx::set_error(ctx, st, cdx::dev_err_message(code));
+    }
+    return CDX_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,300 @@
+// k_cot.cu — K3: chain-of-thought probe-window early exit.
+//
+// Replaces, for every prefix of every request's probe trace (the reference evaluates the
+// decision once per probe as the trace grows):
+//   probe::consistency  (probe.cpp:64-75, usable_up_to :53-60)
+//   probe::should_exit  (probe.cpp:77-85; certainty wins ties)
+//   probe::final_answer (probe.cpp:87-102) after ProgramDriver::terminate (runtime.cpp:405-411)
+// The reference rebuilds the usable list from record 0 at every step (O(P^2) per trace).
+// Here one thread owns one request and slides a register window of the last w usable
+// answers over the probes once: certain_step = first non-hesitant probe whose full window
+// has agree >= a_min(w,tau) (a_min = min{a : (double)a/w >= tau}, computed on the host, so
+// the device decision is an integer compare); budget_step = first probe whose token offset
+// reaches max_tokens.  Equivalence to the prefix replay is property-tested (tests/).
+//
+// Data path: ids u32[R][P] are staged by TMA (2-D tensor map, 128-byte swizzle, 3-stage
+// mbarrier ring) so that each thread reads its own 256-byte row as 16-byte chunks without
+// shared-memory bank conflicts (chunk c of row r sits at chunk c ^ (r & 7)).
+#include "cdx_internal.cuh"
+
+namespace cdx {
+
+constexpr int COT_MAX_STAGES = 3;
+
+struct CotParams {
+    CUtensorMap tmap;  // 64-byte aligned first member
+    const uint32_t* ids;
+    const uint64_t* hes;
+    const int64_t* offsets;
+    int32_t* exit_step;
+    uint8_t* reason;
+    uint32_t* final_id;
+    uint8_t* low_conf;
+    float* ck;
+    uint64_t R;
+    uint64_t ntiles;
+    uint32_t P, hw, boxes, rows;
+    uint32_t stage_bytes, stages;
+    int32_t w, amin;
+    int32_t bstep_implicit;  // first probe index whose implicit offset >= max_tokens, or -1
+    int32_t _pad;
+    int64_t max_tokens;
+};
+
+template <int W, bool TMA>
+__global__ void __launch_bounds__(128) cot_exit_kernel(const __grid_constant__ CotParams p) {
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    // 128B-swizzled TMA destinations must be 1024-byte aligned
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint64_t* bar = reinterpret_cast<uint64_t*>(smem + p.stages * p.stage_bytes);
+    const uint32_t tid = threadIdx.x;
+
+    if (TMA) {
+        if (tid == 0) {
+            tma_prefetch_desc(&p.tmap);
+            for (uint32_t s = 0; s < p.stages; ++s) mbar_init(&bar[s], 1);
+            fence_mbar_init();
+        }
+        __syncthreads();
+    }
+    const uint64_t policy = policy_evict_first();
+    const uint64_t stride = gridDim.x;
+    auto issue = [&](uint64_t tile, uint32_t stage) {
+        uint8_t* dst = smem + stage * p.stage_bytes;
+        mbar_expect_tx(&bar[stage], p.stage_bytes);
+        for (uint32_t b = 0; b < p.boxes; ++b)
+            tma_load_2d(dst + b * p.rows * 128u, &p.tmap, static_cast<int32_t>(b * 32),
+                        static_cast<int32_t>(tile * p.rows), &bar[stage], policy);
+    };
+    if (TMA && tid == 0) {
+        for (uint32_t s = 0; s < p.stages; ++s) {
+            const uint64_t t = blockIdx.x + s * stride;
+            if (t < p.ntiles) issue(t, s);
+        }
+    }
+
+    uint32_t it_count = 0;
+    for (uint64_t tile = blockIdx.x; tile < p.ntiles; tile += stride, ++it_count) {
+        const uint32_t stage = it_count % p.stages;
+        if (TMA) mbar_wait(&bar[stage], (it_count / p.stages) & 1u);
+        const uint8_t* tsm = smem + stage * p.stage_bytes;
+        const uint64_t r = tile * p.rows + tid;
+
+        if (r < p.R) {
+            const uint32_t P = p.P;
+            int32_t bstep = p.bstep_implicit;
+            if (p.offsets) {
+                bstep = -1;
+                for (uint32_t q = 0; q < P; ++q)
+                    if (__ldg(p.offsets + r * P + q) >= p.max_tokens) {
+                        bstep = static_cast<int32_t>(q);
+                        break;
+                    }
+            }
+            uint32_t win[W > 0 ? W : 1];
+#pragma unroll
+            for (int i = 0; i < (W > 0 ? W : 1); ++i) win[i] = 0;
+            int32_t usable = 0, last_agree = -1;
+            uint32_t last_nh = 0;
+            bool has_nh = false, done = false;
+            int32_t ex = -1;
+            uint8_t why = CDX_EXIT_CONTINUE;
+            uint32_t fid = 0;
+            uint8_t low = 0;
+            uint64_t hword = 0;
+            const float inv_dummy = 0.f;
+            (void)inv_dummy;
+
+            for (uint32_t b = 0; b < p.boxes && !(done && !p.ck); ++b) {
+#pragma unroll
+                for (uint32_t c = 0; c < 8; ++c) {
+                    uint4 v4;
+                    const uint32_t col = b * 32 + c * 4;
+                    if (col >= P) break;
+                    if (TMA) {
+                        v4 = *reinterpret_cast<const uint4*>(tsm + b * p.rows * 128u + swz128(tid, c));
+                    } else {
+                        const uint32_t* src = p.ids + r * P + col;
+                        v4.x = __ldg(src);
+                        v4.y = col + 1 < P ? __ldg(src + 1) : 0u;
+                        v4.z = col + 2 < P ? __ldg(src + 2) : 0u;
+                        v4.w = col + 3 < P ? __ldg(src + 3) : 0u;
+                    }
+                    const uint32_t vv[4] = {v4.x, v4.y, v4.z, v4.w};
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) {
+                        const uint32_t q = col + e;
+                        if (q >= P) break;
+                        if ((q & 63u) == 0) hword = __ldg(p.hes + r * p.hw + (q >> 6));
+                        const uint32_t v = vv[e];
+                        const bool hz = (hword >> (q & 63u)) & 1ull;
+                        if (!hz) {
+                            ++usable;
+                            last_nh = v;
+                            has_nh = true;
+                            int32_t agree = -1;
+                            if (W > 0) {
+#pragma unroll
+                                for (int i = 0; i < W - 1; ++i) win[i] = win[i + 1];
+                                win[W > 0 ? W - 1 : 0] = v;
+                                if (usable >= W) {
+                                    agree = 0;
+#pragma unroll
+                                    for (int i = 0; i < W; ++i) agree += win[i] == v ? 1 : 0;
+                                }
+                            } else if (usable >= p.w) {
+                                // generic window: scan back over the last w usable probes
+                                agree = 0;
+                                int32_t seen = 0;
+                                for (int32_t qq = static_cast<int32_t>(q); qq >= 0 && seen < p.w; --qq) {
+                                    const uint64_t hw2 = __ldg(p.hes + r * p.hw + (qq >> 6));
+                                    if ((hw2 >> (qq & 63)) & 1ull) continue;
+                                    ++seen;
+                                    uint32_t x;
+                                    if (TMA) {
+                                        const uint32_t bb = qq >> 5, cc = (qq & 31) >> 2, ee = qq & 3;
+                                        x = *reinterpret_cast<const uint32_t*>(tsm + bb * p.rows * 128u +
+                                                                               swz128(tid, cc) + ee * 4);
+                                    } else {
+                                        x = __ldg(p.ids + r * P + qq);
+                                    }
+                                    agree += x == v ? 1 : 0;
+                                }
+                            }
+                            if (agree >= 0) {
+                                last_agree = agree;
+                                if (!done && agree >= p.amin) {  // C >= tau: exit certain
+                                    done = true;
+                                    ex = static_cast<int32_t>(q);
+                                    why = CDX_EXIT_CERTAIN;
+                                    fid = v;  // the terminating record's answer
+                                    low = 0;
+                                }
+                            }
+                        }
+                        if (p.ck) {
+                            const double cv = last_agree < 0 ? 0.0
+                                                             : __ddiv_rn(static_cast<double>(last_agree),
+                                                                         static_cast<double>(p.w));
+                            p.ck[r * P + q] = static_cast<float>(cv);
+                        }
+                        if (!done && static_cast<int32_t>(q) == bstep) {  // token budget exhausted
+                            done = true;
+                            ex = static_cast<int32_t>(q);
+                            why = CDX_EXIT_BUDGET;
+                            fid = has_nh ? last_nh : v;  // latest non-hesitant, else latest
+                            low = has_nh ? 0 : 1;
+                        }
+                        if (!done && q == P - 1) {  // never exited: final answer of the full trace
+                            fid = has_nh ? last_nh : v;
+                            low = has_nh ? 0 : 1;
+                        }
+                    }
+                }
+            }
+            p.exit_step[r] = ex;
+            p.reason[r] = why;
+            if (p.final_id) p.final_id[r] = fid;
+            if (p.low_conf) p.low_conf[r] = low;
+        }
+        if (TMA) {
+            __syncthreads();
+            if (tid == 0) {
+                const uint64_t nt = tile + static_cast<uint64_t>(p.stages) * stride;
+                if (nt < p.ntiles) issue(nt, stage);
+            }
+        }
+    }
+}
+
+template <int W>
+static void launch_cot(const CotParams& p, bool tma, unsigned grid, size_t smem, cudaStream_t st) {
+    if (tma) {
+        cudaFuncSetAttribute(cot_exit_kernel<W, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             static_cast<int>(smem));
+        cot_exit_kernel<W, true><<<grid, p.rows, smem, st>>>(p);
+    } else {
+        cot_exit_kernel<W, false><<<grid, p.rows, 0, st>>>(p);
+    }
+}
+
+}  // namespace cdx
+
+extern "C" int cdx_cot_exit(cdx_ctx* ctx, const uint32_t* ids, const uint64_t* hes, const int64_t* offsets,
+                            uint64_t R, uint32_t P, const cdx_probe_cfg* cfg, int32_t* exit_step,
+                            uint8_t* reason, uint32_t* final_id, uint8_t* low_conf, float* ck) {
+    using namespace cdx;
+    if (!ctx) return CDX_EINVAL;
+    if (!cfg) return set_error(ctx, CDX_EINVAL, "probe: null config");
+    // ProbeConfig::validate, probe.cpp:19-25
+    if (cfg->interval_tokens < 1) return set_error(ctx, CDX_EINVAL, "probe: interval_tokens must be >= 1");
+    if (cfg->window < 1) return set_error(ctx, CDX_EINVAL, "probe: window must be >= 1");
+    if (cfg->threshold <= 0.0 || cfg->threshold > 1.0)
+        return set_error(ctx, CDX_EINVAL, "probe: threshold must be in (0,1]");
+    if (cfg->max_tokens < 1) return set_error(ctx, CDX_EINVAL, "probe: max_tokens must be >= 1");
+    if (P == 0) return set_error(ctx, CDX_EINVAL, "final_answer: empty trace");
+    if (!ids || !hes || !exit_step || !reason) return set_error(ctx, CDX_EINVAL, "cot_exit: null pointer");
+    if (R == 0) return CDX_OK;
+
+    CotParams p{};
+    p.ids = ids;
+    p.hes = hes;
+    p.offsets = offsets;
+    p.exit_step = exit_step;
+    p.reason = reason;
+    p.final_id = final_id;
+    p.low_conf = low_conf;
+    p.ck = ck;
+    p.R = R;
+    p.P = P;
+    p.hw = (P + 63) / 64;
+    p.boxes = (P + 31) / 32;
+    p.w = cfg->window;
+    int amin = cfg->window + 1;
+    for (int a = 0; a <= cfg->window; ++a)
+        if (static_cast<double>(a) / static_cast<double>(cfg->window) >= cfg->threshold) {
+            amin = a;
+            break;
+        }
+    p.amin = amin;
+    p.max_tokens = cfg->max_tokens;
+    // implicit offsets (p+1)*interval: first probe with offset >= max_tokens
+    {
+        const int64_t I = cfg->interval_tokens;
+        const int64_t k = (cfg->max_tokens + I - 1) / I;  // smallest p+1 with (p+1)*I >= max
+        p.bstep_implicit = (k - 1 < static_cast<int64_t>(P)) ? static_cast<int32_t>(k - 1) : -1;
+    }
+    bool tma = (P % 4 == 0) && (reinterpret_cast<uintptr_t>(ids) % 16 == 0) && P <= 512 && R <= 0x7fffffffull;
+    uint32_t rows = 128;
+    if (tma) {
+        while (rows > 32 && static_cast<uint64_t>(rows) * p.boxes * 128u > 65536u) rows -= 32;
+        p.rows = rows;
+        p.stage_bytes = rows * p.boxes * 128u;
+        p.stages = std::max<uint32_t>(1, std::min<uint32_t>(COT_MAX_STAGES, (192u * 1024u) / p.stage_bytes));
+        tma = encode_tmap_2d(&p.tmap, ids, P, R, static_cast<uint64_t>(P) * 4u, 32, rows,
+                             CU_TENSOR_MAP_DATA_TYPE_UINT32, CU_TENSOR_MAP_SWIZZLE_128B);
+    }
+    if (!tma) {
+        p.rows = 128;
+        p.stages = 1;
+        p.stage_bytes = 0;
+    }
+    p.ntiles = (R + p.rows - 1) / p.rows;
+    const size_t smem = tma ? static_cast<size_t>(p.stages) * p.stage_bytes + 1024 + 8 * COT_MAX_STAGES : 0;
+    int per_sm = 2;
+    const uint64_t grid = std::min<uint64_t>(p.ntiles, static_cast<uint64_t>(ctx->sm_count) * (tma ? per_sm : 8));
+    const unsigned g = static_cast<unsigned>(grid);
+    switch (cfg->window) {
+        case 1: launch_cot<1>(p, tma, g, smem, ctx->stream); break;
+        case 2: launch_cot<2>(p, tma, g, smem, ctx->stream); break;
+        case 3: launch_cot<3>(p, tma, g, smem, ctx->stream); break;
+        case 4: launch_cot<4>(p, tma, g, smem, ctx->stream); break;
+        case 5: launch_cot<5>(p, tma, g, smem, ctx->stream); break;
+        case 6: launch_cot<6>(p, tma, g, smem, ctx->stream); break;
+        case 7: launch_cot<7>(p, tma, g, smem, ctx->stream); break;
+        case 8: launch_cot<8>(p, tma, g, smem, ctx->stream); break;
+        default: launch_cot<0>(p, tma, g, smem, ctx->stream); break;
+    }
+    CDX_CHECK_LAUNCH(ctx, "cot_exit");
+    return CDX_OK;
+}

@@ -1,0 +1,149 @@
+"""GPU parity: K2 sc_certaindex + K5 allocate_scan (+ device generator) vs the oracle.
+
+Bit-exact: meets bits, exit knobs, reasons, grants, budget offsets, kept lists, totals.
+Certaindex values: the fp32 output must equal the fp32 rounding of the oracle's FP64 value
+bit for bit (stronger than the 1e-6 relative tolerance north_star states).
+"""
+import numpy as np
+import pytest
+
+from oracle import oracle as O
+
+pytestmark = pytest.mark.gpu
+
+SIG_E, SIG_R, GE, LE = 0, 1, 0, 1
+
+
+def _gp(**kw):
+    from paper_2412_20993_b200 import GenParams
+    return GenParams(**kw)
+
+
+def _og(**kw):
+    return O.gen_params(**kw)
+
+
+@pytest.mark.parametrize("R,P,S", [(1, 1, 1), (3, 5, 2), (37, 20, 7), (64, 32, 16), (129, 64, 32), (1000, 64, 32),
+                                   (333, 33, 31), (50, 96, 24), (8, 130, 5), (2048, 32, 16)])
+def test_generator_matches_oracle(ctx, R, P, S):
+    ids = ctx.gen_sc(_gp(seed=R * 7 + P, conv_hi=max(1, P)), R, P, S)
+    ref = O.gen_sc(_og(seed=R * 7 + P, conv_hi=max(1, P)), R, P, S)
+    assert np.array_equal(ids.cpu().numpy().view(np.uint32), ref)
+
+
+@pytest.mark.parametrize("R,P,S", [(1, 1, 1), (5, 3, 2), (37, 20, 7), (64, 32, 16), (129, 64, 32), (777, 64, 32),
+                                   (333, 33, 31), (50, 96, 24), (8, 130, 5), (2048, 32, 16), (17, 64, 3),
+                                   (300, 64, 1)])
+@pytest.mark.parametrize("ths", [[(SIG_E, 0.7, GE)], [], [(SIG_E, 0.5, GE), (SIG_E, 0.99, LE)]])
+def test_sc_certaindex_parity(ctx, R, P, S, ths):
+    from paper_2412_20993_b200 import Threshold
+    g = dict(seed=1000 + R + S, conv_hi=max(1, P))
+    ids = ctx.gen_sc(_gp(**g), R, P, S)
+    h, meets = ctx.sc_certaindex(ids, [Threshold(s, c, d) for s, c, d in ths])
+    ctx.sync()
+    oh64, oh32, ometa = O.sc_certaindex(O.gen_sc(_og(**g), R, P, S), ths)
+    assert np.array_equal(h.cpu().numpy().view(np.uint32), oh32.view(np.uint32))
+    assert np.array_equal(meets.cpu().numpy().view(np.uint32), ometa)
+
+
+def test_sc_certaindex_all_partitions_n32(ctx):
+    """Every clustering shape of n=32 in several first-seen orders: exercises the ordered
+    FP64 fold where naive fp32 or reordered sums flip threshold decisions."""
+    import torch
+    rng = np.random.default_rng(5)
+    rows = []
+    def parts(n, mx):
+        if n == 0:
+            yield []
+            return
+        for k in range(min(n, mx), 0, -1):
+            for rest in parts(n - k, k):
+                yield [k] + rest
+    for part in parts(32, 32):
+        labels = np.concatenate([np.full(c, i, np.uint32) for i, c in enumerate(part)])
+        rows.append(labels)
+        rows.append(rng.permutation(labels))
+    ids_np = np.stack(rows).astype(np.uint32)  # (n_rows, 32)
+    n = ids_np.shape[0]
+    pad = (-n) % 64
+    ids_np = np.concatenate([ids_np, np.zeros((pad, 32), np.uint32)])
+    R = ids_np.shape[0] // 64
+    ids3 = ids_np.reshape(R, 64, 32)
+    ths = [(SIG_E, t, GE) for t in (0.7,)]
+    from paper_2412_20993_b200 import Threshold
+    for tau in (0.4, 0.5, 0.7, 0.75, 0.85, 0.99):
+        ths = [(SIG_E, tau, GE)]
+        h, meets = ctx.sc_certaindex(torch.from_numpy(ids3.view(np.int32)).cuda(), [Threshold(*t) for t in ths])
+        ctx.sync()
+        _, oh32, om = O.sc_certaindex(ids3, ths)
+        assert np.array_equal(h.cpu().numpy().view(np.uint32), oh32.view(np.uint32))
+        assert np.array_equal(meets.cpu().numpy().view(np.uint32), om)
+
+
+def test_sc_unaligned_base_pointer(ctx):
+    """A base pointer that is not 16B aligned takes the plain-load tile path."""
+    import torch
+    from paper_2412_20993_b200 import Threshold
+    R, P, S = 40, 8, 3
+    ids = ctx.gen_sc(_gp(seed=4, conv_hi=8), R + 1, P, S)
+    flat = ids.view(-1)[1:1 + R * P * S].view(R, P, S)  # 4-byte offset
+    h, meets = ctx.sc_certaindex(flat, [Threshold(SIG_E, 0.6, GE)])
+    ctx.sync()
+    ref_ids = O.gen_sc(_og(seed=4, conv_hi=8), R + 1, P, S).reshape(-1)[1:1 + R * P * S].reshape(R, P, S)
+    _, oh32, om = O.sc_certaindex(ref_ids, [(SIG_E, 0.6, GE)])
+    assert np.array_equal(h.cpu().numpy().view(np.uint32), oh32.view(np.uint32))
+    assert np.array_equal(meets.cpu().numpy().view(np.uint32), om)
+
+
+def test_sc_errors(ctx):
+    import torch
+    from paper_2412_20993_b200 import CdxInvalidArgument, Threshold
+    ids = torch.zeros((2, 4, 4), dtype=torch.int32, device="cuda")
+    with pytest.raises(CdxInvalidArgument, match="signal 'certaindex_reward' absent"):
+        ctx.sc_certaindex(ids, [Threshold(SIG_R, 0.4, GE)])
+    with pytest.raises(CdxInvalidArgument, match="empty answer set"):
+        ctx.sc_certaindex(torch.zeros((2, 4, 0), dtype=torch.int32, device="cuda"))
+
+
+@pytest.mark.parametrize("kind,detect,cap,recheck", [(2, 5, 64, 1), (4, 5, 64, 1), (4, 3, 60, 7), (0, 1, 64, 1),
+                                                     (2, 64, 64, 1), (4, 1, 1, 1), (2, 1, 33, 1)])
+@pytest.mark.parametrize("R", [1, 1023, 1024, 1025, 5000])
+def test_allocate_scan_parity(ctx, kind, detect, cap, recheck, R):
+    from paper_2412_20993_b200 import AllocPolicy, Threshold
+    P, S = 64, 32
+    if cap > P:
+        pytest.skip()
+    g = dict(seed=77 + R, conv_hi=64)
+    ids = ctx.gen_sc(_gp(**g), R, P, S)
+    _, meets = ctx.sc_certaindex(ids, [Threshold(SIG_E, 0.7, GE)], want_hcert=False)
+    pol = AllocPolicy(kind=kind, detect_at=detect, resource_cap=cap, recheck_every=recheck, tokens_per_unit=64 * S)
+    out = ctx.allocate_scan(meets, R, P, pol, base_offset=12345)
+    ctx.sync()
+    _, _, om = O.sc_certaindex(O.gen_sc(_og(**g), R, P, S), [(SIG_E, 0.7, GE)])
+    ref = O.allocate_scan(om, R, P, kind, detect, cap, recheck, 64 * S, base_offset=12345)
+    for k in ("exit_knob", "reason", "granted", "offsets"):
+        assert np.array_equal(out[k].cpu().numpy(), ref[k].astype(out[k].cpu().numpy().dtype)), k
+    n_kept, saved, total = out["scalars"].cpu().numpy().tolist()
+    assert n_kept == ref["n_kept"]
+    assert saved == ref["tokens_saved"]
+    assert np.array_equal(out["kept"][:n_kept].cpu().numpy().view(np.uint32), ref["kept"])
+    assert total == int((ref["granted"].astype(np.int64) * 64 * S).sum())
+
+
+def test_allocate_scan_large_property(ctx):
+    """Full-size property check at 1M requests: offsets are an exclusive prefix sum of
+    granted*tpu (checked by recomputation on the GPU), kept list strictly increasing."""
+    import torch
+    from paper_2412_20993_b200 import AllocPolicy, Threshold
+    R, P, S = 1 << 20, 64, 32
+    meets = torch.randint(-2**31, 2**31 - 1, (R, 2), dtype=torch.int32, device="cuda")
+    pol = AllocPolicy(kind=4, detect_at=5, resource_cap=64, recheck_every=3, tokens_per_unit=2048)
+    out = ctx.allocate_scan(meets, R, P, pol)
+    ctx.sync()
+    g = out["granted"].to(torch.int64) * 2048
+    excl = torch.cumsum(g, 0) - g
+    assert torch.equal(excl, out["offsets"])
+    n_kept = int(out["scalars"][0])
+    kept = out["kept"][:n_kept].to(torch.int64)
+    assert torch.all(kept[1:] > kept[:-1])
+    assert n_kept == int((out["granted"] > 5).sum())
