@@ -52,6 +52,7 @@ enum DevErr : int {
     DEV_INTERN_COLLISION = 2,
     DEV_INTERN_FULL = 3,
     DEV_BAD_CLUSTERING = 4,  // "semantic_entropy: invalid clustering"
+    DEV_EMPTY_REWARDS = 5,   // "certaindex_reward: empty reward set"
 };
 const char* dev_err_message(int code);
 // cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda needed)

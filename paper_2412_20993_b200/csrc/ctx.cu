@@ -45,6 +45,7 @@ const char* dev_err_message(int code) {
         case DEV_INTERN_COLLISION: return "canon_intern: 64-bit hash collision between distinct answers";
         case DEV_INTERN_FULL: return "canon_intern: intern table full";
         case DEV_BAD_CLUSTERING: return "semantic_entropy: invalid clustering";
+        case DEV_EMPTY_REWARDS: return "certaindex_reward: empty reward set";
     }
     return "device error";
 }
@@ -219,7 +220,10 @@ int cdx_sync(cdx_ctx* ctx) {
     const int code = *ctx->h_err;
     if (code != 0) {
         cudaMemset(ctx->d_err, 0, sizeof(int));
-        const int st = (code == cdx::DEV_REWARD_RANGE || code == cdx::DEV_BAD_CLUSTERING) ? CDX_EINVAL : CDX_ERUNTIME;
+        const int st = (code == cdx::DEV_REWARD_RANGE || code == cdx::DEV_BAD_CLUSTERING ||
+                        code == cdx::DEV_EMPTY_REWARDS)
+                           ? CDX_EINVAL
+                           : CDX_ERUNTIME;
         return cdx::set_error(ctx, st, cdx::dev_err_message(code));
     }
     return CDX_OK;

@@ -15,6 +15,9 @@
 // Data path: ids u32[R][P] are staged by TMA (2-D tensor map, 128-byte swizzle, 3-stage
 // mbarrier ring) so that each thread reads its own 256-byte row as 16-byte chunks without
 // shared-memory bank conflicts (chunk c of row r sits at chunk c ^ (r & 7)).
+#include <algorithm>
+#include <cstdlib>
+
 #include "cdx_internal.cuh"
 
 namespace cdx {
@@ -41,11 +44,31 @@ struct CotParams {
     int64_t max_tokens;
 };
 
+// Per-request state of the sliding window (W = compile-time window, 0 = runtime window).
+template <int W>
+struct CotWin {
+    uint32_t win[W > 0 ? W : 1];
+    int32_t usable = 0, last_agree = -1;
+    uint32_t last_nh = 0;
+    bool has_nh = false;
+};
+
 template <int W, bool TMA>
+__device__ __forceinline__ uint32_t cot_id(const CotParams& p, const uint8_t* tsm, uint32_t tid, uint64_t r,
+                                           uint32_t q) {
+    if (TMA) {
+        const uint32_t bb = q >> 5, cc = (q & 31u) >> 2, ee = q & 3u;
+        return *reinterpret_cast<const uint32_t*>(tsm + bb * p.rows * 128u + swz128(tid, cc) + ee * 4u);
+    }
+    return __ldg(p.ids + r * p.P + q);
+}
+
+// CK = also emit the consistency value C at every probe (runtime.cpp:298 value_or(0.0)).
+template <int W, bool TMA, bool CK>
 __global__ void __launch_bounds__(128) cot_exit_kernel(const __grid_constant__ CotParams p) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     // 128B-swizzled TMA destinations must be 1024-byte aligned
-    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
     uint64_t* bar = reinterpret_cast<uint64_t*>(smem + p.stages * p.stage_bytes);
     const uint32_t tid = threadIdx.x;
 
@@ -73,10 +96,9 @@ __global__ void __launch_bounds__(128) cot_exit_kernel(const __grid_constant__ C
         }
     }
 
-    uint32_t it_count = 0;
-    for (uint64_t tile = blockIdx.x; tile < p.ntiles; tile += stride, ++it_count) {
-        const uint32_t stage = it_count % p.stages;
-        if (TMA) mbar_wait(&bar[stage], (it_count / p.stages) & 1u);
+    uint32_t stage = 0, parity = 0;
+    for (uint64_t tile = blockIdx.x; tile < p.ntiles; tile += stride) {
+        if (TMA) mbar_wait(&bar[stage], parity);
         const uint8_t* tsm = smem + stage * p.stage_bytes;
         const uint64_t r = tile * p.rows + tid;
 
@@ -91,26 +113,34 @@ __global__ void __launch_bounds__(128) cot_exit_kernel(const __grid_constant__ C
                         break;
                     }
             }
-            uint32_t win[W > 0 ? W : 1];
+            // without ck only probes up to the budget step can decide the exit
+            const uint32_t L = CK ? P : (bstep >= 0 ? static_cast<uint32_t>(bstep) + 1 : P);
+            CotWin<W> st;
 #pragma unroll
-            for (int i = 0; i < (W > 0 ? W : 1); ++i) win[i] = 0;
-            int32_t usable = 0, last_agree = -1;
-            uint32_t last_nh = 0;
-            bool has_nh = false, done = false;
-            int32_t ex = -1;
-            uint8_t why = CDX_EXIT_CONTINUE;
-            uint32_t fid = 0;
-            uint8_t low = 0;
-            uint64_t hword = 0;
-            const float inv_dummy = 0.f;
-            (void)inv_dummy;
+            for (int i = 0; i < (W > 0 ? W : 1); ++i) st.win[i] = 0;
+            bool done = false;
+            int32_t cstep = -1;
+            uint32_t cid = 0;
+            // snapshot of the window state at the budget step (CK mode runs past it)
+            uint32_t b_nh = 0;
+            bool b_has = false;
+            uint32_t hw32 = 0;
+            uint64_t hw64 = 0;
 
-            for (uint32_t b = 0; b < p.boxes && !(done && !p.ck); ++b) {
+            for (uint32_t b = 0; b * 32u < L; ++b) {
+                if (!CK && done) break;
+                if ((b & 1u) == 0) {  // one u64 hesitation word covers two 32-probe boxes
+                    hw64 = __ldg(p.hes + r * p.hw + (b >> 1));
+                    hw32 = static_cast<uint32_t>(hw64);
+                } else {
+                    hw32 = static_cast<uint32_t>(hw64 >> 32);
+                }
 #pragma unroll
                 for (uint32_t c = 0; c < 8; ++c) {
+                    const uint32_t col = b * 32u + c * 4u;
+                    if (col >= L) break;
+                    if (!CK && done) break;
                     uint4 v4;
-                    const uint32_t col = b * 32 + c * 4;
-                    if (col >= P) break;
                     if (TMA) {
                         v4 = *reinterpret_cast<const uint4*>(tsm + b * p.rows * 128u + swz128(tid, c));
                     } else {
@@ -122,75 +152,80 @@ __global__ void __launch_bounds__(128) cot_exit_kernel(const __grid_constant__ C
                     }
                     const uint32_t vv[4] = {v4.x, v4.y, v4.z, v4.w};
 #pragma unroll
-                    for (int e = 0; e < 4; ++e) {
+                    for (uint32_t e = 0; e < 4; ++e) {
                         const uint32_t q = col + e;
-                        if (q >= P) break;
-                        if ((q & 63u) == 0) hword = __ldg(p.hes + r * p.hw + (q >> 6));
+                        if (q >= L) break;
                         const uint32_t v = vv[e];
-                        const bool hz = (hword >> (q & 63u)) & 1ull;
+                        const bool hz = (hw32 >> (c * 4u + e)) & 1u;
                         if (!hz) {
-                            ++usable;
-                            last_nh = v;
-                            has_nh = true;
+                            ++st.usable;
+                            st.last_nh = v;
+                            st.has_nh = true;
                             int32_t agree = -1;
                             if (W > 0) {
 #pragma unroll
-                                for (int i = 0; i < W - 1; ++i) win[i] = win[i + 1];
-                                win[W > 0 ? W - 1 : 0] = v;
-                                if (usable >= W) {
+                                for (int i = 0; i < W - 1; ++i) st.win[i] = st.win[i + 1];
+                                st.win[W > 0 ? W - 1 : 0] = v;
+                                if (st.usable >= W) {
                                     agree = 0;
 #pragma unroll
-                                    for (int i = 0; i < W; ++i) agree += win[i] == v ? 1 : 0;
+                                    for (int i = 0; i < W; ++i) agree += st.win[i] == v ? 1 : 0;
                                 }
-                            } else if (usable >= p.w) {
-                                // generic window: scan back over the last w usable probes
+                            } else if (st.usable >= p.w) {
+                                // runtime window: scan back over the last w usable probes
                                 agree = 0;
                                 int32_t seen = 0;
                                 for (int32_t qq = static_cast<int32_t>(q); qq >= 0 && seen < p.w; --qq) {
-                                    const uint64_t hw2 = __ldg(p.hes + r * p.hw + (qq >> 6));
-                                    if ((hw2 >> (qq & 63)) & 1ull) continue;
+                                    const uint64_t h2 = __ldg(p.hes + r * p.hw + (qq >> 6));
+                                    if ((h2 >> (qq & 63)) & 1ull) continue;
                                     ++seen;
-                                    uint32_t x;
-                                    if (TMA) {
-                                        const uint32_t bb = qq >> 5, cc = (qq & 31) >> 2, ee = qq & 3;
-                                        x = *reinterpret_cast<const uint32_t*>(tsm + bb * p.rows * 128u +
-                                                                               swz128(tid, cc) + ee * 4);
-                                    } else {
-                                        x = __ldg(p.ids + r * P + qq);
-                                    }
-                                    agree += x == v ? 1 : 0;
+                                    agree += cot_id<W, TMA>(p, tsm, tid, r, static_cast<uint32_t>(qq)) == v ? 1 : 0;
                                 }
                             }
                             if (agree >= 0) {
-                                last_agree = agree;
+                                st.last_agree = agree;
                                 if (!done && agree >= p.amin) {  // C >= tau: exit certain
                                     done = true;
-                                    ex = static_cast<int32_t>(q);
-                                    why = CDX_EXIT_CERTAIN;
-                                    fid = v;  // the terminating record's answer
-                                    low = 0;
+                                    cstep = static_cast<int32_t>(q);
+                                    cid = v;  // the terminating record's answer
                                 }
                             }
                         }
-                        if (p.ck) {
-                            const double cv = last_agree < 0 ? 0.0
-                                                             : __ddiv_rn(static_cast<double>(last_agree),
-                                                                         static_cast<double>(p.w));
+                        if (CK) {
+                            const double cv = st.last_agree < 0
+                                                  ? 0.0
+                                                  : __ddiv_rn(static_cast<double>(st.last_agree),
+                                                              static_cast<double>(p.w));
                             p.ck[r * P + q] = static_cast<float>(cv);
-                        }
-                        if (!done && static_cast<int32_t>(q) == bstep) {  // token budget exhausted
-                            done = true;
-                            ex = static_cast<int32_t>(q);
-                            why = CDX_EXIT_BUDGET;
-                            fid = has_nh ? last_nh : v;  // latest non-hesitant, else latest
-                            low = has_nh ? 0 : 1;
-                        }
-                        if (!done && q == P - 1) {  // never exited: final answer of the full trace
-                            fid = has_nh ? last_nh : v;
-                            low = has_nh ? 0 : 1;
+                            if (static_cast<int32_t>(q) == bstep) {
+                                b_nh = st.last_nh;
+                                b_has = st.has_nh;
+                            }
                         }
                     }
                 }
+            }
+            if (!CK) {
+                b_nh = st.last_nh;
+                b_has = st.has_nh;
+            }
+            int32_t ex = -1;
+            uint8_t why = CDX_EXIT_CONTINUE;
+            uint32_t fid;
+            uint8_t low = 0;
+            if (cstep >= 0 && (bstep < 0 || cstep <= bstep)) {
+                ex = cstep;
+                why = CDX_EXIT_CERTAIN;
+                fid = cid;
+            } else if (bstep >= 0) {  // token budget exhausted at bstep
+                ex = bstep;
+                why = CDX_EXIT_BUDGET;
+                // latest non-hesitant answer up to bstep, else the latest answer
+                fid = b_has ? b_nh : cot_id<W, TMA>(p, tsm, tid, r, static_cast<uint32_t>(bstep));
+                low = b_has ? 0 : 1;
+            } else {  // never exited: final answer of the full trace (criteria_external)
+                fid = st.has_nh ? st.last_nh : cot_id<W, TMA>(p, tsm, tid, r, P - 1);
+                low = st.has_nh ? 0 : 1;
             }
             p.exit_step[r] = ex;
             p.reason[r] = why;
@@ -203,18 +238,33 @@ __global__ void __launch_bounds__(128) cot_exit_kernel(const __grid_constant__ C
                 const uint64_t nt = tile + static_cast<uint64_t>(p.stages) * stride;
                 if (nt < p.ntiles) issue(nt, stage);
             }
+            if (++stage == p.stages) {
+                stage = 0;
+                parity ^= 1u;
+            }
         }
     }
 }
 
+template <int W, bool TMA, bool CK>
+static void launch_cot_k(cdx_ctx* ctx, const CotParams& p, size_t smem) {
+    auto k = cot_exit_kernel<W, TMA, CK>;
+    if (TMA) cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, p.rows, TMA ? smem : 0);
+    if (per_sm < 1) per_sm = 1;
+    const uint64_t grid = std::min<uint64_t>(p.ntiles, static_cast<uint64_t>(ctx->sm_count) * per_sm);
+    k<<<static_cast<unsigned>(grid), p.rows, TMA ? smem : 0, ctx->stream>>>(p);
+}
+
 template <int W>
-static void launch_cot(const CotParams& p, bool tma, unsigned grid, size_t smem, cudaStream_t st) {
+static void launch_cot(cdx_ctx* ctx, const CotParams& p, bool tma, bool ck, size_t smem) {
     if (tma) {
-        cudaFuncSetAttribute(cot_exit_kernel<W, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             static_cast<int>(smem));
-        cot_exit_kernel<W, true><<<grid, p.rows, smem, st>>>(p);
+        if (ck) launch_cot_k<W, true, true>(ctx, p, smem);
+        else launch_cot_k<W, true, false>(ctx, p, smem);
     } else {
-        cot_exit_kernel<W, false><<<grid, p.rows, 0, st>>>(p);
+        if (ck) launch_cot_k<W, false, true>(ctx, p, smem);
+        else launch_cot_k<W, false, false>(ctx, p, smem);
     }
 }
 
@@ -265,12 +315,19 @@ extern "C" int cdx_cot_exit(cdx_ctx* ctx, const uint32_t* ids, const uint64_t* h
         p.bstep_implicit = (k - 1 < static_cast<int64_t>(P)) ? static_cast<int32_t>(k - 1) : -1;
     }
     bool tma = (P % 4 == 0) && (reinterpret_cast<uintptr_t>(ids) % 16 == 0) && P <= 512 && R <= 0x7fffffffull;
-    uint32_t rows = 128;
+    // rows (= threads) per CTA and ring depth: small single-stage CTAs keep ~28 warps
+    // per SM resident; other CTAs on the SM overlap each one's TMA wait (tuned on B200)
+    uint32_t rows = 64, stages = 1;
+    if (const char* e = getenv("CDX_COT_ROWS")) rows = static_cast<uint32_t>(atoi(e));
+    if (const char* e = getenv("CDX_COT_STAGES")) stages = static_cast<uint32_t>(atoi(e));
+    rows = std::max<uint32_t>(32, std::min<uint32_t>(128, rows / 32 * 32));
+    stages = std::max<uint32_t>(1, std::min<uint32_t>(COT_MAX_STAGES, stages));
     if (tma) {
-        while (rows > 32 && static_cast<uint64_t>(rows) * p.boxes * 128u > 65536u) rows -= 32;
+        while (rows > 32 && static_cast<uint64_t>(rows) * p.boxes * 128u * stages > 96u * 1024u) rows -= 32;
+        while (stages > 1 && static_cast<uint64_t>(rows) * p.boxes * 128u * stages > 200u * 1024u) --stages;
         p.rows = rows;
         p.stage_bytes = rows * p.boxes * 128u;
-        p.stages = std::max<uint32_t>(1, std::min<uint32_t>(COT_MAX_STAGES, (192u * 1024u) / p.stage_bytes));
+        p.stages = stages;
         tma = encode_tmap_2d(&p.tmap, ids, P, R, static_cast<uint64_t>(P) * 4u, 32, rows,
                              CU_TENSOR_MAP_DATA_TYPE_UINT32, CU_TENSOR_MAP_SWIZZLE_128B);
     }
@@ -281,19 +338,17 @@ extern "C" int cdx_cot_exit(cdx_ctx* ctx, const uint32_t* ids, const uint64_t* h
     }
     p.ntiles = (R + p.rows - 1) / p.rows;
     const size_t smem = tma ? static_cast<size_t>(p.stages) * p.stage_bytes + 1024 + 8 * COT_MAX_STAGES : 0;
-    int per_sm = 2;
-    const uint64_t grid = std::min<uint64_t>(p.ntiles, static_cast<uint64_t>(ctx->sm_count) * (tma ? per_sm : 8));
-    const unsigned g = static_cast<unsigned>(grid);
+    const bool want_ck = ck != nullptr;
     switch (cfg->window) {
-        case 1: launch_cot<1>(p, tma, g, smem, ctx->stream); break;
-        case 2: launch_cot<2>(p, tma, g, smem, ctx->stream); break;
-        case 3: launch_cot<3>(p, tma, g, smem, ctx->stream); break;
-        case 4: launch_cot<4>(p, tma, g, smem, ctx->stream); break;
-        case 5: launch_cot<5>(p, tma, g, smem, ctx->stream); break;
-        case 6: launch_cot<6>(p, tma, g, smem, ctx->stream); break;
-        case 7: launch_cot<7>(p, tma, g, smem, ctx->stream); break;
-        case 8: launch_cot<8>(p, tma, g, smem, ctx->stream); break;
-        default: launch_cot<0>(p, tma, g, smem, ctx->stream); break;
+        case 1: launch_cot<1>(ctx, p, tma, want_ck, smem); break;
+        case 2: launch_cot<2>(ctx, p, tma, want_ck, smem); break;
+        case 3: launch_cot<3>(ctx, p, tma, want_ck, smem); break;
+        case 4: launch_cot<4>(ctx, p, tma, want_ck, smem); break;
+        case 5: launch_cot<5>(ctx, p, tma, want_ck, smem); break;
+        case 6: launch_cot<6>(ctx, p, tma, want_ck, smem); break;
+        case 7: launch_cot<7>(ctx, p, tma, want_ck, smem); break;
+        case 8: launch_cot<8>(ctx, p, tma, want_ck, smem); break;
+        default: launch_cot<0>(ctx, p, tma, want_ck, smem); break;
     }
     CDX_CHECK_LAUNCH(ctx, "cot_exit");
     return CDX_OK;

@@ -5,163 +5,201 @@
 // of ProgramDriver::update_certaindex (runtime.cpp:266-271) evaluated at every probe step.
 //
 // Data path (HBM-bound; no tensor cores: nothing here is a contraction):
-//   ids u32[R][P][S] --(cp.async.bulk, 3-stage mbarrier ring, evict-first)--> smem tile of
-//   whole requests --> one warp per group of 32 rows:
-//     __match_any_sync over the row's S lanes = exact-match clusters; the lowest lane of a
-//     match set is the cluster's first-seen answer (cluster order of metrics.cpp:29-31);
-//     ballot of leaders + popc(match) = cluster sizes;
-//   --> per-row ordered FP64 fold h -= term[size] in first-seen order (term[c] =
-//     (c/S)*log(c/S) built on the host with the reference's libm, so the device performs
-//     only IEEE subtract/divide and reproduces the reference bits), clamp, thresholds on the
-//     FP64 value, fp32 store + one meets word per 32 rows.
+//   ids u32[R][P][S] is cut into GROUPS of 32 consecutive probe rows of one request
+//   (<= 4 KB, contiguous).  Every warp streams its own groups through a private ring of
+//   shared-memory stages filled by 1-D bulk copies (cp.async.bulk, evict-first, one
+//   mbarrier per stage): no CTA-wide barrier, so warps never wait for each other.
+//   Per group: __match_any_sync over each row's S lanes = exact-match clusters; the lowest
+//   lane of a match set is the cluster's first-seen answer (cluster order of metrics.cpp:
+//   29-31) and popc(match) its size.  The owner lane of each row then folds the entropy in
+//   FP64 in first-seen order: h -= term[size], with term[c] = (c/S)*log(c/S) built on the
+//   host with the reference's libm, so the device only does IEEE subtract/divide and
+//   reproduces the reference bits; clamp; thresholds on the FP64 value; fp32 store and one
+//   meets word per group.
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <vector>
 
-#include "cdx_internal.cuh"
+#include "k_sc.cuh"
 
 namespace cdx {
 
-constexpr int SC_THREADS = 256;
-constexpr int SC_WARPS = SC_THREADS / 32;
-constexpr int SC_MAX_STAGES = 3;
-constexpr int MAX_TH = 8;
-
-struct ScParams {
-    const uint32_t* ids;
-    float* hcert;
-    uint32_t* meets;
-    uint64_t R;
-    uint64_t ntiles;
-    uint32_t P, S, words, q;  // words = ceil(P/32); q = requests per tile
-    uint32_t tile_stride;     // bytes between smem stages
-    uint32_t stages;
-    int bulk_ok;
-    int n_th;
-    uint8_t th_dir[MAX_TH];
-    double th_cut[MAX_TH];
-    double term[33];
-    double logn;
-};
-
-__device__ __forceinline__ bool sc_tile_bulk(const ScParams& p, uint32_t nreq) {
-    return p.bulk_ok && ((static_cast<uint64_t>(nreq) * p.P * p.S * 4u) % 16u == 0);
-}
-
-__global__ void __launch_bounds__(SC_THREADS, 2) sc_certaindex_kernel(const __grid_constant__ ScParams p) {
-    extern __shared__ __align__(128) uint8_t smem[];
-    uint8_t* cnt_all = smem + p.stages * p.tile_stride;          // [warp][leader s][row] u8
-    double* term = reinterpret_cast<double*>(cnt_all + SC_WARPS * 1024);
-    uint64_t* bar = reinterpret_cast<uint64_t*>(term + 34);
-
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    if (tid < 33) term[tid] = p.term[tid];
-    if (tid == 0) {
-        for (uint32_t s = 0; s < p.stages; ++s) mbar_init(&bar[s], 1);
-        fence_mbar_init();
-    }
-    __syncthreads();
-
-    const uint64_t policy = policy_evict_first();
-    const uint64_t stride = gridDim.x;
-    auto issue = [&](uint64_t tile, uint32_t stage) {
-        const uint64_t r0 = tile * p.q;
-        const uint32_t nreq = static_cast<uint32_t>((p.R - r0 < p.q ? p.R - r0 : static_cast<uint64_t>(p.q)));
-        if (!sc_tile_bulk(p, nreq)) return;
-        const uint32_t bytes = nreq * p.P * p.S * 4u;
-        mbar_expect_tx(&bar[stage], bytes);
-        bulk_g2s(smem + stage * p.tile_stride, p.ids + r0 * p.P * p.S, bytes, &bar[stage], policy);
-    };
-    if (tid == 0) {
-        for (uint32_t s = 0; s < p.stages; ++s) {
-            const uint64_t t = blockIdx.x + s * stride;
-            if (t < p.ntiles) issue(t, s);
-        }
-    }
-
-    const uint32_t S = p.S;
+// One warp, one group of up to 32 rows of one request: cluster every row with a warp
+// match, then fold each row's entropy on its owner lane (lane == row within the group).
+// SCT = compile-time S (a divisor of 32: 1,2,4,8,16,32), or 0 for a runtime S <= 32.
+//
+// Cluster sizes travel through shared memory as one byte per (row, sample): the cluster's
+// size at its first-seen sample, 0 elsewhere ([row][32] bytes per warp).  The owner lane
+// then walks its row's nonzero bytes in sample order = first-seen cluster order.  The
+// byte stores of one row land in one 32-byte segment (no bank conflicts).
+template <int SCT>
+__device__ __forceinline__ void sc_group(const ScParams& p, const uint32_t* __restrict__ base, uint32_t rows,
+                                         uint8_t* __restrict__ cntw, const double* __restrict__ term, uint32_t lane,
+                                         uint64_t req, uint32_t row0, uint32_t g) {
+    const uint32_t S = SCT ? static_cast<uint32_t>(SCT) : p.S;
     const uint32_t rpi = 32u / S;  // rows per match iteration
-    const uint32_t smask = S == 32 ? 0xffffffffu : ((1u << S) - 1u);
+    const uint32_t smask = S >= 32 ? 0xffffffffu : ((1u << S) - 1u);
     const uint32_t sub = lane / S, s = lane - sub * S;
     const bool lane_ok = sub < rpi;
     const uint32_t subm = lane_ok ? (smask << (sub * S)) : 0u;
-    uint8_t* cntw = cnt_all + warp * 1024;
-
-    uint32_t it_count = 0;
-    for (uint64_t tile = blockIdx.x; tile < p.ntiles; tile += stride, ++it_count) {
-        const uint32_t stage = it_count % p.stages;
-        const uint32_t parity = (it_count / p.stages) & 1u;
-        const uint64_t r0 = tile * p.q;
-        const uint32_t nreq = static_cast<uint32_t>((p.R - r0 < p.q ? p.R - r0 : static_cast<uint64_t>(p.q)));
-        const uint32_t* tids = reinterpret_cast<const uint32_t*>(smem + stage * p.tile_stride);
-        if (sc_tile_bulk(p, nreq)) {
-            mbar_wait(&bar[stage], parity);
-        } else {
-            // unaligned / ragged tail tile: cooperative coalesced loads
-            uint32_t* dst = reinterpret_cast<uint32_t*>(smem + stage * p.tile_stride);
-            const uint32_t n = nreq * p.P * S;
-            const uint32_t* src = p.ids + r0 * p.P * S;
-            for (uint32_t i = tid; i < n; i += SC_THREADS) dst[i] = __ldg(src + i);
-            __syncthreads();
+    const uint32_t ltm = (1u << lane) - 1u;  // lanes below me
+    uint8_t* my_cnt = cntw + sub * 32u + s;  // byte (row = it*rpi + sub, sample s)
+    if (SCT != 0 && rows == 32) {
+        // full group, S | 32: row (it*rpi + sub) element s sits at word it*32 + lane
+#pragma unroll 8
+        for (uint32_t it = 0; it < static_cast<uint32_t>(SCT ? SCT : 1); ++it) {
+            const uint32_t m = __match_any_sync(0xffffffffu, base[it * 32u + lane]) & subm;
+            const bool leader = (m & ltm) == 0u;  // first-seen answer of its cluster
+            my_cnt[it * rpi * 32u] = leader ? static_cast<uint8_t>(__popc(m)) : uint8_t(0);
         }
-
-        const uint32_t groups = nreq * p.words;
-        for (uint32_t gi = warp; gi < groups; gi += SC_WARPS) {
-            const uint32_t req = gi / p.words;
-            const uint32_t g = gi - req * p.words;
-            const uint32_t row0 = g * 32u;
-            const uint32_t rows = min(32u, p.P - row0);
-            const uint32_t* base = tids + (req * p.P + row0) * S;
-            const uint32_t iters = (rows + rpi - 1) / rpi;
-            uint32_t my_lm = 0;
-#pragma unroll 4
-            for (uint32_t it = 0; it < iters; ++it) {
-                const uint32_t rloc = it * rpi + sub;
-                const bool act = lane_ok && rloc < rows;
-                const uint32_t v = act ? base[rloc * S + s] : 0xffffffffu;
-                const uint32_t m = __match_any_sync(0xffffffffu, v) & subm;
-                const bool leader = act && (static_cast<uint32_t>(__ffs(m) - 1) == static_cast<uint32_t>(lane));
-                const uint32_t lm = __ballot_sync(0xffffffffu, leader);
-                if (leader) cntw[s * 32 + rloc] = static_cast<uint8_t>(__popc(m));
-                if (it == static_cast<uint32_t>(lane) / rpi)
-                    my_lm = (lm >> ((static_cast<uint32_t>(lane) % rpi) * S)) & smask;
-            }
-            __syncwarp();
-            bool meets = false;
-            if (static_cast<uint32_t>(lane) < rows) {
-                double hc = 1.0;  // metrics.cpp:121: a single path is fully certain
-                if (S > 1) {
-                    double h = 0.0;
-                    uint32_t bits = my_lm;
-                    while (bits) {
-                        const uint32_t l = __ffs(bits) - 1;
-                        bits &= bits - 1;
-                        h = __dsub_rn(h, term[cntw[l * 32 + lane]]);  // h -= p*log(p)
+    } else {
+        const uint32_t iters = (rows + rpi - 1) / rpi;
+        for (uint32_t it = 0; it < iters; ++it) {
+            const uint32_t rloc = it * rpi + sub;
+            const bool act = lane_ok && rloc < rows;
+            const uint32_t v = act ? base[rloc * S + s] : 0xffffffffu;
+            const uint32_t m = __match_any_sync(0xffffffffu, v) & subm;
+            const bool leader = (m & ltm) == 0u;
+            if (act) my_cnt[it * rpi * 32u] = leader ? static_cast<uint8_t>(__popc(m)) : uint8_t(0);
+        }
+    }
+    __syncwarp();
+    bool meets = false;
+    if (lane < rows) {
+        double hc = 1.0;  // metrics.cpp:121: a single path is fully certain
+        const uint4* rowp = reinterpret_cast<const uint4*>(cntw + lane * 32u);
+        const uint4 a = rowp[0];
+        // one cluster holding every answer: H = -(1*log 1) = 0 exactly, so H~ = 1 exactly
+        if (S > 1 && (a.x & 0xffu) != S) {
+            const uint4 b = S > 16 ? rowp[1] : make_uint4(0, 0, 0, 0);
+            const uint32_t wv[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+            double h = 0.0;
+            if (SCT != 0) {
+                // Branch-free fold over every sample slot in order: term[0] = +0.0 and h >= 0,
+                // so a non-leader slot subtracts +0.0, which leaves h bit-identical.  (Data-
+                // dependent loops here cost divergence-unit cycles that the match needs.)
+#pragma unroll
+                for (uint32_t k = 0; k < 8; ++k) {
+                    if (k * 4u >= S) break;
+#pragma unroll
+                    for (uint32_t j = 0; j < 4; ++j) {
+                        if (k * 4u + j >= S) break;
+                        h = __dsub_rn(h, term[__byte_perm(wv[k], 0, 0x4440 + j)]);  // h -= p*log(p)
                     }
-                    h = (0.0 < h) ? h : 0.0;  // std::max(0.0, h)
-                    const double v = __ddiv_rn(__dsub_rn(p.logn, h), p.logn);
-                    hc = v < 0.0 ? 0.0 : (1.0 < v ? 1.0 : v);  // std::clamp
                 }
-                meets = true;
-                for (int t = 0; t < p.n_th; ++t) {
-                    const bool ok = p.th_dir[t] == CDX_DIR_GE ? hc >= p.th_cut[t] : hc <= p.th_cut[t];
-                    meets = meets && ok;
+            } else {
+#pragma unroll
+                for (uint32_t k = 0; k < 8; ++k) {
+                    if (k * 4u >= S) break;
+                    // keep only the bytes of samples < S (the rest of the 32-byte row is stale)
+                    const uint32_t keep = S >= k * 4u + 4u ? 0xffffffffu : ((1u << ((S - k * 4u) * 8u)) - 1u);
+                    uint32_t x = wv[k] & keep;
+                    while (x) {  // nonzero bytes in sample order = first-seen cluster order
+                        const uint32_t sh = static_cast<uint32_t>(__ffs(x) - 1) & ~7u;
+                        const uint32_t c = (x >> sh) & 0xffu;
+                        x &= ~(0xffu << sh);
+                        h = __dsub_rn(h, term[c]);  // h -= p*log(p), metrics.cpp:113-116
+                    }
                 }
-                if (p.hcert) p.hcert[(r0 + req) * p.P + row0 + lane] = static_cast<float>(hc);
             }
-            const uint32_t mw = __ballot_sync(0xffffffffu, meets);
-            if (lane == 0 && p.meets) p.meets[(r0 + req) * p.words + g] = mw;
+            h = (0.0 < h) ? h : 0.0;  // std::max(0.0, h)
+            const double v = __ddiv_rn(__dsub_rn(p.logn, h), p.logn);
+            hc = v < 0.0 ? 0.0 : (1.0 < v ? 1.0 : v);  // std::clamp
+        }
+        meets = true;
+        for (int t = 0; t < p.n_th; ++t) {
+            const bool ok = p.th_dir[t] == CDX_DIR_GE ? hc >= p.th_cut[t] : hc <= p.th_cut[t];
+            meets = meets && ok;
+        }
+        if (p.hcert) p.hcert[req * p.P + row0 + lane] = static_cast<float>(hc);
+    }
+    const uint32_t mw = __ballot_sync(0xffffffffu, meets);
+    if (lane == 0 && p.meets) p.meets[req * p.words + g] = mw;
+    __syncwarp();
+}
+
+// Warp-autonomous streaming: warp w of the grid owns groups w, w + nwarps, ...; each warp
+// keeps `stages` groups in flight in its private ring.
+template <int SCT>
+__global__ void __launch_bounds__(SC_MAX_WARPS * 32) sc_certaindex_kernel(const __grid_constant__ ScParams p) {
+    extern __shared__ __align__(128) uint8_t smem[];
+    const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const uint32_t nw_cta = blockDim.x >> 5;
+    const uint32_t S = SCT ? static_cast<uint32_t>(SCT) : p.S;
+    // per-warp layout: [stages][4 KB ring] [1 KB counts]; CTA tail: term table, mbarriers
+    uint8_t* wbase = smem + warp * (p.stages * SC_GROUP_BYTES + 1024u);
+    uint8_t* cntw = wbase + p.stages * SC_GROUP_BYTES;
+    double* term = reinterpret_cast<double*>(smem + nw_cta * (p.stages * SC_GROUP_BYTES + 1024u));
+    uint64_t* bar = reinterpret_cast<uint64_t*>(term + 34) + warp * SC_MAX_STAGES;
+
+    if (threadIdx.x < 33) term[threadIdx.x] = p.term[threadIdx.x];
+    if (lane == 0) {
+        for (uint32_t s = 0; s < p.stages; ++s) mbar_init(&bar[s], 1);
+        fence_mbar_init();
+    }
+    __syncthreads();  // the only CTA-wide barrier: term table + barrier init
+
+    const uint64_t policy = policy_evict_first();
+    const uint64_t gw = static_cast<uint64_t>(blockIdx.x) * nw_cta + warp;
+    const uint64_t nwarps = static_cast<uint64_t>(gridDim.x) * nw_cta;
+    // group G = (request, g) with G = request * words + g; walk it incrementally (no 64-bit
+    // divisions in the loop): one step = nwarps groups = (dq requests, dr groups)
+    const uint64_t dq = nwarps / p.words;
+    const uint32_t dr = static_cast<uint32_t>(nwarps - dq * p.words);
+    struct Cursor {
+        uint64_t req;
+        uint32_t g;
+    };
+    auto advance = [&](Cursor& c, uint32_t times) {
+        for (uint32_t i = 0; i < times; ++i) {
+            c.req += dq;
+            c.g += dr;
+            if (c.g >= p.words) {
+                c.g -= p.words;
+                ++c.req;
+            }
+        }
+    };
+    auto issue = [&](const Cursor& c, uint32_t stage) {  // lane 0 only
+        const uint32_t rows = min(32u, p.P - c.g * 32u);
+        mbar_expect_tx(&bar[stage], rows * S * 4u);
+        bulk_g2s(wbase + stage * SC_GROUP_BYTES, p.ids + (c.req * p.P + c.g * 32u) * S, rows * S * 4u, &bar[stage],
+                 policy);
+    };
+    Cursor cur{gw / p.words, static_cast<uint32_t>(gw % p.words)};
+    Cursor pre = cur;  // prefetch cursor, stages groups ahead
+    if (lane == 0 && p.bulk_ok)
+        for (uint32_t s = 0; s < p.stages; ++s) {
+            if (pre.req < p.R) issue(pre, s);
+            advance(pre, 1);
+        }
+
+    uint32_t stage = 0, parity = 0;
+    while (cur.req < p.R) {
+        const uint32_t rows = min(32u, p.P - cur.g * 32u);
+        uint32_t* buf = reinterpret_cast<uint32_t*>(wbase + stage * SC_GROUP_BYTES);
+        if (p.bulk_ok) {  // S % 4 == 0 and aligned base: every group is a 16B-multiple
+            mbar_wait(&bar[stage], parity);
+        } else {  // misaligned base or S % 4 != 0: plain coalesced loads
+            const uint32_t* src = p.ids + (cur.req * p.P + cur.g * 32u) * S;
+            for (uint32_t i = lane; i < rows * S; i += 32) buf[i] = __ldg(src + i);
             __syncwarp();
         }
-        __syncthreads();
-        if (tid == 0) {
-            const uint64_t nt = tile + static_cast<uint64_t>(p.stages) * stride;
-            if (nt < p.ntiles) issue(nt, stage);
+        sc_group<SCT>(p, buf, rows, cntw, term, lane, cur.req, cur.g * 32u, cur.g);
+        // sc_group ends with __syncwarp: every lane is done with this stage's data
+        if (lane == 0 && p.bulk_ok) {
+            if (pre.req < p.R) issue(pre, stage);
+            advance(pre, 1);
+        }
+        advance(cur, 1);
+        if (++stage == p.stages) {
+            stage = 0;
+            parity ^= 1u;
         }
     }
 }
 
-// ---------------------------------------------------------------------------------------
 // Full clusterings per row (façade path of metrics::cluster_exact): one warp per 32/S rows.
 __global__ void cluster_rows_kernel(const uint32_t* __restrict__ ids, uint64_t rows, uint32_t S,
                                     uint32_t* __restrict__ ncl, uint32_t* __restrict__ leader,
@@ -240,6 +278,19 @@ int check_thresholds(cdx_ctx* ctx, const cdx_threshold* th, uint32_t n_th, const
     return CDX_OK;
 }
 
+template <int SCT>
+void launch_sc(cdx_ctx* ctx, const ScParams& p, uint32_t warps_per_cta) {
+    const size_t smem = static_cast<size_t>(warps_per_cta) * (p.stages * SC_GROUP_BYTES + 1024u) + 34 * 8 +
+                        SC_MAX_WARPS * SC_MAX_STAGES * 8;
+    cudaFuncSetAttribute(sc_certaindex_kernel<SCT>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sc_certaindex_kernel<SCT>, warps_per_cta * 32, smem);
+    if (per_sm < 1) per_sm = 1;
+    const uint64_t want = (p.ngroups + warps_per_cta - 1) / warps_per_cta;
+    const uint64_t grid = std::min<uint64_t>(want, static_cast<uint64_t>(ctx->sm_count) * per_sm);
+    sc_certaindex_kernel<SCT><<<static_cast<unsigned>(grid), warps_per_cta * 32, smem, ctx->stream>>>(p);
+}
+
 }  // namespace cdx
 
 extern "C" {
@@ -250,7 +301,7 @@ int cdx_sc_certaindex(cdx_ctx* ctx, const uint32_t* ids, uint64_t R, uint32_t P,
     if (!ctx) return CDX_EINVAL;
     if (S == 0) return set_error(ctx, CDX_EINVAL, "cluster_exact: empty answer set");
     if (S > 32) return set_error(ctx, CDX_EINVAL, "sc_certaindex: at most 32 samples per row");
-    if (P == 0 || P > 4096) return set_error(ctx, CDX_EINVAL, "sc_certaindex: probes must be 1..4096");
+    if (P == 0) return set_error(ctx, CDX_EINVAL, "sc_certaindex: probes must be >= 1");
     if (!ids) return set_error(ctx, CDX_EINVAL, "sc_certaindex: null ids");
     const bool present[4] = {true, false, false, false};
     if (int st = check_thresholds(ctx, th, n_th, present)) return st;
@@ -264,21 +315,14 @@ int cdx_sc_certaindex(cdx_ctx* ctx, const uint32_t* ids, uint64_t R, uint32_t P,
     p.P = P;
     p.S = S;
     p.words = (P + 31) / 32;
-    const uint64_t req_bytes = static_cast<uint64_t>(P) * S * 4u;
-    if (req_bytes > 200u * 1024u)
-        return set_error(ctx, CDX_EINVAL, "sc_certaindex: one request (P*S*4 bytes) exceeds 200 KiB");
-    uint32_t q = static_cast<uint32_t>(32768u / req_bytes);
-    if (q < 1) q = 1;
-    // keep every full tile a multiple of 16 bytes so it can be bulk-copied
-    while ((static_cast<uint64_t>(q) * P * S) % 4u) ++q;
-    if (q * req_bytes > 200u * 1024u) q = 1;
-    p.q = q;
-    p.ntiles = (R + q - 1) / q;
-    const uint64_t tile_bytes = q * req_bytes;
-    p.tile_stride = static_cast<uint32_t>((tile_bytes + 127) / 128 * 128);
-    p.stages = static_cast<uint32_t>(std::min<uint64_t>(SC_MAX_STAGES, (200u * 1024u) / p.tile_stride));
-    if (p.stages < 1) p.stages = 1;
-    p.bulk_ok = (reinterpret_cast<uintptr_t>(ids) % 16 == 0) && ((static_cast<uint64_t>(q) * P * S) % 4 == 0);
+    p.ngroups = R * p.words;
+    p.bulk_ok = (reinterpret_cast<uintptr_t>(ids) % 16 == 0) && (S % 4 == 0);
+    // per-warp ring depth and warps per CTA (tuned on B200: see profiles/)
+    uint32_t stages = 1, wpc = 4;
+    if (const char* e = getenv("CDX_SC_STAGES")) stages = static_cast<uint32_t>(atoi(e));
+    if (const char* e = getenv("CDX_SC_WARPS")) wpc = static_cast<uint32_t>(atoi(e));
+    p.stages = std::max<uint32_t>(1, std::min<uint32_t>(SC_MAX_STAGES, stages));
+    wpc = std::max<uint32_t>(1, std::min<uint32_t>(SC_MAX_WARPS, wpc));
     p.n_th = static_cast<int>(n_th);
     for (uint32_t i = 0; i < n_th; ++i) {
         p.th_dir[i] = th[i].dir;
@@ -288,13 +332,20 @@ int cdx_sc_certaindex(cdx_ctx* ctx, const uint32_t* ids, uint64_t R, uint32_t P,
     for (uint32_t c = 1; c <= S; ++c) p.term[c] = host_term(c, S);
     p.logn = std::log(static_cast<double>(S));
 
-    const size_t smem = static_cast<size_t>(p.stages) * p.tile_stride + SC_WARPS * 1024 + 34 * 8 + 8 * SC_MAX_STAGES;
-    cudaFuncSetAttribute(sc_certaindex_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-    int per_sm = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sc_certaindex_kernel, SC_THREADS, smem);
-    if (per_sm < 1) per_sm = 1;
-    const uint64_t grid = std::min<uint64_t>(p.ntiles, static_cast<uint64_t>(ctx->sm_count) * per_sm);
-    sc_certaindex_kernel<<<static_cast<unsigned>(grid), SC_THREADS, smem, ctx->stream>>>(p);
+    // fast path: TMA-staged groups, warp-match + ALU-peel engines side by side (k_sc_fast.cu)
+    if (launch_sc_fast(ctx, p)) {
+        CDX_CHECK_LAUNCH(ctx, "sc_certaindex(fast)");
+        return CDX_OK;
+    }
+    switch (S) {
+        case 32: launch_sc<32>(ctx, p, wpc); break;
+        case 16: launch_sc<16>(ctx, p, wpc); break;
+        case 8: launch_sc<8>(ctx, p, wpc); break;
+        case 4: launch_sc<4>(ctx, p, wpc); break;
+        case 2: launch_sc<2>(ctx, p, wpc); break;
+        case 1: launch_sc<1>(ctx, p, wpc); break;
+        default: launch_sc<0>(ctx, p, wpc); break;
+    }
     CDX_CHECK_LAUNCH(ctx, "sc_certaindex");
     return CDX_OK;
 }
@@ -333,3 +384,4 @@ int cdx_entropy_from_sizes(cdx_ctx* ctx, const uint32_t* sizes, const uint32_t* 
 }
 
 }  // extern "C"
+

@@ -1,0 +1,37 @@
+// k_sc.cuh — shared declarations of the K2 (Self-Consistency certaindex) kernels.
+#pragma once
+
+#include "cdx_internal.cuh"
+
+namespace cdx {
+
+constexpr int SC_MAX_STAGES = 4;
+constexpr int SC_MAX_WARPS = 8;
+constexpr int MAX_TH = 8;
+constexpr uint32_t SC_GROUP_BYTES = 32u * 32u * 4u;  // 32 rows x S<=32 samples x 4 B
+
+struct ScParams {
+    const uint32_t* ids;
+    float* hcert;
+    uint32_t* meets;
+    uint64_t R;
+    uint64_t ngroups;  // R * words
+    uint32_t P, S, words;
+    uint32_t stages;
+    int bulk_ok;  // base 16B-aligned and S % 4 == 0 (every group is then 16B-aligned)
+    int n_th;
+    uint8_t th_dir[MAX_TH];
+    double th_cut[MAX_TH];
+    double term[33];
+    double logn;
+};
+
+// The TMA fast path (S in {4,8,16,32}, P % 32 == 0, 16B-aligned ids).  Returns true when
+// it launched; false when the shape needs the generic warp-match kernel.
+bool launch_sc_fast(cdx_ctx* ctx, const ScParams& p);
+
+// Validate a threshold list against the signals an entry point produces (present[kind]);
+// an absent signal fails with the reference's message (metrics.cpp:163-166).
+int check_thresholds(cdx_ctx* ctx, const cdx_threshold* th, uint32_t n_th, const bool present[4]);
+
+}  // namespace cdx

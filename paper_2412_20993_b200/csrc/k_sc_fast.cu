@@ -1,0 +1,254 @@
+// k_sc_fast.cu — K2 fast path: Self-Consistency certaindex with BOTH cluster engines of
+// the SM running at once.
+//
+// Shapes: S in {4,8,16,32}, P % 32 == 0, 16B-aligned ids (configs A and C).  The ids
+// tensor is viewed as 128-byte lines ([R*P*S/32][32] u32); a GROUP = 32 probe rows of one
+// request = S lines starting at line G*S, staged by one TMA box load into a 128B-swizzled
+// shared buffer (conflict-free 16-byte reads for both engines).
+//
+// Two engines, measured on B200 (tools/mb_match.cu, profiles/):
+//   * warp-match engine: one __match_any_sync per row (lane = sample); the lowest lane of a
+//     match set is the cluster's first-seen answer, popc the size.  MATCH.ANY executes on
+//     the divergence unit (ADU) at ~4 + 1.5 cycles per distinct value per SM, so this
+//     engine alone is ADU-bound (~1.9 ms on config C).
+//   * ALU peel engine: lane = row; the row's S ids sit in registers and clusters are
+//     peeled in first-seen order (first unassigned sample = next leader, S compares per
+//     cluster).  ALU-pipe-bound (~1.9 ms on config C alone).
+// The pipes are independent, so warps of a CTA are split between the engines and pull
+// groups from one global work counter: each engine runs at its own speed and together
+// they move the kernel to the HBM roofline.
+//
+// Both produce, per row, the first-seen-ordered cluster sizes folded in FP64 exactly as
+// metrics.cpp:107-125 (h -= term[size], term[c] = (c/S)*log(c/S) from the host libm;
+// max(0,h); clamp((log n - h)/log n)), thresholds on the FP64 value (metrics.cpp:159-171),
+// an fp32 store and one meets word per group.
+#include <algorithm>
+#include <cstdlib>
+#include <string>
+
+#include "k_sc.cuh"
+
+namespace cdx {
+namespace {
+
+constexpr uint32_t FAST_WARPS = 8;  // max warps per CTA
+
+// bit e set iff x[e] == v; four independent accumulators keep the dependency chains short
+template <int S>
+__device__ __forceinline__ uint32_t eq_mask(const uint32_t (&x)[S], uint32_t v) {
+    uint32_t a0 = 0, a1 = 0, a2 = 0, a3 = 0;
+#pragma unroll
+    for (uint32_t e = 0; e < S; e += 4) {
+        a0 |= (x[e] == v ? 1u : 0u) << e;
+        a1 |= (x[e + 1] == v ? 2u : 0u) << e;
+        a2 |= (x[e + 2] == v ? 4u : 0u) << e;
+        a3 |= (x[e + 3] == v ? 8u : 0u) << e;
+    }
+    return (a0 | a1) | (a2 | a3);
+}
+
+// byte offset of flat 16-byte chunk f of a 128B-swizzled group buffer (line f/8)
+__device__ __forceinline__ uint32_t chunk_addr(uint32_t f) { return (f >> 3) * 128u + (((f & 7u) ^ ((f >> 3) & 7u)) << 4); }
+// byte offset of flat u32 element fe
+__device__ __forceinline__ uint32_t elem_addr(uint32_t fe) { return chunk_addr(fe >> 2) + (fe & 3u) * 4u; }
+
+__device__ __forceinline__ double finish_entropy(double h, double logn) {
+    h = (0.0 < h) ? h : 0.0;  // std::max(0.0, h)
+    const double v = __ddiv_rn(__dsub_rn(logn, h), logn);
+    return v < 0.0 ? 0.0 : (1.0 < v ? 1.0 : v);  // std::clamp(v, 0, 1)
+}
+
+// ALU peel engine: lane owns row `lane` of the group.
+template <int S>
+__device__ __forceinline__ double alu_row(const uint8_t* __restrict__ buf, const double* __restrict__ term,
+                                          uint32_t lane, double logn) {
+    uint32_t x[S];
+#pragma unroll
+    for (uint32_t j = 0; j < S / 4; ++j) {
+        const uint4 v = *reinterpret_cast<const uint4*>(buf + chunk_addr(lane * (S / 4) + j));
+        x[4 * j] = v.x;
+        x[4 * j + 1] = v.y;
+        x[4 * j + 2] = v.z;
+        x[4 * j + 3] = v.w;
+    }
+    uint32_t un = S >= 32 ? 0xffffffffu : ((1u << S) - 1u);
+    // first cluster: its leader is sample 0
+    uint32_t eq = eq_mask<S>(x, x[0]);
+    un &= ~eq;
+    if (un == 0) return 1.0;  // one cluster holds every answer: H = 0, H~ = 1 exactly
+    double h = __dsub_rn(0.0, term[__popc(eq)]);
+    while (un) {
+        const uint32_t l = __ffs(un) - 1;  // first unassigned sample = next cluster's leader
+        const uint32_t v = *reinterpret_cast<const uint32_t*>(buf + elem_addr(lane * S + l));
+        eq = eq_mask<S>(x, v);
+        un &= ~eq;
+        h = __dsub_rn(h, term[__popc(eq)]);  // h -= p*log(p), first-seen order
+    }
+    return finish_entropy(h, logn);
+}
+
+// warp-match engine: lane = sample of the rows of one match iteration; the fold runs on
+// the row's owner lane over the [row][32]-byte size table (0 = not a leader).
+template <int S>
+__device__ __forceinline__ double match_rows(const uint8_t* __restrict__ buf, uint8_t* __restrict__ cntw,
+                                             const double* __restrict__ term, uint32_t lane, double logn) {
+    constexpr uint32_t rpi = 32u / S;
+    constexpr uint32_t smask = S >= 32 ? 0xffffffffu : ((1u << S) - 1u);
+    const uint32_t sub = lane / S, s = lane - sub * S;
+    const uint32_t subm = smask << (sub * S);
+    const uint32_t ltm = (1u << lane) - 1u;
+#pragma unroll 8
+    for (uint32_t it = 0; it < 32u / rpi; ++it) {
+        const uint32_t row = it * rpi + sub;
+        const uint32_t v = *reinterpret_cast<const uint32_t*>(buf + elem_addr(row * S + s));
+        const uint32_t m = __match_any_sync(0xffffffffu, v) & subm;
+        cntw[row * 32u + s] = (m & ltm) == 0u ? static_cast<uint8_t>(__popc(m)) : uint8_t(0);
+    }
+    __syncwarp();
+    const uint4* rowp = reinterpret_cast<const uint4*>(cntw + lane * 32u);
+    const uint4 a = rowp[0];
+    if ((a.x & 0xffu) == S) return 1.0;  // sample 0's cluster holds every answer
+    const uint4 b = S > 16 ? rowp[1] : make_uint4(0, 0, 0, 0);
+    const uint32_t wv[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+    // branch-free fold over every slot in sample order: term[0] = +0.0 and h >= 0, so a
+    // non-leader slot leaves h bit-identical
+    double h = 0.0;
+#pragma unroll
+    for (uint32_t k = 0; k < S / 4; ++k)
+#pragma unroll
+        for (uint32_t j = 0; j < 4; ++j) h = __dsub_rn(h, term[__byte_perm(wv[k], 0, 0x4440 + j)]);
+    return finish_entropy(h, logn);
+}
+
+template <int S>
+__global__ void __launch_bounds__(FAST_WARPS * 32) sc_fast_kernel(const __grid_constant__ CUtensorMap tmap,
+                                                                  const __grid_constant__ ScParams p,
+                                                                  unsigned long long* __restrict__ counter,
+                                                                  uint32_t match_warps) {
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    // 128B-swizzled TMA destinations need 1024-byte alignment (offset the shared array, do
+    // not cast through an integer, so every access stays an LDS)
+    uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+    constexpr uint32_t GB = 32u * S * 4u;  // group bytes
+    const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const uint32_t nw_cta = blockDim.x >> 5;
+    const uint32_t ring = p.stages * GB;
+    uint8_t* wbase = smem + warp * ring;
+    uint8_t* cnt_all = smem + nw_cta * ring;  // [warp][32 rows][32 B]
+    uint8_t* cntw = cnt_all + warp * 1024u;
+    double* term = reinterpret_cast<double*>(cnt_all + nw_cta * 1024u);
+    uint64_t* bar = reinterpret_cast<uint64_t*>(term + 34) + warp * SC_MAX_STAGES;
+    unsigned long long* qG = reinterpret_cast<unsigned long long*>(term + 34 + FAST_WARPS * SC_MAX_STAGES) +
+                             warp * SC_MAX_STAGES;
+
+    if (threadIdx.x < 33) term[threadIdx.x] = p.term[threadIdx.x];
+    if (lane == 0) {
+        if (warp == 0) tma_prefetch_desc(&tmap);
+        for (uint32_t s = 0; s < p.stages; ++s) mbar_init(&bar[s], 1);
+        fence_mbar_init();
+    }
+    __syncthreads();
+
+    const uint64_t policy = policy_evict_first();
+    const bool use_match = warp < match_warps;
+    // lane 0 claims groups from the global counter in chunks of CLAIM (one same-address
+    // atomic per group would serialise at the L2 at ~2 ns each) and starts each TMA load
+    constexpr unsigned long long CLAIM = 16;
+    unsigned long long chunk_next = 0, chunk_end = 0;
+    auto claim_issue = [&](uint32_t stage) {
+        if (chunk_next == chunk_end) {
+            chunk_next = atomicAdd(counter, CLAIM);
+            chunk_end = chunk_next + CLAIM;
+        }
+        const unsigned long long G = chunk_next++;
+        qG[stage] = G;
+        if (G < p.ngroups) {
+            mbar_expect_tx(&bar[stage], GB);
+            tma_load_2d(wbase + stage * GB, &tmap, 0, static_cast<int32_t>(G * S), &bar[stage], policy);
+        }
+    };
+    if (lane == 0)
+        for (uint32_t s = 0; s < p.stages; ++s) claim_issue(s);
+    __syncwarp();
+
+    uint32_t stage = 0, parity = 0;
+    while (true) {
+        const unsigned long long G = qG[stage];
+        if (G >= p.ngroups) break;  // claims are monotone: nothing left for this warp
+        mbar_wait(&bar[stage], parity);
+        const uint8_t* buf = wbase + stage * GB;
+        const double hc = use_match ? match_rows<S>(buf, cntw, term, lane, p.logn)
+                                    : alu_row<S>(buf, term, lane, p.logn);
+        __syncwarp();  // every lane is done with this stage (and with cntw)
+        if (lane == 0) claim_issue(stage);
+        bool meets = true;
+        for (int t = 0; t < p.n_th; ++t) {
+            const bool ok = p.th_dir[t] == CDX_DIR_GE ? hc >= p.th_cut[t] : hc <= p.th_cut[t];
+            meets = meets && ok;
+        }
+        if (p.hcert) p.hcert[G * 32u + lane] = static_cast<float>(hc);
+        const uint32_t mw = __ballot_sync(0xffffffffu, meets);
+        if (lane == 0 && p.meets) p.meets[G] = mw;
+        __syncwarp();  // qG[stage] rewritten by lane 0 is visible before the next lap
+        if (++stage == p.stages) {
+            stage = 0;
+            parity ^= 1u;
+        }
+    }
+}
+
+template <int S>
+void launch_fast(cdx_ctx* ctx, const CUtensorMap& tmap, const ScParams& p, uint32_t wpc, uint32_t match_warps,
+                 unsigned long long* counter) {
+    const size_t smem = 1024 + static_cast<size_t>(wpc) * (p.stages * 32u * S * 4u + 1024u) + 34 * 8 +
+                        FAST_WARPS * SC_MAX_STAGES * 16;
+    cudaFuncSetAttribute(sc_fast_kernel<S>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sc_fast_kernel<S>, wpc * 32, smem);
+    if (per_sm < 1) per_sm = 1;
+    const uint64_t want = (p.ngroups + wpc - 1) / wpc;
+    const uint64_t grid = std::min<uint64_t>(want, static_cast<uint64_t>(ctx->sm_count) * per_sm);
+    sc_fast_kernel<S><<<static_cast<unsigned>(grid), wpc * 32, smem, ctx->stream>>>(tmap, p, counter, match_warps);
+}
+
+}  // namespace
+
+bool launch_sc_fast(cdx_ctx* ctx, const ScParams& p0) {
+    const uint32_t S = p0.S;
+    const uint64_t lines = p0.R * p0.P * S / 32;
+    if (!(S == 4 || S == 8 || S == 16 || S == 32) || p0.P % 32 != 0 ||
+        reinterpret_cast<uintptr_t>(p0.ids) % 16 != 0 || lines >= (1ull << 31))
+        return false;
+    const char* impl = getenv("CDX_SC_IMPL");
+    if (impl && std::string(impl) == "match") return false;
+    CUtensorMap tmap;
+    const uint64_t dims[2] = {32, lines};
+    const uint64_t strides[1] = {128};
+    const uint32_t box[2] = {32, S};
+    if (!encode_tmap(&tmap, p0.ids, 2, dims, strides, box, CU_TENSOR_MAP_DATA_TYPE_UINT32, CU_TENSOR_MAP_SWIZZLE_128B))
+        return false;
+    ScParams p = p0;
+    // warps per CTA, ring depth per warp and how many warps of a CTA run the match engine
+    // (defaults tuned on B200, profiles/)
+    // config C sweep (profiles/r1_sc_tuning.txt): 8 warps x 1 stage, half on each engine
+    uint32_t wpc = 8, stages = 1, mw = 4;
+    if (const char* e = getenv("CDX_SCF_WARPS")) wpc = static_cast<uint32_t>(atoi(e));
+    if (const char* e = getenv("CDX_SCF_STAGES")) stages = static_cast<uint32_t>(atoi(e));
+    if (const char* e = getenv("CDX_SCF_MATCH")) mw = static_cast<uint32_t>(atoi(e));
+    if (impl && std::string(impl) == "alu") mw = 0;
+    if (impl && std::string(impl) == "matchonly") mw = 64;
+    wpc = std::max<uint32_t>(1, std::min<uint32_t>(FAST_WARPS, wpc));
+    p.stages = std::max<uint32_t>(1, std::min<uint32_t>(SC_MAX_STAGES, stages));
+    auto* counter = static_cast<unsigned long long*>(scratch2(ctx, 256));
+    if (!counter) return false;
+    cudaMemsetAsync(counter, 0, sizeof(unsigned long long), ctx->stream);
+    switch (S) {
+        case 32: launch_fast<32>(ctx, tmap, p, wpc, mw, counter); break;
+        case 16: launch_fast<16>(ctx, tmap, p, wpc, mw, counter); break;
+        case 8: launch_fast<8>(ctx, tmap, p, wpc, mw, counter); break;
+        default: launch_fast<4>(ctx, tmap, p, wpc, mw, counter); break;
+    }
+    return true;
+}
+
+}  // namespace cdx

@@ -1,0 +1,123 @@
+"""GPU parity: K1 canon_intern (trim + exact-match interning + hesitation) and K6
+gang_priority / gang_merge vs the oracle (bit-exact ids, flags and orders)."""
+import numpy as np
+import pytest
+
+from oracle import oracle as O
+
+pytestmark = pytest.mark.gpu
+
+
+def _arena(strings):
+    bs = [s.encode() if isinstance(s, str) else s for s in strings]
+    offs = np.zeros(len(bs) + 1, np.uint64)
+    if bs:
+        offs[1:] = np.cumsum([len(b) for b in bs])
+    return np.frombuffer(b"".join(bs) or b"\0", np.uint8).copy(), offs
+
+
+def _intern(ctx, strings, markers=("wait", "hmm")):
+    import torch
+    arena, offs = _arena(strings)
+    ta = torch.from_numpy(arena).cuda()
+    to = torch.from_numpy(offs.view(np.int64)).cuda()
+    ids, hes, first, nu = ctx.canon_intern(ta, to, markers)
+    ctx.sync()
+    return ids.cpu().numpy().view(np.uint32), hes.cpu().numpy(), first.cpu().numpy(), nu
+
+
+@pytest.mark.parametrize("n,vocab", [(1, 3), (10, 3), (5000, 7), (100000, 500), (300000, 40000)])
+def test_intern_parity(ctx, n, vocab):
+    rng = np.random.default_rng(n)
+    base = [f"ans{i}" for i in range(vocab)] + ["wait, 42", "Hmm 7", "HMM", "x  wait", "", "   ", "\t\n"]
+    ws = [" ", "\t", "\n", "\r", "\f", "\v", "", ""]
+    strings = []
+    for k in rng.integers(0, len(base), n):
+        s = base[k]
+        strings.append(ws[rng.integers(0, len(ws))] + s + ws[rng.integers(0, len(ws))])
+    ids, hes, first, nu = _intern(ctx, strings)
+    oid, ohes, onu = O.canon_intern(strings)
+    assert nu == onu
+    assert np.array_equal(ids, oid)
+    assert np.array_equal(hes, ohes)
+    # first_index: arena position of each id's first occurrence
+    for d in range(min(nu, 50)):
+        assert oid[first[d]] == d and (oid[: first[d]] != d).all()
+
+
+def test_intern_spec_examples(ctx):
+    ids, _, _, nu = _intern(ctx, ["12", " 12", "13"])
+    assert ids.tolist() == [0, 0, 1] and nu == 2
+    _, hes, _, _ = _intern(ctx, ["42", "wait, let me check", "Hmm 42", "WAIT"], ("wait", "hmm"))
+    assert hes.tolist() == [0, 1, 1, 1]
+    _, hes, _, _ = _intern(ctx, ["WAIT", "abc"], ("WAIT", ""))  # upper-case / empty markers never match
+    assert hes.tolist() == [0, 0]
+
+
+def _gang_inputs(N, seed, frac_term=0.1, sorted_arrival=True):
+    rng = np.random.default_rng(seed)
+    gaps = rng.exponential(1e-3, N)
+    arrival = np.cumsum(gaps) if sorted_arrival else rng.random(N) * N * 1e-3
+    if not sorted_arrival:
+        arrival[rng.integers(0, N, N // 10)] = arrival[0]  # duplicate arrivals -> id tie-break
+    now = float(arrival.max()) + 1.0
+    last = np.minimum(now, arrival + rng.exponential(0.5, N))
+    cnt = rng.integers(0, 5, N).astype(np.uint32)
+    sums = (rng.integers(32, 512, N) * cnt).astype(np.int64)
+    cap = rng.integers(1, 64, N).astype(np.uint16)
+    knob = np.minimum(cap, rng.integers(0, 64, N)).astype(np.uint16)
+    term = (rng.random(N) < frac_term).astype(np.uint8)
+    return dict(arrival=arrival, last_service=last, iter_tok_sum=sums, iter_count=cnt, knob=knob, cap=cap,
+                terminated=term), now
+
+
+def _to_dev(soa):
+    import torch
+    return {k: torch.from_numpy(np.ascontiguousarray(v)).cuda() if v.dtype != np.uint16 else
+            torch.from_numpy(np.ascontiguousarray(v).view(np.int16)).cuda() for k, v in soa.items()}
+
+
+@pytest.mark.parametrize("N,order,limit,sorted_arrival", [(1, 1, 1.0, True), (1000, 1, 0.7, True),
+                                                          (100000, 1, 0.5, True), (50000, 0, 0.5, True),
+                                                          (70000, 1, 0.9, False), (5000, 0, 100.0, False)])
+def test_gang_parity(ctx, N, order, limit, sorted_arrival):
+    from paper_2412_20993_b200 import InterPolicy
+    soa, now = _gang_inputs(N, N + order, sorted_arrival=sorted_arrival)
+    got, esc, _ = ctx.gang_priority(_to_dev(soa), InterPolicy(order=order, starvation_limit=limit, prior_tokens=128.0),
+                                    now, want_escalated=True)
+    ctx.sync()
+    ref, resc = O.gang_order(soa, order, limit, 128.0, now)
+    assert np.array_equal(esc.cpu().numpy(), resc)
+    assert np.array_equal(got.cpu().numpy().view(np.uint32), ref)
+
+
+def test_gang_merge_equals_single_sort(ctx):
+    """Per-rank sorted runs merged on the device == the one-shot global order (the
+    multi-GPU path: each rank sorts its shard, allgathers keys, merges)."""
+    import torch
+    from paper_2412_20993_b200 import InterPolicy
+    N, ranks = 40000, 4
+    soa, now = _gang_inputs(N, 5)
+    pol = InterPolicy(order=1, starvation_limit=0.6, prior_tokens=128.0)
+    ref, _ = O.gang_order(soa, 1, 0.6, 128.0, now)
+    keys, ids, offs = [], [], [0]
+    for r in range(ranks):
+        sl = slice(r * N // ranks, (r + 1) * N // ranks)
+        part = {k: v[sl] for k, v in soa.items()}
+        o, _, k = ctx.gang_priority(_to_dev(part), pol, now, id_base=sl.start, want_keys=True)
+        keys.append(k)
+        ids.append(o)
+        offs.append(offs[-1] + o.shape[0])
+    out = ctx.gang_merge(torch.cat(keys), torch.cat(ids), torch.tensor(offs, dtype=torch.int64, device="cuda"))
+    ctx.sync()
+    assert np.array_equal(out.cpu().numpy().view(np.uint32), ref)
+
+
+def test_gang_errors(ctx):
+    from paper_2412_20993_b200 import CdxInvalidArgument, InterPolicy
+    soa, now = _gang_inputs(10, 1)
+    with pytest.raises(CdxInvalidArgument, match="starvation_limit"):
+        ctx.gang_priority(_to_dev(soa), InterPolicy(order=1, starvation_limit=0.0), now)
+    soa["arrival"][3] = -1.0
+    with pytest.raises(CdxInvalidArgument, match="finite and >= 0"):
+        ctx.gang_priority(_to_dev(soa), InterPolicy(order=1, starvation_limit=1.0), now)

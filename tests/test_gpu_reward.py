@@ -1,0 +1,111 @@
+"""GPU parity: K4 reward_certaindex (MCTS mean / Rebase max, cumulative) vs the oracle,
+bit-exact on R (fp32 of the FP64 value), H~ and meets bits; overflow (> 8 clusters) and
+the non-TMA path included."""
+import numpy as np
+import pytest
+
+from oracle import oracle as O
+
+pytestmark = pytest.mark.gpu
+
+
+def _run(ctx, rw, ids, agg, th_mean=(), th_max=()):
+    import torch
+    from paper_2412_20993_b200 import Threshold
+    trw = torch.from_numpy(np.ascontiguousarray(rw)).cuda()
+    tid = None if ids is None else torch.from_numpy(np.ascontiguousarray(ids).view(np.int32)).cuda()
+    tagg = torch.from_numpy(np.ascontiguousarray(agg, dtype=np.uint8)).cuda()
+    R, H, meets = ctx.reward_certaindex(trw, tid, tagg, [Threshold(*t) for t in th_mean],
+                                        [Threshold(*t) for t in th_max])
+    ctx.sync()
+    return R.cpu().numpy(), (None if H is None else H.cpu().numpy()), meets.cpu().numpy().view(np.uint32)
+
+
+def _oracle_meets(R64, H, agg, th_mean, th_max):
+    G, T = R64.shape
+    words = (T + 31) // 32
+    out = np.zeros((G, words), np.uint32)
+    for g in range(G):
+        ths = th_max if agg[g] else th_mean
+        for t in range(T):
+            ok = True
+            for sig, cut, d in ths:
+                v = float(np.float64(R64[g, t])) if sig == 1 else float(H64[g, t])
+                ok = ok and (v >= cut if d == 0 else v <= cut)
+            if ok:
+                out[g, t // 32] |= np.uint32(1) << np.uint32(t % 32)
+    return out
+
+
+H64 = None
+
+
+@pytest.mark.parametrize("G,T,W,groups", [(1, 1, 1, 5), (300, 16, 64, 5), (129, 5, 7, 5), (70, 40, 8, 5),
+                                          (200, 16, 64, 40), (64, 3, 32, 200), (513, 16, 4, 3)])
+def test_reward_parity(ctx, G, T, W, groups):
+    global H64
+    g = O.gen_params(seed=G + T + W, groups=groups, conv_hi=max(1, T))
+    rw, ids = O.gen_reward(g, G, T, W)
+    agg = (np.arange(G) % 2).astype(np.uint8)
+    th_mean = [(0, 0.99, 0), (1, 0.4, 0)]   # MCTS/GSM8K
+    th_max = [(0, 0.85, 0), (1, 0.99, 0)]   # Rebase/GSM8K
+    R, H, meets = _run(ctx, rw, ids, agg, th_mean, th_max)
+    R64, R32, Ho = O.reward_certaindex(rw, ids, agg)
+    assert np.array_equal(R.view(np.uint32), R32.view(np.uint32))
+    assert np.array_equal(H.view(np.uint32), Ho.view(np.uint32))
+    # meets: recompute from the oracle's FP64 values (H64 from the reference-pinned entropy)
+    import ctypes as C
+    H64 = np.empty((G, T), np.float64)
+    sizes = (C.c_int * (T * W))()
+    lead = (C.c_int * (T * W))()
+    L = O.lib()
+    L.cdxo_certaindex_entropy.argtypes = [C.c_void_p, C.c_int, C.c_int]
+    for gi in range(G):
+        for t in range(T):
+            n = (t + 1) * W
+            m = L.cdxo_cluster_exact_ids(ids[gi].ravel().ctypes.data_as(C.c_void_p), n, sizes, lead)
+            H64[gi, t] = L.cdxo_certaindex_entropy(sizes, m, n)
+    assert np.array_equal(meets, _oracle_meets(R64, H64, agg, th_mean, th_max))
+
+
+def test_reward_only_mode(ctx):
+    import torch
+    g = O.gen_params(seed=3, conv_hi=16)
+    rw, _ = O.gen_reward(g, 1000, 16, 64)
+    agg = (np.arange(1000) % 3 == 0).astype(np.uint8)
+    R, H, meets = _run(ctx, rw, None, agg, [(1, 0.4, 0)], [(1, 0.99, 0)])
+    _, R32, _ = O.reward_certaindex(rw, None, agg)
+    assert H is None
+    assert np.array_equal(R.view(np.uint32), R32.view(np.uint32))
+
+
+def test_reward_not_on_grid_is_still_exact(ctx):
+    """Arbitrary floats: the device keeps the reference's left fold order, so the mean is
+    bit-identical even when partial sums round."""
+    rng = np.random.default_rng(1)
+    rw = rng.random((257, 9, 12)).astype(np.float32)
+    ids = rng.integers(0, 6, size=(257, 9, 12)).astype(np.uint32)
+    agg = (np.arange(257) % 2).astype(np.uint8)
+    R, H, _ = _run(ctx, rw, ids, agg)
+    _, R32, Ho = O.reward_certaindex(rw, ids, agg)
+    assert np.array_equal(R.view(np.uint32), R32.view(np.uint32))
+    assert np.array_equal(H.view(np.uint32), Ho.view(np.uint32))
+
+
+def test_reward_out_of_range_raises(ctx):
+    from paper_2412_20993_b200 import CdxInvalidArgument
+    rw = np.full((4, 2, 4), 0.5, np.float32)
+    rw[2, 1, 3] = 1.5
+    with pytest.raises(CdxInvalidArgument, match=r"reward outside \[0,1\]"):
+        _run(ctx, rw, None, np.zeros(4, np.uint8))
+
+
+def test_reward_sets_facade(ctx):
+    import torch
+    vals = [[0.9], [0.2, 0.9], [0.2, 0.4, 0.6], [0.5, 0.25, 0.125]]
+    agg = np.array([0, 1, 0, 1], np.uint8)
+    flat = torch.tensor([v for r in vals for v in r], dtype=torch.float64, device="cuda")
+    off = torch.tensor(np.concatenate([[0], np.cumsum([len(r) for r in vals])]), dtype=torch.int64, device="cuda")
+    out = ctx.reward_sets(flat, off, torch.from_numpy(agg).cuda())
+    ctx.sync()
+    assert out.cpu().tolist() == [0.9, 0.9, 0.4000000000000001, 0.5]
