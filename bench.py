@@ -1,22 +1,24 @@
 #!/usr/bin/env python3
-"""bench.py — batched certaindex + early-exit / token-budget decisions on B200.
+"""bench.py — batched certaindex + early-exit / token-budget / gang-priority decisions on B200.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--config C|A|B|D|E] [--impl ours|reference]
 
 Headline workload (BASELINE.json north_star target): config C — Self-Consistency certaindex
 + token-budget allocation over a synthetic trace of 1M requests x 32 samples x 64 probes,
-ids u32[R][P][S] resident in HBM (8.6 GB, > the 126 MB L2, so no flush is needed between
+ids u32[R][P][S] resident in HBM (8.6 GB > the 126 MB L2, so no flush is needed between
 steps).  One step = K2 sc_certaindex (every (r,p) row: exact-match clusters, FP64 entropy
 certaindex, threshold bits) + K5 allocate_scan (static-threshold exit at detect@5, cap 64,
 token budgets, exclusive scan, stable compaction of continuing requests).
+The same JSON line also carries configs A, B, D, E (`other_configs`, N=1 only).
 
 Multi-GPU (torchrun, one process per GPU): requests shard with no data-path collective;
-each rank scores its own 1M-request slice (weak scaling); the only collective is an
-8-byte allgather of shard budget totals for global token offsets.  Time = max over ranks.
+each rank scores its own 1M-request slice (weak scaling); the only collective is an 8-byte
+allgather of shard budget totals for global token offsets.  Time = max over ranks.
 
-Metric: probe-evals/s, one probe-eval = one sampled answer (r,s,p) entering the
-certaindex (BASELINE.md unit "answers/s").  `--impl reference` times the reference's own
-C++ functions (oracle/_ref, compiled from /root/reference/proj/src) on all host cores.
+Metric: probe-evals/s.  One probe-eval = one sampled answer (r,s,p) entering the certaindex
+for SC (A, C), one probe record (r,p) for CoT (B), one node reward (g,t,w) for MCTS/Rebase
+(D), one program ordered for the gang order (E).  `--impl reference` times the reference's
+own C++ functions (oracle/_ref, compiled from /root/reference/proj/src) on all host cores.
 """
 from __future__ import annotations
 
@@ -24,7 +26,6 @@ import argparse
 import json
 import os
 import statistics
-import subprocess
 import sys
 import threading
 import time
@@ -36,80 +37,88 @@ METRIC = "probe-evals/sec + HBM GB/s fraction at 1/2/4/8 B200 vs host-CPU ref"
 UNIT = "probe-evals/s"
 
 CONFIGS = {
-    # north_star target shape (configs[2] of BASELINE.json, sharded per GPU)
-    "C": dict(kind="sc", R=1 << 20, P=64, S=32, tau=0.7, detect=5, cap=64, interval=64, conv_hi=64,
-              desc="SC entropy certaindex + token-budget allocation, 1M req x 32 samples x 64 probes"),
+    # BASELINE.json configs; C is the north_star target shape (sharded per GPU)
     "A": dict(kind="sc", R=1024, P=32, S=16, tau=0.7, detect=5, cap=32, interval=64, conv_hi=32,
               desc="SC entropy certaindex early exit, 1024 queries x 16 samples x 32 probes"),
     "B": dict(kind="cot", R=1 << 20, P=64, w=3, tau=0.9, interval=64, max_tokens=4096, hes=0.05, conv_hi=64,
               desc="CoT probe-window consistency early exit, 1M requests x 64 probes, window 3"),
+    "C": dict(kind="sc", R=1 << 20, P=64, S=32, tau=0.7, detect=5, cap=64, interval=64, conv_hi=64,
+              desc="SC entropy certaindex + token-budget allocation, 1M req x 32 samples x 64 probes"),
+    "D": dict(kind="reward", G=1 << 18, T=16, W=64, conv_hi=16, detect=3,
+              desc="MCTS/Rebase reward + cumulative entropy certaindex, 256K programs x 64 nodes x 16 steps"),
+    "E": dict(kind="gang", N=1 << 22, limit=0.5, prior=128.0,
+              desc="gang-scheduling priority order (escalation + SJF + tie-break), 4M mixed programs"),
 }
+TH_MCTS = [(0, 0.99, 0), (1, 0.4, 0)]   # PAPER.md:963 MCTS/GSM8K thresholds
+TH_REBASE = [(0, 0.85, 0), (1, 0.99, 0)]  # PAPER.md:966 Rebase/GSM8K thresholds
 
 
 def load_peaks():
-    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     try:
-        with open(p) as f:
-            d = json.load(f)
-        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
     except Exception:
         return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
 
 
 class ClockSampler:
     """SM clocks + clock-event (throttle) reasons sampled through NVML every ~2 ms DURING the
-    timed region (the same fields as the recipe's nvidia-smi clocks line)."""
+    timed region (the fields of the recipe's nvidia-smi clocks line)."""
 
-    REASONS = {  # nvmlClocksEventReason* bits
-        0x8: "hw_slowdown", 0x40: "hw_thermal_slowdown", 0x20: "sw_thermal_slowdown", 0x4: "sw_power_cap",
-    }
+    REASONS = {0x8: "hw_slowdown", 0x40: "hw_thermal_slowdown", 0x20: "sw_thermal_slowdown", 0x4: "sw_power_cap"}
 
     def __init__(self, index=0, period=0.002):
-        self.index = index
-        self.period = period
-        self.samples = []
+        self.index, self.period = index, period
+        self.samples, self.max_mhz, self.err = [], None, None
         self._stop = threading.Event()
         self._t = None
-        self.max_mhz = None
-        self.err = None
+
+    def _sample(self):
+        self.samples.append((self._N.nvmlDeviceGetClockInfo(self._h, self._N.NVML_CLOCK_SM), self._rs(self._h)))
 
     def _run(self):
         try:
-            import pynvml as N
-            N.nvmlInit()
-            h = N.nvmlDeviceGetHandleByIndex(self.index)
-            self.max_mhz = N.nvmlDeviceGetMaxClockInfo(h, N.NVML_CLOCK_SM)
             while not self._stop.is_set():
-                sm = N.nvmlDeviceGetClockInfo(h, N.NVML_CLOCK_SM)
-                try:
-                    rs = N.nvmlDeviceGetCurrentClocksEventReasons(h)
-                except AttributeError:
-                    rs = N.nvmlDeviceGetCurrentClocksThrottleReasons(h)
-                self.samples.append((sm, rs))
+                self._sample()
                 self._stop.wait(self.period)
         except Exception as e:  # pragma: no cover - depends on the box
             self.err = repr(e)
 
     def __enter__(self):
+        try:  # NVML init is slow on first use: do it before the timed region starts
+            import pynvml as N
+            N.nvmlInit()
+            self._N = N
+            self._h = N.nvmlDeviceGetHandleByIndex(self.index)
+            self.max_mhz = N.nvmlDeviceGetMaxClockInfo(self._h, N.NVML_CLOCK_SM)
+            self._rs = getattr(N, "nvmlDeviceGetCurrentClocksEventReasons", None) or \
+                N.nvmlDeviceGetCurrentClocksThrottleReasons
+        except Exception as e:  # pragma: no cover - depends on the box
+            self.err = repr(e)
+            return self
         self._t = threading.Thread(target=self._run, daemon=True)
         self._t.start()
-        time.sleep(0.02)
         return self
 
     def __exit__(self, *a):
         self._stop.set()
         if self._t:
             self._t.join(timeout=10)
+        if self._t and not self.samples and self.err is None:
+            try:  # a timed region shorter than one sampling period: take the last sample now
+                self._sample()
+            except Exception as e:  # pragma: no cover
+                self.err = repr(e)
 
     def summary(self):
         if not self.samples:
             return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["unsampled"], "error": self.err}
-        reasons = sorted({name for _, rs in self.samples for bit, name in self.REASONS.items() if rs & bit})
+        reasons = sorted({n for _, rs in self.samples for bit, n in self.REASONS.items() if rs & bit})
         return {"sm_mhz": statistics.median(s for s, _ in self.samples), "sm_max_mhz": self.max_mhz,
                 "reasons": reasons, "samples": len(self.samples)}
 
 
-def dist_setup(n_gpus):
+def dist_setup():
     import torch
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -118,9 +127,8 @@ def dist_setup(n_gpus):
         import torch.distributed as dist
         torch.cuda.set_device(local)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    else:
-        if torch.cuda.is_available():
-            torch.cuda.set_device(0)
+    elif torch.cuda.is_available():
+        torch.cuda.set_device(0)
     return rank, world, local
 
 
@@ -140,41 +148,6 @@ def max_over_ranks(x, world):
     return float(t.item())
 
 
-# --------------------------------------------------------------------------------------
-def cpu_baseline_sc(cfg, nthreads, sample_req, seed):
-    """The reference's own functions (oracle/_ref) on a bounded sample of the workload."""
-    import numpy as np
-
-    from oracle import oracle as O
-    import ctypes as C
-    g = O.gen_params(seed=seed, conv_hi=cfg["conv_hi"])
-    ids = np.empty((sample_req, cfg["P"], cfg["S"]), np.uint32)
-    O.lib().cdxo_gen_sc_mt(C.byref(g), C.c_uint64(0), C.c_uint64(sample_req), C.c_uint32(cfg["P"]),
-                           C.c_uint32(cfg["S"]), ids.ctypes.data_as(C.c_void_p), C.c_int(nthreads))
-    ths = [(0, cfg["tau"], 0)]
-    O.ref_sc_batch(ids[: max(1, sample_req // 64)], 5, ths, nthreads=nthreads)  # warm
-    t0 = time.perf_counter()
-    h, meets = O.ref_sc_batch(ids, 5, ths, nthreads=nthreads)
-    O.allocate_scan(meets, sample_req, cfg["P"], 2, cfg["detect"], cfg["cap"], 1, cfg["interval"] * cfg["S"])
-    dt = time.perf_counter() - t0
-    t1 = time.perf_counter()
-    O.ref_sc_batch(ids, 5, ths, nthreads=nthreads, mode=1, want=False)
-    fill = time.perf_counter() - t1
-    answers = sample_req * cfg["P"] * cfg["S"]
-    return answers / dt, dt, fill
-
-
-def cpu_baseline_cot(cfg, nthreads, sample_req, seed):
-    from oracle import oracle as O
-    g = O.gen_params(seed=seed, conv_hi=cfg["conv_hi"], hesitation_prob=cfg["hes"])
-    ids, hes = O.gen_cot(g, sample_req, cfg["P"])
-    t0 = time.perf_counter()
-    O.ref_cot_batch(ids, hes, 5, cfg["interval"], cfg["w"], cfg["tau"], cfg["max_tokens"], nthreads=nthreads,
-                    want_ck=False)
-    dt = time.perf_counter() - t0
-    return sample_req * cfg["P"] / dt, dt, 0.0
-
-
 def host_threads():
     try:
         return len(os.sched_getaffinity(0))
@@ -182,40 +155,173 @@ def host_threads():
         return os.cpu_count() or 1
 
 
+# ---------------------------------------------------------------- CPU (reference) legs
+def cpu_sc(cfg, nth, R, seed):
+    """Reference cluster_exact + certaindex_entropy + combined_meets_thresholds per row
+    (oracle/_ref) + the SPEC allocate restatement, on R requests of the workload."""
+    import ctypes as C
+
+    import numpy as np
+
+    from oracle import oracle as O
+    g = O.gen_params(seed=seed, conv_hi=cfg["conv_hi"])
+    ids = np.empty((R, cfg["P"], cfg["S"]), np.uint32)
+    O.lib().cdxo_gen_sc_mt(C.byref(g), C.c_uint64(0), C.c_uint64(R), C.c_uint32(cfg["P"]), C.c_uint32(cfg["S"]),
+                           ids.ctypes.data_as(C.c_void_p), C.c_int(nth))
+    ths = [(0, cfg["tau"], 0)]
+    O.ref_sc_batch(ids[: max(1, R // 64)], 5, ths, nthreads=nth)  # warm
+    t0 = time.perf_counter()
+    _, meets = O.ref_sc_batch(ids, 5, ths, nthreads=nth)
+    O.allocate_scan(meets, R, cfg["P"], 2, cfg["detect"], cfg["cap"], 1, cfg["interval"] * cfg["S"])
+    dt = time.perf_counter() - t0
+    t1 = time.perf_counter()
+    O.ref_sc_batch(ids, 5, ths, nthreads=nth, mode=1, want=False)
+    fill = time.perf_counter() - t1
+    n = R * cfg["P"] * cfg["S"]
+    return n / dt, dt, f"{R} requests ({n} probe-evals), {dt:.2f} s incl. {fill:.2f} s std::string row fill"
+
+
+def cpu_cot(cfg, nth, R, seed):
+    """Reference should_exit on every trace prefix + final_answer (oracle/_ref)."""
+    from oracle import oracle as O
+    ids, hes = O.gen_cot(O.gen_params(seed=seed, conv_hi=cfg["conv_hi"], hesitation_prob=cfg["hes"]), R, cfg["P"])
+    t0 = time.perf_counter()
+    O.ref_cot_batch(ids, hes, 5, cfg["interval"], cfg["w"], cfg["tau"], cfg["max_tokens"], nthreads=nth,
+                    want_ck=False)
+    dt = time.perf_counter() - t0
+    n = R * cfg["P"]
+    return n / dt, dt, f"{R} requests ({n} probe records), {dt:.2f} s"
+
+
+def cpu_reward(cfg, nth, G, seed):
+    """Reference cumulative certaindex_reward + certaindex_entropy(cluster_exact(all so far))
+    per step, as runtime.cpp:279-292 recomputes them (oracle/_ref)."""
+    import numpy as np
+
+    from oracle import oracle as O
+    rw, ids = O.gen_reward(O.gen_params(seed=seed, conv_hi=cfg["conv_hi"]), G, cfg["T"], cfg["W"])
+    agg = (np.arange(G) % 2).astype(np.uint8)
+    t0 = time.perf_counter()
+    O.ref_reward_batch(rw, ids, agg, nthreads=nth)
+    dt = time.perf_counter() - t0
+    n = G * cfg["T"] * cfg["W"]
+    return n / dt, dt, f"{G} programs ({n} node rewards), {dt:.2f} s"
+
+
+def gang_inputs(N, seed, limit):
+    import numpy as np
+    rng = np.random.default_rng(seed)
+    arrival = np.cumsum(rng.exponential(1e-3, N))  # lambda = 1000 programs/s
+    now = float(arrival[-1]) + 1e-3
+    # service lags chosen so ~5% of programs exceed the starvation limit
+    last = now - rng.exponential(limit / 3.0, N)
+    last = np.maximum(last, 0.0)
+    cnt = rng.integers(0, 6, N).astype(np.uint32)
+    sums = (rng.integers(32, 1024, N) * cnt).astype(np.int64)
+    cap = rng.integers(4, 64, N).astype(np.uint16)
+    knob = np.minimum(cap, rng.integers(0, 64, N)).astype(np.uint16)
+    arche = rng.random(N)  # 40% SC / 40% CoT / 20% MCTS: terminated by B/C/D-style exits
+    term = (rng.random(N) < np.where(arche < 0.4, 0.3, np.where(arche < 0.8, 0.2, 0.1))).astype(np.uint8)
+    return dict(arrival=arrival, last_service=last, iter_tok_sum=sums, iter_count=cnt, knob=knob, cap=cap,
+                terminated=term), now
+
+
+def cpu_gang(cfg, nth, N, seed):
+    """SPEC restatement (no reference code exists for the scheduler): qsort with the SPEC
+    comparator, oracle/cdx_oracle.c (single thread)."""
+    from oracle import oracle as O
+    soa, now = gang_inputs(N, seed, cfg["limit"])
+    t0 = time.perf_counter()
+    O.gang_order(soa, 1, cfg["limit"], cfg["prior"], now)
+    dt = time.perf_counter() - t0
+    return N / dt, dt, f"{N} programs, {dt:.2f} s (SPEC restatement, 1 thread)"
+
+
+CPU = {"sc": cpu_sc, "cot": cpu_cot, "reward": cpu_reward, "gang": cpu_gang}
+CPU_SAMPLE = {"A": 1024, "B": 1 << 16, "C": 1 << 18, "D": 1 << 14, "E": 1 << 20}
+
+
+def cpu_baseline(name, cfg, sample=None):
+    nth = host_threads() if cfg["kind"] != "gang" else 1
+    n = sample or CPU_SAMPLE[name]
+    v, dt, note = CPU[cfg["kind"]](cfg, nth, n, 20993 + 1)
+    kind = "port" if cfg["kind"] == "gang" else "reference"
+    return {"value": v, "unit": UNIT, "cores": nth, "kind": kind, "sample": f"config {name}: {note}"}
+
+
 def run_reference(args, cfg, rank, world):
     """--impl reference: rank 0 times the reference's CPU path; other ranks exit."""
     if rank != 0:
         return
-    nth = host_threads()
-    R = args.ref_sample or (1 << 17 if cfg["kind"] == "sc" else 1 << 16)
-    if cfg["kind"] == "sc":
-        R = min(R, cfg["R"])
     vals = []
+    n = args.ref_sample or CPU_SAMPLE[args.config]
+    nth = host_threads() if cfg["kind"] != "gang" else 1
+    note = ""
     for i in range(args.warmup + args.steps):
-        fn = cpu_baseline_sc if cfg["kind"] == "sc" else cpu_baseline_cot
-        v, dt, fill = fn(cfg, nth, R, 20993 + i)
+        v, dt, note = CPU[cfg["kind"]](cfg, nth, n, 20993 + i)
         if i >= args.warmup:
             vals.append((v, dt))
     v = statistics.median([x[0] for x in vals])
     ms = statistics.median([x[1] for x in vals]) * 1e3
-    sample = f"{R} requests of config {args.config} per step ({R * cfg['P'] * cfg.get('S', 1)} probe-evals)"
+    kind = "port" if cfg["kind"] == "gang" else "reference"
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": "u32 ids / f64 entropy", "data": "synthetic",
-            "config": {"workload": args.config, "desc": cfg["desc"], "sample_requests": R},
-            "cpu_baseline": {"value": v, "unit": UNIT, "cores": nth, "kind": "reference", "sample": sample},
+            "vs_baseline": None, "dtype": "u32 ids / f64 certaindex", "data": "synthetic",
+            "config": {"workload": args.config, "desc": cfg["desc"]},
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": nth, "kind": kind,
+                             "sample": f"config {args.config}: {note} (per step)"},
             "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
 
-# --------------------------------------------------------------------------------------
-def bench_sc(args, cfg, rank, world, cx):
+# ---------------------------------------------------------------- GPU legs
+def timed(args, world, launch, kernels):
+    """Warm up, then time exactly `steps` calls of launch(i) on torch's current stream with
+    CUDA events (barrier + synchronize on both sides, max over ranks).  `kernels` names the
+    segments launch() brackets with per-segment events (for per-kernel durations)."""
+    import torch
+    stream = torch.cuda.current_stream()
+    for _ in range(args.warmup):
+        launch(None)
+    torch.cuda.synchronize()
+    barrier(world)
+    seg = {k: [] for k in kernels}
+    t0 = torch.cuda.Event(enable_timing=True)
+    t1 = torch.cuda.Event(enable_timing=True)
+    with ClockSampler(torch.cuda.current_device()) as clk:
+        torch.cuda.synchronize()
+        t0.record(stream)
+        for i in range(args.steps):
+            launch(seg)
+        t1.record(stream)
+        torch.cuda.synchronize()
+    barrier(world)
+    ms = max_over_ranks(t0.elapsed_time(t1), world) / args.steps
+    per = {k: statistics.mean(a.elapsed_time(b) for a, b in v) if v else None for k, v in seg.items()}
+    return ms, per, clk.summary()
+
+
+def in_timed(cx, l0, args):
+    """Kernel launches of ours inside the timed region: every step issues the same set, so
+    the count since l0 (warm-up + timed steps) scales to the timed steps."""
+    return (cx.launches - l0) * args.steps // (args.steps + args.warmup)
+
+
+def seg_events(seg, name):
+    import torch
+    if seg is None:
+        return None
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record(torch.cuda.current_stream())
+    seg[name].append((a, b))
+    return b
+
+
+def bench_sc(args, cfg, rank, world, cx, with_e2e=True):
     import torch
     from paper_2412_20993_b200 import AllocPolicy, GenParams, Threshold
     R, P, S = cfg["R"], cfg["P"], cfg["S"]
-    r0 = rank * R
-    gp = GenParams(seed=20993 + 3, conv_hi=cfg["conv_hi"])
-    ids = cx.gen_sc(gp, R, P, S, r0=r0)
+    ids = cx.gen_sc(GenParams(seed=20993 + 3, conv_hi=cfg["conv_hi"]), R, P, S, r0=rank * R)
     hcert = torch.empty((R, P), dtype=torch.float32, device="cuda")
     meets = torch.empty((R, (P + 31) // 32), dtype=torch.int32, device="cuda")
     ths = [Threshold(0, cfg["tau"], 0)]
@@ -225,76 +331,46 @@ def bench_sc(args, cfg, rank, world, cx):
             ("kept", torch.int32))}
     out["scalars"] = torch.zeros((3,), dtype=torch.int64, device="cuda")
     torch.cuda.synchronize()
+    l0 = [0]
 
-    stream = torch.cuda.current_stream()
-    n_ev = args.steps
-    k2s = [torch.cuda.Event(enable_timing=True) for _ in range(n_ev)]
-    k2e = [torch.cuda.Event(enable_timing=True) for _ in range(n_ev)]
-    k5e = [torch.cuda.Event(enable_timing=True) for _ in range(n_ev)]
-
-    def step(i=None):
-        if i is not None:
-            k2s[i].record(stream)
+    def step(seg):
+        e = seg_events(seg, "sc_certaindex")
         cx.sc_certaindex(ids, ths, hcert=hcert, meets=meets)
-        if i is not None:
-            k2e[i].record(stream)
-        cx.allocate_scan(meets, R, P, pol, out=out)
-        if i is not None:
-            k5e[i].record(stream)
+        if e is not None:
+            e.record(torch.cuda.current_stream())
+        e = seg_events(seg, "allocate_scan")
+        cx.allocate_scan(meets, R, P, pol, kept_base=rank * R, out=out)
+        if e is not None:
+            e.record(torch.cuda.current_stream())
 
-    for _ in range(args.warmup):
-        step()
-    torch.cuda.synchronize()
-    barrier(world)
     l0 = cx.launches
-    t_start = torch.cuda.Event(enable_timing=True)
-    t_end = torch.cuda.Event(enable_timing=True)
-    with ClockSampler(torch.cuda.current_device()) as clk:
-        torch.cuda.synchronize()
-        t_start.record(stream)
-        for i in range(args.steps):
-            step(i)
-        t_end.record(stream)
-        torch.cuda.synchronize()
-    launches = cx.launches - l0
-    barrier(world)
-    ms_local = t_start.elapsed_time(t_end)
-    ms = max_over_ranks(ms_local, world)
-    k2_ms = statistics.mean(k2s[i].elapsed_time(k2e[i]) for i in range(n_ev))
-    k5_ms = statistics.mean(k2e[i].elapsed_time(k5e[i]) for i in range(n_ev))
-
-    # global token offsets across ranks: allgather of shard budget totals (8 B per rank)
-    total_b = out["scalars"][2:3].clone()
-    if world > 1:
+    ms, per, clocks = timed(args, world, step, ["sc_certaindex", "allocate_scan"])
+    launches = in_timed(cx, l0, args)
+    if world > 1:  # global token offsets: allgather of shard budget totals (8 B per rank)
         import torch.distributed as dist
-        allt = [torch.zeros_like(total_b) for _ in range(world)]
-        dist.all_gather(allt, total_b)
+        tot = out["scalars"][2:3].clone()
+        allt = [torch.zeros_like(tot) for _ in range(world)]
+        dist.all_gather(allt, tot)
     n_kept = int(out["scalars"][0])
-
-    answers = R * P * S * world
-    value = answers * args.steps / (ms / 1e3)
     k2_bytes = R * P * S * 4 + R * P * 4 + R * ((P + 31) // 32) * 4
     k5_bytes = R * ((P + 31) // 32) * 4 + R * (4 + 1 + 4 + 8) + n_kept * 4
-    peak, peak_src = load_peaks()
-    achieved = k2_bytes / (k2_ms / 1e3) / 1e9
-    res = dict(value=value, ms=ms / args.steps, launches=launches, k2_ms=k2_ms, k5_ms=k5_ms, k2_bytes=k2_bytes,
-               k5_bytes=k5_bytes, achieved=achieved, peak=peak, peak_src=peak_src, clocks=clk.summary(),
-               step_bytes=k2_bytes + k5_bytes, n_kept=n_kept)
-    # e2e through the C-ABI host entry (host buffers, H2D/D2H inside the timed region)
-    res["e2e"] = e2e_sc(args, cfg, cx, ids, ths, pol) if not args.no_e2e else None
+    res = dict(value=R * P * S * world / (ms / 1e3), ms=ms, launches=launches, clocks=clocks,
+               kernel="sc_certaindex", kernel_ms=per["sc_certaindex"], kernel_bytes=k2_bytes,
+               step_bytes=k2_bytes + k5_bytes, extra={"allocate_scan_ms": per["allocate_scan"],
+                                                      "allocate_scan_bytes": k5_bytes})
+    res["e2e"] = e2e_sc(args, cfg, cx, ids, ths, pol) if (with_e2e and not args.no_e2e) else None
     del ids
     return res
 
 
 def e2e_sc(args, cfg, cx, ids_dev, ths, pol):
+    """The same step through the C-ABI host entry cdx_sc_decide_host: ids from pinned host
+    memory, H2D + K2 + K5 + D2H of every decision inside the timed region."""
     import ctypes as C
 
     import torch
-    from paper_2412_20993_b200 import _abi, c_policy, c_thresholds
+    from paper_2412_20993_b200 import c_policy, c_thresholds
     R, P, S = cfg["R"], cfg["P"], cfg["S"]
-    lib = cx.lib
-    if not hasattr(lib, "cdx_sc_decide_host"):
-        return None
     host_ids = torch.empty((R, P, S), dtype=torch.int32, pin_memory=True)
     host_ids.copy_(ids_dev)
     ek = torch.empty((R,), dtype=torch.int32, pin_memory=True)
@@ -305,9 +381,8 @@ def e2e_sc(args, cfg, cx, ids_dev, ths, pol):
     cp = c_policy(pol)
 
     def one():
-        st = lib.cdx_sc_decide_host(cx.h, host_ids.data_ptr(), R, P, S, arr, n, C.byref(cp), ek.data_ptr(),
-                                    why.data_ptr(), off.data_ptr(), None, C.byref(saved))
-        cx._check(st)
+        cx._check(cx.lib.cdx_sc_decide_host(cx.h, host_ids.data_ptr(), R, P, S, arr, n, C.byref(cp), ek.data_ptr(),
+                                            why.data_ptr(), off.data_ptr(), None, C.byref(saved)))
 
     for _ in range(max(1, args.warmup)):
         one()
@@ -317,11 +392,11 @@ def e2e_sc(args, cfg, cx, ids_dev, ths, pol):
         one()
     dt = (time.perf_counter() - t0) / steps
     return {"value": R * P * S / dt, "unit": UNIT, "h2d_bytes_per_step": R * P * S * 4,
-            "d2h_bytes_per_step": R * (4 + 1 + 8) + 8, "ms_per_step": dt * 1e3,
-            "api": "cdx_sc_decide_host (C-ABI, pinned host buffers)"}
+            "d2h_bytes_per_step": R * (4 + 1 + 8) + 16, "ms_per_step": dt * 1e3,
+            "api": "cdx_sc_decide_host (C-ABI, pinned host buffers, wall clock)"}
 
 
-def bench_cot(args, cfg, rank, world, cx):
+def bench_cot(args, cfg, rank, world, cx, with_e2e=True):
     import torch
     from paper_2412_20993_b200 import GenParams, ProbeConfig
     R, P = cfg["R"], cfg["P"]
@@ -330,28 +405,80 @@ def bench_cot(args, cfg, rank, world, cx):
     pc = ProbeConfig(cfg["interval"], cfg["w"], cfg["tau"], cfg["max_tokens"])
     out = {k: torch.empty((R,), dtype=dt, device="cuda") for k, dt in
            (("exit_step", torch.int32), ("reason", torch.uint8), ("final_id", torch.int32), ("low_conf", torch.uint8))}
-    stream = torch.cuda.current_stream()
-    for _ in range(args.warmup):
+
+    def step(seg):
+        e = seg_events(seg, "cot_exit")
         cx.cot_exit(ids, hes, pc, out=out)
-    torch.cuda.synchronize()
-    barrier(world)
+        if e is not None:
+            e.record(torch.cuda.current_stream())
+
     l0 = cx.launches
-    ev = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
-    with ClockSampler(torch.cuda.current_device()) as clk:
-        ev[0].record(stream)
-        for i in range(args.steps):
-            cx.cot_exit(ids, hes, pc, out=out)
-            ev[i + 1].record(stream)
-        torch.cuda.synchronize()
-    launches = cx.launches - l0
-    ms_local = ev[0].elapsed_time(ev[-1])
-    ms = max_over_ranks(ms_local, world)
-    k_ms = statistics.mean(ev[i].elapsed_time(ev[i + 1]) for i in range(args.steps))
-    bytes_ = R * P * 4 + R * ((P + 63) // 64) * 8 + R * (4 + 1 + 4 + 1)
-    peak, peak_src = load_peaks()
-    return dict(value=R * P * world * args.steps / (ms / 1e3), ms=ms / args.steps, launches=launches, k2_ms=k_ms,
-                k2_bytes=bytes_, achieved=bytes_ / (k_ms / 1e3) / 1e9, peak=peak, peak_src=peak_src,
-                clocks=clk.summary(), step_bytes=bytes_, e2e=None)
+    ms, per, clocks = timed(args, world, step, ["cot_exit"])
+    b = R * P * 4 + R * ((P + 63) // 64) * 8 + R * (4 + 1 + 4 + 1)
+    return dict(value=R * P * world / (ms / 1e3), ms=ms, launches=in_timed(cx, l0, args), clocks=clocks,
+                kernel="cot_exit", kernel_ms=per["cot_exit"], kernel_bytes=b, step_bytes=b, extra={}, e2e=None)
+
+
+def bench_reward(args, cfg, rank, world, cx, with_e2e=True):
+    import torch
+    from paper_2412_20993_b200 import AllocPolicy, GenParams, Threshold
+    G, T, W = cfg["G"], cfg["T"], cfg["W"]
+    rw, ids = cx.gen_reward(GenParams(seed=20993 + 4, conv_hi=cfg["conv_hi"]), G, T, W, g0=rank * G)
+    agg = (torch.arange(G, device="cuda") % 2).to(torch.uint8)  # even MCTS (mean), odd Rebase (max)
+    thm = [Threshold(*t) for t in TH_MCTS]
+    thx = [Threshold(*t) for t in TH_REBASE]
+    pol = AllocPolicy(kind=2, detect_at=cfg["detect"], resource_cap=T, tokens_per_unit=W)
+    state = {}
+
+    def step(seg):
+        e = seg_events(seg, "reward_certaindex")
+        R_, H_, m_ = cx.reward_certaindex(rw, ids, agg, thm, thx)
+        if e is not None:
+            e.record(torch.cuda.current_stream())
+        e = seg_events(seg, "allocate_scan")
+        state["alloc"] = cx.allocate_scan(m_, G, T, pol)
+        if e is not None:
+            e.record(torch.cuda.current_stream())
+
+    l0 = cx.launches
+    ms, per, clocks = timed(args, world, step, ["reward_certaindex", "allocate_scan"])
+    b = G * T * W * 8 + G * T * 8 + G * ((T + 31) // 32) * 4
+    return dict(value=G * T * W * world / (ms / 1e3), ms=ms, launches=in_timed(cx, l0, args),
+                clocks=clocks, kernel="reward_certaindex", kernel_ms=per["reward_certaindex"], kernel_bytes=b,
+                step_bytes=b + G * 21, extra={"allocate_scan_ms": per["allocate_scan"]}, e2e=None)
+
+
+def bench_gang(args, cfg, rank, world, cx, with_e2e=True):
+    import numpy as np
+    import torch
+    from paper_2412_20993_b200 import InterPolicy
+    N = cfg["N"]
+    soa, now = gang_inputs(N, 20993 + 5, cfg["limit"])
+    dev = {k: (torch.from_numpy(v.view(np.int16)) if v.dtype == np.uint16 else torch.from_numpy(v)).cuda()
+           for k, v in soa.items()}
+    pol = InterPolicy(order=1, starvation_limit=cfg["limit"], prior_tokens=cfg["prior"])
+
+    def step(seg):
+        e = seg_events(seg, "gang_priority")
+        cx.gang_priority(dev, pol, now)
+        if e is not None:
+            e.record(torch.cuda.current_stream())
+
+    l0 = cx.launches
+    ms, per, clocks = timed(args, world, step, ["gang_priority"])
+    b = N * (8 + 8 + 8 + 4 + 2 + 2 + 1) + N * 4
+    return dict(value=N * world / (ms / 1e3), ms=ms, launches=in_timed(cx, l0, args), clocks=clocks, kernel="gang_priority (radix sort, all passes)",
+                kernel_ms=per["gang_priority"], kernel_bytes=b, step_bytes=b, extra={}, e2e=None)
+
+
+BENCH = {"sc": bench_sc, "cot": bench_cot, "reward": bench_reward, "gang": bench_gang}
+
+
+def summarize(name, cfg, res, peak):
+    ach = res["kernel_bytes"] / (res["kernel_ms"] / 1e3) / 1e9
+    return {"value": res["value"], "unit": UNIT, "ms_per_step": res["ms"], "desc": cfg["desc"],
+            "kernel": res["kernel"], "kernel_ms": res["kernel_ms"], "achieved_gbs": ach, "frac": ach / peak,
+            **res["extra"]}
 
 
 def main():
@@ -363,57 +490,57 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-others", action="store_true", help="skip the other configs at N=1")
     ap.add_argument("--ref-sample", type=int, default=0)
     args = ap.parse_args()
-    if args.warmup < 3:
-        args.warmup = 3
+    args.warmup = max(3, args.warmup)
     cfg = CONFIGS[args.config]
-    rank, world, local = dist_setup(args.gpus)
+    rank, world, local = dist_setup()
     if args.impl == "reference":
         run_reference(args, cfg, rank, world)
         return
 
     from paper_2412_20993_b200 import Context
     cx = Context(local)
-    res = bench_sc(args, cfg, rank, world, cx) if cfg["kind"] == "sc" else bench_cot(args, cfg, rank, world, cx)
-
+    peak, peak_src = load_peaks()
+    res = BENCH[cfg["kind"]](args, cfg, rank, world, cx)
+    others = {}
+    if world == 1 and not args.no_others:
+        sub = argparse.Namespace(**vars(args))
+        sub.steps, sub.warmup = min(args.steps, 20), 3
+        for name, c in CONFIGS.items():
+            if name == args.config:
+                continue
+            r = BENCH[c["kind"]](sub, c, 0, 1, cx, with_e2e=False)
+            others[name] = summarize(name, c, r, peak)
+            if not args.no_cpu_baseline:
+                others[name]["cpu_baseline"] = cpu_baseline(name, c)
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        nth = host_threads()
-        if cfg["kind"] == "sc":
-            R_s = min(cfg["R"], args.ref_sample or (1 << 18))
-            v, dt, fill = cpu_baseline_sc(cfg, nth, R_s, 20993 + 3)
-            cpu = {"value": v, "unit": UNIT, "cores": nth, "kind": "reference",
-                   "sample": f"{R_s} of {cfg['R']} requests of config {args.config} ({R_s * cfg['P'] * cfg['S']} "
-                             f"probe-evals, {dt:.2f} s incl. {fill:.2f} s string row-buffer fill)"}
-        else:
-            R_s = args.ref_sample or (1 << 16)
-            v, dt, _ = cpu_baseline_cot(cfg, nth, R_s, 20993 + 2)
-            cpu = {"value": v, "unit": UNIT, "cores": nth, "kind": "reference",
-                   "sample": f"{R_s} requests of config {args.config} ({R_s * cfg['P']} probe-evals, {dt:.2f} s)"}
+        cpu = cpu_baseline(args.config, cfg, args.ref_sample or None)
     if rank == 0:
-        frac = res["achieved"] / res["peak"]
+        ach = res["kernel_bytes"] / (res["kernel_ms"] / 1e3) / 1e9
+        cfg_out = {"workload": args.config, "desc": cfg["desc"],
+                   **{k: v for k, v in cfg.items() if k not in ("kind", "desc", "conv_hi")},
+                   "parallelism": f"request shards x{world} (no data-path collective)",
+                   "l2": "inputs > L2 (126 MB) for C/B/D/E: no flush needed"}
         line = {
             "metric": METRIC, "value": res["value"], "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": res["ms"], "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": "u32 ids / f64 entropy (f32 store)", "data": "synthetic",
-            "config": {"workload": args.config, "desc": cfg["desc"],
-                       **{k: v for k, v in cfg.items() if k in ("R", "P", "S", "w", "tau", "detect", "cap")},
-                       "requests_per_gpu": cfg["R"], "parallelism": f"request shards x{world} (no data-path collective)",
-                       "l2": "inputs > L2 (126 MB); no flush needed"},
-            "roofline": {"bound": "hbm", "achieved": res["achieved"], "peak": res["peak"], "unit": "GB/s",
-                         "frac": frac, "traffic": None, "peak_source": res["peak_src"],
-                         "kernel": "sc_certaindex" if cfg["kind"] == "sc" else "cot_exit",
-                         "kernel_ms": res["k2_ms"], "algorithmic_bytes_per_launch": res["k2_bytes"],
+            "vs_baseline": None, "dtype": "u32 ids / f64 certaindex (f32 store)", "data": "synthetic",
+            "config": cfg_out,
+            "roofline": {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
+                         "traffic": None, "peak_source": peak_src, "kernel": res["kernel"],
+                         "kernel_ms": res["kernel_ms"], "algorithmic_bytes_per_launch": res["kernel_bytes"],
                          "step_bytes": res["step_bytes"],
-                         "step_frac": res["step_bytes"] / (res["ms"] / 1e3) / 1e9 / res["peak"]},
+                         "step_frac": res["step_bytes"] / (res["ms"] / 1e3) / 1e9 / peak, **res["extra"]},
             "cpu_baseline": cpu,
             "e2e": res["e2e"],
             "gpu_launches": res["launches"],
             "clocks": res["clocks"],
         }
-        if "k5_ms" in res:
-            line["roofline"]["allocate_scan_ms"] = res["k5_ms"]
+        if others:
+            line["other_configs"] = others
         print(json.dumps(line), flush=True)
     if world > 1:
         import torch.distributed as dist

@@ -246,6 +246,143 @@ __global__ void __launch_bounds__(128) cot_exit_kernel(const __grid_constant__ C
     }
 }
 
+// Lean variant for the common threshold regime a_min == w (tau > (w-1)/w, e.g. the paper's
+// w=3, tau=0.9): the window agrees fully iff the last w usable answers are all equal, i.e.
+// iff the run of equal consecutive usable answers ending here is >= w.  One compare and a
+// counter per probe instead of a w-wide window; runtime w; no per-probe consistency output.
+template <bool TMA>
+__global__ void __launch_bounds__(128) cot_run_kernel(const __grid_constant__ CotParams p) {
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+    uint64_t* bar = reinterpret_cast<uint64_t*>(smem + p.stages * p.stage_bytes);
+    const uint32_t tid = threadIdx.x;
+    if (TMA) {
+        if (tid == 0) {
+            tma_prefetch_desc(&p.tmap);
+            for (uint32_t s = 0; s < p.stages; ++s) mbar_init(&bar[s], 1);
+            fence_mbar_init();
+        }
+        __syncthreads();
+    }
+    const uint64_t policy = policy_evict_first();
+    const uint64_t stride = gridDim.x;
+    auto issue = [&](uint64_t tile, uint32_t stage) {
+        uint8_t* dst = smem + stage * p.stage_bytes;
+        mbar_expect_tx(&bar[stage], p.stage_bytes);
+        for (uint32_t b = 0; b < p.boxes; ++b)
+            tma_load_2d(dst + b * p.rows * 128u, &p.tmap, static_cast<int32_t>(b * 32),
+                        static_cast<int32_t>(tile * p.rows), &bar[stage], policy);
+    };
+    if (TMA && tid == 0)
+        for (uint32_t s = 0; s < p.stages; ++s) {
+            const uint64_t t = blockIdx.x + s * stride;
+            if (t < p.ntiles) issue(t, s);
+        }
+    const int32_t w = p.w;
+    uint32_t stage = 0, parity = 0;
+    for (uint64_t tile = blockIdx.x; tile < p.ntiles; tile += stride) {
+        const uint64_t r = tile * p.rows + tid;
+        const bool live = r < p.R;
+        // the first hesitation word is independent of the tile data: load it before the wait
+        uint64_t hw64 = live ? __ldg(p.hes + r * p.hw) : 0ull;
+        int32_t bstep = p.bstep_implicit;
+        if (live && p.offsets) {
+            bstep = -1;
+            for (uint32_t q = 0; q < p.P; ++q)
+                if (__ldg(p.offsets + r * p.P + q) >= p.max_tokens) {
+                    bstep = static_cast<int32_t>(q);
+                    break;
+                }
+        }
+        if (TMA) mbar_wait(&bar[stage], parity);
+        const uint8_t* tsm = smem + stage * p.stage_bytes;
+        if (live) {
+            const uint32_t P = p.P;
+            const uint32_t L = bstep >= 0 ? static_cast<uint32_t>(bstep) + 1 : P;
+            int32_t run = 0, cstep = -1;
+            uint32_t last = 0, cid = 0;
+            bool has = false;
+            for (uint32_t b = 0; b * 32u < L && cstep < 0; ++b) {
+                if (b > 0 && (b & 1u) == 0) hw64 = __ldg(p.hes + r * p.hw + (b >> 1));
+                const uint32_t hw32 = (b & 1u) ? static_cast<uint32_t>(hw64 >> 32) : static_cast<uint32_t>(hw64);
+#pragma unroll
+                for (uint32_t c = 0; c < 8; ++c) {
+                    const uint32_t col = b * 32u + c * 4u;
+                    if (col >= L || cstep >= 0) break;
+                    uint4 v4;
+                    if (TMA) {
+                        v4 = *reinterpret_cast<const uint4*>(tsm + b * p.rows * 128u + swz128(tid, c));
+                    } else {
+                        const uint32_t* src = p.ids + r * P + col;
+                        v4.x = __ldg(src);
+                        v4.y = col + 1 < P ? __ldg(src + 1) : 0u;
+                        v4.z = col + 2 < P ? __ldg(src + 2) : 0u;
+                        v4.w = col + 3 < P ? __ldg(src + 3) : 0u;
+                    }
+                    const uint32_t vv[4] = {v4.x, v4.y, v4.z, v4.w};
+#pragma unroll
+                    for (uint32_t e = 0; e < 4; ++e) {
+                        const uint32_t q = col + e;
+                        const bool use = q < L && cstep < 0 && !((hw32 >> (c * 4u + e)) & 1u);
+                        if (use) {
+                            run = (has && vv[e] == last) ? run + 1 : 1;
+                            last = vv[e];
+                            has = true;
+                            if (run >= w) {  // last w usable answers equal: C = 1 >= tau
+                                cstep = static_cast<int32_t>(q);
+                                cid = vv[e];
+                            }
+                        }
+                    }
+                }
+            }
+            int32_t ex = -1;
+            uint8_t why = CDX_EXIT_CONTINUE;
+            uint32_t fid;
+            uint8_t low = 0;
+            if (cstep >= 0) {  // certainty wins ties with the budget
+                ex = cstep;
+                why = CDX_EXIT_CERTAIN;
+                fid = cid;
+            } else if (bstep >= 0) {
+                ex = bstep;
+                why = CDX_EXIT_BUDGET;
+                fid = has ? last : cot_id<1, TMA>(p, tsm, tid, r, static_cast<uint32_t>(bstep));
+                low = has ? 0 : 1;
+            } else {
+                fid = has ? last : cot_id<1, TMA>(p, tsm, tid, r, P - 1);
+                low = has ? 0 : 1;
+            }
+            p.exit_step[r] = ex;
+            p.reason[r] = why;
+            if (p.final_id) p.final_id[r] = fid;
+            if (p.low_conf) p.low_conf[r] = low;
+        }
+        if (TMA) {
+            __syncthreads();
+            if (tid == 0) {
+                const uint64_t nt = tile + static_cast<uint64_t>(p.stages) * stride;
+                if (nt < p.ntiles) issue(nt, stage);
+            }
+            if (++stage == p.stages) {
+                stage = 0;
+                parity ^= 1u;
+            }
+        }
+    }
+}
+
+template <bool TMA>
+static void launch_cot_run(cdx_ctx* ctx, const CotParams& p, size_t smem) {
+    auto k = cot_run_kernel<TMA>;
+    if (TMA) cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, p.rows, TMA ? smem : 0);
+    if (per_sm < 1) per_sm = 1;
+    const uint64_t grid = std::min<uint64_t>(p.ntiles, static_cast<uint64_t>(ctx->sm_count) * per_sm);
+    k<<<static_cast<unsigned>(grid), p.rows, TMA ? smem : 0, ctx->stream>>>(p);
+}
+
 template <int W, bool TMA, bool CK>
 static void launch_cot_k(cdx_ctx* ctx, const CotParams& p, size_t smem) {
     auto k = cot_exit_kernel<W, TMA, CK>;
@@ -339,6 +476,13 @@ extern "C" int cdx_cot_exit(cdx_ctx* ctx, const uint32_t* ids, const uint64_t* h
     p.ntiles = (R + p.rows - 1) / p.rows;
     const size_t smem = tma ? static_cast<size_t>(p.stages) * p.stage_bytes + 1024 + 8 * COT_MAX_STAGES : 0;
     const bool want_ck = ck != nullptr;
+    const char* impl = getenv("CDX_COT_IMPL");
+    if (!want_ck && amin == cfg->window && !(impl && impl[0] == 'w')) {
+        if (tma) launch_cot_run<true>(ctx, p, smem);
+        else launch_cot_run<false>(ctx, p, smem);
+        CDX_CHECK_LAUNCH(ctx, "cot_exit(run)");
+        return CDX_OK;
+    }
     switch (cfg->window) {
         case 1: launch_cot<1>(ctx, p, tma, want_ck, smem); break;
         case 2: launch_cot<2>(ctx, p, tma, want_ck, smem); break;
