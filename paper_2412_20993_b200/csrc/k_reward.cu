@@ -53,6 +53,7 @@ struct RwParams {
     uint32_t T, W, words;     // words = ceil(T/32)
     uint32_t boxes;           // ceil(W/32)
     uint32_t stage_bytes;     // per array
+    uint32_t stages;          // ring depth (<= RW_STAGES)
     int tma;
     int n_th[2];
     uint8_t th_sig[2][RW_MAX_TH];
@@ -74,7 +75,8 @@ __device__ __forceinline__ bool meets_th(const RwParams& p, int a, double hc, bo
 __global__ void __launch_bounds__(RW_PROGS) reward_kernel(const __grid_constant__ RwParams p) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
-    uint64_t* bar = reinterpret_cast<uint64_t*>(smem + RW_STAGES * 2 * p.stage_bytes);
+    const uint32_t arrays = p.ids ? 2u : 1u;  // rewards (+ ids) staged per step
+    uint64_t* bar = reinterpret_cast<uint64_t*>(smem + p.stages * arrays * p.stage_bytes);
     const uint32_t tid = threadIdx.x;
     const uint64_t g = static_cast<uint64_t>(blockIdx.x) * RW_PROGS + tid;
     const bool live = g < p.G;
@@ -85,12 +87,12 @@ __global__ void __launch_bounds__(RW_PROGS) reward_kernel(const __grid_constant_
     if (p.tma && tid == 0) {
         tma_prefetch_desc(&p.tm_r);
         if (with_ids) tma_prefetch_desc(&p.tm_i);
-        for (uint32_t s = 0; s < RW_STAGES; ++s) mbar_init(&bar[s], 1);
+        for (uint32_t s = 0; s < p.stages; ++s) mbar_init(&bar[s], 1);
         fence_mbar_init();
     }
     __syncthreads();
     auto issue = [&](uint32_t t, uint32_t stage) {
-        uint8_t* dr = smem + stage * 2 * p.stage_bytes;
+        uint8_t* dr = smem + stage * arrays * p.stage_bytes;
         uint8_t* di = dr + p.stage_bytes;
         mbar_expect_tx(&bar[stage], p.stage_bytes * (with_ids ? 2u : 1u));
         const int32_t g0 = static_cast<int32_t>(static_cast<uint64_t>(blockIdx.x) * RW_PROGS);
@@ -103,7 +105,7 @@ __global__ void __launch_bounds__(RW_PROGS) reward_kernel(const __grid_constant_
         }
     };
     if (p.tma && tid == 0)
-        for (uint32_t s = 0; s < RW_STAGES && s < T; ++s) issue(s, s);
+        for (uint32_t s = 0; s < p.stages && s < T; ++s) issue(s, s);
 
     const uint8_t a = live ? p.agg[g] : 0;
     double sum = 0.0;
@@ -117,10 +119,10 @@ __global__ void __launch_bounds__(RW_PROGS) reward_kernel(const __grid_constant_
     uint32_t mword = 0;
 
     for (uint32_t t = 0; t < T; ++t) {
-        const uint32_t stage = t % RW_STAGES;
-        const uint8_t* sr = smem + stage * 2 * p.stage_bytes;
+        const uint32_t stage = t % p.stages;
+        const uint8_t* sr = smem + stage * arrays * p.stage_bytes;
         const uint8_t* si = sr + p.stage_bytes;
-        if (p.tma) mbar_wait(&bar[stage], (t / RW_STAGES) & 1u);
+        if (p.tma) mbar_wait(&bar[stage], (t / p.stages) & 1u);
         if (live) {
             for (uint32_t w0 = 0; w0 < W; w0 += 4) {
                 float rv4[4];
@@ -203,7 +205,7 @@ __global__ void __launch_bounds__(RW_PROGS) reward_kernel(const __grid_constant_
         }
         if (p.tma) {
             __syncthreads();
-            if (tid == 0 && t + RW_STAGES < T) issue(t + RW_STAGES, stage);
+            if (tid == 0 && t + p.stages < T) issue(t + p.stages, stage);
         }
     }
     if (live && bad) set_dev_err(p.d_err, DEV_REWARD_RANGE);
@@ -384,7 +386,12 @@ extern "C" int cdx_reward_certaindex(cdx_ctx* ctx, const float* rewards, const u
                                    CU_TENSOR_MAP_SWIZZLE_128B));
     }
     p.tma = tma ? 1 : 0;
-    const size_t smem = tma ? 1024 + static_cast<size_t>(RW_STAGES) * 2 * p.stage_bytes + 8 * RW_STAGES : 0;
+    // one step staged per CTA (more resident CTAs beat a deeper ring here: each thread
+    // needs its program's whole step row in shared memory); CDX_RW_STAGES=2 for a ring
+    p.stages = 1;
+    if (const char* e = getenv("CDX_RW_STAGES")) p.stages = std::max(1, std::min(RW_STAGES, atoi(e)));
+    const size_t smem = tma ? 1024 + static_cast<size_t>(p.stages) * (ids ? 2 : 1) * p.stage_bytes + 8 * RW_STAGES
+                            : 0;
     const unsigned grid = static_cast<unsigned>((G + RW_PROGS - 1) / RW_PROGS);
     if (tma) cudaFuncSetAttribute(reward_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     reward_kernel<<<grid, RW_PROGS, smem, ctx->stream>>>(p);
