@@ -10,12 +10,28 @@ NVFLAGS := $(ARCH) -O3 -lineinfo -std=c++17 -fmad=false -Xcompiler -fPIC,-O2 \
 PKG     := paper_2412_20993_b200
 SRCS    := $(wildcard $(PKG)/csrc/*.cu) $(wildcard $(PKG)/csrc/*.cpp)
 OBJS    := $(patsubst $(PKG)/csrc/%,build/obj/%.o,$(SRCS))
-HDRS    := $(wildcard $(PKG)/csrc/*.cuh) include/cdx_c.h $(wildcard include/cdx/*.hpp)
+HDRS    := $(wildcard $(PKG)/csrc/*.cuh) include/cdx_c.h
 LIB     := $(PKG)/lib/libcdx.so
+# C++ host layer: the reference's C++ API (include/cdx/*.hpp) over the C-ABI
+HOSTLIB := $(PKG)/lib/libcdxhost.so
+HSRCS   := $(wildcard $(PKG)/csrc/host/*.cpp)
+HOBJS   := $(patsubst $(PKG)/csrc/host/%.cpp,build/host/%.o,$(HSRCS))
+HHDRS   := $(wildcard $(PKG)/csrc/host/*.hpp) include/cdx_c.h $(wildcard include/cdx/*.hpp)
+HOSTCXX := g++
+CXXFLAGS_HOST := -std=c++20 -O2 -fPIC -Wall -Wextra -Iinclude
 
-all: lib oracle
+DROPIN  := tests/cpp/bin/dropin_ours tests/cpp/bin/scheduler_cases
 
-lib: $(LIB)
+all: lib oracle dropin
+
+lib: $(LIB) $(HOSTLIB)
+
+build/host/%.o: $(PKG)/csrc/host/%.cpp $(HHDRS)
+	@mkdir -p build/host
+	$(HOSTCXX) $(CXXFLAGS_HOST) -c $< -o $@
+
+$(HOSTLIB): $(HOBJS) $(LIB)
+	$(HOSTCXX) -shared -o $@ $(HOBJS) -L$(PKG)/lib -lcdx -Wl,-rpath,'$$ORIGIN'
 
 build/obj/%.cu.o: $(PKG)/csrc/%.cu $(HDRS)
 	@mkdir -p build/obj
@@ -32,12 +48,22 @@ $(LIB): $(OBJS)
 oracle:
 	$(MAKE) -C oracle
 
+# drop-in proof: the same caller source the oracle builds against the reference headers
+dropin: $(DROPIN)
+
+CPPTEST = @mkdir -p tests/cpp/bin && $(HOSTCXX) -std=c++20 -O2 -Wall -Iinclude -o $@ $< -L$(PKG)/lib -lcdxhost -lcdx \
+          -Wl,-rpath,'$$ORIGIN/../../../$(PKG)/lib'
+tests/cpp/bin/dropin_ours: tests/cpp/dropin_cases.cpp $(HOSTLIB) $(HHDRS)
+	$(CPPTEST)
+tests/cpp/bin/%: tests/cpp/%.cpp $(HOSTLIB) $(HHDRS)
+	$(CPPTEST)
+
 sass: $(LIB)
 	@mkdir -p profiles
 	/usr/local/cuda/bin/cuobjdump -res-usage $(LIB) > profiles/sass_resources.txt 2>&1 || true
 
 clean:
-	rm -rf build $(PKG)/lib
+	rm -rf build $(PKG)/lib tests/cpp/bin
 	$(MAKE) -C oracle clean
 
-.PHONY: all lib oracle sass clean
+.PHONY: all lib oracle dropin sass clean

@@ -3,7 +3,7 @@
  *
  * Plain pointers and sizes only; no C++ or torch types cross this boundary.  Every entry
  * point is the batched replacement of a scalar routine of the reference library
- * (proj/include/cdx/*.hpp, CPU, one program at a time); the comment above each one
+ * (proj/include/cdx/ headers, CPU, one program at a time); the comment above each one
  * cites the reference interface it replaces.  The reference has no scheduler code: the
  * scheduler rows restate SPEC.md:385-486.
  *
@@ -30,7 +30,7 @@
 extern "C" {
 #endif
 
-#define CDX_ABI_VERSION 1
+#define CDX_ABI_VERSION 2
 
 typedef enum {
     CDX_OK = 0,
@@ -172,13 +172,68 @@ int cdx_cluster_rows(cdx_ctx* ctx, const uint32_t* ids, uint64_t rows, uint32_t 
                      uint32_t* n_clusters, uint32_t* leader, uint32_t* size);
 
 /* Entropy of explicit clusterings (façade path of semantic_entropy/certaindex_entropy):
- * sizes u32[rows][max_m] in cluster order, m u32[rows]; every row's total n must be
- * <= max_n (host bound, sizes the term table); outputs f64 (nullable).  A row with an
- * empty cluster, m == 0 or n > max_n fails at cdx_sync with "semantic_entropy: invalid
- * clustering".  metrics.cpp:107-125                                                      */
+ * sizes u32[rows][max_m] in cluster order, m u32[rows] clusters per row, totals u32[rows]
+ * (Clustering::total; nullable = the sum of the sizes).  Every row's total must be
+ * <= max_n (host bound, sizes the term table); outputs f64 (nullable).  Fails at cdx_sync
+ * with the reference's messages: "semantic_entropy: invalid clustering" (total < 1, m == 0,
+ * or — a documented restriction — a cluster larger than the total), "semantic_entropy:
+ * empty cluster".  The n == 1 -> 1.0 shortcut of certaindex_entropy applies to Hcert.
+ * metrics.cpp:107-125                                                                    */
 int cdx_entropy_from_sizes(cdx_ctx* ctx, const uint32_t* sizes, const uint32_t* m,
-                           uint64_t rows, uint32_t max_m, uint32_t max_n, double* H,
-                           double* Hcert);
+                           const uint32_t* totals, uint64_t rows, uint32_t max_m, uint32_t max_n,
+                           double* H, double* Hcert);
+
+/* One clustering whose total n is known on the host (the scalar façade's path, any n up to
+ * 2^26): sizes u32[m] in cluster order (device).  Same semantics and messages as above. */
+int cdx_entropy_one(cdx_ctx* ctx, const uint32_t* sizes, uint32_t m, uint32_t total, double* H,
+                    double* Hcert);
+
+/* ---- ragged rows behind the scalar C++ API (include/cdx/metrics.hpp, probe.hpp) -------
+ * Rows are concatenated records, row r = [row_off[r], row_off[r+1]).  ids are interned
+ * answers (K1: equal id <=> equal trimmed bytes), hes u8 hesitation flags, step_index i32
+ * and token_offset i64 per record, in trace order.                                        */
+/* probe::consistency(records, k[r], window)  probe.cpp:64-75.  C f64 = agree / window;
+ * ready u8 = 0 where the reference returns nullopt (fewer than window usable records). */
+int cdx_probe_consistency(cdx_ctx* ctx, const uint32_t* ids, const uint8_t* hes,
+                          const int32_t* step_index, const uint64_t* row_off, const int32_t* k,
+                          uint64_t rows, int32_t window, double* C, uint8_t* ready);
+/* probe::should_exit(trace, cfg)  probe.cpp:77-85 -> decision u8 (CDX_EXIT_*).
+ * cfg is validated first with ProbeConfig::validate's messages (probe.cpp:19-25).       */
+int cdx_probe_should_exit(cdx_ctx* ctx, const uint32_t* ids, const uint8_t* hes,
+                          const int32_t* step_index, const int64_t* token_offset,
+                          const uint64_t* row_off, uint64_t rows, const cdx_probe_cfg* cfg,
+                          uint8_t* decision);
+/* probe::final_answer(trace)  probe.cpp:87-102 -> pos u64 (record index within the row of
+ * the reported answer) and low_conf u8.  terminated_at i32[rows] (nullable; INT32_MIN =
+ * nullopt), termination_reason u8[rows] (nullable; probe.hpp:42 ordinals: 0 Certain,
+ * 1 Budget, 2 CriteriaExternal).  Rows must be non-empty (the caller raises
+ * "final_answer: empty trace").                                                          */
+int cdx_probe_final_answer(cdx_ctx* ctx, const uint8_t* hes, const int32_t* step_index,
+                           const uint64_t* row_off, const int32_t* terminated_at,
+                           const uint8_t* termination_reason, uint64_t rows, uint64_t* pos,
+                           uint8_t* low_conf);
+/* metrics::combined_meets_thresholds per row  metrics.cpp:159-171.  signals f64[rows][4]
+ * in SignalKind order, present u8[rows] (bit k = signal k present); meets u8[rows].  An
+ * absent signal reached in threshold order fails at cdx_sync with "combined_meets_
+ * thresholds: signal '<name>' absent".                                                   */
+int cdx_meets_thresholds_rows(cdx_ctx* ctx, const double* signals, const uint8_t* present,
+                              uint64_t rows, const cdx_threshold* th, uint32_t n_th,
+                              uint8_t* meets);
+/* Cluster sizes of dense first-seen ids (output of cdx_canon_intern): counts u32[n_unique]
+ * = the cluster sizes of metrics::cluster_exact in first-seen order (metrics.cpp:21-37). */
+int cdx_id_histogram(cdx_ctx* ctx, const uint32_t* ids, uint64_t n, uint32_t n_unique,
+                     uint32_t* counts);
+
+/* SPEC.md:431-439 estimate_iteration_tokens per program: tokens i64 (completed iteration
+ * token counts, concatenated), row_off u64[rows+1]; est f64 = mean, or prior if empty.  */
+int cdx_iteration_tokens_rows(cdx_ctx* ctx, const int64_t* tokens, const uint64_t* row_off,
+                              uint64_t rows, double prior, double* est);
+
+/* ---- device buffers, stream-ordered on the context stream (hosts without cudart) ------ */
+int cdx_alloc(cdx_ctx* ctx, uint64_t bytes, void** out);
+int cdx_free(cdx_ctx* ctx, void* p);
+int cdx_memcpy(cdx_ctx* ctx, void* dst, const void* src, uint64_t bytes); /* any direction */
+int cdx_memset(cdx_ctx* ctx, void* dst, int value, uint64_t bytes);
 
 /* ---- K5: SPEC allocate + exclusive scan of token budgets + stable compaction --------
  * Replaces scheduler.allocate for a batch of requests whose certaindex

@@ -257,13 +257,13 @@ class Context:
         self._check(self.lib.cdx_cluster_rows(self.h, _ptr(ids2d), rows, S, _ptr(ncl), _ptr(leader), _ptr(size)))
         return ncl, leader, size
 
-    def entropy_from_sizes(self, sizes, m, max_n: int):
+    def entropy_from_sizes(self, sizes, m, max_n: int, totals=None):
         t = self.torch
         rows, max_m = sizes.shape
         H = self.empty((rows,), t.float64)
         Hc = self.empty((rows,), t.float64)
         self._bind_stream()
-        self._check(self.lib.cdx_entropy_from_sizes(self.h, _ptr(sizes), _ptr(m), rows, max_m, max_n, _ptr(H),
+        self._check(self.lib.cdx_entropy_from_sizes(self.h, _ptr(sizes), _ptr(m), _ptr(totals), rows, max_m, max_n, _ptr(H),
                                                     _ptr(Hc)))
         return H, Hc
 

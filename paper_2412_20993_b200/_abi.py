@@ -75,7 +75,18 @@ SIGNATURES = {
     "cdx_gen_reward": (C.c_int, [P, C.POINTER(GenParams), U64, U64, U32, U32, P, P]),
     "cdx_sc_certaindex": (C.c_int, [P, P, U64, U32, U32, C.POINTER(Threshold), U32, P, P]),
     "cdx_cluster_rows": (C.c_int, [P, P, U64, U32, P, P, P]),
-    "cdx_entropy_from_sizes": (C.c_int, [P, P, P, U64, U32, U32, P, P]),
+    "cdx_entropy_from_sizes": (C.c_int, [P, P, P, P, U64, U32, U32, P, P]),
+    "cdx_probe_consistency": (C.c_int, [P, P, P, P, P, P, U64, I32, P, P]),
+    "cdx_probe_should_exit": (C.c_int, [P, P, P, P, P, P, U64, C.POINTER(ProbeCfg), P]),
+    "cdx_probe_final_answer": (C.c_int, [P, P, P, P, P, P, U64, P, P]),
+    "cdx_meets_thresholds_rows": (C.c_int, [P, P, P, U64, C.POINTER(Threshold), U32, P]),
+    "cdx_id_histogram": (C.c_int, [P, P, U64, U32, P]),
+    "cdx_entropy_one": (C.c_int, [P, P, U32, U32, P, P]),
+    "cdx_iteration_tokens_rows": (C.c_int, [P, P, P, U64, C.c_double, P]),
+    "cdx_alloc": (C.c_int, [P, U64, C.POINTER(P)]),
+    "cdx_free": (C.c_int, [P, P]),
+    "cdx_memcpy": (C.c_int, [P, P, P, U64]),
+    "cdx_memset": (C.c_int, [P, P, C.c_int, U64]),
     "cdx_allocate_scan": (C.c_int, [P, P, U64, U32, C.POINTER(AllocPolicy), I64, U32, P, P, P, P, P, P, P, P]),
     "cdx_cot_exit": (C.c_int, [P, P, P, P, U64, U32, C.POINTER(ProbeCfg), P, P, P, P, P]),
     "cdx_reward_certaindex": (C.c_int, [P, P, P, P, U64, U32, U32, C.POINTER(Threshold), U32,

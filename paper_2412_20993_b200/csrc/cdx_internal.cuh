@@ -53,6 +53,8 @@ enum DevErr : int {
     DEV_INTERN_FULL = 3,
     DEV_BAD_CLUSTERING = 4,  // "semantic_entropy: invalid clustering"
     DEV_EMPTY_REWARDS = 5,   // "certaindex_reward: empty reward set"
+    DEV_EMPTY_CLUSTER = 6,   // "semantic_entropy: empty cluster"
+    DEV_ABSENT_SIGNAL = 16,  // + SignalKind: "combined_meets_thresholds: signal '<name>' absent"
 };
 const char* dev_err_message(int code);
 // cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda needed)

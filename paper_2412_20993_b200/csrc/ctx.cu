@@ -46,6 +46,11 @@ const char* dev_err_message(int code) {
         case DEV_INTERN_FULL: return "canon_intern: intern table full";
         case DEV_BAD_CLUSTERING: return "semantic_entropy: invalid clustering";
         case DEV_EMPTY_REWARDS: return "certaindex_reward: empty reward set";
+        case DEV_EMPTY_CLUSTER: return "semantic_entropy: empty cluster";
+        case DEV_ABSENT_SIGNAL + 0: return "combined_meets_thresholds: signal 'certaindex_entropy' absent";
+        case DEV_ABSENT_SIGNAL + 1: return "combined_meets_thresholds: signal 'certaindex_reward' absent";
+        case DEV_ABSENT_SIGNAL + 2: return "combined_meets_thresholds: signal 'mean_output_length' absent";
+        case DEV_ABSENT_SIGNAL + 3: return "combined_meets_thresholds: signal 'mean_norm_logprob' absent";
     }
     return "device error";
 }
@@ -221,7 +226,8 @@ int cdx_sync(cdx_ctx* ctx) {
     if (code != 0) {
         cudaMemset(ctx->d_err, 0, sizeof(int));
         const int st = (code == cdx::DEV_REWARD_RANGE || code == cdx::DEV_BAD_CLUSTERING ||
-                        code == cdx::DEV_EMPTY_REWARDS)
+                        code == cdx::DEV_EMPTY_REWARDS || code == cdx::DEV_EMPTY_CLUSTER ||
+                        (code >= cdx::DEV_ABSENT_SIGNAL && code < cdx::DEV_ABSENT_SIGNAL + 4))
                            ? CDX_EINVAL
                            : CDX_ERUNTIME;
         return cdx::set_error(ctx, st, cdx::dev_err_message(code));

@@ -229,21 +229,38 @@ __global__ void cluster_rows_kernel(const uint32_t* __restrict__ ids, uint64_t r
 }
 
 // Entropy of explicit clusterings from a triangular term table T[n][c] (n <= max_n).
+// totals (nullable): Clustering::total per row; absent -> the sum of the sizes (what
+// cluster_exact produces).  Validation in the reference's order (metrics.cpp:107-112):
+// total < 1 or no clusters -> "invalid clustering"; a cluster of size < 1 -> "empty
+// cluster".  A cluster larger than its total (p > 1) is rejected as an invalid clustering:
+// the host term table only holds c <= n (documented deviation).
 __global__ void entropy_sizes_kernel(const uint32_t* __restrict__ sizes, const uint32_t* __restrict__ m,
-                                     uint64_t rows, uint32_t max_m, const double* __restrict__ tri,
-                                     const double* __restrict__ logs, uint32_t max_n, double* H,
-                                     double* Hc, int* bad) {
+                                     const uint32_t* __restrict__ totals, uint64_t rows, uint32_t max_m,
+                                     const double* __restrict__ tri, const double* __restrict__ logs, uint32_t max_n,
+                                     double* H, double* Hc, int* bad) {
     for (uint64_t r = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; r < rows;
          r += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
         const uint32_t mm = m[r];
         uint64_t n = 0;
-        bool ok = mm >= 1 && mm <= max_m;
-        for (uint32_t k = 0; ok && k < mm; ++k) {
+        if (mm < 1 || mm > max_m || (totals && totals[r] < 1)) {
+            set_dev_err(bad, DEV_BAD_CLUSTERING);
+            continue;
+        }
+        bool empty = false, big = false;
+        for (uint32_t k = 0; k < mm; ++k) {
             const uint32_t c = sizes[r * max_m + k];
-            ok = c >= 1;
+            empty |= c < 1;
             n += c;
         }
-        if (!ok || n > max_n) {
+        if (empty) {
+            set_dev_err(bad, DEV_EMPTY_CLUSTER);
+            continue;
+        }
+        if (totals) {
+            for (uint32_t k = 0; k < mm; ++k) big |= sizes[r * max_m + k] > totals[r];
+            n = totals[r];
+        }
+        if (big || n > max_n) {
             set_dev_err(bad, DEV_BAD_CLUSTERING);
             continue;
         }
@@ -365,19 +382,20 @@ int cdx_cluster_rows(cdx_ctx* ctx, const uint32_t* ids, uint64_t rows, uint32_t 
     return CDX_OK;
 }
 
-int cdx_entropy_from_sizes(cdx_ctx* ctx, const uint32_t* sizes, const uint32_t* m, uint64_t rows,
+int cdx_entropy_from_sizes(cdx_ctx* ctx, const uint32_t* sizes, const uint32_t* m, const uint32_t* totals,
+                           uint64_t rows,
                            uint32_t max_m, uint32_t max_n, double* H, double* Hcert) {
     using namespace cdx;
     if (!ctx) return CDX_EINVAL;
     if (!sizes || !m || max_m == 0) return set_error(ctx, CDX_EINVAL, "semantic_entropy: invalid clustering");
-    if (max_n == 0 || max_n > (1u << 16)) return set_error(ctx, CDX_EINVAL, "entropy_from_sizes: max_n must be 1..65536");
+    if (max_n == 0 || max_n > 2048) return set_error(ctx, CDX_EINVAL, "entropy_from_sizes: max_n must be 1..2048 (use cdx_entropy_one above)");
     if (rows == 0) return CDX_OK;
     std::vector<uint32_t> ns(max_n + 1);
     for (uint32_t i = 0; i <= max_n; ++i) ns[i] = i;
     TermTables tt;
     if (int st = build_term_tables(ctx, ns.data(), max_n + 1, &tt)) return st;
     const uint64_t blocks = std::min<uint64_t>((rows + 255) / 256, static_cast<uint64_t>(ctx->sm_count) * 8);
-    entropy_sizes_kernel<<<static_cast<unsigned>(blocks), 256, 0, ctx->stream>>>(sizes, m, rows, max_m, tt.tab, tt.logs,
+    entropy_sizes_kernel<<<static_cast<unsigned>(blocks), 256, 0, ctx->stream>>>(sizes, m, totals, rows, max_m, tt.tab, tt.logs,
                                                                                max_n, H, Hcert, ctx->d_err);
     CDX_CHECK_LAUNCH(ctx, "entropy_from_sizes");
     return CDX_OK;
