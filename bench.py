@@ -331,7 +331,8 @@ def bench_sc(args, cfg, rank, world, cx, with_e2e=True):
             ("kept", torch.int32))}
     out["scalars"] = torch.zeros((3,), dtype=torch.int64, device="cuda")
     torch.cuda.synchronize()
-    l0 = [0]
+    from paper_2412_20993_b200.sharding import Sharded
+    sh = Sharded(cx)
 
     def step(seg):
         e = seg_events(seg, "sc_certaindex")
@@ -342,15 +343,13 @@ def bench_sc(args, cfg, rank, world, cx, with_e2e=True):
         cx.allocate_scan(meets, R, P, pol, kept_base=rank * R, out=out)
         if e is not None:
             e.record(torch.cuda.current_stream())
+        if world > 1:  # global token offsets: allgather of shard budget totals (8 B/rank) + rebase
+            totals = sh.allgather(out["scalars"][2:3])
+            cx.offsets_rebase(out["offsets"], totals, rank)
 
     l0 = cx.launches
     ms, per, clocks = timed(args, world, step, ["sc_certaindex", "allocate_scan"])
     launches = in_timed(cx, l0, args)
-    if world > 1:  # global token offsets: allgather of shard budget totals (8 B per rank)
-        import torch.distributed as dist
-        tot = out["scalars"][2:3].clone()
-        allt = [torch.zeros_like(tot) for _ in range(world)]
-        dist.all_gather(allt, tot)
     n_kept = int(out["scalars"][0])
     k2_bytes = R * P * S * 4 + R * P * 4 + R * ((P + 31) // 32) * 4
     k5_bytes = R * ((P + 31) // 32) * 4 + R * (4 + 1 + 4 + 8) + n_kept * 4
@@ -449,26 +448,38 @@ def bench_reward(args, cfg, rank, world, cx, with_e2e=True):
 
 
 def bench_gang(args, cfg, rank, world, cx, with_e2e=True):
+    """Config E.  N=1: one radix-sorted order of all programs.  N>1: the 4M programs are
+    sharded (strong scaling of the fixed trace), each rank sorts its shard, the sorted key
+    runs are allgathered over NCCL and merged on every rank (sharding.Sharded.gang_order)."""
     import numpy as np
     import torch
     from paper_2412_20993_b200 import InterPolicy
+    from paper_2412_20993_b200.sharding import Sharded, max_shard, shard_range
     N = cfg["N"]
     soa, now = gang_inputs(N, 20993 + 5, cfg["limit"])
-    dev = {k: (torch.from_numpy(v.view(np.int16)) if v.dtype == np.uint16 else torch.from_numpy(v)).cuda()
-           for k, v in soa.items()}
+    g0, gn = shard_range(N, rank, world)
+    dev = {k: (torch.from_numpy(np.ascontiguousarray(v[g0:g0 + gn]).view(np.int16)) if v.dtype == np.uint16
+               else torch.from_numpy(np.ascontiguousarray(v[g0:g0 + gn]))).cuda() for k, v in soa.items()}
     pol = InterPolicy(order=1, starvation_limit=cfg["limit"], prior_tokens=cfg["prior"])
+    sh = Sharded(cx)
+    stride = max_shard(N, world)
 
     def step(seg):
         e = seg_events(seg, "gang_priority")
-        cx.gang_priority(dev, pol, now)
+        if world == 1:
+            cx.gang_priority(dev, pol, now)
+        else:
+            sh.gang_order(dev, pol, now, g0, stride)
         if e is not None:
             e.record(torch.cuda.current_stream())
 
     l0 = cx.launches
     ms, per, clocks = timed(args, world, step, ["gang_priority"])
-    b = N * (8 + 8 + 8 + 4 + 2 + 2 + 1) + N * 4
-    return dict(value=N * world / (ms / 1e3), ms=ms, launches=in_timed(cx, l0, args), clocks=clocks, kernel="gang_priority (radix sort, all passes)",
-                kernel_ms=per["gang_priority"], kernel_bytes=b, step_bytes=b, extra={}, e2e=None)
+    b = gn * (8 + 8 + 8 + 4 + 2 + 2 + 1) + gn * 4
+    return dict(value=N / (ms / 1e3), ms=ms, launches=in_timed(cx, l0, args), clocks=clocks,
+                kernel="gang_priority (radix sort, all passes)" + (" + allgather + merge" if world > 1 else ""),
+                kernel_ms=per["gang_priority"], kernel_bytes=b, step_bytes=b, extra={}, e2e=None,
+                scaling="strong")
 
 
 BENCH = {"sc": bench_sc, "cot": bench_cot, "reward": bench_reward, "gang": bench_gang}
@@ -522,11 +533,15 @@ def main():
         ach = res["kernel_bytes"] / (res["kernel_ms"] / 1e3) / 1e9
         cfg_out = {"workload": args.config, "desc": cfg["desc"],
                    **{k: v for k, v in cfg.items() if k not in ("kind", "desc", "conv_hi")},
-                   "parallelism": f"request shards x{world} (no data-path collective)",
+                   "parallelism": (f"program shards x{world}, NCCL allgather of sorted key runs + merge"
+                                   if cfg["kind"] == "gang" else
+                                   f"request shards x{world} (no data-path collective; 8 B/rank allgather "
+                                   "of budget totals for global offsets)"),
                    "l2": "inputs > L2 (126 MB) for C/B/D/E: no flush needed"}
         line = {
             "metric": METRIC, "value": res["value"], "unit": UNIT, "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": res["ms"], "higher_is_better": True, "scaling": "weak",
+            "warmup": args.warmup, "ms_per_step": res["ms"], "higher_is_better": True,
+            "scaling": res.get("scaling", "weak"),
             "vs_baseline": None, "dtype": "u32 ids / f64 certaindex (f32 store)", "data": "synthetic",
             "config": cfg_out,
             "roofline": {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,

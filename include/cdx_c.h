@@ -302,10 +302,21 @@ int cdx_canon_intern(cdx_ctx* ctx, const char* bytes, const uint64_t* offsets, u
 int cdx_gang_priority(cdx_ctx* ctx, const cdx_prog_soa* progs, uint64_t N,
                       const cdx_inter_policy* pol, double now, uint32_t* order, uint64_t* n_out,
                       uint8_t* escalated, uint64_t* keys);
-/* Merge `runs` sorted runs (concatenated keys u64[total][3] + ids u32[total], run_off
- * u64[runs+1]) into one global order (ids out u32[total]).  Used after the NCCL allgather. */
-int cdx_gang_merge(cdx_ctx* ctx, const uint64_t* keys, const uint32_t* ids,
-                   const uint64_t* run_off, uint32_t runs, uint32_t* order_out);
+/* Merge `runs` sorted runs of composite keys (from cdx_gang_priority's `keys`, u64[.][3] =
+ * {priority word, arrival bits, program id}) into the global order.  Run q is
+ * keys[q*stride .. q*stride + run_len[q]) — the receive layout of an allgather padded to
+ * `stride` keys per rank.  run_len u64[runs] is a DEVICE array (the gathered per-rank
+ * counts, so no host round trip).  order_out u32[sum run_len] receives program ids;
+ * total (device u64, nullable) their count.  Used after the NCCL allgather (K6).        */
+int cdx_gang_merge(cdx_ctx* ctx, const uint64_t* keys, const uint64_t* run_len, uint32_t runs,
+                   uint64_t stride, uint32_t* order_out, uint64_t* total);
+
+/* Global token offsets across request shards (K5 multi-GPU): offsets[i] += sum of
+ * shard_totals[q] for q < rank.  shard_totals i64[world] is the allgathered vector of
+ * per-rank budget totals (DEVICE).  Concatenating the ranks' offsets then equals the
+ * single-GPU exclusive scan.                                                             */
+int cdx_offsets_rebase(cdx_ctx* ctx, int64_t* offsets, uint64_t R, const int64_t* shard_totals,
+                       uint32_t rank);
 
 /* ---- end-to-end host entry: SC certaindex + allocate from HOST buffers ---------------
  * Streams ids (host, ideally pinned) through the device in chunks of whole requests,

@@ -360,11 +360,16 @@ class Context:
         n = n_out.value
         return order[:n], (esc[:N] if esc is not None else None), (keys[:n] if keys is not None else None)
 
-    def gang_merge(self, keys, ids, run_off):
+    def gang_merge(self, keys, run_len, stride: int, total=None):
+        """keys i64[runs*stride][3] (padded runs), run_len i64[runs] on the device."""
         t = self.torch
-        total = ids.shape[0]
-        out = self.empty((max(total, 1),), t.int32)
+        runs = run_len.shape[0]
+        out = self.empty((max(runs * stride, 1),), t.int32)
         self._bind_stream()
-        self._check(self.lib.cdx_gang_merge(self.h, _ptr(keys), _ptr(ids), _ptr(run_off), run_off.shape[0] - 1,
-                                            _ptr(out)))
-        return out[:total]
+        self._check(self.lib.cdx_gang_merge(self.h, _ptr(keys), _ptr(run_len), runs, stride, _ptr(out),
+                                            _ptr(total)))
+        return out
+
+    def offsets_rebase(self, offsets, shard_totals, rank: int):
+        self._bind_stream()
+        self._check(self.lib.cdx_offsets_rebase(self.h, _ptr(offsets), offsets.shape[0], _ptr(shard_totals), rank))

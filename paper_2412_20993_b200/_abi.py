@@ -95,7 +95,8 @@ SIGNATURES = {
     "cdx_canon_intern": (C.c_int, [P, P, P, U64, C.POINTER(C.c_char_p), U32, P, P, P, C.POINTER(U64)]),
     "cdx_gang_priority": (C.c_int, [P, C.POINTER(ProgSoA), U64, C.POINTER(InterPolicy), C.c_double, P,
                                     C.POINTER(U64), P, P]),
-    "cdx_gang_merge": (C.c_int, [P, P, P, P, U32, P]),
+    "cdx_gang_merge": (C.c_int, [P, P, P, U32, U64, P, P]),
+    "cdx_offsets_rebase": (C.c_int, [P, P, U64, P, U32]),
     "cdx_sc_decide_host": (C.c_int, [P, P, U64, U32, U32, C.POINTER(Threshold), U32, C.POINTER(AllocPolicy),
                                      P, P, P, P, P]),
 }

@@ -273,3 +273,29 @@ extern "C" int cdx_allocate_scan(cdx_ctx* ctx, const uint32_t* meets_bits, uint6
     CDX_CHECK_LAUNCH(ctx, "allocate_scan");
     return CDX_OK;
 }
+
+namespace cdx {
+namespace {
+__global__ void rebase_kernel(int64_t* __restrict__ off, uint64_t n, const int64_t* __restrict__ totals,
+                              uint32_t rank) {
+    int64_t b = 0;
+    for (uint32_t q = 0; q < rank; ++q) b += totals[q];
+    for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<uint64_t>(gridDim.x) * blockDim.x)
+        off[i] += b;
+}
+}  // namespace
+}  // namespace cdx
+
+extern "C" int cdx_offsets_rebase(cdx_ctx* ctx, int64_t* offsets, uint64_t R, const int64_t* shard_totals,
+                                  uint32_t rank) {
+    using namespace cdx;
+    if (!ctx) return CDX_EINVAL;
+    if (R == 0 || rank == 0) return CDX_OK;
+    if (!offsets || !shard_totals) return set_error(ctx, CDX_EINVAL, "offsets_rebase: null pointer");
+    const uint64_t want = (R / 2 + 255) / 256;  // 2 x int64 per thread-iteration is plenty for 8 B/request
+    const unsigned grid = static_cast<unsigned>(std::max<uint64_t>(1, std::min<uint64_t>(want, ctx->sm_count * 4ull)));
+    rebase_kernel<<<grid, 256, 0, ctx->stream>>>(offsets, R, shard_totals, rank);
+    CDX_CHECK_LAUNCH(ctx, "offsets_rebase");
+    return CDX_OK;
+}

@@ -316,26 +316,38 @@ __device__ __forceinline__ bool key_less(const uint64_t* k, uint64_t i, uint64_t
     if (b1 != a1) return b1 < a1;
     return b2 < a2;
 }
-__global__ void merge_rank(const uint64_t* __restrict__ keys, const uint32_t* __restrict__ ids,
-                           const uint64_t* __restrict__ run_off, uint32_t runs, uint64_t total,
-                           uint32_t* __restrict__ out) {
-    for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < total;
+// Merge of per-rank sorted runs laid out with a fixed stride (the NCCL allgather receive
+// buffer: run q occupies [q*stride, q*stride + run_len[q])).  Keys are unique (the id is the
+// last key word), so an element's global position is its index in its own run plus, for
+// every other run, the number of keys there that are smaller: a merge-path rank computed
+// with one binary search per run, no global synchronisation.
+__global__ void merge_rank(const uint64_t* __restrict__ keys, const uint64_t* __restrict__ run_len, uint32_t runs,
+                           uint64_t stride, uint32_t* __restrict__ out, uint64_t* __restrict__ total) {
+    const uint64_t slots = static_cast<uint64_t>(runs) * stride;
+    for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < slots;
          i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
-        uint32_t r = 0;
-        while (r + 1 < runs && run_off[r + 1] <= i) ++r;
+        const uint32_t r = static_cast<uint32_t>(i / stride);
+        const uint64_t j = i - static_cast<uint64_t>(r) * stride;
+        if (j >= run_len[r]) continue;
         const uint64_t a0 = keys[3 * i], a1 = keys[3 * i + 1], a2 = keys[3 * i + 2];
-        uint64_t pos = i - run_off[r];
+        uint64_t pos = j;
         for (uint32_t q = 0; q < runs; ++q) {
             if (q == r) continue;
-            uint64_t lo = run_off[q], hi = run_off[q + 1];
-            while (lo < hi) {  // number of keys in run q that are < (a0,a1,a2)
+            uint64_t lo = static_cast<uint64_t>(q) * stride, hi = lo + run_len[q];
+            const uint64_t base = lo;
+            while (lo < hi) {  // keys of run q that are < (a0,a1,a2)
                 const uint64_t mid = (lo + hi) >> 1;
                 if (key_less(keys, mid, a0, a1, a2)) lo = mid + 1;
                 else hi = mid;
             }
-            pos += lo - run_off[q];
+            pos += lo - base;
         }
-        out[pos] = ids[i];
+        out[pos] = static_cast<uint32_t>(a2);
+    }
+    if (total && blockIdx.x == 0 && threadIdx.x == 0) {
+        uint64_t t = 0;
+        for (uint32_t q = 0; q < runs; ++q) t += run_len[q];
+        *total = t;
     }
 }
 
@@ -428,19 +440,15 @@ extern "C" int cdx_gang_priority(cdx_ctx* ctx, const cdx_prog_soa* progs, uint64
     return CDX_OK;
 }
 
-extern "C" int cdx_gang_merge(cdx_ctx* ctx, const uint64_t* keys, const uint32_t* ids, const uint64_t* run_off,
-                              uint32_t runs, uint32_t* order_out) {
+extern "C" int cdx_gang_merge(cdx_ctx* ctx, const uint64_t* keys, const uint64_t* run_len, uint32_t runs,
+                              uint64_t stride, uint32_t* order_out, uint64_t* total) {
     using namespace cdx;
     if (!ctx) return CDX_EINVAL;
-    if (!keys || !ids || !run_off || !order_out || runs == 0) return set_error(ctx, CDX_EINVAL, "gang_merge: bad args");
-    std::vector<uint64_t> ro(runs + 1);
-    cudaError_t e = cudaMemcpyAsync(ro.data(), run_off, (runs + 1) * 8, cudaMemcpyDeviceToHost, ctx->stream);
-    if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
-    if (e != cudaSuccess) return cuda_fail(ctx, e, "gang_merge");
-    const uint64_t total = ro[runs];
-    if (total == 0) return CDX_OK;
+    if (!keys || !run_len || !order_out || runs == 0) return set_error(ctx, CDX_EINVAL, "gang_merge: bad args");
+    if (stride == 0) return CDX_OK;
     Launch L{ctx};
-    merge_rank<<<L.grid(total), 256, 0, ctx->stream>>>(keys, ids, run_off, runs, total, order_out);
+    merge_rank<<<L.grid(static_cast<uint64_t>(runs) * stride), 256, 0, ctx->stream>>>(keys, run_len, runs, stride,
+                                                                                      order_out, total);
     CDX_CHECK_LAUNCH(ctx, "gang_merge");
     return CDX_OK;
 }

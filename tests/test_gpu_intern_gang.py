@@ -100,17 +100,20 @@ def test_gang_merge_equals_single_sort(ctx):
     soa, now = _gang_inputs(N, 5)
     pol = InterPolicy(order=1, starvation_limit=0.6, prior_tokens=128.0)
     ref, _ = O.gang_order(soa, 1, 0.6, 128.0, now)
-    keys, ids, offs = [], [], [0]
+    stride = N // ranks + 7  # padded receive layout of the allgather
+    keys = torch.full((ranks * stride, 3), -1, dtype=torch.int64, device="cuda")
+    lens = []
     for r in range(ranks):
         sl = slice(r * N // ranks, (r + 1) * N // ranks)
         part = {k: v[sl] for k, v in soa.items()}
         o, _, k = ctx.gang_priority(_to_dev(part), pol, now, id_base=sl.start, want_keys=True)
-        keys.append(k)
-        ids.append(o)
-        offs.append(offs[-1] + o.shape[0])
-    out = ctx.gang_merge(torch.cat(keys), torch.cat(ids), torch.tensor(offs, dtype=torch.int64, device="cuda"))
+        keys[r * stride: r * stride + k.shape[0]] = k
+        lens.append(k.shape[0])
+    total = torch.zeros((1,), dtype=torch.int64, device="cuda")
+    out = ctx.gang_merge(keys, torch.tensor(lens, dtype=torch.int64, device="cuda"), stride, total=total)
     ctx.sync()
-    assert np.array_equal(out.cpu().numpy().view(np.uint32), ref)
+    assert int(total) == len(ref) == sum(lens)
+    assert np.array_equal(out[: len(ref)].cpu().numpy().view(np.uint32), ref)
 
 
 def test_gang_errors(ctx):
