@@ -21,6 +21,8 @@
 // (box {32, 1, PROGS}, 128-byte swizzle) so a thread reads its program's row without bank
 // conflicts; a CTA walks its tile of programs step by step through a 2-deep ring.
 #include <algorithm>
+#include <cmath>
+#include <cstring>
 #include <cstdlib>
 #include <vector>
 
@@ -33,10 +35,15 @@ constexpr int RW_PROGS = 64;   // programs (threads) per CTA
 constexpr int RW_KM = 8;       // register cluster slots per program
 constexpr int RW_STAGES = 2;
 constexpr int RW_MAX_TH = 8;
+constexpr int RQ_PROGS = 32;   // quad kernel: programs per CTA (4 lanes each)
+constexpr int RQ_MAX_T = 64;   // quad kernel: steps staged in the smem output tile
+constexpr int RQ_MAX_BOXES = 4;  // quad kernel: W <= 128
 
 struct RwParams {
-    CUtensorMap tm_r;  // rewards {W, T, G}
+    CUtensorMap tm_r;  // rewards {W, T, G}, box {32, 1, RW_PROGS}
     CUtensorMap tm_i;  // ids     {W, T, G}
+    CUtensorMap tq_r;  // rewards, box {32, 1, RQ_PROGS} (quad kernel)
+    CUtensorMap tq_i;  // ids
     const float* rewards;
     const uint32_t* ids;
     const uint8_t* agg;
@@ -56,10 +63,23 @@ struct RwParams {
     uint32_t stages;          // ring depth (<= RW_STAGES)
     int tma;
     int n_th[2];
+    // the AND of inclusive thresholds per (aggregation, signal) as one closed interval:
+    // lo = max of the >= cutoffs, hi = min of the <= cutoffs; has = any threshold on it
+    double box_lo[2][2], box_hi[2][2];
+    uint8_t box_has[2][2];
     uint8_t th_sig[2][RW_MAX_TH];
     uint8_t th_dir[2][RW_MAX_TH];
     double th_cut[2][RW_MAX_TH];
 };
+
+// combined_meets_thresholds over {H~, R} (metrics.cpp:159-171): an AND of inclusive
+// compares is the interval test above (NaN fails either way); signals without a threshold
+// are not looked at, as in the reference.
+__device__ __forceinline__ bool meets_box(const RwParams& p, int a, double hc, double rv) {
+    const bool okh = !p.box_has[a][0] || (hc >= p.box_lo[a][0] && hc <= p.box_hi[a][0]);
+    const bool okr = !p.box_has[a][1] || (rv >= p.box_lo[a][1] && rv <= p.box_hi[a][1]);
+    return okh && okr;
+}
 
 __device__ __forceinline__ bool meets_th(const RwParams& p, int a, double hc, bool has_h, double rv) {
     bool ok = true;
@@ -216,6 +236,292 @@ __global__ void __launch_bounds__(RW_PROGS) reward_kernel(const __grid_constant_
 }
 
 // ---------------------------------------------------------------------------------------
+// Quad kernel (W % 32 == 0, W <= 128, T <= 64): FOUR lanes per program, 32 programs per CTA.
+//
+// Per step every lane takes W/4 of the program's nodes straight from the TMA-staged,
+// 128B-swizzled step slice (the half of a box a lane reads alternates with the program's
+// parity, so the 8 lanes of a quarter-warp always hit 8 distinct bank groups).  Per node
+// the work is kept to a handful of instructions:
+//   * rewards: the unsigned max and (min - 1) of the float bits (two min/max ops) and an
+//     FP64 add into the lane's partial sum.  On this path summation order does not matter:
+//     when every reward is +0 or a float in [2^-(30-L), 1] (n <= 2^L paths), every partial
+//     sum is a multiple of 2^-(53-L) below 2^L and exact in double, so the quad's sum equals
+//     the reference's left fold (std::accumulate, metrics.cpp:135) bit for bit, and the max
+//     of the bits is the max of the values (std::max_element, :133).  Anything else (tiny,
+//     -0.0, negative, NaN, > 1) sends the program to the serial overflow kernel, which folds
+//     in the reference's order and performs the range check (metrics.cpp:129-132).
+//   * clusters: KW compares against the first-seen table (keys replicated in the 4 lanes),
+//     KW = the warp's largest table size; each hit is a predicated increment.  Unused slots
+//     duplicate key 0, so no slot-validity test sits on the hot compare.  A value in no
+//     valid slot is a miss, detected once per step from the hit total; a step with a miss is
+//     re-walked by its quad in node order (smem broadcast reads) to append new keys in
+//     first-seen order and count their occurrences.  More than KM keys -> overflow kernel.
+// After each step the quad sums its counters (packed xor-shuffles), lane 0 folds
+// h -= T_n[count] in first-seen order (host term row n = (t+1)W), clamps, applies the
+// thresholds and stages R / H~ in a smem tile that is written out coalesced at the end.
+struct QuadLane {
+    double psum = 0.0;         // exact partial sum of this lane's rewards
+    uint32_t maxb = 0;         // max float bits (rewards are >= +0 on the exact path)
+    uint32_t minb = 0xffffffffu;  // min of (bits - 1): +0 maps to 0xffffffff
+    uint32_t key[RW_KM], cnt[RW_KM];
+};
+
+template <int K, int BOXES>
+__device__ __forceinline__ void quad_pass(QuadLane& L, const uint8_t* sr, const uint8_t* si, uint32_t box_bytes,
+                                          uint32_t prow, uint32_t q, bool with_ids) {
+#pragma unroll
+    for (uint32_t j = 0; j < 2 * BOXES; ++j) {
+        const uint32_t b = j >> 1, h = (j ^ prow) & 1u;
+        const uint32_t off = b * box_bytes + swz128(prow, h * 4u + q);
+        const uint4 f = *reinterpret_cast<const uint4*>(sr + off);
+        const uint32_t rb[4] = {f.x, f.y, f.z, f.w};
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+            L.maxb = max(L.maxb, rb[e]);
+            L.minb = min(L.minb, rb[e] - 1u);
+            L.psum = __dadd_rn(L.psum, static_cast<double>(__uint_as_float(rb[e])));
+        }
+        if (K > 0 && with_ids) {
+            const uint4 u = *reinterpret_cast<const uint4*>(si + off);
+            const uint32_t iv[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+#pragma unroll
+                for (int k = 0; k < K; ++k)  // ISETP + predicated IADD per slot
+                    asm("{\n\t.reg .pred p;\n\tsetp.eq.u32 p, %1, %2;\n\t@p add.u32 %0, %0, 1;\n\t}"
+                        : "+r"(L.cnt[k])
+                        : "r"(L.key[k]), "r"(iv[e]));
+            }
+        }
+    }
+}
+
+template <int BOXES>
+__device__ __forceinline__ void quad_pass_k(int K, QuadLane& L, const uint8_t* sr, const uint8_t* si,
+                                            uint32_t box_bytes, uint32_t prow, uint32_t q, bool with_ids) {
+    switch (K) {  // warp-uniform
+        case 0: quad_pass<0, BOXES>(L, sr, si, box_bytes, prow, q, with_ids); break;
+        case 1: quad_pass<1, BOXES>(L, sr, si, box_bytes, prow, q, with_ids); break;
+        case 2: quad_pass<2, BOXES>(L, sr, si, box_bytes, prow, q, with_ids); break;
+        case 3: quad_pass<3, BOXES>(L, sr, si, box_bytes, prow, q, with_ids); break;
+        case 4: quad_pass<4, BOXES>(L, sr, si, box_bytes, prow, q, with_ids); break;
+        case 5: quad_pass<5, BOXES>(L, sr, si, box_bytes, prow, q, with_ids); break;
+        case 6: quad_pass<6, BOXES>(L, sr, si, box_bytes, prow, q, with_ids); break;
+        case 7: quad_pass<7, BOXES>(L, sr, si, box_bytes, prow, q, with_ids); break;
+        default: quad_pass<8, BOXES>(L, sr, si, box_bytes, prow, q, with_ids); break;
+    }
+}
+
+template <int BOXES>
+__global__ void __launch_bounds__(RQ_PROGS * 4) reward_quad_kernel(const __grid_constant__ RwParams p,
+                                                                   uint32_t exact_min_bits) {
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+    const bool with_ids = p.ids != nullptr;
+    const uint32_t arrays = with_ids ? 2u : 1u;
+    const uint32_t box_bytes = RQ_PROGS * 128u;
+    const uint32_t stage_bytes = BOXES * box_bytes;  // per array
+    uint64_t* bar = reinterpret_cast<uint64_t*>(smem + p.stages * arrays * stage_bytes);
+    float* outR = reinterpret_cast<float*>(smem + p.stages * arrays * stage_bytes + 64);
+    float* outH = outR + RQ_PROGS * p.T;
+    uint32_t* outM = reinterpret_cast<uint32_t*>(outH + RQ_PROGS * p.T);
+
+    const uint32_t tid = threadIdx.x, lane = tid & 31u;
+    const uint32_t prow = tid >> 2, q = tid & 3u;  // program row in the CTA, lane in the quad
+    const uint64_t g0 = static_cast<uint64_t>(blockIdx.x) * RQ_PROGS;
+    const uint64_t g = g0 + prow;
+    const bool live = g < p.G;
+    const uint32_t T = p.T, W = p.W;
+    const uint32_t per_lane = W / 4;
+    const uint64_t policy = policy_evict_first();
+
+    if (tid == 0) {
+        tma_prefetch_desc(&p.tq_r);
+        if (with_ids) tma_prefetch_desc(&p.tq_i);
+        for (uint32_t s = 0; s < p.stages; ++s) mbar_init(&bar[s], 1);
+        fence_mbar_init();
+    }
+    __syncthreads();
+    auto issue = [&](uint32_t t, uint32_t stage) {
+        uint8_t* dr = smem + stage * arrays * stage_bytes;
+        mbar_expect_tx(&bar[stage], stage_bytes * arrays);
+        for (uint32_t b = 0; b < BOXES; ++b) {
+            tma_load_3d(dr + b * box_bytes, &p.tq_r, static_cast<int32_t>(b * 32), static_cast<int32_t>(t),
+                        static_cast<int32_t>(g0), &bar[stage], policy);
+            if (with_ids)
+                tma_load_3d(dr + stage_bytes + b * box_bytes, &p.tq_i, static_cast<int32_t>(b * 32),
+                            static_cast<int32_t>(t), static_cast<int32_t>(g0), &bar[stage], policy);
+        }
+    };
+    if (tid == 0)
+        for (uint32_t s = 0; s < p.stages && s < T; ++s) issue(s, s);
+
+    const uint8_t a = live ? p.agg[g] : 0;
+    QuadLane L;
+#pragma unroll
+    for (int k = 0; k < RW_KM; ++k) L.key[k] = L.cnt[k] = 0;
+    uint32_t m = 0;
+    bool ovf = !live;
+    const uint32_t qmask = 0xFu << (lane & ~3u);
+    uint32_t before = 0;  // this lane's hits on valid slots so far (a miss = fewer new hits than nodes)
+
+    uint32_t stage = 0, phase = 0;
+    for (uint32_t t = 0; t < T; ++t) {
+        const uint8_t* sr = smem + stage * arrays * stage_bytes;
+        const uint8_t* si = sr + stage_bytes;
+        const int kw = with_ids ? static_cast<int>(__reduce_max_sync(0xffffffffu, ovf ? 0u : m)) : 0;
+        mbar_wait(&bar[stage], phase);
+        quad_pass_k<BOXES>(kw, L, sr, si, box_bytes, prow, q, with_ids);
+        if (with_ids) {
+            uint32_t after = 0;
+#pragma unroll
+            for (int k = 0; k < RW_KM; ++k) after += static_cast<uint32_t>(k) < m ? L.cnt[k] : 0u;
+            const bool miss = after - before < per_lane;
+            // ---- first-seen insertion.  Each round, every lane finds its earliest node (in
+            // node order) whose value is in no valid slot; the quad's earliest such node is
+            // the next cluster in first-seen order: all 4 lanes append it, then each counts its
+            // own occurrences of it.  Rounds run until no quad of the warp has a miss left
+            // (warp-uniform loop; quads without work idle), one round per new cluster.
+            bool need = (__ballot_sync(0xffffffffu, miss && !ovf) & qmask) != 0;  // quad-uniform
+            while (__any_sync(0xffffffffu, need)) {
+                uint32_t wmin = 0xffffffffu, vmin = 0;
+                if (need) {
+#pragma unroll
+                    for (uint32_t j = 0; j < 2 * BOXES; ++j) {  // own nodes, ascending w
+                        const uint32_t b = j >> 1, h = j & 1u;
+                        const uint4 u = *reinterpret_cast<const uint4*>(si + b * box_bytes + swz128(prow, h * 4u + q));
+                        const uint32_t iv[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+                        for (int e = 0; e < 4; ++e) {
+                            bool in = false;  // unused slots duplicate key 0, so no validity test
+#pragma unroll
+                            for (int k = 0; k < RW_KM; ++k) in = in || L.key[k] == iv[e];
+                            in = in && m > 0;
+                            const uint32_t w = b * 32u + h * 16u + q * 4u + static_cast<uint32_t>(e);
+                            if (!in && w < wmin) {
+                                wmin = w;
+                                vmin = iv[e];
+                            }
+                        }
+                    }
+                }
+#pragma unroll
+                for (int o = 1; o <= 2; o <<= 1) {  // quad min over (w, value of w)
+                    const uint32_t w2 = __shfl_xor_sync(0xffffffffu, wmin, o);
+                    const uint32_t v2 = __shfl_xor_sync(0xffffffffu, vmin, o);
+                    if (w2 < wmin) {
+                        wmin = w2;
+                        vmin = v2;
+                    }
+                }
+                need = need && wmin != 0xffffffffu;
+                if (need && m == RW_KM) {  // a ninth cluster: the overflow kernel finishes it
+                    ovf = true;
+                    need = false;
+                }
+                if (need) {
+#pragma unroll
+                    for (int k = 0; k < RW_KM; ++k) {
+                        if (static_cast<uint32_t>(k) == m || (m == 0 && k > 0)) L.key[k] = vmin;  // dup key 0
+                        if (static_cast<uint32_t>(k) == m) L.cnt[k] = 0;
+                    }
+                    uint32_t c = 0;
+#pragma unroll
+                    for (uint32_t j = 0; j < 2 * BOXES; ++j) {
+                        const uint32_t b = j >> 1, h = j & 1u;
+                        const uint4 u = *reinterpret_cast<const uint4*>(si + b * box_bytes + swz128(prow, h * 4u + q));
+                        c += (u.x == vmin) + (u.y == vmin) + (u.z == vmin) + (u.w == vmin);
+                    }
+#pragma unroll
+                    for (int k = 0; k < RW_KM; ++k)
+                        if (static_cast<uint32_t>(k) == m) L.cnt[k] = c;
+                    ++m;
+                }
+            }
+        }
+        if (with_ids) {
+            before = 0;
+#pragma unroll
+            for (int k = 0; k < RW_KM; ++k) before += static_cast<uint32_t>(k) < m ? L.cnt[k] : 0u;
+        }
+        // ---- quad totals
+        double tot = L.psum;
+        tot = __dadd_rn(tot, __shfl_xor_sync(0xffffffffu, tot, 1));
+        tot = __dadd_rn(tot, __shfl_xor_sync(0xffffffffu, tot, 2));
+        uint32_t mx = L.maxb;
+        mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
+        mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
+        uint32_t tc[RW_KM];
+        if (with_ids) {
+#pragma unroll
+            for (int k = 0; k < RW_KM; k += 2) {  // counts <= 65535: two per shuffle
+                uint32_t pk = L.cnt[k] | (L.cnt[k + 1] << 16);
+                pk += __shfl_xor_sync(0xffffffffu, pk, 1);
+                pk += __shfl_xor_sync(0xffffffffu, pk, 2);
+                tc[k] = pk & 0xffffu;
+                tc[k + 1] = pk >> 16;
+            }
+        }
+        const uint32_t ovf_bal = __ballot_sync(0xffffffffu, ovf);  // every lane votes (no short circuit)
+        ovf = ovf || (ovf_bal & qmask) != 0;
+        if (q == 0 && live) {
+            const uint32_t n = (t + 1) * W;
+            const double rv =
+                a == CDX_AGG_MAX ? static_cast<double>(__uint_as_float(mx)) : __ddiv_rn(tot, static_cast<double>(n));
+            double hc = 0.0;
+            if (with_ids && !ovf) {
+                if (n == 1) {
+                    hc = 1.0;
+                } else {
+                    const double* Tn = p.tab + __ldg(p.row_off + t);
+                    double term[RW_KM];  // every tc[k] <= n (unused slots count key-0 hits): loads in flight together
+#pragma unroll
+                    for (int k = 0; k < RW_KM; ++k) term[k] = __ldg(Tn + tc[k]);
+                    double hh = 0.0;
+#pragma unroll
+                    for (int k = 0; k < RW_KM; ++k)
+                        if (static_cast<uint32_t>(k) < m) hh = __dsub_rn(hh, term[k]);
+                    hh = (0.0 < hh) ? hh : 0.0;
+                    const double ln = __ldg(p.logs + t);
+                    const double v = __ddiv_rn(__dsub_rn(ln, hh), ln);
+                    hc = v < 0.0 ? 0.0 : (1.0 < v ? 1.0 : v);
+                }
+            }
+            outR[prow * T + t] = static_cast<float>(rv);
+            outH[prow * T + t] = static_cast<float>(hc);
+            const bool ok = meets_box(p, a == CDX_AGG_MAX ? 1 : 0, hc, rv);
+            uint32_t& mw = outM[prow * p.words + (t >> 5)];
+            if ((t & 31u) == 0) mw = 0;
+            if (ok) mw |= 1u << (t & 31u);
+        }
+        __syncthreads();  // every lane is done with this stage
+        if (tid == 0 && t + p.stages < T) issue(t + p.stages, stage);
+        if (++stage == p.stages) {
+            stage = 0;
+            phase ^= 1u;
+        }
+    }
+    // ---- programs the fast path cannot finish go to the serial overflow kernel:
+    // every reward must be +0 or in [2^-(30-L), 1] (bits in [exact_min_bits, 0x3f800000])
+    const bool inexact = L.maxb > 0x3f800000u || (L.minb != 0xffffffffu && L.minb + 1u < exact_min_bits);
+    const bool qinexact = (__ballot_sync(0xffffffffu, inexact) & qmask) != 0;
+    if (live && q == 0 && (ovf || qinexact)) {
+        const uint32_t slot = atomicAdd(p.ovf_count, 1u);
+        p.ovf_list[slot] = static_cast<uint32_t>(g);
+    }
+    __syncthreads();
+    // ---- coalesced write-out of the staged tiles (overflow programs are rewritten later)
+    const uint64_t nprog = p.G - g0 < RQ_PROGS ? p.G - g0 : RQ_PROGS;
+    const uint64_t span = nprog * T;
+    for (uint64_t i = tid; i < span; i += blockDim.x) {
+        if (p.R) p.R[g0 * T + i] = outR[i];
+        if (p.H && with_ids) p.H[g0 * T + i] = outH[i];
+    }
+    if (p.meets)
+        for (uint64_t i = tid; i < nprog * p.words; i += blockDim.x) p.meets[g0 * p.words + i] = outM[i];
+}
+
+// ---------------------------------------------------------------------------------------
 // Overflow kernel: one warp per program with > KM distinct answers.  A shared-memory hash
 // table maps answer id -> first-seen ordinal; counts live per ordinal; the entropy fold
 // walks ordinals 0..m-1 (first-seen order) on lane 0.  Rewards are recomputed here too, so
@@ -225,16 +531,16 @@ constexpr int OV_WARPS = 4;
 __global__ void __launch_bounds__(OV_WARPS * 32) reward_overflow_kernel(const __grid_constant__ RwParams p,
                                                                         uint32_t cap_log2) {
     extern __shared__ __align__(16) uint8_t smem[];
-    const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
     const uint32_t cap = 1u << cap_log2;  // hash slots (>= 2 * T * W)
-    const uint32_t nmax = p.T * p.W;
+    const uint32_t nmax = p.ids ? p.T * p.W : 0u;
     uint32_t* hkey = reinterpret_cast<uint32_t*>(smem) + warp * (2 * cap + nmax);
     uint32_t* hord = hkey + cap;
     uint32_t* cnt = hord + cap;
     const uint32_t n_ovf = *p.ovf_count;
-    for (uint32_t j = blockIdx.x * OV_WARPS + warp; j < n_ovf; j += gridDim.x * OV_WARPS) {
+    for (uint32_t j = blockIdx.x * nw + warp; j < n_ovf; j += gridDim.x * nw) {
         const uint64_t g = p.ovf_list[j];
-        for (uint32_t i = lane; i < cap; i += 32) hord[i] = 0xffffffffu;  // empty
+        for (uint32_t i = lane; p.ids && i < cap; i += 32) hord[i] = 0xffffffffu;  // empty
         __syncwarp();
         uint32_t m = 0;
         double sum = 0.0;
@@ -243,7 +549,7 @@ __global__ void __launch_bounds__(OV_WARPS * 32) reward_overflow_kernel(const __
         const uint8_t a = p.agg[g];
         for (uint32_t t = 0; t < p.T; ++t) {
             const uint64_t base = (g * p.T + t) * p.W;
-            for (uint32_t w0 = 0; w0 < p.W; w0 += 32) {
+            for (uint32_t w0 = 0; p.ids && w0 < p.W; w0 += 32) {
                 const uint32_t w = w0 + lane;
                 const bool act = w < p.W;
                 const uint32_t v = act ? __ldg(p.ids + base + w) : 0xffffffffu;
@@ -286,6 +592,7 @@ __global__ void __launch_bounds__(OV_WARPS * 32) reward_overflow_kernel(const __
             if (lane == 0) {
                 for (uint32_t w = 0; w < p.W; ++w) {
                     const float r = __ldg(p.rewards + base + w);
+                    if (r < 0.f || r > 1.f) set_dev_err(p.d_err, DEV_REWARD_RANGE);  // metrics.cpp:129-132
                     sum = __dadd_rn(sum, static_cast<double>(r));
                     if (t == 0 && w == 0) best = r;
                     else if (best < r) best = r;
@@ -293,15 +600,18 @@ __global__ void __launch_bounds__(OV_WARPS * 32) reward_overflow_kernel(const __
                 const uint32_t n = (t + 1) * p.W;
                 const double rv = a == CDX_AGG_MAX ? static_cast<double>(best) : __ddiv_rn(sum, static_cast<double>(n));
                 if (p.R) p.R[g * p.T + t] = static_cast<float>(rv);
-                const double* Tn = p.tab + __ldg(p.row_off + t);
-                double h = 0.0;
-                for (uint32_t k = 0; k < m; ++k) h = __dsub_rn(h, __ldg(Tn + cnt[k]));
-                h = (0.0 < h) ? h : 0.0;
-                const double ln = __ldg(p.logs + t);
-                const double v = __ddiv_rn(__dsub_rn(ln, h), ln);
-                const double hc = n == 1 ? 1.0 : (v < 0.0 ? 0.0 : (1.0 < v ? 1.0 : v));
-                if (p.H) p.H[g * p.T + t] = static_cast<float>(hc);
-                if (meets_th(p, a == CDX_AGG_MAX ? 1 : 0, hc, true, rv)) mword |= 1u << (t & 31u);
+                double hc = 0.0;
+                if (p.ids) {
+                    const double* Tn = p.tab + __ldg(p.row_off + t);
+                    double h = 0.0;
+                    for (uint32_t k = 0; k < m; ++k) h = __dsub_rn(h, __ldg(Tn + cnt[k]));
+                    h = (0.0 < h) ? h : 0.0;
+                    const double ln = __ldg(p.logs + t);
+                    const double v = __ddiv_rn(__dsub_rn(ln, h), ln);
+                    hc = n == 1 ? 1.0 : (v < 0.0 ? 0.0 : (1.0 < v ? 1.0 : v));
+                    if (p.H) p.H[g * p.T + t] = static_cast<float>(hc);
+                }
+                if (meets_th(p, a == CDX_AGG_MAX ? 1 : 0, hc, p.ids != nullptr, rv)) mword |= 1u << (t & 31u);
                 if (p.meets && ((t & 31u) == 31u || t == p.T - 1)) {
                     p.meets[g * p.words + (t >> 5)] = mword;
                     mword = 0;
@@ -347,6 +657,21 @@ extern "C" int cdx_reward_certaindex(cdx_ctx* ctx, const float* rewards, const u
     p.stage_bytes = p.boxes * RW_PROGS * 128u;
     p.n_th[0] = static_cast<int>(n_th_mean);
     p.n_th[1] = static_cast<int>(n_th_max);
+    for (int a = 0; a < 2; ++a) {
+        const cdx_threshold* th = a ? th_max : th_mean;
+        const uint32_t n = a ? n_th_max : n_th_mean;
+        for (int sg = 0; sg < 2; ++sg) {
+            p.box_lo[a][sg] = -INFINITY;
+            p.box_hi[a][sg] = INFINITY;
+            p.box_has[a][sg] = 0;
+        }
+        for (uint32_t i = 0; i < n; ++i) {
+            const int sg = th[i].signal == CDX_SIG_ENTROPY ? 0 : 1;  // validated: entropy or reward
+            p.box_has[a][sg] = 1;
+            if (th[i].dir == CDX_DIR_GE) p.box_lo[a][sg] = std::max(p.box_lo[a][sg], th[i].cutoff);
+            else p.box_hi[a][sg] = std::min(p.box_hi[a][sg], th[i].cutoff);
+        }
+    }
     for (uint32_t i = 0; i < n_th_mean; ++i) {
         p.th_sig[0][i] = th_mean[i].signal;
         p.th_dir[0][i] = th_mean[i].dir;
@@ -386,6 +711,38 @@ extern "C" int cdx_reward_certaindex(cdx_ctx* ctx, const float* rewards, const u
                                    CU_TENSOR_MAP_SWIZZLE_128B));
     }
     p.tma = tma ? 1 : 0;
+    const bool quad = tma && W % 32 == 0 && W <= 32u * RQ_MAX_BOXES && T <= static_cast<uint32_t>(RQ_MAX_T) &&
+                      !getenv("CDX_RW_LEGACY");
+    bool launched_quad = false;
+    if (quad) {
+        const uint64_t dims[3] = {W, T, G};
+        const uint64_t strides[2] = {static_cast<uint64_t>(W) * 4u, static_cast<uint64_t>(T) * W * 4u};
+        const uint32_t box[3] = {32, 1, static_cast<uint32_t>(RQ_PROGS)};
+        if (encode_tmap(&p.tq_r, rewards, 3, dims, strides, box, CU_TENSOR_MAP_DATA_TYPE_FLOAT32,
+                        CU_TENSOR_MAP_SWIZZLE_128B) &&
+            (!ids || encode_tmap(&p.tq_i, ids, 3, dims, strides, box, CU_TENSOR_MAP_DATA_TYPE_UINT32,
+                                 CU_TENSOR_MAP_SWIZZLE_128B))) {
+            p.stages = 2;  // measured: 2 stages beat 1 (0.51 vs 0.59 ms on config D)
+            if (const char* e = getenv("CDX_RQ_STAGES")) p.stages = std::max(1, std::min(RW_STAGES, atoi(e)));
+            const size_t stage = static_cast<size_t>(p.boxes) * RQ_PROGS * 128u * (ids ? 2 : 1);
+            const size_t smem = 1024 + p.stages * stage + 64 + 2u * RQ_PROGS * T * 4u + RQ_PROGS * p.words * 4u;
+            // exact-sum threshold 2^-(30-L), n = T*W <= 2^L (see reward_quad_kernel)
+            int L = 0;
+            while ((1ull << L) < static_cast<uint64_t>(T) * W) ++L;
+            const float exact_min = std::ldexp(1.0f, -(30 - L));
+            uint32_t exact_min_bits;
+            std::memcpy(&exact_min_bits, &exact_min, 4);
+            const unsigned grid = static_cast<unsigned>((G + RQ_PROGS - 1) / RQ_PROGS);
+            void (*kern)(RwParams, uint32_t) = p.boxes == 1   ? reward_quad_kernel<1>
+                                               : p.boxes == 2 ? reward_quad_kernel<2>
+                                               : p.boxes == 3 ? reward_quad_kernel<3>
+                                                              : reward_quad_kernel<4>;
+            cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+            kern<<<grid, RQ_PROGS * 4, smem, ctx->stream>>>(p, exact_min_bits);
+            CDX_CHECK_LAUNCH(ctx, "reward_certaindex(quad)");
+            launched_quad = true;
+        }
+    }
     // one step staged per CTA (more resident CTAs beat a deeper ring here: each thread
     // needs its program's whole step row in shared memory); CDX_RW_STAGES=2 for a ring
     p.stages = 1;
@@ -393,19 +750,24 @@ extern "C" int cdx_reward_certaindex(cdx_ctx* ctx, const float* rewards, const u
     const size_t smem = tma ? 1024 + static_cast<size_t>(p.stages) * (ids ? 2 : 1) * p.stage_bytes + 8 * RW_STAGES
                             : 0;
     const unsigned grid = static_cast<unsigned>((G + RW_PROGS - 1) / RW_PROGS);
-    if (tma) cudaFuncSetAttribute(reward_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-    reward_kernel<<<grid, RW_PROGS, smem, ctx->stream>>>(p);
-    CDX_CHECK_LAUNCH(ctx, "reward_certaindex");
-    if (ids) {
+    if (!launched_quad) {
+        if (tma)
+            cudaFuncSetAttribute(reward_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+        reward_kernel<<<grid, RW_PROGS, smem, ctx->stream>>>(p);
+        CDX_CHECK_LAUNCH(ctx, "reward_certaindex");
+    }
+    if (ids || launched_quad) {
         uint32_t cap_log2 = 1;
-        while ((1u << cap_log2) < 2u * T * W) ++cap_log2;
-        const size_t osmem = static_cast<size_t>(OV_WARPS) * ((2u << cap_log2) + T * W) * 4u;
-        if (osmem > 200u * 1024u) {
-            // very large programs: one warp per CTA
+        while (ids && (1u << cap_log2) < 2u * T * W) ++cap_log2;
+        // per-warp table: 2 * cap hash words + T*W counts; as many warps per CTA as fit
+        const size_t per_warp = ids ? ((2u << cap_log2) + static_cast<size_t>(T) * W) * 4u : 0u;
+        const size_t limit = 220u * 1024u;
+        if (per_warp > limit)
             return set_error(ctx, CDX_EINVAL, "reward_certaindex: T*W too large for the overflow table");
-        }
+        const int warps = per_warp ? static_cast<int>(std::min<size_t>(OV_WARPS, limit / per_warp)) : OV_WARPS;
+        const size_t osmem = std::max<size_t>(16u, warps * per_warp);
         cudaFuncSetAttribute(reward_overflow_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(osmem));
-        reward_overflow_kernel<<<ctx->sm_count, OV_WARPS * 32, osmem, ctx->stream>>>(p, cap_log2);
+        reward_overflow_kernel<<<ctx->sm_count, warps * 32, osmem, ctx->stream>>>(p, cap_log2);
         CDX_CHECK_LAUNCH(ctx, "reward_certaindex(overflow)");
     }
     return CDX_OK;

@@ -109,3 +109,39 @@ def test_reward_sets_facade(ctx):
     out = ctx.reward_sets(flat, off, torch.from_numpy(agg).cuda())
     ctx.sync()
     assert out.cpu().tolist() == [0.9, 0.9, 0.4000000000000001, 0.5]
+
+
+@pytest.mark.parametrize("G,T,W", [(257, 16, 64), (100, 64, 128), (33, 7, 96), (40, 16, 32)])
+@pytest.mark.parametrize("with_ids", [True, False])
+def test_reward_quad_path_arbitrary_floats(ctx, G, T, W, with_ids):
+    """The 4-lanes-per-program kernel (W % 32 == 0) sums in any order only where that is
+    provably exact; programs with tiny values, -0.0 or NaN fall back to the serial left
+    fold.  Every program must still match the reference bit for bit."""
+    rng = np.random.default_rng(G * T + W)
+    rw = rng.random((G, T, W)).astype(np.float32)
+    rw[1, 0, 5] = np.float32(1e-30)          # below the exact-sum threshold
+    rw[2, T - 1, W - 1] = np.float32(-0.0)   # signed zero (max keeps the first maximum)
+    rw[3, :, :] = 0.0
+    rw[4, 0, 0] = np.float32(3.0e-7)
+    rw[5, T // 2, 3] = np.float32(1.0)
+    if G > 6:
+        rw[6, 0, :] = np.float32(2.0 ** -21)
+    ids = rng.integers(0, 7, size=(G, T, W)).astype(np.uint32) if with_ids else None
+    if with_ids:
+        ids[7 % G] = rng.integers(0, 1 << 30, size=(T, W))  # > 8 clusters -> overflow kernel
+        ids[8 % G, :, :] = 42
+    agg = (np.arange(G) % 2).astype(np.uint8)
+    R, H, _ = _run(ctx, rw, ids, agg)
+    _, R32, Ho = O.reward_certaindex(rw, ids, agg)
+    assert np.array_equal(R.view(np.uint32), R32.view(np.uint32))
+    if with_ids:
+        assert np.array_equal(H.view(np.uint32), Ho.view(np.uint32))
+
+
+def test_reward_quad_nan_propagates_like_reference(ctx):
+    rw = np.full((8, 4, 32), 0.5, np.float32)
+    rw[3, 1, 7] = np.nan  # passes the [0,1] check in the reference (comparisons are false)
+    agg = (np.arange(8) % 2).astype(np.uint8)
+    R, _, _ = _run(ctx, rw, None, agg)
+    _, R32, _ = O.reward_certaindex(rw, None, agg)
+    assert np.array_equal(R.view(np.uint32), R32.view(np.uint32))

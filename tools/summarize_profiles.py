@@ -68,47 +68,60 @@ KEYS = [
 ]
 
 
-def full(tag):
+def brief(path):
+    """Summary lines + traffic dict of one `ncu --set full` report."""
+    raw = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    rows = list(csv.reader(raw.splitlines()))
+    if len(rows) < 3:
+        return None, None
+    d = dict(zip(rows[0], rows[2]))
+    u = dict(zip(rows[0], rows[1]))
+    lines = [f"# ncu --set full --clock-control none: {d.get('Kernel Name', path)}"]
+    for key, label in KEYS:
+        if key in d:
+            lines.append(f"{label:32s} {d[key]} {u.get(key, '')}")
+    pipes = {kk.split("pipe_")[1].split(".")[0]: float(v) for kk, v in d.items()
+             if kk.startswith("sm__inst_executed_pipe_") and kk.endswith(".avg.pct_of_peak_sustained_active") and v}
+    lines.append("pipes (% of peak, active): " + ", ".join(f"{a}={b:.1f}" for a, b in
+                                                         sorted(pipes.items(), key=lambda x: -x[1])[:8]))
+    st = {kk.replace("smsp__pcsamp_warps_issue_stalled_", ""): float(v) for kk, v in d.items()
+          if kk.startswith("smsp__pcsamp_warps_issue_stalled_") and not kk.endswith("not_issued") and v}
+    tot = sum(st.values()) or 1
+    lines.append("stall samples: " + ", ".join(f"{a}={b / tot * 100:.1f}%" for a, b in
+                                              sorted(st.items(), key=lambda x: -x[1])[:8]))
+    src = subprocess.run(["ncu", "-i", path, "--page", "source", "--csv", "--print-source", "sass"],
+                         capture_output=True, text=True).stdout
+    ev = {m: src.count(m) for m in ("UTMALDG", "UBLKCP", "SYNCS.ARRIVE.TRANS64", "MATCH.ANY", "LDS.128", "DADD")}
+    lines.append("SASS evidence (static count in the kernel): " + ", ".join(f"{a}={b}" for a, b in ev.items()))
+    traffic = None
+    try:
+        scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+        rb = float(d["dram__bytes_read.sum"]) * scale.get(u.get("dram__bytes_read.sum", "byte"), 1)
+        wb = float(d["dram__bytes_write.sum"]) * scale.get(u.get("dram__bytes_write.sum", "byte"), 1)
+        traffic = {"kernel": d.get("Kernel Name", path), "dram_bytes": rb + wb, "read": rb, "write": wb}
+    except Exception:
+        pass
+    return lines, traffic
+
+
+def full(tag, prefix="r1_full_"):
     traffic = {}
-    for path in sorted(glob.glob(os.path.join(OUT, "r1_full_*.ncu-rep"))):
-        k = path.rsplit("r1_full_", 1)[1].split(".")[0]
-        raw = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
-        rows = list(csv.reader(raw.splitlines()))
-        if len(rows) < 3:
+    for path in sorted(glob.glob(os.path.join(OUT, prefix + "*.ncu-rep"))):
+        k = path.rsplit(prefix, 1)[1].split(".")[0]
+        lines, tr = brief(path)
+        if lines is None:
             continue
-        d = dict(zip(rows[0], rows[2]))
-        u = dict(zip(rows[0], rows[1]))
-        lines = [f"# ncu --set full --clock-control none: {d.get('Kernel Name', k)}"]
-        for key, label in KEYS:
-            if key in d:
-                lines.append(f"{label:32s} {d[key]} {u.get(key, '')}")
-        pipes = {kk.split("pipe_")[1].split(".")[0]: float(v) for kk, v in d.items()
-                 if kk.startswith("sm__inst_executed_pipe_") and kk.endswith(".avg.pct_of_peak_sustained_active") and v}
-        lines.append("pipes (% of peak, active): " + ", ".join(f"{a}={b:.1f}" for a, b in
-                                                             sorted(pipes.items(), key=lambda x: -x[1])[:8]))
-        st = {kk.replace("smsp__pcsamp_warps_issue_stalled_", ""): float(v) for kk, v in d.items()
-              if kk.startswith("smsp__pcsamp_warps_issue_stalled_") and not kk.endswith("not_issued") and v}
-        tot = sum(st.values()) or 1
-        lines.append("stall samples: " + ", ".join(f"{a}={b / tot * 100:.1f}%" for a, b in
-                                                  sorted(st.items(), key=lambda x: -x[1])[:8]))
-        # SASS evidence
-        src = subprocess.run(["ncu", "-i", path, "--page", "source", "--csv", "--print-source", "sass"],
-                             capture_output=True, text=True).stdout
-        ev = {m: src.count(m) for m in ("UTMALDG", "UBLKCP", "SYNCS.ARRIVE.TRANS64", "MATCH.ANY", "LDS.128", "DADD")}
-        lines.append("SASS evidence (static count in the kernel): " + ", ".join(f"{a}={b}" for a, b in ev.items()))
         open(os.path.join(PROF, f"{tag}_full_{k}.txt"), "w").write("\n".join(lines) + "\n")
-        try:
-            unit_r, unit_w = u.get("dram__bytes_read.sum", "byte"), u.get("dram__bytes_write.sum", "byte")
-            scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
-            rb = float(d["dram__bytes_read.sum"]) * scale.get(unit_r, 1)
-            wb = float(d["dram__bytes_write.sum"]) * scale.get(unit_w, 1)
-            traffic[k] = {"kernel": d.get("Kernel Name", k), "dram_bytes": rb + wb, "read": rb, "write": wb}
-        except Exception:
-            pass
+        if tr:
+            traffic[k] = tr
     json.dump(traffic, open(os.path.join(PROF, f"{tag}_traffic.json"), "w"), indent=1)
 
 
 if __name__ == "__main__":
+    if len(sys.argv) > 2 and sys.argv[1] == "--brief":  # ad-hoc: print one report's summary
+        for path in sys.argv[2:]:
+            print("\n".join(brief(path)[0] or [path + ": no data"]) + "\n")
+        sys.exit(0)
     tag = sys.argv[1] if len(sys.argv) > 1 else "r1"
     os.makedirs(PROF, exist_ok=True)
     launches(tag)
