@@ -33,6 +33,11 @@ struct cdx_ctx {
     void* pipe_buf = nullptr;
     size_t pipe_bytes = 0;
     cudaStream_t copy_stream = nullptr;
+    // K5 look-back state, persistent across calls: tile ticket counter + per-tile flags /
+    // aggregates, tagged with a per-call epoch so nothing is cleared between calls
+    void* al_state = nullptr;
+    size_t al_tiles = 0;      // capacity in tiles
+    uint32_t al_epoch = 0;
     // term-table cache (device): keyed by the list of n values it was built for
     double* tt_dev = nullptr;
     size_t tt_bytes = 0;

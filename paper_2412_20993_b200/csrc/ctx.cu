@@ -117,6 +117,7 @@ int build_term_tables(cdx_ctx* ctx, const uint32_t* ns, uint32_t count, TermTabl
     cudaStreamSynchronize(ctx->stream);
     if (bytes > ctx->tt_bytes) {
         if (ctx->tt_dev) cudaFree(ctx->tt_dev);
+    if (ctx->al_state) cudaFree(ctx->al_state);
         ctx->tt_dev = nullptr;
         ctx->tt_bytes = 0;
         if (cudaMalloc(&ctx->tt_dev, bytes) != cudaSuccess) return set_error(ctx, CDX_ECUDA, "term table alloc");
@@ -187,6 +188,7 @@ int cdx_ctx_destroy(cdx_ctx* ctx) {
     if (ctx->scratch2) cudaFree(ctx->scratch2);
     if (ctx->pipe_buf) cudaFree(ctx->pipe_buf);
     if (ctx->tt_dev) cudaFree(ctx->tt_dev);
+    if (ctx->al_state) cudaFree(ctx->al_state);
     if (ctx->d_err) cudaFree(ctx->d_err);
     if (ctx->h_err) cudaFreeHost(ctx->h_err);
     if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);

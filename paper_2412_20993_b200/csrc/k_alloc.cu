@@ -1,8 +1,10 @@
 // k_alloc.cu — K5: certaindex-driven allocation decision + exclusive scan of token budgets
-// + stable compaction of continuing requests, in ONE single-pass kernel (decoupled
-// look-back scan: each tile publishes its aggregate, then resolves its exclusive prefix
-// from its predecessors' published state; tiles are claimed in order from an atomic
-// counter so every predecessor is guaranteed to be resident or finished).
+// + stable compaction of continuing requests, in ONE single-pass kernel with no helper
+// launches (decoupled look-back scan: each tile publishes its aggregate, then resolves its
+// exclusive prefix from its predecessors' published state, 32 tiles per look-back step;
+// tiles take tickets from a persistent counter so every predecessor is resident or done —
+// the last tile to finish rewinds it — and per-call epochs tag the tile records, so
+// nothing is cleared between calls).
 //
 // Semantics restated from SPEC.md:404-412 (scheduler.allocate; no reference code exists):
 //   even               -> grant to the cap
@@ -10,14 +12,26 @@
 //   k_step_threshold   -> re-test every recheck_every units from detect_at on
 //   always terminate at resource_cap.
 // token budget = granted * tokens_per_unit; kept = requests granted past detect_at.
+#include <algorithm>
+
 #include "cdx_internal.cuh"
 
 namespace cdx {
 
 constexpr int AL_THREADS = 256;
-constexpr int AL_ITEMS = 4;
-constexpr int AL_TILE = AL_THREADS * AL_ITEMS;
-constexpr int AL_MAX_WORDS = 128;  // P <= 4096
+constexpr int AL_WARPS = AL_THREADS / 32;
+constexpr int AL_ITEMS = 8;
+constexpr int AL_TILE = AL_THREADS * AL_ITEMS;  // 2048 requests per tile
+constexpr int AL_MAX_WORDS = 128;               // P <= 4096
+
+// Per-tile look-back record.  `flag` = epoch << 2 | state (1 aggregate, 2 inclusive):
+// records from earlier calls carry an older epoch and read as "not yet published".
+struct AlTile {
+    int64_t agg_b, inc_b, agg_s, inc_s;
+    uint32_t agg_k, inc_k;
+    uint32_t flag;
+    uint32_t _pad;
+};
 
 struct AllocParams {
     const uint32_t* meets;
@@ -29,15 +43,13 @@ struct AllocParams {
     uint64_t* n_kept;
     int64_t* tokens_saved;
     int64_t* total_budget;
-    uint32_t* tile_counter;
-    uint32_t* flags;     // [ntiles] 0 = none, 1 = aggregate, 2 = inclusive prefix
-    int64_t* agg_b;      // [ntiles]
-    int64_t* inc_b;
-    uint32_t* agg_k;
-    uint32_t* inc_k;
+    uint32_t* tickets;  // [0] tile tickets, [1] finished tiles; the last tile resets both
+    AlTile* tiles;
     uint64_t R;
     uint32_t ntiles;
-    uint32_t words;
+    uint32_t epoch;
+    uint32_t words;      // meets words per request
+    uint32_t chk_words;  // words that hold a test point (the rest is never read)
     int32_t cap, detect;
     int64_t tpu;
     int64_t base_offset;
@@ -63,137 +75,169 @@ __device__ __forceinline__ T warp_incl_scan(T v, int lane) {
     }
     return v;
 }
+template <typename T>
+__device__ __forceinline__ T warp_sum(T v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
 
+// Striped layout: item i of thread t is request base + i*256 + t, so every load/store
+// instruction is coalesced; request order = (item, warp, lane), which the block scan
+// over (item, warp) totals follows.  Tiles take tickets in launch order, so a tile only
+// ever waits for tiles that are running or done; warp 0 looks back 32 tiles at a time.
 __global__ void __launch_bounds__(AL_THREADS) allocate_scan_kernel(const __grid_constant__ AllocParams p) {
     __shared__ uint32_t s_tile;
-    __shared__ int64_t s_wb[AL_THREADS / 32];
-    __shared__ uint32_t s_wk[AL_THREADS / 32];
+    __shared__ int64_t s_wb[AL_ITEMS * AL_WARPS];
+    __shared__ int64_t s_ws[AL_ITEMS * AL_WARPS];
+    __shared__ uint32_t s_wk[AL_ITEMS * AL_WARPS];
     __shared__ int64_t s_excl_b;
     __shared__ uint32_t s_excl_k;
-    __shared__ int64_t s_saved[AL_THREADS / 32];
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    if (tid == 0) s_tile = atomicAdd(p.tile_counter, 1u);
+    if (tid == 0) s_tile = atomicAdd(&p.tickets[0], 1u);
     __syncthreads();
     const uint32_t tile = s_tile;
+    if (tile >= p.ntiles) __trap();  // a stale ticket counter must fail loudly, never scribble
     const uint64_t base = static_cast<uint64_t>(tile) * AL_TILE;
 
-    // --- per-request decision (thread owns AL_ITEMS consecutive requests) ---
+    // ---- per-request decision, coalesced
     int32_t ek[AL_ITEMS];
-    int64_t tb = 0;
-    uint32_t tk = 0;
-    int64_t saved = 0;
+    int64_t ib[AL_ITEMS];
+    uint32_t ik[AL_ITEMS];
 #pragma unroll
     for (int i = 0; i < AL_ITEMS; ++i) {
-        const uint64_t r = base + static_cast<uint64_t>(tid) * AL_ITEMS + i;
-        ek[i] = 0;
+        const uint64_t r = base + static_cast<uint64_t>(i) * AL_THREADS + tid;
+        int32_t e = 0;
         if (r < p.R) {
-            int32_t e = p.cap;
+            e = p.cap;
             uint8_t why = CDX_EXIT_BUDGET;
-            const uint32_t* mw = p.meets + r * p.words;
-            for (uint32_t w = 0; w < p.words; ++w) {
-                const uint32_t x = __ldg(mw + w) & p.chk[w];
+            for (uint32_t w = 0; w < p.chk_words; ++w) {
+                const uint32_t x = __ldg(p.meets + r * p.words + w) & p.chk[w];
                 if (x) {
                     e = static_cast<int32_t>(w * 32 + __ffs(x));  // knob = probe index + 1
                     why = CDX_EXIT_CERTAIN;
                     break;
                 }
             }
-            ek[i] = e;
             if (p.exit_knob) p.exit_knob[r] = e;
             if (p.reason) p.reason[r] = why;
             if (p.granted) p.granted[r] = e;
-            tb += static_cast<int64_t>(e) * p.tpu;
-            tk += e > p.detect ? 1u : 0u;
-            saved += static_cast<int64_t>(p.cap - e) * p.tpu;
         }
+        ek[i] = e;
+        const int64_t b = static_cast<int64_t>(e) * p.tpu;
+        const uint32_t k = (r < p.R && e > p.detect) ? 1u : 0u;
+        const int64_t sv = r < p.R ? static_cast<int64_t>(p.cap - e) * p.tpu : 0;
+        ib[i] = warp_incl_scan<int64_t>(b, lane);
+        ik[i] = warp_incl_scan<uint32_t>(k, lane);
+        const int64_t ws = warp_sum<int64_t>(sv);
+        if (lane == 31) {
+            s_wb[i * AL_WARPS + warp] = ib[i];
+            s_wk[i * AL_WARPS + warp] = ik[i];
+        }
+        if (lane == 0) s_ws[i * AL_WARPS + warp] = ws;
     }
-
-    // --- block scan of (budget, kept) thread totals ---
-    int64_t ib = warp_incl_scan<int64_t>(tb, lane);
-    uint32_t ik = warp_incl_scan<uint32_t>(tk, lane);
-    int64_t sv = saved;
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) sv += __shfl_down_sync(0xffffffffu, sv, o);
-    if (lane == 31) {
-        s_wb[warp] = ib;
-        s_wk[warp] = ik;
-    }
-    if (lane == 0) s_saved[warp] = sv;
     __syncthreads();
-    int64_t wpre_b = 0;
-    uint32_t wpre_k = 0;
-    int64_t tot_b = 0;
-    uint32_t tot_k = 0;
-    for (int w = 0; w < AL_THREADS / 32; ++w) {
-        if (w < warp) {
-            wpre_b += s_wb[w];
-            wpre_k += s_wk[w];
-        }
-        tot_b += s_wb[w];
-        tot_k += s_wk[w];
-    }
+    // ---- exclusive prefix over the (item, warp) totals: 64 entries, 2 per lane of warp 0
+    if (warp == 0) {
+        const int a0 = 2 * lane, a1 = 2 * lane + 1;
+        const int64_t b0 = s_wb[a0], b1 = s_wb[a1];
+        const uint32_t k0 = s_wk[a0], k1 = s_wk[a1];
+        const int64_t sv = s_ws[a0] + s_ws[a1];
+        const int64_t incb = warp_incl_scan<int64_t>(b0 + b1, lane);
+        const uint32_t inck = warp_incl_scan<uint32_t>(k0 + k1, lane);
+        const int64_t tot_s = warp_sum<int64_t>(sv);
+        const int64_t tot_b = __shfl_sync(0xffffffffu, incb, 31);
+        const uint32_t tot_k = __shfl_sync(0xffffffffu, inck, 31);
+        s_wb[a0] = incb - b0 - b1;
+        s_wb[a1] = incb - b1;
+        s_wk[a0] = inck - k0 - k1;
+        s_wk[a1] = inck - k1;
 
-    // --- decoupled look-back (one thread) ---
-    if (tid == 0) {
-        int64_t tsaved = 0;
-        for (int w = 0; w < AL_THREADS / 32; ++w) tsaved += s_saved[w];
-        if (p.tokens_saved) atomicAdd(reinterpret_cast<unsigned long long*>(p.tokens_saved),
-                                      static_cast<unsigned long long>(tsaved));
-        int64_t eb = 0;
+        // ---- decoupled look-back over earlier tiles, 32 at a time
+        AlTile* T = p.tiles;
+        const uint32_t ep = p.epoch << 2;
+        if (lane == 0) {
+            if (tile == 0) {  // the first tile's aggregate is its inclusive prefix
+                T[0].inc_b = tot_b;
+                T[0].inc_k = tot_k;
+                T[0].inc_s = tot_s;
+            } else {
+                T[tile].agg_b = tot_b;
+                T[tile].agg_k = tot_k;
+                T[tile].agg_s = tot_s;
+            }
+            __threadfence();  // the record is complete before its flag says so
+            st_release(&T[tile].flag, ep | (tile == 0 ? 2u : 1u));
+        }
+        int64_t eb = 0, es = 0;
         uint32_t ekk = 0;
-        if (tile == 0) {
-            p.inc_b[0] = tot_b;
-            p.inc_k[0] = tot_k;
-            __threadfence();
-            st_release(&p.flags[0], 2u);
-        } else {
-            p.agg_b[tile] = tot_b;
-            p.agg_k[tile] = tot_k;
-            __threadfence();
-            st_release(&p.flags[tile], 1u);
-            int64_t j = static_cast<int64_t>(tile) - 1;
-            while (j >= 0) {
+        int64_t j = static_cast<int64_t>(tile) - 1;
+        while (j >= 0) {
+            const int64_t idx = j - lane;
+            uint32_t st = 2;  // before tile 0: an inclusive zero
+            if (idx >= 0) {
                 uint32_t f;
                 do {
-                    f = ld_acquire(&p.flags[j]);
-                } while (f == 0);
-                if (f == 2) {
-                    eb += *reinterpret_cast<volatile int64_t*>(&p.inc_b[j]);
-                    ekk += *reinterpret_cast<volatile uint32_t*>(&p.inc_k[j]);
-                    break;
-                }
-                eb += *reinterpret_cast<volatile int64_t*>(&p.agg_b[j]);
-                ekk += *reinterpret_cast<volatile uint32_t*>(&p.agg_k[j]);
-                --j;
+                    f = ld_acquire(&T[idx].flag);
+                } while ((f & ~3u) != ep || (f & 3u) == 0);
+                st = f & 3u;
             }
-            p.inc_b[tile] = eb + tot_b;
-            p.inc_k[tile] = ekk + tot_k;
-            __threadfence();
-            st_release(&p.flags[tile], 2u);
+            const uint32_t incl = __ballot_sync(0xffffffffu, st == 2);
+            const int stop = incl ? __ffs(incl) - 1 : 31;  // nearest inclusive predecessor
+            int64_t vb = 0, vs = 0;
+            uint32_t vk = 0;
+            if (lane <= stop && idx >= 0) {
+                const volatile AlTile* tv = T + idx;
+                vb = st == 2 ? tv->inc_b : tv->agg_b;
+                vk = st == 2 ? tv->inc_k : tv->agg_k;
+                vs = st == 2 ? tv->inc_s : tv->agg_s;
+            }
+            eb += warp_sum<int64_t>(vb);
+            ekk += warp_sum<uint32_t>(vk);
+            es += warp_sum<int64_t>(vs);
+            if (incl) break;
+            j -= 32;
         }
-        s_excl_b = eb;
-        s_excl_k = ekk;
-        if (tile == p.ntiles - 1) {
-            if (p.n_kept) *p.n_kept = static_cast<uint64_t>(ekk) + tot_k;
-            if (p.total_budget) *p.total_budget = eb + tot_b;
+        if (lane == 0) {
+            if (tile != 0) {
+                T[tile].inc_b = eb + tot_b;
+                T[tile].inc_k = ekk + tot_k;
+                T[tile].inc_s = es + tot_s;
+                __threadfence();
+                st_release(&T[tile].flag, ep | 2u);
+            }
+            s_excl_b = eb;
+            s_excl_k = ekk;
+            if (tile == p.ntiles - 1) {
+                if (p.n_kept) *p.n_kept = static_cast<uint64_t>(ekk) + tot_k;
+                if (p.total_budget) *p.total_budget = eb + tot_b;
+                if (p.tokens_saved) *p.tokens_saved = es + tot_s;
+            }
         }
     }
     __syncthreads();
 
-    // --- scatter offsets and the stable kept list ---
-    int64_t ob = p.base_offset + s_excl_b + wpre_b + (ib - tb);
-    uint32_t ok = s_excl_k + wpre_k + (ik - tk);
+    // ---- global offsets and the stable kept list
 #pragma unroll
     for (int i = 0; i < AL_ITEMS; ++i) {
-        const uint64_t r = base + static_cast<uint64_t>(tid) * AL_ITEMS + i;
-        if (r < p.R) {
-            if (p.offsets) p.offsets[r] = ob;
-            ob += static_cast<int64_t>(ek[i]) * p.tpu;
-            if (ek[i] > p.detect) {
-                if (p.kept) p.kept[ok] = p.kept_base + static_cast<uint32_t>(r);
-                ++ok;
-            }
+        const uint64_t r = base + static_cast<uint64_t>(i) * AL_THREADS + tid;
+        if (r >= p.R) continue;
+        const int64_t b = static_cast<int64_t>(ek[i]) * p.tpu;
+        if (p.offsets) p.offsets[r] = p.base_offset + s_excl_b + s_wb[i * AL_WARPS + warp] + (ib[i] - b);
+        if (ek[i] > p.detect && p.kept) {
+            const uint32_t pos = s_excl_k + s_wk[i * AL_WARPS + warp] + ik[i] - 1u;
+            p.kept[pos] = p.kept_base + static_cast<uint32_t>(r);
+        }
+    }
+    // every tile has drawn its ticket before any tile finishes: the last one to finish
+    // rewinds the counters for the next call (no host-side bookkeeping, no memset launch)
+    if (tid == 0) {
+        __threadfence();
+        if (atomicAdd(&p.tickets[1], 1u) == p.ntiles - 1) {
+            p.tickets[0] = 0;
+            p.tickets[1] = 0;
+            __threadfence();
         }
     }
 }
@@ -249,26 +293,29 @@ extern "C" int cdx_allocate_scan(cdx_ctx* ctx, const uint32_t* meets_bits, uint6
         if (total_budget) cudaMemsetAsync(total_budget, 0, 8, ctx->stream);
         return CDX_OK;
     }
-    if (!meets_bits) p.meets = nullptr;
     p.ntiles = static_cast<uint32_t>((R + AL_TILE - 1) / AL_TILE);
-    // scratch: counter + flags + aggregates
-    const size_t n = p.ntiles;
-    const size_t bytes = 256 + n * 4 + n * 8 * 2 + n * 4 * 2 + 64;
-    uint8_t* s = static_cast<uint8_t*>(scratch(ctx, bytes));
-    if (!s) return set_error(ctx, CDX_ECUDA, "allocate: scratch allocation failed");
-    p.tile_counter = reinterpret_cast<uint32_t*>(s);
-    p.flags = reinterpret_cast<uint32_t*>(s + 256);
-    p.agg_b = reinterpret_cast<int64_t*>(s + 256 + ((n * 4 + 15) / 16) * 16);
-    p.inc_b = p.agg_b + n;
-    p.agg_k = reinterpret_cast<uint32_t*>(p.inc_b + n);
-    p.inc_k = p.agg_k + n;
-    cudaMemsetAsync(s, 0, 256 + n * 4, ctx->stream);
-    if (tokens_saved) cudaMemsetAsync(tokens_saved, 0, 8, ctx->stream);
-    if (pol->kind == CDX_POL_EVEN) {
-        // no meets bits needed: the chk mask is empty, point at a harmless word
-        p.meets = reinterpret_cast<const uint32_t*>(s);
-        p.words = 0;
+    // persistent look-back state: zeroed only when (re)allocated; every call uses a new
+    // epoch and a fresh range of tickets, so no per-call clearing launches are needed
+    if (ctx->al_tiles < p.ntiles || ctx->al_epoch >= (1u << 29)) {
+        cudaStreamSynchronize(ctx->stream);
+        if (ctx->al_state) cudaFree(ctx->al_state);
+        ctx->al_state = nullptr;
+        const size_t cap_tiles = std::max<size_t>(p.ntiles, 1024);
+        if (cudaMalloc(&ctx->al_state, 256 + cap_tiles * sizeof(AlTile)) != cudaSuccess) {
+            ctx->al_tiles = 0;
+            return set_error(ctx, CDX_ECUDA, "allocate: state allocation failed");
+        }
+        cudaMemsetAsync(ctx->al_state, 0, 256 + cap_tiles * sizeof(AlTile), ctx->stream);
+        ctx->al_tiles = cap_tiles;
+        ctx->al_epoch = 0;
     }
+    p.tickets = static_cast<uint32_t*>(ctx->al_state);
+    p.tiles = reinterpret_cast<AlTile*>(static_cast<uint8_t*>(ctx->al_state) + 256);
+    p.epoch = ++ctx->al_epoch;
+    p.chk_words = 0;
+    for (uint32_t w = 0; w < p.words; ++w)
+        if (p.chk[w]) p.chk_words = w + 1;
+    if (pol->kind == CDX_POL_EVEN) p.meets = nullptr;  // no test points: meets is never read
     allocate_scan_kernel<<<p.ntiles, AL_THREADS, 0, ctx->stream>>>(p);
     CDX_CHECK_LAUNCH(ctx, "allocate_scan");
     return CDX_OK;
