@@ -15,9 +15,11 @@
 // (-0.0 canonicalised to +0.0 so bitwise order equals == order).  The (arrival, id)
 // tie-break is applied first by a stable sort on bits(arrival) over the id-ordered input
 // (skipped when arrivals are already non-decreasing), then a stable sort on hi; digits on
-// which all keys agree are skipped.  One pass = upsweep histograms (all 8 digits in one
-// read), an exclusive scan, and a stable scatter whose in-tile ranks come from warp
-// match + popc (the ADU is idle in this kernel, so MATCH is the cheap ranker here).
+// which all keys agree are skipped.  Key build and compaction of live programs are one
+// single-pass kernel (gang_prepare); the sort is onesweep: one histogram read for all 8
+// digits, then one kernel per digit whose tiles rank stably (warp match + popc; the ADU is
+// idle here, so MATCH is the cheap ranker), resolve their offsets by decoupled look-back
+// and scatter.
 #include <algorithm>
 #include <cstring>
 #include <vector>
@@ -52,167 +54,122 @@ __device__ __forceinline__ uint64_t dbits(double x) {
     return static_cast<uint64_t>(__double_as_longlong(x));
 }
 
-// per program: escalation flag, live flag, hi key, arrival bits; bad times flag an error
-__global__ void gang_keys(const GangParams p, uint64_t* __restrict__ hi, uint64_t* __restrict__ arr,
-                          uint32_t* __restrict__ live, int* bad) {
-    for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < p.N;
-         i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
-        const double a = p.arrival[i], ls = p.last_service[i];
-        if (!(a >= 0.0) || !(ls >= 0.0) || isinf(a) || isinf(ls)) atomicExch(bad, 1);
-        const bool esc = (p.now - ls) >= p.limit;  // inclusive escalation
-        if (p.escalated) p.escalated[i] = esc ? 1 : 0;
-        double key;
-        if (esc || p.order == CDX_ORDER_FIFO) {
-            key = a;
-        } else {
-            const uint32_t c = p.iter_count[i];
-            const double est = c ? __ddiv_rn(static_cast<double>(p.iter_tok_sum[i]), static_cast<double>(c)) : p.prior;
-            const int rem = static_cast<int>(p.cap[i]) - static_cast<int>(p.knob[i]);
-            key = __dmul_rn(est, static_cast<double>(rem > 0 ? rem : 0));
-            if (!(key >= 0.0) || isinf(key)) atomicExch(bad, 1);
-        }
-        hi[i] = (esc ? 0ull : (1ull << 63)) | dbits(key);
-        arr[i] = dbits(a);
-        live[i] = p.terminated[i] ? 0u : 1u;
-    }
+// ---- key build + compaction of live programs, one pass ---------------------------------
+// Per program: escalated = now - last_service >= limit (inclusive);
+// est = mean completed iteration tokens or the prior; key = arrival when escalated or
+// fifo, else est * remaining knob; hi = (escalated ? 0 : 1) << 63 | bits(key).  Live
+// (non-terminated) programs are compacted in id order by a single-pass decoupled
+// look-back scan (record = flag << 30 | count), writing hi / arrival bits / id / the
+// identity permutation.  The same pass flags invalid times and whether arrivals are
+// non-decreasing (the (arrival, id) pre-sort can then be skipped).
+constexpr int GP_THREADS = 256, GP_ITEMS = 8, GP_TILE = GP_THREADS * GP_ITEMS;
+constexpr uint32_t GP_AGG = 1u << 30, GP_INC = 2u << 30, GP_CNT = (1u << 30) - 1u;
+
+__device__ __forceinline__ uint32_t ld_acq32(const uint32_t* p) {
+    uint32_t v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_rel32(uint32_t* p, uint32_t v) {
+    asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
-// ---- generic u32 exclusive scan (3 phases) --------------------------------------------
-constexpr int SCAN_T = 512;
-__global__ void scan_blocks(const uint32_t* __restrict__ in, uint32_t* __restrict__ out, uint64_t n,
-                            uint32_t* __restrict__ block_sums) {
-    __shared__ uint32_t s[SCAN_T];
-    const uint64_t i = blockIdx.x * static_cast<uint64_t>(SCAN_T) + threadIdx.x;
-    const uint32_t x = i < n ? in[i] : 0u;
-    s[threadIdx.x] = x;
+// misc: [0] live count, [1] arrivals not sorted, [2] bad time/key, [3] ticket counter
+__global__ void __launch_bounds__(GP_THREADS) gang_prepare(const GangParams p, uint64_t* __restrict__ khi,
+                                                           uint64_t* __restrict__ karr, uint32_t* __restrict__ kid,
+                                                           uint32_t* __restrict__ perm, uint32_t* __restrict__ look,
+                                                           uint32_t* __restrict__ misc, uint32_t ntiles) {
+    __shared__ uint32_t s_tile, s_excl;
+    __shared__ uint32_t s_cnt[GP_ITEMS * (GP_THREADS / 32)];
+    const uint32_t tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
+    if (tid == 0) s_tile = atomicAdd(misc + 3, 1u);
     __syncthreads();
-    for (int o = 1; o < SCAN_T; o <<= 1) {
-        const uint32_t y = threadIdx.x >= static_cast<unsigned>(o) ? s[threadIdx.x - o] : 0u;
-        __syncthreads();
-        s[threadIdx.x] += y;
-        __syncthreads();
-    }
-    if (i < n) out[i] = s[threadIdx.x] - x;
-    if (threadIdx.x == SCAN_T - 1) block_sums[blockIdx.x] = s[threadIdx.x];
-}
-__global__ void scan_sums(uint32_t* __restrict__ sums, uint64_t nb, uint32_t* __restrict__ total) {
-    __shared__ uint32_t s[1024];
-    // chunked single-CTA exclusive scan of nb block sums
-    uint32_t carry = 0;
-    for (uint64_t base = 0; base < nb; base += 1024) {
-        const uint64_t i = base + threadIdx.x;
-        const uint32_t x = i < nb ? sums[i] : 0u;
-        s[threadIdx.x] = x;
-        __syncthreads();
-        for (int o = 1; o < 1024; o <<= 1) {
-            const uint32_t y = threadIdx.x >= static_cast<unsigned>(o) ? s[threadIdx.x - o] : 0u;
-            __syncthreads();
-            s[threadIdx.x] += y;
-            __syncthreads();
-        }
-        if (i < nb) sums[i] = carry + s[threadIdx.x] - x;
-        const uint32_t tot = s[1023];
-        __syncthreads();
-        carry += tot;
-    }
-    if (threadIdx.x == 0 && total) *total = carry;
-}
-__global__ void scan_add(uint32_t* __restrict__ v, uint64_t n, const uint32_t* __restrict__ sums) {
-    const uint64_t i = blockIdx.x * static_cast<uint64_t>(SCAN_T) + threadIdx.x;
-    if (i < n) v[i] += sums[blockIdx.x];
-}
-
-// compaction of live programs: position = excl[i]
-__global__ void gang_compact(uint64_t N, const uint32_t* __restrict__ live, const uint32_t* __restrict__ pos,
-                             const uint64_t* __restrict__ hi, const uint64_t* __restrict__ arr, uint32_t id_base,
-                             uint64_t* __restrict__ khi, uint64_t* __restrict__ karr, uint32_t* __restrict__ kid) {
-    for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < N;
-         i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
-        if (!live[i]) continue;
-        const uint32_t j = pos[i];
-        khi[j] = hi[i];
-        karr[j] = arr[i];
-        kid[j] = id_base + static_cast<uint32_t>(i);
-    }
-}
-
-__global__ void count_unsorted(const uint64_t* __restrict__ k, uint64_t n, uint32_t* __restrict__ flag) {
-    for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i + 1 < n;
-         i += static_cast<uint64_t>(gridDim.x) * blockDim.x)
-        if (k[i] > k[i + 1]) atomicExch(flag, 1u);
-}
-
-// ---- LSD radix sort of (u64 key, u32 value) --------------------------------------------
-// all 8 digit histograms of one tile: hist[(d*256 + digit) * ntiles + tile]
-__global__ void __launch_bounds__(RS_THREADS) rs_upsweep(const uint64_t* __restrict__ keys, uint64_t n,
-                                                         uint32_t ntiles, uint32_t* __restrict__ hist) {
-    __shared__ uint32_t h[8][256];
-    for (int i = threadIdx.x; i < 8 * 256; i += RS_THREADS) (&h[0][0])[i] = 0;
-    __syncthreads();
-    const uint64_t base = static_cast<uint64_t>(blockIdx.x) * RS_TILE;
-    for (int j = 0; j < RS_ITEMS; ++j) {
-        const uint64_t i = base + j * RS_THREADS + threadIdx.x;
-        if (i < n) {
-            const uint64_t k = keys[i];
+    const uint32_t tile = s_tile;
+    const uint64_t base = static_cast<uint64_t>(tile) * GP_TILE;
+    uint64_t hk[GP_ITEMS], ak[GP_ITEMS];
+    uint32_t rank[GP_ITEMS];
+    bool lv[GP_ITEMS];
+    bool bad = false, unsorted = false;
 #pragma unroll
-            for (int d = 0; d < 8; ++d) atomicAdd(&h[d][(k >> (8 * d)) & 0xff], 1u);
+    for (int j = 0; j < GP_ITEMS; ++j) {
+        const uint64_t i = base + static_cast<uint64_t>(j) * GP_THREADS + tid;  // striped: coalesced
+        bool live = false;
+        if (i < p.N) {
+            const double a = p.arrival[i], ls = p.last_service[i];
+            bad = bad || !(a >= 0.0) || !(ls >= 0.0) || isinf(a) || isinf(ls);
+            if (i + 1 < p.N) unsorted = unsorted || a > __ldg(p.arrival + i + 1);
+            const bool esc = (p.now - ls) >= p.limit;  // inclusive escalation
+            if (p.escalated) p.escalated[i] = esc ? 1 : 0;
+            double key;
+            if (esc || p.order == CDX_ORDER_FIFO) {
+                key = a;
+            } else {
+                const uint32_t c = p.iter_count[i];
+                const double est =
+                    c ? __ddiv_rn(static_cast<double>(p.iter_tok_sum[i]), static_cast<double>(c)) : p.prior;
+                const int rem = static_cast<int>(p.cap[i]) - static_cast<int>(p.knob[i]);
+                key = __dmul_rn(est, static_cast<double>(rem > 0 ? rem : 0));
+                bad = bad || !(key >= 0.0) || isinf(key);
+            }
+            hk[j] = (esc ? 0ull : (1ull << 63)) | dbits(key);
+            ak[j] = dbits(a);
+            live = p.terminated[i] == 0;
         }
+        lv[j] = live;
+        const uint32_t m = __ballot_sync(0xffffffffu, live);
+        rank[j] = __popc(m & ((1u << lane) - 1u));
+        if (lane == 0) s_cnt[j * (GP_THREADS / 32) + warp] = __popc(m);
     }
+    if (__any_sync(0xffffffffu, bad) && lane == 0) atomicExch(misc + 2, 1u);
+    if (__any_sync(0xffffffffu, unsorted) && lane == 0) atomicExch(misc + 1, 1u);
     __syncthreads();
-    for (int i = threadIdx.x; i < 8 * 256; i += RS_THREADS) hist[static_cast<uint64_t>(i) * ntiles + blockIdx.x] = (&h[0][0])[i];
-}
-
-// stable scatter of one digit: warp w of a tile owns keys [base + w*32*ITEMS, +32*ITEMS),
-// processed in order 32 at a time; peers with the same digit are ranked by match + popc
-__global__ void __launch_bounds__(RS_THREADS) rs_scatter(const uint64_t* __restrict__ kin,
-                                                         const uint32_t* __restrict__ vin, uint64_t* __restrict__ kout,
-                                                         uint32_t* __restrict__ vout, uint64_t n, uint32_t ntiles,
-                                                         const uint32_t* __restrict__ offs, int shift) {
-    __shared__ uint32_t wcnt[RS_WARPS][256];
-    const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    for (int i = threadIdx.x; i < RS_WARPS * 256; i += RS_THREADS) (&wcnt[0][0])[i] = 0;
-    __syncthreads();
-    const uint64_t base = static_cast<uint64_t>(blockIdx.x) * RS_TILE + static_cast<uint64_t>(warp) * 32 * RS_ITEMS;
-    uint64_t k[RS_ITEMS];
-    uint32_t v[RS_ITEMS], rank[RS_ITEMS], dig[RS_ITEMS];
-    const uint32_t lt = (1u << lane) - 1u;
+    if (warp == 0) {  // exclusive prefix over the 64 (item, warp) counts, then look-back
+        const uint32_t a0 = s_cnt[2 * lane], a1 = s_cnt[2 * lane + 1];
+        uint32_t inc = a0 + a1;
 #pragma unroll
-    for (int j = 0; j < RS_ITEMS; ++j) {
-        const uint64_t i = base + j * 32 + lane;
-        const bool ok = i < n;
-        k[j] = ok ? kin[i] : 0;
-        v[j] = ok ? vin[i] : 0;
-        const uint32_t d = ok ? static_cast<uint32_t>((k[j] >> shift) & 0xff) : 256u + lane;  // unique dummy
-        dig[j] = d;
-        const uint32_t peers = __match_any_sync(0xffffffffu, d);
-        uint32_t before = 0;
-        if (ok) before = wcnt[warp][d];
-        __syncwarp();
-        rank[j] = before + __popc(peers & lt);
-        if (ok && (peers & lt) == 0) wcnt[warp][d] = before + __popc(peers);
-        __syncwarp();
-    }
-    __syncthreads();
-    // exclusive prefix of each digit's count over the warps of this tile
-    for (int d = threadIdx.x; d < 256; d += RS_THREADS) {
-        uint32_t acc = 0;
-        for (int w = 0; w < RS_WARPS; ++w) {
-            const uint32_t c = wcnt[w][d];
-            wcnt[w][d] = acc;
-            acc += c;
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
+            if (lane >= static_cast<uint32_t>(o)) inc += y;
+        }
+        const uint32_t tot = __shfl_sync(0xffffffffu, inc, 31);
+        s_cnt[2 * lane] = inc - a0 - a1;
+        s_cnt[2 * lane + 1] = inc - a1;
+        if (lane == 0) st_rel32(look + tile, (tile == 0 ? GP_INC : GP_AGG) | tot);
+        uint32_t excl = 0;
+        int64_t jt = static_cast<int64_t>(tile) - 1;
+        while (jt >= 0) {  // 32 predecessors per step
+            const int64_t idx = jt - lane;
+            uint32_t f = GP_INC;  // before tile 0: an inclusive zero
+            if (idx >= 0) {
+                do {
+                    f = ld_acq32(look + idx);
+                } while ((f & ~GP_CNT) == 0);
+            }
+            const uint32_t incl = __ballot_sync(0xffffffffu, (f & GP_INC) != 0);
+            const int stop = incl ? __ffs(incl) - 1 : 31;
+            uint32_t v = (static_cast<int>(lane) <= stop) ? (f & GP_CNT) : 0u;
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+            excl += v;
+            if (incl) break;
+            jt -= 32;
+        }
+        if (lane == 0) {
+            if (tile != 0) st_rel32(look + tile, GP_INC | (excl + tot));
+            s_excl = excl;
+            if (tile == ntiles - 1) misc[0] = excl + tot;
         }
     }
     __syncthreads();
 #pragma unroll
-    for (int j = 0; j < RS_ITEMS; ++j) {
-        const uint64_t i = base + j * 32 + lane;
-        if (i < n) {
-            const uint32_t d = dig[j];
-            const uint64_t pos = static_cast<uint64_t>(offs[static_cast<uint64_t>(d) * ntiles + blockIdx.x]) +
-                                 wcnt[warp][d] + rank[j];
-            kout[pos] = k[j];
-            vout[pos] = v[j];
-        }
+    for (int j = 0; j < GP_ITEMS; ++j) {
+        if (!lv[j]) continue;
+        const uint64_t i = base + static_cast<uint64_t>(j) * GP_THREADS + tid;
+        const uint32_t pos = s_excl + s_cnt[j * (GP_THREADS / 32) + warp] + rank[j];
+        khi[pos] = hk[j];
+        karr[pos] = ak[j];
+        kid[pos] = p.id_base + static_cast<uint32_t>(i);
+        perm[pos] = pos;
     }
 }
 
@@ -229,10 +186,131 @@ __global__ void pack_keys(const uint64_t* __restrict__ shi, const uint64_t* __re
     }
 }
 
-__global__ void iota_u32(uint32_t* __restrict__ v, uint64_t n) {
-    for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n;
-         i += static_cast<uint64_t>(gridDim.x) * blockDim.x)
-        v[i] = static_cast<uint32_t>(i);
+
+// ---- Onesweep LSD radix sort of (u64 key, u32 value) -------------------------------------
+// One histogram kernel reads the keys once and counts all 8 digits (global digit counts do
+// not depend on the order), then ONE kernel per non-trivial digit: each tile ranks its keys
+// stably (warp match + popc, warps in tile order), publishes its per-digit counts and
+// resolves its exclusive per-digit offsets by decoupled look-back over earlier tiles
+// (flag and count packed in one 32-bit word), then scatters.  Tiles take tickets in
+// launch order, so look-back only ever waits on running or finished tiles.
+constexpr uint32_t LB_AGG = 1u << 30, LB_INC = 2u << 30, LB_CNT = (1u << 30) - 1u;
+
+__device__ __forceinline__ uint32_t ld_acq_u32(const uint32_t* p) {
+    uint32_t v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_rel_u32(uint32_t* p, uint32_t v) {
+    asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+__global__ void __launch_bounds__(RS_THREADS) os_histogram(const uint64_t* __restrict__ keys, uint64_t n,
+                                                           uint32_t* __restrict__ ghist) {
+    __shared__ uint32_t h[8][256];
+    for (int i = threadIdx.x; i < 8 * 256; i += RS_THREADS) (&h[0][0])[i] = 0;
+    __syncthreads();
+    for (uint64_t i = blockIdx.x * static_cast<uint64_t>(RS_THREADS) + threadIdx.x; i < n;
+         i += static_cast<uint64_t>(gridDim.x) * RS_THREADS) {
+        const uint64_t k = keys[i];
+#pragma unroll
+        for (int d = 0; d < 8; ++d) atomicAdd(&h[d][(k >> (8 * d)) & 0xff], 1u);
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < 8 * 256; i += RS_THREADS) {
+        const uint32_t c = (&h[0][0])[i];
+        if (c) atomicAdd(ghist + i, c);
+    }
+}
+
+__global__ void __launch_bounds__(RS_THREADS) os_pass(const uint64_t* __restrict__ kin,
+                                                      const uint32_t* __restrict__ vin, uint64_t* __restrict__ kout,
+                                                      uint32_t* __restrict__ vout, uint64_t n, int shift,
+                                                      const uint32_t* __restrict__ ghist, uint32_t* __restrict__ look,
+                                                      uint32_t* __restrict__ counter) {
+    __shared__ uint32_t s_tile;
+    __shared__ uint32_t wcnt[RS_WARPS][256];
+    __shared__ uint32_t s_base[256];
+    __shared__ uint32_t s_wsum[RS_WARPS];
+    const uint32_t tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
+    if (tid == 0) s_tile = atomicAdd(counter, 1u);
+    for (int i = tid; i < RS_WARPS * 256; i += RS_THREADS) (&wcnt[0][0])[i] = 0;
+    // global exclusive base of this thread's digit: block scan of the 256 digit counts
+    const uint32_t g = ghist[tid];
+    uint32_t incl = g;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= static_cast<uint32_t>(o)) incl += y;
+    }
+    if (lane == 31) s_wsum[warp] = incl;
+    __syncthreads();
+    uint32_t wpre = 0;
+    for (uint32_t w = 0; w < warp; ++w) wpre += s_wsum[w];
+    s_base[tid] = wpre + incl - g;
+    const uint32_t tile = s_tile;
+    const uint64_t base = static_cast<uint64_t>(tile) * RS_TILE + static_cast<uint64_t>(warp) * 32 * RS_ITEMS;
+    uint64_t k[RS_ITEMS];
+    uint32_t v[RS_ITEMS], rank[RS_ITEMS], dig[RS_ITEMS];
+    const uint32_t lt = (1u << lane) - 1u;
+#pragma unroll
+    for (int j = 0; j < RS_ITEMS; ++j) {
+        const uint64_t i = base + j * 32 + lane;
+        const bool ok = i < n;
+        k[j] = ok ? kin[i] : 0;
+        v[j] = ok ? vin[i] : 0;
+    }
+#pragma unroll
+    for (int j = 0; j < RS_ITEMS; ++j) {
+        const bool ok = base + j * 32 + lane < n;
+        const uint32_t d = ok ? static_cast<uint32_t>((k[j] >> shift) & 0xff) : 256u + lane;  // unique dummy
+        dig[j] = d;
+        const uint32_t peers = __match_any_sync(0xffffffffu, d);
+        uint32_t before = 0;
+        if (ok) before = wcnt[warp][d];
+        __syncwarp();
+        rank[j] = before + __popc(peers & lt);
+        if (ok && (peers & lt) == 0) wcnt[warp][d] = before + __popc(peers);
+        __syncwarp();
+    }
+    __syncthreads();
+    // thread d: this tile's count of digit d, the warps' exclusive prefixes, look-back
+    {
+        const uint32_t d = tid;
+        uint32_t c = 0;
+        for (int w = 0; w < RS_WARPS; ++w) {
+            const uint32_t x = wcnt[w][d];
+            wcnt[w][d] = c;
+            c += x;
+        }
+        uint32_t excl = 0;
+        if (tile == 0) {
+            st_rel_u32(look + d, LB_INC | c);
+        } else {
+            st_rel_u32(look + static_cast<uint64_t>(tile) * 256 + d, LB_AGG | c);
+            for (int64_t j = static_cast<int64_t>(tile) - 1; j >= 0; --j) {
+                uint32_t f;
+                do {
+                    f = ld_acq_u32(look + static_cast<uint64_t>(j) * 256 + d);
+                } while ((f & ~LB_CNT) == 0);
+                excl += f & LB_CNT;
+                if (f & LB_INC) break;
+            }
+            st_rel_u32(look + static_cast<uint64_t>(tile) * 256 + d, LB_INC | (excl + c));
+        }
+        s_base[d] += excl;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < RS_ITEMS; ++j) {
+        const uint64_t i = base + j * 32 + lane;
+        if (i < n) {
+            const uint32_t d = dig[j];
+            const uint64_t pos = static_cast<uint64_t>(s_base[d]) + wcnt[warp][d] + rank[j];
+            kout[pos] = k[j];
+            vout[pos] = v[j];
+        }
+    }
 }
 
 template <typename T>
@@ -249,55 +327,43 @@ struct Launch {
     }
 };
 
-// exclusive scan of n u32 in place (out may alias in); returns total via device scalar
-int scan_u32(cdx_ctx* ctx, const uint32_t* in, uint32_t* out, uint64_t n, uint32_t* sums, uint32_t* total) {
-    const uint64_t nb = (n + SCAN_T - 1) / SCAN_T;
-    scan_blocks<<<static_cast<unsigned>(nb), SCAN_T, 0, ctx->stream>>>(in, out, n, sums);
-    CDX_CHECK_LAUNCH(ctx, "scan(blocks)");
-    scan_sums<<<1, 1024, 0, ctx->stream>>>(sums, nb, total);
-    CDX_CHECK_LAUNCH(ctx, "scan(sums)");
-    scan_add<<<static_cast<unsigned>(nb), SCAN_T, 0, ctx->stream>>>(out, n, sums);
-    CDX_CHECK_LAUNCH(ctx, "scan(add)");
-    return CDX_OK;
-}
-
-// Stable LSD radix sort of (keys, vals) over 8-bit digits; digits where every key agrees
-// are skipped (decided on the host from the upsweep histograms).  Returns which buffer
-// holds the result (0: k0/v0, 1: k1/v1).
-int radix_sort(cdx_ctx* ctx, uint64_t* k0, uint32_t* v0, uint64_t* k1, uint32_t* v1, uint64_t n, uint32_t* hist,
-               uint32_t* sums, int* which) {
+// Stable LSD radix sort of (keys, vals) over 8-bit digits (onesweep).  `lb` is scratch of
+// 8*256 + 16 + 8*ntiles*256 u32 (global digit counts, pass tickets, look-back records),
+// cleared by one memset per sort; digits where every key agrees are skipped (decided on
+// the host from the global counts: one 8 KB copy).  Returns which buffer holds the result
+// (0: k0/v0, 1: k1/v1).
+int radix_sort(cdx_ctx* ctx, uint64_t* k0, uint32_t* v0, uint64_t* k1, uint32_t* v1, uint64_t n, uint32_t* lb,
+               int* which) {
     *which = 0;
     if (n <= 1) return CDX_OK;
     const uint32_t ntiles = static_cast<uint32_t>((n + RS_TILE - 1) / RS_TILE);
-    rs_upsweep<<<ntiles, RS_THREADS, 0, ctx->stream>>>(k0, n, ntiles, hist);
-    CDX_CHECK_LAUNCH(ctx, "radix(upsweep)");
-    // per-digit totals to decide which passes are needed
-    std::vector<uint32_t> h(static_cast<size_t>(8) * 256 * ntiles);
-    cudaError_t e = cudaMemcpyAsync(h.data(), hist, h.size() * 4, cudaMemcpyDeviceToHost, ctx->stream);
+    uint32_t* ghist = lb;
+    uint32_t* tickets = lb + 8 * 256;
+    uint32_t* look = tickets + 16;
+    cudaError_t e = cudaMemsetAsync(lb, 0, (8 * 256 + 16 + static_cast<size_t>(8) * ntiles * 256) * 4, ctx->stream);
+    if (e != cudaSuccess) return cuda_fail(ctx, e, "radix(clear)");
+    const unsigned hgrid = static_cast<unsigned>(std::min<uint64_t>(ntiles, static_cast<uint64_t>(ctx->sm_count) * 4));
+    os_histogram<<<hgrid, RS_THREADS, 0, ctx->stream>>>(k0, n, ghist);
+    CDX_CHECK_LAUNCH(ctx, "radix(histogram)");
+    uint32_t h[8 * 256];
+    e = cudaMemcpyAsync(h, ghist, sizeof(h), cudaMemcpyDeviceToHost, ctx->stream);
     if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
-    if (e != cudaSuccess) return cuda_fail(ctx, e, "radix(histograms)");
+    if (e != cudaSuccess) return cuda_fail(ctx, e, "radix(histogram)");
     uint64_t* kin = k0;
     uint32_t* vin = v0;
     uint64_t* kout = k1;
     uint32_t* vout = v1;
     for (int d = 0; d < 8; ++d) {
         bool trivial = false;
-        for (int b = 0; b < 256 && !trivial; ++b) {
-            uint64_t tot = 0;
-            const uint32_t* row = h.data() + (static_cast<size_t>(d) * 256 + b) * ntiles;
-            for (uint32_t t = 0; t < ntiles; ++t) tot += row[t];
-            if (tot == n) trivial = true;
-            if (tot) break;  // first non-empty bucket decides
-        }
+        for (int b = 0; b < 256; ++b)
+            if (h[d * 256 + b]) {
+                trivial = h[d * 256 + b] == n;
+                break;
+            }
         if (trivial) continue;
-        uint32_t* dh = hist + static_cast<size_t>(d) * 256 * ntiles;
-        // NOTE: digit histograms were taken on the ORIGINAL order; per-tile counts must
-        // match the current order, so recompute this digit's histogram on kin.
-        rs_upsweep<<<ntiles, RS_THREADS, 0, ctx->stream>>>(kin, n, ntiles, hist);
-        CDX_CHECK_LAUNCH(ctx, "radix(upsweep)");
-        if (int st = scan_u32(ctx, dh, dh, static_cast<uint64_t>(256) * ntiles, sums, nullptr)) return st;
-        rs_scatter<<<ntiles, RS_THREADS, 0, ctx->stream>>>(kin, vin, kout, vout, n, ntiles, dh, 8 * d);
-        CDX_CHECK_LAUNCH(ctx, "radix(scatter)");
+        os_pass<<<ntiles, RS_THREADS, 0, ctx->stream>>>(kin, vin, kout, vout, n, 8 * d, ghist + d * 256,
+                                                        look + static_cast<size_t>(d) * ntiles * 256, tickets + d);
+        CDX_CHECK_LAUNCH(ctx, "radix(pass)");
         std::swap(kin, kout);
         std::swap(vin, vout);
     }
@@ -370,34 +436,27 @@ extern "C" int cdx_gang_priority(cdx_ctx* ctx, const cdx_prog_soa* progs, uint64
                  progs->cap, progs->terminated, escalated, N, progs->id_base, pol->order, now,
                  pol->starvation_limit, pol->prior_tokens};
     const uint32_t ntiles = static_cast<uint32_t>((N + RS_TILE - 1) / RS_TILE);
-    const uint64_t nb = (N + SCAN_T - 1) / SCAN_T + 1;
-    const uint64_t nh = static_cast<uint64_t>(8) * 256 * ntiles;
-    // scratch layout
-    const size_t bytes = N * 8 * 6 + N * 4 * 6 + nh * 4 + (nb + std::max<uint64_t>(nh / SCAN_T + 2, 1)) * 4 + 256;
+    const uint32_t gtiles = static_cast<uint32_t>((N + GP_TILE - 1) / GP_TILE);
+    const uint64_t nh = static_cast<uint64_t>(8) * 256 * ntiles + 8 * 256 + 16;  // radix look-back scratch
+    // scratch: khi karr t0 t1 (u64) | kid va vb perm (u32) | misc | prepare look-back | radix
+    const size_t bytes = N * 8 * 4 + N * 4 * 4 + 64 + (gtiles + 16) * 4 + nh * 4 + 256;
     uint8_t* s = static_cast<uint8_t*>(scratch(ctx, bytes));
     if (!s) return set_error(ctx, CDX_ECUDA, "gang_priority: scratch allocation failed");
-    uint64_t* hi = reinterpret_cast<uint64_t*>(s);
-    uint64_t* arr = hi + N;
-    uint64_t* khi = arr + N;
+    uint64_t* khi = reinterpret_cast<uint64_t*>(s);
     uint64_t* karr = khi + N;
     uint64_t* t0 = karr + N;
     uint64_t* t1 = t0 + N;
-    uint32_t* live = reinterpret_cast<uint32_t*>(t1 + N);
-    uint32_t* pos = live + N;
-    uint32_t* kid = pos + N;
+    uint32_t* kid = reinterpret_cast<uint32_t*>(t1 + N);
     uint32_t* va = kid + N;
     uint32_t* vb = va + N;
     uint32_t* perm = vb + N;
-    uint32_t* hist = perm + N;
-    uint32_t* sums = hist + nh;
-    uint32_t* misc = sums + std::max<uint64_t>(nb, nh / SCAN_T + 2);  // [0] total, [1] unsorted flag, [2] bad
-    cudaMemsetAsync(misc, 0, 16, ctx->stream);
+    uint32_t* misc = perm + N;  // 16 words
+    uint32_t* plook = misc + 16;
+    uint32_t* hist = plook + gtiles + 16;
+    cudaMemsetAsync(misc, 0, (16 + gtiles) * 4, ctx->stream);
     Launch L{ctx};
-    gang_keys<<<L.grid(N), 256, 0, ctx->stream>>>(p, hi, arr, live, reinterpret_cast<int*>(misc + 2));
-    CDX_CHECK_LAUNCH(ctx, "gang_priority(keys)");
-    if (int st = scan_u32(ctx, live, pos, N, sums, misc)) return st;
-    gang_compact<<<L.grid(N), 256, 0, ctx->stream>>>(N, live, pos, hi, arr, progs->id_base, khi, karr, kid);
-    CDX_CHECK_LAUNCH(ctx, "gang_priority(compact)");
+    gang_prepare<<<gtiles, GP_THREADS, 0, ctx->stream>>>(p, khi, karr, kid, va, plook, misc, gtiles);
+    CDX_CHECK_LAUNCH(ctx, "gang_priority(prepare)");
     uint32_t hm[3];
     cudaError_t e = cudaMemcpyAsync(hm, misc, 12, cudaMemcpyDeviceToHost, ctx->stream);
     if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
@@ -406,35 +465,32 @@ extern "C" int cdx_gang_priority(cdx_ctx* ctx, const cdx_prog_soa* progs, uint64
     const uint64_t n = hm[0];
     *n_out = n;
     if (n == 0) return CDX_OK;
-    // 1) (arrival, id): programs are in id order; a stable sort on arrival bits yields the
-    //    tie-break order.  Skip it when arrivals are already non-decreasing.
-    count_unsorted<<<L.grid(n), 256, 0, ctx->stream>>>(karr, n, misc + 1);
-    CDX_CHECK_LAUNCH(ctx, "gang_priority(sorted?)");
-    e = cudaMemcpyAsync(hm, misc, 8, cudaMemcpyDeviceToHost, ctx->stream);
-    if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
-    if (e != cudaSuccess) return cuda_fail(ctx, e, "gang_priority");
-    iota_u32<<<L.grid(n), 256, 0, ctx->stream>>>(va, n);
-    CDX_CHECK_LAUNCH(ctx, "gang_priority(iota)");
-    uint32_t* p1 = va;  // permutation: position -> compacted index
+    // 1) (arrival, id): programs are compacted in id order, so a stable sort on arrival
+    //    bits yields the tie-break order; skipped when arrivals are non-decreasing.
+    uint32_t* p1 = va;  // permutation: position -> compacted index (identity from prepare)
     if (hm[1]) {
         cudaMemcpyAsync(t0, karr, n * 8, cudaMemcpyDeviceToDevice, ctx->stream);
         int which = 0;
-        if (int st = radix_sort(ctx, t0, va, t1, vb, n, hist, sums, &which)) return st;
+        if (int st = radix_sort(ctx, t0, va, t1, vb, n, hist, &which)) return st;
         p1 = which ? vb : va;
     }
     // 2) stable sort on hi over the (arrival, id) order
-    gather<uint64_t><<<L.grid(n), 256, 0, ctx->stream>>>(khi, p1, t0, n);
-    CDX_CHECK_LAUNCH(ctx, "gang_priority(gather)");
-    uint32_t* pa = p1 == va ? vb : va;  // free buffer pair for the second sort's values
-    cudaMemcpyAsync(pa, p1, n * 4, cudaMemcpyDeviceToDevice, ctx->stream);
+    uint64_t* hin = khi;  // already in (arrival, id) order when the pre-sort was skipped
+    uint32_t* pa = p1;
     uint32_t* pb = perm;
+    if (hm[1]) {
+        gather<uint64_t><<<L.grid(n), 256, 0, ctx->stream>>>(khi, p1, t0, n);
+        CDX_CHECK_LAUNCH(ctx, "gang_priority(gather)");
+        hin = t0;
+    }
     int which = 0;
-    if (int st = radix_sort(ctx, t0, pa, t1, pb, n, hist, sums, &which)) return st;
+    uint64_t* hout = hin == t0 ? t1 : t0;
+    if (int st = radix_sort(ctx, hin, pa, hout, pb, n, hist, &which)) return st;
     uint32_t* fin = which ? pb : pa;  // position -> compacted index
     gather<uint32_t><<<L.grid(n), 256, 0, ctx->stream>>>(kid, fin, order, n);
     CDX_CHECK_LAUNCH(ctx, "gang_priority(order)");
     if (keys) {
-        pack_keys<<<L.grid(n), 256, 0, ctx->stream>>>(which ? t1 : t0, karr, kid, fin, keys, n);
+        pack_keys<<<L.grid(n), 256, 0, ctx->stream>>>(which ? hout : hin, karr, kid, fin, keys, n);
         CDX_CHECK_LAUNCH(ctx, "gang_priority(keys)");
     }
     return CDX_OK;

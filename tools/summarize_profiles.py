@@ -24,8 +24,8 @@ OUT = os.path.join(ROOT, "gpurun_out")
 PROF = os.path.join(ROOT, "profiles")
 
 
-def launches(tag):
-    for path in sorted(glob.glob(os.path.join(OUT, "r1_launches_*.csv"))):
+def launches(tag, prefix="r1_launches_"):
+    for path in sorted(glob.glob(os.path.join(OUT, prefix + "*.csv"))):
         cfg = path.rsplit("_", 1)[1].split(".")[0]
         rows = list(csv.reader(l for l in open(path) if l.startswith('"')))
         hdr = rows[0]
@@ -123,7 +123,8 @@ if __name__ == "__main__":
             print("\n".join(brief(path)[0] or [path + ": no data"]) + "\n")
         sys.exit(0)
     tag = sys.argv[1] if len(sys.argv) > 1 else "r1"
+    src = sys.argv[2] if len(sys.argv) > 2 else "r1"  # gpurun_out/<src>_launches_*.csv, <src>_full_*.ncu-rep
     os.makedirs(PROF, exist_ok=True)
-    launches(tag)
-    full(tag)
+    launches(tag, src + "_launches_")
+    full(tag, src + "_full_")
     print("\n".join(sorted(os.listdir(PROF))))
