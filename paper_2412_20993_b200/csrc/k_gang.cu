@@ -58,33 +58,80 @@ __device__ __forceinline__ uint64_t dbits(double x) {
 // Per program: escalated = now - last_service >= limit (inclusive);
 // est = mean completed iteration tokens or the prior; key = arrival when escalated or
 // fifo, else est * remaining knob; hi = (escalated ? 0 : 1) << 63 | bits(key).  Live
-// (non-terminated) programs are compacted in id order by a single-pass decoupled
-// look-back scan (record = flag << 30 | count), writing hi / arrival bits / id / the
-// identity permutation.  The same pass flags invalid times and whether arrivals are
+// (non-terminated) programs are compacted in id order (reduce-then-scan: per-tile live
+// counts from the terminated bytes, one-CTA scan, then this pass), writing hi / arrival
+// bits / id / the identity permutation.  The same pass flags invalid times and whether arrivals are
 // non-decreasing (the (arrival, id) pre-sort can then be skipped).
-constexpr int GP_THREADS = 256, GP_ITEMS = 8, GP_TILE = GP_THREADS * GP_ITEMS;
-constexpr uint32_t GP_AGG = 1u << 30, GP_INC = 2u << 30, GP_CNT = (1u << 30) - 1u;
-
-__device__ __forceinline__ uint32_t ld_acq32(const uint32_t* p) {
-    uint32_t v;
-    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-    return v;
+constexpr int GP_THREADS = 256, GP_ITEMS = 4, GP_TILE = GP_THREADS * GP_ITEMS;
+// live programs per tile (reads only the terminated bytes)
+__global__ void __launch_bounds__(GP_THREADS) gang_count(const uint8_t* __restrict__ term, uint64_t N,
+                                                         uint32_t* __restrict__ tile_cnt) {
+    __shared__ uint32_t s[GP_THREADS / 32];
+    const uint64_t base = static_cast<uint64_t>(blockIdx.x) * GP_TILE;
+    uint32_t c = 0;
+#pragma unroll
+    for (int j = 0; j < GP_ITEMS; ++j) {
+        const uint64_t i = base + static_cast<uint64_t>(j) * GP_THREADS + threadIdx.x;
+        c += (i < N && term[i] == 0) ? 1u : 0u;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+    if ((threadIdx.x & 31) == 0) s[threadIdx.x >> 5] = c;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        uint32_t t = 0;
+        for (int w = 0; w < GP_THREADS / 32; ++w) t += s[w];
+        tile_cnt[blockIdx.x] = t;
+    }
 }
-__device__ __forceinline__ void st_rel32(uint32_t* p, uint32_t v) {
-    asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+
+// exclusive scan of the tile counts in place (one CTA), total -> misc[0]
+__global__ void __launch_bounds__(1024) gang_scan_tiles(uint32_t* __restrict__ v, uint32_t n, uint32_t* misc) {
+    __shared__ uint32_t ws[32];
+    __shared__ uint32_t carry;
+    if (threadIdx.x == 0) carry = 0;
+    __syncthreads();
+    const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    for (uint32_t b = 0; b < n; b += 1024) {
+        const uint32_t i = b + threadIdx.x;
+        const uint32_t x = i < n ? v[i] : 0u;
+        uint32_t inc = x;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
+            if (lane >= static_cast<uint32_t>(o)) inc += y;
+        }
+        if (lane == 31) ws[warp] = inc;
+        __syncthreads();
+        if (warp == 0) {
+            uint32_t w = ws[lane];
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t y = __shfl_up_sync(0xffffffffu, w, o);
+                if (lane >= static_cast<uint32_t>(o)) w += y;
+            }
+            ws[lane] = w;  // inclusive over warps
+        }
+        __syncthreads();
+        const uint32_t before = carry + (warp ? ws[warp - 1] : 0u);
+        if (i < n) v[i] = before + inc - x;
+        __syncthreads();
+        if (threadIdx.x == 0) carry += ws[31];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) misc[0] = carry;
 }
 
-// misc: [0] live count, [1] arrivals not sorted, [2] bad time/key, [3] ticket counter
+// misc: [0] live count (from gang_scan_tiles), [1] arrivals not sorted, [2] bad time/key
 __global__ void __launch_bounds__(GP_THREADS) gang_prepare(const GangParams p, uint64_t* __restrict__ khi,
                                                            uint64_t* __restrict__ karr, uint32_t* __restrict__ kid,
-                                                           uint32_t* __restrict__ perm, uint32_t* __restrict__ look,
-                                                           uint32_t* __restrict__ misc, uint32_t ntiles) {
-    __shared__ uint32_t s_tile, s_excl;
+                                                           uint32_t* __restrict__ perm,
+                                                           const uint32_t* __restrict__ tile_excl,
+                                                           uint32_t* __restrict__ misc) {
+    __shared__ uint32_t s_excl;
     __shared__ uint32_t s_cnt[GP_ITEMS * (GP_THREADS / 32)];
     const uint32_t tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
-    if (tid == 0) s_tile = atomicAdd(misc + 3, 1u);
-    __syncthreads();
-    const uint32_t tile = s_tile;
+    const uint32_t tile = blockIdx.x;
     const uint64_t base = static_cast<uint64_t>(tile) * GP_TILE;
     uint64_t hk[GP_ITEMS], ak[GP_ITEMS];
     uint32_t rank[GP_ITEMS];
@@ -95,70 +142,53 @@ __global__ void __launch_bounds__(GP_THREADS) gang_prepare(const GangParams p, u
         const uint64_t i = base + static_cast<uint64_t>(j) * GP_THREADS + tid;  // striped: coalesced
         bool live = false;
         if (i < p.N) {
-            const double a = p.arrival[i], ls = p.last_service[i];
+            // every field is loaded up front (one memory round trip per item, not two)
+            const double a = __ldg(p.arrival + i), ls = __ldg(p.last_service + i);
+            const double an = i + 1 < p.N ? __ldg(p.arrival + i + 1) : a;
+            const int64_t sum = __ldg(p.iter_tok_sum + i);
+            const uint32_t c = __ldg(p.iter_count + i);
+            const int rem = static_cast<int>(__ldg(p.cap + i)) - static_cast<int>(__ldg(p.knob + i));
+            live = __ldg(p.terminated + i) == 0;
             bad = bad || !(a >= 0.0) || !(ls >= 0.0) || isinf(a) || isinf(ls);
-            if (i + 1 < p.N) unsorted = unsorted || a > __ldg(p.arrival + i + 1);
+            unsorted = unsorted || a > an;
             const bool esc = (p.now - ls) >= p.limit;  // inclusive escalation
             if (p.escalated) p.escalated[i] = esc ? 1 : 0;
             double key;
             if (esc || p.order == CDX_ORDER_FIFO) {
                 key = a;
             } else {
-                const uint32_t c = p.iter_count[i];
-                const double est =
-                    c ? __ddiv_rn(static_cast<double>(p.iter_tok_sum[i]), static_cast<double>(c)) : p.prior;
-                const int rem = static_cast<int>(p.cap[i]) - static_cast<int>(p.knob[i]);
+                const double est = c ? __ddiv_rn(static_cast<double>(sum), static_cast<double>(c)) : p.prior;
                 key = __dmul_rn(est, static_cast<double>(rem > 0 ? rem : 0));
                 bad = bad || !(key >= 0.0) || isinf(key);
             }
             hk[j] = (esc ? 0ull : (1ull << 63)) | dbits(key);
             ak[j] = dbits(a);
-            live = p.terminated[i] == 0;
         }
         lv[j] = live;
-        const uint32_t m = __ballot_sync(0xffffffffu, live);
+    }
+    // ranks after all loads are issued (no warp vote between the items' loads)
+#pragma unroll
+    for (int j = 0; j < GP_ITEMS; ++j) {
+        const uint32_t m = __ballot_sync(0xffffffffu, lv[j]);
         rank[j] = __popc(m & ((1u << lane) - 1u));
         if (lane == 0) s_cnt[j * (GP_THREADS / 32) + warp] = __popc(m);
     }
     if (__any_sync(0xffffffffu, bad) && lane == 0) atomicExch(misc + 2, 1u);
     if (__any_sync(0xffffffffu, unsorted) && lane == 0) atomicExch(misc + 1, 1u);
     __syncthreads();
-    if (warp == 0) {  // exclusive prefix over the 64 (item, warp) counts, then look-back
-        const uint32_t a0 = s_cnt[2 * lane], a1 = s_cnt[2 * lane + 1];
+    if (warp == 0) {  // exclusive prefix over the (item, warp) counts of this tile
+        static_assert(GP_ITEMS * (GP_THREADS / 32) <= 64, "two counts per lane");
+        const bool h0 = 2 * lane < GP_ITEMS * (GP_THREADS / 32), h1 = 2 * lane + 1 < GP_ITEMS * (GP_THREADS / 32);
+        const uint32_t a0 = h0 ? s_cnt[2 * lane] : 0u, a1 = h1 ? s_cnt[2 * lane + 1] : 0u;
         uint32_t inc = a0 + a1;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
             const uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
             if (lane >= static_cast<uint32_t>(o)) inc += y;
         }
-        const uint32_t tot = __shfl_sync(0xffffffffu, inc, 31);
-        s_cnt[2 * lane] = inc - a0 - a1;
-        s_cnt[2 * lane + 1] = inc - a1;
-        if (lane == 0) st_rel32(look + tile, (tile == 0 ? GP_INC : GP_AGG) | tot);
-        uint32_t excl = 0;
-        int64_t jt = static_cast<int64_t>(tile) - 1;
-        while (jt >= 0) {  // 32 predecessors per step
-            const int64_t idx = jt - lane;
-            uint32_t f = GP_INC;  // before tile 0: an inclusive zero
-            if (idx >= 0) {
-                do {
-                    f = ld_acq32(look + idx);
-                } while ((f & ~GP_CNT) == 0);
-            }
-            const uint32_t incl = __ballot_sync(0xffffffffu, (f & GP_INC) != 0);
-            const int stop = incl ? __ffs(incl) - 1 : 31;
-            uint32_t v = (static_cast<int>(lane) <= stop) ? (f & GP_CNT) : 0u;
-#pragma unroll
-            for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-            excl += v;
-            if (incl) break;
-            jt -= 32;
-        }
-        if (lane == 0) {
-            if (tile != 0) st_rel32(look + tile, GP_INC | (excl + tot));
-            s_excl = excl;
-            if (tile == ntiles - 1) misc[0] = excl + tot;
-        }
+        if (h0) s_cnt[2 * lane] = inc - a0 - a1;
+        if (h1) s_cnt[2 * lane + 1] = inc - a1;
+        if (lane == 0) s_excl = tile_excl[tile];
     }
     __syncthreads();
 #pragma unroll
@@ -453,9 +483,13 @@ extern "C" int cdx_gang_priority(cdx_ctx* ctx, const cdx_prog_soa* progs, uint64
     uint32_t* misc = perm + N;  // 16 words
     uint32_t* plook = misc + 16;
     uint32_t* hist = plook + gtiles + 16;
-    cudaMemsetAsync(misc, 0, (16 + gtiles) * 4, ctx->stream);
+    cudaMemsetAsync(misc, 0, 16 * 4, ctx->stream);
     Launch L{ctx};
-    gang_prepare<<<gtiles, GP_THREADS, 0, ctx->stream>>>(p, khi, karr, kid, va, plook, misc, gtiles);
+    gang_count<<<gtiles, GP_THREADS, 0, ctx->stream>>>(progs->terminated, N, plook);
+    CDX_CHECK_LAUNCH(ctx, "gang_priority(count)");
+    gang_scan_tiles<<<1, 1024, 0, ctx->stream>>>(plook, gtiles, misc);
+    CDX_CHECK_LAUNCH(ctx, "gang_priority(scan)");
+    gang_prepare<<<gtiles, GP_THREADS, 0, ctx->stream>>>(p, khi, karr, kid, va, plook, misc);
     CDX_CHECK_LAUNCH(ctx, "gang_priority(prepare)");
     uint32_t hm[3];
     cudaError_t e = cudaMemcpyAsync(hm, misc, 12, cudaMemcpyDeviceToHost, ctx->stream);
