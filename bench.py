@@ -53,6 +53,26 @@ TH_MCTS = [(0, 0.99, 0), (1, 0.4, 0)]   # PAPER.md:963 MCTS/GSM8K thresholds
 TH_REBASE = [(0, 0.85, 0), (1, 0.99, 0)]  # PAPER.md:966 Rebase/GSM8K thresholds
 
 
+TRAFFIC_KEY = {"sc": "sc", "cot": "cot", "reward": "reward", "gang": "gang"}
+
+
+def load_traffic(kind):
+    """DRAM bytes per launch of this config's dominant kernel from the newest committed
+    `ncu --set full` summary (profiles/<round>_traffic.json, tools/summarize_profiles.py):
+    ncu's dram__bytes_read.sum + dram__bytes_write.sum, or None when none was captured."""
+    import glob
+    best = None
+    for path in sorted(glob.glob(os.path.join(ROOT, "profiles", "r*_traffic.json"))):  # round order
+        try:
+            with open(path) as f:
+                d = json.load(f).get(TRAFFIC_KEY[kind])
+        except Exception:
+            continue
+        if d:
+            best = {"bytes": d["dram_bytes"], "source": os.path.relpath(path, ROOT), "kernel": d["kernel"]}
+    return best
+
+
 def load_peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -530,6 +550,7 @@ def main():
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cpu = cpu_baseline(args.config, cfg, args.ref_sample or None)
     if rank == 0:
+        traffic = load_traffic(cfg["kind"])
         ach = res["kernel_bytes"] / (res["kernel_ms"] / 1e3) / 1e9
         cfg_out = {"workload": args.config, "desc": cfg["desc"],
                    **{k: v for k, v in cfg.items() if k not in ("kind", "desc", "conv_hi")},
@@ -545,7 +566,9 @@ def main():
             "vs_baseline": None, "dtype": "u32 ids / f64 certaindex (f32 store)", "data": "synthetic",
             "config": cfg_out,
             "roofline": {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
-                         "traffic": None, "peak_source": peak_src, "kernel": res["kernel"],
+                         "traffic": traffic["bytes"] if traffic else None,
+                         "traffic_source": traffic and f"{traffic['source']} ({traffic['kernel'][:60]})",
+                         "peak_source": peak_src, "kernel": res["kernel"],
                          "kernel_ms": res["kernel_ms"], "algorithmic_bytes_per_launch": res["kernel_bytes"],
                          "step_bytes": res["step_bytes"],
                          "step_frac": res["step_bytes"] / (res["ms"] / 1e3) / 1e9 / peak, **res["extra"]},
