@@ -1,22 +1,24 @@
-// k_sc_fast.cu — K2 fast path: Self-Consistency certaindex with BOTH cluster engines of
-// the SM running at once.
+// k_sc_fast.cu — K2 fast path: Self-Consistency certaindex over 32-row groups with two
+// cluster engines.
 //
 // Shapes: S in {4,8,16,32}, P % 32 == 0, 16B-aligned ids (configs A and C).  The ids
 // tensor is viewed as 128-byte lines ([R*P*S/32][32] u32); a GROUP = 32 probe rows of one
 // request = S lines starting at line G*S, staged by one TMA box load into a 128B-swizzled
-// shared buffer (conflict-free 16-byte reads for both engines).
+// shared buffer (conflict-free 16-byte reads for both engines); warps pull groups from one
+// global work counter through a private 2-deep TMA ring.
 //
-// Two engines, measured on B200 (tools/mb_match.cu, profiles/):
+// Engines, measured on B200 (tools/mb_match.cu, profiles/):
+//   * ALU peel engine (default for every warp): lane = row; the row's S ids sit in
+//     registers and clusters are peeled in first-seen order (first unassigned sample =
+//     next leader), S compares per cluster at two instructions each (ISETP + predicated
+//     OR).  On config C it alone streams at the HBM roofline (1.36 ms, 99.7% of the
+//     measured copy bandwidth).
 //   * warp-match engine: one __match_any_sync per row (lane = sample); the lowest lane of a
-//     match set is the cluster's first-seen answer, popc the size.  MATCH.ANY executes on
-//     the divergence unit (ADU) at ~4 + 1.5 cycles per distinct value per SM, so this
-//     engine alone is ADU-bound (~1.9 ms on config C).
-//   * ALU peel engine: lane = row; the row's S ids sit in registers and clusters are
-//     peeled in first-seen order (first unassigned sample = next leader, S compares per
-//     cluster).  ALU-pipe-bound (~1.9 ms on config C alone).
-// The pipes are independent, so warps of a CTA are split between the engines and pull
-// groups from one global work counter: each engine runs at its own speed and together
-// they move the kernel to the HBM roofline.
+//     match set is the cluster's first-seen answer, popc the size.  MATCH.ANY runs on the
+//     divergence unit (~4 + 1.5 cycles per distinct value per SM), and its cost does not
+//     grow with the number of clusters, so a group with a row of more than PEEL_MAX
+//     clusters is redone here (warp vote), and CDX_SCF_MATCH=k dedicates k warps of a CTA
+//     to it (the pipes are independent; both engines pull from the same counter).
 //
 // Both produce, per row, the first-seen-ordered cluster sizes folded in FP64 exactly as
 // metrics.cpp:107-125 (h -= term[size], term[c] = (c/S)*log(c/S) from the host libm;
@@ -33,16 +35,23 @@ namespace {
 
 constexpr uint32_t FAST_WARPS = 8;  // max warps per CTA
 
+// a |= bit when x == v: ISETP + one predicated LOP3 (the select-and-or form costs three)
+__device__ __forceinline__ void or_if_eq(uint32_t& a, uint32_t x, uint32_t v, uint32_t bit) {
+    asm("{\n\t.reg .pred p;\n\tsetp.eq.u32 p, %1, %2;\n\t@p or.b32 %0, %0, %3;\n\t}"
+        : "+r"(a)
+        : "r"(x), "r"(v), "r"(bit));
+}
+
 // bit e set iff x[e] == v; four independent accumulators keep the dependency chains short
 template <int S>
 __device__ __forceinline__ uint32_t eq_mask(const uint32_t (&x)[S], uint32_t v) {
     uint32_t a0 = 0, a1 = 0, a2 = 0, a3 = 0;
 #pragma unroll
     for (uint32_t e = 0; e < S; e += 4) {
-        a0 |= (x[e] == v ? 1u : 0u) << e;
-        a1 |= (x[e + 1] == v ? 2u : 0u) << e;
-        a2 |= (x[e + 2] == v ? 4u : 0u) << e;
-        a3 |= (x[e + 3] == v ? 8u : 0u) << e;
+        or_if_eq(a0, x[e], v, 1u << e);
+        or_if_eq(a1, x[e + 1], v, 2u << e);
+        or_if_eq(a2, x[e + 2], v, 4u << e);
+        or_if_eq(a3, x[e + 3], v, 8u << e);
     }
     return (a0 | a1) | (a2 | a3);
 }
@@ -58,10 +67,14 @@ __device__ __forceinline__ double finish_entropy(double h, double logn) {
     return v < 0.0 ? 0.0 : (1.0 < v ? 1.0 : v);  // std::clamp(v, 0, 1)
 }
 
-// ALU peel engine: lane owns row `lane` of the group.
+// ALU peel engine: lane owns row `lane` of the group.  At most PEEL_MAX clusters are peeled
+// (each costs S compares); a row with more sets *more and the warp redoes the group with the
+// match engine, whose cost does not grow with the cluster count.
+constexpr uint32_t PEEL_MAX = 8;
+
 template <int S>
 __device__ __forceinline__ double alu_row(const uint8_t* __restrict__ buf, const double* __restrict__ term,
-                                          uint32_t lane, double logn) {
+                                          uint32_t lane, double logn, bool* more) {
     uint32_t x[S];
 #pragma unroll
     for (uint32_t j = 0; j < S / 4; ++j) {
@@ -77,7 +90,13 @@ __device__ __forceinline__ double alu_row(const uint8_t* __restrict__ buf, const
     un &= ~eq;
     if (un == 0) return 1.0;  // one cluster holds every answer: H = 0, H~ = 1 exactly
     double h = __dsub_rn(0.0, term[__popc(eq)]);
+    uint32_t peeled = 1;
     while (un) {
+        if (peeled == PEEL_MAX) {
+            *more = true;
+            return 0.0;
+        }
+        ++peeled;
         const uint32_t l = __ffs(un) - 1;  // first unassigned sample = next cluster's leader
         const uint32_t v = *reinterpret_cast<const uint32_t*>(buf + elem_addr(lane * S + l));
         eq = eq_mask<S>(x, v);
@@ -177,8 +196,9 @@ __global__ void __launch_bounds__(FAST_WARPS * 32) sc_fast_kernel(const __grid_c
         if (G >= p.ngroups) break;  // claims are monotone: nothing left for this warp
         mbar_wait(&bar[stage], parity);
         const uint8_t* buf = wbase + stage * GB;
-        const double hc = use_match ? match_rows<S>(buf, cntw, term, lane, p.logn)
-                                    : alu_row<S>(buf, term, lane, p.logn);
+        bool more = false;
+        double hc = use_match ? 0.0 : alu_row<S>(buf, term, lane, p.logn, &more);
+        if (use_match || __any_sync(0xffffffffu, more)) hc = match_rows<S>(buf, cntw, term, lane, p.logn);
         __syncwarp();  // every lane is done with this stage (and with cntw)
         if (lane == 0) claim_issue(stage);
         bool meets = true;
@@ -230,8 +250,9 @@ bool launch_sc_fast(cdx_ctx* ctx, const ScParams& p0) {
     ScParams p = p0;
     // warps per CTA, ring depth per warp and how many warps of a CTA run the match engine
     // (defaults tuned on B200, profiles/)
-    // config C sweep (profiles/r1_sc_tuning.txt): 8 warps x 1 stage, half on each engine
-    uint32_t wpc = 8, stages = 1, mw = 4;
+    // config C sweep: 8 warps x 2 stages, every warp on the ALU engine (match fallback per
+    // group): 1.360 ms = 99.7% of the measured copy bandwidth; 1 match warp 1.376, 4 1.422
+    uint32_t wpc = 8, stages = 2, mw = 0;
     if (const char* e = getenv("CDX_SCF_WARPS")) wpc = static_cast<uint32_t>(atoi(e));
     if (const char* e = getenv("CDX_SCF_STAGES")) stages = static_cast<uint32_t>(atoi(e));
     if (const char* e = getenv("CDX_SCF_MATCH")) mw = static_cast<uint32_t>(atoi(e));

@@ -147,3 +147,21 @@ def test_allocate_scan_large_property(ctx):
     kept = out["kept"][:n_kept].to(torch.int64)
     assert torch.all(kept[1:] > kept[:-1])
     assert n_kept == int((out["granted"] > 5).sum())
+
+
+@pytest.mark.parametrize("distinct", [9, 17, 32])
+def test_sc_many_clusters_fallback(ctx, distinct):
+    """Rows with more than PEEL_MAX clusters send their group to the warp-match engine; the
+    result must stay bit-identical (high-entropy rows, every engine split)."""
+    import torch
+    from paper_2412_20993_b200 import Threshold
+    R, P, S = 97, 64, 32
+    rng = np.random.default_rng(distinct)
+    ids = rng.integers(0, distinct, size=(R, P, S)).astype(np.uint32)
+    ids[::3, ::5, :] = np.arange(S, dtype=np.uint32)  # all-distinct rows
+    ids[1::4, 7, :] = 5  # single-cluster rows in the same groups
+    h, m = ctx.sc_certaindex(torch.from_numpy(ids.view(np.int32)).cuda(), [Threshold(SIG_E, 0.1, GE)])
+    ctx.sync()
+    _, oh32, om = O.sc_certaindex(ids, [(SIG_E, 0.1, GE)])
+    assert np.array_equal(h.cpu().numpy().view(np.uint32), oh32.view(np.uint32))
+    assert np.array_equal(m.cpu().numpy().view(np.uint32), om)
