@@ -318,6 +318,23 @@ int cdx_gang_merge(cdx_ctx* ctx, const uint64_t* keys, const uint64_t* run_len, 
 int cdx_offsets_rebase(cdx_ctx* ctx, int64_t* offsets, uint64_t R, const int64_t* shard_totals,
                        uint32_t rank);
 
+/* ---- aggregation: the final answer per archetype (ProgramDriver::aggregate_prefix,
+ * runtime.cpp:318-403) --------------------------------------------------
+ * SC: plurality over the exit row's answers, earliest-seen cluster wins ties.  ids
+ * u32[R][P][S], exit_knob i32[R] (1-based knob unit, e.g. K5's exit_knob) -> answer u32[R].
+ * A knob outside [1, P] fails at cdx_sync.                                                */
+int cdx_sc_aggregate(cdx_ctx* ctx, const uint32_t* ids, uint64_t R, uint32_t P, uint32_t S,
+                     const int32_t* exit_knob, uint32_t* answer);
+/* MCTS (agg CDX_AGG_MEAN): answer of the first maximum-reward path over steps 0..t.
+ * Rebase (agg CDX_AGG_MAX): softmax-weighted plurality (sum of exp(reward) per cluster in
+ * path order) over the last full layer, step t.  rewards f32[G][T][W], ids u32[G][T][W],
+ * exit_step i32[G] (0-based step t) -> answer u32[G]; W <= 256.  exp() is the host libm's on
+ * the 2^-24 grid of [0,1]; *inexact (device u64, required) counts rewards off that grid,
+ * whose weights use the device exp (<= 1 ulp from the host's).                           */
+int cdx_reward_aggregate(cdx_ctx* ctx, const float* rewards, const uint32_t* ids, const uint8_t* agg,
+                         uint64_t G, uint32_t T, uint32_t W, const int32_t* exit_step,
+                         uint32_t* answer, uint64_t* inexact);
+
 /* ---- end-to-end host entry: SC certaindex + allocate from HOST buffers ---------------
  * Streams ids (host, ideally pinned) through the device in chunks of whole requests,
  * overlapping H2D copies with K2+K5, and copies exit_knob/reason/granted/offsets and the

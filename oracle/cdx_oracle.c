@@ -694,3 +694,67 @@ int cdxo_canon_intern(const char* bytes, const uint64_t* offsets, uint64_t n, co
     free(tab);
     return CDX_OK;
 }
+
+/* ===================================================================================== */
+/* Aggregation, runtime.cpp:316-403 (weighted_plurality :316-336, aggregate_prefix       */
+/* :345-403): SC plurality, MCTS first argmax, Rebase exp-weighted plurality over the     */
+/* last full layer.  exp() is this libm's, the same glibc the reference links.           */
+/* ===================================================================================== */
+/* weighted plurality over n answers (ids) with optional weights: first-seen clusters,
+ * strict > over the summed weights (weights summed in path order, starting from 0.0) */
+static uint32_t plurality_ids(const uint32_t* v, const double* w, int n) {
+    uint32_t keys[1024];
+    double tot[1024];
+    int m = 0;
+    for (int i = 0; i < n; ++i) {
+        int c = 0;
+        while (c < m && keys[c] != v[i]) ++c;
+        if (c == m) {
+            keys[m] = v[i];
+            tot[m] = 0.0;
+            ++m;
+        }
+        tot[c] += w ? w[i] : 1.0;
+    }
+    uint32_t best = keys[0];
+    double bw = -1.0;
+    for (int c = 0; c < m; ++c)
+        if (tot[c] > bw) {
+            bw = tot[c];
+            best = keys[c];
+        }
+    return best;
+}
+
+int cdxo_sc_aggregate(const uint32_t* ids, uint64_t R, uint32_t P, uint32_t S, const int32_t* exit_knob,
+                      uint32_t* answer) {
+    if (S == 0 || S > 1024 || P == 0) return CDX_EINVAL;
+    for (uint64_t r = 0; r < R; ++r) {
+        if (exit_knob[r] < 1 || (uint32_t)exit_knob[r] > P) return CDX_EINVAL;
+        answer[r] = plurality_ids(ids + (r * P + (uint64_t)(exit_knob[r] - 1)) * S, NULL, (int)S);
+    }
+    return CDX_OK;
+}
+
+int cdxo_reward_aggregate(const float* rw, const uint32_t* ids, const uint8_t* agg, uint64_t G, uint32_t T,
+                          uint32_t W, const int32_t* exit_step, uint32_t* answer) {
+    if (W == 0 || W > 1024 || T == 0) return CDX_EINVAL;
+    double w[1024];
+    for (uint64_t g = 0; g < G; ++g) {
+        const int32_t t = exit_step[g];
+        if (t < 0 || (uint32_t)t >= T) return CDX_EINVAL;
+        const uint64_t base = g * T * W;
+        if (agg[g] == CDX_AGG_MEAN) { /* MCTS: runtime.cpp:380-389 */
+            const uint64_t n = (uint64_t)(t + 1) * W;
+            uint64_t best = 0;
+            for (uint64_t i = 1; i < n; ++i)
+                if ((double)rw[base + i] > (double)rw[base + best]) best = i;
+            answer[g] = ids[base + best];
+        } else { /* Rebase: runtime.cpp:357-378, last full layer = step t */
+            const uint64_t l0 = base + (uint64_t)t * W;
+            for (uint32_t i = 0; i < W; ++i) w[i] = exp((double)rw[l0 + i]);
+            answer[g] = plurality_ids(ids + l0, w, (int)W);
+        }
+    }
+    return CDX_OK;
+}

@@ -103,6 +103,12 @@ int cdxo_canon_intern(const char* bytes, const uint64_t* offsets, uint64_t n,
 int cdxo_flag_hesitation(const char* s, size_t len, const char* markers,
                          const uint32_t* marker_offsets, uint32_t n_markers);
 
+/* ---- aggregation (runtime.cpp:316-403) ------------------------------------------------ */
+int cdxo_sc_aggregate(const uint32_t* ids, uint64_t R, uint32_t P, uint32_t S, const int32_t* exit_knob,
+                      uint32_t* answer);
+int cdxo_reward_aggregate(const float* rw, const uint32_t* ids, const uint8_t* agg, uint64_t G, uint32_t T,
+                          uint32_t W, const int32_t* exit_step, uint32_t* answer);
+
 #ifdef __cplusplus
 }
 #endif

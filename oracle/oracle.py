@@ -440,3 +440,43 @@ def hardware_threads():
         return int(ref().ref_hardware_threads())
     except Exception:
         return os.cpu_count() or 1
+
+
+# ---------------------------------------------------------------- aggregation (runtime.cpp:316-403)
+def sc_aggregate(ids, exit_knob):
+    R, P_, S = ids.shape
+    out = np.empty(max(R, 1), np.uint32)
+    lib().cdxo_sc_aggregate.argtypes = [P, C.c_uint64, C.c_uint32, C.c_uint32, P, P]
+    st = lib().cdxo_sc_aggregate(_p(np.ascontiguousarray(ids)), R, P_, S,
+                                 _p(np.ascontiguousarray(exit_knob, dtype=np.int32)), _p(out))
+    if st:
+        raise ValueError(f"oracle sc_aggregate status {st}")
+    return out[:R]
+
+
+def reward_aggregate(rw, ids, agg, exit_step):
+    G, T, W = rw.shape
+    out = np.empty(max(G, 1), np.uint32)
+    lib().cdxo_reward_aggregate.argtypes = [P, P, P, C.c_uint64, C.c_uint32, C.c_uint32, P, P]
+    st = lib().cdxo_reward_aggregate(_p(np.ascontiguousarray(rw)), _p(np.ascontiguousarray(ids)),
+                                     _p(np.ascontiguousarray(agg, dtype=np.uint8)), G, T, W,
+                                     _p(np.ascontiguousarray(exit_step, dtype=np.int32)), _p(out))
+    if st:
+        raise ValueError(f"oracle reward_aggregate status {st}")
+    return out[:G]
+
+
+def ref_aggregate(archetype, ids, rewards, layer_widths, units, vocab_list):
+    """The reference's own ProgramDriver::aggregate_prefix on injected paths -> vocab index."""
+    n = len(ids)
+    a_ids = (C.c_uint32 * max(n, 1))(*[int(x) for x in ids])
+    a_rw = None if rewards is None else (C.c_double * max(n, 1))(*[float(x) for x in rewards])
+    a_lw = (C.c_int * max(1, len(layer_widths)))(*layer_widths)
+    v, nv = _vocab_c(vocab_list)
+    out = C.c_uint32(0)
+    f = ref().ref_aggregate
+    f.argtypes = [C.c_int, P, P, C.c_int, P, C.c_int, C.c_int, P, C.c_uint32, P]
+    if f(archetype, C.cast(a_ids, P), None if a_rw is None else C.cast(a_rw, P), n, C.cast(a_lw, P),
+         len(layer_widths), units, C.cast(v, P), nv, C.byref(out)) < 0:
+        raise RefError(_ref_err())
+    return out.value

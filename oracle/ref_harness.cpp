@@ -419,4 +419,40 @@ int ref_reward_batch(const float* rewards, const uint32_t* ids, const uint8_t* a
     return fail ? -1 : 0;
 }
 
+// ProgramDriver::aggregate_prefix (runtime.cpp:345-403) of an SC / Rebase / MCTS program
+// whose paths are injected: answers vocab[ids[i]], rewards (nullable), Rebase layers of
+// widths layer_w.  Writes the index into vocab of the trimmed answer; returns 0 or -1.
+int ref_aggregate(int archetype, const uint32_t* ids, const double* rewards, int n, const int* layer_w,
+                  int n_layers, int units, const char* const* vocab, uint32_t nvocab, uint32_t* out) {
+    try {
+        const auto voc = make_vocab(vocab, nvocab);
+        cdx::runtime::SyntheticProgramSpec spec;
+        spec.archetype = static_cast<cdx::runtime::Archetype>(archetype);
+        spec.resource_cap = std::max(units, n);
+        if (spec.archetype != cdx::runtime::Archetype::SC) spec.rewards = cdx::runtime::RewardModel{};
+        cdx::runtime::ProgramDriver d(7, "p", spec, 1);
+        auto& st = d.program().state;
+        st.paths.clear();
+        for (int i = 0; i < n; ++i) {
+            cdx::runtime::PathSample ps;
+            ps.knob_point = i + 1;
+            ps.answer = voc[ids[i]];
+            if (rewards) ps.reward = rewards[i];
+            st.paths.push_back(ps);
+        }
+        st.layer_widths.assign(layer_w, layer_w + n_layers);
+        const auto res = d.aggregate_prefix(units);
+        for (uint32_t k = 0; k < nvocab; ++k)
+            if (cdx::metrics::trim(voc[k]) == res.answer) {
+                *out = k;
+                return 0;
+            }
+        g_err = "ref_aggregate: answer not in vocabulary: " + res.answer;
+        return -1;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return -1;
+    }
+}
+
 }  // extern "C"

@@ -373,3 +373,22 @@ class Context:
     def offsets_rebase(self, offsets, shard_totals, rank: int):
         self._bind_stream()
         self._check(self.lib.cdx_offsets_rebase(self.h, _ptr(offsets), offsets.shape[0], _ptr(shard_totals), rank))
+
+    # -- aggregation (runtime.cpp:318-403) --
+    def sc_aggregate(self, ids, exit_knob):
+        t = self.torch
+        R, P, S = ids.shape
+        ans = self.empty((max(R, 1),), t.int32)
+        self._bind_stream()
+        self._check(self.lib.cdx_sc_aggregate(self.h, _ptr(ids), R, P, S, _ptr(exit_knob), _ptr(ans)))
+        return ans[:R]
+
+    def reward_aggregate(self, rewards, ids, agg, exit_step):
+        t = self.torch
+        G, T, W = rewards.shape
+        ans = self.empty((max(G, 1),), t.int32)
+        inexact = self.torch.zeros((1,), dtype=t.int64, device=self.dev)
+        self._bind_stream()
+        self._check(self.lib.cdx_reward_aggregate(self.h, _ptr(rewards), _ptr(ids), _ptr(agg), G, T, W,
+                                                  _ptr(exit_step), _ptr(ans), _ptr(inexact)))
+        return ans[:G], inexact

@@ -38,6 +38,8 @@ struct cdx_ctx {
     void* al_state = nullptr;
     size_t al_tiles = 0;      // capacity in tiles
     uint32_t al_epoch = 0;
+    // std::exp on the 2^-24 grid of [0,1] (Rebase aggregation), built on first use
+    double* exp_tab = nullptr;
     // term-table cache (device): keyed by the list of n values it was built for
     double* tt_dev = nullptr;
     size_t tt_bytes = 0;

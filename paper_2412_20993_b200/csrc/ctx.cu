@@ -118,6 +118,7 @@ int build_term_tables(cdx_ctx* ctx, const uint32_t* ns, uint32_t count, TermTabl
     if (bytes > ctx->tt_bytes) {
         if (ctx->tt_dev) cudaFree(ctx->tt_dev);
     if (ctx->al_state) cudaFree(ctx->al_state);
+    if (ctx->exp_tab) cudaFree(ctx->exp_tab);
         ctx->tt_dev = nullptr;
         ctx->tt_bytes = 0;
         if (cudaMalloc(&ctx->tt_dev, bytes) != cudaSuccess) return set_error(ctx, CDX_ECUDA, "term table alloc");
@@ -189,6 +190,7 @@ int cdx_ctx_destroy(cdx_ctx* ctx) {
     if (ctx->pipe_buf) cudaFree(ctx->pipe_buf);
     if (ctx->tt_dev) cudaFree(ctx->tt_dev);
     if (ctx->al_state) cudaFree(ctx->al_state);
+    if (ctx->exp_tab) cudaFree(ctx->exp_tab);
     if (ctx->d_err) cudaFree(ctx->d_err);
     if (ctx->h_err) cudaFreeHost(ctx->h_err);
     if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);

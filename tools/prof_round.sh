@@ -10,8 +10,8 @@ for c in C B D E; do
 done
 timeout 300 ncu --set full --clock-control none --import-source on -k regex:sc_fast_kernel -s 3 -c 1 -o gpurun_out/${tag}_full_sc $B --config C > /dev/null 2>&1
 timeout 300 ncu --set full --clock-control none --import-source on -k regex:allocate_scan -s 3 -c 1 -o gpurun_out/${tag}_full_alloc $B --config C > /dev/null 2>&1
-timeout 300 ncu --set full --clock-control none --import-source on -k regex:cot_run -s 3 -c 1 -o gpurun_out/${tag}_full_cot $B --config B > /dev/null 2>&1
+timeout 300 ncu --set full --clock-control none --import-source on -k regex:cot_run64 -s 3 -c 1 -o gpurun_out/${tag}_full_cot $B --config B > /dev/null 2>&1
 timeout 300 ncu --set full --clock-control none --import-source on -k regex:reward_quad -s 2 -c 1 -o gpurun_out/${tag}_full_reward $B --config D > /dev/null 2>&1
-timeout 300 ncu --set full --clock-control none --import-source on -k regex:rs_scatter -s 8 -c 1 -o gpurun_out/${tag}_full_gang $B --config E > /dev/null 2>&1
+timeout 300 ncu --set full --clock-control none --import-source on -k regex:os_pass -s 8 -c 1 -o gpurun_out/${tag}_full_gang $B --config E > /dev/null 2>&1
 timeout 900 python bench.py > gpurun_out/${tag}_bench.json 2> gpurun_out/${tag}_bench.err
 ls gpurun_out | grep $tag
