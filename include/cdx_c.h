@@ -318,6 +318,20 @@ int cdx_gang_merge(cdx_ctx* ctx, const uint64_t* keys, const uint64_t* run_len, 
 int cdx_offsets_rebase(cdx_ctx* ctx, int64_t* offsets, uint64_t R, const int64_t* shard_totals,
                        uint32_t rank);
 
+/* ---- epsilon-accuracy stop test (alternative CoT stop rule) ----------------------------
+ * probe::stationary_by_epsilon_test (probe.cpp:104-120) over theory::epsilon_stop_test
+ * (theory.cpp:100-146).  Batched over CoT traces (ids u32[R][P], hes u64[R][ceil(P/64)],
+ * P <= 64), evaluated at every prefix: eps_step i32[R] = first probe where it returns true
+ * (-1 if none), state u8[R][P] (nullable) = 0 nullopt / 1 false / 2 true per prefix.
+ * Errors as the reference: "epsilon_stop_test: k must be >= 1", "... epsilon must be > 0". */
+int cdx_cot_eps_stop(cdx_ctx* ctx, const uint32_t* ids, const uint64_t* hes, uint64_t R, uint32_t P,
+                     int32_t k, double epsilon, int32_t* eps_step, uint8_t* state);
+/* The same test on ragged record rows (the scalar API): whole row r = one record span,
+ * hes u8 per record; state u8[rows]; at most 1024 non-hesitant records per row.          */
+int cdx_probe_eps_stop_rows(cdx_ctx* ctx, const uint32_t* ids, const uint8_t* hes,
+                            const uint64_t* row_off, uint64_t rows, int32_t k, double epsilon,
+                            uint8_t* state);
+
 /* ---- aggregation: the final answer per archetype (ProgramDriver::aggregate_prefix,
  * runtime.cpp:318-403) --------------------------------------------------
  * SC: plurality over the exit row's answers, earliest-seen cluster wins ties.  ids

@@ -758,3 +758,67 @@ int cdxo_reward_aggregate(const float* rw, const uint32_t* ids, const uint8_t* a
     }
     return CDX_OK;
 }
+
+/* ===================================================================================== */
+/* Epsilon-accuracy stop test, probe.cpp:104-120 over theory.cpp:100-146, at every prefix */
+/* of every CoT trace: state 0 nullopt / 1 false / 2 true; step = first true (or -1).     */
+/* Restated with the reference's dense per-group vectors (window_counts, tv_raw).         */
+/* ===================================================================================== */
+static void eps_window_counts(const int* g, int start, int len, int m, double* out) {
+    for (int i = 0; i < m; ++i) out[i] = 0.0;
+    for (int t = 0; t < len; ++t) out[g[start + t]] += 1.0;
+    for (int i = 0; i < m; ++i) out[i] /= (double)len;
+}
+static double eps_tv(const double* a, const double* b, int m) {
+    double l1 = 0.0;
+    for (int i = 0; i < m; ++i) l1 += fabs(a[i] - b[i]);
+    return 0.5 * l1;
+}
+static int eps_test(const int* g, int n, int k, double epsilon) {
+    if (n < 2 * k) return 0;
+    const int anchor = n - 2 * k;
+    int m = 0;
+    for (int i = 0; i < n; ++i)
+        if (g[i] + 1 > m) m = g[i] + 1;
+    const double limit = epsilon / 3.0;
+    double ref[1024], probe[1024];
+    eps_window_counts(g, anchor, k, m, ref);
+    for (int j = 1; j <= k; ++j) {
+        eps_window_counts(g, anchor + j, k, m, probe);
+        if (eps_tv(ref, probe, m) > limit) return 1;
+    }
+    if (k >= 2) {
+        eps_window_counts(g, anchor, k - 1, m, ref);
+        for (int j = 1; j <= k - 1; ++j) {
+            eps_window_counts(g, anchor + j, k - 1, m, probe);
+            if (eps_tv(ref, probe, m) > limit) return 1;
+        }
+    }
+    return 2;
+}
+
+int cdxo_cot_eps_stop(const uint32_t* ids, const uint64_t* hes, uint64_t R, uint32_t P, int k, double epsilon,
+                      int32_t* step, uint8_t* state) {
+    if (k < 1 || !(epsilon > 0.0) || P == 0 || P > 1024) return CDX_EINVAL;
+    const uint32_t hw = (P + 63) / 64;
+    int g[1024];
+    uint32_t seen[1024];
+    for (uint64_t r = 0; r < R; ++r) {
+        int n = 0, m = 0;
+        int32_t first = -1;
+        for (uint32_t p = 0; p < P; ++p) {
+            if (!((hes[r * hw + p / 64] >> (p % 64)) & 1ull)) {
+                const uint32_t v = ids[r * P + p];
+                int c = 0;
+                while (c < m && seen[c] != v) ++c;
+                if (c == m) seen[m++] = v;
+                g[n++] = c;
+            }
+            const int st = eps_test(g, n, k, epsilon);
+            if (state) state[r * P + p] = (uint8_t)st;
+            if (st == 2 && first < 0) first = (int32_t)p;
+        }
+        step[r] = first;
+    }
+    return CDX_OK;
+}

@@ -103,6 +103,10 @@ int cdxo_canon_intern(const char* bytes, const uint64_t* offsets, uint64_t n,
 int cdxo_flag_hesitation(const char* s, size_t len, const char* markers,
                          const uint32_t* marker_offsets, uint32_t n_markers);
 
+/* ---- epsilon-accuracy stop test at every CoT prefix (probe.cpp:104-120) -------------- */
+int cdxo_cot_eps_stop(const uint32_t* ids, const uint64_t* hes, uint64_t R, uint32_t P, int k, double epsilon,
+                      int32_t* step, uint8_t* state);
+
 /* ---- aggregation (runtime.cpp:316-403) ------------------------------------------------ */
 int cdxo_sc_aggregate(const uint32_t* ids, uint64_t R, uint32_t P, uint32_t S, const int32_t* exit_knob,
                       uint32_t* answer);

@@ -480,3 +480,29 @@ def ref_aggregate(archetype, ids, rewards, layer_widths, units, vocab_list):
          len(layer_widths), units, C.cast(v, P), nv, C.byref(out)) < 0:
         raise RefError(_ref_err())
     return out.value
+
+
+# ---------------------------------------------------------------- epsilon stop test (probe.cpp:104-120)
+def cot_eps_stop(ids, hes, k, epsilon):
+    R, P_ = ids.shape
+    step = np.empty(max(R, 1), np.int32)
+    state = np.empty((R, P_), np.uint8)
+    lib().cdxo_cot_eps_stop.argtypes = [P, P, C.c_uint64, C.c_uint32, C.c_int, C.c_double, P, P]
+    st = lib().cdxo_cot_eps_stop(_p(np.ascontiguousarray(ids)), _p(np.ascontiguousarray(hes)), R, P_, k,
+                                 float(epsilon), _p(step), _p(state))
+    if st:
+        raise ValueError(f"oracle cot_eps_stop status {st}")
+    return step[:R], state
+
+
+def ref_eps_prefixes(ids, hes, k, epsilon, vocab_list):
+    """The reference's stationary_by_epsilon_test at every prefix -> state u8[R][P]."""
+    R, P_ = ids.shape
+    state = np.empty((R, P_), np.uint8)
+    v, nv = _vocab_c(vocab_list)
+    f = ref().ref_eps_prefixes
+    f.argtypes = [P, P, C.c_uint64, C.c_uint32, C.c_int, C.c_double, P, C.c_uint32, P]
+    if f(_p(np.ascontiguousarray(ids)), _p(np.ascontiguousarray(hes)), R, P_, k, float(epsilon), C.cast(v, P), nv,
+         _p(state)) < 0:
+        raise RefError(_ref_err())
+    return state

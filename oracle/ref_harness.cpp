@@ -455,4 +455,32 @@ int ref_aggregate(int archetype, const uint32_t* ids, const double* rewards, int
     }
 }
 
+// probe::stationary_by_epsilon_test (probe.cpp:104-120) of every prefix of each trace:
+// ids[R][P] (answers vocab[id]), hes bits u64[R][ceil(P/64)] -> state u8[R][P] (0 nullopt,
+// 1 false, 2 true).  Returns 0, or -1 with the exception text (k / epsilon validation).
+int ref_eps_prefixes(const uint32_t* ids, const uint64_t* hes, uint64_t R, uint32_t P, int k, double epsilon,
+                     const char* const* vocab, uint32_t nvocab, uint8_t* state) {
+    try {
+        const auto voc = make_vocab(vocab, nvocab);
+        const uint32_t hw = (P + 63) / 64;
+        for (uint64_t r = 0; r < R; ++r) {
+            std::vector<cdx::probe::AnswerRecord> recs;
+            for (uint32_t p = 0; p < P; ++p) {
+                cdx::probe::AnswerRecord a;
+                a.step_index = static_cast<int>(p) + 1;
+                a.token_offset = 64L * (p + 1);
+                a.answer = voc[ids[r * P + p]];
+                a.hesitant = (hes[r * hw + p / 64] >> (p % 64)) & 1ull;
+                recs.push_back(a);
+                const auto res = cdx::probe::stationary_by_epsilon_test(recs, k, epsilon);
+                state[r * P + p] = res ? (*res ? 2 : 1) : 0;
+            }
+        }
+        return 0;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return -1;
+    }
+}
+
 }  // extern "C"

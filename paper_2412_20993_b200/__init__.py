@@ -392,3 +392,14 @@ class Context:
         self._check(self.lib.cdx_reward_aggregate(self.h, _ptr(rewards), _ptr(ids), _ptr(agg), G, T, W,
                                                   _ptr(exit_step), _ptr(ans), _ptr(inexact)))
         return ans[:G], inexact
+
+    # -- epsilon-accuracy stop test (probe.cpp:104-120, theory.cpp:117-146) --
+    def cot_eps_stop(self, ids, hes, k: int, epsilon: float, want_state: bool = False):
+        t = self.torch
+        R, P = ids.shape
+        step = self.empty((max(R, 1),), t.int32)
+        state = self.empty((R, P), t.uint8) if want_state else None
+        self._bind_stream()
+        self._check(self.lib.cdx_cot_eps_stop(self.h, _ptr(ids), _ptr(hes), R, P, k, float(epsilon), _ptr(step),
+                                              _ptr(state)))
+        return step[:R], state

@@ -5,6 +5,7 @@
 //   consistency      K1 ids + cdx_probe_consistency                   probe.cpp:48-75
 //   should_exit      K1 ids + cdx_probe_should_exit                   probe.cpp:77-85
 //   final_answer     cdx_probe_final_answer (record index), trimmed   probe.cpp:87-102
+//   stationary_by_epsilon_test  K1 ids + cdx_probe_eps_stop_rows      probe.cpp:104-120
 // ProbeConfig::validate and the enum names are host-side configuration checks with the
 // reference's messages.  JSONL trace I/O lives in facade_jsonl.cpp.
 
@@ -126,6 +127,27 @@ FinalAnswer final_answer(const ProbeTrace& trace) {
                                     d_why.data(), 1, pos.data(), low.data()));
     const uint64_t p = pos.download()[0];
     return {std::string(metrics::trim(trace.records[p].answer)), low.download()[0] != 0};
+}
+
+std::optional<bool> stationary_by_epsilon_test(std::span<const AnswerRecord> records, int k, double epsilon) {
+    auto& cx = detail::scalar_ctx();
+    if (records.empty()) {  // validation first, as theory.cpp:118-119, then "not enough probes"
+        cdx_ctx* h = cx.raw();
+        batch::DeviceArray<uint64_t> off(cx, 2);
+        off.zero();
+        batch::DeviceArray<uint8_t> st(cx, 1);
+        batch::DeviceArray<uint32_t> ids(cx, 1);
+        batch::DeviceArray<uint8_t> hs(cx, 1);
+        cx.check(cdx_probe_eps_stop_rows(h, ids.data(), hs.data(), off.data(), 1, k, epsilon, st.data()));
+        return std::nullopt;
+    }
+    auto t = upload(cx, records, true, false);
+    batch::DeviceArray<uint8_t> st(cx, 1);
+    cx.check(cdx_probe_eps_stop_rows(cx.raw(), t.in.ids.data(), t.hes.data(), t.row_off.data(), 1, k, epsilon,
+                                     st.data()));
+    const uint8_t v = st.download()[0];
+    if (v == 0) return std::nullopt;
+    return v == 2;
 }
 
 }  // namespace cdx::probe

@@ -267,6 +267,12 @@ void random_cases(int count) {
             run("should_exit " + id, [&] { return std::to_string(static_cast<int>(probe::should_exit(t, cfg))); });
             if (!recs.empty() && below(2)) t.terminated_at = recs[below(static_cast<uint32_t>(recs.size()))].step_index + (below(5) == 0 ? 1 : 0);
             t.termination_reason = static_cast<probe::TerminationReason>(below(3));
+            const int ek = static_cast<int>(below(5)) - (below(15) == 0 ? 1 : 0);
+            const double eps = below(12) == 0 ? 0.0 : 0.05 + unit();
+            run("eps_test " + id, [&] {
+                auto e = probe::stationary_by_epsilon_test(recs, ek, eps);
+                return e ? std::to_string(*e) : std::string("nullopt");
+            });
             run("final_answer " + id, [&] {
                 auto f = probe::final_answer(t);
                 return esc(f.answer) + " low=" + std::to_string(f.low_confidence);
