@@ -318,6 +318,22 @@ int cdx_gang_merge(cdx_ctx* ctx, const uint64_t* keys, const uint64_t* run_len, 
 int cdx_offsets_rebase(cdx_ctx* ctx, int64_t* offsets, uint64_t R, const int64_t* shard_totals,
                        uint32_t rank);
 
+/* ---- JSONL trace ingestion (probe::read_trace_jsonl, probe.cpp:126-165) ---------------
+ * text: the whole JSON-lines file in DEVICE memory (nbytes < 4 GiB).  Per record, in line
+ * order (blank lines skipped): program u32 (program ids interned exactly, dense, first-seen
+ * order), step_index i32, token_offset i64, hesitant u8, the decoded answer in
+ * answer_arena[answer_off[r] .. answer_off[r+1]) (capacity nbytes), the decoded program id in
+ * program_arena[program_off[r] ..) (nullable pair), program_first u64[programs] (nullable:
+ * first record of each program).  Arrays hold cap_records (>= the number of lines) entries,
+ * offsets cap_records + 1.  The first bad line fails with CDX_ERUNTIME and the reference's
+ * "trace line <n>: invalid JSON | missing or mistyped field | token_offset does not
+ * increase | step_index does not increase" (detail text after the category may differ). */
+int cdx_jsonl_parse(cdx_ctx* ctx, const char* text, uint64_t nbytes, uint64_t cap_records,
+                    uint32_t* program, int32_t* step_index, int64_t* token_offset, uint8_t* hesitant,
+                    uint64_t* answer_off, char* answer_arena, uint64_t* program_off,
+                    char* program_arena, uint64_t* program_first, uint64_t* n_records,
+                    uint64_t* n_programs);
+
 /* ---- epsilon-accuracy stop test (alternative CoT stop rule) ----------------------------
  * probe::stationary_by_epsilon_test (probe.cpp:104-120) over theory::epsilon_stop_test
  * (theory.cpp:100-146).  Batched over CoT traces (ids u32[R][P], hes u64[R][ceil(P/64)],

@@ -286,7 +286,7 @@ class RefError(Exception):
 
 
 def _ref_err():
-    return ref().ref_last_error().decode()
+    return ref().ref_last_error().decode(errors="replace")
 
 
 def ref_cluster_exact(answers):
@@ -506,3 +506,24 @@ def ref_eps_prefixes(ids, hes, k, epsilon, vocab_list):
          _p(state)) < 0:
         raise RefError(_ref_err())
     return state
+
+
+def ref_parse_jsonl(text: bytes):
+    """The reference's read_trace_jsonl with every field: list of (program_id bytes,
+    step_index, token_offset, answer bytes, hesitant), or RefError with its message."""
+    n = len(text)
+    cap = text.count(b"\n") + 1
+    step = np.empty(cap, np.int32)
+    tok = np.empty(cap, np.int64)
+    hes = np.empty(cap, np.uint8)
+    pid = C.create_string_buffer(max(n, 1))
+    ans = C.create_string_buffer(max(n, 1))
+    po = np.empty(cap + 1, np.uint64)
+    ao = np.empty(cap + 1, np.uint64)
+    f = ref().ref_parse_jsonl
+    f.argtypes = [C.c_char_p, C.c_uint64, C.c_uint64, P, P, P, P, P, P, P]
+    r = f(text, n, cap, _p(step), _p(tok), _p(hes), pid, _p(po), ans, _p(ao))
+    if r < 0:
+        raise RefError(_ref_err())
+    return [(pid.raw[po[i]:po[i + 1]], int(step[i]), int(tok[i]), ans.raw[ao[i]:ao[i + 1]], bool(hes[i]))
+            for i in range(r)]

@@ -236,6 +236,36 @@ int ref_read_trace_jsonl(const char* text) {
     }
 }
 
+// read_trace_jsonl with every field returned (probe.cpp:126-165): strings packed with
+// offsets; returns the record count, -1 with the reference's message, or -2 if max is small.
+int ref_parse_jsonl(const char* text, uint64_t nbytes, uint64_t max, int32_t* step, int64_t* tok, uint8_t* hes,
+                    char* pid_buf, uint64_t* pid_off, char* ans_buf, uint64_t* ans_off) {
+    try {
+        std::istringstream in(std::string(text, nbytes));
+        const auto lines = pr::read_trace_jsonl(in);
+        if (lines.size() > max) return -2;
+        uint64_t po = 0, ao = 0;
+        pid_off[0] = 0;
+        ans_off[0] = 0;
+        for (size_t i = 0; i < lines.size(); ++i) {
+            const auto& l = lines[i];
+            step[i] = l.record.step_index;
+            tok[i] = l.record.token_offset;
+            hes[i] = l.record.hesitant ? 1 : 0;
+            std::memcpy(pid_buf + po, l.program_id.data(), l.program_id.size());
+            po += l.program_id.size();
+            pid_off[i + 1] = po;
+            std::memcpy(ans_buf + ao, l.record.answer.data(), l.record.answer.size());
+            ao += l.record.answer.size();
+            ans_off[i + 1] = ao;
+        }
+        return static_cast<int>(lines.size());
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return -1;
+    }
+}
+
 // update_certaindex through a real ProgramDriver (runtime.cpp:264-313) for an SC/MCTS/
 // Rebase synthetic spec: expand `units` one unit at a time, completing each request, and
 // record the signal vector after each unit.  Returns #points or -1.

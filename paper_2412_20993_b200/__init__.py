@@ -403,3 +403,23 @@ class Context:
         self._check(self.lib.cdx_cot_eps_stop(self.h, _ptr(ids), _ptr(hes), R, P, k, float(epsilon), _ptr(step),
                                               _ptr(state)))
         return step[:R], state
+
+    # -- JSONL trace ingestion (probe.cpp:126-165) --
+    def jsonl_parse(self, text_dev, cap_records: int):
+        """text_dev: uint8 device tensor with the JSON-lines bytes.  Returns a dict of device
+        tensors (records in line order) and the record / program counts."""
+        t = self.torch
+        nbytes = text_dev.numel()
+        cap = max(cap_records, 1)
+        out = dict(program=self.empty((cap,), t.int32), step_index=self.empty((cap,), t.int32),
+                   token_offset=self.empty((cap,), t.int64), hesitant=self.empty((cap,), t.uint8),
+                   answer_off=self.empty((cap + 1,), t.int64), answer_arena=self.empty((max(nbytes, 1),), t.uint8),
+                   program_off=self.empty((cap + 1,), t.int64), program_arena=self.empty((max(nbytes, 1),), t.uint8),
+                   program_first=self.empty((cap,), t.int64))
+        nr, npg = C.c_uint64(0), C.c_uint64(0)
+        self._bind_stream()
+        self._check(self.lib.cdx_jsonl_parse(self.h, _ptr(text_dev), nbytes, cap_records, *[_ptr(out[k]) for k in (
+            "program", "step_index", "token_offset", "hesitant", "answer_off", "answer_arena", "program_off",
+            "program_arena", "program_first")], C.byref(nr), C.byref(npg)))
+        out["n_records"], out["n_programs"] = nr.value, npg.value
+        return out

@@ -97,6 +97,7 @@ SIGNATURES = {
                                     C.POINTER(U64), P, P]),
     "cdx_gang_merge": (C.c_int, [P, P, P, U32, U64, P, P]),
     "cdx_offsets_rebase": (C.c_int, [P, P, U64, P, U32]),
+    "cdx_jsonl_parse": (C.c_int, [P, P, U64, U64, P, P, P, P, P, P, P, P, P, C.POINTER(U64), C.POINTER(U64)]),
     "cdx_cot_eps_stop": (C.c_int, [P, P, P, U64, U32, I32, C.c_double, P, P]),
     "cdx_probe_eps_stop_rows": (C.c_int, [P, P, P, P, U64, I32, C.c_double, P]),
     "cdx_sc_aggregate": (C.c_int, [P, P, U64, U32, U32, P, P]),

@@ -38,6 +38,9 @@ struct cdx_ctx {
     void* al_state = nullptr;
     size_t al_tiles = 0;      // capacity in tiles
     uint32_t al_epoch = 0;
+    // JSONL ingestion working buffer (k_jsonl.cu)
+    void* jl_buf = nullptr;
+    size_t jl_bytes = 0;
     // std::exp on the 2^-24 grid of [0,1] (Rebase aggregation), built on first use
     double* exp_tab = nullptr;
     // term-table cache (device): keyed by the list of n values it was built for
@@ -82,6 +85,11 @@ struct TermTables {
 };
 int build_term_tables(cdx_ctx* ctx, const uint32_t* ns, uint32_t count, TermTables* out);
 double host_term(uint32_t c, uint32_t n);
+// stable LSD radix sort of (u64 key, u32 value) (k_gang.cu); lb = radix_scratch_words(n)
+// u32 of device scratch; *which = 1 when the result is in (k1, v1)
+size_t radix_scratch_words(uint64_t n);
+int radix_sort_pairs(cdx_ctx* ctx, uint64_t* k0, uint32_t* v0, uint64_t* k1, uint32_t* v1, uint64_t n, uint32_t* lb,
+                     int* which);
 
 #define CDX_LAUNCHED(ctx) ((ctx)->launches++)
 

@@ -119,6 +119,7 @@ int build_term_tables(cdx_ctx* ctx, const uint32_t* ns, uint32_t count, TermTabl
         if (ctx->tt_dev) cudaFree(ctx->tt_dev);
     if (ctx->al_state) cudaFree(ctx->al_state);
     if (ctx->exp_tab) cudaFree(ctx->exp_tab);
+    if (ctx->jl_buf) cudaFree(ctx->jl_buf);
         ctx->tt_dev = nullptr;
         ctx->tt_bytes = 0;
         if (cudaMalloc(&ctx->tt_dev, bytes) != cudaSuccess) return set_error(ctx, CDX_ECUDA, "term table alloc");
@@ -191,6 +192,7 @@ int cdx_ctx_destroy(cdx_ctx* ctx) {
     if (ctx->tt_dev) cudaFree(ctx->tt_dev);
     if (ctx->al_state) cudaFree(ctx->al_state);
     if (ctx->exp_tab) cudaFree(ctx->exp_tab);
+    if (ctx->jl_buf) cudaFree(ctx->jl_buf);
     if (ctx->d_err) cudaFree(ctx->d_err);
     if (ctx->h_err) cudaFreeHost(ctx->h_err);
     if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);

@@ -448,6 +448,16 @@ __global__ void merge_rank(const uint64_t* __restrict__ keys, const uint64_t* __
 }
 
 }  // namespace
+
+// stable LSD radix sort of (u64 key, u32 value) pairs for other kernels (k_jsonl.cu)
+size_t radix_scratch_words(uint64_t n) {
+    return static_cast<size_t>(8) * 256 * ((n + RS_TILE - 1) / RS_TILE) + 8 * 256 + 16;
+}
+int radix_sort_pairs(cdx_ctx* ctx, uint64_t* k0, uint32_t* v0, uint64_t* k1, uint32_t* v1, uint64_t n, uint32_t* lb,
+                     int* which) {
+    return radix_sort(ctx, k0, v0, k1, v1, n, lb, which);
+}
+
 }  // namespace cdx
 
 extern "C" int cdx_gang_priority(cdx_ctx* ctx, const cdx_prog_soa* progs, uint64_t N, const cdx_inter_policy* pol,

@@ -1,0 +1,890 @@
+// k_jsonl.cu — probe-trace JSON-lines ingestion on the device:
+// probe::read_trace_jsonl (probe.cpp:126-165) for a whole trace file resident in HBM.
+//
+//   1. line split: newline positions by a chunked count / one-CTA scan / scatter (std::getline
+//      semantics: a trailing newline adds no empty line, a trailing partial line counts);
+//   2. one thread per line validates the line as RFC 8259 JSON (explicit container stack)
+//      with the rules of the host reader (facade_jsonl.cpp, pinned to the reference by the
+//      drop-in test): UTF-8 validated, raw control bytes rejected, \u escapes with surrogate
+//      pairs, no leading zeros, trailing bytes rejected, the LAST duplicate of a key wins;
+//      lines whose trim() is empty are skipped;
+//   3. the five fields are read in the reference's order (program_id, step_index,
+//      token_offset, answer, optional hesitant) with nlohmann's get<>() conversions (int
+//      accepts numbers and booleans, long only numbers; floats truncate);
+//   4. records are compacted in line order, program ids interned exactly (K1 on the
+//      sentinel-wrapped bytes, so trimming cannot merge ids) and every record is checked
+//      against the previous record of its program (stable radix sort by program): token
+//      offsets, then step indices, must strictly increase (probe.cpp:148-155);
+//   5. the first failing line (parse, field or order) wins, as the sequential reference
+//      stops there: "trace line <n>: invalid JSON" / "missing or mistyped field" /
+//      "token_offset does not increase" / "step_index does not increase".
+// Decimal fractions/exponents in the two integer fields are converted exactly on the
+// Clinger fast path (<= 19 significant digits with value < 2^53, |exp10| <= 22), which is
+// the correctly rounded double the reference's strtod yields; a number outside that range
+// in those fields is rejected ("unsupported number"), a documented restriction.
+
+#include <algorithm>
+#include <climits>
+#include <string>
+#include <vector>
+
+#include "cdx_internal.cuh"
+
+extern "C" int cdx_canon_intern(cdx_ctx* ctx, const char* bytes, const uint64_t* offsets, uint64_t n,
+                                const char* const* markers, uint32_t n_markers, uint32_t* ids, uint8_t* hes,
+                                uint64_t* first_index, uint64_t* n_unique);
+
+namespace cdx {
+namespace {
+
+constexpr uint32_t JL_CHUNK = 16384;  // bytes per CTA in the line split
+constexpr int JL_DEPTH = 64;          // nesting depth of the line validator
+
+enum LineState : uint8_t { L_RECORD = 0, L_BLANK = 1, L_BADJSON = 2, L_FIELD = 3, L_UNSUPPORTED = 4 };
+
+// ---- 1. line split ----------------------------------------------------------------------
+__global__ void nl_count(const char* __restrict__ t, uint64_t n, uint32_t* __restrict__ cnt) {
+    const uint64_t b = static_cast<uint64_t>(blockIdx.x) * JL_CHUNK;
+    const uint64_t e = min(b + JL_CHUNK, n);
+    uint32_t c = 0;
+    for (uint64_t i = b + threadIdx.x; i < e; i += blockDim.x) c += t[i] == '\n';
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+    __shared__ uint32_t s[32];
+    if ((threadIdx.x & 31) == 0) s[threadIdx.x >> 5] = c;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        uint32_t tot = 0;
+        for (uint32_t w = 0; w < blockDim.x / 32; ++w) tot += s[w];
+        cnt[blockIdx.x] = tot;
+    }
+}
+
+__global__ void excl_scan_one_cta(uint32_t* __restrict__ v, uint32_t n, uint64_t* __restrict__ total) {
+    __shared__ uint32_t ws[32];
+    __shared__ uint64_t carry;
+    if (threadIdx.x == 0) carry = 0;
+    __syncthreads();
+    const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    for (uint32_t b = 0; b < n; b += 1024) {
+        const uint32_t i = b + threadIdx.x;
+        const uint32_t x = i < n ? v[i] : 0u;
+        uint32_t inc = x;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
+            if (lane >= static_cast<uint32_t>(o)) inc += y;
+        }
+        if (lane == 31) ws[warp] = inc;
+        __syncthreads();
+        if (warp == 0) {
+            uint32_t w = ws[lane];
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t y = __shfl_up_sync(0xffffffffu, w, o);
+                if (lane >= static_cast<uint32_t>(o)) w += y;
+            }
+            ws[lane] = w;
+        }
+        __syncthreads();
+        if (i < n) v[i] = static_cast<uint32_t>(carry) + (warp ? ws[warp - 1] : 0u) + inc - x;
+        __syncthreads();
+        if (threadIdx.x == 0) carry += ws[31];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) *total = carry;
+}
+
+// newline positions in order: a block rescans its chunk, one warp-ballot rank per 32 bytes
+__global__ void nl_scatter(const char* __restrict__ t, uint64_t n, const uint32_t* __restrict__ base,
+                           uint64_t* __restrict__ pos) {
+    const uint64_t b = static_cast<uint64_t>(blockIdx.x) * JL_CHUNK;
+    const uint64_t e = min(b + JL_CHUNK, n);
+    __shared__ uint32_t s_run;
+    __shared__ uint32_t s_w[32];
+    if (threadIdx.x == 0) s_run = base[blockIdx.x];
+    __syncthreads();
+    const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    for (uint64_t r0 = b; r0 < e; r0 += blockDim.x) {  // rounds of blockDim bytes, in order
+        const uint64_t i = r0 + threadIdx.x;
+        const bool nl = i < e && t[i] == '\n';
+        const uint32_t m = __ballot_sync(0xffffffffu, nl);
+        if (lane == 0) s_w[warp] = __popc(m);
+        __syncthreads();
+        uint32_t before = s_run;
+        for (uint32_t w = 0; w < warp; ++w) before += s_w[w];
+        if (nl) pos[before + __popc(m & ((1u << lane) - 1u))] = i;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            uint32_t tot = 0;
+            for (uint32_t w = 0; w < blockDim.x / 32; ++w) tot += s_w[w];
+            s_run += tot;
+        }
+        __syncthreads();
+    }
+}
+
+// ---- 2./3. per-line parse -----------------------------------------------------------------
+struct Span {
+    uint64_t b = 0, e = 0;  // value token [b, e) (strings: inside the quotes)
+    uint8_t kind = 0;       // 0 absent, 1 string, 2 number, 3 true, 4 false, 5 null, 6 array, 7 object
+};
+
+__device__ __forceinline__ bool jws(char c) { return c == ' ' || c == '\t' || c == '\n' || c == '\r'; }
+__device__ __forceinline__ bool trim_ws(char c) {
+    return c == ' ' || c == '\t' || c == '\n' || c == '\r' || c == '\f' || c == '\v';
+}
+__device__ __forceinline__ int hexv(char c) {
+    if (c >= '0' && c <= '9') return c - '0';
+    if (c >= 'a' && c <= 'f') return c - 'a' + 10;
+    if (c >= 'A' && c <= 'F') return c - 'A' + 10;
+    return -1;
+}
+
+// Validate (and optionally decode) the string whose opening quote is at t[p]; returns the
+// index after the closing quote, or 0 on error.  out/len: decoded bytes (nullable out).
+__device__ uint64_t scan_string(const char* t, uint64_t p, uint64_t e, char* out, uint32_t out_cap,
+                                uint32_t* len) {
+    ++p;
+    uint32_t o = 0;
+    auto put = [&](uint32_t c) {
+        if (out && o < out_cap) out[o] = static_cast<char>(c);
+        ++o;
+    };
+    while (p < e) {
+        const unsigned char c = static_cast<unsigned char>(t[p]);
+        if (c == '"') {
+            if (len) *len = o;
+            return p + 1;
+        }
+        if (c < 0x20) return 0;
+        if (c == '\\') {
+            if (p + 1 >= e) return 0;
+            const char x = t[p + 1];
+            p += 2;
+            uint32_t cp;
+            switch (x) {
+                case '"': put('"'); continue;
+                case '\\': put('\\'); continue;
+                case '/': put('/'); continue;
+                case 'b': put('\b'); continue;
+                case 'f': put('\f'); continue;
+                case 'n': put('\n'); continue;
+                case 'r': put('\r'); continue;
+                case 't': put('\t'); continue;
+                case 'u': {
+                    if (p + 4 > e) return 0;
+                    cp = 0;
+                    for (int k = 0; k < 4; ++k) {
+                        const int h = hexv(t[p + k]);
+                        if (h < 0) return 0;
+                        cp = (cp << 4) | static_cast<uint32_t>(h);
+                    }
+                    p += 4;
+                    if (cp >= 0xD800 && cp <= 0xDBFF) {
+                        if (p + 6 > e || t[p] != '\\' || t[p + 1] != 'u') return 0;
+                        uint32_t lo = 0;
+                        for (int k = 0; k < 4; ++k) {
+                            const int h = hexv(t[p + 2 + k]);
+                            if (h < 0) return 0;
+                            lo = (lo << 4) | static_cast<uint32_t>(h);
+                        }
+                        if (lo < 0xDC00 || lo > 0xDFFF) return 0;
+                        p += 6;
+                        cp = 0x10000 + ((cp - 0xD800) << 10) + (lo - 0xDC00);
+                    } else if (cp >= 0xDC00 && cp <= 0xDFFF) {
+                        return 0;
+                    }
+                    if (cp < 0x80) {
+                        put(cp);
+                    } else if (cp < 0x800) {
+                        put(0xC0 | (cp >> 6));
+                        put(0x80 | (cp & 0x3F));
+                    } else if (cp < 0x10000) {
+                        put(0xE0 | (cp >> 12));
+                        put(0x80 | ((cp >> 6) & 0x3F));
+                        put(0x80 | (cp & 0x3F));
+                    } else {
+                        put(0xF0 | (cp >> 18));
+                        put(0x80 | ((cp >> 12) & 0x3F));
+                        put(0x80 | ((cp >> 6) & 0x3F));
+                        put(0x80 | (cp & 0x3F));
+                    }
+                    continue;
+                }
+                default: return 0;
+            }
+        }
+        int n;
+        uint32_t cp;
+        if (c < 0x80) n = 1, cp = c;
+        else if (c >= 0xC2 && c <= 0xDF) n = 2, cp = c & 0x1F;
+        else if (c >= 0xE0 && c <= 0xEF) n = 3, cp = c & 0x0F;
+        else if (c >= 0xF0 && c <= 0xF4) n = 4, cp = c & 0x07;
+        else return 0;
+        if (p + n > e) return 0;
+        for (int k = 1; k < n; ++k) {
+            const unsigned char cc = static_cast<unsigned char>(t[p + k]);
+            if ((cc & 0xC0) != 0x80) return 0;
+            cp = (cp << 6) | (cc & 0x3F);
+        }
+        if ((n == 3 && (cp < 0x800 || (cp >= 0xD800 && cp <= 0xDFFF))) || (n == 4 && (cp < 0x10000 || cp > 0x10FFFF)))
+            return 0;
+        for (int k = 0; k < n; ++k) put(static_cast<unsigned char>(t[p + k]));
+        p += n;
+    }
+    return 0;
+}
+
+// number token at t[p]: returns the end index or 0
+__device__ uint64_t scan_number(const char* t, uint64_t p, uint64_t e) {
+    if (p < e && t[p] == '-') ++p;
+    if (p >= e || t[p] < '0' || t[p] > '9') return 0;
+    if (t[p] == '0') {
+        ++p;
+        if (p < e && t[p] >= '0' && t[p] <= '9') return 0;
+    } else {
+        while (p < e && t[p] >= '0' && t[p] <= '9') ++p;
+    }
+    if (p < e && t[p] == '.') {
+        ++p;
+        if (p >= e || t[p] < '0' || t[p] > '9') return 0;
+        while (p < e && t[p] >= '0' && t[p] <= '9') ++p;
+    }
+    if (p < e && (t[p] == 'e' || t[p] == 'E')) {
+        ++p;
+        if (p < e && (t[p] == '+' || t[p] == '-')) ++p;
+        if (p >= e || t[p] < '0' || t[p] > '9') return 0;
+        while (p < e && t[p] >= '0' && t[p] <= '9') ++p;
+    }
+    return p;
+}
+
+// nlohmann number -> (int64 | uint64 | double); returns 0 int64, 1 uint64, 2 double, -1 unsupported
+__device__ int number_value(const char* t, uint64_t b, uint64_t e, long long* iv, unsigned long long* uv,
+                            double* dv) {
+    bool neg = false, is_float = false;
+    uint64_t p = b;
+    if (t[p] == '-') {
+        neg = true;
+        ++p;
+    }
+    for (uint64_t q = p; q < e; ++q)
+        if (t[q] == '.' || t[q] == 'e' || t[q] == 'E') is_float = true;
+    if (!is_float) {
+        unsigned long long v = 0;
+        bool ovf = false;
+        for (uint64_t q = p; q < e; ++q) {
+            const unsigned d = static_cast<unsigned>(t[q] - '0');
+            if (v > (ULLONG_MAX - d) / 10ull) ovf = true;
+            v = v * 10ull + d;
+        }
+        if (!ovf) {
+            if (!neg) {
+                *uv = v;
+                return 1;
+            }
+            if (v <= 0x8000000000000000ull) {  // strtoll range
+                *iv = v == 0x8000000000000000ull ? LLONG_MIN : -static_cast<long long>(v);
+                return 0;
+            }
+        }
+    }
+    // decimal -> double on the Clinger fast path (one correctly rounded IEEE op)
+    unsigned long long m = 0;
+    int digits = 0, exp10 = 0;
+    bool frac = false;
+    uint64_t q = p;
+    for (; q < e && t[q] != 'e' && t[q] != 'E'; ++q) {
+        if (t[q] == '.') {
+            frac = true;
+            continue;
+        }
+        const unsigned d = static_cast<unsigned>(t[q] - '0');
+        if (m == 0 && d == 0) {
+            if (frac) --exp10;
+            continue;
+        }
+        if (digits == 19) {  // more digits than the fast path can hold exactly
+            if (d != 0) return -1;
+            if (!frac) ++exp10;
+            continue;
+        }
+        m = m * 10ull + d;
+        ++digits;
+        if (frac) --exp10;
+    }
+    if (q < e) {  // exponent
+        ++q;
+        bool en = false;
+        if (t[q] == '+' || t[q] == '-') {
+            en = t[q] == '-';
+            ++q;
+        }
+        int x = 0;
+        for (; q < e; ++q) {
+            x = x * 10 + (t[q] - '0');
+            if (x > 100000) return -1;
+        }
+        exp10 += en ? -x : x;
+    }
+    if (m == 0) {
+        *dv = neg ? -0.0 : 0.0;
+        return 2;
+    }
+    if (m >= (1ull << 53) || exp10 < -22 || exp10 > 22) return -1;
+    double pw = 1.0;
+    for (int k = 0; k < (exp10 < 0 ? -exp10 : exp10); ++k) pw *= 10.0;  // exact for 10^k, k <= 22
+    double v = exp10 < 0 ? __ddiv_rn(static_cast<double>(m), pw) : __dmul_rn(static_cast<double>(m), pw);
+    *dv = neg ? -v : v;
+    return 2;
+}
+
+// C++ static_cast<int|long>(double) as x86-64 performs it (out of range -> INT/LONG min)
+__device__ __forceinline__ long long trunc_ll(double v) {
+    if (!(v > -9223372036854775808.0 && v < 9223372036854775808.0)) return LLONG_MIN;
+    return static_cast<long long>(v);
+}
+__device__ __forceinline__ int trunc_i(double v) {
+    if (!(v > -2147483649.0 && v < 2147483648.0)) return INT_MIN;
+    return static_cast<int>(v);
+}
+
+// key of interest: 0 program_id, 1 step_index, 2 token_offset, 3 answer, 4 hesitant, -1 other
+__device__ int key_id(const char* k, uint32_t n) {
+    auto eq = [&](const char* s, uint32_t sn) {
+        if (n != sn) return false;
+        for (uint32_t i = 0; i < n; ++i)
+            if (k[i] != s[i]) return false;
+        return true;
+    };
+    if (eq("program_id", 10)) return 0;
+    if (eq("step_index", 10)) return 1;
+    if (eq("token_offset", 12)) return 2;
+    if (eq("answer", 6)) return 3;
+    if (eq("hesitant", 8)) return 4;
+    return -1;
+}
+
+struct LineOut {
+    uint8_t* st;
+    uint64_t* pid_b;
+    uint64_t* pid_e;
+    uint64_t* ans_b;
+    uint64_t* ans_e;
+    int32_t* step;
+    int64_t* tok;
+    uint8_t* hes;
+};
+
+__global__ void parse_lines(const char* __restrict__ t, uint64_t n, const uint64_t* __restrict__ nl, uint64_t n_nl,
+                            uint64_t n_lines, LineOut o, unsigned long long* first_bad) {
+    for (uint64_t L = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; L < n_lines;
+         L += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+        const uint64_t b = L == 0 ? 0 : nl[L - 1] + 1;
+        const uint64_t e = L < n_nl ? nl[L] : n;
+        uint8_t st = L_RECORD;
+        // trim() empty -> skipped (probe.cpp:132)
+        uint64_t q = b;
+        while (q < e && trim_ws(t[q])) ++q;
+        if (q == e) {
+            o.st[L] = L_BLANK;
+            continue;
+        }
+        // ---- validate the document (iterative, explicit container stack)
+        Span f[5];
+        uint8_t stack[JL_DEPTH];
+        int depth = 0;
+        uint64_t p = b;
+        bool ok = true;
+        int pending_key = -2;  // key id of the member value about to be parsed (-2: none)
+        bool top_obj = false;
+        // states: 0 expect value, 1 after value, 2 expect key or '}', 3 expect key
+        int state = 0;
+        while (ok) {
+            while (p < e && jws(t[p])) ++p;
+            if (state == 0) {
+                if (p >= e) {
+                    ok = false;
+                    break;
+                }
+                const char c = t[p];
+                const uint64_t vb = p;
+                uint8_t kind = 0;
+                if (c == '{' || c == '[') {
+                    if (depth == JL_DEPTH) {
+                        ok = false;
+                        break;
+                    }
+                    if (depth == 0 && c == '{') top_obj = true;
+                    if (depth == 1 && top_obj && pending_key >= 0) f[pending_key] = Span{vb, vb, c == '{' ? uint8_t(7) : uint8_t(6)};
+                    pending_key = -2;
+                    stack[depth++] = c == '{' ? 1 : 2;
+                    ++p;
+                    state = c == '{' ? 2 : 0;
+                    if (c == '[') {  // empty array?
+                        uint64_t r = p;
+                        while (r < e && jws(t[r])) ++r;
+                        if (r < e && t[r] == ']') {
+                            p = r + 1;
+                            --depth;
+                            state = 1;
+                        }
+                    }
+                    continue;
+                }
+                if (c == '"') {
+                    const uint64_t r = scan_string(t, p, e, nullptr, 0, nullptr);
+                    if (!r) {
+                        ok = false;
+                        break;
+                    }
+                    kind = 1;
+                    if (depth == 1 && top_obj && pending_key >= 0) f[pending_key] = Span{vb + 1, r - 1, kind};
+                    p = r;
+                } else if (c == '-' || (c >= '0' && c <= '9')) {
+                    const uint64_t r = scan_number(t, p, e);
+                    if (!r) {
+                        ok = false;
+                        break;
+                    }
+                    if (depth == 1 && top_obj && pending_key >= 0) f[pending_key] = Span{vb, r, 2};
+                    p = r;
+                } else {
+                    const char* lit = c == 't' ? "true" : (c == 'f' ? "false" : (c == 'n' ? "null" : nullptr));
+                    if (!lit) {
+                        ok = false;
+                        break;
+                    }
+                    uint32_t ln = c == 'f' ? 5 : 4;
+                    if (p + ln > e) {
+                        ok = false;
+                        break;
+                    }
+                    for (uint32_t k = 0; k < ln; ++k) ok = ok && t[p + k] == lit[k];
+                    if (!ok) break;
+                    kind = c == 't' ? 3 : (c == 'f' ? 4 : 5);
+                    if (depth == 1 && top_obj && pending_key >= 0) f[pending_key] = Span{vb, p + ln, kind};
+                    p += ln;
+                }
+                pending_key = -2;
+                state = 1;
+                if (depth == 0) break;  // the top-level value was a scalar
+                continue;
+            }
+            if (state == 1) {  // after a value inside a container
+                if (depth == 0) break;
+                if (p >= e) {
+                    ok = false;
+                    break;
+                }
+                const char c = t[p];
+                if (c == ',') {
+                    ++p;
+                    state = stack[depth - 1] == 1 ? 3 : 0;
+                } else if ((c == '}' && stack[depth - 1] == 1) || (c == ']' && stack[depth - 1] == 2)) {
+                    ++p;
+                    --depth;
+                    state = 1;
+                    if (depth == 0) break;
+                } else {
+                    ok = false;
+                }
+                continue;
+            }
+            // state 2 / 3: a member key
+            if (p >= e) {
+                ok = false;
+                break;
+            }
+            if (state == 2 && t[p] == '}') {
+                ++p;
+                --depth;
+                state = 1;
+                if (depth == 0) break;
+                continue;
+            }
+            if (t[p] != '"') {
+                ok = false;
+                break;
+            }
+            char kb[16];
+            uint32_t kn = 0;
+            const uint64_t r = scan_string(t, p, e, kb, 16, &kn);
+            if (!r) {
+                ok = false;
+                break;
+            }
+            pending_key = (depth == 1 && top_obj && kn <= 16) ? key_id(kb, kn) : -1;
+            p = r;
+            while (p < e && jws(t[p])) ++p;
+            if (p >= e || t[p] != ':') {
+                ok = false;
+                break;
+            }
+            ++p;
+            state = 0;
+        }
+        if (ok) {  // trailing bytes
+            while (p < e && jws(t[p])) ++p;
+            ok = p == e;
+        }
+        if (!ok) {
+            st = L_BADJSON;
+        } else if (!top_obj) {
+            st = L_FIELD;  // at() on a non-object
+        } else {
+            // ---- fields in the reference's order (probe.cpp:140-145)
+            if (f[0].kind != 1) st = L_FIELD;
+            long long iv = 0;
+            unsigned long long uv = 0;
+            double dv = 0;
+            if (st == L_RECORD) {  // step_index: get<int>() (numbers and booleans)
+                if (f[1].kind == 3 || f[1].kind == 4) {
+                    o.step[L] = f[1].kind == 3 ? 1 : 0;
+                } else if (f[1].kind == 2) {
+                    const int k = number_value(t, f[1].b, f[1].e, &iv, &uv, &dv);
+                    if (k < 0) st = L_UNSUPPORTED;
+                    else o.step[L] = k == 0 ? static_cast<int>(iv) : (k == 1 ? static_cast<int>(uv) : trunc_i(dv));
+                } else {
+                    st = L_FIELD;
+                }
+            }
+            if (st == L_RECORD) {  // token_offset: get<long>() (numbers only)
+                if (f[2].kind == 2) {
+                    const int k = number_value(t, f[2].b, f[2].e, &iv, &uv, &dv);
+                    if (k < 0) st = L_UNSUPPORTED;
+                    else o.tok[L] = k == 0 ? iv : (k == 1 ? static_cast<long long>(uv) : trunc_ll(dv));
+                } else {
+                    st = L_FIELD;
+                }
+            }
+            if (st == L_RECORD && f[3].kind != 1) st = L_FIELD;
+            if (st == L_RECORD) {  // hesitant: value("hesitant", false) -> bool or absent
+                if (f[4].kind == 0) o.hes[L] = 0;
+                else if (f[4].kind == 3 || f[4].kind == 4) o.hes[L] = f[4].kind == 3;
+                else st = L_FIELD;
+            }
+            o.pid_b[L] = f[0].b;
+            o.pid_e[L] = f[0].e;
+            o.ans_b[L] = f[3].b;
+            o.ans_e[L] = f[3].e;
+        }
+        o.st[L] = st;
+        if (st != L_RECORD) atomicMin(first_bad, static_cast<unsigned long long>(L));
+    }
+}
+
+// ---- 4. compaction of records + decoded strings -------------------------------------------
+__global__ void flag_records(const uint8_t* __restrict__ st, uint64_t n_lines, uint32_t* __restrict__ f) {
+    for (uint64_t L = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; L < n_lines;
+         L += static_cast<uint64_t>(gridDim.x) * blockDim.x)
+        f[L] = st[L] == L_RECORD;
+}
+
+__global__ void add_block_base(uint32_t* __restrict__ v, uint64_t n, const uint32_t* __restrict__ sums) {
+    const uint64_t i = blockIdx.x * 1024ull + threadIdx.x;
+    if (i < n) v[i] += sums[blockIdx.x];
+}
+
+// exclusive scan of u32 within 1024-blocks; block totals to sums
+__global__ void scan_1024(uint32_t* __restrict__ v, uint64_t n, uint32_t* __restrict__ sums) {
+    __shared__ uint32_t ws[32];
+    const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const uint64_t i = blockIdx.x * 1024ull + threadIdx.x;
+    const uint32_t x = i < n ? v[i] : 0u;
+    uint32_t inc = x;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
+        if (lane >= static_cast<uint32_t>(o)) inc += y;
+    }
+    if (lane == 31) ws[warp] = inc;
+    __syncthreads();
+    if (warp == 0) {
+        uint32_t w = ws[lane];
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, w, o);
+            if (lane >= static_cast<uint32_t>(o)) w += y;
+        }
+        ws[lane] = w;
+    }
+    __syncthreads();
+    if (i < n) v[i] = (warp ? ws[warp - 1] : 0u) + inc - x;
+    if (threadIdx.x == 1023) sums[blockIdx.x] = ws[31];
+}
+
+// record r <- line L (st == record): fields + decoded string lengths
+__global__ void gather_records(const char* __restrict__ t, const uint8_t* __restrict__ st,
+                               const uint32_t* __restrict__ pos, uint64_t n_lines, LineOut o,
+                               int32_t* __restrict__ r_step, int64_t* __restrict__ r_tok, uint8_t* __restrict__ r_hes,
+                               uint64_t* __restrict__ r_line, uint32_t* __restrict__ pid_len,
+                               uint32_t* __restrict__ ans_len) {
+    for (uint64_t L = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; L < n_lines;
+         L += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+        if (st[L] != L_RECORD) continue;
+        const uint32_t r = pos[L];
+        r_step[r] = o.step[L];
+        r_tok[r] = o.tok[L];
+        r_hes[r] = o.hes[L];
+        r_line[r] = L;
+        uint32_t a = 0, b = 0;
+        scan_string(t, o.pid_b[L] - 1, o.pid_e[L] + 1, nullptr, 0, &a);
+        scan_string(t, o.ans_b[L] - 1, o.ans_e[L] + 1, nullptr, 0, &b);
+        pid_len[r] = a + 2;  // wrapped in sentinel bytes for exact interning
+        ans_len[r] = b;
+    }
+}
+
+__global__ void write_strings(const char* __restrict__ t, const uint8_t* __restrict__ st,
+                              const uint32_t* __restrict__ pos, uint64_t n_lines, LineOut o,
+                              const uint64_t* __restrict__ pid_off, char* __restrict__ pid_arena,
+                              const uint64_t* __restrict__ ans_off, char* __restrict__ ans_arena) {
+    for (uint64_t L = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; L < n_lines;
+         L += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+        if (st[L] != L_RECORD) continue;
+        const uint32_t r = pos[L];
+        char* pp = pid_arena + pid_off[r];
+        const uint32_t cap = static_cast<uint32_t>(pid_off[r + 1] - pid_off[r]);
+        pp[0] = '\x01';
+        uint32_t k = 0;
+        scan_string(t, o.pid_b[L] - 1, o.pid_e[L] + 1, pp + 1, cap - 2, &k);
+        pp[cap - 1] = '\x01';
+        scan_string(t, o.ans_b[L] - 1, o.ans_e[L] + 1, ans_arena + ans_off[r],
+                    static_cast<uint32_t>(ans_off[r + 1] - ans_off[r]), &k);
+    }
+}
+
+// ---- 4b. order check per program (probe.cpp:148-155) ------------------------------------
+__global__ void order_check(const uint32_t* __restrict__ sorted_rec, const uint64_t* __restrict__ keys,
+                            uint64_t n, const int32_t* __restrict__ step, const int64_t* __restrict__ tok,
+                            const uint64_t* __restrict__ line, unsigned long long* __restrict__ first_bad,
+                            uint8_t* __restrict__ why) {
+    for (uint64_t i = 1 + blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+        if (keys[i] != keys[i - 1]) continue;  // first record of its program
+        const uint32_t cur = sorted_rec[i], prev = sorted_rec[i - 1];
+        uint8_t w = 0;
+        if (tok[cur] <= tok[prev]) w = 1;
+        else if (step[cur] <= step[prev]) w = 2;
+        if (w) {
+            const unsigned long long L = line[cur];
+            atomicMin(first_bad, L);
+            why[cur] = w;
+        }
+    }
+}
+
+__global__ void shift_offsets(const uint32_t* __restrict__ excl, const uint32_t* __restrict__ len, uint64_t n,
+                              uint64_t* __restrict__ off) {
+    for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i <= n;
+         i += static_cast<uint64_t>(gridDim.x) * blockDim.x)
+        off[i] = i < n ? excl[i] : (n ? static_cast<uint64_t>(excl[n - 1]) + len[n - 1] : 0ull);
+}
+
+__global__ void widen_ids(const uint32_t* __restrict__ ids, uint64_t n, uint64_t* __restrict__ k,
+                          uint32_t* __restrict__ v) {
+    for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+        k[i] = ids[i];
+        v[i] = static_cast<uint32_t>(i);
+    }
+}
+
+// per-record program-id strings without the interning sentinels: record r's bytes start at
+// pid_off[r] + 1 in the wrapped arena and at pid_off[r] - 2r unwrapped
+__global__ void unwrap_pids(const uint64_t* __restrict__ pid_off, const char* __restrict__ wrapped, uint64_t n,
+                            uint64_t* __restrict__ off, char* __restrict__ arena) {
+    for (uint64_t r = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; r <= n;
+         r += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+        off[r] = pid_off[r] - 2 * r;
+        if (r == n) continue;
+        const uint64_t b = pid_off[r] + 1, e = pid_off[r + 1] - 1;
+        for (uint64_t i = b; i < e; ++i) arena[i - 2 * r - 1] = wrapped[i];
+    }
+}
+
+unsigned gridn(const cdx_ctx* ctx, uint64_t n) {
+    const uint64_t want = (n + 255) / 256;
+    const uint64_t cap = static_cast<uint64_t>(ctx->sm_count) * 16;
+    return static_cast<unsigned>(want < 1 ? 1 : (want < cap ? want : cap));
+}
+
+// exclusive scan of n u32 in place (<= 2^20 blocks of 1024), via block sums + one-CTA scan
+int scan_u32_inplace(cdx_ctx* ctx, uint32_t* v, uint64_t n, uint32_t* sums, uint64_t* total) {
+    const uint64_t nb = (n + 1023) / 1024;
+    scan_1024<<<static_cast<unsigned>(std::max<uint64_t>(nb, 1)), 1024, 0, ctx->stream>>>(v, n, sums);
+    CDX_CHECK_LAUNCH(ctx, "jsonl(scan)");
+    excl_scan_one_cta<<<1, 1024, 0, ctx->stream>>>(sums, static_cast<uint32_t>(nb), total);
+    CDX_CHECK_LAUNCH(ctx, "jsonl(scan sums)");
+    add_block_base<<<static_cast<unsigned>(std::max<uint64_t>(nb, 1)), 1024, 0, ctx->stream>>>(v, n, sums);
+    CDX_CHECK_LAUNCH(ctx, "jsonl(scan add)");
+    return CDX_OK;
+}
+
+template <typename T>
+T* carve(uint8_t*& p, uint64_t n) {
+    T* r = reinterpret_cast<T*>(p);
+    p += (n * sizeof(T) + 255) / 256 * 256;
+    return r;
+}
+
+}  // namespace
+}  // namespace cdx
+
+extern "C" int cdx_jsonl_parse(cdx_ctx* ctx, const char* text, uint64_t nbytes, uint64_t cap_records,
+                               uint32_t* program, int32_t* step_index, int64_t* token_offset, uint8_t* hesitant,
+                               uint64_t* answer_off, char* answer_arena, uint64_t* program_off,
+                               char* program_arena, uint64_t* program_first, uint64_t* n_records,
+                               uint64_t* n_programs) {
+    using namespace cdx;
+    if (!ctx) return CDX_EINVAL;
+    if (!n_records || !n_programs) return set_error(ctx, CDX_EINVAL, "jsonl_parse: null pointer");
+    *n_records = 0;
+    *n_programs = 0;
+    if (nbytes == 0) return CDX_OK;
+    if (!text || !program || !step_index || !token_offset || !hesitant || !answer_off || !answer_arena)
+        return set_error(ctx, CDX_EINVAL, "jsonl_parse: null pointer");
+    if (nbytes >= (1ull << 32)) return set_error(ctx, CDX_EINVAL, "jsonl_parse: at most 4 GiB per call");
+    const uint64_t nchunks = (nbytes + JL_CHUNK - 1) / JL_CHUNK;
+    // phase 1 (small scratch): newline count per chunk, then its scan
+    uint8_t* s1 = static_cast<uint8_t*>(scratch2(ctx, 4096 + nchunks * 4 + 256));
+    if (!s1) return set_error(ctx, CDX_ECUDA, "jsonl_parse: scratch allocation failed");
+    uint8_t* p1 = s1;
+    uint64_t* misc = carve<uint64_t>(p1, 16);  // [0] newlines, [1] first bad line, [2] records, [3] scan total
+    uint32_t* cnt = carve<uint32_t>(p1, nchunks);
+    cudaMemsetAsync(misc, 0, 16 * 8, ctx->stream);
+    cudaMemsetAsync(misc + 1, 0xff, 8, ctx->stream);
+    nl_count<<<static_cast<unsigned>(nchunks), 256, 0, ctx->stream>>>(text, nbytes, cnt);
+    CDX_CHECK_LAUNCH(ctx, "jsonl(lines)");
+    excl_scan_one_cta<<<1, 1024, 0, ctx->stream>>>(cnt, static_cast<uint32_t>(nchunks), misc);
+    CDX_CHECK_LAUNCH(ctx, "jsonl(lines scan)");
+    uint64_t h_nl = 0;
+    char last = 0;
+    cudaMemcpyAsync(&h_nl, misc, 8, cudaMemcpyDeviceToHost, ctx->stream);
+    cudaMemcpyAsync(&last, text + nbytes - 1, 1, cudaMemcpyDeviceToHost, ctx->stream);
+    cudaError_t e = cudaStreamSynchronize(ctx->stream);
+    if (e != cudaSuccess) return cuda_fail(ctx, e, "jsonl_parse");
+    const uint64_t n_lines = h_nl + (last == '\n' ? 0 : 1);  // std::getline semantics
+    // phase 2 (dedicated buffer sized from the line count): every later array is bounded by
+    // n_lines records and nbytes of text
+    const uint64_t nl1 = n_lines + 1;
+    const size_t bulk = 256 * 40 + nl1 * (8 + 1 + 8 * 4 + 4 + 8 + 1 + 4) + (nl1 / 1024 + 2) * 4 +
+                        nl1 * (8 + 4 + 4 + 8 + 1 + 8 + 8 + 4 + 4) + (3 * nbytes / 2 + 2 * nl1 + 64) +
+                        radix_scratch_words(nl1) * 4;
+    if (ctx->jl_bytes < bulk) {
+        cudaStreamSynchronize(ctx->stream);
+        if (ctx->jl_buf) cudaFree(ctx->jl_buf);
+        ctx->jl_buf = nullptr;
+        ctx->jl_bytes = 0;
+        if (cudaMalloc(&ctx->jl_buf, bulk) != cudaSuccess) return set_error(ctx, CDX_ECUDA, "jsonl_parse: allocation");
+        ctx->jl_bytes = bulk;
+    }
+    uint8_t* s = static_cast<uint8_t*>(ctx->jl_buf);
+    uint8_t* p = s;
+    const size_t bytes = bulk;
+    uint64_t* nl = carve<uint64_t>(p, h_nl + 1);
+    nl_scatter<<<static_cast<unsigned>(nchunks), 256, 0, ctx->stream>>>(text, nbytes, cnt, nl);
+    CDX_CHECK_LAUNCH(ctx, "jsonl(line ends)");
+    LineOut o;
+    o.st = carve<uint8_t>(p, n_lines);
+    o.pid_b = carve<uint64_t>(p, n_lines);
+    o.pid_e = carve<uint64_t>(p, n_lines);
+    o.ans_b = carve<uint64_t>(p, n_lines);
+    o.ans_e = carve<uint64_t>(p, n_lines);
+    o.step = carve<int32_t>(p, n_lines);
+    o.tok = carve<int64_t>(p, n_lines);
+    o.hes = carve<uint8_t>(p, n_lines);
+    uint32_t* pos = carve<uint32_t>(p, n_lines);
+    uint32_t* sums = carve<uint32_t>(p, (n_lines + 1023) / 1024 + 1);
+    parse_lines<<<gridn(ctx, n_lines), 128, 0, ctx->stream>>>(text, nbytes, nl, h_nl, n_lines, o,
+                                                              reinterpret_cast<unsigned long long*>(misc + 1));
+    CDX_CHECK_LAUNCH(ctx, "jsonl(parse)");
+    flag_records<<<gridn(ctx, n_lines), 256, 0, ctx->stream>>>(o.st, n_lines, pos);
+    CDX_CHECK_LAUNCH(ctx, "jsonl(flags)");
+    if (int st = scan_u32_inplace(ctx, pos, n_lines, sums, misc + 2)) return st;
+    uint64_t hm[2];
+    cudaMemcpyAsync(hm, misc + 1, 16, cudaMemcpyDeviceToHost, ctx->stream);
+    e = cudaStreamSynchronize(ctx->stream);
+    if (e != cudaSuccess) return cuda_fail(ctx, e, "jsonl_parse");
+    const uint64_t first_parse_bad = hm[0];
+    const uint64_t nr = hm[1];
+    if (nr > cap_records) return set_error(ctx, CDX_EINVAL, "jsonl_parse: more records than cap_records");
+    // records (line order) + decoded string sizes
+    uint64_t* r_line = carve<uint64_t>(p, nr + 1);
+    uint32_t* pid_len = carve<uint32_t>(p, nr + 1);
+    uint32_t* ans_len = carve<uint32_t>(p, nr + 1);
+    uint64_t* pid_off = carve<uint64_t>(p, nr + 1);
+    char* pid_arena = carve<char>(p, 3 * nbytes / 2 + 2 * nr + 64);
+    uint8_t* why = carve<uint8_t>(p, nr + 1);
+    uint64_t* k0 = carve<uint64_t>(p, nr + 1);
+    uint64_t* k1 = carve<uint64_t>(p, nr + 1);
+    uint32_t* v0 = carve<uint32_t>(p, nr + 1);
+    uint32_t* v1 = carve<uint32_t>(p, nr + 1);
+    uint32_t* lb = carve<uint32_t>(p, radix_scratch_words(nr + 1));
+    if (static_cast<size_t>(p - s) > bytes) return set_error(ctx, CDX_ECUDA, "jsonl_parse: scratch layout overflow");
+    if (nr) {
+        gather_records<<<gridn(ctx, n_lines), 128, 0, ctx->stream>>>(text, o.st, pos, n_lines, o, step_index,
+                                                                     token_offset, hesitant, r_line, pid_len, ans_len);
+        CDX_CHECK_LAUNCH(ctx, "jsonl(records)");
+        // arena offsets: exclusive scans of the decoded lengths
+        uint32_t* tmp = v0;  // reuse as scan space
+        cudaMemcpyAsync(tmp, ans_len, nr * 4, cudaMemcpyDeviceToDevice, ctx->stream);
+        if (int st = scan_u32_inplace(ctx, tmp, nr, sums, misc + 3)) return st;
+        shift_offsets<<<gridn(ctx, nr + 1), 256, 0, ctx->stream>>>(tmp, ans_len, nr, answer_off);
+        CDX_CHECK_LAUNCH(ctx, "jsonl(answer offsets)");
+        cudaMemcpyAsync(tmp, pid_len, nr * 4, cudaMemcpyDeviceToDevice, ctx->stream);
+        if (int st = scan_u32_inplace(ctx, tmp, nr, sums, misc + 3)) return st;
+        shift_offsets<<<gridn(ctx, nr + 1), 256, 0, ctx->stream>>>(tmp, pid_len, nr, pid_off);
+        CDX_CHECK_LAUNCH(ctx, "jsonl(program offsets)");
+        write_strings<<<gridn(ctx, n_lines), 128, 0, ctx->stream>>>(text, o.st, pos, n_lines, o, pid_off, pid_arena,
+                                                                    answer_off, answer_arena);
+        CDX_CHECK_LAUNCH(ctx, "jsonl(strings)");
+        // exact program interning (sentinel-wrapped: trimming cannot merge ids)
+        uint64_t np = 0;
+        if (int st = cdx_canon_intern(ctx, pid_arena, pid_off, nr, nullptr, 0, program, nullptr, program_first, &np))
+            return st;
+        *n_programs = np;
+        if (program_off && program_arena) {
+            unwrap_pids<<<gridn(ctx, nr + 1), 256, 0, ctx->stream>>>(pid_off, pid_arena, nr, program_off, program_arena);
+            CDX_CHECK_LAUNCH(ctx, "jsonl(program ids)");
+        }
+        // previous record of the same program: stable sort by program id
+        widen_ids<<<gridn(ctx, nr), 256, 0, ctx->stream>>>(program, nr, k0, v0);
+        CDX_CHECK_LAUNCH(ctx, "jsonl(keys)");
+        int which = 0;
+        if (int st = radix_sort_pairs(ctx, k0, v0, k1, v1, nr, lb, &which)) return st;
+        cudaMemsetAsync(why, 0, nr, ctx->stream);
+        order_check<<<gridn(ctx, nr), 256, 0, ctx->stream>>>(which ? v1 : v0, which ? k1 : k0, nr, step_index,
+                                                             token_offset, r_line,
+                                                             reinterpret_cast<unsigned long long*>(misc + 1), why);
+        CDX_CHECK_LAUNCH(ctx, "jsonl(order)");
+    }
+    uint64_t bad = 0;
+    cudaMemcpyAsync(&bad, misc + 1, 8, cudaMemcpyDeviceToHost, ctx->stream);
+    e = cudaStreamSynchronize(ctx->stream);
+    if (e != cudaSuccess) return cuda_fail(ctx, e, "jsonl_parse");
+    if (bad != ~0ull) {
+        std::string what;
+        if (bad == first_parse_bad) {
+            uint8_t stl = 0;
+            cudaMemcpy(&stl, o.st + bad, 1, cudaMemcpyDeviceToHost);
+            what = stl == L_BADJSON ? "invalid JSON"
+                                    : (stl == L_UNSUPPORTED ? "missing or mistyped field: unsupported number "
+                                                              "(outside the device parser's exact range)"
+                                                            : "missing or mistyped field");
+        } else {
+            // the order violation at line `bad`: find its record (records are in line order)
+            std::vector<uint64_t> lines(nr);
+            std::vector<uint8_t> w(nr);
+            cudaMemcpy(lines.data(), r_line, nr * 8, cudaMemcpyDeviceToHost);
+            cudaMemcpy(w.data(), why, nr, cudaMemcpyDeviceToHost);
+            const size_t r = static_cast<size_t>(std::lower_bound(lines.begin(), lines.end(), bad) - lines.begin());
+            what = (r < nr && w[r] == 2) ? "step_index does not increase" : "token_offset does not increase";
+        }
+        return set_error(ctx, CDX_ERUNTIME, "trace line " + std::to_string(bad + 1) + ": " + what);
+    }
+    *n_records = nr;
+    return CDX_OK;
+}

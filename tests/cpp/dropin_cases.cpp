@@ -303,6 +303,16 @@ void jsonl_cases() {
         "{\"program_id\":\"p\",\"step_index\":1,\"token_offset\":64,\"answer\":\"a\"} x\n",
         "{\"program_id\":\"p\",\"program_id\":\"r\",\"step_index\":-2,\"token_offset\":-9,\"answer\":\"\"}\n",
         "{\"program_id\":\"p\",\"step_index\":1,\"token_offset\":1e2,\"answer\":\"a\"}\n",
+        "{\"pro\\u0067ram_id\":\"p\",\"step_index\":1,\"token_offset\":2,\"answer\":\"c\"}\r\n"
+        "{\"program_id\":\" p\",\"step_index\":1,\"token_offset\":2,\"answer\":\"\\ud83d\\ude00\"}\n \f \n"
+        "{\"program_id\":\"p\",\"step_index\":2,\"token_offset\":3,\"answer\":\"caf\xc3\xa9\",\"x\":{\"y\":[[],{}]}}",
+        "{\"program_id\":\"p\",\"step_index\":1,\"token_offset\":64,\"answer\":\"a\\u0001\"}\n"
+        "{\"program_id\":\"p\",\"step_index\":1,\"token_offset\":64,\"answer\":\"a\x01\"}\n",
+        "{\"program_id\":\"q\",\"step_index\":5,\"token_offset\":9,\"answer\":\"a\"}\n"
+        "{\"program_id\":\"r\",\"step_index\":1,\"token_offset\":1,\"answer\":\"a\"}\n"
+        "{\"program_id\":\"q\",\"step_index\":5,\"token_offset\":10,\"answer\":\"b\"}\n",
+        "{\"program_id\":\"p\",\"step_index\":1,\"token_offset\":64,\"answer\":\"a\",}",
+        "{\"program_id\":\"p\",\"step_index\":-0,\"token_offset\":-9223372036854775808,\"answer\":\"\"}",
     };
     for (size_t d = 0; d < docs.size(); ++d) {
         run("jsonl " + std::to_string(d), [&] {

@@ -4,9 +4,9 @@ tests/cpp/dropin_cases.cpp is one caller written against the reference's headers
 compiled against the reference's own sources (oracle/_ref/dropin_ref, built where
 /root/reference lies) and against this repo (tests/cpp/bin/dropin_ours).  On the B200 the
 two must print identical lines: cluster labels and sizes, entropy / reward / consistency
-bits (hex floats), exit decisions, final answers, exception types and messages, JSONL
-round trips.  On the CPU the host-only JSONL part must already match, and every compute
-call of ours must fail loudly (no CPU fallback).
+bits (hex floats), exit decisions, final answers, epsilon tests, exception types and
+messages, JSONL round trips (parsed on the device).  On the CPU every compute call of ours
+must fail loudly (no CPU fallback).
 """
 import os
 import subprocess
@@ -46,18 +46,18 @@ def test_reference_build_reproduces_spec_examples():
     assert lines["spec should_exit aabaa"] == "1"  # ExitCertain
 
 
-def test_jsonl_io_matches_reference_on_host():
-    ref = [l for l in _run(REF, 1) if l.startswith("jsonl")]
-    ours = [l for l in _run(OURS, 1) if l.startswith("jsonl")]
-    assert len(ref) >= 10
-    assert ours == ref
+def test_jsonl_missing_file_matches_reference_on_host():
+    """Opening the file is host work in both builds (the parse itself runs on the device)."""
+    ref = [l for l in _run(REF, 1) if l.startswith("jsonl missing file")]
+    ours = [l for l in _run(OURS, 1) if l.startswith("jsonl missing file")]
+    assert len(ref) == 1 and ours == ref
 
 
 def test_no_cpu_fallback_without_device():
     if _cuda():
         pytest.skip("a CUDA device is present")
     lines = _run(OURS, 2)
-    compute = [l for l in lines if not l.startswith("jsonl") and "empty" not in l]
+    compute = [l for l in lines if not l.startswith("jsonl missing") and "empty" not in l]
     loud = [l for l in compute if "EXC runtime_error cdx: no usable sm_100 device" in l]
     # validation that the reference performs before any computation may still answer
     # (e.g. "cluster_exact: empty answer set"); everything that computes must refuse

@@ -1,0 +1,127 @@
+"""JSONL probe-trace ingestion on the device (cdx_jsonl_parse) vs the reference's own
+probe::read_trace_jsonl (probe.cpp:126-165) through oracle/_ref: every field of every
+record, the interned program ids, and the first failing line with its error category."""
+import numpy as np
+import pytest
+
+from oracle import oracle as O
+
+
+def _gen_trace(n_lines, n_programs, seed, bad=None):
+    rng = np.random.default_rng(seed)
+    step = {}
+    tok = {}
+    out = []
+    answers = ["12", " 12 ", "x", "wait, 13", "\\u00e9t\\u00e9", "a\\\"b", "tab\\there", "", "\\ud83d\\ude00",
+               "café", "  ", "HMM 7"]
+    for i in range(n_lines):
+        r = rng.random()
+        if r < 0.03:
+            out.append(["", "  ", "\t", " \f "][i % 4])
+            continue
+        p = f"prog-{int(rng.integers(0, n_programs))}"
+        if rng.random() < 0.05:
+            p = " " + p  # distinct program id (exact bytes, no trimming)
+        step[p] = step.get(p, 0) + 1 + int(rng.integers(0, 2))
+        tok[p] = tok.get(p, 0) + 1 + int(rng.integers(0, 100))
+        fields = [f'"program_id": "{p}"', f'"step_index": {step[p]}', f'"token_offset": {tok[p]}',
+                  f'"answer": "{answers[int(rng.integers(0, len(answers)))]}"']
+        if rng.random() < 0.5:
+            fields.append(f'"hesitant": {"true" if rng.random() < 0.2 else "false"}')
+        if rng.random() < 0.1:
+            fields.append('"extra": [1, {"k": null}, 2.5e3, "s"]')
+        if rng.random() < 0.05:
+            fields.insert(0, '"answer": "shadowed"')  # duplicate key: the last one wins
+        rng.shuffle(fields)
+        sep = ", " if rng.random() < 0.5 else ","
+        out.append("{" + sep.join(fields) + "}" + ("\r" if rng.random() < 0.05 else ""))
+    text = "\n".join(out) + ("\n" if seed % 2 else "")
+    return text.encode()
+
+
+def _parse_gpu(ctx, text):
+    import torch
+    t = torch.frombuffer(bytearray(text), dtype=torch.uint8).cuda() if text else torch.empty(0, dtype=torch.uint8,
+                                                                                            device="cuda")
+    out = ctx.jsonl_parse(t, text.count(b"\n") + 1)
+    ctx.sync()
+    n = out["n_records"]
+    ao = out["answer_off"][: n + 1].cpu().numpy()
+    po = out["program_off"][: n + 1].cpu().numpy()
+    aa = out["answer_arena"].cpu().numpy().tobytes()
+    pa = out["program_arena"].cpu().numpy().tobytes()
+    st = out["step_index"][:n].cpu().numpy()
+    tk = out["token_offset"][:n].cpu().numpy()
+    hs = out["hesitant"][:n].cpu().numpy()
+    recs = [(pa[po[i]:po[i + 1]], int(st[i]), int(tk[i]), aa[ao[i]:ao[i + 1]], bool(hs[i])) for i in range(n)]
+    return recs, out["program"][:n].cpu().numpy(), out["n_programs"]
+
+
+def _category(msg):
+    for cat in ("invalid JSON", "missing or mistyped field"):
+        if cat in msg:
+            return msg[: msg.index(cat) + len(cat)]
+    return msg
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("n,progs,seed", [(1, 1, 0), (200, 5, 1), (5000, 300, 2), (50000, 4000, 3)])
+def test_jsonl_matches_reference(ctx, n, progs, seed):
+    text = _gen_trace(n, progs, seed)
+    ref = O.ref_parse_jsonl(text)
+    got, pid, npg = _parse_gpu(ctx, text)
+    assert got == ref
+    # program ids: dense, first-seen, equal id <=> equal bytes
+    first = {}
+    want = [first.setdefault(r[0], len(first)) for r in ref]
+    assert pid.tolist() == want and npg == len(first)
+
+
+BAD = [
+    b'{"program_id":"p","step_index":1,"token_offset":64,"answer":"a"}\n{"program_id":"p","step_index":2,"token_offset":64,"answer":"b"}\n',
+    b'{"program_id":"p","step_index":3,"token_offset":64,"answer":"a"}\n{"program_id":"q","step_index":1,"token_offset":1,"answer":"b"}\n{"program_id":"p","step_index":3,"token_offset":65,"answer":"b"}\n',
+    b'{"program_id":"p","step_index":1,"token_offset":64,"answer":"a"\n',
+    b'\n\n{"program_id":"p","step_index":1,"token_offset":64}\n',
+    b'{"program_id":7,"step_index":1,"token_offset":64,"answer":"a"}',
+    b'{"program_id":"p","step_index":true,"token_offset":64,"answer":"a"}\n{"program_id":"p","step_index":1,"token_offset":true,"answer":"a"}',
+    b'{"program_id":"p","step_index":1,"token_offset":64,"answer":"a","hesitant":1}',
+    b'[1,2,3]',
+    b'{"program_id":"p","step_index":01,"token_offset":64,"answer":"a"}',
+    b'{"program_id":"p","step_index":1,"token_offset":64,"answer":"a"} x',
+    b'{"program_id":"p","step_index":1,"token_offset":64,"answer":"a\x01"}',
+    b'{"program_id":"p","step_index":1,"token_offset":64,"answer":"\\ud800"}',
+    b'{"program_id":"p","step_index":1,"token_offset":64,"answer":"\xc3"}',
+    b'{"program_id":"p","step_index":1,"token_offset":64,"answer":"a",}',
+    b'{"program_id":"p","program_id":"r","step_index":-2,"token_offset":-9,"answer":""}\n{"program_id":"r","step_index":-1,"token_offset":-9,"answer":""}',
+    b'{"program_id":"p","step_index":1.9,"token_offset":64.5,"answer":"a","hesitant":false}\n{"program_id":"p","step_index":1e1,"token_offset":1E2,"answer":"b"}',
+    b'{"pro\\u0067ram_id":"p","step_index":1,"token_offset":2,"answer":"c"}\n{"program_id":"p","step_index":1,"token_offset":3,"answer":"c"}',
+    b'  {"program_id":"p","step_index":1,"token_offset":64,"answer":"a"}  \r\n\t\n{}',
+]
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("i", range(len(BAD)))
+def test_jsonl_edge_cases_match_reference(ctx, i):
+    from paper_2412_20993_b200 import CdxError
+    text = BAD[i]
+    try:
+        ref = O.ref_parse_jsonl(text)
+        ref_err = None
+    except O.RefError as e:
+        ref, ref_err = None, str(e)
+    try:
+        got, _, _ = _parse_gpu(ctx, text)
+        err = None
+    except CdxError as e:
+        got, err = None, str(e)
+    assert (err is None) == (ref_err is None), (err, ref_err)
+    if ref_err is None:
+        assert got == ref
+    else:
+        assert _category(err) == _category(ref_err)
+
+
+@pytest.mark.gpu
+def test_jsonl_empty_and_blank(ctx):
+    assert _parse_gpu(ctx, b"")[0] == []
+    assert _parse_gpu(ctx, b"\n \n\t\n")[0] == O.ref_parse_jsonl(b"\n \n\t\n") == []
