@@ -17,7 +17,7 @@ allgather of shard budget totals for global token offsets.  Time = max over rank
 
 Metric: probe-evals/s.  One probe-eval = one sampled answer (r,s,p) entering the certaindex
 for SC (A, C), one probe record (r,p) for CoT (B), one node reward (g,t,w) for MCTS/Rebase
-(D), one program ordered for the gang order (E).  `--impl reference` times the reference's
+(D), one program ordered for the gang order (E), one trace record ingested (J).  `--impl reference` times the reference's
 own C++ functions (oracle/_ref, compiled from /root/reference/proj/src) on all host cores.
 """
 from __future__ import annotations
@@ -48,12 +48,14 @@ CONFIGS = {
               desc="MCTS/Rebase reward + cumulative entropy certaindex, 256K programs x 64 nodes x 16 steps"),
     "E": dict(kind="gang", N=1 << 22, limit=0.5, prior=128.0,
               desc="gang-scheduling priority order (escalation + SJF + tie-break), 4M mixed programs"),
+    "J": dict(kind="jsonl", lines=1 << 20, programs=1 << 14,
+              desc="probe-trace JSONL ingestion (read_trace_jsonl), 1M records over 16K programs"),
 }
 TH_MCTS = [(0, 0.99, 0), (1, 0.4, 0)]   # PAPER.md:963 MCTS/GSM8K thresholds
 TH_REBASE = [(0, 0.85, 0), (1, 0.99, 0)]  # PAPER.md:966 Rebase/GSM8K thresholds
 
 
-TRAFFIC_KEY = {"sc": "sc", "cot": "cot", "reward": "reward", "gang": "gang"}
+TRAFFIC_KEY = {"sc": "sc", "cot": "cot", "reward": "reward", "gang": "gang", "jsonl": "jsonl"}
 
 
 def load_traffic(kind):
@@ -257,12 +259,44 @@ def cpu_gang(cfg, nth, N, seed):
     return N / dt, dt, f"{N} programs, {dt:.2f} s (SPEC restatement, 1 thread)"
 
 
-CPU = {"sc": cpu_sc, "cot": cpu_cot, "reward": cpu_reward, "gang": cpu_gang}
-CPU_SAMPLE = {"A": 1024, "B": 1 << 16, "C": 1 << 18, "D": 1 << 14, "E": 1 << 20}
+def jsonl_text(lines, programs, seed):
+    """Synthetic probe trace in the reference's JSONL schema (probe.hpp:12-14): programs
+    interleaved, per-program strictly increasing step/offset, ~5% hesitant probes."""
+    import numpy as np
+    rng = np.random.default_rng(seed)
+    prog = rng.integers(0, programs, lines)
+    ans = rng.integers(0, 5, lines)
+    hes = rng.random(lines) < 0.05
+    step = np.zeros(programs, np.int64)
+    names = ["S", "D1", "D2", "D3", "D4"]
+    out = []
+    for i in range(lines):
+        p = int(prog[i])
+        step[p] += 1
+        s = int(step[p])
+        a = ("wait, " if hes[i] else "") + names[int(ans[i])]
+        out.append(f'{{"program_id": "prog-{p}", "step_index": {s}, "token_offset": {64 * s}, "answer": "{a}", '
+                   f'"hesitant": {"true" if hes[i] else "false"}}}')
+    return ("\n".join(out) + "\n").encode()
+
+
+def cpu_jsonl(cfg, nth, lines, seed):
+    """The reference's read_trace_jsonl (nlohmann parse + checks) on one thread: it is a
+    single sequential stream in the reference (probe.cpp:126-165)."""
+    from oracle import oracle as O
+    text = jsonl_text(lines, max(1, cfg["programs"] * lines // cfg["lines"]), seed)
+    t0 = time.perf_counter()
+    n = O.ref_read_trace_jsonl(text)
+    dt = time.perf_counter() - t0
+    return n / dt, dt, f"{n} records ({len(text)} bytes), {dt:.2f} s (1 thread: one sequential stream)"
+
+
+CPU = {"sc": cpu_sc, "cot": cpu_cot, "reward": cpu_reward, "gang": cpu_gang, "jsonl": cpu_jsonl}
+CPU_SAMPLE = {"A": 1024, "B": 1 << 16, "C": 1 << 18, "D": 1 << 14, "E": 1 << 20, "J": 1 << 17}
 
 
 def cpu_baseline(name, cfg, sample=None):
-    nth = host_threads() if cfg["kind"] != "gang" else 1
+    nth = host_threads() if cfg["kind"] not in ("gang", "jsonl") else 1
     n = sample or CPU_SAMPLE[name]
     v, dt, note = CPU[cfg["kind"]](cfg, nth, n, 20993 + 1)
     kind = "port" if cfg["kind"] == "gang" else "reference"
@@ -275,7 +309,7 @@ def run_reference(args, cfg, rank, world):
         return
     vals = []
     n = args.ref_sample or CPU_SAMPLE[args.config]
-    nth = host_threads() if cfg["kind"] != "gang" else 1
+    nth = host_threads() if cfg["kind"] not in ("gang", "jsonl") else 1
     note = ""
     for i in range(args.warmup + args.steps):
         v, dt, note = CPU[cfg["kind"]](cfg, nth, n, 20993 + i)
@@ -502,7 +536,30 @@ def bench_gang(args, cfg, rank, world, cx, with_e2e=True):
                 scaling="strong")
 
 
-BENCH = {"sc": bench_sc, "cot": bench_cot, "reward": bench_reward, "gang": bench_gang}
+def bench_jsonl(args, cfg, rank, world, cx, with_e2e=True):
+    """Config J: device-resident JSONL text -> parsed, checked, interned records."""
+    import torch
+    text = jsonl_text(cfg["lines"], cfg["programs"], 20993 + 6 + rank)
+    dev = torch.frombuffer(bytearray(text), dtype=torch.uint8).cuda()
+    cap = cfg["lines"] + 1
+    out = {}
+
+    def step(seg):
+        e = seg_events(seg, "jsonl_parse")
+        out.update(cx.jsonl_parse(dev, cap))
+        if e is not None:
+            e.record(torch.cuda.current_stream())
+
+    l0 = cx.launches
+    ms, per, clocks = timed(args, world, step, ["jsonl_parse"])
+    n = out["n_records"]
+    b = len(text) + n * (4 + 4 + 8 + 1 + 8 + 8) + n * 8
+    return dict(value=n * world / (ms / 1e3), ms=ms, launches=in_timed(cx, l0, args), clocks=clocks,
+                kernel="jsonl_parse (all passes)", kernel_ms=per["jsonl_parse"], kernel_bytes=b, step_bytes=b,
+                extra={"text_bytes": len(text)}, e2e=None)
+
+
+BENCH = {"sc": bench_sc, "cot": bench_cot, "reward": bench_reward, "gang": bench_gang, "jsonl": bench_jsonl}
 
 
 def summarize(name, cfg, res, peak):

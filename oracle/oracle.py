@@ -375,7 +375,7 @@ def ref_final_answer(records, terminated_at=None, reason=1):
 
 
 def ref_read_trace_jsonl(text):
-    r = ref().ref_read_trace_jsonl(text.encode())
+    r = ref().ref_read_trace_jsonl(text.encode() if isinstance(text, str) else text)
     if r < 0:
         raise RefError(_ref_err())
     return r
@@ -525,5 +525,6 @@ def ref_parse_jsonl(text: bytes):
     r = f(text, n, cap, _p(step), _p(tok), _p(hes), pid, _p(po), ans, _p(ao))
     if r < 0:
         raise RefError(_ref_err())
-    return [(pid.raw[po[i]:po[i + 1]], int(step[i]), int(tok[i]), ans.raw[ao[i]:ao[i + 1]], bool(hes[i]))
+    praw, araw = pid.raw, ans.raw
+    return [(praw[po[i]:po[i + 1]], int(step[i]), int(tok[i]), araw[ao[i]:ao[i + 1]], bool(hes[i]))
             for i in range(r)]

@@ -131,17 +131,40 @@ __global__ void scan_blocks(uint32_t* __restrict__ v, uint64_t n, uint32_t* __re
     if (i < n) v[i] = s[threadIdx.x] - x;  // exclusive within the block
     if (threadIdx.x == SCAN_T - 1) block_sums[blockIdx.x] = s[threadIdx.x];
 }
+// exclusive scan of the block sums by one CTA (1024 per round), total -> *total
 __global__ void scan_sums(uint32_t* __restrict__ sums, uint64_t nb, uint32_t* __restrict__ total) {
-    // one thread: nb = n / 512 is small (<= 8M)
-    if (threadIdx.x == 0 && blockIdx.x == 0) {
-        uint32_t acc = 0;
-        for (uint64_t b = 0; b < nb; ++b) {
-            const uint32_t x = sums[b];
-            sums[b] = acc;
-            acc += x;
+    __shared__ uint32_t ws[32];
+    __shared__ uint32_t carry;
+    if (threadIdx.x == 0) carry = 0;
+    __syncthreads();
+    const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    for (uint64_t b = 0; b < nb; b += 1024) {
+        const uint64_t i = b + threadIdx.x;
+        const uint32_t x = i < nb ? sums[i] : 0u;
+        uint32_t inc = x;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
+            if (lane >= static_cast<uint32_t>(o)) inc += y;
         }
-        *total = acc;
+        if (lane == 31) ws[warp] = inc;
+        __syncthreads();
+        if (warp == 0) {
+            uint32_t w = ws[lane];
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t y = __shfl_up_sync(0xffffffffu, w, o);
+                if (lane >= static_cast<uint32_t>(o)) w += y;
+            }
+            ws[lane] = w;
+        }
+        __syncthreads();
+        if (i < nb) sums[i] = carry + (warp ? ws[warp - 1] : 0u) + inc - x;
+        __syncthreads();
+        if (threadIdx.x == 0) carry += ws[31];
+        __syncthreads();
     }
+    if (threadIdx.x == 0) *total = carry;
 }
 __global__ void intern_finish(uint64_t n, const uint32_t* __restrict__ excl, const uint32_t* __restrict__ sums,
                               const uint32_t* __restrict__ first, const uint32_t* __restrict__ slot_of,
@@ -203,7 +226,7 @@ extern "C" int cdx_canon_intern(cdx_ctx* ctx, const char* bytes, const uint64_t*
     CDX_CHECK_LAUNCH(ctx, "canon_intern(verify)");
     scan_blocks<<<static_cast<unsigned>(nb), SCAN_T, 0, ctx->stream>>>(flags, n, sums);
     CDX_CHECK_LAUNCH(ctx, "canon_intern(scan)");
-    scan_sums<<<1, 32, 0, ctx->stream>>>(sums, nb, total);
+    scan_sums<<<1, 1024, 0, ctx->stream>>>(sums, nb, total);
     CDX_CHECK_LAUNCH(ctx, "canon_intern(scan sums)");
     intern_finish<<<grid, 256, 0, ctx->stream>>>(n, flags, sums, first, slot_of, ids,
                                                   reinterpret_cast<unsigned long long*>(first_index));

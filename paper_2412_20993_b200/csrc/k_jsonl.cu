@@ -43,11 +43,37 @@ constexpr int JL_DEPTH = 64;          // nesting depth of the line validator
 enum LineState : uint8_t { L_RECORD = 0, L_BLANK = 1, L_BADJSON = 2, L_FIELD = 3, L_UNSUPPORTED = 4 };
 
 // ---- 1. line split ----------------------------------------------------------------------
+// Thread t of a CTA owns the contiguous 64 bytes [chunk + 64t, +64) (256 x 64 = JL_CHUNK),
+// read as four 16-byte loads when the text is 16-byte aligned.
+constexpr uint32_t JL_PER_THREAD = 64;
+
+__device__ __forceinline__ uint64_t nl_mask64(const char* __restrict__ t, uint64_t b, uint64_t n) {
+    uint64_t m = 0;
+    if (b + JL_PER_THREAD <= n && (reinterpret_cast<uintptr_t>(t + b) & 15u) == 0) {
+#pragma unroll
+        for (int v = 0; v < 4; ++v) {
+            const uint4 x = __ldg(reinterpret_cast<const uint4*>(t + b) + v);
+            const uint32_t w[4] = {x.x, x.y, x.z, x.w};
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                // bytes equal to '\n' (0x0a): zero-byte test on w ^ 0x0a0a0a0a, per byte exact
+                const uint32_t y = w[k] ^ 0x0a0a0a0au;
+                uint32_t z = ((y & 0x7f7f7f7fu) + 0x7f7f7f7fu) | y;
+                z = ~(z | 0x7f7f7f7fu);  // bit 7 of each byte set iff that byte is '\n'
+                const uint32_t bits = ((z >> 7) & 1u) | ((z >> 14) & 2u) | ((z >> 21) & 4u) | ((z >> 28) & 8u);
+                m |= static_cast<uint64_t>(bits) << (v * 16 + k * 4);
+            }
+        }
+    } else {
+        for (uint32_t i = 0; i < JL_PER_THREAD && b + i < n; ++i)
+            if (t[b + i] == '\n') m |= 1ull << i;
+    }
+    return m;
+}
+
 __global__ void nl_count(const char* __restrict__ t, uint64_t n, uint32_t* __restrict__ cnt) {
-    const uint64_t b = static_cast<uint64_t>(blockIdx.x) * JL_CHUNK;
-    const uint64_t e = min(b + JL_CHUNK, n);
-    uint32_t c = 0;
-    for (uint64_t i = b + threadIdx.x; i < e; i += blockDim.x) c += t[i] == '\n';
+    const uint64_t b = static_cast<uint64_t>(blockIdx.x) * JL_CHUNK + threadIdx.x * JL_PER_THREAD;
+    uint32_t c = b < n ? __popcll(nl_mask64(t, b, n)) : 0u;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
     __shared__ uint32_t s[32];
@@ -95,32 +121,27 @@ __global__ void excl_scan_one_cta(uint32_t* __restrict__ v, uint32_t n, uint64_t
     if (threadIdx.x == 0) *total = carry;
 }
 
-// newline positions in order: a block rescans its chunk, one warp-ballot rank per 32 bytes
+// newline positions in order: each thread's 64-byte mask, a block scan of the counts
 __global__ void nl_scatter(const char* __restrict__ t, uint64_t n, const uint32_t* __restrict__ base,
                            uint64_t* __restrict__ pos) {
-    const uint64_t b = static_cast<uint64_t>(blockIdx.x) * JL_CHUNK;
-    const uint64_t e = min(b + JL_CHUNK, n);
-    __shared__ uint32_t s_run;
     __shared__ uint32_t s_w[32];
-    if (threadIdx.x == 0) s_run = base[blockIdx.x];
-    __syncthreads();
     const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    for (uint64_t r0 = b; r0 < e; r0 += blockDim.x) {  // rounds of blockDim bytes, in order
-        const uint64_t i = r0 + threadIdx.x;
-        const bool nl = i < e && t[i] == '\n';
-        const uint32_t m = __ballot_sync(0xffffffffu, nl);
-        if (lane == 0) s_w[warp] = __popc(m);
-        __syncthreads();
-        uint32_t before = s_run;
-        for (uint32_t w = 0; w < warp; ++w) before += s_w[w];
-        if (nl) pos[before + __popc(m & ((1u << lane) - 1u))] = i;
-        __syncthreads();
-        if (threadIdx.x == 0) {
-            uint32_t tot = 0;
-            for (uint32_t w = 0; w < blockDim.x / 32; ++w) tot += s_w[w];
-            s_run += tot;
-        }
-        __syncthreads();
+    const uint64_t b = static_cast<uint64_t>(blockIdx.x) * JL_CHUNK + threadIdx.x * JL_PER_THREAD;
+    uint64_t m = b < n ? nl_mask64(t, b, n) : 0ull;
+    const uint32_t c = __popcll(m);
+    uint32_t inc = c;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
+        if (lane >= static_cast<uint32_t>(o)) inc += y;
+    }
+    if (lane == 31) s_w[warp] = inc;
+    __syncthreads();
+    uint32_t before = base[blockIdx.x] + inc - c;
+    for (uint32_t w = 0; w < warp; ++w) before += s_w[w];
+    while (m) {
+        pos[before++] = b + static_cast<uint64_t>(__ffsll(static_cast<long long>(m)) - 1);
+        m &= m - 1;
     }
 }
 
