@@ -38,8 +38,9 @@ UNIT = "probe-evals/s"
 
 CONFIGS = {
     # BASELINE.json configs; C is the north_star target shape (sharded per GPU)
-    "A": dict(kind="sc", R=1024, P=32, S=16, tau=0.7, detect=5, cap=32, interval=64, conv_hi=32,
-              desc="SC entropy certaindex early exit, 1024 queries x 16 samples x 32 probes"),
+    "A": dict(kind="sc", R=1024, P=32, S=16, tau=0.7, detect=5, cap=32, interval=64, conv_hi=32, graph=True,
+              desc="SC entropy certaindex early exit, 1024 queries x 16 samples x 32 probes (K2 + K5 replayed as "
+                   "one CUDA graph: launch-bound size)"),
     "B": dict(kind="cot", R=1 << 20, P=64, w=3, tau=0.9, interval=64, max_tokens=4096, hes=0.05, conv_hi=64,
               desc="CoT probe-window consistency early exit, 1M requests x 64 probes, window 3"),
     "C": dict(kind="sc", R=1 << 20, P=64, S=32, tau=0.7, detect=5, cap=64, interval=64, conv_hi=64,
@@ -400,6 +401,18 @@ def bench_sc(args, cfg, rank, world, cx, with_e2e=True):
         if world > 1:  # global token offsets: allgather of shard budget totals (8 B/rank) + rebase
             totals = sh.allgather(out["scalars"][2:3])
             cx.offsets_rebase(out["offsets"], totals, rank)
+
+    if cfg.get("graph") and world == 1:
+        # launch-bound size: capture K2 + K5 once, replay the graph (one launch per step)
+        g = cx.graph_capture(lambda: step(None))
+
+        def step(seg):  # noqa: F811 - the timed step is the graph replay
+            e = seg_events(seg, "sc_certaindex")
+            g()
+            if e is not None:
+                e.record(torch.cuda.current_stream())
+            if seg is not None:
+                seg["allocate_scan"].append(seg["sc_certaindex"][-1])
 
     l0 = cx.launches
     ms, per, clocks = timed(args, world, step, ["sc_certaindex", "allocate_scan"])

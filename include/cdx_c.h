@@ -147,6 +147,16 @@ int cdx_abi_version(void);
 /* Number of kernel launches this context has issued (the bench's gpu_launches count). */
 uint64_t cdx_launch_count(const cdx_ctx* ctx);
 
+/* ---- CUDA graphs: capture a sequence of cdx_* calls on the context stream and replay it
+ * with one launch (small, launch-bound batches).  The stream must not be a default stream;
+ * calls that synchronise with the host (buffer growth, canon_intern, gang_priority, jsonl)
+ * cannot be captured.  Captured calls replay on the same buffers with the same arguments. */
+typedef struct cdx_graph cdx_graph;
+int cdx_graph_begin(cdx_ctx* ctx);
+int cdx_graph_end(cdx_ctx* ctx, cdx_graph** out);
+int cdx_graph_launch(cdx_ctx* ctx, cdx_graph* g);
+int cdx_graph_destroy(cdx_graph* g);
+
 /* ---- synthetic trace generation on the device (runtime.cpp:91-117 restated) ------- */
 int cdx_gen_sc(cdx_ctx* ctx, const cdx_gen_params* g, uint64_t r0, uint64_t R, uint32_t P,
                uint32_t S, uint32_t* ids);

@@ -423,3 +423,34 @@ class Context:
             "program_arena", "program_first")], C.byref(nr), C.byref(npg)))
         out["n_records"], out["n_programs"] = nr.value, npg.value
         return out
+
+    # -- CUDA graphs of call sequences (launch-bound small batches) --
+    def graph_capture(self, fn):
+        """Capture fn() (a sequence of Context calls) on a side stream into a replayable
+        graph; returns a callable that replays it on torch's current stream."""
+        t = self.torch
+        side = t.cuda.Stream(device=self.dev)
+        side.wait_stream(t.cuda.current_stream(self.dev))
+        with t.cuda.stream(side):
+            fn()  # warm: allocations and table builds happen outside the capture
+            self.sync()
+            self._bind_stream()
+            self._check(self.lib.cdx_graph_begin(self.h))
+            try:
+                fn()
+            finally:
+                g = C.c_void_p()
+                st = self.lib.cdx_graph_end(self.h, C.byref(g))
+            self._check(st)
+        t.cuda.current_stream(self.dev).wait_stream(side)
+        ctx = self
+
+        class _Graph:
+            def __call__(self):
+                ctx._bind_stream()
+                ctx._check(ctx.lib.cdx_graph_launch(ctx.h, g))
+
+            def __del__(self):
+                ctx.lib.cdx_graph_destroy(g)
+
+        return _Graph()

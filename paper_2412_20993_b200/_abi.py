@@ -70,6 +70,10 @@ SIGNATURES = {
     "cdx_sync": (C.c_int, [P]),
     "cdx_last_error": (C.c_char_p, [P]),
     "cdx_launch_count": (U64, [P]),
+    "cdx_graph_begin": (C.c_int, [P]),
+    "cdx_graph_end": (C.c_int, [P, C.POINTER(P)]),
+    "cdx_graph_launch": (C.c_int, [P, P]),
+    "cdx_graph_destroy": (C.c_int, [P]),
     "cdx_gen_sc": (C.c_int, [P, C.POINTER(GenParams), U64, U64, U32, U32, P]),
     "cdx_gen_cot": (C.c_int, [P, C.POINTER(GenParams), U64, U64, U32, P, P]),
     "cdx_gen_reward": (C.c_int, [P, C.POINTER(GenParams), U64, U64, U32, U32, P, P]),

@@ -20,6 +20,7 @@ struct cdx_ctx {
     cudaStream_t stream = nullptr;
     std::string err;
     uint64_t launches = 0;
+    uint64_t graph_mark = 0;  // launches before the current graph capture
     // device error word: 0 ok, else a CDX_E* code set by a kernel (validated on sync)
     int* d_err = nullptr;
     int* h_err = nullptr;  // pinned mirror
@@ -37,7 +38,6 @@ struct cdx_ctx {
     // aggregates, tagged with a per-call epoch so nothing is cleared between calls
     void* al_state = nullptr;
     size_t al_tiles = 0;      // capacity in tiles
-    uint32_t al_epoch = 0;
     // JSONL ingestion working buffer (k_jsonl.cu)
     void* jl_buf = nullptr;
     size_t jl_bytes = 0;

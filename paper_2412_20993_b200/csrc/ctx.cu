@@ -242,3 +242,57 @@ int cdx_sync(cdx_ctx* ctx) {
 }
 
 }  // extern "C"
+
+// ---- CUDA graphs of a call sequence on the context stream (launch-bound small batches) ----
+struct cdx_graph {
+    cudaGraph_t graph = nullptr;
+    cudaGraphExec_t exec = nullptr;
+    uint64_t launches = 0;  // kernels per replay (for cdx_launch_count)
+};
+
+extern "C" {
+
+int cdx_graph_begin(cdx_ctx* ctx) {
+    if (!ctx) return CDX_EINVAL;
+    if (ctx->stream == nullptr || ctx->stream == cudaStreamLegacy || ctx->stream == cudaStreamPerThread)
+        return cdx::set_error(ctx, CDX_EINVAL, "graph: capture needs a non-default stream (cdx_ctx_set_stream)");
+    ctx->graph_mark = ctx->launches;
+    cudaError_t e = cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal);
+    if (e != cudaSuccess) return cdx::cuda_fail(ctx, e, "graph: begin capture");
+    return CDX_OK;
+}
+
+int cdx_graph_end(cdx_ctx* ctx, cdx_graph** out) {
+    if (!ctx || !out) return CDX_EINVAL;
+    *out = nullptr;
+    auto* g = new cdx_graph();
+    cudaError_t e = cudaStreamEndCapture(ctx->stream, &g->graph);
+    if (e == cudaSuccess) e = cudaGraphInstantiate(&g->exec, g->graph, 0);
+    if (e != cudaSuccess) {
+        if (g->graph) cudaGraphDestroy(g->graph);
+        delete g;
+        return cdx::cuda_fail(ctx, e, "graph: end capture / instantiate");
+    }
+    g->launches = ctx->launches - ctx->graph_mark;
+    ctx->launches = ctx->graph_mark;  // captured launches count when replayed
+    *out = g;
+    return CDX_OK;
+}
+
+int cdx_graph_launch(cdx_ctx* ctx, cdx_graph* g) {
+    if (!ctx || !g) return CDX_EINVAL;
+    cudaError_t e = cudaGraphLaunch(g->exec, ctx->stream);
+    if (e != cudaSuccess) return cdx::cuda_fail(ctx, e, "graph: launch");
+    ctx->launches += g->launches;
+    return CDX_OK;
+}
+
+int cdx_graph_destroy(cdx_graph* g) {
+    if (!g) return CDX_OK;
+    if (g->exec) cudaGraphExecDestroy(g->exec);
+    if (g->graph) cudaGraphDestroy(g->graph);
+    delete g;
+    return CDX_OK;
+}
+
+}  // extern "C"

@@ -3,8 +3,8 @@
 // launches (decoupled look-back scan: each tile publishes its aggregate, then resolves its
 // exclusive prefix from its predecessors' published state, 32 tiles per look-back step;
 // tiles take tickets from a persistent counter so every predecessor is resident or done —
-// the last tile to finish rewinds it — and per-call epochs tag the tile records, so
-// nothing is cleared between calls).
+// the last tile to finish rewinds it and advances a device-side epoch that tags the tile
+// records, so nothing is cleared between calls and a captured CUDA graph replays correctly).
 //
 // Semantics restated from SPEC.md:404-412 (scheduler.allocate; no reference code exists):
 //   even               -> grant to the cap
@@ -43,11 +43,11 @@ struct AllocParams {
     uint64_t* n_kept;
     int64_t* tokens_saved;
     int64_t* total_budget;
-    uint32_t* tickets;  // [0] tile tickets, [1] finished tiles; the last tile resets both
+    uint32_t* tickets;  // [0] tile tickets, [1] finished tiles, [2] epoch; the last tile resets
+                        // [0] and [1] and advances [2]
     AlTile* tiles;
     uint64_t R;
     uint32_t ntiles;
-    uint32_t epoch;
     uint32_t words;      // meets words per request
     uint32_t chk_words;  // words that hold a test point (the rest is never read)
     int32_t cap, detect;
@@ -95,7 +95,11 @@ __global__ void __launch_bounds__(AL_THREADS) allocate_scan_kernel(const __grid_
     __shared__ uint32_t s_excl_k;
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    if (tid == 0) s_tile = atomicAdd(&p.tickets[0], 1u);
+    __shared__ uint32_t s_epoch;
+    if (tid == 0) {
+        s_tile = atomicAdd(&p.tickets[0], 1u);
+        s_epoch = ld_acquire(&p.tickets[2]);  // constant until every tile of this call is done
+    }
     __syncthreads();
     const uint32_t tile = s_tile;
     if (tile >= p.ntiles) __trap();  // a stale ticket counter must fail loudly, never scribble
@@ -156,7 +160,7 @@ __global__ void __launch_bounds__(AL_THREADS) allocate_scan_kernel(const __grid_
 
         // ---- decoupled look-back over earlier tiles, 32 at a time
         AlTile* T = p.tiles;
-        const uint32_t ep = p.epoch << 2;
+        const uint32_t ep = (s_epoch & 0x3fffffffu) << 2;
         if (lane == 0) {
             if (tile == 0) {  // the first tile's aggregate is its inclusive prefix
                 T[0].inc_b = tot_b;
@@ -237,6 +241,7 @@ __global__ void __launch_bounds__(AL_THREADS) allocate_scan_kernel(const __grid_
         if (atomicAdd(&p.tickets[1], 1u) == p.ntiles - 1) {
             p.tickets[0] = 0;
             p.tickets[1] = 0;
+            p.tickets[2] = (p.tickets[2] + 1u) & 0x3fffffffu;  // next call's records are new
             __threadfence();
         }
     }
@@ -296,7 +301,7 @@ extern "C" int cdx_allocate_scan(cdx_ctx* ctx, const uint32_t* meets_bits, uint6
     p.ntiles = static_cast<uint32_t>((R + AL_TILE - 1) / AL_TILE);
     // persistent look-back state: zeroed only when (re)allocated; every call uses a new
     // epoch and a fresh range of tickets, so no per-call clearing launches are needed
-    if (ctx->al_tiles < p.ntiles || ctx->al_epoch >= (1u << 29)) {
+    if (ctx->al_tiles < p.ntiles) {
         cudaStreamSynchronize(ctx->stream);
         if (ctx->al_state) cudaFree(ctx->al_state);
         ctx->al_state = nullptr;
@@ -307,11 +312,9 @@ extern "C" int cdx_allocate_scan(cdx_ctx* ctx, const uint32_t* meets_bits, uint6
         }
         cudaMemsetAsync(ctx->al_state, 0, 256 + cap_tiles * sizeof(AlTile), ctx->stream);
         ctx->al_tiles = cap_tiles;
-        ctx->al_epoch = 0;
     }
     p.tickets = static_cast<uint32_t*>(ctx->al_state);
     p.tiles = reinterpret_cast<AlTile*>(static_cast<uint8_t*>(ctx->al_state) + 256);
-    p.epoch = ++ctx->al_epoch;
     p.chk_words = 0;
     for (uint32_t w = 0; w < p.words; ++w)
         if (p.chk[w]) p.chk_words = w + 1;

@@ -165,3 +165,41 @@ def test_sc_many_clusters_fallback(ctx, distinct):
     _, oh32, om = O.sc_certaindex(ids, [(SIG_E, 0.1, GE)])
     assert np.array_equal(h.cpu().numpy().view(np.uint32), oh32.view(np.uint32))
     assert np.array_equal(m.cpu().numpy().view(np.uint32), om)
+
+
+def test_graph_replay_of_sc_step(ctx):
+    """A captured K2 + K5 step (config A shape) replays bit-identically, replay after replay
+    (K5's look-back records are tagged by a device-side epoch, so replays never see stale
+    records), and its kernels count in cdx_launch_count."""
+    import torch
+    from paper_2412_20993_b200 import AllocPolicy, Threshold
+    R, P, S = 1024, 32, 16
+    ids = ctx.gen_sc(_gp(seed=21, conv_hi=32), R, P, S)
+    ths = [Threshold(SIG_E, 0.7, GE)]
+    pol = AllocPolicy(kind=2, detect_at=5, resource_cap=32, tokens_per_unit=64 * S)
+    hc = torch.empty((R, P), dtype=torch.float32, device="cuda")
+    mt = torch.empty((R, 1), dtype=torch.int32, device="cuda")
+    out = {k: torch.empty((R,), dtype=dt, device="cuda") for k, dt in
+           (("exit_knob", torch.int32), ("reason", torch.uint8), ("granted", torch.int32), ("offsets", torch.int64),
+            ("kept", torch.int32))}
+    out["scalars"] = torch.zeros((3,), dtype=torch.int64, device="cuda")
+
+    def step():
+        ctx.sc_certaindex(ids, ths, hcert=hc, meets=mt)
+        ctx.allocate_scan(mt, R, P, pol, base_offset=7, out=out)
+
+    g = ctx.graph_capture(step)
+    _, _, om = O.sc_certaindex(O.gen_sc(_og(seed=21, conv_hi=32), R, P, S), [(SIG_E, 0.7, GE)])
+    ref = O.allocate_scan(om, R, P, 2, 5, 32, 1, 64 * S, base_offset=7)
+    for _ in range(3):
+        for k in out:
+            if k != "scalars":
+                out[k].fill_(-1)
+        l0 = ctx.launches
+        g()
+        ctx.sync()
+        assert ctx.launches > l0
+        for k in ("exit_knob", "reason", "granted", "offsets"):
+            assert np.array_equal(out[k].cpu().numpy(), ref[k].astype(out[k].cpu().numpy().dtype)), k
+        assert int(out["scalars"][0]) == ref["n_kept"]
+        assert np.array_equal(mt.cpu().numpy().view(np.uint32), om)
