@@ -11,6 +11,10 @@
 //   reward_certaindex  K4  cumulative certaindex_reward (+ entropy) per (program, step)
 //   canon_intern       K1  trim + intern + flag_hesitation over a string arena
 //   gang_priority      K6  escalate + estimate + next_batch program order (radix sort)
+//   sc_aggregate / reward_aggregate   final answers per archetype (runtime.cpp:316-403)
+//   cot_eps_stop       the epsilon-accuracy stop rule at every CoT prefix (probe.cpp:104-120)
+//   jsonl_parse        probe-trace JSONL ingestion (probe.cpp:126-165)
+//   Graph              capture / replay of a call sequence (launch-bound small batches)
 
 #include <cstddef>
 #include <cstdint>
@@ -157,5 +161,68 @@ uint64_t canon_intern(Context& cx, const char* arena, const uint64_t* offsets, u
 uint64_t gang_priority(Context& cx, const cdx_prog_soa& progs, uint64_t n,
                        const scheduler::InterSchedPolicy& policy, double now, uint32_t* order,
                        uint8_t* escalated, uint64_t* keys);
+
+// ---- aggregation (runtime.cpp:316-403) ---------------------------------------------------
+
+// SC plurality over each request's exit row (exit_knob i32[R], 1-based) -> answer u32[R]
+void sc_aggregate(Context& cx, const uint32_t* ids, const ScShape& shape, const int32_t* exit_knob,
+                  uint32_t* answer);
+// MCTS first argmax / Rebase exp-weighted plurality at exit step t (0-based); returns the
+// number of rewards off the 2^-24 grid (whose exp used the device's exp)
+uint64_t reward_aggregate(Context& cx, const float* rewards, const uint32_t* ids, const uint8_t* agg,
+                          uint64_t programs, uint32_t steps, uint32_t width, const int32_t* exit_step,
+                          uint32_t* answer);
+
+// ---- epsilon-accuracy stop test (probe.cpp:104-120) -----------------------------------------
+
+// eps_step i32[R] = first probe where the test holds (-1 none); state u8[R][P] nullable
+void cot_eps_stop(Context& cx, const uint32_t* ids, const uint64_t* hes, uint64_t requests, uint32_t probes,
+                  int k, double epsilon, int32_t* eps_step, uint8_t* state);
+
+// ---- JSONL ingestion (probe.cpp:126-165) ----------------------------------------------------
+
+struct JsonlRecords {
+    uint32_t* program = nullptr;       // u32[cap] interned program ids (first-seen, dense)
+    int32_t* step_index = nullptr;     // i32[cap]
+    int64_t* token_offset = nullptr;   // i64[cap]
+    uint8_t* hesitant = nullptr;       // u8[cap]
+    uint64_t* answer_off = nullptr;    // u64[cap + 1]
+    char* answer_arena = nullptr;      // nbytes
+    uint64_t* program_off = nullptr;   // u64[cap + 1] (nullable with program_arena)
+    char* program_arena = nullptr;     // nbytes
+    uint64_t* program_first = nullptr; // u64[cap] (nullable)
+};
+
+// text: device bytes; returns {records, programs}; throws std::runtime_error("trace line n: ...")
+std::pair<uint64_t, uint64_t> jsonl_parse(Context& cx, const char* text, uint64_t nbytes, uint64_t cap_records,
+                                          const JsonlRecords& out);
+
+// ---- CUDA graphs ---------------------------------------------------------------------------
+
+class Graph {
+public:
+    // Captures the calls fn makes on cx (its stream must not be a default stream).
+    template <class F>
+    Graph(Context& cx, F&& fn) : cx_(&cx) {
+        cx.check(cdx_graph_begin(cx.raw()));
+        try {
+            fn();
+        } catch (...) {
+            cdx_graph* g = nullptr;
+            cdx_graph_end(cx.raw(), &g);
+            cdx_graph_destroy(g);
+            throw;
+        }
+        cx.check(cdx_graph_end(cx.raw(), &g_));
+    }
+    ~Graph() { cdx_graph_destroy(g_); }
+    Graph(const Graph&) = delete;
+    Graph& operator=(const Graph&) = delete;
+    void launch() { cx_->check(cdx_graph_launch(cx_->raw(), g_)); }
+
+private:
+    Context* cx_;
+    cdx_graph* g_ = nullptr;
+};
 
 }  // namespace cdx::batch

@@ -128,6 +128,30 @@ uint64_t gang_priority(Context& cx, const cdx_prog_soa& progs, uint64_t n, const
     return n_out;
 }
 
+void sc_aggregate(Context& cx, const uint32_t* ids, const ScShape& s, const int32_t* exit_knob, uint32_t* answer) {
+    cx.check(cdx_sc_aggregate(cx.raw(), ids, s.requests, s.probes, s.samples, exit_knob, answer));
+}
+
+uint64_t reward_aggregate(Context& cx, const float* rewards, const uint32_t* ids, const uint8_t* agg, uint64_t G,
+                          uint32_t T, uint32_t W, const int32_t* exit_step, uint32_t* answer) {
+    DeviceArray<uint64_t> inexact(cx, 1);
+    cx.check(cdx_reward_aggregate(cx.raw(), rewards, ids, agg, G, T, W, exit_step, answer, inexact.data()));
+    return inexact.download()[0];
+}
+
+void cot_eps_stop(Context& cx, const uint32_t* ids, const uint64_t* hes, uint64_t R, uint32_t P, int k,
+                  double epsilon, int32_t* eps_step, uint8_t* state) {
+    cx.check(cdx_cot_eps_stop(cx.raw(), ids, hes, R, P, k, epsilon, eps_step, state));
+}
+
+std::pair<uint64_t, uint64_t> jsonl_parse(Context& cx, const char* text, uint64_t nbytes, uint64_t cap,
+                                          const JsonlRecords& o) {
+    uint64_t nr = 0, np = 0;
+    cx.check(cdx_jsonl_parse(cx.raw(), text, nbytes, cap, o.program, o.step_index, o.token_offset, o.hesitant,
+                             o.answer_off, o.answer_arena, o.program_off, o.program_arena, o.program_first, &nr, &np));
+    return {nr, np};
+}
+
 }  // namespace cdx::batch
 
 namespace cdx::detail {
