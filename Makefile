@@ -20,7 +20,7 @@ HHDRS   := $(wildcard $(PKG)/csrc/host/*.hpp) include/cdx_c.h $(wildcard include
 HOSTCXX := g++
 CXXFLAGS_HOST := -std=c++20 -O2 -fPIC -Wall -Wextra -Iinclude
 
-DROPIN  := tests/cpp/bin/dropin_ours tests/cpp/bin/scheduler_cases tests/cpp/bin/batch_pipeline
+DROPIN  := tests/cpp/bin/dropin_ours tests/cpp/bin/scheduler_cases tests/cpp/bin/batch_pipeline tests/cpp/bin/sim_cases
 
 all: lib oracle dropin
 

@@ -364,6 +364,14 @@ __global__ void __launch_bounds__(RQ_PROGS * 4) reward_quad_kernel(const __grid_
     bool ovf = !live;
     const uint32_t qmask = 0xFu << (lane & ~3u);
     uint32_t before = 0;  // this lane's hits on valid slots so far (a miss = fewer new hits than nodes)
+    struct {
+        double tot;
+        uint32_t mx, m, t;
+        uint32_t tc[RW_KM];
+        bool ovf, valid;
+    } pend{};
+    for (uint32_t i = tid; i < RQ_PROGS * p.words; i += blockDim.x) outM[i] = 0;  // bits land by atomicOr
+    __syncthreads();
 
     uint32_t stage = 0, phase = 0;
     for (uint32_t t = 0; t < T; ++t) {
@@ -377,69 +385,74 @@ __global__ void __launch_bounds__(RQ_PROGS * 4) reward_quad_kernel(const __grid_
 #pragma unroll
             for (int k = 0; k < RW_KM; ++k) after += static_cast<uint32_t>(k) < m ? L.cnt[k] : 0u;
             const bool miss = after - before < per_lane;
-            // ---- first-seen insertion.  Each round, every lane finds its earliest node (in
-            // node order) whose value is in no valid slot; the quad's earliest such node is
-            // the next cluster in first-seen order: all 4 lanes append it, then each counts its
-            // own occurrences of it.  Rounds run until no quad of the warp has a miss left
-            // (warp-uniform loop; quads without work idle), one round per new cluster.
+            // ---- first-seen insertion.  One scan marks this lane's nodes whose value is in no
+            // valid slot (a bit per node, ascending node order); each round the quad takes its
+            // earliest marked node (the next cluster in first-seen order), all 4 lanes append
+            // it, and each lane counts and clears its own marked nodes holding that value.
+            // Rounds run while any quad of the warp has marks (warp-uniform loop).
             bool need = (__ballot_sync(0xffffffffu, miss && !ovf) & qmask) != 0;  // quad-uniform
-            while (__any_sync(0xffffffffu, need)) {
-                uint32_t wmin = 0xffffffffu, vmin = 0;
+            if (__any_sync(0xffffffffu, need)) {
+                constexpr int NV = 8 * BOXES;  // this lane's nodes per step
+                uint32_t iv[NV];
+                uint32_t mk = 0;  // bit i: own node i (node w = b*32 + h*16 + q*4 + e, i = (2b+h)*4 + e)
+#pragma unroll
+                for (uint32_t j = 0; j < 2 * BOXES; ++j) {
+                    const uint32_t b = j >> 1, h = j & 1u;
+                    const uint4 u = *reinterpret_cast<const uint4*>(si + b * box_bytes + swz128(prow, h * 4u + q));
+                    iv[4 * j] = u.x;
+                    iv[4 * j + 1] = u.y;
+                    iv[4 * j + 2] = u.z;
+                    iv[4 * j + 3] = u.w;
+                }
                 if (need) {
 #pragma unroll
-                    for (uint32_t j = 0; j < 2 * BOXES; ++j) {  // own nodes, ascending w
-                        const uint32_t b = j >> 1, h = j & 1u;
-                        const uint4 u = *reinterpret_cast<const uint4*>(si + b * box_bytes + swz128(prow, h * 4u + q));
-                        const uint32_t iv[4] = {u.x, u.y, u.z, u.w};
+                    for (int i = 0; i < NV; ++i) {
+                        bool in = false;  // unused slots duplicate key 0, so no validity test
 #pragma unroll
-                        for (int e = 0; e < 4; ++e) {
-                            bool in = false;  // unused slots duplicate key 0, so no validity test
+                        for (int k = 0; k < RW_KM; ++k) in = in || L.key[k] == iv[i];
+                        if (!(in && m > 0)) mk |= 1u << i;
+                    }
+                }
+                while (__any_sync(0xffffffffu, need)) {
+                    uint32_t wmin = 0xffffffffu, vmin = 0;
+                    if (mk) {
+                        const uint32_t i = static_cast<uint32_t>(__ffs(mk) - 1);
+                        wmin = (i >> 3) * 32u + ((i >> 2) & 1u) * 16u + q * 4u + (i & 3u);
 #pragma unroll
-                            for (int k = 0; k < RW_KM; ++k) in = in || L.key[k] == iv[e];
-                            in = in && m > 0;
-                            const uint32_t w = b * 32u + h * 16u + q * 4u + static_cast<uint32_t>(e);
-                            if (!in && w < wmin) {
-                                wmin = w;
-                                vmin = iv[e];
-                            }
+                        for (int k = 0; k < NV; ++k)
+                            if (static_cast<uint32_t>(k) == i) vmin = iv[k];
+                    }
+#pragma unroll
+                    for (int o = 1; o <= 2; o <<= 1) {  // quad min over (w, value of w)
+                        const uint32_t w2 = __shfl_xor_sync(0xffffffffu, wmin, o);
+                        const uint32_t v2 = __shfl_xor_sync(0xffffffffu, vmin, o);
+                        if (w2 < wmin) {
+                            wmin = w2;
+                            vmin = v2;
                         }
                     }
-                }
-#pragma unroll
-                for (int o = 1; o <= 2; o <<= 1) {  // quad min over (w, value of w)
-                    const uint32_t w2 = __shfl_xor_sync(0xffffffffu, wmin, o);
-                    const uint32_t v2 = __shfl_xor_sync(0xffffffffu, vmin, o);
-                    if (w2 < wmin) {
-                        wmin = w2;
-                        vmin = v2;
+                    need = need && wmin != 0xffffffffu;
+                    if (need && m == RW_KM) {  // a ninth cluster: the overflow kernel finishes it
+                        ovf = true;
+                        need = false;
                     }
-                }
-                need = need && wmin != 0xffffffffu;
-                if (need && m == RW_KM) {  // a ninth cluster: the overflow kernel finishes it
-                    ovf = true;
-                    need = false;
-                }
-                if (need) {
+                    if (need) {
+                        uint32_t c = 0;
 #pragma unroll
-                    for (int k = 0; k < RW_KM; ++k) {
-                        if (static_cast<uint32_t>(k) == m || (m == 0 && k > 0)) L.key[k] = vmin;  // dup key 0
-                        if (static_cast<uint32_t>(k) == m) L.cnt[k] = 0;
+                        for (int i = 0; i < NV; ++i) {
+                            const bool hit = ((mk >> i) & 1u) && iv[i] == vmin;
+                            c += hit ? 1u : 0u;
+                            mk &= hit ? ~(1u << i) : 0xffffffffu;
+                        }
+#pragma unroll
+                        for (int k = 0; k < RW_KM; ++k) {
+                            if (static_cast<uint32_t>(k) == m || (m == 0 && k > 0)) L.key[k] = vmin;  // dup key 0
+                            if (static_cast<uint32_t>(k) == m) L.cnt[k] = c;
+                        }
+                        ++m;
                     }
-                    uint32_t c = 0;
-#pragma unroll
-                    for (uint32_t j = 0; j < 2 * BOXES; ++j) {
-                        const uint32_t b = j >> 1, h = j & 1u;
-                        const uint4 u = *reinterpret_cast<const uint4*>(si + b * box_bytes + swz128(prow, h * 4u + q));
-                        c += (u.x == vmin) + (u.y == vmin) + (u.z == vmin) + (u.w == vmin);
-                    }
-#pragma unroll
-                    for (int k = 0; k < RW_KM; ++k)
-                        if (static_cast<uint32_t>(k) == m) L.cnt[k] = c;
-                    ++m;
                 }
             }
-        }
-        if (with_ids) {
             before = 0;
 #pragma unroll
             for (int k = 0; k < RW_KM; ++k) before += static_cast<uint32_t>(k) < m ? L.cnt[k] : 0u;
@@ -464,35 +477,50 @@ __global__ void __launch_bounds__(RQ_PROGS * 4) reward_quad_kernel(const __grid_
         }
         const uint32_t ovf_bal = __ballot_sync(0xffffffffu, ovf);  // every lane votes (no short circuit)
         ovf = ovf || (ovf_bal & qmask) != 0;
-        if (q == 0 && live) {
-            const uint32_t n = (t + 1) * W;
-            const double rv =
-                a == CDX_AGG_MAX ? static_cast<double>(__uint_as_float(mx)) : __ddiv_rn(tot, static_cast<double>(n));
-            double hc = 0.0;
-            if (with_ids && !ovf) {
-                if (n == 1) {
-                    hc = 1.0;
-                } else {
-                    const double* Tn = p.tab + __ldg(p.row_off + t);
-                    double term[RW_KM];  // every tc[k] <= n (unused slots count key-0 hits): loads in flight together
+        // ---- the fold is deferred: lane t % 4 keeps step t's totals, and every 4 steps the
+        // quad's 4 lanes fold 4 steps at once (the fold is serial per step, so it would
+        // otherwise run on one lane of four)
+        if ((t & 3u) == q) {
+            pend.t = t;
+            pend.tot = tot;
+            pend.mx = mx;
+            pend.m = m;
+            pend.ovf = ovf;
 #pragma unroll
-                    for (int k = 0; k < RW_KM; ++k) term[k] = __ldg(Tn + tc[k]);
-                    double hh = 0.0;
+            for (int k = 0; k < RW_KM; ++k) pend.tc[k] = with_ids ? tc[k] : 0u;
+            pend.valid = true;
+        }
+        if ((t & 3u) == 3u || t + 1 == T) {
+            if (pend.valid && live) {
+                const uint32_t pt = pend.t;
+                const uint32_t n = (pt + 1) * W;
+                const double rv = a == CDX_AGG_MAX ? static_cast<double>(__uint_as_float(pend.mx))
+                                                   : __ddiv_rn(pend.tot, static_cast<double>(n));
+                double hc = 0.0;
+                if (with_ids && !pend.ovf) {
+                    if (n == 1) {
+                        hc = 1.0;
+                    } else {
+                        const double* Tn = p.tab + __ldg(p.row_off + pt);
+                        double term[RW_KM];  // every tc[k] <= n (unused slots count key-0 hits)
 #pragma unroll
-                    for (int k = 0; k < RW_KM; ++k)
-                        if (static_cast<uint32_t>(k) < m) hh = __dsub_rn(hh, term[k]);
-                    hh = (0.0 < hh) ? hh : 0.0;
-                    const double ln = __ldg(p.logs + t);
-                    const double v = __ddiv_rn(__dsub_rn(ln, hh), ln);
-                    hc = v < 0.0 ? 0.0 : (1.0 < v ? 1.0 : v);
+                        for (int k = 0; k < RW_KM; ++k) term[k] = __ldg(Tn + pend.tc[k]);
+                        double hh = 0.0;
+#pragma unroll
+                        for (int k = 0; k < RW_KM; ++k)
+                            if (static_cast<uint32_t>(k) < pend.m) hh = __dsub_rn(hh, term[k]);
+                        hh = (0.0 < hh) ? hh : 0.0;
+                        const double ln = __ldg(p.logs + pt);
+                        const double v = __ddiv_rn(__dsub_rn(ln, hh), ln);
+                        hc = v < 0.0 ? 0.0 : (1.0 < v ? 1.0 : v);
+                    }
                 }
+                outR[prow * T + pt] = static_cast<float>(rv);
+                outH[prow * T + pt] = static_cast<float>(hc);
+                if (meets_box(p, a == CDX_AGG_MAX ? 1 : 0, hc, rv))
+                    atomicOr(&outM[prow * p.words + (pt >> 5)], 1u << (pt & 31u));
             }
-            outR[prow * T + t] = static_cast<float>(rv);
-            outH[prow * T + t] = static_cast<float>(hc);
-            const bool ok = meets_box(p, a == CDX_AGG_MAX ? 1 : 0, hc, rv);
-            uint32_t& mw = outM[prow * p.words + (t >> 5)];
-            if ((t & 31u) == 0) mw = 0;
-            if (ok) mw |= 1u << (t & 31u);
+            pend.valid = false;
         }
         __syncthreads();  // every lane is done with this stage
         if (tid == 0 && t + p.stages < T) issue(t + p.stages, stage);
