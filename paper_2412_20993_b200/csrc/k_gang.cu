@@ -21,6 +21,7 @@
 // idle here, so MATCH is the cheap ranker), resolve their offsets by decoupled look-back
 // and scatter.
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 
@@ -357,6 +358,111 @@ struct Launch {
     }
 };
 
+// ---- Range LSD radix pass (reduce-then-scan, no look-back) -------------------------------
+// Block b owns a contiguous range of RS_RANGE_TILES tiles.  Per pass: (1) each range counts
+// its digits (hist[b][256]); (2) one CTA turns the counts into exclusive offsets in
+// (digit, range) order; (3) each range re-reads its tiles in order, ranks every tile
+// stably (warp match + popc, warps in order) and scatters at running per-digit offsets.
+__global__ void __launch_bounds__(RS_THREADS) rr_hist(const uint64_t* __restrict__ keys, uint64_t n, uint64_t range,
+                                                      int shift, uint32_t* __restrict__ hist) {
+    __shared__ uint32_t h[256];
+    h[threadIdx.x] = 0;
+    __syncthreads();
+    const uint64_t b = static_cast<uint64_t>(blockIdx.x) * range;
+    const uint64_t e = min(b + range, n);
+    for (uint64_t i = b + threadIdx.x; i < e; i += RS_THREADS) atomicAdd(&h[(keys[i] >> shift) & 0xff], 1u);
+    __syncthreads();
+    hist[static_cast<uint64_t>(blockIdx.x) * 256 + threadIdx.x] = h[threadIdx.x];
+}
+
+// thread d: exclusive prefix over ranges of digit d, then the digit bases (one CTA of 256)
+__global__ void __launch_bounds__(256) rr_scan(uint32_t* __restrict__ hist, uint32_t nr) {
+    __shared__ uint32_t tot[256];
+    __shared__ uint32_t ws[8];
+    const uint32_t d = threadIdx.x, lane = d & 31, warp = d >> 5;
+    uint32_t acc = 0;
+    for (uint32_t b = 0; b < nr; ++b) {
+        const uint32_t c = hist[static_cast<uint64_t>(b) * 256 + d];
+        hist[static_cast<uint64_t>(b) * 256 + d] = acc;
+        acc += c;
+    }
+    uint32_t inc = acc;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
+        if (lane >= static_cast<uint32_t>(o)) inc += y;
+    }
+    if (lane == 31) ws[warp] = inc;
+    __syncthreads();
+    uint32_t base = inc - acc;
+    for (uint32_t w = 0; w < warp; ++w) base += ws[w];
+    tot[d] = base;
+    __syncthreads();
+    for (uint32_t b = 0; b < nr; ++b) hist[static_cast<uint64_t>(b) * 256 + d] += tot[d];
+}
+
+__global__ void __launch_bounds__(RS_THREADS) rr_scatter(const uint64_t* __restrict__ kin,
+                                                         const uint32_t* __restrict__ vin, uint64_t* __restrict__ kout,
+                                                         uint32_t* __restrict__ vout, uint64_t n, uint64_t range,
+                                                         int shift, const uint32_t* __restrict__ offs) {
+    __shared__ uint32_t run[256];
+    __shared__ uint32_t wcnt[RS_WARPS][256];
+    const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    run[threadIdx.x] = offs[static_cast<uint64_t>(blockIdx.x) * 256 + threadIdx.x];
+    const uint64_t rb = static_cast<uint64_t>(blockIdx.x) * range;
+    const uint64_t re = min(rb + range, n);
+    const uint32_t lt = (1u << lane) - 1u;
+    for (uint64_t tb = rb; tb < re; tb += RS_TILE) {
+        for (int i = threadIdx.x; i < RS_WARPS * 256; i += RS_THREADS) (&wcnt[0][0])[i] = 0;
+        __syncthreads();
+        const uint64_t base = tb + static_cast<uint64_t>(warp) * 32 * RS_ITEMS;
+        uint64_t k[RS_ITEMS];
+        uint32_t v[RS_ITEMS], rank[RS_ITEMS], dig[RS_ITEMS];
+#pragma unroll
+        for (int j = 0; j < RS_ITEMS; ++j) {
+            const uint64_t i = base + j * 32 + lane;
+            const bool ok = i < re;
+            k[j] = ok ? kin[i] : 0;
+            v[j] = ok ? vin[i] : 0;
+        }
+#pragma unroll
+        for (int j = 0; j < RS_ITEMS; ++j) {
+            const bool ok = base + j * 32 + lane < re;
+            const uint32_t d = ok ? static_cast<uint32_t>((k[j] >> shift) & 0xff) : 256u + lane;
+            dig[j] = d;
+            const uint32_t peers = __match_any_sync(0xffffffffu, d);
+            uint32_t before = 0;
+            if (ok) before = wcnt[warp][d];
+            __syncwarp();
+            rank[j] = before + __popc(peers & lt);
+            if (ok && (peers & lt) == 0) wcnt[warp][d] = before + __popc(peers);
+            __syncwarp();
+        }
+        __syncthreads();
+        {  // warps' exclusive prefixes per digit, and this tile's total
+            const uint32_t d = threadIdx.x;
+            uint32_t c = 0;
+            for (int w = 0; w < RS_WARPS; ++w) {
+                const uint32_t x = wcnt[w][d];
+                wcnt[w][d] = c + run[d];
+                c += x;
+            }
+            __syncthreads();
+            run[d] += c;
+        }
+#pragma unroll
+        for (int j = 0; j < RS_ITEMS; ++j) {
+            const uint64_t i = base + j * 32 + lane;
+            if (i < re) {
+                const uint64_t pos = static_cast<uint64_t>(wcnt[warp][dig[j]]) + rank[j];
+                kout[pos] = k[j];
+                vout[pos] = v[j];
+            }
+        }
+        __syncthreads();
+    }
+}
+
 // Stable LSD radix sort of (keys, vals) over 8-bit digits (onesweep).  `lb` is scratch of
 // 8*256 + 16 + 8*ntiles*256 u32 (global digit counts, pass tickets, look-back records),
 // cleared by one memset per sort; digits where every key agrees are skipped (decided on
@@ -383,6 +489,13 @@ int radix_sort(cdx_ctx* ctx, uint64_t* k0, uint32_t* v0, uint64_t* k1, uint32_t*
     uint32_t* vin = v0;
     uint64_t* kout = k1;
     uint32_t* vout = v1;
+    // range passes (default; CDX_RADIX=onesweep selects the look-back passes): ranges of
+    // several tiles, one per resident CTA slot, so no tile waits on another
+    const char* impl = getenv("CDX_RADIX");
+    const bool ranges = !(impl && std::strcmp(impl, "onesweep") == 0);
+    const uint64_t want = static_cast<uint64_t>(ctx->sm_count) * 2;
+    const uint64_t range = std::max<uint64_t>(RS_TILE, ((n + want - 1) / want + RS_TILE - 1) / RS_TILE * RS_TILE);
+    const uint32_t nr = static_cast<uint32_t>((n + range - 1) / range);
     for (int d = 0; d < 8; ++d) {
         bool trivial = false;
         for (int b = 0; b < 256; ++b)
@@ -391,6 +504,18 @@ int radix_sort(cdx_ctx* ctx, uint64_t* k0, uint32_t* v0, uint64_t* k1, uint32_t*
                 break;
             }
         if (trivial) continue;
+        if (ranges) {
+            uint32_t* rh = look;  // [nr][256], reused every pass (stream-ordered)
+            rr_hist<<<nr, RS_THREADS, 0, ctx->stream>>>(kin, n, range, 8 * d, rh);
+            CDX_CHECK_LAUNCH(ctx, "radix(range hist)");
+            rr_scan<<<1, 256, 0, ctx->stream>>>(rh, nr);
+            CDX_CHECK_LAUNCH(ctx, "radix(range scan)");
+            rr_scatter<<<nr, RS_THREADS, 0, ctx->stream>>>(kin, vin, kout, vout, n, range, 8 * d, rh);
+            CDX_CHECK_LAUNCH(ctx, "radix(range scatter)");
+            std::swap(kin, kout);
+            std::swap(vin, vout);
+            continue;
+        }
         os_pass<<<ntiles, RS_THREADS, 0, ctx->stream>>>(kin, vin, kout, vout, n, 8 * d, ghist + d * 256,
                                                         look + static_cast<size_t>(d) * ntiles * 256, tickets + d);
         CDX_CHECK_LAUNCH(ctx, "radix(pass)");
