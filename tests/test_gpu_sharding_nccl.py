@@ -1,0 +1,60 @@
+"""The sharded path's collectives over a real NCCL communicator on the B200 (world size 1:
+this harness reaches one GPU; the multi-rank exchange logic is covered by the gloo tests).
+all_gather_into_tensor of the budget totals and of the padded key runs, then the device
+rebase and merge, must reproduce the single-GPU results."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import oracle as O
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def nccl():
+    import torch.distributed as dist
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", rank=0, world_size=1,
+                            device_id=torch.device("cuda", 0))
+    yield dist
+    dist.destroy_process_group()
+
+
+def test_sc_decide_and_gang_order_through_nccl(ctx, nccl):
+    from paper_2412_20993_b200 import AllocPolicy, GenParams, InterPolicy, Threshold
+    from paper_2412_20993_b200.sharding import Sharded
+    sh = Sharded(ctx, force_collectives=True)
+    assert sh.nccl and sh.world == 1
+    R, P, S = 3000, 64, 32
+    ids = ctx.gen_sc(GenParams(seed=41, conv_hi=64), R, P, S)
+    pol = AllocPolicy(kind=2, detect_at=5, resource_cap=64, tokens_per_unit=64 * S)
+    res = sh.sc_decide(ids, [Threshold(0, 0.7, 0)], pol, r0=0)
+    ctx.sync()
+    _, _, om = O.sc_certaindex(O.gen_sc(O.gen_params(seed=41, conv_hi=64), R, P, S), [(0, 0.7, 0)])
+    ref = O.allocate_scan(om, R, P, 2, 5, 64, 1, 64 * S)
+    assert np.array_equal(res["offsets"].cpu().numpy(), ref["offsets"])
+    assert int(res["shard_totals"][0]) == int((ref["granted"].astype(np.int64) * 64 * S).sum())
+    # gang order: padded allgather of the sorted key run + device merge
+    N = 20000
+    rng = np.random.default_rng(3)
+    arrival = np.cumsum(rng.exponential(1e-3, N))
+    now = float(arrival[-1]) + 1e-3
+    cnt = rng.integers(0, 5, N).astype(np.uint32)
+    soa = dict(arrival=arrival, last_service=np.maximum(now - rng.exponential(0.2, N), 0.0),
+               iter_tok_sum=(rng.integers(1, 500, N) * cnt).astype(np.int64), iter_count=cnt,
+               cap=rng.integers(1, 30, N).astype(np.uint16), terminated=(rng.random(N) < 0.2).astype(np.uint8))
+    soa["knob"] = np.minimum(soa["cap"], rng.integers(0, 30, N)).astype(np.uint16)
+    dev = {k: (torch.from_numpy(v.view(np.int16)) if v.dtype == np.uint16 else torch.from_numpy(v)).cuda()
+           for k, v in soa.items()}
+    order, total = sh.gang_order(dev, InterPolicy(order=1, starvation_limit=0.15, prior_tokens=128.0), now, 0, N + 5)
+    ctx.sync()
+    gref, _ = O.gang_order(soa, 1, 0.15, 128.0, now)
+    assert int(total) == len(gref)
+    assert np.array_equal(order[: len(gref)].cpu().numpy().view(np.uint32), gref)
