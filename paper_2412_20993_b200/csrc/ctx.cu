@@ -117,9 +117,6 @@ int build_term_tables(cdx_ctx* ctx, const uint32_t* ns, uint32_t count, TermTabl
     cudaStreamSynchronize(ctx->stream);
     if (bytes > ctx->tt_bytes) {
         if (ctx->tt_dev) cudaFree(ctx->tt_dev);
-    if (ctx->al_state) cudaFree(ctx->al_state);
-    if (ctx->exp_tab) cudaFree(ctx->exp_tab);
-    if (ctx->jl_buf) cudaFree(ctx->jl_buf);
         ctx->tt_dev = nullptr;
         ctx->tt_bytes = 0;
         if (cudaMalloc(&ctx->tt_dev, bytes) != cudaSuccess) return set_error(ctx, CDX_ECUDA, "term table alloc");

@@ -489,10 +489,11 @@ int radix_sort(cdx_ctx* ctx, uint64_t* k0, uint32_t* v0, uint64_t* k1, uint32_t*
     uint32_t* vin = v0;
     uint64_t* kout = k1;
     uint32_t* vout = v1;
-    // range passes (default; CDX_RADIX=onesweep selects the look-back passes): ranges of
-    // several tiles, one per resident CTA slot, so no tile waits on another
+    // onesweep look-back passes by default; CDX_RADIX=ranges selects the reduce-then-scan
+    // range passes (ranges of several tiles, no tile waits on another) — measured slower on
+    // config E (0.76 vs 0.60 ms: three launches and a serial one-CTA scan per digit)
     const char* impl = getenv("CDX_RADIX");
-    const bool ranges = !(impl && std::strcmp(impl, "onesweep") == 0);
+    const bool ranges = impl && std::strcmp(impl, "ranges") == 0;
     const uint64_t want = static_cast<uint64_t>(ctx->sm_count) * 2;
     const uint64_t range = std::max<uint64_t>(RS_TILE, ((n + want - 1) / want + RS_TILE - 1) / RS_TILE * RS_TILE);
     const uint32_t nr = static_cast<uint32_t>((n + range - 1) / range);
