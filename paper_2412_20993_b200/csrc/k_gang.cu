@@ -17,9 +17,10 @@
 // (skipped when arrivals are already non-decreasing), then a stable sort on hi; digits on
 // which all keys agree are skipped.  Key build and compaction of live programs are one
 // single-pass kernel (gang_prepare); the sort is onesweep: one histogram read for all 8
-// digits, then one kernel per digit whose tiles rank stably (warp match + popc; the ADU is
-// idle here, so MATCH is the cheap ranker), resolve their offsets by decoupled look-back
-// and scatter.
+// digits (fused into the key-build sync), then one kernel per digit whose tiles rank
+// stably (warp match + a shared-memory atomic per digit group), sort themselves by digit in
+// shared memory, resolve their offsets by windowed decoupled look-back and write digit
+// runs; the last pass writes program ids directly.
 #include <algorithm>
 #include <cstdlib>
 #include <cstring>
@@ -227,18 +228,52 @@ __global__ void pack_keys(const uint64_t* __restrict__ shi, const uint64_t* __re
 // launch order, so look-back only ever waits on running or finished tiles.
 constexpr uint32_t LB_AGG = 1u << 30, LB_INC = 2u << 30, LB_CNT = (1u << 30) - 1u;
 
-__device__ __forceinline__ uint32_t ld_acq_u32(const uint32_t* p) {
+// The look-back records carry their payload in the flag word itself (flag | count), so no
+// other memory is published through them: relaxed gpu-scope accesses suffice, and skip
+// the fence a release store implies.
+__device__ __forceinline__ uint32_t ld_rlx_u32(const uint32_t* p) {
     uint32_t v;
-    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
     return v;
 }
-__device__ __forceinline__ void st_rel_u32(uint32_t* p, uint32_t v) {
-    asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+__device__ __forceinline__ void st_rlx_u32(uint32_t* p, uint32_t v) {
+    asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+// Exclusive prefix of digit d over tiles [0, tile): the records of `win` predecessors are
+// loaded together and consumed in order up to the first inclusive one; an unpublished
+// record restarts the window there.
+constexpr int LB_WIN = 8;  // measured on config E: 4 and 8 equal, 16 slower, 1 (serial) 25 % slower
+template <int WIN>
+__device__ __forceinline__ uint32_t lookback_win(const uint32_t* look, uint32_t tile, uint32_t d) {
+    uint32_t excl = 0;
+    int64_t j = static_cast<int64_t>(tile) - 1;
+    while (j >= 0) {
+        uint32_t f[WIN];
+#pragma unroll
+        for (int q = 0; q < WIN; ++q)
+            f[q] = j - q >= 0 ? ld_rlx_u32(look + static_cast<uint64_t>(j - q) * 256 + d) : LB_INC;
+        int used = 0;
+        bool done = false;
+#pragma unroll
+        for (int q = 0; q < WIN; ++q) {
+            if (done || used != q || (f[q] & ~LB_CNT) == 0) continue;
+            excl += f[q] & LB_CNT;
+            used = q + 1;
+            done = (f[q] & LB_INC) != 0;
+        }
+        if (done) break;
+        j -= used;
+    }
+    return excl;
 }
 
+// n_dev (nullable): the key count is read on the device (the gang path histograms its
+// compacted keys before the host has learned how many there are: one sync, not two)
 __global__ void __launch_bounds__(RS_THREADS) os_histogram(const uint64_t* __restrict__ keys, uint64_t n,
-                                                           uint32_t* __restrict__ ghist) {
+                                                           uint32_t* __restrict__ ghist,
+                                                           const uint32_t* __restrict__ n_dev) {
     __shared__ uint32_t h[8][256];
+    if (n_dev) n = *n_dev;
     for (int i = threadIdx.x; i < 8 * 256; i += RS_THREADS) (&h[0][0])[i] = 0;
     __syncthreads();
     for (uint64_t i = blockIdx.x * static_cast<uint64_t>(RS_THREADS) + threadIdx.x; i < n;
@@ -254,19 +289,33 @@ __global__ void __launch_bounds__(RS_THREADS) os_histogram(const uint64_t* __res
     }
 }
 
-__global__ void __launch_bounds__(RS_THREADS) os_pass(const uint64_t* __restrict__ kin,
-                                                      const uint32_t* __restrict__ vin, uint64_t* __restrict__ kout,
-                                                      uint32_t* __restrict__ vout, uint64_t n, int shift,
-                                                      const uint32_t* __restrict__ ghist, uint32_t* __restrict__ look,
-                                                      uint32_t* __restrict__ counter) {
-    __shared__ uint32_t s_tile;
-    __shared__ uint32_t wcnt[RS_WARPS][256];
-    __shared__ uint32_t s_base[256];
-    __shared__ uint32_t s_wsum[RS_WARPS];
+// Same pass with a tile-local counting sort through shared memory: after ranking, every
+// key goes to its digit-sorted slot in the tile (smem), and the global scatter then walks
+// the tile in sorted order, so consecutive threads write consecutive addresses of one
+// digit run (~16 keys per digit per tile) instead of 32 unrelated sectors per store.  The
+// tile's aggregate is published before the local shuffle and the look-back runs after it,
+// so waiting on a predecessor overlaps this tile's own work.  Ranking: per item, the warp's
+// lanes with equal digits find each other with MATCH; the group's first lane adds the group
+// size to the warp's private counter with a shared-memory atomic (a warp's atomics on one
+// address are performed in issue order, so ranks stay stable across items without a warp
+// barrier per item) and the base is broadcast back with one shuffle.  Full tiles (all but
+// the last) run without bounds checks.
+constexpr int RS2_SMEM = RS_TILE * 12 + RS_WARPS * 256 * 4 + 2 * 256 * 4 + 64;
+
+template <bool FULL, int WIN>
+__device__ __forceinline__ void os_tile(const uint64_t* __restrict__ kin, const uint32_t* __restrict__ vin,
+                                        uint64_t* __restrict__ kout, uint32_t* __restrict__ vout, uint64_t n,
+                                        int shift, const uint32_t* __restrict__ ghist, uint32_t* __restrict__ look,
+                                        uint32_t tile, uint8_t* rs2_smem, const uint32_t* __restrict__ vmap) {
+    uint64_t* sk = reinterpret_cast<uint64_t*>(rs2_smem);
+    uint32_t* sv = reinterpret_cast<uint32_t*>(sk + RS_TILE);
+    uint32_t(*wcnt)[256] = reinterpret_cast<uint32_t(*)[256]>(sv + RS_TILE);
+    uint32_t* s_gbase = &wcnt[RS_WARPS][0];
+    uint32_t* s_wsum = s_gbase + 256;  // [RS_WARPS] x 2
     const uint32_t tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
-    if (tid == 0) s_tile = atomicAdd(counter, 1u);
-    for (int i = tid; i < RS_WARPS * 256; i += RS_THREADS) (&wcnt[0][0])[i] = 0;
-    // global exclusive base of this thread's digit: block scan of the 256 digit counts
+#pragma unroll
+    for (int i = 0; i < RS_WARPS; ++i) wcnt[i][tid] = 0;
+    // global exclusive base of digit `tid`
     const uint32_t g = ghist[tid];
     uint32_t incl = g;
 #pragma unroll
@@ -277,71 +326,117 @@ __global__ void __launch_bounds__(RS_THREADS) os_pass(const uint64_t* __restrict
     if (lane == 31) s_wsum[warp] = incl;
     __syncthreads();
     uint32_t wpre = 0;
-    for (uint32_t w = 0; w < warp; ++w) wpre += s_wsum[w];
-    s_base[tid] = wpre + incl - g;
-    const uint32_t tile = s_tile;
-    const uint64_t base = static_cast<uint64_t>(tile) * RS_TILE + static_cast<uint64_t>(warp) * 32 * RS_ITEMS;
+#pragma unroll
+    for (uint32_t w = 0; w < RS_WARPS; ++w) wpre += w < warp ? s_wsum[w] : 0u;
+    const uint32_t gbase = wpre + incl - g;
+    const uint64_t tbase = static_cast<uint64_t>(tile) * RS_TILE;
+    const uint32_t tile_n = FULL ? RS_TILE : static_cast<uint32_t>(n - tbase);
+    const uint64_t* tk = kin + tbase + warp * 32 * RS_ITEMS + lane;
+    const uint32_t* tv = vin + tbase + warp * 32 * RS_ITEMS + lane;
+    const uint32_t wofs = warp * 32 * RS_ITEMS + lane;  // item j of this thread: tile index wofs + 32 j
     uint64_t k[RS_ITEMS];
-    uint32_t v[RS_ITEMS], rank[RS_ITEMS], dig[RS_ITEMS];
+    uint32_t v[RS_ITEMS], rank[RS_ITEMS];
     const uint32_t lt = (1u << lane) - 1u;
 #pragma unroll
     for (int j = 0; j < RS_ITEMS; ++j) {
-        const uint64_t i = base + j * 32 + lane;
-        const bool ok = i < n;
-        k[j] = ok ? kin[i] : 0;
-        v[j] = ok ? vin[i] : 0;
-    }
-#pragma unroll
-    for (int j = 0; j < RS_ITEMS; ++j) {
-        const bool ok = base + j * 32 + lane < n;
-        const uint32_t d = ok ? static_cast<uint32_t>((k[j] >> shift) & 0xff) : 256u + lane;  // unique dummy
-        dig[j] = d;
-        const uint32_t peers = __match_any_sync(0xffffffffu, d);
-        uint32_t before = 0;
-        if (ok) before = wcnt[warp][d];
-        __syncwarp();
-        rank[j] = before + __popc(peers & lt);
-        if (ok && (peers & lt) == 0) wcnt[warp][d] = before + __popc(peers);
-        __syncwarp();
-    }
-    __syncthreads();
-    // thread d: this tile's count of digit d, the warps' exclusive prefixes, look-back
-    {
-        const uint32_t d = tid;
-        uint32_t c = 0;
-        for (int w = 0; w < RS_WARPS; ++w) {
-            const uint32_t x = wcnt[w][d];
-            wcnt[w][d] = c;
-            c += x;
-        }
-        uint32_t excl = 0;
-        if (tile == 0) {
-            st_rel_u32(look + d, LB_INC | c);
+        if (FULL || wofs + 32 * j < tile_n) {
+            k[j] = tk[32 * j];
+            v[j] = tv[32 * j];
         } else {
-            st_rel_u32(look + static_cast<uint64_t>(tile) * 256 + d, LB_AGG | c);
-            for (int64_t j = static_cast<int64_t>(tile) - 1; j >= 0; --j) {
-                uint32_t f;
-                do {
-                    f = ld_acq_u32(look + static_cast<uint64_t>(j) * 256 + d);
-                } while ((f & ~LB_CNT) == 0);
-                excl += f & LB_CNT;
-                if (f & LB_INC) break;
-            }
-            st_rel_u32(look + static_cast<uint64_t>(tile) * 256 + d, LB_INC | (excl + c));
+            k[j] = 0;
+            v[j] = 0;
         }
-        s_base[d] += excl;
     }
-    __syncthreads();
 #pragma unroll
     for (int j = 0; j < RS_ITEMS; ++j) {
-        const uint64_t i = base + j * 32 + lane;
-        if (i < n) {
-            const uint32_t d = dig[j];
-            const uint64_t pos = static_cast<uint64_t>(s_base[d]) + wcnt[warp][d] + rank[j];
-            kout[pos] = k[j];
-            vout[pos] = v[j];
+        const bool ok = FULL || wofs + 32 * j < tile_n;
+        const uint32_t d = ok ? static_cast<uint32_t>((k[j] >> shift) & 0xff) : 256u + lane;  // unique dummy
+        const uint32_t peers = __match_any_sync(0xffffffffu, d);
+        const uint32_t below = peers & lt;
+        uint32_t old = 0;
+        if (ok && below == 0) old = atomicAdd(&wcnt[warp][d], static_cast<uint32_t>(__popc(peers)));
+        rank[j] = __shfl_sync(0xffffffffu, old, __ffs(peers) - 1) + __popc(below);
+    }
+    __syncthreads();
+    // thread d: tile count of digit d, publish the aggregate, tile offsets by digit, and
+    // per-warp slots: wcnt[w][d] = first tile-sorted index of warp w's digit-d keys
+    const uint32_t d = tid;
+    uint32_t cw[RS_WARPS];
+    uint32_t c = 0;
+#pragma unroll
+    for (int w = 0; w < RS_WARPS; ++w) {
+        cw[w] = wcnt[w][d];
+        c += cw[w];
+    }
+    if (tile == 0)
+        st_rlx_u32(look + d, LB_INC | c);
+    else
+        st_rlx_u32(look + static_cast<uint64_t>(tile) * 256 + d, LB_AGG | c);
+    incl = c;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= static_cast<uint32_t>(o)) incl += y;
+    }
+    if (lane == 31) s_wsum[RS_WARPS + warp] = incl;
+    __syncthreads();
+    wpre = 0;
+#pragma unroll
+    for (uint32_t w = 0; w < RS_WARPS; ++w) wpre += w < warp ? s_wsum[RS_WARPS + w] : 0u;
+    const uint32_t toff = wpre + incl - c;
+    {
+        uint32_t run = toff;
+#pragma unroll
+        for (int w = 0; w < RS_WARPS; ++w) {
+            wcnt[w][d] = run;
+            run += cw[w];
         }
     }
+    __syncthreads();
+    // digit-sorted tile in shared memory
+#pragma unroll
+    for (int j = 0; j < RS_ITEMS; ++j) {
+        if (FULL || wofs + 32 * j < tile_n) {
+            const uint32_t lp = wcnt[warp][(k[j] >> shift) & 0xff] + rank[j];
+            sk[lp] = k[j];
+            sv[lp] = v[j];
+        }
+    }
+    // look-back for digit d over earlier tiles
+    uint32_t excl = 0;
+    if (tile != 0) {
+        excl = lookback_win<WIN>(look, tile, d);
+        st_rlx_u32(look + static_cast<uint64_t>(tile) * 256 + d, LB_INC | (excl + c));
+    }
+    s_gbase[d] = gbase + excl - toff;  // position = s_gbase[digit] + sorted tile index
+    __syncthreads();
+#pragma unroll 4
+    for (uint32_t j = 0; j < RS_ITEMS; ++j) {
+        const uint32_t i = j * RS_THREADS + tid;
+        if (FULL || i < tile_n) {
+            const uint64_t key = sk[i];
+            const uint32_t pos = s_gbase[(key >> shift) & 0xff] + i;
+            kout[pos] = key;
+            vout[pos] = vmap ? vmap[sv[i]] : sv[i];
+        }
+    }
+}
+
+// Tiles take tickets in launch order (look-back only waits on running or finished tiles);
+// every tile but the last is full.
+__global__ void __launch_bounds__(RS_THREADS, 2)
+    os_pass2(const uint64_t* __restrict__ kin, const uint32_t* __restrict__ vin, uint64_t* __restrict__ kout,
+             uint32_t* __restrict__ vout, uint64_t n, int shift, const uint32_t* __restrict__ ghist,
+             uint32_t* __restrict__ look, uint32_t* __restrict__ counter, const uint32_t* __restrict__ vmap) {
+    extern __shared__ __align__(16) uint8_t rs2_smem[];
+    uint32_t* s_tile = reinterpret_cast<uint32_t*>(rs2_smem + RS2_SMEM - 16);
+    if (threadIdx.x == 0) *s_tile = atomicAdd(counter, 1u);
+    __syncthreads();
+    const uint32_t tile = *s_tile;
+    if ((static_cast<uint64_t>(tile) + 1) * RS_TILE <= n)
+        os_tile<true, LB_WIN>(kin, vin, kout, vout, n, shift, ghist, look, tile, rs2_smem, vmap);
+    else
+        os_tile<false, LB_WIN>(kin, vin, kout, vout, n, shift, ghist, look, tile, rs2_smem, vmap);
 }
 
 template <typename T>
@@ -464,47 +559,66 @@ __global__ void __launch_bounds__(RS_THREADS) rr_scatter(const uint64_t* __restr
 }
 
 // Stable LSD radix sort of (keys, vals) over 8-bit digits (onesweep).  `lb` is scratch of
-// 8*256 + 16 + 8*ntiles*256 u32 (global digit counts, pass tickets, look-back records),
-// cleared by one memset per sort; digits where every key agrees are skipped (decided on
-// the host from the global counts: one 8 KB copy).  Returns which buffer holds the result
-// (0: k0/v0, 1: k1/v1).
+// 8*256 + 16 + 8*ntiles*256 u32 (global digit counts, pass tickets, look-back records);
+// digits where every key agrees are skipped (decided on the host from the global counts).
+// `hh` (nullable): the caller already histogrammed the keys into lb[0, 2048) and holds the
+// counts on the host (saves a launch and a sync).  `vmap`/`vfinal` (nullable): the last
+// pass writes vmap[value] to vfinal instead of the value (folds the caller's final gather).
+// *which: 0 result in k0/v0, 1 in k1/v1, 2 keys in k0/k1 as for (pass count & 1) and the
+// mapped values in vfinal.
 int radix_sort(cdx_ctx* ctx, uint64_t* k0, uint32_t* v0, uint64_t* k1, uint32_t* v1, uint64_t n, uint32_t* lb,
-               int* which) {
+               int* which, const uint32_t* hh, const uint32_t* vmap, uint32_t* vfinal) {
     *which = 0;
     if (n <= 1) return CDX_OK;
     const uint32_t ntiles = static_cast<uint32_t>((n + RS_TILE - 1) / RS_TILE);
     uint32_t* ghist = lb;
     uint32_t* tickets = lb + 8 * 256;
     uint32_t* look = tickets + 16;
-    cudaError_t e = cudaMemsetAsync(lb, 0, (8 * 256 + 16 + static_cast<size_t>(8) * ntiles * 256) * 4, ctx->stream);
+    const size_t clear = (16 + static_cast<size_t>(8) * ntiles * 256) * 4;
+    cudaError_t e = hh ? cudaMemsetAsync(tickets, 0, clear, ctx->stream)
+                       : cudaMemsetAsync(lb, 0, clear + 8 * 256 * 4, ctx->stream);
     if (e != cudaSuccess) return cuda_fail(ctx, e, "radix(clear)");
-    const unsigned hgrid = static_cast<unsigned>(std::min<uint64_t>(ntiles, static_cast<uint64_t>(ctx->sm_count) * 4));
-    os_histogram<<<hgrid, RS_THREADS, 0, ctx->stream>>>(k0, n, ghist);
-    CDX_CHECK_LAUNCH(ctx, "radix(histogram)");
     uint32_t h[8 * 256];
-    e = cudaMemcpyAsync(h, ghist, sizeof(h), cudaMemcpyDeviceToHost, ctx->stream);
-    if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
-    if (e != cudaSuccess) return cuda_fail(ctx, e, "radix(histogram)");
+    if (!hh) {
+        const unsigned hgrid =
+            static_cast<unsigned>(std::min<uint64_t>(ntiles, static_cast<uint64_t>(ctx->sm_count) * 4));
+        os_histogram<<<hgrid, RS_THREADS, 0, ctx->stream>>>(k0, n, ghist, nullptr);
+        CDX_CHECK_LAUNCH(ctx, "radix(histogram)");
+        e = cudaMemcpyAsync(h, ghist, sizeof(h), cudaMemcpyDeviceToHost, ctx->stream);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
+        if (e != cudaSuccess) return cuda_fail(ctx, e, "radix(histogram)");
+        hh = h;
+    }
     uint64_t* kin = k0;
     uint32_t* vin = v0;
     uint64_t* kout = k1;
     uint32_t* vout = v1;
     // onesweep look-back passes by default; CDX_RADIX=ranges selects the reduce-then-scan
     // range passes (ranges of several tiles, no tile waits on another) — measured slower on
-    // config E (0.76 vs 0.60 ms: three launches and a serial one-CTA scan per digit)
+    // config E (three launches and a serial one-CTA scan per digit)
     const char* impl = getenv("CDX_RADIX");
     const bool ranges = impl && std::strcmp(impl, "ranges") == 0;
+    if (!ranges) {  // per call: cheap, and correct for every device of the process
+        e = cudaFuncSetAttribute(os_pass2, cudaFuncAttributeMaxDynamicSharedMemorySize, RS2_SMEM);
+        if (e != cudaSuccess) return cuda_fail(ctx, e, "radix(smem attribute)");
+    }
     const uint64_t want = static_cast<uint64_t>(ctx->sm_count) * 2;
     const uint64_t range = std::max<uint64_t>(RS_TILE, ((n + want - 1) / want + RS_TILE - 1) / RS_TILE * RS_TILE);
     const uint32_t nr = static_cast<uint32_t>((n + range - 1) / range);
+    int last = -1;
+    bool nontrivial[8];
     for (int d = 0; d < 8; ++d) {
-        bool trivial = false;
+        nontrivial[d] = true;
         for (int b = 0; b < 256; ++b)
-            if (h[d * 256 + b]) {
-                trivial = h[d * 256 + b] == n;
+            if (hh[d * 256 + b]) {
+                nontrivial[d] = hh[d * 256 + b] != n;
                 break;
             }
-        if (trivial) continue;
+        if (nontrivial[d]) last = d;
+    }
+    bool mapped = false;
+    for (int d = 0; d < 8; ++d) {
+        if (!nontrivial[d]) continue;
         if (ranges) {
             uint32_t* rh = look;  // [nr][256], reused every pass (stream-ordered)
             rr_hist<<<nr, RS_THREADS, 0, ctx->stream>>>(kin, n, range, 8 * d, rh);
@@ -513,17 +627,18 @@ int radix_sort(cdx_ctx* ctx, uint64_t* k0, uint32_t* v0, uint64_t* k1, uint32_t*
             CDX_CHECK_LAUNCH(ctx, "radix(range scan)");
             rr_scatter<<<nr, RS_THREADS, 0, ctx->stream>>>(kin, vin, kout, vout, n, range, 8 * d, rh);
             CDX_CHECK_LAUNCH(ctx, "radix(range scatter)");
-            std::swap(kin, kout);
-            std::swap(vin, vout);
-            continue;
+        } else {
+            const bool fold = vmap && vfinal && d == last;
+            os_pass2<<<ntiles, RS_THREADS, RS2_SMEM, ctx->stream>>>(
+                kin, vin, kout, fold ? vfinal : vout, n, 8 * d, ghist + d * 256,
+                look + static_cast<size_t>(d) * ntiles * 256, tickets + d, fold ? vmap : nullptr);
+            CDX_CHECK_LAUNCH(ctx, "radix(pass)");
+            mapped = fold;
         }
-        os_pass<<<ntiles, RS_THREADS, 0, ctx->stream>>>(kin, vin, kout, vout, n, 8 * d, ghist + d * 256,
-                                                        look + static_cast<size_t>(d) * ntiles * 256, tickets + d);
-        CDX_CHECK_LAUNCH(ctx, "radix(pass)");
         std::swap(kin, kout);
         std::swap(vin, vout);
     }
-    *which = kin == k0 ? 0 : 1;
+    *which = mapped ? 2 : (kin == k0 ? 0 : 1);
     return CDX_OK;
 }
 
@@ -581,7 +696,7 @@ size_t radix_scratch_words(uint64_t n) {
 }
 int radix_sort_pairs(cdx_ctx* ctx, uint64_t* k0, uint32_t* v0, uint64_t* k1, uint32_t* v1, uint64_t n, uint32_t* lb,
                      int* which) {
-    return radix_sort(ctx, k0, v0, k1, v1, n, lb, which);
+    return radix_sort(ctx, k0, v0, k1, v1, n, lb, which, nullptr, nullptr, nullptr);
 }
 
 }  // namespace cdx
@@ -627,8 +742,16 @@ extern "C" int cdx_gang_priority(cdx_ctx* ctx, const cdx_prog_soa* progs, uint64
     CDX_CHECK_LAUNCH(ctx, "gang_priority(scan)");
     gang_prepare<<<gtiles, GP_THREADS, 0, ctx->stream>>>(p, khi, karr, kid, va, plook, misc);
     CDX_CHECK_LAUNCH(ctx, "gang_priority(prepare)");
+    // digit counts of the live hi keys (count read on the device), fetched with the flags
+    cudaMemsetAsync(hist, 0, 8 * 256 * 4, ctx->stream);
+    os_histogram<<<static_cast<unsigned>(std::min<uint64_t>(ntiles, static_cast<uint64_t>(ctx->sm_count) * 4)),
+                   RS_THREADS, 0, ctx->stream>>>(khi, N, hist, misc);
+    CDX_CHECK_LAUNCH(ctx, "gang_priority(histogram)");
     uint32_t hm[3];
+    std::vector<uint32_t> hh(8 * 256);
     cudaError_t e = cudaMemcpyAsync(hm, misc, 12, cudaMemcpyDeviceToHost, ctx->stream);
+    if (e == cudaSuccess)
+        e = cudaMemcpyAsync(hh.data(), hist, 8 * 256 * 4, cudaMemcpyDeviceToHost, ctx->stream);
     if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
     if (e != cudaSuccess) return cuda_fail(ctx, e, "gang_priority");
     if (hm[2]) return set_error(ctx, CDX_EINVAL, "gang_priority: times and keys must be finite and >= 0");
@@ -641,7 +764,7 @@ extern "C" int cdx_gang_priority(cdx_ctx* ctx, const cdx_prog_soa* progs, uint64
     if (hm[1]) {
         cudaMemcpyAsync(t0, karr, n * 8, cudaMemcpyDeviceToDevice, ctx->stream);
         int which = 0;
-        if (int st = radix_sort(ctx, t0, va, t1, vb, n, hist, &which)) return st;
+        if (int st = radix_sort(ctx, t0, va, t1, vb, n, hist, &which, nullptr, nullptr, nullptr)) return st;
         p1 = which ? vb : va;
     }
     // 2) stable sort on hi over the (arrival, id) order
@@ -655,7 +778,12 @@ extern "C" int cdx_gang_priority(cdx_ctx* ctx, const cdx_prog_soa* progs, uint64
     }
     int which = 0;
     uint64_t* hout = hin == t0 ? t1 : t0;
-    if (int st = radix_sort(ctx, hin, pa, hout, pb, n, hist, &which)) return st;
+    // the hi counts on the device are still valid unless the pre-sort overwrote them; the
+    // last pass writes program ids straight into `order` unless the keys are wanted too
+    if (int st = radix_sort(ctx, hin, pa, hout, pb, n, hist, &which, hm[1] ? nullptr : hh.data(),
+                            keys ? nullptr : kid, keys ? nullptr : order))
+        return st;
+    if (which == 2) return CDX_OK;
     uint32_t* fin = which ? pb : pa;  // position -> compacted index
     gather<uint32_t><<<L.grid(n), 256, 0, ctx->stream>>>(kid, fin, order, n);
     CDX_CHECK_LAUNCH(ctx, "gang_priority(order)");
