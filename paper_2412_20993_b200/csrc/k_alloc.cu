@@ -25,9 +25,12 @@ constexpr int AL_TILE = AL_THREADS * AL_ITEMS;  // 2048 requests per tile
 constexpr int AL_MAX_WORDS = 128;               // P <= 4096
 
 // Per-tile look-back record.  `flag` = epoch << 2 | state (1 aggregate, 2 inclusive):
-// records from earlier calls carry an older epoch and read as "not yet published".
+// records from earlier calls carry an older epoch and read as "not yet published".  The
+// scan carries granted units and kept counts only: budgets are units x tokens_per_unit and
+// the tokens saved are (valid requests x cap - units) x tokens_per_unit, both equal to the
+// per-request int64 sums bit for bit (multiplication distributes over sums mod 2^64).
 struct AlTile {
-    int64_t agg_b, inc_b, agg_s, inc_s;
+    uint64_t agg_e, inc_e;
     uint32_t agg_k, inc_k;
     uint32_t flag;
     uint32_t _pad;
@@ -84,15 +87,16 @@ __device__ __forceinline__ T warp_sum(T v) {
 
 // Striped layout: item i of thread t is request base + i*256 + t, so every load/store
 // instruction is coalesced; request order = (item, warp, lane), which the block scan
-// over (item, warp) totals follows.  Tiles take tickets in launch order, so a tile only
-// ever waits for tiles that are running or done; warp 0 looks back 32 tiles at a time.
+// over (item, warp) totals follows.  Per item one u32 warp scan carries both the granted
+// units and the kept flag (units << 12 | kept: a warp's units <= 32 * 4096 = 2^17).  Tiles
+// take tickets in launch order, so a tile only ever waits for tiles that are running or
+// done.
 __global__ void __launch_bounds__(AL_THREADS) allocate_scan_kernel(const __grid_constant__ AllocParams p) {
     __shared__ uint32_t s_tile;
-    __shared__ int64_t s_wb[AL_ITEMS * AL_WARPS];
-    __shared__ int64_t s_ws[AL_ITEMS * AL_WARPS];
+    __shared__ uint32_t s_we[AL_ITEMS * AL_WARPS];  // exclusive units before (item, warp) in the tile
     __shared__ uint32_t s_wk[AL_ITEMS * AL_WARPS];
-    __shared__ int64_t s_excl_b;
-    __shared__ uint32_t s_excl_k;
+    __shared__ uint64_t s_excl_e, s_red_e[AL_WARPS];
+    __shared__ uint32_t s_excl_k, s_tot_e, s_tot_k, s_red_k[AL_WARPS], s_first[AL_WARPS];
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     __shared__ uint32_t s_epoch;
@@ -106,79 +110,75 @@ __global__ void __launch_bounds__(AL_THREADS) allocate_scan_kernel(const __grid_
     const uint64_t base = static_cast<uint64_t>(tile) * AL_TILE;
 
     // ---- per-request decision, coalesced
-    int32_t ek[AL_ITEMS];
-    int64_t ib[AL_ITEMS];
-    uint32_t ik[AL_ITEMS];
+    uint32_t pk[AL_ITEMS];  // inclusive warp scan of (units << 12 | kept)
 #pragma unroll
     for (int i = 0; i < AL_ITEMS; ++i) {
         const uint64_t r = base + static_cast<uint64_t>(i) * AL_THREADS + tid;
-        int32_t e = 0;
+        uint32_t e = 0;
         if (r < p.R) {
-            e = p.cap;
+            e = static_cast<uint32_t>(p.cap);
             uint8_t why = CDX_EXIT_BUDGET;
             for (uint32_t w = 0; w < p.chk_words; ++w) {
                 const uint32_t x = __ldg(p.meets + r * p.words + w) & p.chk[w];
                 if (x) {
-                    e = static_cast<int32_t>(w * 32 + __ffs(x));  // knob = probe index + 1
+                    e = w * 32 + static_cast<uint32_t>(__ffs(x));  // knob = probe index + 1
                     why = CDX_EXIT_CERTAIN;
                     break;
                 }
             }
-            if (p.exit_knob) p.exit_knob[r] = e;
+            if (p.exit_knob) p.exit_knob[r] = static_cast<int32_t>(e);
             if (p.reason) p.reason[r] = why;
-            if (p.granted) p.granted[r] = e;
+            if (p.granted) p.granted[r] = static_cast<int32_t>(e);
         }
-        ek[i] = e;
-        const int64_t b = static_cast<int64_t>(e) * p.tpu;
-        const uint32_t k = (r < p.R && e > p.detect) ? 1u : 0u;
-        const int64_t sv = r < p.R ? static_cast<int64_t>(p.cap - e) * p.tpu : 0;
-        ib[i] = warp_incl_scan<int64_t>(b, lane);
-        ik[i] = warp_incl_scan<uint32_t>(k, lane);
-        const int64_t ws = warp_sum<int64_t>(sv);
-        if (lane == 31) {
-            s_wb[i * AL_WARPS + warp] = ib[i];
-            s_wk[i * AL_WARPS + warp] = ik[i];
-        }
-        if (lane == 0) s_ws[i * AL_WARPS + warp] = ws;
+        const uint32_t k = (r < p.R && static_cast<int32_t>(e) > p.detect) ? 1u : 0u;
+        pk[i] = warp_incl_scan<uint32_t>((e << 12) | k, lane);
+        if (lane == 31) s_we[i * AL_WARPS + warp] = pk[i];
     }
     __syncthreads();
     // ---- exclusive prefix over the (item, warp) totals: 64 entries, 2 per lane of warp 0
     if (warp == 0) {
         const int a0 = 2 * lane, a1 = 2 * lane + 1;
-        const int64_t b0 = s_wb[a0], b1 = s_wb[a1];
-        const uint32_t k0 = s_wk[a0], k1 = s_wk[a1];
-        const int64_t sv = s_ws[a0] + s_ws[a1];
-        const int64_t incb = warp_incl_scan<int64_t>(b0 + b1, lane);
+        const uint32_t x0 = s_we[a0], x1 = s_we[a1];
+        const uint32_t e0 = x0 >> 12, e1 = x1 >> 12, k0 = x0 & 0xfffu, k1 = x1 & 0xfffu;
+        const uint32_t ince = warp_incl_scan<uint32_t>(e0 + e1, lane);  // tile units <= 2^23
         const uint32_t inck = warp_incl_scan<uint32_t>(k0 + k1, lane);
-        const int64_t tot_s = warp_sum<int64_t>(sv);
-        const int64_t tot_b = __shfl_sync(0xffffffffu, incb, 31);
+        const uint32_t tot_e = __shfl_sync(0xffffffffu, ince, 31);
         const uint32_t tot_k = __shfl_sync(0xffffffffu, inck, 31);
-        s_wb[a0] = incb - b0 - b1;
-        s_wb[a1] = incb - b1;
+        __syncwarp();
+        s_we[a0] = ince - e0 - e1;
+        s_we[a1] = ince - e1;
         s_wk[a0] = inck - k0 - k1;
         s_wk[a1] = inck - k1;
 
-        // ---- decoupled look-back over earlier tiles, 32 at a time
-        AlTile* T = p.tiles;
-        const uint32_t ep = (s_epoch & 0x3fffffffu) << 2;
         if (lane == 0) {
+            s_tot_e = tot_e;
+            s_tot_k = tot_k;
+            AlTile* T = p.tiles;
+            const uint32_t ep = (s_epoch & 0x3fffffffu) << 2;
             if (tile == 0) {  // the first tile's aggregate is its inclusive prefix
-                T[0].inc_b = tot_b;
+                T[0].inc_e = tot_e;
                 T[0].inc_k = tot_k;
-                T[0].inc_s = tot_s;
             } else {
-                T[tile].agg_b = tot_b;
+                T[tile].agg_e = tot_e;
                 T[tile].agg_k = tot_k;
-                T[tile].agg_s = tot_s;
             }
             __threadfence();  // the record is complete before its flag says so
             st_release(&T[tile].flag, ep | (tile == 0 ? 2u : 1u));
         }
-        int64_t eb = 0, es = 0;
+    }
+    __syncthreads();
+    // ---- decoupled look-back over earlier tiles with the whole CTA, 256 records per round.
+    // When a wave of tiles publishes its aggregates together, a tile walks back until it
+    // meets an inclusive record — up to its distance from the wave's start — so the window
+    // width, not the chain, sets the cost: 256 wide, a 512-tile grid needs at most 2 rounds.
+    {
+        const AlTile* T = p.tiles;
+        const uint32_t ep = (s_epoch & 0x3fffffffu) << 2;
+        uint64_t ee = 0;
         uint32_t ekk = 0;
         int64_t j = static_cast<int64_t>(tile) - 1;
-        while (j >= 0) {
-            const int64_t idx = j - lane;
+        while (j >= 0) {  // block-uniform
+            const int64_t idx = j - tid;
             uint32_t st = 2;  // before tile 0: an inclusive zero
             if (idx >= 0) {
                 uint32_t f;
@@ -188,49 +188,72 @@ __global__ void __launch_bounds__(AL_THREADS) allocate_scan_kernel(const __grid_
                 st = f & 3u;
             }
             const uint32_t incl = __ballot_sync(0xffffffffu, st == 2);
-            const int stop = incl ? __ffs(incl) - 1 : 31;  // nearest inclusive predecessor
-            int64_t vb = 0, vs = 0;
+            if (lane == 0) s_first[warp] = incl ? static_cast<uint32_t>(warp * 32 + __ffs(incl) - 1) : 0xffffffffu;
+            __syncthreads();
+            uint32_t stop = 0xffffffffu;  // nearest inclusive predecessor in this window
+#pragma unroll
+            for (int w = 0; w < AL_WARPS; ++w) stop = min(stop, s_first[w]);
+            uint64_t ve = 0;
             uint32_t vk = 0;
-            if (lane <= stop && idx >= 0) {
+            if (static_cast<uint32_t>(tid) <= stop && idx >= 0) {
                 const volatile AlTile* tv = T + idx;
-                vb = st == 2 ? tv->inc_b : tv->agg_b;
+                ve = st == 2 ? tv->inc_e : tv->agg_e;
                 vk = st == 2 ? tv->inc_k : tv->agg_k;
-                vs = st == 2 ? tv->inc_s : tv->agg_s;
             }
-            eb += warp_sum<int64_t>(vb);
-            ekk += warp_sum<uint32_t>(vk);
-            es += warp_sum<int64_t>(vs);
-            if (incl) break;
-            j -= 32;
+            ve = warp_sum<uint64_t>(ve);
+            vk = warp_sum<uint32_t>(vk);
+            if (lane == 0) {
+                s_red_e[warp] = ve;
+                s_red_k[warp] = vk;
+            }
+            __syncthreads();
+#pragma unroll
+            for (int w = 0; w < AL_WARPS; ++w) {
+                ee += s_red_e[w];
+                ekk += s_red_k[w];
+            }
+            __syncthreads();  // s_first / s_red are rewritten next round
+            if (stop != 0xffffffffu) break;
+            j -= AL_THREADS;
         }
-        if (lane == 0) {
+        if (tid == 0) {
+            const uint32_t tot_e = s_tot_e, tot_k = s_tot_k;
             if (tile != 0) {
-                T[tile].inc_b = eb + tot_b;
-                T[tile].inc_k = ekk + tot_k;
-                T[tile].inc_s = es + tot_s;
+                AlTile* Tw = p.tiles;
+                Tw[tile].inc_e = ee + tot_e;
+                Tw[tile].inc_k = ekk + tot_k;
                 __threadfence();
-                st_release(&T[tile].flag, ep | 2u);
+                st_release(&Tw[tile].flag, ep | 2u);
             }
-            s_excl_b = eb;
+            s_excl_e = ee;
             s_excl_k = ekk;
             if (tile == p.ntiles - 1) {
+                const uint64_t units = ee + tot_e;
                 if (p.n_kept) *p.n_kept = static_cast<uint64_t>(ekk) + tot_k;
-                if (p.total_budget) *p.total_budget = eb + tot_b;
-                if (p.tokens_saved) *p.tokens_saved = es + tot_s;
+                if (p.total_budget) *p.total_budget = static_cast<int64_t>(units * static_cast<uint64_t>(p.tpu));
+                if (p.tokens_saved)
+                    *p.tokens_saved = static_cast<int64_t>(
+                        (p.R * static_cast<uint64_t>(p.cap) - units) * static_cast<uint64_t>(p.tpu));
             }
         }
     }
     __syncthreads();
 
     // ---- global offsets and the stable kept list
+    const uint64_t tpu = static_cast<uint64_t>(p.tpu);
+    const uint64_t ebase = s_excl_e;
+    const uint32_t kbase = s_excl_k;
 #pragma unroll
     for (int i = 0; i < AL_ITEMS; ++i) {
         const uint64_t r = base + static_cast<uint64_t>(i) * AL_THREADS + tid;
+        const uint32_t x = pk[i];
+        const uint32_t own = __shfl_up_sync(0xffffffffu, x, 1);  // exclusive = inclusive of lane - 1
+        const uint32_t ex = lane ? own : 0u;
         if (r >= p.R) continue;
-        const int64_t b = static_cast<int64_t>(ek[i]) * p.tpu;
-        if (p.offsets) p.offsets[r] = p.base_offset + s_excl_b + s_wb[i * AL_WARPS + warp] + (ib[i] - b);
-        if (ek[i] > p.detect && p.kept) {
-            const uint32_t pos = s_excl_k + s_wk[i * AL_WARPS + warp] + ik[i] - 1u;
+        const uint64_t units = ebase + s_we[i * AL_WARPS + warp] + (ex >> 12);
+        if (p.offsets) p.offsets[r] = p.base_offset + static_cast<int64_t>(units * tpu);
+        if (p.kept && ((x - ex) & 1u)) {
+            const uint32_t pos = kbase + s_wk[i * AL_WARPS + warp] + (ex & 0xfffu);
             p.kept[pos] = p.kept_base + static_cast<uint32_t>(r);
         }
     }

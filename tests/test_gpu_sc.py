@@ -149,6 +149,30 @@ def test_allocate_scan_large_property(ctx):
     assert n_kept == int((out["granted"] > 5).sum())
 
 
+@pytest.mark.parametrize("kind,detect,cap,recheck", [(4, 1, 4096, 1000), (2, 4096, 4096, 1), (0, 1, 4096, 1),
+                                                     (4, 7, 4000, 1)])
+def test_allocate_scan_max_probes(ctx, kind, detect, cap, recheck):
+    """P = cap = 4096 (the largest knob): per-warp unit sums reach 32 x 4096 and per-tile sums
+    2048 x 4096, the limits of the packed scans; sparse random meets bits."""
+    import torch
+    from paper_2412_20993_b200 import AllocPolicy
+    R, P = 6001, 4096
+    rng = np.random.default_rng(cap + detect)
+    om = (rng.random((R, P // 32, 32)) < 0.002)
+    om = (om * (1 << np.arange(32, dtype=np.uint64))).sum(axis=2).astype(np.uint32)
+    meets = torch.from_numpy(om.view(np.int32)).cuda()
+    pol = AllocPolicy(kind=kind, detect_at=detect, resource_cap=cap, recheck_every=recheck, tokens_per_unit=3 << 30)
+    out = ctx.allocate_scan(meets, R, P, pol, base_offset=-5)
+    ctx.sync()
+    ref = O.allocate_scan(om, R, P, kind, detect, cap, recheck, 3 << 30, base_offset=-5)
+    for k in ("exit_knob", "reason", "granted", "offsets"):
+        assert np.array_equal(out[k].cpu().numpy(), ref[k].astype(out[k].cpu().numpy().dtype)), k
+    n_kept, saved, total = out["scalars"].cpu().numpy().tolist()
+    assert n_kept == ref["n_kept"]
+    assert saved == ref["tokens_saved"]
+    assert np.array_equal(out["kept"][:n_kept].cpu().numpy().view(np.uint32), ref["kept"])
+
+
 @pytest.mark.parametrize("distinct", [9, 17, 32])
 def test_sc_many_clusters_fallback(ctx, distinct):
     """Rows with more than PEEL_MAX clusters send their group to the warp-match engine; the
