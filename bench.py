@@ -38,7 +38,7 @@ UNIT = "probe-evals/s"
 
 CONFIGS = {
     # BASELINE.json configs; C is the north_star target shape (sharded per GPU)
-    "A": dict(kind="sc", R=1024, P=32, S=16, tau=0.7, detect=5, cap=32, interval=64, conv_hi=32, graph=True,
+    "A": dict(kind="sc", R=1024, P=32, S=16, tau=0.7, detect=5, cap=32, interval=64, conv_hi=32, graph=True, flush_l2=True,
               desc="SC entropy certaindex early exit, 1024 queries x 16 samples x 32 probes (K2 + K5 replayed as "
                    "one CUDA graph: launch-bound size)"),
     "B": dict(kind="cot", R=1 << 20, P=64, w=3, tau=0.9, interval=64, max_tokens=4096, hes=0.05, conv_hi=64,
@@ -49,7 +49,7 @@ CONFIGS = {
               desc="MCTS/Rebase reward + cumulative entropy certaindex, 256K programs x 64 nodes x 16 steps"),
     "E": dict(kind="gang", N=1 << 22, limit=0.5, prior=128.0,
               desc="gang-scheduling priority order (escalation + SJF + tie-break), 4M mixed programs"),
-    "J": dict(kind="jsonl", lines=1 << 20, programs=1 << 14,
+    "J": dict(kind="jsonl", lines=1 << 20, programs=1 << 14, flush_l2=True,
               desc="probe-trace JSONL ingestion (read_trace_jsonl), 1M records over 16K programs"),
 }
 TH_MCTS = [(0, 0.99, 0), (1, 0.4, 0)]   # PAPER.md:963 MCTS/GSM8K thresholds
@@ -330,10 +330,16 @@ def run_reference(args, cfg, rank, world):
 
 
 # ---------------------------------------------------------------- GPU legs
-def timed(args, world, launch, kernels):
+L2_FLUSH_BYTES = 512 << 20  # > the 126 MB L2
+NOMINAL_HBM_GBS = 8000.0     # B200 nominal HBM3e (SURVEY.md §8(d) reports against both)
+
+
+def timed(args, world, launch, kernels, flush_l2=False):
     """Warm up, then time exactly `steps` calls of launch(i) on torch's current stream with
     CUDA events (barrier + synchronize on both sides, max over ranks).  `kernels` names the
-    segments launch() brackets with per-segment events (for per-kernel durations)."""
+    segments launch() brackets with per-segment events (for per-kernel durations).
+    flush_l2 (working sets that fit in L2): a 512 MB buffer is rewritten before every step,
+    outside the step's own event pair, and the step time is the sum of the per-step pairs."""
     import torch
     stream = torch.cuda.current_stream()
     for _ in range(args.warmup):
@@ -343,15 +349,26 @@ def timed(args, world, launch, kernels):
     seg = {k: [] for k in kernels}
     t0 = torch.cuda.Event(enable_timing=True)
     t1 = torch.cuda.Event(enable_timing=True)
+    junk = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.int32, device="cuda") if flush_l2 else None
+    pairs = []
     with ClockSampler(torch.cuda.current_device()) as clk:
         torch.cuda.synchronize()
         t0.record(stream)
         for i in range(args.steps):
-            launch(seg)
+            if junk is not None:
+                junk.fill_(i)
+                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a.record(stream)
+                launch(seg)
+                b.record(stream)
+                pairs.append((a, b))
+            else:
+                launch(seg)
         t1.record(stream)
         torch.cuda.synchronize()
     barrier(world)
-    ms = max_over_ranks(t0.elapsed_time(t1), world) / args.steps
+    total = sum(a.elapsed_time(b) for a, b in pairs) if pairs else t0.elapsed_time(t1)
+    ms = max_over_ranks(total, world) / args.steps
     per = {k: statistics.mean(a.elapsed_time(b) for a, b in v) if v else None for k, v in seg.items()}
     return ms, per, clk.summary()
 
@@ -415,7 +432,7 @@ def bench_sc(args, cfg, rank, world, cx, with_e2e=True):
                 seg["allocate_scan"].append(seg["sc_certaindex"][-1])
 
     l0 = cx.launches
-    ms, per, clocks = timed(args, world, step, ["sc_certaindex", "allocate_scan"])
+    ms, per, clocks = timed(args, world, step, ["sc_certaindex", "allocate_scan"], cfg.get("flush_l2", False))
     launches = in_timed(cx, l0, args)
     n_kept = int(out["scalars"][0])
     k2_bytes = R * P * S * 4 + R * P * 4 + R * ((P + 31) // 32) * 4
@@ -564,7 +581,7 @@ def bench_jsonl(args, cfg, rank, world, cx, with_e2e=True):
             e.record(torch.cuda.current_stream())
 
     l0 = cx.launches
-    ms, per, clocks = timed(args, world, step, ["jsonl_parse"])
+    ms, per, clocks = timed(args, world, step, ["jsonl_parse"], cfg.get("flush_l2", False))
     n = out["n_records"]
     b = len(text) + n * (4 + 4 + 8 + 1 + 8 + 8) + n * 8
     return dict(value=n * world / (ms / 1e3), ms=ms, launches=in_timed(cx, l0, args), clocks=clocks,
@@ -579,7 +596,8 @@ def summarize(name, cfg, res, peak):
     ach = res["kernel_bytes"] / (res["kernel_ms"] / 1e3) / 1e9
     return {"value": res["value"], "unit": UNIT, "ms_per_step": res["ms"], "desc": cfg["desc"],
             "kernel": res["kernel"], "kernel_ms": res["kernel_ms"], "achieved_gbs": ach, "frac": ach / peak,
-            **res["extra"]}
+            "frac_nominal": ach / NOMINAL_HBM_GBS,
+            "l2": "flushed before every timed step" if cfg.get("flush_l2") else "inputs > L2", **res["extra"]}
 
 
 def main():
@@ -628,7 +646,8 @@ def main():
                                    if cfg["kind"] == "gang" else
                                    f"request shards x{world} (no data-path collective; 8 B/rank allgather "
                                    "of budget totals for global offsets)"),
-                   "l2": "inputs > L2 (126 MB) for C/B/D/E: no flush needed"}
+                   "l2": ("L2 flushed before every timed step (512 MB write, outside the step's events)"
+                          if cfg.get("flush_l2") else "inputs > L2 (126 MB): no flush needed")}
         line = {
             "metric": METRIC, "value": res["value"], "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": res["ms"], "higher_is_better": True,
@@ -636,6 +655,7 @@ def main():
             "vs_baseline": None, "dtype": "u32 ids / f64 certaindex (f32 store)", "data": "synthetic",
             "config": cfg_out,
             "roofline": {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
+                         "frac_nominal": ach / NOMINAL_HBM_GBS,  # also vs the 8 TB/s nominal
                          "traffic": traffic["bytes"] if traffic else None,
                          "traffic_source": traffic and f"{traffic['source']} ({traffic['kernel'][:60]})",
                          "peak_source": peak_src, "kernel": res["kernel"],
