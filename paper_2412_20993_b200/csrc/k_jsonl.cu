@@ -281,6 +281,59 @@ __device__ uint64_t scan_number(const char* t, uint64_t p, uint64_t e) {
     return p;
 }
 
+// strtod overflow (nlohmann: out_of_range.406 "number overflow", a parse error of the whole
+// line, for a number at any depth): a decimal rounds to infinity iff its value is at least
+// 2^1024 - 2^970 (the midpoint above DBL_MAX; ties go to the even, infinite, side).  With
+// E10 the decimal exponent of the leading significant digit, E10 > 308 always overflows,
+// E10 < 308 never does, and E10 == 308 compares the digit string with the boundary's 309.
+__constant__ char kOvfDigits[310] =
+    "179769313486231580793728971405303415079934132710037826936173778980444968292764750946649017977587207096330286416692887910946555547851940402630657488671505820681908902000708383676273854845817711531764475730270069855571366959622842914819860834936475292719074168444365510704342711559699508093042880177904174497792";
+
+// number token [b, e) (grammar already validated); exponents saturate far beyond +-308
+__device__ bool num_overflows(const char* t, uint64_t b, uint64_t e) {
+    uint64_t p = b;
+    if (t[p] == '-') ++p;
+    long long e10;
+    uint64_t first;  // index of the first significant digit
+    uint64_t q = p;
+    while (q < e && t[q] >= '0' && t[q] <= '9') ++q;
+    const uint64_t int_end = q;
+    if (!(int_end - p == 1 && t[p] == '0')) {
+        first = p;
+        e10 = static_cast<long long>(int_end - p) - 1;
+    } else {  // 0.000ddd: the first nonzero fraction digit
+        if (q >= e || t[q] != '.') return false;  // plain 0 (with or without exponent)
+        ++q;
+        const uint64_t fb = q;
+        while (q < e && t[q] == '0') ++q;
+        if (q >= e || t[q] < '1' || t[q] > '9') return false;  // the value is zero
+        first = q;
+        e10 = -static_cast<long long>(q - fb) - 1;
+    }
+    uint64_t x = first;
+    while (x < e && t[x] != 'e' && t[x] != 'E') ++x;
+    if (x < e) {  // exponent, saturated
+        ++x;
+        bool en = false;
+        if (t[x] == '+' || t[x] == '-') {
+            en = t[x] == '-';
+            ++x;
+        }
+        long long v = 0;
+        for (; x < e; ++x) v = v < 100000000 ? v * 10 + (t[x] - '0') : v;
+        e10 += en ? -v : v;
+    }
+    if (e10 != 308) return e10 > 308;
+    int k = 0;  // digits compared so far
+    for (uint64_t y = first; y < e && t[y] != 'e' && t[y] != 'E'; ++y) {
+        if (t[y] == '.') continue;
+        if (k == 309) return true;  // equal on all 309 digits, more follow: >= the boundary
+        const char c = t[y], d = kOvfDigits[k++];
+        if (c != d) return c > d;
+    }
+    return k == 309;  // a shorter equal prefix is below the boundary (its tail is nonzero)
+}
+
 // nlohmann number -> (int64 | uint64 | double); returns 0 int64, 1 uint64, 2 double, -1 unsupported
 __device__ int number_value(const char* t, uint64_t b, uint64_t e, long long* iv, unsigned long long* uv,
                             double* dv) {
@@ -465,7 +518,7 @@ __global__ void parse_lines(const char* __restrict__ t, uint64_t n, const uint64
                     p = r;
                 } else if (c == '-' || (c >= '0' && c <= '9')) {
                     const uint64_t r = scan_number(t, p, e);
-                    if (!r) {
+                    if (!r || num_overflows(t, p, r)) {
                         ok = false;
                         break;
                     }
