@@ -151,7 +151,10 @@ struct Span {
     uint8_t kind = 0;       // 0 absent, 1 string, 2 number, 3 true, 4 false, 5 null, 6 array, 7 object
 };
 
-__device__ __forceinline__ bool jws(char c) { return c == ' ' || c == '\t' || c == '\n' || c == '\r'; }
+__device__ __forceinline__ bool jws(char c) {  // ' ' \t \n \r as one mask test
+    const uint32_t u = static_cast<unsigned char>(c);
+    return u <= 32u && ((0x100002600ull >> u) & 1ull);
+}
 __device__ __forceinline__ bool trim_ws(char c) {
     return c == ' ' || c == '\t' || c == '\n' || c == '\r' || c == '\f' || c == '\v';
 }
@@ -163,23 +166,63 @@ __device__ __forceinline__ int hexv(char c) {
 }
 
 // Validate (and optionally decode) the string whose opening quote is at t[p]; returns the
-// index after the closing quote, or 0 on error.  out/len: decoded bytes (nullable out).
-__device__ uint64_t scan_string(const char* t, uint64_t p, uint64_t e, char* out, uint32_t out_cap,
-                                uint32_t* len) {
+// index after the closing quote, or 0 on error.  len: decoded length; esc: a backslash
+// escape occurred.  MODE 0 validates only, 1 also packs the first 16 decoded bytes into
+// k0/k1 (member keys), 2 also writes the decoded bytes to out[0, out_cap).
+// Runs of plain bytes (0x20..0x7F except '"' and '\') are taken 8 at a time: one aligned
+// 16-byte window per step (inside the text: nt is its length), the classes found with SWAR
+// byte tests whose lowest flagged byte is exact (borrows only travel upward).
+template <int MODE>
+__device__ __forceinline__ uint64_t scan_str(const char* __restrict__ t, uint64_t p, uint64_t e, uint64_t nt,
+                                             uint32_t& len, bool& esc, uint64_t& k0, uint64_t& k1,
+                                             char* __restrict__ out, uint32_t out_cap) {
     ++p;
     uint32_t o = 0;
     auto put = [&](uint32_t c) {
-        if (out && o < out_cap) out[o] = static_cast<char>(c);
+        if (MODE == 1) {
+            if (o < 8) k0 |= static_cast<uint64_t>(c) << (8 * o);
+            else if (o < 16) k1 |= static_cast<uint64_t>(c) << (8 * (o - 8));
+        }
+        if (MODE == 2 && o < out_cap) out[o] = static_cast<char>(c);
         ++o;
     };
+    constexpr uint64_t ONES = 0x0101010101010101ull, HI = 0x8080808080808080ull;
     while (p < e) {
+        if (p + 8 <= e && (p & ~7ull) + 16 <= nt) {
+            const uint64_t al = p & ~7ull;
+            const uint32_t sh = static_cast<uint32_t>(p & 7) * 8;
+            const uint64_t w0 = *reinterpret_cast<const uint64_t*>(t + al);
+            const uint64_t w1 = *reinterpret_cast<const uint64_t*>(t + al + 8);
+            const uint64_t x = sh ? (w0 >> sh) | (w1 << (64 - sh)) : w0;
+            const uint64_t q = x ^ (ONES * '"'), b = x ^ (ONES * '\\');
+            const uint64_t m = ((x - ONES * 0x20) & ~x) | ((q - ONES) & ~q) | ((b - ONES) & ~b) | x;
+            const uint64_t f = m & HI;
+            const uint32_t j = f ? static_cast<uint32_t>(__ffsll(static_cast<long long>(f)) - 1) >> 3 : 8u;
+            if (MODE == 1) {  // the j plain bytes enter the packed key at byte offset o
+                const uint64_t c = j == 8 ? x : x & ((1ull << (8 * j)) - 1ull);
+                if (o < 8) {
+                    k0 |= c << (8 * o);
+                    if (o) k1 |= c >> (64 - 8 * o);
+                } else if (o < 16) {
+                    k1 |= c << (8 * (o - 8));
+                }
+                o += j;
+            } else if (MODE == 2) {
+                for (uint32_t k = 0; k < j; ++k) put(static_cast<uint32_t>(x >> (8 * k)) & 0xffu);
+            } else {
+                o += j;
+            }
+            p += j;
+            if (j == 8) continue;
+        }
         const unsigned char c = static_cast<unsigned char>(t[p]);
         if (c == '"') {
-            if (len) *len = o;
+            len = o;
             return p + 1;
         }
         if (c < 0x20) return 0;
         if (c == '\\') {
+            esc = true;
             if (p + 1 >= e) return 0;
             const char x = t[p + 1];
             p += 2;
@@ -257,8 +300,11 @@ __device__ uint64_t scan_string(const char* t, uint64_t p, uint64_t e, char* out
     return 0;
 }
 
-// number token at t[p]: returns the end index or 0
-__device__ uint64_t scan_number(const char* t, uint64_t p, uint64_t e) {
+// number token at t[p]: returns the end index or 0; big: it has an exponent or is long
+// enough (> 300 bytes) that it could overflow a double
+__device__ uint64_t scan_number(const char* t, uint64_t p, uint64_t e, bool& big) {
+    const uint64_t p0 = p;
+    big = false;
     if (p < e && t[p] == '-') ++p;
     if (p >= e || t[p] < '0' || t[p] > '9') return 0;
     if (t[p] == '0') {
@@ -273,11 +319,13 @@ __device__ uint64_t scan_number(const char* t, uint64_t p, uint64_t e) {
         while (p < e && t[p] >= '0' && t[p] <= '9') ++p;
     }
     if (p < e && (t[p] == 'e' || t[p] == 'E')) {
+        big = true;
         ++p;
         if (p < e && (t[p] == '+' || t[p] == '-')) ++p;
         if (p >= e || t[p] < '0' || t[p] > '9') return 0;
         while (p < e && t[p] >= '0' && t[p] <= '9') ++p;
     }
+    big = big || p - p0 > 300;
     return p;
 }
 
@@ -425,23 +473,26 @@ __device__ __forceinline__ int trunc_i(double v) {
 }
 
 // key of interest: 0 program_id, 1 step_index, 2 token_offset, 3 answer, 4 hesitant, -1 other
-__device__ int key_id(const char* k, uint32_t n) {
-    auto eq = [&](const char* s, uint32_t sn) {
-        if (n != sn) return false;
-        for (uint32_t i = 0; i < n; ++i)
-            if (k[i] != s[i]) return false;
-        return true;
-    };
-    if (eq("program_id", 10)) return 0;
-    if (eq("step_index", 10)) return 1;
-    if (eq("token_offset", 12)) return 2;
-    if (eq("answer", 6)) return 3;
-    if (eq("hesitant", 8)) return 4;
+// (decoded key: length n, first 16 bytes packed little-endian in k0/k1)
+constexpr uint64_t pack8(const char* s, int from, int n) {
+    uint64_t v = 0;
+    for (int i = 0; i < 8 && from + i < n; ++i) v |= static_cast<uint64_t>(static_cast<unsigned char>(s[from + i])) << (8 * i);
+    return v;
+}
+__device__ __forceinline__ int key_id(uint64_t k0, uint64_t k1, uint32_t n) {
+    if (n == 10 && k0 == pack8("program_id", 0, 10) && k1 == pack8("program_id", 8, 10)) return 0;
+    if (n == 10 && k0 == pack8("step_index", 0, 10) && k1 == pack8("step_index", 8, 10)) return 1;
+    if (n == 12 && k0 == pack8("token_offset", 0, 12) && k1 == pack8("token_offset", 8, 12)) return 2;
+    if (n == 6 && k0 == pack8("answer", 0, 6) && k1 == 0) return 3;
+    if (n == 8 && k0 == pack8("hesitant", 0, 8) && k1 == 0) return 4;
     return -1;
 }
 
 struct LineOut {
     uint8_t* st;
+    uint32_t* pid_len;  // decoded lengths of the program id and the answer
+    uint32_t* ans_len;
+    uint8_t* esc;       // bit 0: the program id has escapes, bit 1: the answer has
     uint64_t* pid_b;
     uint64_t* pid_e;
     uint64_t* ans_b;
@@ -451,8 +502,14 @@ struct LineOut {
     uint8_t* hes;
 };
 
-__global__ void parse_lines(const char* __restrict__ t, uint64_t n, const uint64_t* __restrict__ nl, uint64_t n_nl,
-                            uint64_t n_lines, LineOut o, unsigned long long* first_bad) {
+// One thread per line.  The container stack is a bitmask (bit d: the container at depth
+// d is an object), the five fields of interest live in registers (written through an
+// unrolled select, so no local-memory array), member keys are decoded into two registers
+// and compared as packed words, and strings advance 8 plain bytes per step (scan_str).
+__global__ void __launch_bounds__(128) parse_lines(const char* __restrict__ t, uint64_t n,
+                                                   const uint64_t* __restrict__ nl, uint64_t n_nl, uint64_t n_lines,
+                                                   LineOut o, unsigned long long* first_bad) {
+    static_assert(JL_DEPTH <= 64, "one bit per nesting level");
     for (uint64_t L = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; L < n_lines;
          L += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
         const uint64_t b = L == 0 ? 0 : nl[L - 1] + 1;
@@ -466,8 +523,17 @@ __global__ void parse_lines(const char* __restrict__ t, uint64_t n, const uint64
             continue;
         }
         // ---- validate the document (iterative, explicit container stack)
-        Span f[5];
-        uint8_t stack[JL_DEPTH];
+        uint64_t fb[5], fe[5];
+        uint32_t fl[5];
+        uint8_t fk[5], fx[5];
+#pragma unroll
+        for (int k = 0; k < 5; ++k) fb[k] = fe[k] = 0, fl[k] = 0, fk[k] = 0, fx[k] = 0;
+        auto set_field = [&](int key, uint64_t vb, uint64_t ve, uint8_t kind, uint32_t dl, bool dx) {
+#pragma unroll
+            for (int k = 0; k < 5; ++k)
+                if (k == key) fb[k] = vb, fe[k] = ve, fk[k] = kind, fl[k] = dl, fx[k] = dx;
+        };
+        uint64_t objmask = 0;  // bit d: container at depth d is an object
         int depth = 0;
         uint64_t p = b;
         bool ok = true;
@@ -475,6 +541,9 @@ __global__ void parse_lines(const char* __restrict__ t, uint64_t n, const uint64
         bool top_obj = false;
         // states: 0 expect value, 1 after value, 2 expect key or '}', 3 expect key
         int state = 0;
+        uint64_t k0, k1;
+        uint32_t slen;
+        bool sesc;
         while (ok) {
             while (p < e && jws(t[p])) ++p;
             if (state == 0) {
@@ -484,16 +553,17 @@ __global__ void parse_lines(const char* __restrict__ t, uint64_t n, const uint64
                 }
                 const char c = t[p];
                 const uint64_t vb = p;
-                uint8_t kind = 0;
+                const bool field = depth == 1 && top_obj && pending_key >= 0;
                 if (c == '{' || c == '[') {
                     if (depth == JL_DEPTH) {
                         ok = false;
                         break;
                     }
                     if (depth == 0 && c == '{') top_obj = true;
-                    if (depth == 1 && top_obj && pending_key >= 0) f[pending_key] = Span{vb, vb, c == '{' ? uint8_t(7) : uint8_t(6)};
+                    if (field) set_field(pending_key, vb, vb, c == '{' ? uint8_t(7) : uint8_t(6), 0, false);
                     pending_key = -2;
-                    stack[depth++] = c == '{' ? 1 : 2;
+                    objmask = (objmask & ~(1ull << depth)) | (static_cast<uint64_t>(c == '{') << depth);
+                    ++depth;
                     ++p;
                     state = c == '{' ? 2 : 0;
                     if (c == '[') {  // empty array?
@@ -508,37 +578,38 @@ __global__ void parse_lines(const char* __restrict__ t, uint64_t n, const uint64
                     continue;
                 }
                 if (c == '"') {
-                    const uint64_t r = scan_string(t, p, e, nullptr, 0, nullptr);
+                    sesc = false;
+                    const uint64_t r = scan_str<0>(t, p, e, n, slen, sesc, k0, k1, nullptr, 0);
                     if (!r) {
                         ok = false;
                         break;
                     }
-                    kind = 1;
-                    if (depth == 1 && top_obj && pending_key >= 0) f[pending_key] = Span{vb + 1, r - 1, kind};
+                    if (field) set_field(pending_key, vb + 1, r - 1, 1, slen, sesc);
                     p = r;
                 } else if (c == '-' || (c >= '0' && c <= '9')) {
-                    const uint64_t r = scan_number(t, p, e);
-                    if (!r || num_overflows(t, p, r)) {
+                    bool big;
+                    const uint64_t r = scan_number(t, p, e, big);
+                    if (!r || (big && num_overflows(t, p, r))) {
                         ok = false;
                         break;
                     }
-                    if (depth == 1 && top_obj && pending_key >= 0) f[pending_key] = Span{vb, r, 2};
+                    if (field) set_field(pending_key, vb, r, 2, 0, false);
                     p = r;
                 } else {
-                    const char* lit = c == 't' ? "true" : (c == 'f' ? "false" : (c == 'n' ? "null" : nullptr));
-                    if (!lit) {
+                    // true / false / null, compared as one packed word
+                    const uint32_t ln = c == 'f' ? 5 : 4;
+                    const uint64_t want = c == 't' ? 0x65757274ull : (c == 'f' ? 0x65736c6166ull : 0x6c6c756eull);
+                    if ((c != 't' && c != 'f' && c != 'n') || p + ln > e) {
                         ok = false;
                         break;
                     }
-                    uint32_t ln = c == 'f' ? 5 : 4;
-                    if (p + ln > e) {
+                    uint64_t got = 0;
+                    for (uint32_t k = 0; k < ln; ++k) got |= static_cast<uint64_t>(static_cast<unsigned char>(t[p + k])) << (8 * k);
+                    if (got != want) {
                         ok = false;
                         break;
                     }
-                    for (uint32_t k = 0; k < ln; ++k) ok = ok && t[p + k] == lit[k];
-                    if (!ok) break;
-                    kind = c == 't' ? 3 : (c == 'f' ? 4 : 5);
-                    if (depth == 1 && top_obj && pending_key >= 0) f[pending_key] = Span{vb, p + ln, kind};
+                    if (field) set_field(pending_key, vb, p + ln, c == 't' ? 3 : (c == 'f' ? 4 : 5), 0, false);
                     p += ln;
                 }
                 pending_key = -2;
@@ -546,6 +617,7 @@ __global__ void parse_lines(const char* __restrict__ t, uint64_t n, const uint64
                 if (depth == 0) break;  // the top-level value was a scalar
                 continue;
             }
+            const bool in_obj = depth > 0 && ((objmask >> (depth - 1)) & 1ull);
             if (state == 1) {  // after a value inside a container
                 if (depth == 0) break;
                 if (p >= e) {
@@ -555,8 +627,8 @@ __global__ void parse_lines(const char* __restrict__ t, uint64_t n, const uint64
                 const char c = t[p];
                 if (c == ',') {
                     ++p;
-                    state = stack[depth - 1] == 1 ? 3 : 0;
-                } else if ((c == '}' && stack[depth - 1] == 1) || (c == ']' && stack[depth - 1] == 2)) {
+                    state = in_obj ? 3 : 0;
+                } else if ((c == '}' && in_obj) || (c == ']' && !in_obj)) {
                     ++p;
                     --depth;
                     state = 1;
@@ -582,14 +654,13 @@ __global__ void parse_lines(const char* __restrict__ t, uint64_t n, const uint64
                 ok = false;
                 break;
             }
-            char kb[16];
-            uint32_t kn = 0;
-            const uint64_t r = scan_string(t, p, e, kb, 16, &kn);
+            k0 = k1 = 0;
+            const uint64_t r = scan_str<1>(t, p, e, n, slen, sesc, k0, k1, nullptr, 0);
             if (!r) {
                 ok = false;
                 break;
             }
-            pending_key = (depth == 1 && top_obj && kn <= 16) ? key_id(kb, kn) : -1;
+            pending_key = (depth == 1 && top_obj) ? key_id(k0, k1, slen) : -1;
             p = r;
             while (p < e && jws(t[p])) ++p;
             if (p >= e || t[p] != ':') {
@@ -609,15 +680,15 @@ __global__ void parse_lines(const char* __restrict__ t, uint64_t n, const uint64
             st = L_FIELD;  // at() on a non-object
         } else {
             // ---- fields in the reference's order (probe.cpp:140-145)
-            if (f[0].kind != 1) st = L_FIELD;
+            if (fk[0] != 1) st = L_FIELD;
             long long iv = 0;
             unsigned long long uv = 0;
             double dv = 0;
             if (st == L_RECORD) {  // step_index: get<int>() (numbers and booleans)
-                if (f[1].kind == 3 || f[1].kind == 4) {
-                    o.step[L] = f[1].kind == 3 ? 1 : 0;
-                } else if (f[1].kind == 2) {
-                    const int k = number_value(t, f[1].b, f[1].e, &iv, &uv, &dv);
+                if (fk[1] == 3 || fk[1] == 4) {
+                    o.step[L] = fk[1] == 3 ? 1 : 0;
+                } else if (fk[1] == 2) {
+                    const int k = number_value(t, fb[1], fe[1], &iv, &uv, &dv);
                     if (k < 0) st = L_UNSUPPORTED;
                     else o.step[L] = k == 0 ? static_cast<int>(iv) : (k == 1 ? static_cast<int>(uv) : trunc_i(dv));
                 } else {
@@ -625,24 +696,27 @@ __global__ void parse_lines(const char* __restrict__ t, uint64_t n, const uint64
                 }
             }
             if (st == L_RECORD) {  // token_offset: get<long>() (numbers only)
-                if (f[2].kind == 2) {
-                    const int k = number_value(t, f[2].b, f[2].e, &iv, &uv, &dv);
+                if (fk[2] == 2) {
+                    const int k = number_value(t, fb[2], fe[2], &iv, &uv, &dv);
                     if (k < 0) st = L_UNSUPPORTED;
                     else o.tok[L] = k == 0 ? iv : (k == 1 ? static_cast<long long>(uv) : trunc_ll(dv));
                 } else {
                     st = L_FIELD;
                 }
             }
-            if (st == L_RECORD && f[3].kind != 1) st = L_FIELD;
+            if (st == L_RECORD && fk[3] != 1) st = L_FIELD;
             if (st == L_RECORD) {  // hesitant: value("hesitant", false) -> bool or absent
-                if (f[4].kind == 0) o.hes[L] = 0;
-                else if (f[4].kind == 3 || f[4].kind == 4) o.hes[L] = f[4].kind == 3;
+                if (fk[4] == 0) o.hes[L] = 0;
+                else if (fk[4] == 3 || fk[4] == 4) o.hes[L] = fk[4] == 3;
                 else st = L_FIELD;
             }
-            o.pid_b[L] = f[0].b;
-            o.pid_e[L] = f[0].e;
-            o.ans_b[L] = f[3].b;
-            o.ans_e[L] = f[3].e;
+            o.pid_b[L] = fb[0];
+            o.pid_e[L] = fe[0];
+            o.ans_b[L] = fb[3];
+            o.ans_e[L] = fe[3];
+            o.pid_len[L] = fl[0];
+            o.ans_len[L] = fl[3];
+            o.esc[L] = static_cast<uint8_t>(fx[0] | (fx[3] << 1));
         }
         o.st[L] = st;
         if (st != L_RECORD) atomicMin(first_bad, static_cast<unsigned long long>(L));
@@ -703,15 +777,12 @@ __global__ void gather_records(const char* __restrict__ t, const uint8_t* __rest
         r_tok[r] = o.tok[L];
         r_hes[r] = o.hes[L];
         r_line[r] = L;
-        uint32_t a = 0, b = 0;
-        scan_string(t, o.pid_b[L] - 1, o.pid_e[L] + 1, nullptr, 0, &a);
-        scan_string(t, o.ans_b[L] - 1, o.ans_e[L] + 1, nullptr, 0, &b);
-        pid_len[r] = a + 2;  // wrapped in sentinel bytes for exact interning
-        ans_len[r] = b;
+        pid_len[r] = o.pid_len[L] + 2;  // wrapped in sentinel bytes for exact interning
+        ans_len[r] = o.ans_len[L];
     }
 }
 
-__global__ void write_strings(const char* __restrict__ t, const uint8_t* __restrict__ st,
+__global__ void write_strings(const char* __restrict__ t, uint64_t n, const uint8_t* __restrict__ st,
                               const uint32_t* __restrict__ pos, uint64_t n_lines, LineOut o,
                               const uint64_t* __restrict__ pid_off, char* __restrict__ pid_arena,
                               const uint64_t* __restrict__ ans_off, char* __restrict__ ans_arena) {
@@ -722,11 +793,21 @@ __global__ void write_strings(const char* __restrict__ t, const uint8_t* __restr
         char* pp = pid_arena + pid_off[r];
         const uint32_t cap = static_cast<uint32_t>(pid_off[r + 1] - pid_off[r]);
         pp[0] = '\x01';
+        const uint8_t x = o.esc[L];
         uint32_t k = 0;
-        scan_string(t, o.pid_b[L] - 1, o.pid_e[L] + 1, pp + 1, cap - 2, &k);
+        bool dx = false;
+        uint64_t d0 = 0, d1 = 0;
+        if (x & 1u)
+            scan_str<2>(t, o.pid_b[L] - 1, o.pid_e[L] + 1, n, k, dx, d0, d1, pp + 1, cap - 2);
+        else
+            for (uint64_t i = o.pid_b[L]; i < o.pid_e[L]; ++i) pp[1 + i - o.pid_b[L]] = t[i];
         pp[cap - 1] = '\x01';
-        scan_string(t, o.ans_b[L] - 1, o.ans_e[L] + 1, ans_arena + ans_off[r],
-                    static_cast<uint32_t>(ans_off[r + 1] - ans_off[r]), &k);
+        char* ap = ans_arena + ans_off[r];
+        if (x & 2u)
+            scan_str<2>(t, o.ans_b[L] - 1, o.ans_e[L] + 1, n, k, dx, d0, d1, ap,
+                        static_cast<uint32_t>(ans_off[r + 1] - ans_off[r]));
+        else
+            for (uint64_t i = o.ans_b[L]; i < o.ans_e[L]; ++i) ap[i - o.ans_b[L]] = t[i];
     }
 }
 
@@ -844,7 +925,7 @@ extern "C" int cdx_jsonl_parse(cdx_ctx* ctx, const char* text, uint64_t nbytes, 
     // phase 2 (dedicated buffer sized from the line count): every later array is bounded by
     // n_lines records and nbytes of text
     const uint64_t nl1 = n_lines + 1;
-    const size_t bulk = 256 * 40 + nl1 * (8 + 1 + 8 * 4 + 4 + 8 + 1 + 4) + (nl1 / 1024 + 2) * 4 +
+    const size_t bulk = 256 * 40 + nl1 * (8 + 1 + 8 * 4 + 4 + 8 + 1 + 4 + 4 + 4 + 1) + (nl1 / 1024 + 2) * 4 +
                         nl1 * (8 + 4 + 4 + 8 + 1 + 8 + 8 + 4 + 4) + (3 * nbytes / 2 + 2 * nl1 + 64) +
                         radix_scratch_words(nl1) * 4;
     if (ctx->jl_bytes < bulk) {
@@ -870,6 +951,9 @@ extern "C" int cdx_jsonl_parse(cdx_ctx* ctx, const char* text, uint64_t nbytes, 
     o.step = carve<int32_t>(p, n_lines);
     o.tok = carve<int64_t>(p, n_lines);
     o.hes = carve<uint8_t>(p, n_lines);
+    o.pid_len = carve<uint32_t>(p, n_lines);
+    o.ans_len = carve<uint32_t>(p, n_lines);
+    o.esc = carve<uint8_t>(p, n_lines);
     uint32_t* pos = carve<uint32_t>(p, n_lines);
     uint32_t* sums = carve<uint32_t>(p, (n_lines + 1023) / 1024 + 1);
     parse_lines<<<gridn(ctx, n_lines), 128, 0, ctx->stream>>>(text, nbytes, nl, h_nl, n_lines, o,
@@ -912,7 +996,7 @@ extern "C" int cdx_jsonl_parse(cdx_ctx* ctx, const char* text, uint64_t nbytes, 
         if (int st = scan_u32_inplace(ctx, tmp, nr, sums, misc + 3)) return st;
         shift_offsets<<<gridn(ctx, nr + 1), 256, 0, ctx->stream>>>(tmp, pid_len, nr, pid_off);
         CDX_CHECK_LAUNCH(ctx, "jsonl(program offsets)");
-        write_strings<<<gridn(ctx, n_lines), 128, 0, ctx->stream>>>(text, o.st, pos, n_lines, o, pid_off, pid_arena,
+        write_strings<<<gridn(ctx, n_lines), 128, 0, ctx->stream>>>(text, nbytes, o.st, pos, n_lines, o, pid_off, pid_arena,
                                                                     answer_off, answer_arena);
         CDX_CHECK_LAUNCH(ctx, "jsonl(strings)");
         // exact program interning (sentinel-wrapped: trimming cannot merge ids)
