@@ -79,7 +79,9 @@ def _to_dev(soa):
 
 @pytest.mark.parametrize("N,order,limit,sorted_arrival", [(1, 1, 1.0, True), (1000, 1, 0.7, True),
                                                           (100000, 1, 0.5, True), (50000, 0, 0.5, True),
-                                                          (70000, 1, 0.9, False), (5000, 0, 100.0, False)])
+                                                          (70000, 1, 0.9, False), (5000, 0, 100.0, False),
+                                                          (4096, 1, 0.5, True), (4097, 1, 0.5, False),
+                                                          (8193, 0, 0.5, False), (1 << 22, 1, 0.5, True)])
 def test_gang_parity(ctx, N, order, limit, sorted_arrival):
     from paper_2412_20993_b200 import InterPolicy
     soa, now = _gang_inputs(N, N + order, sorted_arrival=sorted_arrival)
@@ -88,6 +90,39 @@ def test_gang_parity(ctx, N, order, limit, sorted_arrival):
     ctx.sync()
     ref, resc = O.gang_order(soa, order, limit, 128.0, now)
     assert np.array_equal(esc.cpu().numpy(), resc)
+    assert np.array_equal(got.cpu().numpy().view(np.uint32), ref)
+
+
+@pytest.mark.parametrize("case", ["identical", "all_escalated", "one_digit"])
+def test_gang_degenerate_keys(ctx, case):
+    """Keys that agree on most or all radix digits (skipped passes, single-digit sorts,
+    ties resolved purely by arrival then program id)."""
+    from paper_2412_20993_b200 import InterPolicy
+    N = 20000
+    soa, now = _gang_inputs(N, 3, frac_term=0.0)
+    if case == "identical":
+        for k in ("arrival", "last_service"):
+            soa[k][:] = 1.0
+        soa["iter_tok_sum"][:] = 640
+        soa["iter_count"][:] = 5
+        soa["cap"][:] = 10
+        soa["knob"][:] = 3
+        now = 1.5
+    elif case == "all_escalated":
+        soa["last_service"][:] = 0.0
+        now = float(soa["arrival"].max()) + 10.0
+    else:  # sjf keys that differ only in their lowest mantissa byte
+        soa["iter_count"][:] = 1
+        soa["iter_tok_sum"][:] = 1 << 20
+        soa["cap"][:] = 2
+        soa["knob"][:] = 1
+        soa["arrival"][:] = np.sort(soa["arrival"])
+        soa["last_service"][:] = soa["arrival"]
+        now = float(soa["arrival"].max()) + 0.1
+    pol = InterPolicy(order=1, starvation_limit=1.0, prior_tokens=128.0)
+    got, _, _ = ctx.gang_priority(_to_dev(soa), pol, now)
+    ctx.sync()
+    ref, _ = O.gang_order(soa, 1, 1.0, 128.0, now)
     assert np.array_equal(got.cpu().numpy().view(np.uint32), ref)
 
 
