@@ -565,9 +565,9 @@ __global__ void __launch_bounds__(RS_THREADS) rr_scatter(const uint64_t* __restr
 // counts on the host (saves a launch and a sync).  `vmap`/`vfinal` (nullable): the last
 // pass writes vmap[value] to vfinal instead of the value (folds the caller's final gather).
 // *which: 0 result in k0/v0, 1 in k1/v1, 2 keys in k0/k1 as for (pass count & 1) and the
-// mapped values in vfinal.
+// mapped values in vfinal.  dlo: sort by digits [dlo, 8) only (the upper bytes).
 int radix_sort(cdx_ctx* ctx, uint64_t* k0, uint32_t* v0, uint64_t* k1, uint32_t* v1, uint64_t n, uint32_t* lb,
-               int* which, const uint32_t* hh, const uint32_t* vmap, uint32_t* vfinal) {
+               int* which, const uint32_t* hh, const uint32_t* vmap, uint32_t* vfinal, int dlo = 0) {
     *which = 0;
     if (n <= 1) return CDX_OK;
     const uint32_t ntiles = static_cast<uint32_t>((n + RS_TILE - 1) / RS_TILE);
@@ -608,7 +608,8 @@ int radix_sort(cdx_ctx* ctx, uint64_t* k0, uint32_t* v0, uint64_t* k1, uint32_t*
     int last = -1;
     bool nontrivial[8];
     for (int d = 0; d < 8; ++d) {
-        nontrivial[d] = true;
+        nontrivial[d] = d >= dlo;  // digits below dlo are left to the caller
+        if (!nontrivial[d]) continue;
         for (int b = 0; b < 256; ++b)
             if (hh[d * 256 + b]) {
                 nontrivial[d] = hh[d * 256 + b] != n;
@@ -640,6 +641,79 @@ int radix_sort(cdx_ctx* ctx, uint64_t* k0, uint32_t* v0, uint64_t* k1, uint32_t*
     }
     *which = mapped ? 2 : (kin == k0 ? 0 : 1);
     return CDX_OK;
+}
+
+// ---- upper-half sort + run fix-up --------------------------------------------------------
+// The priority word is first sorted (stably, over the (arrival, id) pre-order) by its upper
+// 32 bits only: 4 radix passes instead of 8.  Keys then differ from the full order only
+// inside runs of equal upper halves, and only where the lower halves descend.  Pass A
+// writes order[i] = id of position i for everyone and lists each run that holds a descent
+// (its first descent reports the run start, found by a backward scan of at most 64 keys);
+// pass B sorts each listed run by the full key (insertion sort: stable, so ties keep the
+// pre-order) and rewrites its order entries.  A descending run longer than 64 raises the
+// fallback flag and the caller re-sorts with all 8 digits: only adversarial inputs get
+// there.  With no descents (integer-valued keys, distinct upper halves) pass B is skipped.
+constexpr uint32_t FIX_RUN = 64;
+
+// fix[0] fallback flag, fix[1] listed runs, fix[2..] run starts
+__global__ void gang_fix_a(const uint64_t* __restrict__ k, const uint32_t* __restrict__ v,
+                           const uint32_t* __restrict__ kid, uint64_t n, uint32_t* __restrict__ order,
+                           uint32_t* __restrict__ fix, uint32_t list_cap) {
+    for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+        order[i] = kid[v[i]];
+        if (i == 0) continue;
+        const uint64_t ki = k[i], kp = k[i - 1];
+        const uint32_t h = static_cast<uint32_t>(ki >> 32);
+        if (static_cast<uint32_t>(kp >> 32) != h || ki >= kp) continue;
+        // a descent inside a run: the first one of its run lists the run start
+        uint64_t j = i - 1;
+        bool first = true;
+        while (j > 0 && static_cast<uint32_t>(k[j - 1] >> 32) == h) {
+            if (i - j >= FIX_RUN) break;
+            first = first && !(k[j] < k[j - 1]);
+            --j;
+        }
+        const bool reach = j == 0 || static_cast<uint32_t>(k[j - 1] >> 32) != h;
+        if (!reach) {
+            atomicOr(fix, 1u);  // the run is longer than the fix-up handles
+        } else if (first) {
+            uint64_t e = i + 1;  // the run must also end within reach
+            while (e < n && e - j <= FIX_RUN && static_cast<uint32_t>(k[e] >> 32) == h) ++e;
+            if (e - j > FIX_RUN) {
+                atomicOr(fix, 1u);
+                continue;
+            }
+            const uint32_t slot = atomicAdd(fix + 1, 1u);
+            if (slot < list_cap) fix[2 + slot] = static_cast<uint32_t>(j);
+            else atomicOr(fix, 1u);
+        }
+    }
+}
+
+__global__ void gang_fix_b(uint64_t* __restrict__ k, uint32_t* __restrict__ v, const uint32_t* __restrict__ kid,
+                           uint64_t n, uint32_t* __restrict__ order, const uint32_t* __restrict__ fix) {
+    const uint32_t cnt = fix[1];
+    for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < cnt; t += gridDim.x * blockDim.x) {
+        const uint64_t i = fix[2 + t];
+        const uint32_t h = static_cast<uint32_t>(k[i] >> 32);
+        uint64_t e = i + 1;
+        while (e < n && static_cast<uint32_t>(k[e] >> 32) == h) ++e;
+        if (e - i > FIX_RUN) continue;  // flagged by pass A; the caller falls back
+        for (uint64_t a = i + 1; a < e; ++a) {  // stable insertion sort by the full key
+            const uint64_t ka = k[a];
+            const uint32_t va = v[a];
+            uint64_t b = a;
+            while (b > i && k[b - 1] > ka) {
+                k[b] = k[b - 1];
+                v[b] = v[b - 1];
+                --b;
+            }
+            k[b] = ka;
+            v[b] = va;
+        }
+        for (uint64_t a = i; a < e; ++a) order[a] = kid[v[a]];
+    }
 }
 
 // ---- merge of sorted runs by ranking: pos = own index + #smaller keys in every other run
@@ -701,18 +775,15 @@ int radix_sort_pairs(cdx_ctx* ctx, uint64_t* k0, uint32_t* v0, uint64_t* k1, uin
 
 }  // namespace cdx
 
-extern "C" int cdx_gang_priority(cdx_ctx* ctx, const cdx_prog_soa* progs, uint64_t N, const cdx_inter_policy* pol,
-                                 double now, uint32_t* order, uint64_t* n_out, uint8_t* escalated, uint64_t* keys) {
-    using namespace cdx;
-    if (!ctx) return CDX_EINVAL;
-    if (!progs || !pol || !order || !n_out) return set_error(ctx, CDX_EINVAL, "gang_priority: null pointer");
-    if (!(pol->starvation_limit > 0.0))
-        return set_error(ctx, CDX_EINVAL, "scheduler: starvation_limit must be > 0");
-    if (pol->order != CDX_ORDER_FIFO && pol->order != CDX_ORDER_SJF)
-        return set_error(ctx, CDX_EINVAL, "scheduler: order must be fifo or sjf_estimated");
-    if (N >= 0xffffffffull) return set_error(ctx, CDX_EINVAL, "gang_priority: at most 2^32-2 programs");
-    *n_out = 0;
-    if (N == 0) return CDX_OK;
+namespace cdx {
+namespace {
+// One evaluation.  full = false sorts the priority word by its upper half and fixes the
+// runs (see gang_fix_runs); *need_full reports a run too long for the fix-up, and the
+// caller then repeats with full = true (all 8 digits, the final gather folded in).
+int gang_priority_run(cdx_ctx* ctx, const cdx_prog_soa* progs, uint64_t N, const cdx_inter_policy* pol, double now,
+                      uint32_t* order, uint64_t* n_out, uint8_t* escalated, uint64_t* keys, bool full,
+                      bool* need_full) {
+    *need_full = false;
     GangParams p{progs->arrival, progs->last_service, progs->iter_tok_sum, progs->iter_count, progs->knob,
                  progs->cap, progs->terminated, escalated, N, progs->id_base, pol->order, now,
                  pol->starvation_limit, pol->prior_tokens};
@@ -778,10 +849,40 @@ extern "C" int cdx_gang_priority(cdx_ctx* ctx, const cdx_prog_soa* progs, uint64
     }
     int which = 0;
     uint64_t* hout = hin == t0 ? t1 : t0;
-    // the hi counts on the device are still valid unless the pre-sort overwrote them; the
-    // last pass writes program ids straight into `order` unless the keys are wanted too
-    if (int st = radix_sort(ctx, hin, pa, hout, pb, n, hist, &which, hm[1] ? nullptr : hh.data(),
-                            keys ? nullptr : kid, keys ? nullptr : order))
+    // the hi counts on the device are still valid unless the pre-sort overwrote them
+    const uint32_t* hhp = hm[1] ? nullptr : hh.data();
+    if (!full) {
+        if (int st = radix_sort(ctx, hin, pa, hout, pb, n, hist, &which, hhp, nullptr, nullptr, 4)) return st;
+        uint64_t* ks = which ? hout : hin;
+        uint32_t* vs = which ? pb : pa;  // position -> compacted index
+        // run list: the radix look-back scratch is free again (>= 8*256*ntiles words)
+        uint32_t* fix = hist;
+        const uint32_t list_cap = static_cast<uint32_t>(std::min<uint64_t>(nh - 2, 0xffffffffull));
+        cudaMemsetAsync(fix, 0, 8, ctx->stream);
+        gang_fix_a<<<L.grid(n), 256, 0, ctx->stream>>>(ks, vs, kid, n, order, fix, list_cap);
+        CDX_CHECK_LAUNCH(ctx, "gang_priority(order)");
+        uint32_t fb[2] = {0, 0};
+        e = cudaMemcpyAsync(fb, fix, 8, cudaMemcpyDeviceToHost, ctx->stream);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
+        if (e != cudaSuccess) return cuda_fail(ctx, e, "gang_priority(runs)");
+        if (fb[0]) {
+            *need_full = true;
+            return CDX_OK;
+        }
+        if (fb[1]) {
+            gang_fix_b<<<L.grid(fb[1]), 256, 0, ctx->stream>>>(ks, vs, kid, n, order, fix);
+            CDX_CHECK_LAUNCH(ctx, "gang_priority(runs)");
+        }
+        if (keys) {
+            pack_keys<<<L.grid(n), 256, 0, ctx->stream>>>(ks, karr, kid, vs, keys, n);
+            CDX_CHECK_LAUNCH(ctx, "gang_priority(keys)");
+        }
+        return CDX_OK;
+    }
+    // all 8 digits; the last pass writes program ids straight into `order` unless the keys
+    // are wanted too
+    if (int st = radix_sort(ctx, hin, pa, hout, pb, n, hist, &which, hhp, keys ? nullptr : kid,
+                            keys ? nullptr : order))
         return st;
     if (which == 2) return CDX_OK;
     uint32_t* fin = which ? pb : pa;  // position -> compacted index
@@ -792,6 +893,29 @@ extern "C" int cdx_gang_priority(cdx_ctx* ctx, const cdx_prog_soa* progs, uint64
         CDX_CHECK_LAUNCH(ctx, "gang_priority(keys)");
     }
     return CDX_OK;
+}
+}  // namespace
+}  // namespace cdx
+
+
+extern "C" int cdx_gang_priority(cdx_ctx* ctx, const cdx_prog_soa* progs, uint64_t N, const cdx_inter_policy* pol,
+                                 double now, uint32_t* order, uint64_t* n_out, uint8_t* escalated, uint64_t* keys) {
+    using namespace cdx;
+    if (!ctx) return CDX_EINVAL;
+    if (!progs || !pol || !order || !n_out) return set_error(ctx, CDX_EINVAL, "gang_priority: null pointer");
+    if (!(pol->starvation_limit > 0.0))
+        return set_error(ctx, CDX_EINVAL, "scheduler: starvation_limit must be > 0");
+    if (pol->order != CDX_ORDER_FIFO && pol->order != CDX_ORDER_SJF)
+        return set_error(ctx, CDX_EINVAL, "scheduler: order must be fifo or sjf_estimated");
+    if (N >= 0xffffffffull) return set_error(ctx, CDX_EINVAL, "gang_priority: at most 2^32-2 programs");
+    *n_out = 0;
+    if (N == 0) return CDX_OK;
+    bool need_full = false;
+    const bool force_full = getenv("CDX_GANG_FULL") != nullptr;  // 8-digit sort only (A/B timing, tests)
+    if (int st = gang_priority_run(ctx, progs, N, pol, now, order, n_out, escalated, keys, force_full, &need_full))
+        return st;
+    if (!need_full) return CDX_OK;
+    return gang_priority_run(ctx, progs, N, pol, now, order, n_out, escalated, keys, true, &need_full);
 }
 
 extern "C" int cdx_gang_merge(cdx_ctx* ctx, const uint64_t* keys, const uint64_t* run_len, uint32_t runs,

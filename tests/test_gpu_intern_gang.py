@@ -93,7 +93,7 @@ def test_gang_parity(ctx, N, order, limit, sorted_arrival):
     assert np.array_equal(got.cpu().numpy().view(np.uint32), ref)
 
 
-@pytest.mark.parametrize("case", ["identical", "all_escalated", "one_digit"])
+@pytest.mark.parametrize("case", ["identical", "all_escalated", "one_digit", "upper_half_ties", "short_runs"])
 def test_gang_degenerate_keys(ctx, case):
     """Keys that agree on most or all radix digits (skipped passes, single-digit sorts,
     ties resolved purely by arrival then program id)."""
@@ -111,6 +111,21 @@ def test_gang_degenerate_keys(ctx, case):
     elif case == "all_escalated":
         soa["last_service"][:] = 0.0
         now = float(soa["arrival"].max()) + 10.0
+    elif case == "upper_half_ties":  # equal upper 32 bits, shuffled lower bits: the 8-digit fallback
+        soa["iter_count"][:] = 1
+        soa["iter_tok_sum"][:] = (1 << 40) + np.random.default_rng(9).integers(0, 1000, N)
+        soa["cap"][:] = 2
+        soa["knob"][:] = 1
+        soa["last_service"][:] = soa["arrival"]
+        now = float(soa["arrival"].max()) + 0.1
+    elif case == "short_runs":  # pairs/triples of keys sharing upper halves, fixed up in place
+        base = np.random.default_rng(10).integers(1 << 30, 1 << 31, N // 3 + 1)
+        soa["iter_count"][:] = 1
+        soa["iter_tok_sum"][:] = (np.repeat(base, 3)[:N] << 12) + np.random.default_rng(11).integers(0, 64, N)
+        soa["cap"][:] = 2
+        soa["knob"][:] = 1
+        soa["last_service"][:] = soa["arrival"]
+        now = float(soa["arrival"].max()) + 0.1
     else:  # sjf keys that differ only in their lowest mantissa byte
         soa["iter_count"][:] = 1
         soa["iter_tok_sum"][:] = 1 << 20
@@ -123,6 +138,18 @@ def test_gang_degenerate_keys(ctx, case):
     got, _, _ = ctx.gang_priority(_to_dev(soa), pol, now)
     ctx.sync()
     ref, _ = O.gang_order(soa, 1, 1.0, 128.0, now)
+    assert np.array_equal(got.cpu().numpy().view(np.uint32), ref)
+
+
+@pytest.mark.parametrize("N", [5000, 300000])
+def test_gang_full_sort_mode(ctx, N, monkeypatch):
+    """The 8-digit sort (the fallback of the upper-half sort + run fix-up) on its own."""
+    from paper_2412_20993_b200 import InterPolicy
+    monkeypatch.setenv("CDX_GANG_FULL", "1")
+    soa, now = _gang_inputs(N, 77)
+    got, _, _ = ctx.gang_priority(_to_dev(soa), InterPolicy(order=1, starvation_limit=0.5, prior_tokens=128.0), now)
+    ctx.sync()
+    ref, _ = O.gang_order(soa, 1, 0.5, 128.0, now)
     assert np.array_equal(got.cpu().numpy().view(np.uint32), ref)
 
 
