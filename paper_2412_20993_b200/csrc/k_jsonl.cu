@@ -86,40 +86,6 @@ __global__ void nl_count(const char* __restrict__ t, uint64_t n, uint32_t* __res
     }
 }
 
-__global__ void excl_scan_one_cta(uint32_t* __restrict__ v, uint32_t n, uint64_t* __restrict__ total) {
-    __shared__ uint32_t ws[32];
-    __shared__ uint64_t carry;
-    if (threadIdx.x == 0) carry = 0;
-    __syncthreads();
-    const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    for (uint32_t b = 0; b < n; b += 1024) {
-        const uint32_t i = b + threadIdx.x;
-        const uint32_t x = i < n ? v[i] : 0u;
-        uint32_t inc = x;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
-            if (lane >= static_cast<uint32_t>(o)) inc += y;
-        }
-        if (lane == 31) ws[warp] = inc;
-        __syncthreads();
-        if (warp == 0) {
-            uint32_t w = ws[lane];
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const uint32_t y = __shfl_up_sync(0xffffffffu, w, o);
-                if (lane >= static_cast<uint32_t>(o)) w += y;
-            }
-            ws[lane] = w;
-        }
-        __syncthreads();
-        if (i < n) v[i] = static_cast<uint32_t>(carry) + (warp ? ws[warp - 1] : 0u) + inc - x;
-        __syncthreads();
-        if (threadIdx.x == 0) carry += ws[31];
-        __syncthreads();
-    }
-    if (threadIdx.x == 0) *total = carry;
-}
 
 // newline positions in order: each thread's 64-byte mask, a block scan of the counts
 __global__ void nl_scatter(const char* __restrict__ t, uint64_t n, const uint32_t* __restrict__ base,
@@ -724,44 +690,8 @@ __global__ void __launch_bounds__(128) parse_lines(const char* __restrict__ t, u
 }
 
 // ---- 4. compaction of records + decoded strings -------------------------------------------
-__global__ void flag_records(const uint8_t* __restrict__ st, uint64_t n_lines, uint32_t* __restrict__ f) {
-    for (uint64_t L = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; L < n_lines;
-         L += static_cast<uint64_t>(gridDim.x) * blockDim.x)
-        f[L] = st[L] == L_RECORD;
-}
 
-__global__ void add_block_base(uint32_t* __restrict__ v, uint64_t n, const uint32_t* __restrict__ sums) {
-    const uint64_t i = blockIdx.x * 1024ull + threadIdx.x;
-    if (i < n) v[i] += sums[blockIdx.x];
-}
 
-// exclusive scan of u32 within 1024-blocks; block totals to sums
-__global__ void scan_1024(uint32_t* __restrict__ v, uint64_t n, uint32_t* __restrict__ sums) {
-    __shared__ uint32_t ws[32];
-    const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const uint64_t i = blockIdx.x * 1024ull + threadIdx.x;
-    const uint32_t x = i < n ? v[i] : 0u;
-    uint32_t inc = x;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-        const uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
-        if (lane >= static_cast<uint32_t>(o)) inc += y;
-    }
-    if (lane == 31) ws[warp] = inc;
-    __syncthreads();
-    if (warp == 0) {
-        uint32_t w = ws[lane];
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const uint32_t y = __shfl_up_sync(0xffffffffu, w, o);
-            if (lane >= static_cast<uint32_t>(o)) w += y;
-        }
-        ws[lane] = w;
-    }
-    __syncthreads();
-    if (i < n) v[i] = (warp ? ws[warp - 1] : 0u) + inc - x;
-    if (threadIdx.x == 1023) sums[blockIdx.x] = ws[31];
-}
 
 // record r <- line L (st == record): fields + decoded string lengths
 __global__ void gather_records(const char* __restrict__ t, const uint8_t* __restrict__ st,
@@ -828,6 +758,103 @@ __global__ void write_strings(const char* __restrict__ t, uint64_t n, const uint
     }
 }
 
+// ---- single-pass exclusive scan (decoupled look-back) --------------------------------------
+// out[i] = sum of ld(j) for j < i; with `total_slot`, out[n] = the grand total as well (arena
+// offsets are n + 1 long).  Tiles of 2048 elements, 8 consecutive per thread; the tile
+// records pack state (bits 62-63: 1 aggregate, 2 inclusive) with a 62-bit value, so one
+// 64-bit store publishes both.  Tickets order the tiles; records and ticket are cleared by
+// the caller before each call.
+constexpr int SL_THREADS = 256, SL_ITEMS = 8, SL_TILE = SL_THREADS * SL_ITEMS;
+constexpr uint64_t SL_AGG = 1ull << 62, SL_INC = 2ull << 62, SL_VAL = (1ull << 62) - 1;
+
+struct LoadRecordFlag {  // 1 for a line that is a record
+    const uint8_t* st;
+    __device__ uint32_t operator()(uint64_t i) const { return st[i] == L_RECORD ? 1u : 0u; }
+};
+struct LoadU32 {
+    const uint32_t* v;
+    __device__ uint32_t operator()(uint64_t i) const { return v[i]; }
+};
+
+template <class Load, typename Out>
+__global__ void __launch_bounds__(SL_THREADS) scan_lb(Load ld, uint64_t n, Out* __restrict__ out, bool total_slot,
+                                                      uint64_t* __restrict__ rec, uint32_t* __restrict__ ticket,
+                                                      uint64_t* __restrict__ total) {
+    __shared__ uint32_t s_tile;
+    __shared__ uint64_t s_w[SL_THREADS / 32];
+    __shared__ uint64_t s_excl;
+    const uint32_t tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
+    if (tid == 0) s_tile = atomicAdd(ticket, 1u);
+    __syncthreads();
+    const uint32_t tile = s_tile;
+    const uint64_t b = static_cast<uint64_t>(tile) * SL_TILE + static_cast<uint64_t>(tid) * SL_ITEMS;
+    uint32_t v[SL_ITEMS];
+    uint64_t sum = 0;
+#pragma unroll
+    for (int j = 0; j < SL_ITEMS; ++j) {
+        v[j] = b + j < n ? ld(b + j) : 0u;
+        sum += v[j];
+    }
+    uint64_t inc = sum;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint64_t y = __shfl_up_sync(0xffffffffu, inc, o);
+        if (lane >= static_cast<uint32_t>(o)) inc += y;
+    }
+    if (lane == 31) s_w[warp] = inc;
+    __syncthreads();
+    uint64_t tot = 0, wpre = 0;
+#pragma unroll
+    for (int w = 0; w < SL_THREADS / 32; ++w) {
+        wpre += w < static_cast<int>(warp) ? s_w[w] : 0ull;
+        tot += s_w[w];
+    }
+    if (warp == 0) {
+        if (lane == 0) {
+            volatile uint64_t* r = rec + tile;
+            __threadfence();
+            *r = (tile == 0 ? SL_INC : SL_AGG) | tot;
+        }
+        uint64_t ex = 0;
+        int64_t j = static_cast<int64_t>(tile) - 1;
+        while (j >= 0) {
+            const int64_t idx = j - lane;
+            uint64_t f = SL_INC;  // before tile 0: an inclusive zero
+            if (idx >= 0) {
+                do {
+                    f = *reinterpret_cast<volatile uint64_t*>(rec + idx);
+                } while ((f >> 62) == 0);
+            }
+            const uint32_t incl = __ballot_sync(0xffffffffu, (f >> 62) == 2);
+            const int stop = incl ? __ffs(incl) - 1 : 31;
+            uint64_t val = (lane <= static_cast<uint32_t>(stop) && idx >= 0) ? (f & SL_VAL) : 0ull;
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) val += __shfl_xor_sync(0xffffffffu, val, o);
+            ex += val;
+            if (incl) break;
+            j -= 32;
+        }
+        if (lane == 0) {
+            if (tile != 0) {
+                __threadfence();
+                *reinterpret_cast<volatile uint64_t*>(rec + tile) = SL_INC | (ex + tot);
+            }
+            s_excl = ex;
+            if (static_cast<uint64_t>(tile + 1) * SL_TILE >= n) {  // the last tile
+                if (total) *total = ex + tot;
+                if (total_slot) out[n] = static_cast<Out>(ex + tot);
+            }
+        }
+    }
+    __syncthreads();
+    uint64_t run = s_excl + wpre + inc - sum;
+#pragma unroll
+    for (int j = 0; j < SL_ITEMS; ++j) {
+        if (b + j < n) out[b + j] = static_cast<Out>(run);
+        run += v[j];
+    }
+}
+
 // ---- 4b. order check per program (probe.cpp:148-155) ------------------------------------
 __global__ void order_check(const uint32_t* __restrict__ sorted_rec, const uint64_t* __restrict__ keys,
                             uint64_t n, const int32_t* __restrict__ step, const int64_t* __restrict__ tok,
@@ -848,12 +875,6 @@ __global__ void order_check(const uint32_t* __restrict__ sorted_rec, const uint6
     }
 }
 
-__global__ void shift_offsets(const uint32_t* __restrict__ excl, const uint32_t* __restrict__ len, uint64_t n,
-                              uint64_t* __restrict__ off) {
-    for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i <= n;
-         i += static_cast<uint64_t>(gridDim.x) * blockDim.x)
-        off[i] = i < n ? excl[i] : (n ? static_cast<uint64_t>(excl[n - 1]) + len[n - 1] : 0ull);
-}
 
 __global__ void widen_ids(const uint32_t* __restrict__ ids, uint64_t n, uint64_t* __restrict__ k,
                           uint32_t* __restrict__ v) {
@@ -883,15 +904,20 @@ unsigned gridn(const cdx_ctx* ctx, uint64_t n) {
     return static_cast<unsigned>(want < 1 ? 1 : (want < cap ? want : cap));
 }
 
-// exclusive scan of n u32 in place (<= 2^20 blocks of 1024), via block sums + one-CTA scan
-int scan_u32_inplace(cdx_ctx* ctx, uint32_t* v, uint64_t n, uint32_t* sums, uint64_t* total) {
-    const uint64_t nb = (n + 1023) / 1024;
-    scan_1024<<<static_cast<unsigned>(std::max<uint64_t>(nb, 1)), 1024, 0, ctx->stream>>>(v, n, sums);
+// one single-pass scan launch (records + ticket cleared first)
+template <class Load, typename Out>
+int scan_excl(cdx_ctx* ctx, Load ld, uint64_t n, Out* out, bool total_slot, uint64_t* rec, uint64_t* total) {
+    const uint64_t tiles = (n + SL_TILE - 1) / SL_TILE;
+    if (n == 0) {
+        if (total) cudaMemsetAsync(total, 0, 8, ctx->stream);
+        if (total_slot) cudaMemsetAsync(out, 0, sizeof(Out), ctx->stream);
+        return CDX_OK;
+    }
+    uint32_t* ticket = reinterpret_cast<uint32_t*>(rec + tiles);
+    cudaMemsetAsync(rec, 0, tiles * 8 + 8, ctx->stream);
+    scan_lb<Load, Out><<<static_cast<unsigned>(tiles), SL_THREADS, 0, ctx->stream>>>(ld, n, out, total_slot, rec,
+                                                                                      ticket, total);
     CDX_CHECK_LAUNCH(ctx, "jsonl(scan)");
-    excl_scan_one_cta<<<1, 1024, 0, ctx->stream>>>(sums, static_cast<uint32_t>(nb), total);
-    CDX_CHECK_LAUNCH(ctx, "jsonl(scan sums)");
-    add_block_base<<<static_cast<unsigned>(std::max<uint64_t>(nb, 1)), 1024, 0, ctx->stream>>>(v, n, sums);
-    CDX_CHECK_LAUNCH(ctx, "jsonl(scan add)");
     return CDX_OK;
 }
 
@@ -921,17 +947,17 @@ extern "C" int cdx_jsonl_parse(cdx_ctx* ctx, const char* text, uint64_t nbytes, 
     if (nbytes >= (1ull << 32)) return set_error(ctx, CDX_EINVAL, "jsonl_parse: at most 4 GiB per call");
     const uint64_t nchunks = (nbytes + JL_CHUNK - 1) / JL_CHUNK;
     // phase 1 (small scratch): newline count per chunk, then its scan
-    uint8_t* s1 = static_cast<uint8_t*>(scratch2(ctx, 4096 + nchunks * 4 + 256));
+    uint8_t* s1 = static_cast<uint8_t*>(scratch2(ctx, 4096 + nchunks * 4 + 256 + (nchunks / SL_TILE + 2) * 8 + 256));
     if (!s1) return set_error(ctx, CDX_ECUDA, "jsonl_parse: scratch allocation failed");
     uint8_t* p1 = s1;
     uint64_t* misc = carve<uint64_t>(p1, 16);  // [0] newlines, [1] first bad line, [2] records, [3] scan total
     uint32_t* cnt = carve<uint32_t>(p1, nchunks);
+    uint64_t* crec = carve<uint64_t>(p1, nchunks / SL_TILE + 2);
     cudaMemsetAsync(misc, 0, 16 * 8, ctx->stream);
     cudaMemsetAsync(misc + 1, 0xff, 8, ctx->stream);
     nl_count<<<static_cast<unsigned>(nchunks), 256, 0, ctx->stream>>>(text, nbytes, cnt);
     CDX_CHECK_LAUNCH(ctx, "jsonl(lines)");
-    excl_scan_one_cta<<<1, 1024, 0, ctx->stream>>>(cnt, static_cast<uint32_t>(nchunks), misc);
-    CDX_CHECK_LAUNCH(ctx, "jsonl(lines scan)");
+    if (int st = scan_excl(ctx, LoadU32{cnt}, nchunks, cnt, false, crec, misc)) return st;  // in place
     uint64_t h_nl = 0;
     char last = 0;
     cudaMemcpyAsync(&h_nl, misc, 8, cudaMemcpyDeviceToHost, ctx->stream);
@@ -972,13 +998,11 @@ extern "C" int cdx_jsonl_parse(cdx_ctx* ctx, const char* text, uint64_t nbytes, 
     o.ans_len = carve<uint32_t>(p, n_lines);
     o.esc = carve<uint8_t>(p, n_lines);
     uint32_t* pos = carve<uint32_t>(p, n_lines);
-    uint32_t* sums = carve<uint32_t>(p, (n_lines + 1023) / 1024 + 1);
+    uint64_t* srec = carve<uint64_t>(p, (n_lines + SL_TILE - 1) / SL_TILE + 2);  // scan tile records + ticket
     parse_lines<<<gridn(ctx, n_lines), 128, 0, ctx->stream>>>(text, nbytes, nl, h_nl, n_lines, o,
                                                               reinterpret_cast<unsigned long long*>(misc + 1));
     CDX_CHECK_LAUNCH(ctx, "jsonl(parse)");
-    flag_records<<<gridn(ctx, n_lines), 256, 0, ctx->stream>>>(o.st, n_lines, pos);
-    CDX_CHECK_LAUNCH(ctx, "jsonl(flags)");
-    if (int st = scan_u32_inplace(ctx, pos, n_lines, sums, misc + 2)) return st;
+    if (int st = scan_excl(ctx, LoadRecordFlag{o.st}, n_lines, pos, false, srec, misc + 2)) return st;
     uint64_t hm[2];
     cudaMemcpyAsync(hm, misc + 1, 16, cudaMemcpyDeviceToHost, ctx->stream);
     e = cudaStreamSynchronize(ctx->stream);
@@ -1004,15 +1028,8 @@ extern "C" int cdx_jsonl_parse(cdx_ctx* ctx, const char* text, uint64_t nbytes, 
                                                                      token_offset, hesitant, r_line, pid_len, ans_len);
         CDX_CHECK_LAUNCH(ctx, "jsonl(records)");
         // arena offsets: exclusive scans of the decoded lengths
-        uint32_t* tmp = v0;  // reuse as scan space
-        cudaMemcpyAsync(tmp, ans_len, nr * 4, cudaMemcpyDeviceToDevice, ctx->stream);
-        if (int st = scan_u32_inplace(ctx, tmp, nr, sums, misc + 3)) return st;
-        shift_offsets<<<gridn(ctx, nr + 1), 256, 0, ctx->stream>>>(tmp, ans_len, nr, answer_off);
-        CDX_CHECK_LAUNCH(ctx, "jsonl(answer offsets)");
-        cudaMemcpyAsync(tmp, pid_len, nr * 4, cudaMemcpyDeviceToDevice, ctx->stream);
-        if (int st = scan_u32_inplace(ctx, tmp, nr, sums, misc + 3)) return st;
-        shift_offsets<<<gridn(ctx, nr + 1), 256, 0, ctx->stream>>>(tmp, pid_len, nr, pid_off);
-        CDX_CHECK_LAUNCH(ctx, "jsonl(program offsets)");
+        if (int st = scan_excl(ctx, LoadU32{ans_len}, nr, answer_off, true, srec, nullptr)) return st;
+        if (int st = scan_excl(ctx, LoadU32{pid_len}, nr, pid_off, true, srec, nullptr)) return st;
         write_strings<<<gridn(ctx, n_lines), 128, 0, ctx->stream>>>(text, nbytes, o.st, pos, n_lines, o, pid_off, pid_arena,
                                                                     answer_off, answer_arena);
         CDX_CHECK_LAUNCH(ctx, "jsonl(strings)");
