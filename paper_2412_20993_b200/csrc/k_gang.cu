@@ -208,7 +208,8 @@ __global__ void __launch_bounds__(GP_THREADS) gang_prepare(const GangParams p, u
 // keys[i] = {hi, arrival bits, id} of the i-th program in priority order (merge input)
 __global__ void pack_keys(const uint64_t* __restrict__ shi, const uint64_t* __restrict__ karr,
                           const uint32_t* __restrict__ kid, const uint32_t* __restrict__ fin, uint64_t* __restrict__ keys,
-                          uint64_t n) {
+                          uint64_t n, const uint32_t* __restrict__ n_dev = nullptr) {
+    if (n_dev) n = *n_dev;
     for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n;
          i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
         const uint32_t j = fin[i];
@@ -269,6 +270,8 @@ __device__ __forceinline__ uint32_t lookback_win(const uint32_t* look, uint32_t 
 
 // n_dev (nullable): the key count is read on the device (the gang path histograms its
 // compacted keys before the host has learned how many there are: one sync, not two)
+// DLO: digits below it are not counted (their rows stay zero; the upper-half sort skips them)
+template <int DLO = 0>
 __global__ void __launch_bounds__(RS_THREADS) os_histogram(const uint64_t* __restrict__ keys, uint64_t n,
                                                            uint32_t* __restrict__ ghist,
                                                            const uint32_t* __restrict__ n_dev) {
@@ -280,7 +283,7 @@ __global__ void __launch_bounds__(RS_THREADS) os_histogram(const uint64_t* __res
          i += static_cast<uint64_t>(gridDim.x) * RS_THREADS) {
         const uint64_t k = keys[i];
 #pragma unroll
-        for (int d = 0; d < 8; ++d) atomicAdd(&h[d][(k >> (8 * d)) & 0xff], 1u);
+        for (int d = DLO; d < 8; ++d) atomicAdd(&h[d][(k >> (8 * d)) & 0xff], 1u);
     }
     __syncthreads();
     for (int i = threadIdx.x; i < 8 * 256; i += RS_THREADS) {
@@ -424,15 +427,31 @@ __device__ __forceinline__ void os_tile(const uint64_t* __restrict__ kin, const 
 
 // Tiles take tickets in launch order (look-back only waits on running or finished tiles);
 // every tile but the last is full.
+// n_dev (nullable): the key count lives on the device and `n` only bounds it (the grid is
+// sized for the bound; tiles past the count exit).  The host has then not seen the digit
+// counts either, so a digit on which every key agrees is detected here and the pass
+// degenerates to a copy (the ping-pong parity stays what the host planned).
 __global__ void __launch_bounds__(RS_THREADS, 2)
     os_pass2(const uint64_t* __restrict__ kin, const uint32_t* __restrict__ vin, uint64_t* __restrict__ kout,
              uint32_t* __restrict__ vout, uint64_t n, int shift, const uint32_t* __restrict__ ghist,
-             uint32_t* __restrict__ look, uint32_t* __restrict__ counter, const uint32_t* __restrict__ vmap) {
+             uint32_t* __restrict__ look, uint32_t* __restrict__ counter, const uint32_t* __restrict__ vmap,
+             const uint32_t* __restrict__ n_dev) {
     extern __shared__ __align__(16) uint8_t rs2_smem[];
     uint32_t* s_tile = reinterpret_cast<uint32_t*>(rs2_smem + RS2_SMEM - 16);
     if (threadIdx.x == 0) *s_tile = atomicAdd(counter, 1u);
+    if (n_dev) n = *n_dev;
     __syncthreads();
     const uint32_t tile = *s_tile;
+    const uint64_t tb = static_cast<uint64_t>(tile) * RS_TILE;
+    if (tb >= n) return;
+    if (n_dev && __syncthreads_or(ghist[threadIdx.x] == n)) {  // trivial digit: copy the tile
+        const uint64_t te = tb + RS_TILE < n ? tb + RS_TILE : n;
+        for (uint64_t i = tb + threadIdx.x; i < te; i += RS_THREADS) {
+            kout[i] = kin[i];
+            vout[i] = vmap ? vmap[vin[i]] : vin[i];
+        }
+        return;
+    }
     if ((static_cast<uint64_t>(tile) + 1) * RS_TILE <= n)
         os_tile<true, LB_WIN>(kin, vin, kout, vout, n, shift, ghist, look, tile, rs2_smem, vmap);
     else
@@ -582,7 +601,7 @@ int radix_sort(cdx_ctx* ctx, uint64_t* k0, uint32_t* v0, uint64_t* k1, uint32_t*
     if (!hh) {
         const unsigned hgrid =
             static_cast<unsigned>(std::min<uint64_t>(ntiles, static_cast<uint64_t>(ctx->sm_count) * 4));
-        os_histogram<<<hgrid, RS_THREADS, 0, ctx->stream>>>(k0, n, ghist, nullptr);
+        os_histogram<0><<<hgrid, RS_THREADS, 0, ctx->stream>>>(k0, n, ghist, nullptr);
         CDX_CHECK_LAUNCH(ctx, "radix(histogram)");
         e = cudaMemcpyAsync(h, ghist, sizeof(h), cudaMemcpyDeviceToHost, ctx->stream);
         if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
@@ -632,7 +651,7 @@ int radix_sort(cdx_ctx* ctx, uint64_t* k0, uint32_t* v0, uint64_t* k1, uint32_t*
             const bool fold = vmap && vfinal && d == last;
             os_pass2<<<ntiles, RS_THREADS, RS2_SMEM, ctx->stream>>>(
                 kin, vin, kout, fold ? vfinal : vout, n, 8 * d, ghist + d * 256,
-                look + static_cast<size_t>(d) * ntiles * 256, tickets + d, fold ? vmap : nullptr);
+                look + static_cast<size_t>(d) * ntiles * 256, tickets + d, fold ? vmap : nullptr, nullptr);
             CDX_CHECK_LAUNCH(ctx, "radix(pass)");
             mapped = fold;
         }
@@ -658,7 +677,8 @@ constexpr uint32_t FIX_RUN = 64;
 // fix[0] fallback flag, fix[1] listed runs, fix[2..] run starts
 __global__ void gang_fix_a(const uint64_t* __restrict__ k, const uint32_t* __restrict__ v,
                            const uint32_t* __restrict__ kid, uint64_t n, uint32_t* __restrict__ order,
-                           uint32_t* __restrict__ fix, uint32_t list_cap) {
+                           uint32_t* __restrict__ fix, uint32_t list_cap, const uint32_t* __restrict__ n_dev) {
+    if (n_dev) n = *n_dev;
     for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n;
          i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
         order[i] = kid[v[i]];
@@ -692,7 +712,10 @@ __global__ void gang_fix_a(const uint64_t* __restrict__ k, const uint32_t* __res
 }
 
 __global__ void gang_fix_b(uint64_t* __restrict__ k, uint32_t* __restrict__ v, const uint32_t* __restrict__ kid,
-                           uint64_t n, uint32_t* __restrict__ order, const uint32_t* __restrict__ fix) {
+                           uint64_t n, uint32_t* __restrict__ order, const uint32_t* __restrict__ fix,
+                           const uint32_t* __restrict__ n_dev) {
+    if (n_dev) n = *n_dev;
+    if (fix[0]) return;  // the caller falls back to the full sort
     const uint32_t cnt = fix[1];
     for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < cnt; t += gridDim.x * blockDim.x) {
         const uint64_t i = fix[2 + t];
@@ -714,6 +737,36 @@ __global__ void gang_fix_b(uint64_t* __restrict__ k, uint32_t* __restrict__ v, c
         }
         for (uint64_t a = i; a < e; ++a) order[a] = kid[v[a]];
     }
+}
+
+// Digits [dlo, 8) with the key count on the device (n_dev; nmax bounds it): the caller has
+// histogrammed the keys into lb[0, 2048) already.  No host round trip: every digit gets a
+// pass (trivial ones copy), so the result lands in k0/v0 for an even pass count.
+int radix_sort_dev(cdx_ctx* ctx, uint64_t* k0, uint32_t* v0, uint64_t* k1, uint32_t* v1, uint64_t nmax,
+                   const uint32_t* n_dev, uint32_t* lb, int dlo, int* which) {
+    const uint32_t ntiles = static_cast<uint32_t>((nmax + RS_TILE - 1) / RS_TILE);
+    *which = 0;
+    if (nmax == 0) return CDX_OK;
+    uint32_t* ghist = lb;
+    uint32_t* tickets = lb + 8 * 256;
+    uint32_t* look = tickets + 16;
+    cudaError_t e = cudaMemsetAsync(tickets, 0, (16 + static_cast<size_t>(8) * ntiles * 256) * 4, ctx->stream);
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(os_pass2, cudaFuncAttributeMaxDynamicSharedMemorySize, RS2_SMEM);
+    if (e != cudaSuccess) return cuda_fail(ctx, e, "radix(device count)");
+    uint64_t* kin = k0;
+    uint32_t* vin = v0;
+    uint64_t* kout = k1;
+    uint32_t* vout = v1;
+    for (int d = dlo; d < 8; ++d) {
+        os_pass2<<<ntiles, RS_THREADS, RS2_SMEM, ctx->stream>>>(kin, vin, kout, vout, nmax, 8 * d, ghist + d * 256,
+                                                                look + static_cast<size_t>(d) * ntiles * 256,
+                                                                tickets + d, nullptr, n_dev);
+        CDX_CHECK_LAUNCH(ctx, "radix(pass)");
+        std::swap(kin, kout);
+        std::swap(vin, vout);
+    }
+    *which = kin == k0 ? 0 : 1;
+    return CDX_OK;
 }
 
 // ---- merge of sorted runs by ranking: pos = own index + #smaller keys in every other run
@@ -777,13 +830,15 @@ int radix_sort_pairs(cdx_ctx* ctx, uint64_t* k0, uint32_t* v0, uint64_t* k1, uin
 
 namespace cdx {
 namespace {
-// One evaluation.  full = false sorts the priority word by its upper half and fixes the
-// runs (see gang_fix_runs); *need_full reports a run too long for the fix-up, and the
-// caller then repeats with full = true (all 8 digits, the final gather folded in).
+// One evaluation.  GANG_FAST: no pre-sort, device-side count, one sync (see below).
+// GANG_CHECKED: host-driven, with the (arrival, id) pre-sort when arrivals are unsorted and
+// the upper-half sort + run fix-up.  GANG_FULL: all 8 digits.  *redo names the path the
+// caller must run instead when this one could not finish (unsorted arrivals, a long run).
+enum GangMode { GANG_FAST = 0, GANG_CHECKED = 1, GANG_FULL = 2 };
 int gang_priority_run(cdx_ctx* ctx, const cdx_prog_soa* progs, uint64_t N, const cdx_inter_policy* pol, double now,
-                      uint32_t* order, uint64_t* n_out, uint8_t* escalated, uint64_t* keys, bool full,
-                      bool* need_full) {
-    *need_full = false;
+                      uint32_t* order, uint64_t* n_out, uint8_t* escalated, uint64_t* keys, int mode, int* redo) {
+    *redo = GANG_FAST;
+    const bool full = mode == GANG_FULL;
     GangParams p{progs->arrival, progs->last_service, progs->iter_tok_sum, progs->iter_count, progs->knob,
                  progs->cap, progs->terminated, escalated, N, progs->id_base, pol->order, now,
                  pol->starvation_limit, pol->prior_tokens};
@@ -815,9 +870,43 @@ int gang_priority_run(cdx_ctx* ctx, const cdx_prog_soa* progs, uint64_t N, const
     CDX_CHECK_LAUNCH(ctx, "gang_priority(prepare)");
     // digit counts of the live hi keys (count read on the device), fetched with the flags
     cudaMemsetAsync(hist, 0, 8 * 256 * 4, ctx->stream);
-    os_histogram<<<static_cast<unsigned>(std::min<uint64_t>(ntiles, static_cast<uint64_t>(ctx->sm_count) * 4)),
-                   RS_THREADS, 0, ctx->stream>>>(khi, N, hist, misc);
+    const unsigned hgrid = static_cast<unsigned>(std::min<uint64_t>(ntiles, static_cast<uint64_t>(ctx->sm_count) * 4));
+    if (full)
+        os_histogram<0><<<hgrid, RS_THREADS, 0, ctx->stream>>>(khi, N, hist, misc);
+    else
+        os_histogram<4><<<hgrid, RS_THREADS, 0, ctx->stream>>>(khi, N, hist, misc);
     CDX_CHECK_LAUNCH(ctx, "gang_priority(histogram)");
+    if (mode == GANG_FAST) {
+        // Optimistic single-round-trip path: arrivals assumed non-decreasing (no pre-sort),
+        // the key count stays on the device, 4 upper-half passes (even count: the result is
+        // back in khi/va), the run fix-up, then ONE sync that fetches the count and every
+        // flag.  Unsorted arrivals or a long descending run send the caller to the checked /
+        // full path, which recomputes everything.
+        int which = 0;
+        if (int st = radix_sort_dev(ctx, khi, va, t0, vb, N, misc, hist, 4, &which)) return st;
+        uint32_t* fix = hist;  // the digit counts are consumed: reuse for the run list
+        const uint32_t list_cap = static_cast<uint32_t>(std::min<uint64_t>(nh - 2, 0xffffffffull));
+        cudaMemsetAsync(fix, 0, 8, ctx->stream);
+        gang_fix_a<<<L.grid(N), 256, 0, ctx->stream>>>(khi, va, kid, N, order, fix, list_cap, misc);
+        CDX_CHECK_LAUNCH(ctx, "gang_priority(order)");
+        gang_fix_b<<<ctx->sm_count * 2, 256, 0, ctx->stream>>>(khi, va, kid, N, order, fix, misc);
+        CDX_CHECK_LAUNCH(ctx, "gang_priority(runs)");
+        if (keys) {
+            pack_keys<<<L.grid(N), 256, 0, ctx->stream>>>(khi, karr, kid, va, keys, N, misc);
+            CDX_CHECK_LAUNCH(ctx, "gang_priority(keys)");
+        }
+        uint32_t hm[3], fb[2];
+        cudaError_t e = cudaMemcpyAsync(hm, misc, 12, cudaMemcpyDeviceToHost, ctx->stream);
+        if (e == cudaSuccess) e = cudaMemcpyAsync(fb, fix, 8, cudaMemcpyDeviceToHost, ctx->stream);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
+        if (e != cudaSuccess) return cuda_fail(ctx, e, "gang_priority");
+        if (hm[2]) return set_error(ctx, CDX_EINVAL, "gang_priority: times and keys must be finite and >= 0");
+        *n_out = hm[0];
+        if (hm[0] == 0) return CDX_OK;
+        if (hm[1]) *redo = GANG_CHECKED;
+        else if (fb[0]) *redo = GANG_FULL;
+        return CDX_OK;
+    }
     uint32_t hm[3];
     std::vector<uint32_t> hh(8 * 256);
     cudaError_t e = cudaMemcpyAsync(hm, misc, 12, cudaMemcpyDeviceToHost, ctx->stream);
@@ -859,18 +948,18 @@ int gang_priority_run(cdx_ctx* ctx, const cdx_prog_soa* progs, uint64_t N, const
         uint32_t* fix = hist;
         const uint32_t list_cap = static_cast<uint32_t>(std::min<uint64_t>(nh - 2, 0xffffffffull));
         cudaMemsetAsync(fix, 0, 8, ctx->stream);
-        gang_fix_a<<<L.grid(n), 256, 0, ctx->stream>>>(ks, vs, kid, n, order, fix, list_cap);
+        gang_fix_a<<<L.grid(n), 256, 0, ctx->stream>>>(ks, vs, kid, n, order, fix, list_cap, nullptr);
         CDX_CHECK_LAUNCH(ctx, "gang_priority(order)");
         uint32_t fb[2] = {0, 0};
         e = cudaMemcpyAsync(fb, fix, 8, cudaMemcpyDeviceToHost, ctx->stream);
         if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
         if (e != cudaSuccess) return cuda_fail(ctx, e, "gang_priority(runs)");
         if (fb[0]) {
-            *need_full = true;
+            *redo = GANG_FULL;
             return CDX_OK;
         }
         if (fb[1]) {
-            gang_fix_b<<<L.grid(fb[1]), 256, 0, ctx->stream>>>(ks, vs, kid, n, order, fix);
+            gang_fix_b<<<L.grid(fb[1]), 256, 0, ctx->stream>>>(ks, vs, kid, n, order, fix, nullptr);
             CDX_CHECK_LAUNCH(ctx, "gang_priority(runs)");
         }
         if (keys) {
@@ -910,12 +999,15 @@ extern "C" int cdx_gang_priority(cdx_ctx* ctx, const cdx_prog_soa* progs, uint64
     if (N >= 0xffffffffull) return set_error(ctx, CDX_EINVAL, "gang_priority: at most 2^32-2 programs");
     *n_out = 0;
     if (N == 0) return CDX_OK;
-    bool need_full = false;
-    const bool force_full = getenv("CDX_GANG_FULL") != nullptr;  // 8-digit sort only (A/B timing, tests)
-    if (int st = gang_priority_run(ctx, progs, N, pol, now, order, n_out, escalated, keys, force_full, &need_full))
-        return st;
-    if (!need_full) return CDX_OK;
-    return gang_priority_run(ctx, progs, N, pol, now, order, n_out, escalated, keys, true, &need_full);
+    // CDX_GANG_MODE=checked|full pins the path (A/B timing, tests of the fallbacks)
+    const char* fm = getenv("CDX_GANG_MODE");
+    int mode = fm && !std::strcmp(fm, "full") ? GANG_FULL : (fm && !std::strcmp(fm, "checked") ? GANG_CHECKED : GANG_FAST);
+    for (;;) {
+        int redo = GANG_FAST;
+        if (int st = gang_priority_run(ctx, progs, N, pol, now, order, n_out, escalated, keys, mode, &redo)) return st;
+        if (redo == GANG_FAST || redo <= mode) return CDX_OK;
+        mode = redo;
+    }
 }
 
 extern "C" int cdx_gang_merge(cdx_ctx* ctx, const uint64_t* keys, const uint64_t* run_len, uint32_t runs,

@@ -141,12 +141,14 @@ def test_gang_degenerate_keys(ctx, case):
     assert np.array_equal(got.cpu().numpy().view(np.uint32), ref)
 
 
-@pytest.mark.parametrize("N", [5000, 300000])
-def test_gang_full_sort_mode(ctx, N, monkeypatch):
-    """The 8-digit sort (the fallback of the upper-half sort + run fix-up) on its own."""
+@pytest.mark.parametrize("mode", ["full", "checked"])
+@pytest.mark.parametrize("N,sorted_arrival", [(5000, True), (300000, True), (70000, False)])
+def test_gang_pinned_modes(ctx, N, sorted_arrival, mode, monkeypatch):
+    """The host-driven paths on their own: `checked` (pre-sort when arrivals are unsorted,
+    upper-half sort + run fix-up) and `full` (8 digits), the fallbacks of the one-sync path."""
     from paper_2412_20993_b200 import InterPolicy
-    monkeypatch.setenv("CDX_GANG_FULL", "1")
-    soa, now = _gang_inputs(N, 77)
+    monkeypatch.setenv("CDX_GANG_MODE", mode)
+    soa, now = _gang_inputs(N, 77, sorted_arrival=sorted_arrival)
     got, _, _ = ctx.gang_priority(_to_dev(soa), InterPolicy(order=1, starvation_limit=0.5, prior_tokens=128.0), now)
     ctx.sync()
     ref, _ = O.gang_order(soa, 1, 0.5, 128.0, now)
