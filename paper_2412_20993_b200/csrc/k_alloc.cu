@@ -100,9 +100,11 @@ __global__ void __launch_bounds__(AL_THREADS) allocate_scan_kernel(const __grid_
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     __shared__ uint32_t s_epoch;
+    // a one-tile call (small batches) needs no ticket, no records and no look-back
+    const bool single = p.ntiles == 1;
     if (tid == 0) {
-        s_tile = atomicAdd(&p.tickets[0], 1u);
-        s_epoch = ld_acquire(&p.tickets[2]);  // constant until every tile of this call is done
+        s_tile = single ? 0u : atomicAdd(&p.tickets[0], 1u);
+        s_epoch = single ? 0u : ld_acquire(&p.tickets[2]);  // constant until every tile of this call is done
     }
     __syncthreads();
     const uint32_t tile = s_tile;
@@ -153,6 +155,8 @@ __global__ void __launch_bounds__(AL_THREADS) allocate_scan_kernel(const __grid_
         if (lane == 0) {
             s_tot_e = tot_e;
             s_tot_k = tot_k;
+        }
+        if (lane == 0 && !single) {
             AlTile* T = p.tiles;
             const uint32_t ep = (s_epoch & 0x3fffffffu) << 2;
             if (tile == 0) {  // the first tile's aggregate is its inclusive prefix
@@ -218,7 +222,7 @@ __global__ void __launch_bounds__(AL_THREADS) allocate_scan_kernel(const __grid_
         }
         if (tid == 0) {
             const uint32_t tot_e = s_tot_e, tot_k = s_tot_k;
-            if (tile != 0) {
+            if (tile != 0 && !single) {
                 AlTile* Tw = p.tiles;
                 Tw[tile].inc_e = ee + tot_e;
                 Tw[tile].inc_k = ekk + tot_k;
@@ -259,7 +263,7 @@ __global__ void __launch_bounds__(AL_THREADS) allocate_scan_kernel(const __grid_
     }
     // every tile has drawn its ticket before any tile finishes: the last one to finish
     // rewinds the counters for the next call (no host-side bookkeeping, no memset launch)
-    if (tid == 0) {
+    if (tid == 0 && !single) {
         __threadfence();
         if (atomicAdd(&p.tickets[1], 1u) == p.ntiles - 1) {
             p.tickets[0] = 0;
