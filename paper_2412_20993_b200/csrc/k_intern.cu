@@ -97,6 +97,23 @@ __global__ void intern_insert(const uint8_t* __restrict__ arena, const uint64_t*
     }
 }
 
+// 8 arena bytes from pos (little-endian; bytes past `end` read as 0): one aligned 16-byte
+// window (two loads and a funnel shift) when it lies inside the arena [base, end), byte
+// loads otherwise.  Alignment is taken on the absolute address (the arena is the caller's).
+__device__ __forceinline__ uint64_t load8(const uint8_t* __restrict__ a, uint64_t pos, uint64_t end) {
+    const uintptr_t base = reinterpret_cast<uintptr_t>(a);
+    const uintptr_t addr = base + pos, al = addr & ~static_cast<uintptr_t>(7);
+    if (al >= base && al + 16 <= base + end && pos + 8 <= end) {
+        const uint64_t w0 = *reinterpret_cast<const uint64_t*>(al);
+        const uint64_t w1 = *reinterpret_cast<const uint64_t*>(al + 8);
+        const uint32_t sh = static_cast<uint32_t>(addr & 7) * 8;
+        return sh ? (w0 >> sh) | (w1 << (64 - sh)) : w0;
+    }
+    uint64_t v = 0;
+    for (uint32_t k = 0; k < 8 && pos + k < end; ++k) v |= static_cast<uint64_t>(a[pos + k]) << (8 * k);
+    return v;
+}
+
 __global__ void intern_verify(const uint8_t* __restrict__ arena, const uint64_t* __restrict__ off, uint64_t n,
                               const uint32_t* __restrict__ first, const uint32_t* __restrict__ slot_of,
                               uint32_t* __restrict__ is_first, int* d_err) {
@@ -107,8 +124,12 @@ __global__ void intern_verify(const uint8_t* __restrict__ arena, const uint64_t*
         if (rep != i) {
             const Trim a = trim(arena, off[i], off[i + 1]);
             const Trim b = trim(arena, off[rep], off[rep + 1]);
-            bool same = (a.e - a.b) == (b.e - b.b);
-            for (uint64_t k = 0; same && k < a.e - a.b; ++k) same = arena[a.b + k] == arena[b.b + k];
+            const uint64_t len = a.e - a.b, end = off[n];
+            bool same = len == b.e - b.b;
+            for (uint64_t k = 0; same && k < len; k += 8) {  // 8 bytes per compare
+                const uint64_t m = len - k >= 8 ? ~0ull : (1ull << (8 * (len - k))) - 1ull;
+                same = ((load8(arena, a.b + k, end) ^ load8(arena, b.b + k, end)) & m) == 0;
+            }
             if (!same) set_dev_err(d_err, DEV_INTERN_COLLISION);
         }
     }
