@@ -111,8 +111,21 @@ __global__ void __launch_bounds__(AL_THREADS) allocate_scan_kernel(const __grid_
     if (tile >= p.ntiles) __trap();  // a stale ticket counter must fail loudly, never scribble
     const uint64_t base = static_cast<uint64_t>(tile) * AL_TILE;
 
-    // ---- per-request decision, coalesced
+    // ---- per-request decision, coalesced.  The first meets word of
+    // every item is loaded before any is used: one memory round trip for the tile, not one
+    // per item (the scan loop below has a data-dependent exit the compiler will not hoist
+    // loads across).  Further words (P > 32 with test points past probe 32) load on demand.
+    uint32_t m0[AL_ITEMS];
+#pragma unroll
+    for (int i = 0; i < AL_ITEMS; ++i) {
+        const uint64_t r = base + static_cast<uint64_t>(i) * AL_THREADS + tid;
+        m0[i] = (p.chk_words && r < p.R) ? __ldg(p.meets + r * p.words) : 0u;
+    }
+    // No global store happens before the tile's aggregate is published: the flag is a
+    // release store, and a release waits for every earlier store of its thread.  The
+    // per-request outputs are written in the last phase instead.
     uint32_t pk[AL_ITEMS];  // inclusive warp scan of (units << 12 | kept)
+    uint32_t certain = 0;   // bit i: item i terminated on a threshold
 #pragma unroll
     for (int i = 0; i < AL_ITEMS; ++i) {
         const uint64_t r = base + static_cast<uint64_t>(i) * AL_THREADS + tid;
@@ -121,16 +134,14 @@ __global__ void __launch_bounds__(AL_THREADS) allocate_scan_kernel(const __grid_
             e = static_cast<uint32_t>(p.cap);
             uint8_t why = CDX_EXIT_BUDGET;
             for (uint32_t w = 0; w < p.chk_words; ++w) {
-                const uint32_t x = __ldg(p.meets + r * p.words + w) & p.chk[w];
+                const uint32_t x = (w ? __ldg(p.meets + r * p.words + w) : m0[i]) & p.chk[w];
                 if (x) {
                     e = w * 32 + static_cast<uint32_t>(__ffs(x));  // knob = probe index + 1
                     why = CDX_EXIT_CERTAIN;
                     break;
                 }
             }
-            if (p.exit_knob) p.exit_knob[r] = static_cast<int32_t>(e);
-            if (p.reason) p.reason[r] = why;
-            if (p.granted) p.granted[r] = static_cast<int32_t>(e);
+            certain |= (why == CDX_EXIT_CERTAIN ? 1u : 0u) << i;
         }
         const uint32_t k = (r < p.R && static_cast<int32_t>(e) > p.detect) ? 1u : 0u;
         pk[i] = warp_incl_scan<uint32_t>((e << 12) | k, lane);
@@ -166,7 +177,6 @@ __global__ void __launch_bounds__(AL_THREADS) allocate_scan_kernel(const __grid_
                 T[tile].agg_e = tot_e;
                 T[tile].agg_k = tot_k;
             }
-            __threadfence();  // the record is complete before its flag says so
             st_release(&T[tile].flag, ep | (tile == 0 ? 2u : 1u));
         }
     }
@@ -226,7 +236,6 @@ __global__ void __launch_bounds__(AL_THREADS) allocate_scan_kernel(const __grid_
                 AlTile* Tw = p.tiles;
                 Tw[tile].inc_e = ee + tot_e;
                 Tw[tile].inc_k = ekk + tot_k;
-                __threadfence();
                 st_release(&Tw[tile].flag, ep | 2u);
             }
             s_excl_e = ee;
@@ -254,6 +263,10 @@ __global__ void __launch_bounds__(AL_THREADS) allocate_scan_kernel(const __grid_
         const uint32_t own = __shfl_up_sync(0xffffffffu, x, 1);  // exclusive = inclusive of lane - 1
         const uint32_t ex = lane ? own : 0u;
         if (r >= p.R) continue;
+        const int32_t e = static_cast<int32_t>((x - ex) >> 12);  // this request's granted units
+        if (p.exit_knob) p.exit_knob[r] = e;
+        if (p.reason) p.reason[r] = ((certain >> i) & 1u) ? CDX_EXIT_CERTAIN : CDX_EXIT_BUDGET;
+        if (p.granted) p.granted[r] = e;
         const uint64_t units = ebase + s_we[i * AL_WARPS + warp] + (ex >> 12);
         if (p.offsets) p.offsets[r] = p.base_offset + static_cast<int64_t>(units * tpu);
         if (p.kept && ((x - ex) & 1u)) {
