@@ -1,7 +1,7 @@
 #!/bin/bash
 # prof_round.sh <tag>: launch lists (C, B, D, E) + one `ncu --set full` capture per hot kernel
 # + the default bench line, all under gpurun_out/ (summarise with tools/summarize_profiles.py)
-tag=${1:-r1e}
+tag=${1:-r1f}
 mkdir -p gpurun_out
 B="python bench.py --steps 3 --warmup 3 --no-others --no-cpu-baseline --no-e2e"
 M="gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum"
@@ -12,7 +12,7 @@ timeout 300 ncu --set full --clock-control none --import-source on -k regex:sc_f
 timeout 300 ncu --set full --clock-control none --import-source on -k regex:allocate_scan -s 3 -c 1 -o gpurun_out/${tag}_full_alloc $B --config C > /dev/null 2>&1
 timeout 300 ncu --set full --clock-control none --import-source on -k regex:cot_run64 -s 3 -c 1 -o gpurun_out/${tag}_full_cot $B --config B > /dev/null 2>&1
 timeout 300 ncu --set full --clock-control none --import-source on -k regex:reward_quad -s 2 -c 1 -o gpurun_out/${tag}_full_reward $B --config D > /dev/null 2>&1
-timeout 300 ncu --set full --clock-control none --import-source on -k regex:os_pass -s 8 -c 1 -o gpurun_out/${tag}_full_gang $B --config E > /dev/null 2>&1
+timeout 300 ncu --set full --clock-control none --import-source on -k regex:os_pass -s 4 -c 1 -o gpurun_out/${tag}_full_gang $B --config E > /dev/null 2>&1
 timeout 300 ncu --set full --clock-control none --import-source on -k regex:parse_lines -s 1 -c 1 -o gpurun_out/${tag}_full_jsonl $B --config J > /dev/null 2>&1
 timeout 900 python bench.py > gpurun_out/${tag}_bench.json 2> gpurun_out/${tag}_bench.err
 ls gpurun_out | grep $tag
