@@ -96,3 +96,21 @@ def test_cot_errors(ctx):
         ctx.cot_exit(ids, hes, ProbeConfig(0, 3, 0.5, 100))
     with pytest.raises(CdxInvalidArgument, match="max_tokens must be >= 1"):
         ctx.cot_exit(ids, hes, ProbeConfig(64, 3, 0.5, 0))
+
+
+@pytest.mark.parametrize("w", [1, 2, 3, 4])
+def test_cot_exhaustive_len8(ctx, w):
+    """SURVEY §4 plan item 2 at full length: all 6,561 traces of length 8 over 3 answers x all
+    256 hesitation masks (1,679,616 traces), against the literal prefix replay of
+    should_exit, for 5 thresholds x 3 budgets per window."""
+    P = 8
+    seqs = np.array(list(itertools.product(range(3), repeat=P)), np.uint32)
+    masks = np.arange(1 << P, dtype=np.uint64)
+    ids = np.repeat(seqs, len(masks), axis=0)
+    hes = np.tile(masks, len(seqs)).reshape(-1, 1)
+    for tau in (0.5, 0.6, 0.75, 0.9, 1.0):
+        for mt in (10 ** 6, 64 * 5, 64 * 8):
+            cfg = O.probe_cfg(64, w, tau, mt)
+            ref = O.cot_exit(ids, hes, cfg, replay=True, want_ck=True)
+            got = _run(ctx, ids, hes, cfg)
+            _check(got, ref)

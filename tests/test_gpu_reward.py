@@ -145,3 +145,52 @@ def test_reward_quad_nan_propagates_like_reference(ctx):
     R, _, _ = _run(ctx, rw, None, agg)
     _, R32, _ = O.reward_certaindex(rw, None, agg)
     assert np.array_equal(R.view(np.uint32), R32.view(np.uint32))
+
+
+def _partitions(n):
+    """All integer partitions of n, largest part first (ZS1, anti-lexicographic)."""
+    x = [1] * (n + 1)
+    x[1], m, h = n, 1, 1
+    yield x[1:m + 1]
+    while x[1] != 1:
+        if x[h] == 2:
+            m, x[h], h = m + 1, 1, h - 1
+        else:
+            r, t = x[h] - 1, m - h + 1
+            x[h] = r
+            while t >= r:
+                h += 1
+                x[h], t = r, t - r
+            if t == 0:
+                m = h
+            else:
+                m = h + 1
+                if t > 1:
+                    h += 1
+                    x[h] = t
+        yield x[1:m + 1]
+
+
+@pytest.mark.parametrize("n", [16, 32, 64])
+def test_reward_entropy_all_partitions(ctx, n):
+    """SURVEY §4 plan item 2: every clustering shape of n answers (p(64) = 1,741,630), each in
+    sorted and in a shuffled first-seen order, as one MCTS step of W = n nodes.  The FP64
+    fold over first-seen clusters must give the oracle's H~ bits for all of them; shapes
+    with more than 8 clusters run through the overflow kernel."""
+    flat, lens = [], []
+    for p in _partitions(n):
+        flat.extend(p)
+        lens.append(len(p))
+    flat, lens = np.array(flat, np.int64), np.array(lens, np.int64)
+    starts = np.concatenate([[0], np.cumsum(lens)[:-1]])
+    labels = (np.arange(len(flat)) - np.repeat(starts, lens)).astype(np.uint32)
+    ids = np.repeat(labels, flat).reshape(len(lens), n)
+    shuf = np.random.default_rng(n).permuted(ids, axis=1)  # other first-seen orders
+    ids = np.concatenate([ids, shuf])[:, None, :]  # (G, T=1, W=n)
+    G = ids.shape[0]
+    rw = np.full((G, 1, n), 0.5, np.float32)
+    agg = (np.arange(G) % 2).astype(np.uint8)
+    R, H, _ = _run(ctx, rw, ids, agg)
+    _, R32, Ho = O.reward_certaindex(rw, ids, agg)
+    assert np.array_equal(H.view(np.uint32), Ho.view(np.uint32))
+    assert np.array_equal(R.view(np.uint32), R32.view(np.uint32))
