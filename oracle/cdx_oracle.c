@@ -526,6 +526,14 @@ int cdxo_cot_exit_batched(const uint32_t* ids, const uint64_t* hes, const int64_
 int cdxo_reward_certaindex(const float* rewards, const uint32_t* ids, const uint8_t* agg,
                            uint64_t G, uint32_t T, uint32_t W, double* R64, float* Rout,
                            float* Hout) {
+    return cdxo_reward_certaindex2(rewards, ids, agg, G, T, W, R64, Rout, Hout, NULL);
+}
+
+/* The same with the FP64 certaindex as well (H64, nullable): the value the thresholds are
+ * applied to (runtime.cpp:279-292 -> combined_meets_thresholds, metrics.cpp:159-171). */
+int cdxo_reward_certaindex2(const float* rewards, const uint32_t* ids, const uint8_t* agg,
+                            uint64_t G, uint32_t T, uint32_t W, double* R64, float* Rout,
+                            float* Hout, double* H64) {
     const size_t n_all = (size_t)T * W;
     int* sizes = (int*)malloc(sizeof(int) * (n_all ? n_all : 1));
     int* leaders = (int*)malloc(sizeof(int) * (n_all ? n_all : 1));
@@ -556,9 +564,11 @@ int cdxo_reward_certaindex(const float* rewards, const uint32_t* ids, const uint
             const double rv = agg[g] == CDX_AGG_MAX ? best : sum / (double)n;
             if (R64) R64[g * T + t] = rv;
             if (Rout) Rout[g * T + t] = (float)rv;
-            if (ids && Hout) {
+            if (ids && (Hout || H64)) {
                 const int m = cdxo_cluster_exact_ids(ids + g * n_all, (int)n, sizes, leaders);
-                Hout[g * T + t] = (float)cdxo_certaindex_entropy(sizes, m, (int)n);
+                const double h = cdxo_certaindex_entropy(sizes, m, (int)n);
+                if (Hout) Hout[g * T + t] = (float)h;
+                if (H64) H64[g * T + t] = h;
             }
         }
         if (st) break;

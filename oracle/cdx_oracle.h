@@ -89,6 +89,9 @@ int cdxo_cot_amin(int w, double tau);
 int cdxo_reward_certaindex(const float* rewards, const uint32_t* ids, const uint8_t* agg,
                            uint64_t G, uint32_t T, uint32_t W, double* R64, float* Rout,
                            float* Hout);
+int cdxo_reward_certaindex2(const float* rewards, const uint32_t* ids, const uint8_t* agg,
+                            uint64_t G, uint32_t T, uint32_t W, double* R64, float* Rout,
+                            float* Hout, double* H64);
 
 /* ---- gang priority order (K6), SPEC.md:422-448,467-472 ----------------------------- */
 int cdxo_gang_order(const cdx_prog_soa* progs, uint64_t N, const cdx_inter_policy* pol,

@@ -224,17 +224,20 @@ def cot_exit(ids, hes, cfg, offsets=None, replay=False, want_ck=False):
     return dict(exit_step=ex, reason=why, final_id=fid, low_conf=low, ck=ck)
 
 
-def reward_certaindex(rw, ids, agg):
+def reward_certaindex(rw, ids, agg, want_h64=False):
+    """(R64, R32, H32) — plus H64 (the FP64 certaindex the thresholds see) with want_h64."""
     G, T, W = rw.shape
     R64 = np.empty((G, T), np.float64)
     R32 = np.empty((G, T), np.float32)
     H = np.empty((G, T), np.float32) if ids is not None else None
-    st = lib().cdxo_reward_certaindex(_p(np.ascontiguousarray(rw)), _p(None if ids is None else np.ascontiguousarray(ids)),
-                                      _p(np.ascontiguousarray(agg, dtype=np.uint8)), C.c_uint64(G), C.c_uint32(T),
-                                      C.c_uint32(W), _p(R64), _p(R32), _p(H))
+    H64 = np.empty((G, T), np.float64) if (ids is not None and want_h64) else None
+    st = lib().cdxo_reward_certaindex2(_p(np.ascontiguousarray(rw)),
+                                       _p(None if ids is None else np.ascontiguousarray(ids)),
+                                       _p(np.ascontiguousarray(agg, dtype=np.uint8)), C.c_uint64(G), C.c_uint32(T),
+                                       C.c_uint32(W), _p(R64), _p(R32), _p(H), _p(H64))
     if st:
         raise ValueError(f"oracle reward status {st}")
-    return R64, R32, H
+    return (R64, R32, H, H64) if want_h64 else (R64, R32, H)
 
 
 def gang_order(soa, order_kind, starvation_limit, prior, now, id_base=0):
