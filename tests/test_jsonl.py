@@ -65,7 +65,8 @@ def _category(msg):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("n,progs,seed", [(1, 1, 0), (200, 5, 1), (5000, 300, 2), (50000, 4000, 3)])
+@pytest.mark.parametrize("n,progs,seed", [(1, 1, 0), (200, 5, 1), (5000, 300, 2), (50000, 4000, 3),
+                                           (1 << 20, 1 << 14, 5)])  # the last: config J's size
 def test_jsonl_matches_reference(ctx, n, progs, seed):
     text = _gen_trace(n, progs, seed)
     ref = O.ref_parse_jsonl(text)
