@@ -15,7 +15,7 @@ import subprocess
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-ORACLE_SO = os.path.join(HERE, "liboracle.so")
+ORACLE_SO = os.environ.get("CDX_ORACLE_SO", os.path.join(HERE, "liboracle.so"))  # override: sanitizer builds
 REF_SO = os.path.join(HERE, "_ref", "libcdxref.so")
 
 P = C.c_void_p
