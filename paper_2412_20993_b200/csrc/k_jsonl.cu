@@ -71,9 +71,14 @@ __device__ __forceinline__ uint64_t nl_mask64(const char* __restrict__ t, uint64
     return m;
 }
 
-__global__ void nl_count(const char* __restrict__ t, uint64_t n, uint32_t* __restrict__ cnt) {
+// counts per chunk; each thread's 64-bit newline mask is kept (n/8 bytes) so the scatter
+// pass reads the masks instead of the text a second time
+__global__ void nl_count(const char* __restrict__ t, uint64_t n, uint32_t* __restrict__ cnt,
+                         uint64_t* __restrict__ masks) {
     const uint64_t b = static_cast<uint64_t>(blockIdx.x) * JL_CHUNK + threadIdx.x * JL_PER_THREAD;
-    uint32_t c = b < n ? __popcll(nl_mask64(t, b, n)) : 0u;
+    const uint64_t m = b < n ? nl_mask64(t, b, n) : 0ull;
+    masks[static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x] = m;
+    uint32_t c = __popcll(m);
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
     __shared__ uint32_t s[32];
@@ -88,12 +93,12 @@ __global__ void nl_count(const char* __restrict__ t, uint64_t n, uint32_t* __res
 
 
 // newline positions in order: each thread's 64-byte mask, a block scan of the counts
-__global__ void nl_scatter(const char* __restrict__ t, uint64_t n, const uint32_t* __restrict__ base,
+__global__ void nl_scatter(const uint64_t* __restrict__ masks, uint64_t n, const uint32_t* __restrict__ base,
                            uint64_t* __restrict__ pos) {
     __shared__ uint32_t s_w[32];
     const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const uint64_t b = static_cast<uint64_t>(blockIdx.x) * JL_CHUNK + threadIdx.x * JL_PER_THREAD;
-    uint64_t m = b < n ? nl_mask64(t, b, n) : 0ull;
+    uint64_t m = b < n ? masks[static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x] : 0ull;
     const uint32_t c = __popcll(m);
     uint32_t inc = c;
 #pragma unroll
@@ -947,7 +952,8 @@ extern "C" int cdx_jsonl_parse(cdx_ctx* ctx, const char* text, uint64_t nbytes, 
     if (nbytes >= (1ull << 32)) return set_error(ctx, CDX_EINVAL, "jsonl_parse: at most 4 GiB per call");
     const uint64_t nchunks = (nbytes + JL_CHUNK - 1) / JL_CHUNK;
     // phase 1 (small scratch): newline count per chunk, then its scan
-    uint8_t* s1 = static_cast<uint8_t*>(scratch2(ctx, 4096 + nchunks * 4 + 256 + (nchunks / SL_TILE + 2) * 8 + 256));
+    uint8_t* s1 = static_cast<uint8_t*>(
+        scratch2(ctx, 4096 + nchunks * 4 + 256 + (nchunks / SL_TILE + 2) * 8 + 256 + nchunks * 256 * 8 + 256));
     if (!s1) return set_error(ctx, CDX_ECUDA, "jsonl_parse: scratch allocation failed");
     uint8_t* p1 = s1;
     uint64_t* misc = carve<uint64_t>(p1, 16);  // [0] newlines, [1] first bad line, [2] records, [3] scan total
@@ -955,7 +961,8 @@ extern "C" int cdx_jsonl_parse(cdx_ctx* ctx, const char* text, uint64_t nbytes, 
     uint64_t* crec = carve<uint64_t>(p1, nchunks / SL_TILE + 2);
     cudaMemsetAsync(misc, 0, 16 * 8, ctx->stream);
     cudaMemsetAsync(misc + 1, 0xff, 8, ctx->stream);
-    nl_count<<<static_cast<unsigned>(nchunks), 256, 0, ctx->stream>>>(text, nbytes, cnt);
+    uint64_t* nlm = carve<uint64_t>(p1, nchunks * 256);
+    nl_count<<<static_cast<unsigned>(nchunks), 256, 0, ctx->stream>>>(text, nbytes, cnt, nlm);
     CDX_CHECK_LAUNCH(ctx, "jsonl(lines)");
     if (int st = scan_excl(ctx, LoadU32{cnt}, nchunks, cnt, false, crec, misc)) return st;  // in place
     uint64_t h_nl = 0;
@@ -983,7 +990,7 @@ extern "C" int cdx_jsonl_parse(cdx_ctx* ctx, const char* text, uint64_t nbytes, 
     uint8_t* p = s;
     const size_t bytes = bulk;
     uint64_t* nl = carve<uint64_t>(p, h_nl + 1);
-    nl_scatter<<<static_cast<unsigned>(nchunks), 256, 0, ctx->stream>>>(text, nbytes, cnt, nl);
+    nl_scatter<<<static_cast<unsigned>(nchunks), 256, 0, ctx->stream>>>(nlm, nbytes, cnt, nl);
     CDX_CHECK_LAUNCH(ctx, "jsonl(line ends)");
     LineOut o;
     o.st = carve<uint8_t>(p, n_lines);
