@@ -148,8 +148,16 @@ def dist_setup():
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world > 1:
         import torch.distributed as dist
+        # test hooks: CDX_BENCH_BACKEND=gloo with CDX_BENCH_SHARE_DEVICE=1 runs every rank on
+        # cuda:0 (exercises the N>1 path on a one-GPU box; its numbers mean nothing)
+        backend = os.environ.get("CDX_BENCH_BACKEND", "nccl")
+        if os.environ.get("CDX_BENCH_SHARE_DEVICE") == "1":
+            local = 0
         torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     elif torch.cuda.is_available():
         torch.cuda.set_device(0)
     return rank, world, local

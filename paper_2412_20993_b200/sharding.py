@@ -56,9 +56,12 @@ class Sharded:
             out = torch.empty((self.world * t.shape[0],) + tuple(t.shape[1:]), dtype=t.dtype, device=t.device)
             self.dist.all_gather_into_tensor(out, t.contiguous(), group=self.group)
             return out
-        parts = [torch.empty_like(t) for _ in range(self.world)]
-        self.dist.all_gather(parts, t.contiguous(), group=self.group)
-        return torch.cat(parts)
+        # gloo (the CPU tests, and the one-GPU multi-rank tests) gathers host tensors only
+        src = t.contiguous().cpu() if t.is_cuda else t.contiguous()
+        parts = [torch.empty_like(src) for _ in range(self.world)]
+        self.dist.all_gather(parts, src, group=self.group)
+        out = torch.cat(parts)
+        return out.to(t.device) if t.is_cuda else out
 
     # ---- K2 + K5 with global token offsets ------------------------------------------
     def sc_decide(self, ids, thresholds, policy, r0: int, out: Optional[dict] = None, hcert=None, meets=None):
