@@ -43,6 +43,7 @@ struct cdx_ctx {
     size_t jl_bytes = 0;
     // std::exp on the 2^-24 grid of [0,1] (Rebase aggregation), built on first use
     double* exp_tab = nullptr;
+    double* comp_tab[17] = {};  // K2: H~ per first-seen cluster-size composition, S <= 16 (k_sc.cu)
     // term-table cache (device): keyed by the list of n values it was built for
     double* tt_dev = nullptr;
     size_t tt_bytes = 0;

@@ -189,6 +189,8 @@ int cdx_ctx_destroy(cdx_ctx* ctx) {
     if (ctx->tt_dev) cudaFree(ctx->tt_dev);
     if (ctx->al_state) cudaFree(ctx->al_state);
     if (ctx->exp_tab) cudaFree(ctx->exp_tab);
+    for (double* t : ctx->comp_tab)
+        if (t) cudaFree(t);
     if (ctx->jl_buf) cudaFree(ctx->jl_buf);
     if (ctx->d_err) cudaFree(ctx->d_err);
     if (ctx->h_err) cudaFreeHost(ctx->h_err);

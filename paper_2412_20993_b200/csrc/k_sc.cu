@@ -308,6 +308,48 @@ void launch_sc(cdx_ctx* ctx, const ScParams& p, uint32_t warps_per_cta) {
     sc_certaindex_kernel<SCT><<<static_cast<unsigned>(grid), warps_per_cta * 32, smem, ctx->stream>>>(p);
 }
 
+// H~ of a row depends only on its cluster sizes in first-seen order, a composition of S.
+// For S <= 16 there are 2^(S-1) of them (cut bit c-1 set for every cumulative size c < S),
+// so the host evaluates every one once per context with exactly the device's IEEE
+// sequence (h = 0 - T[s1] - T[s2] - ..., max(0, h), (log S - h) / log S, clamp: only
+// subtractions and one division, nothing to contract) and the peel engine replaces its
+// FP64 fold and division by one table load.  The result is the same double bit for bit.
+int comp_table(cdx_ctx* ctx, const ScParams& p) {
+    const uint32_t S = p.S;
+    if (ctx->comp_tab[S]) return CDX_OK;  // term[] and log S depend on S only
+    const uint32_t n = 1u << (S - 1);
+    std::vector<double> tab(n);
+    for (uint32_t code = 0; code < n; ++code) {
+        if (code == 0) {  // one cluster holds every answer
+            tab[code] = 1.0;
+            continue;
+        }
+        double h = 0.0;
+        uint32_t prev = 0;
+        bool first = true;
+        for (uint32_t c = 1; c <= S; ++c) {
+            if (c < S && !((code >> (c - 1)) & 1u)) continue;
+            const uint32_t size = c - prev;
+            prev = c;
+            h = first ? 0.0 - p.term[size] : h - p.term[size];
+            first = false;
+        }
+        h = (0.0 < h) ? h : 0.0;
+        const double v = (p.logn - h) / p.logn;
+        tab[code] = v < 0.0 ? 0.0 : (1.0 < v ? 1.0 : v);
+    }
+    double* d = nullptr;
+    if (cudaMalloc(&d, n * sizeof(double)) != cudaSuccess) return set_error(ctx, CDX_ECUDA, "sc_certaindex: table");
+    const cudaError_t e = cudaMemcpyAsync(d, tab.data(), n * sizeof(double), cudaMemcpyHostToDevice, ctx->stream);
+    if (e == cudaSuccess) cudaStreamSynchronize(ctx->stream);  // tab is a host temporary
+    if (e != cudaSuccess) {
+        cudaFree(d);
+        return cuda_fail(ctx, e, "sc_certaindex: table");
+    }
+    ctx->comp_tab[S] = d;
+    return CDX_OK;
+}
+
 }  // namespace cdx
 
 extern "C" {
@@ -349,6 +391,11 @@ int cdx_sc_certaindex(cdx_ctx* ctx, const uint32_t* ids, uint64_t R, uint32_t P,
     for (uint32_t c = 1; c <= S; ++c) p.term[c] = host_term(c, S);
     p.logn = std::log(static_cast<double>(S));
 
+    p.comp = nullptr;
+    if (S >= 2 && S <= 16) {
+        if (int st = comp_table(ctx, p)) return st;
+        p.comp = ctx->comp_tab[S];
+    }
     // fast path: TMA-staged groups, warp-match + ALU-peel engines side by side (k_sc_fast.cu)
     if (launch_sc_fast(ctx, p)) {
         CDX_CHECK_LAUNCH(ctx, "sc_certaindex(fast)");

@@ -24,6 +24,7 @@ struct ScParams {
     double th_cut[MAX_TH];
     double term[33];
     double logn;
+    const double* comp;  // S <= 16: H~ of every first-seen size composition (null: fold)
 };
 
 // The TMA fast path (S in {4,8,16,32}, P % 32 == 0, 16B-aligned ids).  Returns true when

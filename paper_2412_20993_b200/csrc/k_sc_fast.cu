@@ -74,7 +74,8 @@ constexpr uint32_t PEEL_MAX = 8;
 
 template <int S>
 __device__ __forceinline__ double alu_row(const uint8_t* __restrict__ buf, const double* __restrict__ term,
-                                          uint32_t lane, double logn, bool* more) {
+                                          uint32_t lane, double logn, bool* more,
+                                          const double* __restrict__ comp) {
     uint32_t x[S];
 #pragma unroll
     for (uint32_t j = 0; j < S / 4; ++j) {
@@ -89,6 +90,24 @@ __device__ __forceinline__ double alu_row(const uint8_t* __restrict__ buf, const
     uint32_t eq = eq_mask<S>(x, x[0]);
     un &= ~eq;
     if (un == 0) return 1.0;  // one cluster holds every answer: H = 0, H~ = 1 exactly
+    if (S <= 16 && comp) {  // composition code: a cut bit after every cluster but the last
+        uint32_t cum = __popc(eq), code = 1u << (cum - 1);
+        uint32_t peeled = 1;
+        while (un) {
+            if (peeled == PEEL_MAX) {
+                *more = true;
+                return 0.0;
+            }
+            ++peeled;
+            const uint32_t l = __ffs(un) - 1;
+            const uint32_t v = *reinterpret_cast<const uint32_t*>(buf + elem_addr(lane * S + l));
+            eq = eq_mask<S>(x, v);
+            un &= ~eq;
+            cum += __popc(eq);
+            code |= 1u << (cum - 1);
+        }
+        return __ldg(comp + (code & ((1u << (S - 1)) - 1u)));
+    }
     double h = __dsub_rn(0.0, term[__popc(eq)]);
     uint32_t peeled = 1;
     while (un) {
@@ -149,9 +168,12 @@ __global__ void __launch_bounds__(FAST_WARPS * 32) sc_fast_kernel(const __grid_c
     // not cast through an integer, so every access stays an LDS)
     uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
     constexpr uint32_t GB = 32u * S * 4u;  // group bytes
+    // stage stride: the 128B swizzle repeats every 1024 B and is keyed on address bits 7-9,
+    // so every stage must start 1024-aligned (S = 4 groups are only 512 B)
+    constexpr uint32_t GS = GB < 1024u ? 1024u : GB;
     const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const uint32_t nw_cta = blockDim.x >> 5;
-    const uint32_t ring = p.stages * GB;
+    const uint32_t ring = p.stages * GS;
     uint8_t* wbase = smem + warp * ring;
     uint8_t* cnt_all = smem + nw_cta * ring;  // [warp][32 rows][32 B]
     uint8_t* cntw = cnt_all + warp * 1024u;
@@ -183,7 +205,7 @@ __global__ void __launch_bounds__(FAST_WARPS * 32) sc_fast_kernel(const __grid_c
         qG[stage] = G;
         if (G < p.ngroups) {
             mbar_expect_tx(&bar[stage], GB);
-            tma_load_2d(wbase + stage * GB, &tmap, 0, static_cast<int32_t>(G * S), &bar[stage], policy);
+            tma_load_2d(wbase + stage * GS, &tmap, 0, static_cast<int32_t>(G * S), &bar[stage], policy);
         }
     };
     if (lane == 0)
@@ -195,9 +217,9 @@ __global__ void __launch_bounds__(FAST_WARPS * 32) sc_fast_kernel(const __grid_c
         const unsigned long long G = qG[stage];
         if (G >= p.ngroups) break;  // claims are monotone: nothing left for this warp
         mbar_wait(&bar[stage], parity);
-        const uint8_t* buf = wbase + stage * GB;
+        const uint8_t* buf = wbase + stage * GS;
         bool more = false;
-        double hc = use_match ? 0.0 : alu_row<S>(buf, term, lane, p.logn, &more);
+        double hc = use_match ? 0.0 : alu_row<S>(buf, term, lane, p.logn, &more, p.comp);
         if (use_match || __any_sync(0xffffffffu, more)) hc = match_rows<S>(buf, cntw, term, lane, p.logn);
         __syncwarp();  // every lane is done with this stage (and with cntw)
         if (lane == 0) claim_issue(stage);
@@ -220,7 +242,7 @@ __global__ void __launch_bounds__(FAST_WARPS * 32) sc_fast_kernel(const __grid_c
 template <int S>
 void launch_fast(cdx_ctx* ctx, const CUtensorMap& tmap, const ScParams& p, uint32_t wpc, uint32_t match_warps,
                  unsigned long long* counter) {
-    const size_t smem = 1024 + static_cast<size_t>(wpc) * (p.stages * 32u * S * 4u + 1024u) + 34 * 8 +
+    const size_t smem = 1024 + static_cast<size_t>(wpc) * (p.stages * std::max(32u * S * 4u, 1024u) + 1024u) + 34 * 8 +
                         FAST_WARPS * SC_MAX_STAGES * 16;
     cudaFuncSetAttribute(sc_fast_kernel<S>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     int per_sm = 0;

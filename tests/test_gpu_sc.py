@@ -33,7 +33,7 @@ def test_generator_matches_oracle(ctx, R, P, S):
 
 @pytest.mark.parametrize("R,P,S", [(1, 1, 1), (5, 3, 2), (37, 20, 7), (64, 32, 16), (129, 64, 32), (777, 64, 32),
                                    (333, 33, 31), (50, 96, 24), (8, 130, 5), (2048, 32, 16), (17, 64, 3),
-                                   (300, 64, 1)])
+                                   (300, 64, 1), (500, 64, 8), (700, 32, 4), (300, 64, 12)])
 @pytest.mark.parametrize("ths", [[(SIG_E, 0.7, GE)], [], [(SIG_E, 0.5, GE), (SIG_E, 0.99, LE)]])
 def test_sc_certaindex_parity(ctx, R, P, S, ths):
     from paper_2412_20993_b200 import Threshold
@@ -44,6 +44,29 @@ def test_sc_certaindex_parity(ctx, R, P, S, ths):
     oh64, oh32, ometa = O.sc_certaindex(O.gen_sc(_og(**g), R, P, S), ths)
     assert np.array_equal(h.cpu().numpy().view(np.uint32), oh32.view(np.uint32))
     assert np.array_equal(meets.cpu().numpy().view(np.uint32), ometa)
+
+
+@pytest.mark.parametrize("S", [4, 8, 16])
+def test_sc_certaindex_all_compositions(ctx, S):
+    """Every first-seen cluster-size composition of S answers (2^(S-1); K2 reads H~ for
+    S <= 16 from a per-context table of them), laid out as consecutive label runs, plus a
+    shuffled copy of each row: the certaindex bits and meets must equal the oracle's fold."""
+    import torch
+    from paper_2412_20993_b200 import Threshold
+    codes = np.arange(1 << (S - 1), dtype=np.uint64)
+    cuts = ((codes[:, None] >> np.arange(S - 1, dtype=np.uint64)) & 1).astype(np.uint32)  # cut after sample j
+    labels = np.concatenate([np.zeros((len(codes), 1), np.uint32), np.cumsum(cuts, axis=1, dtype=np.uint32)], 1)
+    rows = np.concatenate([labels, np.random.default_rng(S).permuted(labels, axis=1)])
+    P = 32
+    pad = (-len(rows)) % P
+    rows = np.concatenate([rows, np.zeros((pad, S), np.uint32)])
+    ids = rows.reshape(-1, P, S)
+    ths = [(SIG_E, 0.5, GE)]
+    h, m = ctx.sc_certaindex(torch.from_numpy(ids.view(np.int32)).cuda(), [Threshold(*t) for t in ths])
+    ctx.sync()
+    _, oh32, om = O.sc_certaindex(ids, ths)
+    assert np.array_equal(h.cpu().numpy().view(np.uint32), oh32.view(np.uint32))
+    assert np.array_equal(m.cpu().numpy().view(np.uint32), om)
 
 
 def test_sc_certaindex_all_partitions_n32(ctx):
