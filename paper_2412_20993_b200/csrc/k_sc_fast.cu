@@ -1,9 +1,9 @@
 // k_sc_fast.cu — K2 fast path: Self-Consistency certaindex over 32-row groups with two
 // cluster engines.
 //
-// Shapes: S in {4,8,16,32}, P % 32 == 0, 16B-aligned ids (configs A and C).  The ids
-// tensor is viewed as 128-byte lines ([R*P*S/32][32] u32); a GROUP = 32 probe rows of one
-// request = S lines starting at line G*S, staged by one TMA box load into a 128B-swizzled
+// Shapes: S in {4,8,16,32}, R*P*S % 32 == 0, 16B-aligned ids (configs A and C).  The ids
+// tensor is viewed as 128-byte lines ([R*P*S/32][32] u32); a GROUP = 32 consecutive rows
+// of the flat row sequence (32 probes of one request when P % 32 == 0) = S lines at G*S, staged by one TMA box load into a 128B-swizzled
 // shared buffer (conflict-free 16-byte reads for both engines); warps pull groups from one
 // global work counter through a private 2-deep TMA ring.
 //
@@ -228,9 +228,21 @@ __global__ void __launch_bounds__(FAST_WARPS * 32) sc_fast_kernel(const __grid_c
             const bool ok = p.th_dir[t] == CDX_DIR_GE ? hc >= p.th_cut[t] : hc <= p.th_cut[t];
             meets = meets && ok;
         }
-        if (p.hcert) p.hcert[G * 32u + lane] = static_cast<float>(hc);
-        const uint32_t mw = __ballot_sync(0xffffffffu, meets);
-        if (lane == 0 && p.meets) p.meets[G] = mw;
+        const uint64_t row = G * 32u + lane;  // flat row r * P + p
+        if (p.P % 32u == 0) {  // a group is 32 probes of one request: one meets word
+            if (p.hcert) p.hcert[row] = static_cast<float>(hc);
+            const uint32_t mw = __ballot_sync(0xffffffffu, meets);
+            if (lane == 0 && p.meets) p.meets[G] = mw;
+        } else {  // flat groups straddle requests: OR each word's bits in (meets zeroed first)
+            const bool valid = row < p.R * p.P;
+            if (p.hcert && valid) p.hcert[row] = static_cast<float>(hc);
+            const uint64_t r = row / p.P;
+            const uint32_t pp = static_cast<uint32_t>(row - r * p.P);
+            const uint64_t word = valid ? r * p.words + (pp >> 5) : ~0ull;
+            const uint32_t grp = __match_any_sync(0xffffffffu, word);
+            const uint32_t bits = __reduce_or_sync(grp, (valid && meets) ? 1u << (pp & 31u) : 0u);
+            if (p.meets && valid && bits && (grp & ((1u << lane) - 1u)) == 0) atomicOr(p.meets + word, bits);
+        }
         __syncwarp();  // qG[stage] rewritten by lane 0 is visible before the next lap
         if (++stage == p.stages) {
             stage = 0;
@@ -262,8 +274,12 @@ void launch_fast(cdx_ctx* ctx, const CUtensorMap& tmap, const ScParams& p, uint3
 
 bool launch_sc_fast(cdx_ctx* ctx, const ScParams& p0) {
     const uint32_t S = p0.S;
-    const uint64_t lines = p0.R * p0.P * S / 32;
-    if (!(S == 4 || S == 8 || S == 16 || S == 32) || p0.P % 32 != 0 ||
+    // Groups are 32 consecutive rows of the flat [R*P] row sequence.  With P % 32 == 0 a
+    // group is 32 probes of one request; otherwise it may straddle requests and each row's
+    // meets bit is OR-ed into its word.  The rows must fill whole 128-byte lines.
+    const uint64_t rows = p0.R * p0.P;
+    const uint64_t lines = rows * S / 32;
+    if (!(S == 4 || S == 8 || S == 16 || S == 32) || (rows * S) % 32 != 0 ||
         reinterpret_cast<uintptr_t>(p0.ids) % 16 != 0 || lines >= (1ull << 31))
         return false;
     const char* impl = getenv("CDX_SC_IMPL");
@@ -275,6 +291,10 @@ bool launch_sc_fast(cdx_ctx* ctx, const ScParams& p0) {
     if (!encode_tmap(&tmap, p0.ids, 2, dims, strides, box, CU_TENSOR_MAP_DATA_TYPE_UINT32, CU_TENSOR_MAP_SWIZZLE_128B))
         return false;
     ScParams p = p0;
+    p.ngroups = (rows + 31) / 32;
+    if (p.P % 32 != 0 && p.meets) {
+        if (cudaMemsetAsync(p.meets, 0, p.R * p.words * 4, ctx->stream) != cudaSuccess) return false;
+    }
     // warps per CTA, ring depth per warp and how many warps of a CTA run the match engine
     // (defaults tuned on B200, profiles/)
     // config C sweep: 8 warps x 2 stages, every warp on the ALU engine (match fallback per

@@ -33,7 +33,9 @@ def test_generator_matches_oracle(ctx, R, P, S):
 
 @pytest.mark.parametrize("R,P,S", [(1, 1, 1), (5, 3, 2), (37, 20, 7), (64, 32, 16), (129, 64, 32), (777, 64, 32),
                                    (333, 33, 31), (50, 96, 24), (8, 130, 5), (2048, 32, 16), (17, 64, 3),
-                                   (300, 64, 1), (500, 64, 8), (700, 32, 4), (300, 64, 12)])
+                                   (300, 64, 1), (500, 64, 8), (700, 32, 4), (300, 64, 12),
+                                   (301, 63, 32), (500, 48, 16), (257, 50, 16), (333, 9, 8), (1001, 17, 32),
+                                   (64, 40, 4)])
 @pytest.mark.parametrize("ths", [[(SIG_E, 0.7, GE)], [], [(SIG_E, 0.5, GE), (SIG_E, 0.99, LE)]])
 def test_sc_certaindex_parity(ctx, R, P, S, ths):
     from paper_2412_20993_b200 import Threshold
