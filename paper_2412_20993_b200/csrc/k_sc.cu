@@ -25,6 +25,85 @@
 
 namespace cdx {
 
+// ALU peel engine for a runtime S (SB = S rounded up to a multiple of 8): lane = row, the
+// row's S ids in registers, clusters peeled in first-seen order with S compares each
+// (ISETP + predicated OR).  Rows with more than RT_PEEL_MAX clusters report *more and the
+// warp redoes the group with the match engine below.  The same fold as every engine: the
+// composition table for S <= 16, else h -= term[size] in first-seen order in FP64.
+constexpr uint32_t RT_PEEL_MAX = 8;
+
+__device__ __forceinline__ void or_if_eq_rt(uint32_t& a, uint32_t x, uint32_t v, uint32_t bit) {
+    asm("{\n\t.reg .pred p;\n\tsetp.eq.u32 p, %1, %2;\n\t@p or.b32 %0, %0, %3;\n\t}"
+        : "+r"(a)
+        : "r"(x), "r"(v), "r"(bit));
+}
+template <int SB>
+__device__ __forceinline__ uint32_t eq_mask_rt(const uint32_t (&x)[SB], uint32_t v) {
+    uint32_t a0 = 0, a1 = 0, a2 = 0, a3 = 0;
+#pragma unroll
+    for (uint32_t e = 0; e < SB; e += 4) {
+        or_if_eq_rt(a0, x[e], v, 1u << e);
+        or_if_eq_rt(a1, x[e + 1], v, 2u << e);
+        or_if_eq_rt(a2, x[e + 2], v, 4u << e);
+        or_if_eq_rt(a3, x[e + 3], v, 8u << e);
+    }
+    return (a0 | a1) | (a2 | a3);
+}
+
+template <int SB>
+__device__ __forceinline__ double alu_row_rt(const uint32_t* __restrict__ row, uint32_t S,
+                                             const double* __restrict__ term, double logn,
+                                             const double* __restrict__ comp, bool* more) {
+    uint32_t x[SB];
+    if ((S & 3u) == 0) {  // 16-byte rows: vector loads (rows of a group are 16B-aligned)
+#pragma unroll
+        for (uint32_t j = 0; j < SB / 4; ++j) {
+            const uint4 v = j * 4 < S ? reinterpret_cast<const uint4*>(row)[j] : make_uint4(0, 0, 0, 0);
+            x[4 * j] = v.x;
+            x[4 * j + 1] = v.y;
+            x[4 * j + 2] = v.z;
+            x[4 * j + 3] = v.w;
+        }
+    } else {  // odd strides are bank-conflict free for scalar loads
+#pragma unroll
+        for (uint32_t e = 0; e < SB; ++e) x[e] = e < S ? row[e] : 0u;
+    }
+    const uint32_t valid = S >= 32 ? 0xffffffffu : ((1u << S) - 1u);
+    uint32_t eq = eq_mask_rt<SB>(x, x[0]) & valid;
+    uint32_t un = valid & ~eq;
+    if (un == 0) return 1.0;  // one cluster holds every answer: H~ = 1 exactly
+    uint32_t peeled = 1;
+    if (comp) {  // S <= 16: composition code -> table
+        uint32_t cum = __popc(eq), code = 1u << (cum - 1);
+        while (un) {
+            if (peeled == RT_PEEL_MAX) {
+                *more = true;
+                return 0.0;
+            }
+            ++peeled;
+            eq = eq_mask_rt<SB>(x, row[__ffs(un) - 1]) & valid;
+            un &= ~eq;
+            cum += __popc(eq);
+            code |= 1u << (cum - 1);
+        }
+        return __ldg(comp + (code & ((1u << (S - 1)) - 1u)));
+    }
+    double h = __dsub_rn(0.0, term[__popc(eq)]);
+    while (un) {
+        if (peeled == RT_PEEL_MAX) {
+            *more = true;
+            return 0.0;
+        }
+        ++peeled;
+        eq = eq_mask_rt<SB>(x, row[__ffs(un) - 1]) & valid;
+        un &= ~eq;
+        h = __dsub_rn(h, term[__popc(eq)]);  // h -= p*log(p), first-seen order
+    }
+    h = (0.0 < h) ? h : 0.0;
+    const double v = __ddiv_rn(__dsub_rn(logn, h), logn);
+    return v < 0.0 ? 0.0 : (1.0 < v ? 1.0 : v);
+}
+
 // One warp, one group of up to 32 rows of one request: cluster every row with a warp
 // match, then fold each row's entropy on its owner lane (lane == row within the group).
 // SCT = compile-time S (a divisor of 32: 1,2,4,8,16,32), or 0 for a runtime S <= 32.
@@ -45,6 +124,32 @@ __device__ __forceinline__ void sc_group(const ScParams& p, const uint32_t* __re
     const uint32_t subm = lane_ok ? (smask << (sub * S)) : 0u;
     const uint32_t ltm = (1u << lane) - 1u;  // lanes below me
     uint8_t* my_cnt = cntw + sub * 32u + s;  // byte (row = it*rpi + sub, sample s)
+    if (SCT == 0) {  // runtime S: the ALU engine first, the match engine only for its overflow
+        bool more = false;
+        double hc = 1.0;
+        if (lane < rows) {
+            const uint32_t* rowp = base + lane * S;
+            if (S <= 8) hc = alu_row_rt<8>(rowp, S, term, p.logn, p.comp, &more);
+            else if (S <= 16) hc = alu_row_rt<16>(rowp, S, term, p.logn, p.comp, &more);
+            else if (S <= 24) hc = alu_row_rt<24>(rowp, S, term, p.logn, p.comp, &more);
+            else hc = alu_row_rt<32>(rowp, S, term, p.logn, p.comp, &more);
+        }
+        if (!__any_sync(0xffffffffu, more)) {
+            bool meets = false;
+            if (lane < rows) {
+                meets = true;
+                for (int t = 0; t < p.n_th; ++t) {
+                    const bool ok = p.th_dir[t] == CDX_DIR_GE ? hc >= p.th_cut[t] : hc <= p.th_cut[t];
+                    meets = meets && ok;
+                }
+                if (p.hcert) p.hcert[req * p.P + row0 + lane] = static_cast<float>(hc);
+            }
+            const uint32_t mw = __ballot_sync(0xffffffffu, meets);
+            if (lane == 0 && p.meets) p.meets[req * p.words + g] = mw;
+            __syncwarp();
+            return;
+        }
+    }
     if (SCT != 0 && rows == 32) {
         // full group, S | 32: row (it*rpi + sub) element s sits at word it*32 + lane
 #pragma unroll 8
@@ -161,6 +266,12 @@ __global__ void __launch_bounds__(SC_MAX_WARPS * 32) sc_certaindex_kernel(const 
             }
         }
     };
+    // a group goes by bulk copy when its bytes start 16B-aligned and fill whole 16-byte
+    // units (every group when S % 4 == 0; full groups of any S when P % 4 == 0)
+    auto bulkable = [&](const Cursor& c) {
+        const uint32_t rows = min(32u, p.P - c.g * 32u);
+        return p.bulk_ok && (((c.req * p.P + c.g * 32u) * S) & 3u) == 0 && ((rows * S) & 3u) == 0;
+    };
     auto issue = [&](const Cursor& c, uint32_t stage) {  // lane 0 only
         const uint32_t rows = min(32u, p.P - c.g * 32u);
         mbar_expect_tx(&bar[stage], rows * S * 4u);
@@ -169,9 +280,9 @@ __global__ void __launch_bounds__(SC_MAX_WARPS * 32) sc_certaindex_kernel(const 
     };
     Cursor cur{gw / p.words, static_cast<uint32_t>(gw % p.words)};
     Cursor pre = cur;  // prefetch cursor, stages groups ahead
-    if (lane == 0 && p.bulk_ok)
+    if (lane == 0)
         for (uint32_t s = 0; s < p.stages; ++s) {
-            if (pre.req < p.R) issue(pre, s);
+            if (pre.req < p.R && bulkable(pre)) issue(pre, s);
             advance(pre, 1);
         }
 
@@ -179,17 +290,17 @@ __global__ void __launch_bounds__(SC_MAX_WARPS * 32) sc_certaindex_kernel(const 
     while (cur.req < p.R) {
         const uint32_t rows = min(32u, p.P - cur.g * 32u);
         uint32_t* buf = reinterpret_cast<uint32_t*>(wbase + stage * SC_GROUP_BYTES);
-        if (p.bulk_ok) {  // S % 4 == 0 and aligned base: every group is a 16B-multiple
+        if (bulkable(cur)) {
             mbar_wait(&bar[stage], parity);
-        } else {  // misaligned base or S % 4 != 0: plain coalesced loads
+        } else {  // misaligned base or a group of odd size: plain coalesced loads
             const uint32_t* src = p.ids + (cur.req * p.P + cur.g * 32u) * S;
             for (uint32_t i = lane; i < rows * S; i += 32) buf[i] = __ldg(src + i);
             __syncwarp();
         }
         sc_group<SCT>(p, buf, rows, cntw, term, lane, cur.req, cur.g * 32u, cur.g);
         // sc_group ends with __syncwarp: every lane is done with this stage's data
-        if (lane == 0 && p.bulk_ok) {
-            if (pre.req < p.R) issue(pre, stage);
+        if (lane == 0) {
+            if (pre.req < p.R && bulkable(pre)) issue(pre, stage);
             advance(pre, 1);
         }
         advance(cur, 1);
@@ -375,7 +486,7 @@ int cdx_sc_certaindex(cdx_ctx* ctx, const uint32_t* ids, uint64_t R, uint32_t P,
     p.S = S;
     p.words = (P + 31) / 32;
     p.ngroups = R * p.words;
-    p.bulk_ok = (reinterpret_cast<uintptr_t>(ids) % 16 == 0) && (S % 4 == 0);
+    p.bulk_ok = reinterpret_cast<uintptr_t>(ids) % 16 == 0;  // per group: see bulkable()
     // per-warp ring depth and warps per CTA (tuned on B200: see profiles/)
     uint32_t stages = 1, wpc = 4;
     if (const char* e = getenv("CDX_SC_STAGES")) stages = static_cast<uint32_t>(atoi(e));

@@ -18,7 +18,7 @@ struct ScParams {
     uint64_t ngroups;  // R * words
     uint32_t P, S, words;
     uint32_t stages;
-    int bulk_ok;  // base 16B-aligned and S % 4 == 0 (every group is then 16B-aligned)
+    int bulk_ok;  // ids base 16B-aligned (the generic kernel then bulk-copies every group whose bytes are 16B units)
     int n_th;
     uint8_t th_dir[MAX_TH];
     double th_cut[MAX_TH];

@@ -35,7 +35,7 @@ def test_generator_matches_oracle(ctx, R, P, S):
                                    (333, 33, 31), (50, 96, 24), (8, 130, 5), (2048, 32, 16), (17, 64, 3),
                                    (300, 64, 1), (500, 64, 8), (700, 32, 4), (300, 64, 12),
                                    (301, 63, 32), (500, 48, 16), (257, 50, 16), (333, 9, 8), (1001, 17, 32),
-                                   (64, 40, 4)])
+                                   (64, 40, 4), (2000, 64, 24), (999, 64, 31), (1500, 40, 20), (700, 64, 13), (400, 37, 29), (300, 64, 6)])
 @pytest.mark.parametrize("ths", [[(SIG_E, 0.7, GE)], [], [(SIG_E, 0.5, GE), (SIG_E, 0.99, LE)]])
 def test_sc_certaindex_parity(ctx, R, P, S, ths):
     from paper_2412_20993_b200 import Threshold
