@@ -48,7 +48,7 @@ def test_sc_certaindex_parity(ctx, R, P, S, ths):
     assert np.array_equal(meets.cpu().numpy().view(np.uint32), ometa)
 
 
-@pytest.mark.parametrize("S", [4, 8, 16])
+@pytest.mark.parametrize("S", [4, 5, 8, 12, 16])
 def test_sc_certaindex_all_compositions(ctx, S):
     """Every first-seen cluster-size composition of S answers (2^(S-1); K2 reads H~ for
     S <= 16 from a per-context table of them), laid out as consecutive label runs, plus a
