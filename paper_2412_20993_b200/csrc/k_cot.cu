@@ -40,6 +40,7 @@ struct CotParams {
     uint32_t stage_bytes, stages;
     int32_t w, amin;
     int32_t bstep_implicit;  // first probe index whose implicit offset >= max_tokens, or -1
+    const int32_t* bsteps;   // explicit offsets: per-request budget step (cot_budget_steps), or null
     int32_t _pad;
     int64_t max_tokens;
 };
@@ -104,15 +105,7 @@ __global__ void __launch_bounds__(128) cot_exit_kernel(const __grid_constant__ C
 
         if (r < p.R) {
             const uint32_t P = p.P;
-            int32_t bstep = p.bstep_implicit;
-            if (p.offsets) {
-                bstep = -1;
-                for (uint32_t q = 0; q < P; ++q)
-                    if (__ldg(p.offsets + r * P + q) >= p.max_tokens) {
-                        bstep = static_cast<int32_t>(q);
-                        break;
-                    }
-            }
+            const int32_t bstep = p.bsteps ? __ldg(p.bsteps + r) : p.bstep_implicit;
             // without ck only probes up to the budget step can decide the exit
             const uint32_t L = CK ? P : (bstep >= 0 ? static_cast<uint32_t>(bstep) + 1 : P);
             CotWin<W> st;
@@ -285,15 +278,7 @@ __global__ void __launch_bounds__(128) cot_run_kernel(const __grid_constant__ Co
         const bool live = r < p.R;
         // the first hesitation word is independent of the tile data: load it before the wait
         uint64_t hw64 = live ? __ldg(p.hes + r * p.hw) : 0ull;
-        int32_t bstep = p.bstep_implicit;
-        if (live && p.offsets) {
-            bstep = -1;
-            for (uint32_t q = 0; q < p.P; ++q)
-                if (__ldg(p.offsets + r * p.P + q) >= p.max_tokens) {
-                    bstep = static_cast<int32_t>(q);
-                    break;
-                }
-        }
+        const int32_t bstep = (live && p.bsteps) ? __ldg(p.bsteps + r) : p.bstep_implicit;
         if (TMA) mbar_wait(&bar[stage], parity);
         const uint8_t* tsm = smem + stage * p.stage_bytes;
         if (live) {
@@ -405,12 +390,13 @@ __global__ void __launch_bounds__(128) cot_run64_kernel(const __grid_constant__ 
             if (t < p.ntiles) issue(t, s);
         }
     const int32_t w = p.w;
-    const int32_t bstep = p.bstep_implicit;  // -1: the budget never fires within the trace
-    const uint64_t lim = (bstep < 0 || bstep >= 63) ? ~0ull : ((2ull << bstep) - 1ull);
+    const int32_t bstep_u = p.bstep_implicit;  // -1: the budget never fires within the trace
     uint32_t stage = 0, parity = 0;
     for (uint64_t tile = blockIdx.x; tile < p.ntiles; tile += stride) {
         const uint64_t r = tile * p.rows + tid;
         const bool live = r < p.R;
+        const int32_t bstep = (live && p.bsteps) ? __ldg(p.bsteps + r) : bstep_u;
+        const uint64_t lim = (bstep < 0 || bstep >= 63) ? ~0ull : ((2ull << bstep) - 1ull);
         const uint64_t umask = live ? (~__ldg(p.hes + r) & lim) : 0ull;  // usable probes <= budget step
         mbar_wait(&bar[stage], parity);
         const uint8_t* tsm = smem + stage * p.stage_bytes;
@@ -473,6 +459,27 @@ __global__ void __launch_bounds__(128) cot_run64_kernel(const __grid_constant__ 
             stage = 0;
             parity ^= 1u;
         }
+    }
+}
+
+// Explicit token offsets: the budget step of every request (first probe whose offset is
+// >= max_tokens, hesitant or not, probe.cpp:77-85) in one coalesced pass, a warp
+// per request and a ballot per 32 probes, instead of a serial offset scan in every lane.
+__global__ void cot_budget_steps(const int64_t* __restrict__ off, uint64_t R, uint32_t P, int64_t max_tokens,
+                                 int32_t* __restrict__ bsteps) {
+    const uint32_t lane = threadIdx.x & 31u;
+    const uint64_t nw = (static_cast<uint64_t>(gridDim.x) * blockDim.x) >> 5;
+    for (uint64_t r = (blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x) >> 5; r < R; r += nw) {
+        int32_t b = -1;
+        for (uint32_t q0 = 0; q0 < P; q0 += 32) {
+            const uint32_t q = q0 + lane;
+            const uint32_t hit = __ballot_sync(0xffffffffu, q < P && __ldg(off + r * P + q) >= max_tokens);
+            if (hit) {
+                b = static_cast<int32_t>(q0 + __ffs(hit) - 1);
+                break;
+            }
+        }
+        if (lane == 0) bsteps[r] = b;
     }
 }
 
@@ -555,12 +562,22 @@ extern "C" int cdx_cot_exit(cdx_ctx* ctx, const uint32_t* ids, const uint64_t* h
         const int64_t k = (cfg->max_tokens + I - 1) / I;  // smallest p+1 with (p+1)*I >= max
         p.bstep_implicit = (k - 1 < static_cast<int64_t>(P)) ? static_cast<int32_t>(k - 1) : -1;
     }
+    p.bsteps = nullptr;
+    if (offsets) {  // per-request budget steps in one coalesced pass
+        auto* bs = static_cast<int32_t*>(scratch(ctx, R * 4 + 256));
+        if (!bs) return set_error(ctx, CDX_ECUDA, "cot_exit: scratch allocation failed");
+        const uint64_t want = (R + 7) / 8;  // 8 warps (requests) per 256-thread block
+        cot_budget_steps<<<static_cast<unsigned>(std::min<uint64_t>(want, static_cast<uint64_t>(ctx->sm_count) * 16)),
+                           256, 0, ctx->stream>>>(offsets, R, P, cfg->max_tokens, bs);
+        CDX_CHECK_LAUNCH(ctx, "cot_exit(budget steps)");
+        p.bsteps = bs;
+    }
     bool tma = (P % 4 == 0) && (reinterpret_cast<uintptr_t>(ids) % 16 == 0) && P <= 512 && R <= 0x7fffffffull;
     // rows (= threads) per CTA and ring depth: small single-stage CTAs keep ~28 warps
     // per SM resident; other CTAs on the SM overlap each one's TMA wait (tuned on B200)
-    // run64 path (P == 64, implicit offsets, a_min == w): 128-request CTAs with a 2-deep ring
+    // run64 path (P == 64, a_min == w): 128-request CTAs with a 2-deep ring
     // measured best on B200 (51 us on config B vs 55 us for 64 x 1)
-    const bool run64 = P == 64 && !offsets && !ck && amin == cfg->window;
+    const bool run64 = P == 64 && !ck && amin == cfg->window;
     uint32_t rows = run64 ? 128 : 64, stages = run64 ? 2 : 1;
     if (const char* e = getenv("CDX_COT_ROWS")) rows = static_cast<uint32_t>(atoi(e));
     if (const char* e = getenv("CDX_COT_STAGES")) stages = static_cast<uint32_t>(atoi(e));
@@ -585,7 +602,7 @@ extern "C" int cdx_cot_exit(cdx_ctx* ctx, const uint32_t* ids, const uint64_t* h
     const bool want_ck = ck != nullptr;
     const char* impl = getenv("CDX_COT_IMPL");
     if (!want_ck && amin == cfg->window && !(impl && impl[0] == 'w')) {
-        if (tma && P == 64 && !offsets && !(impl && impl[0] == 'r')) {
+        if (tma && P == 64 && !(impl && impl[0] == 'r')) {
             cudaFuncSetAttribute(cot_run64_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
             int per_sm = 0;
             cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, cot_run64_kernel, p.rows, smem);

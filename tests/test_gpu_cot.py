@@ -114,3 +114,21 @@ def test_cot_exhaustive_len8(ctx, w):
             ref = O.cot_exit(ids, hes, cfg, replay=True, want_ck=True)
             got = _run(ctx, ids, hes, cfg)
             _check(got, ref)
+
+
+@pytest.mark.parametrize("R,P", [(1000, 64), (257, 64), (500, 40), (300, 128), (33, 7)])
+@pytest.mark.parametrize("w,tau", [(3, 0.9), (4, 0.7), (1, 1.0)])
+def test_cot_explicit_offsets_parity(ctx, R, P, w, tau):
+    """Explicit token offsets without ck: the per-request budget steps come from the coalesced
+    pre-pass and feed every kernel (run64 included); offsets not monotone, some rows never
+    reach the budget, some reach it at probe 0."""
+    rng = np.random.default_rng(R + P + w)
+    g = O.gen_params(seed=R * 7 + P, conv_hi=max(1, P), hesitation_prob=0.1)
+    ids, hes = O.gen_cot(g, R, P)
+    offsets = rng.integers(0, 5000, size=(R, P)).astype(np.int64)
+    offsets[::5] = np.cumsum(rng.integers(1, 40, size=(len(offsets[::5]), P)), axis=1)
+    offsets[1::7, 0] = 10 ** 6
+    cfg = O.probe_cfg(64, w, tau, 4000)
+    ref = O.cot_exit(ids, hes, cfg, offsets=offsets)
+    got = _run(ctx, ids, hes, cfg, offsets=offsets, want_ck=False)
+    _check(got, ref, want_ck=False)
