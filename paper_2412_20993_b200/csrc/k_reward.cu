@@ -36,7 +36,7 @@ constexpr int RW_KM = 8;       // register cluster slots per program
 constexpr int RW_STAGES = 2;
 constexpr int RW_MAX_TH = 8;
 constexpr int RQ_PROGS = 32;   // quad kernel: programs per CTA (4 lanes each)
-constexpr int RQ_MAX_T = 64;   // quad kernel: steps staged in the smem output tile
+constexpr int RQ_MAX_T = 256;  // quad kernel: steps staged in the smem output tile (8 B per program-step)
 constexpr int RQ_MAX_BOXES = 4;  // quad kernel: W <= 128
 
 struct RwParams {
@@ -556,13 +556,16 @@ __global__ void __launch_bounds__(RQ_PROGS * 4) reward_quad_kernel(const __grid_
 // the program's outputs are written by exactly one kernel.
 constexpr int OV_WARPS = 4;
 
+// gtab (nullable): programs too large for a shared-memory table (2 * cap + T * W words per
+// warp over ~220 KB) keep it in global memory instead, one slice per warp of the grid.
 __global__ void __launch_bounds__(OV_WARPS * 32) reward_overflow_kernel(const __grid_constant__ RwParams p,
-                                                                        uint32_t cap_log2) {
+                                                                        uint32_t cap_log2, uint32_t* gtab) {
     extern __shared__ __align__(16) uint8_t smem[];
     const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
     const uint32_t cap = 1u << cap_log2;  // hash slots (>= 2 * T * W)
     const uint32_t nmax = p.ids ? p.T * p.W : 0u;
-    uint32_t* hkey = reinterpret_cast<uint32_t*>(smem) + warp * (2 * cap + nmax);
+    uint32_t* hkey = gtab ? gtab + static_cast<size_t>(blockIdx.x * nw + warp) * (2 * cap + nmax)
+                          : reinterpret_cast<uint32_t*>(smem) + warp * (2 * cap + nmax);
     uint32_t* hord = hkey + cap;
     uint32_t* cnt = hord + cap;
     const uint32_t n_ovf = *p.ovf_count;
@@ -790,12 +793,22 @@ extern "C" int cdx_reward_certaindex(cdx_ctx* ctx, const float* rewards, const u
         // per-warp table: 2 * cap hash words + T*W counts; as many warps per CTA as fit
         const size_t per_warp = ids ? ((2u << cap_log2) + static_cast<size_t>(T) * W) * 4u : 0u;
         const size_t limit = 220u * 1024u;
-        if (per_warp > limit)
-            return set_error(ctx, CDX_EINVAL, "reward_certaindex: T*W too large for the overflow table");
-        const int warps = per_warp ? static_cast<int>(std::min<size_t>(OV_WARPS, limit / per_warp)) : OV_WARPS;
-        const size_t osmem = std::max<size_t>(16u, warps * per_warp);
-        cudaFuncSetAttribute(reward_overflow_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(osmem));
-        reward_overflow_kernel<<<ctx->sm_count, warps * 32, osmem, ctx->stream>>>(p, cap_log2);
+        if (per_warp <= limit) {
+            const int warps = per_warp ? static_cast<int>(std::min<size_t>(OV_WARPS, limit / per_warp)) : OV_WARPS;
+            const size_t osmem = std::max<size_t>(16u, warps * per_warp);
+            cudaFuncSetAttribute(reward_overflow_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(osmem));
+            reward_overflow_kernel<<<ctx->sm_count, warps * 32, osmem, ctx->stream>>>(p, cap_log2, nullptr);
+        } else {  // global-memory tables: up to ~256 MB of them, at least one warp
+            uint64_t nwarps = std::max<uint64_t>(
+                1, std::min<uint64_t>(static_cast<uint64_t>(ctx->sm_count) * OV_WARPS, (256ull << 20) / per_warp));
+            const unsigned wpb = static_cast<unsigned>(std::min<uint64_t>(OV_WARPS, nwarps));
+            nwarps = nwarps / wpb * wpb;  // whole CTAs: one table slice per launched warp
+            const unsigned blocks = static_cast<unsigned>(nwarps / wpb);
+            auto* gtab = static_cast<uint32_t*>(scratch2(ctx, nwarps * per_warp));
+            if (!gtab) return set_error(ctx, CDX_ECUDA, "reward_certaindex: overflow table allocation failed");
+            reward_overflow_kernel<<<blocks, wpb * 32, 16, ctx->stream>>>(p, cap_log2, gtab);
+        }
         CDX_CHECK_LAUNCH(ctx, "reward_certaindex(overflow)");
     }
     return CDX_OK;
