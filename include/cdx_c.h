@@ -169,7 +169,8 @@ int cdx_gen_reward(cdx_ctx* ctx, const cdx_gen_params* g, uint64_t g0, uint64_t 
  * Replaces, per (request r, probe p) row of S sampled answers,
  *   metrics::certaindex_entropy(metrics::cluster_exact(row))        metrics.hpp:44,66
  *   metrics::combined_meets_thresholds({H~}, thresholds)            metrics.hpp:116
- * ids: u32[R][P][S] interned answer ids (equal id <=> equal trimmed bytes).
+ * ids: u32[R][P][S] interned answer ids (equal id <=> equal trimmed bytes), 1 <= S <= 4096
+ * (S <= 32: 32-row groups through the TMA / bulk-copy engines; S > 32: a warp per row).
  * hcert: f32[R][P] (nullable).  meets_bits: u32[R][ceil(P/32)], bit p%32 of word p/32.
  * Decisions are taken on the FP64 certaindex; hcert is its fp32 rounding.               */
 int cdx_sc_certaindex(cdx_ctx* ctx, const uint32_t* ids, uint64_t R, uint32_t P, uint32_t S,

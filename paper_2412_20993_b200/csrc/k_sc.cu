@@ -419,6 +419,102 @@ void launch_sc(cdx_ctx* ctx, const ScParams& p, uint32_t warps_per_cta) {
     sc_certaindex_kernel<SCT><<<static_cast<unsigned>(grid), warps_per_cta * 32, smem, ctx->stream>>>(p);
 }
 
+// ---- wide rows (32 < S <= SC_WIDE_MAX): a warp per row ----------------------------------
+// The row streams through the warp 32 answers at a time.  Per round, equal values find
+// each other with MATCH; the round's first occurrence of each value looks it up in the
+// warp's shared-memory hash (value -> first-seen ordinal); values not seen before take
+// ordinals in lane order = first-seen order, one insertion at a time.  The owner (lane 0)
+// folds h -= T_S[count] over ordinals 0..m-1 in FP64 (term row T_S from the host libm),
+// clamps, applies the thresholds and ORs the row's meets bit into its word.
+constexpr uint32_t SC_WIDE_MAX = 4096;
+constexpr uint32_t SC_WIDE_WARPS = 4;
+
+struct WideParams {
+    const uint32_t* ids;
+    float* hcert;
+    uint32_t* meets;
+    const double* tab;  // T_S[0..S]
+    double logn;
+    uint64_t rows;      // R * P
+    uint32_t P, S, words, cap_log2;
+    int n_th;
+    uint8_t th_dir[MAX_TH];
+    double th_cut[MAX_TH];
+};
+
+__global__ void __launch_bounds__(SC_WIDE_WARPS * 32) sc_wide_kernel(const __grid_constant__ WideParams p) {
+    extern __shared__ __align__(16) uint8_t smem[];
+    const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    const uint32_t cap = 1u << p.cap_log2;
+    uint32_t* hkey = reinterpret_cast<uint32_t*>(smem) + warp * (2 * cap + p.S);
+    uint32_t* hord = hkey + cap;
+    uint32_t* cnt = hord + cap;
+    const uint64_t gw = static_cast<uint64_t>(blockIdx.x) * nw + warp, nwarps = static_cast<uint64_t>(gridDim.x) * nw;
+    for (uint64_t row = gw; row < p.rows; row += nwarps) {
+        for (uint32_t i = lane; i < cap; i += 32) hord[i] = 0xffffffffu;  // empty
+        __syncwarp();
+        uint32_t m = 0;
+        const uint32_t* src = p.ids + row * p.S;
+        for (uint32_t c0 = 0; c0 < p.S; c0 += 32) {
+            const uint32_t e = c0 + lane;
+            const bool act = e < p.S;
+            const uint32_t v = act ? __ldg(src + e) : 0u;
+            const uint32_t mm = __match_any_sync(0xffffffffu, v) & __ballot_sync(0xffffffffu, act);
+            const bool lead = act && (mm & ((1u << lane) - 1u)) == 0u;
+            uint32_t slot = (v * 0x9E3779B1u) >> (32 - p.cap_log2);
+            bool fresh = false;
+            if (lead) {
+                while (true) {
+                    if (hord[slot] == 0xffffffffu) {
+                        fresh = true;
+                        break;
+                    }
+                    if (hkey[slot] == v) break;
+                    slot = (slot + 1) & (cap - 1);
+                }
+            }
+            const uint32_t fb = __ballot_sync(0xffffffffu, fresh);
+            for (uint32_t bits = fb; bits; bits &= bits - 1) {  // new values in lane order
+                const uint32_t l = __ffs(bits) - 1;
+                if (lane == l) {
+                    uint32_t s2 = slot;
+                    while (hord[s2] != 0xffffffffu) s2 = (s2 + 1) & (cap - 1);
+                    hkey[s2] = v;
+                    hord[s2] = m;
+                    cnt[m] = 0;
+                    slot = s2;
+                }
+                ++m;
+                __syncwarp();
+            }
+            if (lead) cnt[hord[slot]] += __popc(mm);
+            __syncwarp();
+        }
+        if (lane == 0) {
+            double hc = 1.0;  // one cluster holds every answer: H~ = 1 exactly
+            if (m > 1) {
+                double h = 0.0;
+                for (uint32_t k = 0; k < m; ++k) h = __dsub_rn(h, __ldg(p.tab + cnt[k]));  // first-seen order
+                h = (0.0 < h) ? h : 0.0;
+                const double v = __ddiv_rn(__dsub_rn(p.logn, h), p.logn);
+                hc = v < 0.0 ? 0.0 : (1.0 < v ? 1.0 : v);
+            }
+            bool meets = true;
+            for (int t = 0; t < p.n_th; ++t) {
+                const bool ok = p.th_dir[t] == CDX_DIR_GE ? hc >= p.th_cut[t] : hc <= p.th_cut[t];
+                meets = meets && ok;
+            }
+            if (p.hcert) p.hcert[row] = static_cast<float>(hc);
+            if (p.meets && meets) {
+                const uint64_t r = row / p.P;
+                const uint32_t pp = static_cast<uint32_t>(row - r * p.P);
+                atomicOr(p.meets + r * p.words + (pp >> 5), 1u << (pp & 31u));
+            }
+        }
+        __syncwarp();
+    }
+}
+
 // H~ of a row depends only on its cluster sizes in first-seen order, a composition of S.
 // For S <= 16 there are 2^(S-1) of them (cut bit c-1 set for every cumulative size c < S),
 // so the host evaluates every one once per context with exactly the device's IEEE
@@ -470,12 +566,46 @@ int cdx_sc_certaindex(cdx_ctx* ctx, const uint32_t* ids, uint64_t R, uint32_t P,
     using namespace cdx;
     if (!ctx) return CDX_EINVAL;
     if (S == 0) return set_error(ctx, CDX_EINVAL, "cluster_exact: empty answer set");
-    if (S > 32) return set_error(ctx, CDX_EINVAL, "sc_certaindex: at most 32 samples per row");
+    if (S > SC_WIDE_MAX) return set_error(ctx, CDX_EINVAL, "sc_certaindex: at most 4096 samples per row");
     if (P == 0) return set_error(ctx, CDX_EINVAL, "sc_certaindex: probes must be >= 1");
     if (!ids) return set_error(ctx, CDX_EINVAL, "sc_certaindex: null ids");
     const bool present[4] = {true, false, false, false};
     if (int st = check_thresholds(ctx, th, n_th, present)) return st;
     if (R == 0) return CDX_OK;
+    if (S > 32) {  // wide rows: a warp per row, shared-memory hash of first-seen ordinals
+        WideParams w{};
+        w.ids = ids;
+        w.hcert = hcert;
+        w.meets = meets_bits;
+        w.rows = R * P;
+        w.P = P;
+        w.S = S;
+        w.words = (P + 31) / 32;
+        w.cap_log2 = 1;
+        while ((1u << w.cap_log2) < 2u * S) ++w.cap_log2;
+        w.n_th = static_cast<int>(n_th);
+        for (uint32_t i = 0; i < n_th; ++i) {
+            w.th_dir[i] = th[i].dir;
+            w.th_cut[i] = th[i].cutoff;
+        }
+        TermTables tt;
+        const uint32_t ns[1] = {S};
+        if (int st = build_term_tables(ctx, ns, 1, &tt)) return st;
+        w.tab = tt.tab;
+        w.logn = std::log(static_cast<double>(S));
+        if (meets_bits) cudaMemsetAsync(meets_bits, 0, R * w.words * 4, ctx->stream);  // bits are OR-ed in
+        const size_t per_warp = ((2u << w.cap_log2) + S) * 4u;
+        const uint32_t wpc = static_cast<uint32_t>(std::max<size_t>(1, std::min<size_t>(SC_WIDE_WARPS, (200u << 10) / per_warp)));
+        const size_t smem = wpc * per_warp;
+        cudaFuncSetAttribute(sc_wide_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+        int per_sm = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sc_wide_kernel, wpc * 32, smem);
+        const uint64_t want = (w.rows + wpc - 1) / wpc;
+        const uint64_t grid = std::min<uint64_t>(want, static_cast<uint64_t>(ctx->sm_count) * std::max(per_sm, 1));
+        sc_wide_kernel<<<static_cast<unsigned>(grid), wpc * 32, smem, ctx->stream>>>(w);
+        CDX_CHECK_LAUNCH(ctx, "sc_certaindex(wide)");
+        return CDX_OK;
+    }
 
     ScParams p{};
     p.ids = ids;

@@ -48,6 +48,24 @@ def test_sc_certaindex_parity(ctx, R, P, S, ths):
     assert np.array_equal(meets.cpu().numpy().view(np.uint32), ometa)
 
 
+@pytest.mark.parametrize("R,P,S,groups", [(50, 20, 33, 5), (64, 64, 64, 8), (30, 40, 100, 60), (9, 5, 1000, 300),
+                                          (2, 3, 4096, 5000), (40, 7, 48, 48)])
+def test_sc_certaindex_wide_rows(ctx, R, P, S, groups):
+    """More than 32 samples per row (the reference clusters any number): a warp per row,
+    first-seen ordinals through a shared-memory hash, the same FP64 fold."""
+    import torch
+    from paper_2412_20993_b200 import Threshold
+    rng = np.random.default_rng(S + P)
+    ids = rng.integers(0, groups, size=(R, P, S)).astype(np.uint32)
+    ids[:, ::3, :] = ids[:, ::3, :1]  # single-cluster rows
+    ths = [(SIG_E, 0.6, GE)]
+    h, m = ctx.sc_certaindex(torch.from_numpy(ids.view(np.int32)).cuda(), [Threshold(*t) for t in ths])
+    ctx.sync()
+    _, oh32, om = O.sc_certaindex(ids, ths)
+    assert np.array_equal(h.cpu().numpy().view(np.uint32), oh32.view(np.uint32))
+    assert np.array_equal(m.cpu().numpy().view(np.uint32), om)
+
+
 @pytest.mark.parametrize("S", [4, 5, 8, 12, 16])
 def test_sc_certaindex_all_compositions(ctx, S):
     """Every first-seen cluster-size composition of S answers (2^(S-1); K2 reads H~ for
