@@ -363,6 +363,8 @@ __global__ void __launch_bounds__(128) cot_run_kernel(const __grid_constant__ Co
 // exit, no data-dependent branches) and every probe whose run reaches w sets a bit in a
 // 64-bit hit mask, so the certain step is the mask's lowest bit.  Same decisions as
 // cot_run_kernel (and therefore as the reference's prefix replay).
+// NB = P / 32 boxes: P = 64 (config B) or P = 32; the probe mask is one 64-bit word.
+template <int NB>
 __global__ void __launch_bounds__(128) cot_run64_kernel(const __grid_constant__ CotParams p) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
@@ -380,7 +382,7 @@ __global__ void __launch_bounds__(128) cot_run64_kernel(const __grid_constant__ 
         uint8_t* dst = smem + stage * p.stage_bytes;
         mbar_expect_tx(&bar[stage], p.stage_bytes);
 #pragma unroll
-        for (uint32_t b = 0; b < 2; ++b)
+        for (uint32_t b = 0; b < NB; ++b)
             tma_load_2d(dst + b * p.rows * 128u, &p.tmap, static_cast<int32_t>(b * 32),
                         static_cast<int32_t>(tile * p.rows), &bar[stage], policy);
     };
@@ -397,7 +399,8 @@ __global__ void __launch_bounds__(128) cot_run64_kernel(const __grid_constant__ 
         const bool live = r < p.R;
         const int32_t bstep = (live && p.bsteps) ? __ldg(p.bsteps + r) : bstep_u;
         const uint64_t lim = (bstep < 0 || bstep >= 63) ? ~0ull : ((2ull << bstep) - 1ull);
-        const uint64_t umask = live ? (~__ldg(p.hes + r) & lim) : 0ull;  // usable probes <= budget step
+        const uint64_t pm = NB == 2 ? ~0ull : 0xffffffffull;  // probes that exist
+        const uint64_t umask = live ? (~__ldg(p.hes + r) & lim & pm) : 0ull;  // usable probes <= budget step
         mbar_wait(&bar[stage], parity);
         const uint8_t* tsm = smem + stage * p.stage_bytes;
         if (live) {
@@ -405,7 +408,7 @@ __global__ void __launch_bounds__(128) cot_run64_kernel(const __grid_constant__ 
             int32_t run = 0;
             uint32_t last = 0, hlo = 0, hhi = 0;
 #pragma unroll
-            for (uint32_t c = 0; c < 16; ++c) {  // 16-byte chunks: box c/8, chunk c%8
+            for (uint32_t c = 0; c < 8 * NB; ++c) {  // 16-byte chunks: box c/8, chunk c%8
                 const uint4 v4 = *reinterpret_cast<const uint4*>(tsm + (c >> 3) * p.rows * 128u + swz128(tid, c & 7u));
                 const uint32_t vv[4] = {v4.x, v4.y, v4.z, v4.w};
 #pragma unroll
@@ -435,7 +438,7 @@ __global__ void __launch_bounds__(128) cot_run64_kernel(const __grid_constant__ 
                 fid = *reinterpret_cast<const uint32_t*>(tsm + (cs >> 5) * p.rows * 128u + swz128(tid, (cs & 31u) >> 2) +
                                                          (cs & 3u) * 4u);
             } else {
-                const uint32_t end = bstep >= 0 ? static_cast<uint32_t>(bstep) : 63u;  // last probe seen
+                const uint32_t end = bstep >= 0 ? static_cast<uint32_t>(bstep) : 32u * NB - 1u;  // last probe seen
                 if (bstep >= 0) {
                     ex = bstep;
                     why = CDX_EXIT_BUDGET;
@@ -577,7 +580,7 @@ extern "C" int cdx_cot_exit(cdx_ctx* ctx, const uint32_t* ids, const uint64_t* h
     // per SM resident; other CTAs on the SM overlap each one's TMA wait (tuned on B200)
     // run64 path (P == 64, a_min == w): 128-request CTAs with a 2-deep ring
     // measured best on B200 (51 us on config B vs 55 us for 64 x 1)
-    const bool run64 = P == 64 && !ck && amin == cfg->window;
+    const bool run64 = (P == 64 || P == 32) && !ck && amin == cfg->window;
     uint32_t rows = run64 ? 128 : 64, stages = run64 ? 2 : 1;
     if (const char* e = getenv("CDX_COT_ROWS")) rows = static_cast<uint32_t>(atoi(e));
     if (const char* e = getenv("CDX_COT_STAGES")) stages = static_cast<uint32_t>(atoi(e));
@@ -602,12 +605,13 @@ extern "C" int cdx_cot_exit(cdx_ctx* ctx, const uint32_t* ids, const uint64_t* h
     const bool want_ck = ck != nullptr;
     const char* impl = getenv("CDX_COT_IMPL");
     if (!want_ck && amin == cfg->window && !(impl && impl[0] == 'w')) {
-        if (tma && P == 64 && !(impl && impl[0] == 'r')) {
-            cudaFuncSetAttribute(cot_run64_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+        if (tma && (P == 64 || P == 32) && !(impl && impl[0] == 'r')) {
+            auto k = P == 64 ? cot_run64_kernel<2> : cot_run64_kernel<1>;
+            cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
             int per_sm = 0;
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, cot_run64_kernel, p.rows, smem);
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, p.rows, smem);
             const uint64_t grid = std::min<uint64_t>(p.ntiles, static_cast<uint64_t>(ctx->sm_count) * std::max(per_sm, 1));
-            cot_run64_kernel<<<static_cast<unsigned>(grid), p.rows, smem, ctx->stream>>>(p);
+            k<<<static_cast<unsigned>(grid), p.rows, smem, ctx->stream>>>(p);
             CDX_CHECK_LAUNCH(ctx, "cot_exit(run64)");
             return CDX_OK;
         }

@@ -116,7 +116,18 @@ def test_cot_exhaustive_len8(ctx, w):
             _check(got, ref)
 
 
-@pytest.mark.parametrize("R,P", [(1000, 64), (257, 64), (500, 40), (300, 128), (33, 7)])
+@pytest.mark.parametrize("R,P", [(1000, 32), (129, 32), (1000, 64), (3, 64)])
+@pytest.mark.parametrize("w,tau,max_tokens", [(3, 0.9, 4096), (1, 1.0, 640), (5, 1.0, 10 ** 6), (2, 0.5, 64)])
+def test_cot_run_kernel_parity_no_ck(ctx, R, P, w, tau, max_tokens):
+    """The branch-free run kernel (P = 32 or 64, a_min == w, no C_k output), implicit offsets."""
+    g = O.gen_params(seed=R + P + w, conv_hi=max(1, P), hesitation_prob=0.15)
+    ids, hes = O.gen_cot(g, R, P)
+    cfg = O.probe_cfg(64, w, tau, max_tokens)
+    ref = O.cot_exit(ids, hes, cfg)
+    _check(_run(ctx, ids, hes, cfg, want_ck=False), ref, want_ck=False)
+
+
+@pytest.mark.parametrize("R,P", [(1000, 64), (257, 64), (500, 40), (300, 128), (33, 7), (700, 32)])
 @pytest.mark.parametrize("w,tau", [(3, 0.9), (4, 0.7), (1, 1.0)])
 def test_cot_explicit_offsets_parity(ctx, R, P, w, tau):
     """Explicit token offsets without ck: the per-request budget steps come from the coalesced
