@@ -363,7 +363,7 @@ __global__ void __launch_bounds__(128) cot_run_kernel(const __grid_constant__ Co
 // exit, no data-dependent branches) and every probe whose run reaches w sets a bit in a
 // 64-bit hit mask, so the certain step is the mask's lowest bit.  Same decisions as
 // cot_run_kernel (and therefore as the reference's prefix replay).
-// NB = P / 32 boxes: P = 64 (config B) or P = 32; the probe mask is one 64-bit word.
+// NB = P / 32 boxes (P = 32, 64 = config B, 96, 128); the usable / hit masks are NB words.
 template <int NB>
 __global__ void __launch_bounds__(128) cot_run64_kernel(const __grid_constant__ CotParams p) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -398,15 +398,26 @@ __global__ void __launch_bounds__(128) cot_run64_kernel(const __grid_constant__ 
         const uint64_t r = tile * p.rows + tid;
         const bool live = r < p.R;
         const int32_t bstep = (live && p.bsteps) ? __ldg(p.bsteps + r) : bstep_u;
-        const uint64_t lim = (bstep < 0 || bstep >= 63) ? ~0ull : ((2ull << bstep) - 1ull);
-        const uint64_t pm = NB == 2 ? ~0ull : 0xffffffffull;  // probes that exist
-        const uint64_t umask = live ? (~__ldg(p.hes + r) & lim & pm) : 0ull;  // usable probes <= budget step
+        // usable probes (not hesitant, <= the budget step) as NB 32-bit words
+        uint32_t uw[NB];
+        bool any_usable = false;
+#pragma unroll
+        for (int k = 0; k < NB; ++k) {
+            const uint64_t hw = live ? __ldg(p.hes + r * p.hw + (k >> 1)) : ~0ull;
+            const uint32_t nh = ~static_cast<uint32_t>(hw >> (32 * (k & 1)));
+            const int32_t rel = bstep - 32 * k;  // budget step relative to this word
+            const uint32_t lim = (bstep < 0 || rel >= 31) ? 0xffffffffu : (rel < 0 ? 0u : ((2u << rel) - 1u));
+            uw[k] = live ? (nh & lim) : 0u;
+            any_usable = any_usable || uw[k] != 0u;
+        }
         mbar_wait(&bar[stage], parity);
         const uint8_t* tsm = smem + stage * p.stage_bytes;
         if (live) {
-            const uint32_t ulo = static_cast<uint32_t>(umask), uhi = static_cast<uint32_t>(umask >> 32);
             int32_t run = 0;
-            uint32_t last = 0, hlo = 0, hhi = 0;
+            uint32_t last = 0;
+            uint32_t hw[NB];
+#pragma unroll
+            for (int k = 0; k < NB; ++k) hw[k] = 0u;
 #pragma unroll
             for (uint32_t c = 0; c < 8 * NB; ++c) {  // 16-byte chunks: box c/8, chunk c%8
                 const uint4 v4 = *reinterpret_cast<const uint4*>(tsm + (c >> 3) * p.rows * 128u + swz128(tid, c & 7u));
@@ -415,25 +426,23 @@ __global__ void __launch_bounds__(128) cot_run64_kernel(const __grid_constant__ 
                 for (uint32_t e = 0; e < 4; ++e) {
                     const uint32_t q = c * 4 + e;
                     const uint32_t bit = 1u << (q & 31u);  // compile-time mask: one LOP3 test
-                    const bool use = ((q < 32 ? ulo : uhi) & bit) != 0;
-                    if (use) {
+                    if (uw[q >> 5] & bit) {
                         run = vv[e] == last ? run + 1 : 1;  // first usable: run 0 -> 1
                         last = vv[e];
-                        if (run >= w) {
-                            if (q < 32) hlo |= bit;
-                            else hhi |= bit;
-                        }
+                        if (run >= w) hw[q >> 5] |= bit;
                     }
                 }
             }
-            const uint64_t hits = (static_cast<uint64_t>(hhi) << 32) | hlo;
+            int32_t cs = -1;  // first certain probe
+#pragma unroll
+            for (int k = NB - 1; k >= 0; --k)
+                if (hw[k]) cs = 32 * k + __ffs(hw[k]) - 1;
             int32_t ex = -1;
             uint8_t why = CDX_EXIT_CONTINUE;
             uint32_t fid;
             uint8_t low = 0;
-            if (hits) {  // certainty wins ties with the budget
-                const uint32_t cs = static_cast<uint32_t>(__ffsll(static_cast<long long>(hits)) - 1);
-                ex = static_cast<int32_t>(cs);
+            if (cs >= 0) {  // certainty wins ties with the budget
+                ex = cs;
                 why = CDX_EXIT_CERTAIN;
                 fid = *reinterpret_cast<const uint32_t*>(tsm + (cs >> 5) * p.rows * 128u + swz128(tid, (cs & 31u) >> 2) +
                                                          (cs & 3u) * 4u);
@@ -443,10 +452,10 @@ __global__ void __launch_bounds__(128) cot_run64_kernel(const __grid_constant__ 
                     ex = bstep;
                     why = CDX_EXIT_BUDGET;
                 }
-                low = umask ? 0 : 1;  // every probe up to the end hesitated
-                fid = umask ? last
-                            : *reinterpret_cast<const uint32_t*>(tsm + (end >> 5) * p.rows * 128u +
-                                                                 swz128(tid, (end & 31u) >> 2) + (end & 3u) * 4u);
+                low = any_usable ? 0 : 1;  // every probe up to the end hesitated
+                fid = any_usable ? last
+                                 : *reinterpret_cast<const uint32_t*>(tsm + (end >> 5) * p.rows * 128u +
+                                                                      swz128(tid, (end & 31u) >> 2) + (end & 3u) * 4u);
             }
             p.exit_step[r] = ex;
             p.reason[r] = why;
@@ -580,7 +589,7 @@ extern "C" int cdx_cot_exit(cdx_ctx* ctx, const uint32_t* ids, const uint64_t* h
     // per SM resident; other CTAs on the SM overlap each one's TMA wait (tuned on B200)
     // run64 path (P == 64, a_min == w): 128-request CTAs with a 2-deep ring
     // measured best on B200 (51 us on config B vs 55 us for 64 x 1)
-    const bool run64 = (P == 64 || P == 32) && !ck && amin == cfg->window;
+    const bool run64 = P % 32 == 0 && P <= 128 && !ck && amin == cfg->window;
     uint32_t rows = run64 ? 128 : 64, stages = run64 ? 2 : 1;
     if (const char* e = getenv("CDX_COT_ROWS")) rows = static_cast<uint32_t>(atoi(e));
     if (const char* e = getenv("CDX_COT_STAGES")) stages = static_cast<uint32_t>(atoi(e));
@@ -605,8 +614,9 @@ extern "C" int cdx_cot_exit(cdx_ctx* ctx, const uint32_t* ids, const uint64_t* h
     const bool want_ck = ck != nullptr;
     const char* impl = getenv("CDX_COT_IMPL");
     if (!want_ck && amin == cfg->window && !(impl && impl[0] == 'w')) {
-        if (tma && (P == 64 || P == 32) && !(impl && impl[0] == 'r')) {
-            auto k = P == 64 ? cot_run64_kernel<2> : cot_run64_kernel<1>;
+        if (tma && P % 32 == 0 && P <= 128 && !(impl && impl[0] == 'r')) {
+            auto k = P == 64 ? cot_run64_kernel<2>
+                             : (P == 32 ? cot_run64_kernel<1> : (P == 96 ? cot_run64_kernel<3> : cot_run64_kernel<4>));
             cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
             int per_sm = 0;
             cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, p.rows, smem);

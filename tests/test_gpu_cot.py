@@ -116,7 +116,7 @@ def test_cot_exhaustive_len8(ctx, w):
             _check(got, ref)
 
 
-@pytest.mark.parametrize("R,P", [(1000, 32), (129, 32), (1000, 64), (3, 64)])
+@pytest.mark.parametrize("R,P", [(1000, 32), (129, 32), (1000, 64), (3, 64), (500, 96), (700, 128), (65, 128)])
 @pytest.mark.parametrize("w,tau,max_tokens", [(3, 0.9, 4096), (1, 1.0, 640), (5, 1.0, 10 ** 6), (2, 0.5, 64)])
 def test_cot_run_kernel_parity_no_ck(ctx, R, P, w, tau, max_tokens):
     """The branch-free run kernel (P = 32 or 64, a_min == w, no C_k output), implicit offsets."""
