@@ -601,8 +601,22 @@ extern "C" int cdx_cot_exit(cdx_ctx* ctx, const uint32_t* ids, const uint64_t* h
         p.rows = rows;
         p.stage_bytes = rows * p.boxes * 128u;
         p.stages = stages;
-        tma = encode_tmap_2d(&p.tmap, ids, P, R, static_cast<uint64_t>(P) * 4u, 32, rows,
-                             CU_TENSOR_MAP_DATA_TYPE_UINT32, CU_TENSOR_MAP_SWIZZLE_128B);
+        // the descriptor depends only on (ids, R, P, rows): re-encode only when they change
+        // (a repeated batch then costs one launch of host work; config B's kernel is ~47 us)
+        struct TmapCache {
+            const void* ids = nullptr;
+            uint64_t R = 0;
+            uint32_t P = 0, rows = 0;
+            CUtensorMap map;
+        };
+        static thread_local TmapCache tc;
+        if (tc.ids == ids && tc.R == R && tc.P == P && tc.rows == rows) {
+            p.tmap = tc.map;
+        } else {
+            tma = encode_tmap_2d(&p.tmap, ids, P, R, static_cast<uint64_t>(P) * 4u, 32, rows,
+                                 CU_TENSOR_MAP_DATA_TYPE_UINT32, CU_TENSOR_MAP_SWIZZLE_128B);
+            if (tma) tc = TmapCache{ids, R, P, rows, p.tmap};
+        }
     }
     if (!tma) {
         p.rows = 128;
@@ -617,9 +631,23 @@ extern "C" int cdx_cot_exit(cdx_ctx* ctx, const uint32_t* ids, const uint64_t* h
         if (tma && P % 32 == 0 && P <= 128 && !(impl && impl[0] == 'r')) {
             auto k = P == 64 ? cot_run64_kernel<2>
                              : (P == 32 ? cot_run64_kernel<1> : (P == 96 ? cot_run64_kernel<3> : cot_run64_kernel<4>));
-            cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+            // attribute + occupancy per (kernel, device, shape), not per call
+            struct OccCache {
+                const void* k = nullptr;
+                int dev = -1;
+                uint32_t rows = 0;
+                size_t smem = 0;
+                int per_sm = 0;
+            };
+            static thread_local OccCache oc;
             int per_sm = 0;
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, p.rows, smem);
+            if (oc.k == reinterpret_cast<const void*>(k) && oc.dev == ctx->device && oc.rows == p.rows && oc.smem == smem) {
+                per_sm = oc.per_sm;
+            } else {
+                cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+                cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, p.rows, smem);
+                oc = OccCache{reinterpret_cast<const void*>(k), ctx->device, p.rows, smem, per_sm};
+            }
             const uint64_t grid = std::min<uint64_t>(p.ntiles, static_cast<uint64_t>(ctx->sm_count) * std::max(per_sm, 1));
             k<<<static_cast<unsigned>(grid), p.rows, smem, ctx->stream>>>(p);
             CDX_CHECK_LAUNCH(ctx, "cot_exit(run64)");

@@ -256,9 +256,22 @@ void launch_fast(cdx_ctx* ctx, const CUtensorMap& tmap, const ScParams& p, uint3
                  unsigned long long* counter) {
     const size_t smem = 1024 + static_cast<size_t>(wpc) * (p.stages * std::max(32u * S * 4u, 1024u) + 1024u) + 34 * 8 +
                         FAST_WARPS * SC_MAX_STAGES * 16;
-    cudaFuncSetAttribute(sc_fast_kernel<S>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    // attribute + occupancy once per (device, CTA shape): host work per call stays one launch
+    struct Occ {
+        int dev = -1;
+        uint32_t wpc = 0;
+        size_t smem = 0;
+        int per_sm = 0;
+    };
+    static thread_local Occ oc;
     int per_sm = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sc_fast_kernel<S>, wpc * 32, smem);
+    if (oc.dev == ctx->device && oc.wpc == wpc && oc.smem == smem) {
+        per_sm = oc.per_sm;
+    } else {
+        cudaFuncSetAttribute(sc_fast_kernel<S>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sc_fast_kernel<S>, wpc * 32, smem);
+        oc = Occ{ctx->device, wpc, smem, per_sm};
+    }
     if (per_sm < 1) per_sm = 1;
     const uint64_t want = (p.ngroups + wpc - 1) / wpc;
     const uint64_t grid = std::min<uint64_t>(want, static_cast<uint64_t>(ctx->sm_count) * per_sm);
@@ -284,12 +297,26 @@ bool launch_sc_fast(cdx_ctx* ctx, const ScParams& p0) {
         return false;
     const char* impl = getenv("CDX_SC_IMPL");
     if (impl && std::string(impl) == "match") return false;
+    // the descriptor depends only on (ids, lines, S): re-encode only when they change
+    struct Tmc {
+        const void* ids = nullptr;
+        uint64_t lines = 0;
+        uint32_t S = 0;
+        CUtensorMap map;
+    };
+    static thread_local Tmc tc;
     CUtensorMap tmap;
-    const uint64_t dims[2] = {32, lines};
-    const uint64_t strides[1] = {128};
-    const uint32_t box[2] = {32, S};
-    if (!encode_tmap(&tmap, p0.ids, 2, dims, strides, box, CU_TENSOR_MAP_DATA_TYPE_UINT32, CU_TENSOR_MAP_SWIZZLE_128B))
-        return false;
+    if (tc.ids == p0.ids && tc.lines == lines && tc.S == S) {
+        tmap = tc.map;
+    } else {
+        const uint64_t dims[2] = {32, lines};
+        const uint64_t strides[1] = {128};
+        const uint32_t box[2] = {32, S};
+        if (!encode_tmap(&tmap, p0.ids, 2, dims, strides, box, CU_TENSOR_MAP_DATA_TYPE_UINT32,
+                         CU_TENSOR_MAP_SWIZZLE_128B))
+            return false;
+        tc = Tmc{p0.ids, lines, S, tmap};
+    }
     ScParams p = p0;
     p.ngroups = (rows + 31) / 32;
     if (p.P % 32 != 0 && p.meets) {
