@@ -72,3 +72,36 @@ def test_dropin_matches_reference_on_b200():
     assert len(ours) == len(ref)
     bad = [(r, o) for r, o in zip(ref, ours) if r != o]
     assert not bad, f"{len(bad)} of {len(ref)} lines differ; first: {bad[:3]}"
+
+
+RT_REF = os.path.join(ROOT, "oracle", "_ref", "runtime_ref")
+RT_OURS = os.path.join(ROOT, "oracle", "_ref", "runtime_ours")
+
+
+def _run_plain(exe, timeout=600):
+    if not os.path.exists(exe):
+        pytest.fail(f"{exe} not built (oracle/Makefile, where /root/reference is present)")
+    out = subprocess.run([exe], capture_output=True, text=True, timeout=timeout)
+    assert out.returncode == 0, out.stderr
+    return out.stdout.splitlines()
+
+
+@pytest.mark.gpu
+def test_reference_runtime_unchanged_on_b200():
+    """The reference's own caller, runtime.cpp (ProgramDriver: expand / on_request_complete /
+    update_certaindex / aggregate, generate_workload, replay_trace_lines), compiled unchanged
+    against this repo's metrics/probe headers and linked with libcdxhost.so, drives SC,
+    Rebase, MCTS and CoT programs with every certaindex on the B200: its output equals the
+    all-reference build line for line."""
+    ref = _run_plain(RT_REF)
+    ours = _run_plain(RT_OURS)
+    assert len(ref) > 500 and len(ours) == len(ref)
+    bad = [(r, o) for r, o in zip(ref, ours) if r != o]
+    assert not bad, f"{len(bad)} of {len(ref)} lines differ; first: {bad[:3]}"
+
+
+def test_reference_runtime_fails_loudly_without_device():
+    if _cuda():
+        pytest.skip("a CUDA device is present")
+    lines = _run_plain(RT_OURS)
+    assert any("no usable sm_100 device" in l for l in lines)
