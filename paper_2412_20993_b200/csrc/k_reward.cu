@@ -266,12 +266,13 @@ struct QuadLane {
     uint32_t key[RW_KM], cnt[RW_KM];
 };
 
-template <int K, int BOXES>
+template <int K, int BOXES, bool HALF>
 __device__ __forceinline__ void quad_pass(QuadLane& L, const uint8_t* sr, const uint8_t* si, uint32_t box_bytes,
-                                          uint32_t prow, uint32_t q, bool with_ids) {
+                                          uint32_t prow, uint32_t q, bool with_ids, uint32_t W) {
 #pragma unroll
     for (uint32_t j = 0; j < 2 * BOXES; ++j) {
         const uint32_t b = j >> 1, h = (j ^ prow) & 1u;
+        if (HALF && b * 32u + h * 16u >= W) continue;  // W % 16 == 0: a half box is all in or all out
         const uint32_t off = b * box_bytes + swz128(prow, h * 4u + q);
         const uint4 f = *reinterpret_cast<const uint4*>(sr + off);
         const uint32_t rb[4] = {f.x, f.y, f.z, f.w};
@@ -296,23 +297,24 @@ __device__ __forceinline__ void quad_pass(QuadLane& L, const uint8_t* sr, const 
     }
 }
 
-template <int BOXES>
+template <int BOXES, bool HALF>
 __device__ __forceinline__ void quad_pass_k(int K, QuadLane& L, const uint8_t* sr, const uint8_t* si,
-                                            uint32_t box_bytes, uint32_t prow, uint32_t q, bool with_ids) {
+                                            uint32_t box_bytes, uint32_t prow, uint32_t q, bool with_ids, uint32_t W) {
     switch (K) {  // warp-uniform
-        case 0: quad_pass<0, BOXES>(L, sr, si, box_bytes, prow, q, with_ids); break;
-        case 1: quad_pass<1, BOXES>(L, sr, si, box_bytes, prow, q, with_ids); break;
-        case 2: quad_pass<2, BOXES>(L, sr, si, box_bytes, prow, q, with_ids); break;
-        case 3: quad_pass<3, BOXES>(L, sr, si, box_bytes, prow, q, with_ids); break;
-        case 4: quad_pass<4, BOXES>(L, sr, si, box_bytes, prow, q, with_ids); break;
-        case 5: quad_pass<5, BOXES>(L, sr, si, box_bytes, prow, q, with_ids); break;
-        case 6: quad_pass<6, BOXES>(L, sr, si, box_bytes, prow, q, with_ids); break;
-        case 7: quad_pass<7, BOXES>(L, sr, si, box_bytes, prow, q, with_ids); break;
-        default: quad_pass<8, BOXES>(L, sr, si, box_bytes, prow, q, with_ids); break;
+        case 0: quad_pass<0, BOXES, HALF>(L, sr, si, box_bytes, prow, q, with_ids, W); break;
+        case 1: quad_pass<1, BOXES, HALF>(L, sr, si, box_bytes, prow, q, with_ids, W); break;
+        case 2: quad_pass<2, BOXES, HALF>(L, sr, si, box_bytes, prow, q, with_ids, W); break;
+        case 3: quad_pass<3, BOXES, HALF>(L, sr, si, box_bytes, prow, q, with_ids, W); break;
+        case 4: quad_pass<4, BOXES, HALF>(L, sr, si, box_bytes, prow, q, with_ids, W); break;
+        case 5: quad_pass<5, BOXES, HALF>(L, sr, si, box_bytes, prow, q, with_ids, W); break;
+        case 6: quad_pass<6, BOXES, HALF>(L, sr, si, box_bytes, prow, q, with_ids, W); break;
+        case 7: quad_pass<7, BOXES, HALF>(L, sr, si, box_bytes, prow, q, with_ids, W); break;
+        default: quad_pass<8, BOXES, HALF>(L, sr, si, box_bytes, prow, q, with_ids, W); break;
     }
 }
 
-template <int BOXES>
+// HALF: W % 32 == 16 (the last box is half past W: those nodes are skipped)
+template <int BOXES, bool HALF>
 __global__ void __launch_bounds__(RQ_PROGS * 4) reward_quad_kernel(const __grid_constant__ RwParams p,
                                                                    uint32_t exact_min_bits) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -379,7 +381,7 @@ __global__ void __launch_bounds__(RQ_PROGS * 4) reward_quad_kernel(const __grid_
         const uint8_t* si = sr + stage_bytes;
         const int kw = with_ids ? static_cast<int>(__reduce_max_sync(0xffffffffu, ovf ? 0u : m)) : 0;
         mbar_wait(&bar[stage], phase);
-        quad_pass_k<BOXES>(kw, L, sr, si, box_bytes, prow, q, with_ids);
+        quad_pass_k<BOXES, HALF>(kw, L, sr, si, box_bytes, prow, q, with_ids, W);
         if (with_ids) {
             uint32_t after = 0;
 #pragma unroll
@@ -407,6 +409,8 @@ __global__ void __launch_bounds__(RQ_PROGS * 4) reward_quad_kernel(const __grid_
                 if (need) {
 #pragma unroll
                     for (int i = 0; i < NV; ++i) {
+                        if (HALF && static_cast<uint32_t>(i >> 3) * 32u + static_cast<uint32_t>((i >> 2) & 1) * 16u >= W)
+                            continue;  // node past W (zero-filled by TMA): never a cluster
                         bool in = false;  // unused slots duplicate key 0, so no validity test
 #pragma unroll
                         for (int k = 0; k < RW_KM; ++k) in = in || L.key[k] == iv[i];
@@ -742,7 +746,10 @@ extern "C" int cdx_reward_certaindex(cdx_ctx* ctx, const float* rewards, const u
                                    CU_TENSOR_MAP_SWIZZLE_128B));
     }
     p.tma = tma ? 1 : 0;
-    const bool quad = tma && W % 32 == 0 && W <= 32u * RQ_MAX_BOXES && T <= static_cast<uint32_t>(RQ_MAX_T) &&
+    // W % 32 == 16 above one box (48, 80, 112): the last box runs half empty, still well ahead of
+    // the one-thread kernel; W = 16 is not (half of every box would be wasted)
+    const bool quad = tma && (W % 32 == 0 || (W % 16 == 0 && W > 32)) && W <= 32u * RQ_MAX_BOXES &&
+                      T <= static_cast<uint32_t>(RQ_MAX_T) &&
                       !getenv("CDX_RW_LEGACY");
     bool launched_quad = false;
     if (quad) {
@@ -764,10 +771,14 @@ extern "C" int cdx_reward_certaindex(cdx_ctx* ctx, const float* rewards, const u
             uint32_t exact_min_bits;
             std::memcpy(&exact_min_bits, &exact_min, 4);
             const unsigned grid = static_cast<unsigned>((G + RQ_PROGS - 1) / RQ_PROGS);
-            void (*kern)(RwParams, uint32_t) = p.boxes == 1   ? reward_quad_kernel<1>
-                                               : p.boxes == 2 ? reward_quad_kernel<2>
-                                               : p.boxes == 3 ? reward_quad_kernel<3>
-                                                              : reward_quad_kernel<4>;
+            const bool half = W % 32 != 0;
+            void (*kern)(RwParams, uint32_t) =
+                half ? (p.boxes == 2 ? reward_quad_kernel<2, true>
+                                     : p.boxes == 3 ? reward_quad_kernel<3, true> : reward_quad_kernel<4, true>)
+                     : (p.boxes == 1   ? reward_quad_kernel<1, false>
+                        : p.boxes == 2 ? reward_quad_kernel<2, false>
+                        : p.boxes == 3 ? reward_quad_kernel<3, false>
+                                       : reward_quad_kernel<4, false>);
             cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
             kern<<<grid, RQ_PROGS * 4, smem, ctx->stream>>>(p, exact_min_bits);
             CDX_CHECK_LAUNCH(ctx, "reward_certaindex(quad)");

@@ -43,7 +43,9 @@ H64 = None
 @pytest.mark.parametrize("G,T,W,groups", [(1, 1, 1, 5), (300, 16, 64, 5), (129, 5, 7, 5), (70, 40, 8, 5),
                                           (200, 16, 64, 40), (64, 3, 32, 200), (513, 16, 4, 3),
                                           (100, 100, 64, 5), (40, 256, 32, 7), (65, 70, 128, 5),
-                                          (9, 200, 128, 300)])  # T*W past the shared-memory overflow table
+                                          (9, 200, 128, 300),  # T*W past the shared-memory overflow table
+                                          (300, 16, 48, 5), (500, 12, 16, 5), (200, 9, 80, 12), (100, 7, 112, 40),
+                                          (64, 5, 16, 30)])  # W % 16 == 0: half boxes past W skipped
 def test_reward_parity(ctx, G, T, W, groups):
     global H64
     g = O.gen_params(seed=G + T + W, groups=groups, conv_hi=max(1, T))
