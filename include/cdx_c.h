@@ -176,7 +176,7 @@ int cdx_gen_reward(cdx_ctx* ctx, const cdx_gen_params* g, uint64_t g0, uint64_t 
 int cdx_sc_certaindex(cdx_ctx* ctx, const uint32_t* ids, uint64_t R, uint32_t P, uint32_t S,
                       const cdx_threshold* th, uint32_t n_th, float* hcert, uint32_t* meets_bits);
 
-/* Per-row clusters in first-seen order (the full metrics::Clustering of every row):
+/* Per-row clusters in first-seen order (the full metrics::Clustering of every row), 1 <= S <= 4096:
  * n_clusters u32[rows], leader u32[rows][S] (sample index of the cluster's first answer,
  * first n_clusters entries valid), size u32[rows][S].  metrics.cpp:21-37               */
 int cdx_cluster_rows(cdx_ctx* ctx, const uint32_t* ids, uint64_t rows, uint32_t S,

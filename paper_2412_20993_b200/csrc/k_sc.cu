@@ -442,6 +442,54 @@ struct WideParams {
     double th_cut[MAX_TH];
 };
 
+// One row of S answers clustered by the warp: ordinal k (first-seen order) gets its count in
+// cnt[k] and, when `first` is given, the sample index of its first answer.  Returns m.
+__device__ uint32_t wide_cluster(const uint32_t* __restrict__ src, uint32_t S, uint32_t cap_log2,
+                                 uint32_t* __restrict__ hkey, uint32_t* __restrict__ hord,
+                                 uint32_t* __restrict__ cnt, uint32_t* __restrict__ first, uint32_t lane) {
+    const uint32_t cap = 1u << cap_log2;
+    for (uint32_t i = lane; i < cap; i += 32) hord[i] = 0xffffffffu;  // empty
+    __syncwarp();
+    uint32_t m = 0;
+    for (uint32_t c0 = 0; c0 < S; c0 += 32) {
+        const uint32_t e = c0 + lane;
+        const bool act = e < S;
+        const uint32_t v = act ? __ldg(src + e) : 0u;
+        const uint32_t mm = __match_any_sync(0xffffffffu, v) & __ballot_sync(0xffffffffu, act);
+        const bool lead = act && (mm & ((1u << lane) - 1u)) == 0u;
+        uint32_t slot = (v * 0x9E3779B1u) >> (32 - cap_log2);
+        bool fresh = false;
+        if (lead) {
+            while (true) {
+                if (hord[slot] == 0xffffffffu) {
+                    fresh = true;
+                    break;
+                }
+                if (hkey[slot] == v) break;
+                slot = (slot + 1) & (cap - 1);
+            }
+        }
+        const uint32_t fb = __ballot_sync(0xffffffffu, fresh);
+        for (uint32_t bits = fb; bits; bits &= bits - 1) {  // new values in lane order
+            const uint32_t l = __ffs(bits) - 1;
+            if (lane == l) {
+                uint32_t s2 = slot;
+                while (hord[s2] != 0xffffffffu) s2 = (s2 + 1) & (cap - 1);
+                hkey[s2] = v;
+                hord[s2] = m;
+                cnt[m] = 0;
+                if (first) first[m] = e;
+                slot = s2;
+            }
+            ++m;
+            __syncwarp();
+        }
+        if (lead) cnt[hord[slot]] += __popc(mm);
+        __syncwarp();
+    }
+    return m;
+}
+
 __global__ void __launch_bounds__(SC_WIDE_WARPS * 32) sc_wide_kernel(const __grid_constant__ WideParams p) {
     extern __shared__ __align__(16) uint8_t smem[];
     const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
@@ -451,45 +499,7 @@ __global__ void __launch_bounds__(SC_WIDE_WARPS * 32) sc_wide_kernel(const __gri
     uint32_t* cnt = hord + cap;
     const uint64_t gw = static_cast<uint64_t>(blockIdx.x) * nw + warp, nwarps = static_cast<uint64_t>(gridDim.x) * nw;
     for (uint64_t row = gw; row < p.rows; row += nwarps) {
-        for (uint32_t i = lane; i < cap; i += 32) hord[i] = 0xffffffffu;  // empty
-        __syncwarp();
-        uint32_t m = 0;
-        const uint32_t* src = p.ids + row * p.S;
-        for (uint32_t c0 = 0; c0 < p.S; c0 += 32) {
-            const uint32_t e = c0 + lane;
-            const bool act = e < p.S;
-            const uint32_t v = act ? __ldg(src + e) : 0u;
-            const uint32_t mm = __match_any_sync(0xffffffffu, v) & __ballot_sync(0xffffffffu, act);
-            const bool lead = act && (mm & ((1u << lane) - 1u)) == 0u;
-            uint32_t slot = (v * 0x9E3779B1u) >> (32 - p.cap_log2);
-            bool fresh = false;
-            if (lead) {
-                while (true) {
-                    if (hord[slot] == 0xffffffffu) {
-                        fresh = true;
-                        break;
-                    }
-                    if (hkey[slot] == v) break;
-                    slot = (slot + 1) & (cap - 1);
-                }
-            }
-            const uint32_t fb = __ballot_sync(0xffffffffu, fresh);
-            for (uint32_t bits = fb; bits; bits &= bits - 1) {  // new values in lane order
-                const uint32_t l = __ffs(bits) - 1;
-                if (lane == l) {
-                    uint32_t s2 = slot;
-                    while (hord[s2] != 0xffffffffu) s2 = (s2 + 1) & (cap - 1);
-                    hkey[s2] = v;
-                    hord[s2] = m;
-                    cnt[m] = 0;
-                    slot = s2;
-                }
-                ++m;
-                __syncwarp();
-            }
-            if (lead) cnt[hord[slot]] += __popc(mm);
-            __syncwarp();
-        }
+        const uint32_t m = wide_cluster(p.ids + row * p.S, p.S, p.cap_log2, hkey, hord, cnt, nullptr, lane);
         if (lane == 0) {
             double hc = 1.0;  // one cluster holds every answer: H~ = 1 exactly
             if (m > 1) {
@@ -511,6 +521,29 @@ __global__ void __launch_bounds__(SC_WIDE_WARPS * 32) sc_wide_kernel(const __gri
                 atomicOr(p.meets + r * p.words + (pp >> 5), 1u << (pp & 31u));
             }
         }
+        __syncwarp();
+    }
+}
+
+// cluster_rows for S > 32: the same warp clustering, leaders and sizes in first-seen order
+__global__ void __launch_bounds__(SC_WIDE_WARPS * 32) cluster_rows_wide_kernel(
+    const uint32_t* __restrict__ ids, uint64_t rows, uint32_t S, uint32_t cap_log2, uint32_t* __restrict__ ncl,
+    uint32_t* __restrict__ leader, uint32_t* __restrict__ size) {
+    extern __shared__ __align__(16) uint8_t smem[];
+    const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    const uint32_t cap = 1u << cap_log2;
+    uint32_t* hkey = reinterpret_cast<uint32_t*>(smem) + warp * (2 * cap + 2 * S);
+    uint32_t* hord = hkey + cap;
+    uint32_t* cnt = hord + cap;
+    uint32_t* first = cnt + S;
+    const uint64_t gw = static_cast<uint64_t>(blockIdx.x) * nw + warp, nwarps = static_cast<uint64_t>(gridDim.x) * nw;
+    for (uint64_t row = gw; row < rows; row += nwarps) {
+        const uint32_t m = wide_cluster(ids + row * S, S, cap_log2, hkey, hord, cnt, first, lane);
+        for (uint32_t k = lane; k < m; k += 32) {
+            leader[row * S + k] = first[k];
+            size[row * S + k] = cnt[k];
+        }
+        if (lane == 0) ncl[row] = m;
         __syncwarp();
     }
 }
@@ -660,9 +693,23 @@ int cdx_cluster_rows(cdx_ctx* ctx, const uint32_t* ids, uint64_t rows, uint32_t 
     using namespace cdx;
     if (!ctx) return CDX_EINVAL;
     if (S == 0) return set_error(ctx, CDX_EINVAL, "cluster_exact: empty answer set");
-    if (S > 32) return set_error(ctx, CDX_EINVAL, "cluster_rows: at most 32 answers per row");
+    if (S > SC_WIDE_MAX) return set_error(ctx, CDX_EINVAL, "cluster_rows: at most 4096 answers per row");
     if (!ids || !n_clusters || !leader || !size) return set_error(ctx, CDX_EINVAL, "cluster_rows: null pointer");
     if (rows == 0) return CDX_OK;
+    if (S > 32) {  // a warp per row, shared-memory hash of first-seen ordinals
+        uint32_t cap_log2 = 1;
+        while ((1u << cap_log2) < 2u * S) ++cap_log2;
+        const size_t per_warp = ((2u << cap_log2) + 2u * S) * 4u;
+        const uint32_t wpc = static_cast<uint32_t>(std::max<size_t>(1, std::min<size_t>(SC_WIDE_WARPS, (200u << 10) / per_warp)));
+        const size_t smem = wpc * per_warp;
+        cudaFuncSetAttribute(cluster_rows_wide_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             static_cast<int>(smem));
+        const uint64_t grid = std::min<uint64_t>((rows + wpc - 1) / wpc, static_cast<uint64_t>(ctx->sm_count) * 8);
+        cluster_rows_wide_kernel<<<static_cast<unsigned>(grid), wpc * 32, smem, ctx->stream>>>(
+            ids, rows, S, cap_log2, n_clusters, leader, size);
+        CDX_CHECK_LAUNCH(ctx, "cluster_rows(wide)");
+        return CDX_OK;
+    }
     const uint64_t warps = (rows + (32 / S) - 1) / (32 / S);
     const uint64_t blocks = std::min<uint64_t>((warps + 7) / 8, static_cast<uint64_t>(ctx->sm_count) * 16);
     cluster_rows_kernel<<<static_cast<unsigned>(blocks), 256, 0, ctx->stream>>>(ids, rows, S, n_clusters, leader, size);

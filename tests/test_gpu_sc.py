@@ -270,3 +270,25 @@ def test_graph_replay_of_sc_step(ctx):
             assert np.array_equal(out[k].cpu().numpy(), ref[k].astype(out[k].cpu().numpy().dtype)), k
         assert int(out["scalars"][0]) == ref["n_kept"]
         assert np.array_equal(mt.cpu().numpy().view(np.uint32), om)
+
+
+@pytest.mark.parametrize("rows,S,groups", [(100, 1, 1), (257, 7, 3), (300, 16, 5), (200, 32, 40), (90, 33, 5),
+                                           (64, 100, 70), (5, 4096, 900)])
+def test_cluster_rows_parity(ctx, rows, S, groups):
+    """cdx_cluster_rows (the full metrics::Clustering of every row: cluster count, first-seen
+    leader sample and size per cluster) against the oracle's cluster_exact, S = 1 .. 4096."""
+    import ctypes as C
+    import torch
+    rng = np.random.default_rng(rows + S)
+    ids = rng.integers(0, groups, size=(rows, S)).astype(np.uint32)
+    ncl, lead, size = ctx.cluster_rows(torch.from_numpy(ids.view(np.int32)).cuda())
+    ctx.sync()
+    ncl, lead, size = ncl.cpu().numpy(), lead.cpu().numpy(), size.cpu().numpy()
+    L = O.lib()
+    sz = (C.c_int * S)()
+    ld = (C.c_int * S)()
+    for r in range(rows):
+        row = np.ascontiguousarray(ids[r])
+        m = L.cdxo_cluster_exact_ids(row.ctypes.data_as(C.c_void_p), S, sz, ld)
+        assert ncl[r] == m
+        assert list(lead[r, :m]) == list(ld[:m]) and list(size[r, :m]) == list(sz[:m])
