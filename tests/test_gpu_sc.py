@@ -292,3 +292,39 @@ def test_cluster_rows_parity(ctx, rows, S, groups):
         m = L.cdxo_cluster_exact_ids(row.ctypes.data_as(C.c_void_p), S, sz, ld)
         assert ncl[r] == m
         assert list(lead[r, :m]) == list(ld[:m]) and list(size[r, :m]) == list(sz[:m])
+
+
+@pytest.mark.parametrize("rows,max_m,max_n", [(1, 1, 1), (500, 8, 64), (300, 40, 1000), (64, 5, 5)])
+def test_entropy_from_sizes_parity(ctx, rows, max_m, max_n):
+    """cdx_entropy_from_sizes (explicit clusterings: the facade path of semantic_entropy /
+    certaindex_entropy over many rows, totals implicit or given) against the oracle's FP64
+    fold, bit for bit; invalid rows fail with the reference's messages."""
+    import ctypes as C
+    import torch
+    from paper_2412_20993_b200 import CdxInvalidArgument
+    rng = np.random.default_rng(rows + max_m)
+    m = rng.integers(1, max_m + 1, size=rows).astype(np.uint32)
+    sizes = np.zeros((rows, max_m), np.uint32)
+    for r in range(rows):
+        cuts = np.sort(rng.choice(np.arange(1, max_n), size=min(int(m[r]) - 1, max_n - 1), replace=False)) \
+            if max_n > 1 else np.array([], np.int64)
+        parts = np.diff(np.concatenate([[0], cuts, [rng.integers(max(cuts.max() + 1 if len(cuts) else 1, 1), max_n + 1)]]))
+        m[r] = len(parts)
+        sizes[r, :len(parts)] = parts
+    tot = sizes.sum(axis=1).astype(np.uint32)
+    H, Hc = ctx.entropy_from_sizes(torch.from_numpy(sizes.view(np.int32)).cuda(), torch.from_numpy(m.view(np.int32)).cuda(),
+                                   max_n)
+    ctx.sync()
+    H, Hc = H.cpu().numpy(), Hc.cpu().numpy()
+    L = O.lib()
+    for r in range(rows):
+        k = int(m[r])
+        sz = (C.c_int * k)(*[int(x) for x in sizes[r, :k]])
+        assert H[r] == L.cdxo_semantic_entropy(sz, k, int(tot[r]))
+        assert Hc[r] == L.cdxo_certaindex_entropy(sz, k, int(tot[r]))
+    bad = sizes.copy()
+    bad[0, 0] = 0
+    with pytest.raises(CdxInvalidArgument, match="empty cluster|invalid clustering"):
+        ctx.entropy_from_sizes(torch.from_numpy(bad.view(np.int32)).cuda(), torch.from_numpy(m.view(np.int32)).cuda(),
+                               max_n)
+        ctx.sync()
