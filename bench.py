@@ -459,14 +459,16 @@ def bench_sc(args, cfg, rank, world, cx, with_e2e=True):
                kernel="sc_certaindex", kernel_ms=per["sc_certaindex"], kernel_bytes=k2_bytes,
                step_bytes=k2_bytes + k5_bytes, extra={"allocate_scan_ms": per["allocate_scan"],
                                                       "allocate_scan_bytes": k5_bytes})
-    res["e2e"] = e2e_sc(args, cfg, cx, ids, ths, pol) if (with_e2e and not args.no_e2e) else None
+    res["e2e"] = e2e_sc(args, cfg, cx, ids, ths, pol, world) if (with_e2e and not args.no_e2e) else None
     del ids
     return res
 
 
-def e2e_sc(args, cfg, cx, ids_dev, ths, pol):
+def e2e_sc(args, cfg, cx, ids_dev, ths, pol, world=1):
     """The same step through the C-ABI host entry cdx_sc_decide_host: ids from pinned host
-    memory, H2D + K2 + K5 + D2H of every decision inside the timed region."""
+    memory, H2D + K2 + K5 + D2H of every decision inside the timed region.  At N > 1 every
+    rank streams its own shard from its own pinned buffers; barrier on both sides, the
+    slowest rank's time, whole-job throughput."""
     import ctypes as C
 
     import torch
@@ -488,12 +490,14 @@ def e2e_sc(args, cfg, cx, ids_dev, ths, pol):
     for _ in range(max(1, args.warmup)):
         one()
     steps = max(1, min(args.steps, 5))
+    barrier(world)
     t0 = time.perf_counter()
     for _ in range(steps):
         one()
-    dt = (time.perf_counter() - t0) / steps
-    return {"value": R * P * S / dt, "unit": UNIT, "h2d_bytes_per_step": R * P * S * 4,
-            "d2h_bytes_per_step": R * (4 + 1 + 8) + 16, "ms_per_step": dt * 1e3,
+    dt = max_over_ranks((time.perf_counter() - t0) / steps, world)
+    barrier(world)
+    return {"value": R * P * S * world / dt, "unit": UNIT, "h2d_bytes_per_step": R * P * S * 4 * world,
+            "d2h_bytes_per_step": (R * (4 + 1 + 8) + 16) * world, "ms_per_step": dt * 1e3,
             "api": "cdx_sc_decide_host (C-ABI, pinned host buffers, wall clock)"}
 
 
