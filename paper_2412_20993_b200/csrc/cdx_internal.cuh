@@ -11,6 +11,19 @@
 
 #include "../../include/cdx_c.h"
 
+// NVTX ranges (header-only NVTX v3): every C-ABI entry that launches work opens a named
+// range, so ncu --nvtx / nsys timelines group kernels by the reference function they replace.
+#include <nvtx3/nvToolsExt.h>
+namespace cdx {
+struct NvtxRange {
+    explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+    NvtxRange(const NvtxRange&) = delete;
+    NvtxRange& operator=(const NvtxRange&) = delete;
+};
+}  // namespace cdx
+#define CDX_NVTX(name) ::cdx::NvtxRange cdx_nvtx_range_(name)
+
 #define CDX_SMS 148
 
 struct cdx_ctx {

@@ -131,6 +131,7 @@ unsigned grid_of(const cdx_ctx* ctx, uint64_t n, unsigned t) {
 extern "C" int cdx_sc_aggregate(cdx_ctx* ctx, const uint32_t* ids, uint64_t R, uint32_t P, uint32_t S,
                                 const int32_t* exit_knob, uint32_t* answer) {
     using namespace cdx;
+    CDX_NVTX("cdx_sc_aggregate");
     if (!ctx) return CDX_EINVAL;
     if (P == 0 || S == 0) return set_error(ctx, CDX_ERUNTIME, "aggregate: empty program");  // runtime.cpp:347
     if (R == 0) return CDX_OK;
@@ -144,6 +145,7 @@ extern "C" int cdx_reward_aggregate(cdx_ctx* ctx, const float* rewards, const ui
                                     uint64_t G, uint32_t T, uint32_t W, const int32_t* exit_step, uint32_t* answer,
                                     uint64_t* inexact) {
     using namespace cdx;
+    CDX_NVTX("cdx_reward_aggregate");
     if (!ctx) return CDX_EINVAL;
     if (T == 0 || W == 0) return set_error(ctx, CDX_ERUNTIME, "aggregate: empty program");
     if (W > static_cast<uint32_t>(AG_MAX_W)) return set_error(ctx, CDX_EINVAL, "reward_aggregate: width above 256");

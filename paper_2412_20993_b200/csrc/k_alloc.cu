@@ -295,6 +295,7 @@ extern "C" int cdx_allocate_scan(cdx_ctx* ctx, const uint32_t* meets_bits, uint6
                                  uint32_t* kept, uint64_t* n_kept, int64_t* tokens_saved,
                                  int64_t* total_budget) {
     using namespace cdx;
+    CDX_NVTX("cdx_allocate_scan");
     if (!ctx) return CDX_EINVAL;
     if (!pol) return set_error(ctx, CDX_EINVAL, "allocate: null policy");
     if (P == 0 || P > 32 * AL_MAX_WORDS) return set_error(ctx, CDX_EINVAL, "allocate: probes must be 1..4096");

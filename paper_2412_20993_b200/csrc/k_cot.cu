@@ -534,6 +534,7 @@ extern "C" int cdx_cot_exit(cdx_ctx* ctx, const uint32_t* ids, const uint64_t* h
                             uint64_t R, uint32_t P, const cdx_probe_cfg* cfg, int32_t* exit_step,
                             uint8_t* reason, uint32_t* final_id, uint8_t* low_conf, float* ck) {
     using namespace cdx;
+    CDX_NVTX("cdx_cot_exit");
     if (!ctx) return CDX_EINVAL;
     if (!cfg) return set_error(ctx, CDX_EINVAL, "probe: null config");
     // ProbeConfig::validate, probe.cpp:19-25

@@ -135,6 +135,7 @@ int check_eps(cdx_ctx* ctx, int32_t k, double epsilon) {  // theory.cpp:118-119
 extern "C" int cdx_cot_eps_stop(cdx_ctx* ctx, const uint32_t* ids, const uint64_t* hes, uint64_t R, uint32_t P,
                                 int32_t k, double epsilon, int32_t* eps_step, uint8_t* state) {
     using namespace cdx;
+    CDX_NVTX("cdx_cot_eps_stop");
     if (!ctx) return CDX_EINVAL;
     if (int st = check_eps(ctx, k, epsilon)) return st;
     if (P == 0 || P > static_cast<uint32_t>(EPS_MAX_P))

@@ -990,6 +990,7 @@ int gang_priority_run(cdx_ctx* ctx, const cdx_prog_soa* progs, uint64_t N, const
 extern "C" int cdx_gang_priority(cdx_ctx* ctx, const cdx_prog_soa* progs, uint64_t N, const cdx_inter_policy* pol,
                                  double now, uint32_t* order, uint64_t* n_out, uint8_t* escalated, uint64_t* keys) {
     using namespace cdx;
+    CDX_NVTX("cdx_gang_priority");
     if (!ctx) return CDX_EINVAL;
     if (!progs || !pol || !order || !n_out) return set_error(ctx, CDX_EINVAL, "gang_priority: null pointer");
     if (!(pol->starvation_limit > 0.0))
@@ -1013,6 +1014,7 @@ extern "C" int cdx_gang_priority(cdx_ctx* ctx, const cdx_prog_soa* progs, uint64
 extern "C" int cdx_gang_merge(cdx_ctx* ctx, const uint64_t* keys, const uint64_t* run_len, uint32_t runs,
                               uint64_t stride, uint32_t* order_out, uint64_t* total) {
     using namespace cdx;
+    CDX_NVTX("cdx_gang_merge");
     if (!ctx) return CDX_EINVAL;
     if (!keys || !run_len || !order_out || runs == 0) return set_error(ctx, CDX_EINVAL, "gang_merge: bad args");
     if (stride == 0) return CDX_OK;

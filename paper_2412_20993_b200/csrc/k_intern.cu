@@ -206,6 +206,7 @@ extern "C" int cdx_canon_intern(cdx_ctx* ctx, const char* bytes, const uint64_t*
                                 const char* const* markers, uint32_t n_markers, uint32_t* ids, uint8_t* hes,
                                 uint64_t* first_index, uint64_t* n_unique) {
     using namespace cdx;
+    CDX_NVTX("cdx_canon_intern");
     if (!ctx) return CDX_EINVAL;
     if (!offsets || !ids || !n_unique) return set_error(ctx, CDX_EINVAL, "canon_intern: null pointer");
     if (n >= 0xffffffffull) return set_error(ctx, CDX_EINVAL, "canon_intern: at most 2^32-2 answers per call");

@@ -942,6 +942,7 @@ extern "C" int cdx_jsonl_parse(cdx_ctx* ctx, const char* text, uint64_t nbytes, 
                                char* program_arena, uint64_t* program_first, uint64_t* n_records,
                                uint64_t* n_programs) {
     using namespace cdx;
+    CDX_NVTX("cdx_jsonl_parse");
     if (!ctx) return CDX_EINVAL;
     if (!n_records || !n_programs) return set_error(ctx, CDX_EINVAL, "jsonl_parse: null pointer");
     *n_records = 0;

@@ -665,6 +665,7 @@ extern "C" int cdx_reward_certaindex(cdx_ctx* ctx, const float* rewards, const u
                                      uint32_t n_th_mean, const cdx_threshold* th_max, uint32_t n_th_max, float* R,
                                      float* H, uint32_t* meets_bits) {
     using namespace cdx;
+    CDX_NVTX("cdx_reward_certaindex");
     if (!ctx) return CDX_EINVAL;
     if (!rewards || !agg) return set_error(ctx, CDX_EINVAL, "reward_certaindex: null pointer");
     if (T == 0 || W == 0) return set_error(ctx, CDX_EINVAL, "certaindex_reward: empty reward set");

@@ -597,6 +597,7 @@ extern "C" {
 int cdx_sc_certaindex(cdx_ctx* ctx, const uint32_t* ids, uint64_t R, uint32_t P, uint32_t S,
                       const cdx_threshold* th, uint32_t n_th, float* hcert, uint32_t* meets_bits) {
     using namespace cdx;
+    CDX_NVTX("cdx_sc_certaindex");
     if (!ctx) return CDX_EINVAL;
     if (S == 0) return set_error(ctx, CDX_EINVAL, "cluster_exact: empty answer set");
     if (S > SC_WIDE_MAX) return set_error(ctx, CDX_EINVAL, "sc_certaindex: at most 4096 samples per row");
@@ -691,6 +692,7 @@ int cdx_sc_certaindex(cdx_ctx* ctx, const uint32_t* ids, uint64_t R, uint32_t P,
 int cdx_cluster_rows(cdx_ctx* ctx, const uint32_t* ids, uint64_t rows, uint32_t S, uint32_t* n_clusters,
                      uint32_t* leader, uint32_t* size) {
     using namespace cdx;
+    CDX_NVTX("cdx_cluster_rows");
     if (!ctx) return CDX_EINVAL;
     if (S == 0) return set_error(ctx, CDX_EINVAL, "cluster_exact: empty answer set");
     if (S > SC_WIDE_MAX) return set_error(ctx, CDX_EINVAL, "cluster_rows: at most 4096 answers per row");
@@ -721,6 +723,7 @@ int cdx_entropy_from_sizes(cdx_ctx* ctx, const uint32_t* sizes, const uint32_t* 
                            uint64_t rows,
                            uint32_t max_m, uint32_t max_n, double* H, double* Hcert) {
     using namespace cdx;
+    CDX_NVTX("cdx_entropy_from_sizes");
     if (!ctx) return CDX_EINVAL;
     if (!sizes || !m || max_m == 0) return set_error(ctx, CDX_EINVAL, "semantic_entropy: invalid clustering");
     if (max_n == 0 || max_n > 2048) return set_error(ctx, CDX_EINVAL, "entropy_from_sizes: max_n must be 1..2048 (use cdx_entropy_one above)");
