@@ -137,11 +137,7 @@ __device__ __forceinline__ void sc_group(const ScParams& p, const uint32_t* __re
         if (!__any_sync(0xffffffffu, more)) {
             bool meets = false;
             if (lane < rows) {
-                meets = true;
-                for (int t = 0; t < p.n_th; ++t) {
-                    const bool ok = p.th_dir[t] == CDX_DIR_GE ? hc >= p.th_cut[t] : hc <= p.th_cut[t];
-                    meets = meets && ok;
-                }
+                meets = sc_meets(p, hc);
                 if (p.hcert) p.hcert[req * p.P + row0 + lane] = static_cast<float>(hc);
             }
             const uint32_t mw = __ballot_sync(0xffffffffu, meets);
@@ -658,9 +654,15 @@ int cdx_sc_certaindex(cdx_ctx* ctx, const uint32_t* ids, uint64_t R, uint32_t P,
     p.stages = std::max<uint32_t>(1, std::min<uint32_t>(SC_MAX_STAGES, stages));
     wpc = std::max<uint32_t>(1, std::min<uint32_t>(SC_MAX_WARPS, wpc));
     p.n_th = static_cast<int>(n_th);
+    p.box_lo = -HUGE_VAL;
+    p.box_hi = HUGE_VAL;
+    p.box_never = 0;
     for (uint32_t i = 0; i < n_th; ++i) {
         p.th_dir[i] = th[i].dir;
         p.th_cut[i] = th[i].cutoff;
+        if (std::isnan(th[i].cutoff)) p.box_never = 1;
+        else if (th[i].dir == CDX_DIR_GE) p.box_lo = std::max(p.box_lo, th[i].cutoff);
+        else p.box_hi = std::min(p.box_hi, th[i].cutoff);
     }
     p.term[0] = 0.0;
     for (uint32_t c = 1; c <= S; ++c) p.term[c] = host_term(c, S);

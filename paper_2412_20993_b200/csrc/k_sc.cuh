@@ -25,7 +25,17 @@ struct ScParams {
     double term[33];
     double logn;
     const double* comp;  // S <= 16: H~ of every first-seen size composition (null: fold)
+    // the AND of the inclusive thresholds on the one signal as a closed interval
+    // (metrics.cpp:159-171): lo = max of the >= cutoffs, hi = min of the <= cutoffs;
+    // box_never: a NaN cutoff (every compare false)
+    double box_lo, box_hi;
+    int box_never;
 };
+
+// meets for an SC certaindex value (finite, in [0, 1]): the interval form of the AND
+__device__ __forceinline__ bool sc_meets(const ScParams& p, double hc) {
+    return p.n_th == 0 || (!p.box_never && hc >= p.box_lo && hc <= p.box_hi);
+}
 
 // The TMA fast path (S in {4,8,16,32}, P % 32 == 0, 16B-aligned ids).  Returns true when
 // it launched; false when the shape needs the generic warp-match kernel.

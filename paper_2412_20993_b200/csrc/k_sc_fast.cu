@@ -223,11 +223,7 @@ __global__ void __launch_bounds__(FAST_WARPS * 32) sc_fast_kernel(const __grid_c
         if (use_match || __any_sync(0xffffffffu, more)) hc = match_rows<S>(buf, cntw, term, lane, p.logn);
         __syncwarp();  // every lane is done with this stage (and with cntw)
         if (lane == 0) claim_issue(stage);
-        bool meets = true;
-        for (int t = 0; t < p.n_th; ++t) {
-            const bool ok = p.th_dir[t] == CDX_DIR_GE ? hc >= p.th_cut[t] : hc <= p.th_cut[t];
-            meets = meets && ok;
-        }
+        const bool meets = sc_meets(p, hc);
         const uint64_t row = G * 32u + lane;  // flat row r * P + p
         if (p.P % 32u == 0) {  // a group is 32 probes of one request: one meets word
             if (p.hcert) p.hcert[row] = static_cast<float>(hc);
