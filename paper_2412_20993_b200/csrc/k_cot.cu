@@ -12,7 +12,7 @@
 // the device decision is an integer compare); budget_step = first probe whose token offset
 // reaches max_tokens.  Equivalence to the prefix replay is property-tested (tests/).
 //
-// Data path: ids u32[R][P] are staged by TMA (2-D tensor map, 128-byte swizzle, 3-stage
+// Data path: ids u32[R][P] are staged by TMA (2-D tensor map, 128-byte swizzle, multi-stage
 // mbarrier ring) so that each thread reads its own 256-byte row as 16-byte chunks without
 // shared-memory bank conflicts (chunk c of row r sits at chunk c ^ (r & 7)).
 #include <algorithm>
@@ -357,13 +357,13 @@ __global__ void __launch_bounds__(128) cot_run_kernel(const __grid_constant__ Co
     }
 }
 
-// Branch-free variant of the run-length rule for P == 64 probes with implicit token offsets
-// (config B's shape): the budget step and the hesitation bits fold into one 64-bit usable
-// mask up front; the 64 probes are then walked fully unrolled with selects only (no early
-// exit, no data-dependent branches) and every probe whose run reaches w sets a bit in a
-// 64-bit hit mask, so the certain step is the mask's lowest bit.  Same decisions as
-// cot_run_kernel (and therefore as the reference's prefix replay).
-// NB = P / 32 boxes (P = 32, 64 = config B, 96, 128); the usable / hit masks are NB words.
+// Branch-free variant of the run-length rule for P = 32 * NB probes (NB = 1..4; config B is
+// P = 64): the budget step (implicit, or per request from cot_budget_steps) and the
+// hesitation bits fold into a usable mask of P bits up front; the probes are then walked
+// fully unrolled with selects only (no early exit, no data-dependent branches) and every
+// probe whose run reaches w sets a bit in a P-bit hit mask, so the certain step is the
+// mask's lowest bit.  Same decisions as cot_run_kernel (and therefore as the reference's
+// prefix replay).
 template <int NB>
 __global__ void __launch_bounds__(128) cot_run64_kernel(const __grid_constant__ CotParams p) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -588,7 +588,7 @@ extern "C" int cdx_cot_exit(cdx_ctx* ctx, const uint32_t* ids, const uint64_t* h
     bool tma = (P % 4 == 0) && (reinterpret_cast<uintptr_t>(ids) % 16 == 0) && P <= 512 && R <= 0x7fffffffull;
     // rows (= threads) per CTA and ring depth: small single-stage CTAs keep ~28 warps
     // per SM resident; other CTAs on the SM overlap each one's TMA wait (tuned on B200)
-    // run64 path (P == 64, a_min == w): 128-request CTAs with a 2-deep ring
+    // run path (P a multiple of 32 up to 128, a_min == w, no ck): 128-request CTAs with a 2-deep ring
     // measured best on B200 (51 us on config B vs 55 us for 64 x 1)
     const bool run64 = P % 32 == 0 && P <= 128 && !ck && amin == cfg->window;
     uint32_t rows = run64 ? 128 : 64, stages = run64 ? 2 : 1;

@@ -236,7 +236,7 @@ __global__ void __launch_bounds__(RW_PROGS) reward_kernel(const __grid_constant_
 }
 
 // ---------------------------------------------------------------------------------------
-// Quad kernel (W % 32 == 0, W <= 128, T <= 64): FOUR lanes per program, 32 programs per CTA.
+// Quad kernel (W in {32, 48, 64, ..., 128}, T <= 256): FOUR lanes per program, 32 programs per CTA.
 //
 // Per step every lane takes W/4 of the program's nodes straight from the TMA-staged,
 // 128B-swizzled step slice (the half of a box a lane reads alternates with the program's
