@@ -516,13 +516,18 @@ __global__ void __launch_bounds__(128) parse_lines(const char* __restrict__ t, u
         uint32_t slen;
         bool sesc;
         while (ok) {
-            while (p < e && jws(t[p])) ++p;
+            char c = 0;  // the next non-whitespace byte (0 at the line end): read once per token
+            while (p < e) {
+                c = t[p];
+                if (!jws(c)) break;
+                ++p;
+            }
+            if (p >= e) c = 0;
             if (state == 0) {
                 if (p >= e) {
                     ok = false;
                     break;
                 }
-                const char c = t[p];
                 const uint64_t vb = p;
                 const bool field = depth == 1 && top_obj && pending_key >= 0;
                 if (c == '{' || c == '[') {
@@ -595,7 +600,6 @@ __global__ void __launch_bounds__(128) parse_lines(const char* __restrict__ t, u
                     ok = false;
                     break;
                 }
-                const char c = t[p];
                 if (c == ',') {
                     ++p;
                     state = in_obj ? 3 : 0;
@@ -614,14 +618,14 @@ __global__ void __launch_bounds__(128) parse_lines(const char* __restrict__ t, u
                 ok = false;
                 break;
             }
-            if (state == 2 && t[p] == '}') {
+            if (state == 2 && c == '}') {
                 ++p;
                 --depth;
                 state = 1;
                 if (depth == 0) break;
                 continue;
             }
-            if (t[p] != '"') {
+            if (c != '"') {
                 ok = false;
                 break;
             }
