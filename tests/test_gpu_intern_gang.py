@@ -141,6 +141,20 @@ def test_gang_degenerate_keys(ctx, case):
     assert np.array_equal(got.cpu().numpy().view(np.uint32), ref)
 
 
+@pytest.mark.parametrize("N", [5000, 300000])
+def test_gang_range_radix_option(ctx, N, monkeypatch):
+    """CDX_RADIX=ranges (reduce-then-scan range passes instead of onesweep look-back) on the
+    host-driven full sort: the documented alternative must give the same order."""
+    from paper_2412_20993_b200 import InterPolicy
+    monkeypatch.setenv("CDX_GANG_MODE", "full")
+    monkeypatch.setenv("CDX_RADIX", "ranges")
+    soa, now = _gang_inputs(N, 91, sorted_arrival=False)
+    got, _, _ = ctx.gang_priority(_to_dev(soa), InterPolicy(order=1, starvation_limit=0.5, prior_tokens=128.0), now)
+    ctx.sync()
+    ref, _ = O.gang_order(soa, 1, 0.5, 128.0, now)
+    assert np.array_equal(got.cpu().numpy().view(np.uint32), ref)
+
+
 @pytest.mark.parametrize("mode", ["full", "checked"])
 @pytest.mark.parametrize("N,sorted_arrival", [(5000, True), (300000, True), (70000, False)])
 def test_gang_pinned_modes(ctx, N, sorted_arrival, mode, monkeypatch):
