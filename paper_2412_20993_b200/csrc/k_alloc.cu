@@ -129,6 +129,11 @@ __global__ void __launch_bounds__(AL_THREADS) allocate_scan_kernel(const __grid_
 #pragma unroll
     for (int i = 0; i < AL_ITEMS; ++i) {
         const uint64_t r = base + static_cast<uint64_t>(i) * AL_THREADS + tid;
+        if (base + static_cast<uint64_t>(i) * AL_THREADS >= p.R) {  // whole item row past R (CTA-uniform)
+            pk[i] = 0;
+            if (lane == 31) s_we[i * AL_WARPS + warp] = 0;
+            continue;
+        }
         uint32_t e = 0;
         if (r < p.R) {
             e = static_cast<uint32_t>(p.cap);
@@ -258,6 +263,7 @@ __global__ void __launch_bounds__(AL_THREADS) allocate_scan_kernel(const __grid_
     const uint32_t kbase = s_excl_k;
 #pragma unroll
     for (int i = 0; i < AL_ITEMS; ++i) {
+        if (base + static_cast<uint64_t>(i) * AL_THREADS >= p.R) break;  // CTA-uniform: rows past R
         const uint64_t r = base + static_cast<uint64_t>(i) * AL_THREADS + tid;
         const uint32_t x = pk[i];
         const uint32_t own = __shfl_up_sync(0xffffffffu, x, 1);  // exclusive = inclusive of lane - 1
