@@ -53,3 +53,35 @@ def test_no_device_memory_growth(ctx):
     torch.cuda.empty_cache()
     free1, _ = torch.cuda.mem_get_info()
     assert free1 >= free0 - (64 << 20), (free0, free1)  # no growth beyond 64 MB of allocator slack
+
+
+def test_streams_own_and_foreign(ctx):
+    """The context's own non-blocking stream (cdx_ctx_use_own_stream) and a foreign torch
+    stream give the same results; work on one stream is ordered before cdx_sync returns."""
+    import torch
+    from paper_2412_20993_b200 import GenParams, Threshold
+    R, P, S = 700, 64, 32
+    ids = ctx.gen_sc(GenParams(seed=5, conv_hi=P), R, P, S)
+    ctx.sync()
+    outs = []
+    for mode in ("own", "foreign"):
+        if mode == "own":
+            assert ctx.lib.cdx_ctx_use_own_stream(ctx.h) == 0
+            h = torch.empty((R, P), dtype=torch.float32, device="cuda")
+            m = torch.empty((R, 2), dtype=torch.int32, device="cuda")
+            import ctypes as C
+            from paper_2412_20993_b200 import c_thresholds
+            arr, n = c_thresholds([Threshold(0, 0.7, 0)])
+            assert ctx.lib.cdx_sc_certaindex(ctx.h, C.c_void_p(ids.data_ptr()), R, P, S, arr, n,
+                                             C.c_void_p(h.data_ptr()), C.c_void_p(m.data_ptr())) == 0
+            assert ctx.lib.cdx_sync(ctx.h) == 0
+        else:
+            s = torch.cuda.Stream()
+            with torch.cuda.stream(s):
+                h, m = ctx.sc_certaindex(ids, [Threshold(0, 0.7, 0)])
+            ctx.sync()
+        outs.append((h.cpu().numpy().copy(), m.cpu().numpy().copy()))
+    assert np.array_equal(outs[0][0].view(np.uint32), outs[1][0].view(np.uint32))
+    assert np.array_equal(outs[0][1], outs[1][1])
+    _, oh32, om = O.sc_certaindex(O.gen_sc(O.gen_params(seed=5, conv_hi=P), R, P, S), [(0, 0.7, 0)])
+    assert np.array_equal(outs[0][0].view(np.uint32), oh32.view(np.uint32))
