@@ -387,6 +387,7 @@ __global__ void __launch_bounds__(RQ_PROGS * 4) reward_quad_kernel(const __grid_
 #pragma unroll
             for (int k = 0; k < RW_KM; ++k) after += static_cast<uint32_t>(k) < m ? L.cnt[k] : 0u;
             const bool miss = after - before < per_lane;
+            uint32_t ins = 0;  // this lane's nodes counted into slots appended this step
             // ---- first-seen insertion.  One scan marks this lane's nodes whose value is in no
             // valid slot (a bit per node, ascending node order); each round the quad takes its
             // earliest marked node (the next cluster in first-seen order), all 4 lanes append
@@ -453,13 +454,12 @@ __global__ void __launch_bounds__(RQ_PROGS * 4) reward_quad_kernel(const __grid_
                             if (static_cast<uint32_t>(k) == m || (m == 0 && k > 0)) L.key[k] = vmin;  // dup key 0
                             if (static_cast<uint32_t>(k) == m) L.cnt[k] = c;
                         }
+                        ins += c;
                         ++m;
                     }
                 }
             }
-            before = 0;
-#pragma unroll
-            for (int k = 0; k < RW_KM; ++k) before += static_cast<uint32_t>(k) < m ? L.cnt[k] : 0u;
+            before = after + ins;  // the valid slots' total: old slots (after) + appended ones
         }
         // ---- quad totals
         double tot = L.psum;
