@@ -13,6 +13,9 @@
 //   always terminate at resource_cap.
 // token budget = granted * tokens_per_unit; kept = requests granted past detect_at.
 #include <algorithm>
+#include <cstdlib>
+
+#include <cooperative_groups.h>
 
 #include "cdx_internal.cuh"
 
@@ -57,6 +60,7 @@ struct AllocParams {
     int64_t tpu;
     int64_t base_offset;
     uint32_t kept_base;
+    int coop;  // cooperative launch: every tile resident, prefixes by grid barrier (no look-back)
     uint32_t chk[AL_MAX_WORDS];  // knob positions (bit p = knob p+1) at which to test
 };
 
@@ -102,9 +106,10 @@ __global__ void __launch_bounds__(AL_THREADS) allocate_scan_kernel(const __grid_
     __shared__ uint32_t s_epoch;
     // a one-tile call (small batches) needs no ticket, no records and no look-back
     const bool single = p.ntiles == 1;
+    const bool coop = p.coop != 0;  // tiles in block order, no tickets, no epochs
     if (tid == 0) {
-        s_tile = single ? 0u : atomicAdd(&p.tickets[0], 1u);
-        s_epoch = single ? 0u : ld_acquire(&p.tickets[2]);  // constant until every tile of this call is done
+        s_tile = (single || coop) ? blockIdx.x : atomicAdd(&p.tickets[0], 1u);
+        s_epoch = (single || coop) ? 0u : ld_acquire(&p.tickets[2]);  // constant until every tile of this call is done
     }
     __syncthreads();
     const uint32_t tile = s_tile;
@@ -172,7 +177,11 @@ __global__ void __launch_bounds__(AL_THREADS) allocate_scan_kernel(const __grid_
             s_tot_e = tot_e;
             s_tot_k = tot_k;
         }
-        if (lane == 0 && !single) {
+        if (lane == 0 && coop) {  // aggregates only: read after the grid barrier, never by flag
+            p.tiles[tile].agg_e = tot_e;
+            p.tiles[tile].agg_k = tot_k;
+        }
+        if (lane == 0 && !single && !coop) {
             AlTile* T = p.tiles;
             const uint32_t ep = (s_epoch & 0x3fffffffu) << 2;
             if (tile == 0) {  // the first tile's aggregate is its inclusive prefix
@@ -196,6 +205,28 @@ __global__ void __launch_bounds__(AL_THREADS) allocate_scan_kernel(const __grid_
         uint64_t ee = 0;
         uint32_t ekk = 0;
         int64_t j = static_cast<int64_t>(tile) - 1;
+        if (coop) {  // every tile's aggregate is written: one grid barrier, then sum the predecessors
+            cooperative_groups::this_grid().sync();
+            uint64_t ve = 0;
+            uint32_t vk = 0;
+            for (uint32_t q = tid; q < tile; q += AL_THREADS) {
+                ve += __ldcg(reinterpret_cast<const unsigned long long*>(&T[q].agg_e));
+                vk += __ldcg(&T[q].agg_k);
+            }
+            ve = warp_sum<uint64_t>(ve);
+            vk = warp_sum<uint32_t>(vk);
+            if (lane == 0) {
+                s_red_e[warp] = ve;
+                s_red_k[warp] = vk;
+            }
+            __syncthreads();
+#pragma unroll
+            for (int w = 0; w < AL_WARPS; ++w) {
+                ee += s_red_e[w];
+                ekk += s_red_k[w];
+            }
+            j = -1;  // skip the look-back
+        }
         while (j >= 0) {  // block-uniform
             const int64_t idx = j - tid;
             uint32_t st = 2;  // before tile 0: an inclusive zero
@@ -237,7 +268,7 @@ __global__ void __launch_bounds__(AL_THREADS) allocate_scan_kernel(const __grid_
         }
         if (tid == 0) {
             const uint32_t tot_e = s_tot_e, tot_k = s_tot_k;
-            if (tile != 0 && !single) {
+            if (tile != 0 && !single && !coop) {
                 AlTile* Tw = p.tiles;
                 Tw[tile].inc_e = ee + tot_e;
                 Tw[tile].inc_k = ekk + tot_k;
@@ -282,7 +313,7 @@ __global__ void __launch_bounds__(AL_THREADS) allocate_scan_kernel(const __grid_
     }
     // every tile has drawn its ticket before any tile finishes: the last one to finish
     // rewinds the counters for the next call (no host-side bookkeeping, no memset launch)
-    if (tid == 0 && !single) {
+    if (tid == 0 && !single && !coop) {
         __threadfence();
         if (atomicAdd(&p.tickets[1], 1u) == p.ntiles - 1) {
             p.tickets[0] = 0;
@@ -366,7 +397,25 @@ extern "C" int cdx_allocate_scan(cdx_ctx* ctx, const uint32_t* meets_bits, uint6
     for (uint32_t w = 0; w < p.words; ++w)
         if (p.chk[w]) p.chk_words = w + 1;
     if (pol->kind == CDX_POL_EVEN) p.meets = nullptr;  // no test points: meets is never read
-    allocate_scan_kernel<<<p.ntiles, AL_THREADS, 0, ctx->stream>>>(p);
+    // every tile resident at once (C: 512 tiles, D: 128): cooperative launch, prefixes after
+    // one grid barrier instead of a look-back chain; larger grids use the ticketed look-back
+    static thread_local int coop_cap = -1, coop_dev = -1;
+    if (coop_dev != ctx->device) {
+        int per_sm = 0, attr = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, allocate_scan_kernel, AL_THREADS, 0);
+        cudaDeviceGetAttribute(&attr, cudaDevAttrCooperativeLaunch, ctx->device);
+        coop_cap = attr ? per_sm * ctx->sm_count : 0;
+        coop_dev = ctx->device;
+    }
+    p.coop = (p.ntiles > 1 && static_cast<int64_t>(p.ntiles) <= coop_cap && !getenv("CDX_ALLOC_LOOKBACK")) ? 1 : 0;
+    if (p.coop) {
+        void* args[] = {&p};
+        const cudaError_t e = cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(allocate_scan_kernel),
+                                                          dim3(p.ntiles), dim3(AL_THREADS), args, 0, ctx->stream);
+        if (e != cudaSuccess) return cuda_fail(ctx, e, "allocate_scan(cooperative)");
+    } else {
+        allocate_scan_kernel<<<p.ntiles, AL_THREADS, 0, ctx->stream>>>(p);
+    }
     CDX_CHECK_LAUNCH(ctx, "allocate_scan");
     return CDX_OK;
 }
