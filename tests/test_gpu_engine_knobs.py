@@ -56,3 +56,28 @@ def test_reward_legacy_knob(ctx, monkeypatch, G, T, W):
     _, R32, Ho = O.reward_certaindex(rw, ids, agg)
     assert np.array_equal(R.cpu().numpy().view(np.uint32), R32.view(np.uint32))
     assert np.array_equal(H.cpu().numpy().view(np.uint32), Ho.view(np.uint32))
+
+
+@pytest.mark.parametrize("lookback", ["1", None])
+@pytest.mark.parametrize("R", [5000, 1 << 20, 5 << 20])  # 5M requests: more tiles than fit at once
+def test_allocate_lookback_and_cooperative(ctx, monkeypatch, lookback, R):
+    """K5's two multi-tile schemes (cooperative grid barrier / ticketed look-back, forced by
+    CDX_ALLOC_LOOKBACK or by a grid too large to be resident) give the oracle's offsets and
+    kept list."""
+    import torch
+    from paper_2412_20993_b200 import AllocPolicy
+    if lookback:
+        monkeypatch.setenv("CDX_ALLOC_LOOKBACK", lookback)
+    P = 64
+    rng = np.random.default_rng(R)
+    om = (rng.random((R, 2)) < 0.3).astype(np.uint32) * rng.integers(1, 1 << 31, size=(R, 2)).astype(np.uint32)
+    meets = torch.from_numpy(om.view(np.int32)).cuda()
+    pol = AllocPolicy(kind=4, detect_at=5, resource_cap=64, recheck_every=3, tokens_per_unit=2048)
+    out = ctx.allocate_scan(meets, R, P, pol, base_offset=11)
+    ctx.sync()
+    ref = O.allocate_scan(om, R, P, 4, 5, 64, 3, 2048, base_offset=11)
+    for k in ("exit_knob", "granted", "offsets"):
+        assert np.array_equal(out[k].cpu().numpy(), ref[k].astype(out[k].cpu().numpy().dtype)), k
+    n_kept, saved, _ = out["scalars"].cpu().numpy().tolist()
+    assert n_kept == ref["n_kept"] and saved == ref["tokens_saved"]
+    assert np.array_equal(out["kept"][:n_kept].cpu().numpy().view(np.uint32), ref["kept"])
