@@ -28,6 +28,8 @@
 #include <string>
 #include <vector>
 
+#include <cooperative_groups.h>
+
 #include "cdx_internal.cuh"
 
 extern "C" int cdx_canon_intern(cdx_ctx* ctx, const char* bytes, const uint64_t* offsets, uint64_t n,
@@ -786,14 +788,16 @@ struct LoadU32 {
 };
 
 template <class Load, typename Out>
+// coop: launched cooperatively with every tile resident; tile aggregates are summed after
+// one grid barrier (no tickets, no look-back chain)
 __global__ void __launch_bounds__(SL_THREADS) scan_lb(Load ld, uint64_t n, Out* __restrict__ out, bool total_slot,
                                                       uint64_t* __restrict__ rec, uint32_t* __restrict__ ticket,
-                                                      uint64_t* __restrict__ total) {
+                                                      uint64_t* __restrict__ total, int coop) {
     __shared__ uint32_t s_tile;
     __shared__ uint64_t s_w[SL_THREADS / 32];
     __shared__ uint64_t s_excl;
     const uint32_t tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
-    if (tid == 0) s_tile = atomicAdd(ticket, 1u);
+    if (tid == 0) s_tile = coop ? blockIdx.x : atomicAdd(ticket, 1u);
     __syncthreads();
     const uint32_t tile = s_tile;
     const uint64_t b = static_cast<uint64_t>(tile) * SL_TILE + static_cast<uint64_t>(tid) * SL_ITEMS;
@@ -818,7 +822,26 @@ __global__ void __launch_bounds__(SL_THREADS) scan_lb(Load ld, uint64_t n, Out* 
         wpre += w < static_cast<int>(warp) ? s_w[w] : 0ull;
         tot += s_w[w];
     }
-    if (warp == 0) {
+    if (coop) {
+        if (tid == 0) rec[tile] = tot;
+        cooperative_groups::this_grid().sync();
+        uint64_t sv = 0;
+        for (uint32_t q = tid; q < tile; q += SL_THREADS) sv += __ldcg(reinterpret_cast<const unsigned long long*>(rec + q));
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) sv += __shfl_xor_sync(0xffffffffu, sv, o);
+        __shared__ uint64_t s_red[SL_THREADS / 32];
+        if (lane == 0) s_red[warp] = sv;
+        __syncthreads();
+        if (tid == 0) {
+            uint64_t ex = 0;
+            for (int w = 0; w < SL_THREADS / 32; ++w) ex += s_red[w];
+            s_excl = ex;
+            if (static_cast<uint64_t>(tile + 1) * SL_TILE >= n) {  // the last tile
+                if (total) *total = ex + tot;
+                if (total_slot) out[n] = static_cast<Out>(ex + tot);
+            }
+        }
+    } else if (warp == 0) {
         if (lane == 0) {
             volatile uint64_t* r = rec + tile;
             __threadfence();
@@ -923,9 +946,26 @@ int scan_excl(cdx_ctx* ctx, Load ld, uint64_t n, Out* out, bool total_slot, uint
         return CDX_OK;
     }
     uint32_t* ticket = reinterpret_cast<uint32_t*>(rec + tiles);
-    cudaMemsetAsync(rec, 0, tiles * 8 + 8, ctx->stream);
-    scan_lb<Load, Out><<<static_cast<unsigned>(tiles), SL_THREADS, 0, ctx->stream>>>(ld, n, out, total_slot, rec,
-                                                                                      ticket, total);
+    static thread_local int cap = -1, cap_dev = -1;
+    if (cap_dev != ctx->device) {
+        int per_sm = 0, attr = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, scan_lb<Load, Out>, SL_THREADS, 0);
+        cudaDeviceGetAttribute(&attr, cudaDevAttrCooperativeLaunch, ctx->device);
+        cap = attr ? per_sm * ctx->sm_count : 0;
+        cap_dev = ctx->device;
+    }
+    int coop = tiles > 1 && static_cast<int64_t>(tiles) <= cap;
+    if (coop) {
+        void* args[] = {&ld, &n, &out, &total_slot, &rec, &ticket, &total, &coop};
+        const cudaError_t e = cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(scan_lb<Load, Out>),
+                                                          dim3(static_cast<unsigned>(tiles)), dim3(SL_THREADS), args, 0,
+                                                          ctx->stream);
+        if (e != cudaSuccess) return cuda_fail(ctx, e, "jsonl(scan, cooperative)");
+    } else {
+        cudaMemsetAsync(rec, 0, tiles * 8 + 8, ctx->stream);
+        scan_lb<Load, Out><<<static_cast<unsigned>(tiles), SL_THREADS, 0, ctx->stream>>>(ld, n, out, total_slot, rec,
+                                                                                          ticket, total, 0);
+    }
     CDX_CHECK_LAUNCH(ctx, "jsonl(scan)");
     return CDX_OK;
 }
