@@ -1,7 +1,7 @@
 #!/bin/bash
 # prof_round.sh <tag>: launch lists (C, B, D, E) + one `ncu --set full` capture per hot kernel
 # + the default bench line, all under gpurun_out/ (summarise with tools/summarize_profiles.py)
-tag=${1:-r1h}
+tag=${1:-r1i}
 mkdir -p gpurun_out
 B="python bench.py --steps 3 --warmup 3 --no-others --no-cpu-baseline --no-e2e"
 M="gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum"
