@@ -20,6 +20,7 @@
 #include <vector>
 
 #include "cdx_internal.cuh"
+#include "k_scan.cuh"
 
 namespace cdx {
 namespace {
@@ -136,64 +137,13 @@ __global__ void intern_verify(const uint8_t* __restrict__ arena, const uint64_t*
 }
 
 // simple three-phase exclusive scan of u32 flags (n < 2^32)
-constexpr int SCAN_T = 512;
-__global__ void scan_blocks(uint32_t* __restrict__ v, uint64_t n, uint32_t* __restrict__ block_sums) {
-    __shared__ uint32_t s[SCAN_T];
-    const uint64_t i = blockIdx.x * static_cast<uint64_t>(SCAN_T) + threadIdx.x;
-    const uint32_t x = i < n ? v[i] : 0u;
-    s[threadIdx.x] = x;
-    __syncthreads();
-    for (int o = 1; o < SCAN_T; o <<= 1) {
-        const uint32_t y = threadIdx.x >= static_cast<unsigned>(o) ? s[threadIdx.x - o] : 0u;
-        __syncthreads();
-        s[threadIdx.x] += y;
-        __syncthreads();
-    }
-    if (i < n) v[i] = s[threadIdx.x] - x;  // exclusive within the block
-    if (threadIdx.x == SCAN_T - 1) block_sums[blockIdx.x] = s[threadIdx.x];
-}
-// exclusive scan of the block sums by one CTA (1024 per round), total -> *total
-__global__ void scan_sums(uint32_t* __restrict__ sums, uint64_t nb, uint32_t* __restrict__ total) {
-    __shared__ uint32_t ws[32];
-    __shared__ uint32_t carry;
-    if (threadIdx.x == 0) carry = 0;
-    __syncthreads();
-    const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    for (uint64_t b = 0; b < nb; b += 1024) {
-        const uint64_t i = b + threadIdx.x;
-        const uint32_t x = i < nb ? sums[i] : 0u;
-        uint32_t inc = x;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
-            if (lane >= static_cast<uint32_t>(o)) inc += y;
-        }
-        if (lane == 31) ws[warp] = inc;
-        __syncthreads();
-        if (warp == 0) {
-            uint32_t w = ws[lane];
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const uint32_t y = __shfl_up_sync(0xffffffffu, w, o);
-                if (lane >= static_cast<uint32_t>(o)) w += y;
-            }
-            ws[lane] = w;
-        }
-        __syncthreads();
-        if (i < nb) sums[i] = carry + (warp ? ws[warp - 1] : 0u) + inc - x;
-        __syncthreads();
-        if (threadIdx.x == 0) carry += ws[31];
-        __syncthreads();
-    }
-    if (threadIdx.x == 0) *total = carry;
-}
-__global__ void intern_finish(uint64_t n, const uint32_t* __restrict__ excl, const uint32_t* __restrict__ sums,
+__global__ void intern_finish(uint64_t n, const uint32_t* __restrict__ excl,
                               const uint32_t* __restrict__ first, const uint32_t* __restrict__ slot_of,
                               uint32_t* __restrict__ ids, unsigned long long* __restrict__ first_index) {
     for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n;
          i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
         const uint32_t rep = first[slot_of[i]];
-        const uint32_t dense = excl[rep] + sums[rep / SCAN_T];
+        const uint32_t dense = excl[rep];  // first occurrences before rep = its dense id
         ids[i] = dense;
         if (rep == i && first_index) first_index[dense] = i;
     }
@@ -228,16 +178,16 @@ extern "C" int cdx_canon_intern(cdx_ctx* ctx, const char* bytes, const uint64_t*
 
     uint64_t cap = 1024;
     while (cap < 2 * n) cap <<= 1;
-    const uint64_t nb = (n + SCAN_T - 1) / SCAN_T;
-    const size_t bytes_need = cap * 8 + cap * 4 + n * 4 * 2 + nb * 4 + 64;
+    const uint64_t nrec = (n + scan::SL_TILE - 1) / scan::SL_TILE + 2;  // scan tile records + ticket
+    const size_t bytes_need = cap * 8 + cap * 4 + n * 4 * 2 + 16 + nrec * 8 + 16;
     uint8_t* s = static_cast<uint8_t*>(scratch(ctx, bytes_need));
     if (!s) return set_error(ctx, CDX_ECUDA, "canon_intern: scratch allocation failed");
     auto* keys = reinterpret_cast<unsigned long long*>(s);
     auto* first = reinterpret_cast<uint32_t*>(s + cap * 8);
     auto* slot_of = first + cap;
     auto* flags = slot_of + n;
-    auto* sums = flags + n;
-    auto* total = sums + nb + 1;
+    auto* rec = reinterpret_cast<uint64_t*>(reinterpret_cast<uintptr_t>(flags + n + 3) & ~static_cast<uintptr_t>(7));
+    auto* total = rec + nrec;
     cudaMemsetAsync(keys, 0, cap * 8, ctx->stream);
     cudaMemsetAsync(first, 0xff, cap * 4, ctx->stream);
     const unsigned grid = static_cast<unsigned>(std::min<uint64_t>((n + 255) / 256, ctx->sm_count * 16ull));
@@ -246,15 +196,13 @@ extern "C" int cdx_canon_intern(cdx_ctx* ctx, const char* bytes, const uint64_t*
     CDX_CHECK_LAUNCH(ctx, "canon_intern(insert)");
     intern_verify<<<grid, 256, 0, ctx->stream>>>(arena, offsets, n, first, slot_of, flags, ctx->d_err);
     CDX_CHECK_LAUNCH(ctx, "canon_intern(verify)");
-    scan_blocks<<<static_cast<unsigned>(nb), SCAN_T, 0, ctx->stream>>>(flags, n, sums);
-    CDX_CHECK_LAUNCH(ctx, "canon_intern(scan)");
-    scan_sums<<<1, 1024, 0, ctx->stream>>>(sums, nb, total);
-    CDX_CHECK_LAUNCH(ctx, "canon_intern(scan sums)");
-    intern_finish<<<grid, 256, 0, ctx->stream>>>(n, flags, sums, first, slot_of, ids,
+    // first-occurrence flags -> exclusive prefix in place = dense first-seen ids
+    if (int st = scan::scan_excl(ctx, scan::LoadU32{flags}, n, flags, false, rec, total)) return st;
+    intern_finish<<<grid, 256, 0, ctx->stream>>>(n, flags, first, slot_of, ids,
                                                   reinterpret_cast<unsigned long long*>(first_index));
     CDX_CHECK_LAUNCH(ctx, "canon_intern(finish)");
-    uint32_t h_total = 0;
-    cudaError_t e = cudaMemcpyAsync(&h_total, total, 4, cudaMemcpyDeviceToHost, ctx->stream);
+    uint64_t h_total = 0;
+    cudaError_t e = cudaMemcpyAsync(&h_total, total, 8, cudaMemcpyDeviceToHost, ctx->stream);
     if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
     if (e != cudaSuccess) return cuda_fail(ctx, e, "canon_intern");
     *n_unique = h_total;
