@@ -87,17 +87,25 @@ __global__ void __launch_bounds__(GP_THREADS) gang_count(const uint8_t* __restri
     }
 }
 
-// exclusive scan of the tile counts in place (one CTA), total -> misc[0]
+// exclusive scan of the tile counts in place (one CTA), total -> misc[0]; 4 counts per thread
+// per pass (uint4 when aligned), so config E's 4096 tile counts take one pass.
 __global__ void __launch_bounds__(1024) gang_scan_tiles(uint32_t* __restrict__ v, uint32_t n, uint32_t* misc) {
     __shared__ uint32_t ws[32];
-    __shared__ uint32_t carry;
-    if (threadIdx.x == 0) carry = 0;
-    __syncthreads();
     const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    for (uint32_t b = 0; b < n; b += 1024) {
-        const uint32_t i = b + threadIdx.x;
-        const uint32_t x = i < n ? v[i] : 0u;
-        uint32_t inc = x;
+    uint32_t carry = 0;
+    for (uint32_t b = 0; b < n; b += 4096) {
+        const uint32_t i = b + 4 * threadIdx.x;
+        uint32_t x[4];
+        const bool vec = i + 4 <= n && (reinterpret_cast<uintptr_t>(v + i) & 15) == 0;
+        if (vec) {
+            const uint4 q = *reinterpret_cast<const uint4*>(v + i);
+            x[0] = q.x; x[1] = q.y; x[2] = q.z; x[3] = q.w;
+        } else {
+#pragma unroll
+            for (int j = 0; j < 4; ++j) x[j] = i + j < n ? v[i + j] : 0u;
+        }
+        const uint32_t t = x[0] + x[1] + x[2] + x[3];
+        uint32_t inc = t;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
             const uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
@@ -115,11 +123,19 @@ __global__ void __launch_bounds__(1024) gang_scan_tiles(uint32_t* __restrict__ v
             ws[lane] = w;  // inclusive over warps
         }
         __syncthreads();
-        const uint32_t before = carry + (warp ? ws[warp - 1] : 0u);
-        if (i < n) v[i] = before + inc - x;
-        __syncthreads();
-        if (threadIdx.x == 0) carry += ws[31];
-        __syncthreads();
+        uint32_t e = carry + (warp ? ws[warp - 1] : 0u) + inc - t;
+        uint32_t o4[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) { o4[j] = e; e += x[j]; }
+        if (vec) {
+            *reinterpret_cast<uint4*>(v + i) = make_uint4(o4[0], o4[1], o4[2], o4[3]);
+        } else {
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+                if (i + j < n) v[i + j] = o4[j];
+        }
+        carry += ws[31];
+        __syncthreads();  // ws reused by the next pass
     }
     if (threadIdx.x == 0) misc[0] = carry;
 }
