@@ -71,10 +71,18 @@ __global__ void __launch_bounds__(GP_THREADS) gang_count(const uint8_t* __restri
     __shared__ uint32_t s[GP_THREADS / 32];
     const uint64_t base = static_cast<uint64_t>(blockIdx.x) * GP_TILE;
     uint32_t c = 0;
+    if (base + GP_TILE <= N && (reinterpret_cast<uintptr_t>(term) & 3) == 0) {
+        // full aligned tile: one word of GP_ITEMS flags per thread, live = zero bytes
+        static_assert(GP_ITEMS == 4, "one u32 per thread");
+        const uint32_t w = __ldg(reinterpret_cast<const uint32_t*>(term + base) + threadIdx.x);
+        const uint32_t nz = (((w & 0x7f7f7f7fu) + 0x7f7f7f7fu) | w) & 0x80808080u;
+        c = 4u - static_cast<uint32_t>(__popc(nz));
+    } else {
 #pragma unroll
-    for (int j = 0; j < GP_ITEMS; ++j) {
-        const uint64_t i = base + static_cast<uint64_t>(j) * GP_THREADS + threadIdx.x;
-        c += (i < N && term[i] == 0) ? 1u : 0u;
+        for (int j = 0; j < GP_ITEMS; ++j) {
+            const uint64_t i = base + static_cast<uint64_t>(j) * GP_THREADS + threadIdx.x;
+            c += (i < N && term[i] == 0) ? 1u : 0u;
+        }
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
@@ -141,7 +149,7 @@ __global__ void __launch_bounds__(1024) gang_scan_tiles(uint32_t* __restrict__ v
 }
 
 // misc: [0] live count (from gang_scan_tiles), [1] arrivals not sorted, [2] bad time/key
-__global__ void __launch_bounds__(GP_THREADS) gang_prepare(const GangParams p, uint64_t* __restrict__ khi,
+__global__ void __launch_bounds__(GP_THREADS, 6) gang_prepare(const GangParams p, uint64_t* __restrict__ khi,
                                                            uint64_t* __restrict__ karr, uint32_t* __restrict__ kid,
                                                            uint32_t* __restrict__ perm,
                                                            const uint32_t* __restrict__ tile_excl,
