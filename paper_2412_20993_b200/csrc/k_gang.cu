@@ -303,11 +303,23 @@ __global__ void __launch_bounds__(RS_THREADS) os_histogram(const uint64_t* __res
     if (n_dev) n = *n_dev;
     for (int i = threadIdx.x; i < 8 * 256; i += RS_THREADS) (&h[0][0])[i] = 0;
     __syncthreads();
-    for (uint64_t i = blockIdx.x * static_cast<uint64_t>(RS_THREADS) + threadIdx.x; i < n;
-         i += static_cast<uint64_t>(gridDim.x) * RS_THREADS) {
-        const uint64_t k = keys[i];
+    // eight keys in flight per thread per round: the loop is load-latency bound, not atomic bound
+    // (warp-aggregating the skewed top digits with MATCH was measured slower: 19 -> 27 us)
+    constexpr uint32_t U = 8;
+    const uint64_t stride = static_cast<uint64_t>(gridDim.x) * RS_THREADS * U;
+    for (uint64_t b = blockIdx.x * static_cast<uint64_t>(RS_THREADS) * U + threadIdx.x; b < n; b += stride) {
+        uint64_t k[U];
 #pragma unroll
-        for (int d = DLO; d < 8; ++d) atomicAdd(&h[d][(k >> (8 * d)) & 0xff], 1u);
+        for (uint32_t u = 0; u < U; ++u) {
+            const uint64_t i = b + u * RS_THREADS;
+            k[u] = i < n ? __ldg(keys + i) : 0ull;
+        }
+#pragma unroll
+        for (uint32_t u = 0; u < U; ++u) {
+            if (b + u * RS_THREADS >= n) break;
+#pragma unroll
+            for (int d = DLO; d < 8; ++d) atomicAdd(&h[d][(k[u] >> (8 * d)) & 0xff], 1u);
+        }
     }
     __syncthreads();
     for (int i = threadIdx.x; i < 8 * 256; i += RS_THREADS) {

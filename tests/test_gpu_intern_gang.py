@@ -93,6 +93,26 @@ def test_gang_parity(ctx, N, order, limit, sorted_arrival):
     assert np.array_equal(got.cpu().numpy().view(np.uint32), ref)
 
 
+@pytest.mark.parametrize("N,off", [(1 << 16, 1), (70001, 3), (4096, 2), (1 << 20, 0)])
+def test_gang_flag_bytes_and_alignment(ctx, N, off):
+    """The live count reads the terminated flags a word at a time when the tile is full and the
+    flags are 4-byte aligned, a byte at a time otherwise: any non-zero byte is terminated
+    (oracle/cdx_oracle.c's `if (terminated[i]) continue`), whatever the pointer's alignment."""
+    import torch
+    from paper_2412_20993_b200 import InterPolicy
+    soa, now = _gang_inputs(N, 900 + off)
+    rng = np.random.default_rng(off)
+    soa["terminated"] = (soa["terminated"] * rng.integers(1, 256, N)).astype(np.uint8)
+    dev = _to_dev(soa)
+    store = torch.zeros(N + 8, dtype=torch.uint8, device="cuda")
+    store[off:off + N] = dev["terminated"]
+    dev["terminated"] = store[off:off + N]
+    got, _, _ = ctx.gang_priority(dev, InterPolicy(order=1, starvation_limit=0.5, prior_tokens=128.0), now)
+    ctx.sync()
+    ref, _ = O.gang_order(soa, 1, 0.5, 128.0, now)
+    assert np.array_equal(got.cpu().numpy().view(np.uint32), ref)
+
+
 @pytest.mark.parametrize("case", ["identical", "all_escalated", "one_digit", "upper_half_ties", "short_runs"])
 def test_gang_degenerate_keys(ctx, case):
     """Keys that agree on most or all radix digits (skipped passes, single-digit sorts,
