@@ -153,7 +153,7 @@ __global__ void __launch_bounds__(GP_THREADS, 6) gang_prepare(const GangParams p
                                                            uint64_t* __restrict__ karr, uint32_t* __restrict__ kid,
                                                            uint32_t* __restrict__ perm,
                                                            const uint32_t* __restrict__ tile_excl,
-                                                           uint32_t* __restrict__ misc) {
+                                                           uint32_t* __restrict__ misc, uint32_t lean) {
     __shared__ uint32_t s_excl;
     __shared__ uint32_t s_cnt[GP_ITEMS * (GP_THREADS / 32)];
     const uint32_t tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
@@ -223,9 +223,13 @@ __global__ void __launch_bounds__(GP_THREADS, 6) gang_prepare(const GangParams p
         const uint64_t i = base + static_cast<uint64_t>(j) * GP_THREADS + tid;
         const uint32_t pos = s_excl + s_cnt[j * (GP_THREADS / 32) + warp] + rank[j];
         khi[pos] = hk[j];
-        karr[pos] = ak[j];
-        kid[pos] = p.id_base + static_cast<uint32_t>(i);
-        perm[pos] = pos;
+        if (lean) {  // the sort carries the program id itself; arrival keys are not needed
+            perm[pos] = p.id_base + static_cast<uint32_t>(i);
+        } else {
+            karr[pos] = ak[j];
+            kid[pos] = p.id_base + static_cast<uint32_t>(i);
+            perm[pos] = pos;
+        }
     }
 }
 
@@ -717,7 +721,7 @@ __global__ void gang_fix_a(const uint64_t* __restrict__ k, const uint32_t* __res
     if (n_dev) n = *n_dev;
     for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n;
          i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
-        order[i] = kid[v[i]];
+        order[i] = kid ? kid[v[i]] : v[i];
         if (i == 0) continue;
         const uint64_t ki = k[i], kp = k[i - 1];
         const uint32_t h = static_cast<uint32_t>(ki >> 32);
@@ -771,7 +775,7 @@ __global__ void gang_fix_b(uint64_t* __restrict__ k, uint32_t* __restrict__ v, c
             k[b] = ka;
             v[b] = va;
         }
-        for (uint64_t a = i; a < e; ++a) order[a] = kid[v[a]];
+        for (uint64_t a = i; a < e; ++a) order[a] = kid ? kid[v[a]] : v[a];
     }
 }
 
@@ -902,7 +906,10 @@ int gang_priority_run(cdx_ctx* ctx, const cdx_prog_soa* progs, uint64_t N, const
     CDX_CHECK_LAUNCH(ctx, "gang_priority(count)");
     gang_scan_tiles<<<1, 1024, 0, ctx->stream>>>(plook, gtiles, misc);
     CDX_CHECK_LAUNCH(ctx, "gang_priority(scan)");
-    gang_prepare<<<gtiles, GP_THREADS, 0, ctx->stream>>>(p, khi, karr, kid, va, plook, misc);
+    // lean: the fast path without key output sorts the ids themselves (no position -> id
+    // gather afterwards, no arrival keys or id table written); any redo re-runs prepare
+    const uint32_t lean = mode == GANG_FAST && !keys ? 1u : 0u;
+    gang_prepare<<<gtiles, GP_THREADS, 0, ctx->stream>>>(p, khi, karr, kid, va, plook, misc, lean);
     CDX_CHECK_LAUNCH(ctx, "gang_priority(prepare)");
     // digit counts of the live hi keys (count read on the device), fetched with the flags
     cudaMemsetAsync(hist, 0, 8 * 256 * 4, ctx->stream);
@@ -923,9 +930,10 @@ int gang_priority_run(cdx_ctx* ctx, const cdx_prog_soa* progs, uint64_t N, const
         uint32_t* fix = hist;  // the digit counts are consumed: reuse for the run list
         const uint32_t list_cap = static_cast<uint32_t>(std::min<uint64_t>(nh - 2, 0xffffffffull));
         cudaMemsetAsync(fix, 0, 8, ctx->stream);
-        gang_fix_a<<<L.grid(N), 256, 0, ctx->stream>>>(khi, va, kid, N, order, fix, list_cap, misc);
+        const uint32_t* vid = lean ? nullptr : kid;  // values are ids already when lean
+        gang_fix_a<<<L.grid(N), 256, 0, ctx->stream>>>(khi, va, vid, N, order, fix, list_cap, misc);
         CDX_CHECK_LAUNCH(ctx, "gang_priority(order)");
-        gang_fix_b<<<ctx->sm_count * 2, 256, 0, ctx->stream>>>(khi, va, kid, N, order, fix, misc);
+        gang_fix_b<<<ctx->sm_count * 2, 256, 0, ctx->stream>>>(khi, va, vid, N, order, fix, misc);
         CDX_CHECK_LAUNCH(ctx, "gang_priority(runs)");
         if (keys) {
             pack_keys<<<L.grid(N), 256, 0, ctx->stream>>>(khi, karr, kid, va, keys, N, misc);
