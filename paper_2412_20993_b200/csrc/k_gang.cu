@@ -66,33 +66,34 @@ __device__ __forceinline__ uint64_t dbits(double x) {
 // non-decreasing (the (arrival, id) pre-sort can then be skipped).
 constexpr int GP_THREADS = 256, GP_ITEMS = 4, GP_TILE = GP_THREADS * GP_ITEMS;
 // live programs per tile (reads only the terminated bytes)
-__global__ void __launch_bounds__(GP_THREADS) gang_count(const uint8_t* __restrict__ term, uint64_t N,
-                                                         uint32_t* __restrict__ tile_cnt) {
-    __shared__ uint32_t s[GP_THREADS / 32];
-    const uint64_t base = static_cast<uint64_t>(blockIdx.x) * GP_TILE;
+// One warp per 1-KB tile of flags (8 tiles per CTA): 32 B per lane as two 16-byte loads when
+// the tile is full and aligned, live = zero bytes; a warp reduction, no shared memory.
+__device__ __forceinline__ uint32_t zero_bytes(uint32_t w) {
+    return 4u - static_cast<uint32_t>(__popc((((w & 0x7f7f7f7fu) + 0x7f7f7f7fu) | w) & 0x80808080u));
+}
+__global__ void __launch_bounds__(256) gang_count(const uint8_t* __restrict__ term, uint64_t N,
+                                                  uint32_t* __restrict__ tile_cnt, uint32_t ntiles) {
+    const uint32_t tile = blockIdx.x * 8u + (threadIdx.x >> 5), lane = threadIdx.x & 31u;
+    if (tile >= ntiles) return;
+    const uint64_t base = static_cast<uint64_t>(tile) * GP_TILE;
     uint32_t c = 0;
-    if (base + GP_TILE <= N && (reinterpret_cast<uintptr_t>(term) & 3) == 0) {
-        // full aligned tile: one word of GP_ITEMS flags per thread, live = zero bytes
-        static_assert(GP_ITEMS == 4, "one u32 per thread");
-        const uint32_t w = __ldg(reinterpret_cast<const uint32_t*>(term + base) + threadIdx.x);
-        const uint32_t nz = (((w & 0x7f7f7f7fu) + 0x7f7f7f7fu) | w) & 0x80808080u;
-        c = 4u - static_cast<uint32_t>(__popc(nz));
-    } else {
+    if (base + GP_TILE <= N && (reinterpret_cast<uintptr_t>(term) & 15) == 0) {
+        static_assert(GP_TILE == 32 * 32, "two uint4 per lane");
+        const uint4* q = reinterpret_cast<const uint4*>(term + base);
 #pragma unroll
-        for (int j = 0; j < GP_ITEMS; ++j) {
-            const uint64_t i = base + static_cast<uint64_t>(j) * GP_THREADS + threadIdx.x;
+        for (int j = 0; j < 2; ++j) {
+            const uint4 w = __ldg(q + lane + 32 * j);
+            c += zero_bytes(w.x) + zero_bytes(w.y) + zero_bytes(w.z) + zero_bytes(w.w);
+        }
+    } else {
+        for (uint32_t j = lane; j < GP_TILE; j += 32) {
+            const uint64_t i = base + j;
             c += (i < N && term[i] == 0) ? 1u : 0u;
         }
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
-    if ((threadIdx.x & 31) == 0) s[threadIdx.x >> 5] = c;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        uint32_t t = 0;
-        for (int w = 0; w < GP_THREADS / 32; ++w) t += s[w];
-        tile_cnt[blockIdx.x] = t;
-    }
+    if (lane == 0) tile_cnt[tile] = c;
 }
 
 // exclusive scan of the tile counts in place (one CTA), total -> misc[0]; 4 counts per thread
@@ -902,7 +903,7 @@ int gang_priority_run(cdx_ctx* ctx, const cdx_prog_soa* progs, uint64_t N, const
     uint32_t* hist = plook + gtiles + 16;
     cudaMemsetAsync(misc, 0, 16 * 4, ctx->stream);
     Launch L{ctx};
-    gang_count<<<gtiles, GP_THREADS, 0, ctx->stream>>>(progs->terminated, N, plook);
+    gang_count<<<(gtiles + 7) / 8, 256, 0, ctx->stream>>>(progs->terminated, N, plook, gtiles);
     CDX_CHECK_LAUNCH(ctx, "gang_priority(count)");
     gang_scan_tiles<<<1, 1024, 0, ctx->stream>>>(plook, gtiles, misc);
     CDX_CHECK_LAUNCH(ctx, "gang_priority(scan)");
