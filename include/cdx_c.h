@@ -199,6 +199,14 @@ int cdx_entropy_from_sizes(cdx_ctx* ctx, const uint32_t* sizes, const uint32_t* 
 int cdx_entropy_one(cdx_ctx* ctx, const uint32_t* sizes, uint32_t m, uint32_t total, double* H,
                     double* Hcert);
 
+/* One explicit Clustering of the scalar façade (metrics::semantic_entropy /
+ * certaindex_entropy, metrics.cpp:107-125) with HOST cluster sizes in cluster order and any
+ * total, a cluster larger than the total included (p > 1, as the reference computes it).
+ * One term (c/total)*log(c/total) per cluster from the host libm, folded on the device in
+ * cluster order.  H, Hcert: DEVICE f64 (nullable).  Errors as the reference, in its order. */
+int cdx_entropy_sizes_host(cdx_ctx* ctx, const int32_t* sizes, uint32_t m, int32_t total, double* H,
+                           double* Hcert);
+
 /* ---- ragged rows behind the scalar C++ API (include/cdx/metrics.hpp, probe.hpp) -------
  * Rows are concatenated records, row r = [row_off[r], row_off[r+1]).  ids are interned
  * answers (K1: equal id <=> equal trimmed bytes), hes u8 hesitation flags, step_index i32
@@ -287,6 +295,15 @@ int cdx_reward_certaindex(cdx_ctx* ctx, const float* rewards, const uint32_t* id
                           const cdx_threshold* th_max, uint32_t n_th_max, float* R, float* H,
                           uint32_t* meets_bits);
 
+/* The same over f64 rewards (RewardSet / PathSample::reward hold doubles, metrics.hpp:74-77):
+ * rewards f64[G][T][W]; every program is folded in the reference's left-fold order (one warp
+ * per program); outputs as above (R, H fp32 stores of the FP64 values the decisions use).   */
+int cdx_reward_certaindex_f64(cdx_ctx* ctx, const double* rewards, const uint32_t* ids,
+                              const uint8_t* agg, uint64_t G, uint32_t T, uint32_t W,
+                              const cdx_threshold* th_mean, uint32_t n_th_mean,
+                              const cdx_threshold* th_max, uint32_t n_th_max, float* R, float* H,
+                              uint32_t* meets_bits);
+
 /* Scalar-façade reward path: RewardSet of f64 values, rows of variable length.
  * values f64 concatenated, row_off u64[rows+1], agg u8[rows]; out f64[rows]. */
 int cdx_reward_sets(cdx_ctx* ctx, const double* values, const uint64_t* row_off,
@@ -369,12 +386,23 @@ int cdx_sc_aggregate(cdx_ctx* ctx, const uint32_t* ids, uint64_t R, uint32_t P, 
 /* MCTS (agg CDX_AGG_MEAN): answer of the first maximum-reward path over steps 0..t.
  * Rebase (agg CDX_AGG_MAX): softmax-weighted plurality (sum of exp(reward) per cluster in
  * path order) over the last full layer, step t.  rewards f32[G][T][W], ids u32[G][T][W],
- * exit_step i32[G] (0-based step t) -> answer u32[G]; W <= 256.  exp() is the host libm's on
- * the 2^-24 grid of [0,1]; *inexact (device u64, required) counts rewards off that grid,
- * whose weights use the device exp (<= 1 ulp from the host's).                           */
+ * exit_step i32[G] (0-based step t) -> answer u32[G]; W <= 256.  exp() is the host libm's
+ * algorithm restated bit for bit on the device (cdx_libm_exp), so weights equal the
+ * reference's for every reward.  A Rebase layer whose weights are all NaN has no winner (the
+ * reference returns an empty string): answer = CDX_NO_ANSWER.  *inexact (device u64,
+ * nullable; ABI v2) is zeroed: no weight is approximated.                                 */
+#define CDX_NO_ANSWER 0xffffffffu
 int cdx_reward_aggregate(cdx_ctx* ctx, const float* rewards, const uint32_t* ids, const uint8_t* agg,
                          uint64_t G, uint32_t T, uint32_t W, const int32_t* exit_step,
                          uint32_t* answer, uint64_t* inexact);
+/* The same over f64 rewards (PathSample::reward and RewardSet hold doubles,
+ * runtime.hpp / metrics.hpp:74-77).                                                        */
+int cdx_reward_aggregate_f64(cdx_ctx* ctx, const double* rewards, const uint32_t* ids, const uint8_t* agg,
+                             uint64_t G, uint32_t T, uint32_t W, const int32_t* exit_step,
+                             uint32_t* answer);
+/* y[i] = std::exp(x[i]) with the host libm's bits (glibc's table-driven exp, FMA build),
+ * evaluated on the device; x, y DEVICE f64[n].  The weight function of the Rebase vote.   */
+int cdx_libm_exp(cdx_ctx* ctx, const double* x, uint64_t n, double* y);
 
 /* ---- end-to-end host entry: SC certaindex + allocate from HOST buffers ---------------
  * Streams ids (host, ideally pinned) through the device in chunks of whole requests,

@@ -531,15 +531,30 @@ int cdxo_reward_certaindex(const float* rewards, const uint32_t* ids, const uint
 
 /* The same with the FP64 certaindex as well (H64, nullable): the value the thresholds are
  * applied to (runtime.cpp:279-292 -> combined_meets_thresholds, metrics.cpp:159-171). */
+static int reward_certaindex_any(const float* rewards, const double* rewards64, const uint32_t* ids,
+                                 const uint8_t* agg, uint64_t G, uint32_t T, uint32_t W, double* R64,
+                                 float* Rout, float* Hout, double* H64);
 int cdxo_reward_certaindex2(const float* rewards, const uint32_t* ids, const uint8_t* agg,
                             uint64_t G, uint32_t T, uint32_t W, double* R64, float* Rout,
                             float* Hout, double* H64) {
+    return reward_certaindex_any(rewards, NULL, ids, agg, G, T, W, R64, Rout, Hout, H64);
+}
+/* f64 rewards (RewardSet holds doubles, metrics.hpp:74-77) */
+int cdxo_reward_certaindex_f64(const double* rewards, const uint32_t* ids, const uint8_t* agg,
+                               uint64_t G, uint32_t T, uint32_t W, double* R64, float* Rout,
+                               float* Hout, double* H64) {
+    return reward_certaindex_any(NULL, rewards, ids, agg, G, T, W, R64, Rout, Hout, H64);
+}
+static int reward_certaindex_any(const float* rewards, const double* rewards64, const uint32_t* ids,
+                                 const uint8_t* agg, uint64_t G, uint32_t T, uint32_t W, double* R64,
+                                 float* Rout, float* Hout, double* H64) {
     const size_t n_all = (size_t)T * W;
     int* sizes = (int*)malloc(sizeof(int) * (n_all ? n_all : 1));
     int* leaders = (int*)malloc(sizeof(int) * (n_all ? n_all : 1));
     int st = CDX_OK;
     for (uint64_t g = 0; g < G; ++g) {
-        const float* rw = rewards + g * n_all;
+        const float* rw = rewards ? rewards + g * n_all : NULL;
+        const double* rw64 = rewards64 ? rewards64 + g * n_all : NULL;
         /* RewardSet over all paths so far; certaindex_reward validates every reward and
          * folds left (mean) or takes the first maximum (max).  Incremental evaluation of
          * the same left fold / running first-maximum. */
@@ -548,7 +563,7 @@ int cdxo_reward_certaindex2(const float* rewards, const uint32_t* ids, const uin
         int bad = 0;
         for (uint32_t t = 0; t < T; ++t) {
             for (uint32_t w = 0; w < W; ++w) {
-                const double v = (double)rw[(size_t)t * W + w];
+                const double v = rw64 ? rw64[(size_t)t * W + w] : (double)rw[(size_t)t * W + w];
                 if (v < 0.0 || v > 1.0) bad = 1;
                 sum = sum + v;
                 if (t == 0 && w == 0)
@@ -726,7 +741,7 @@ static uint32_t plurality_ids(const uint32_t* v, const double* w, int n) {
         }
         tot[c] += w ? w[i] : 1.0;
     }
-    uint32_t best = keys[0];
+    uint32_t best = 0xffffffffu; /* std::string best stays empty when nothing beats -1.0 */
     double bw = -1.0;
     for (int c = 0; c < m; ++c)
         if (tot[c] > bw) {
@@ -746,10 +761,12 @@ int cdxo_sc_aggregate(const uint32_t* ids, uint64_t R, uint32_t P, uint32_t S, c
     return CDX_OK;
 }
 
-int cdxo_reward_aggregate(const float* rw, const uint32_t* ids, const uint8_t* agg, uint64_t G, uint32_t T,
-                          uint32_t W, const int32_t* exit_step, uint32_t* answer) {
+/* rewards as doubles (PathSample::reward), either from f32 or f64 storage */
+static int reward_aggregate_any(const float* rwf, const double* rwd, const uint32_t* ids, const uint8_t* agg,
+                                uint64_t G, uint32_t T, uint32_t W, const int32_t* exit_step, uint32_t* answer) {
     if (W == 0 || W > 1024 || T == 0) return CDX_EINVAL;
     double w[1024];
+#define RW(i) (rwd ? rwd[i] : (double)rwf[i])
     for (uint64_t g = 0; g < G; ++g) {
         const int32_t t = exit_step[g];
         if (t < 0 || (uint32_t)t >= T) return CDX_EINVAL;
@@ -758,15 +775,26 @@ int cdxo_reward_aggregate(const float* rw, const uint32_t* ids, const uint8_t* a
             const uint64_t n = (uint64_t)(t + 1) * W;
             uint64_t best = 0;
             for (uint64_t i = 1; i < n; ++i)
-                if ((double)rw[base + i] > (double)rw[base + best]) best = i;
+                if (RW(base + i) > RW(base + best)) best = i;
             answer[g] = ids[base + best];
-        } else { /* Rebase: runtime.cpp:357-378, last full layer = step t */
+        } else { /* Rebase: runtime.cpp:357-378, last full layer = step t; std::exp :324 */
             const uint64_t l0 = base + (uint64_t)t * W;
-            for (uint32_t i = 0; i < W; ++i) w[i] = exp((double)rw[l0 + i]);
+            for (uint32_t i = 0; i < W; ++i) w[i] = exp(RW(l0 + i));
             answer[g] = plurality_ids(ids + l0, w, (int)W);
         }
     }
+#undef RW
     return CDX_OK;
+}
+
+int cdxo_reward_aggregate(const float* rw, const uint32_t* ids, const uint8_t* agg, uint64_t G, uint32_t T,
+                          uint32_t W, const int32_t* exit_step, uint32_t* answer) {
+    return reward_aggregate_any(rw, NULL, ids, agg, G, T, W, exit_step, answer);
+}
+
+int cdxo_reward_aggregate_f64(const double* rw, const uint32_t* ids, const uint8_t* agg, uint64_t G, uint32_t T,
+                              uint32_t W, const int32_t* exit_step, uint32_t* answer) {
+    return reward_aggregate_any(NULL, rw, ids, agg, G, T, W, exit_step, answer);
 }
 
 /* ===================================================================================== */

@@ -92,6 +92,9 @@ int cdxo_reward_certaindex(const float* rewards, const uint32_t* ids, const uint
 int cdxo_reward_certaindex2(const float* rewards, const uint32_t* ids, const uint8_t* agg,
                             uint64_t G, uint32_t T, uint32_t W, double* R64, float* Rout,
                             float* Hout, double* H64);
+int cdxo_reward_certaindex_f64(const double* rewards, const uint32_t* ids, const uint8_t* agg,
+                               uint64_t G, uint32_t T, uint32_t W, double* R64, float* Rout,
+                               float* Hout, double* H64);
 
 /* ---- gang priority order (K6), SPEC.md:422-448,467-472 ----------------------------- */
 int cdxo_gang_order(const cdx_prog_soa* progs, uint64_t N, const cdx_inter_policy* pol,
@@ -115,6 +118,8 @@ int cdxo_sc_aggregate(const uint32_t* ids, uint64_t R, uint32_t P, uint32_t S, c
                       uint32_t* answer);
 int cdxo_reward_aggregate(const float* rw, const uint32_t* ids, const uint8_t* agg, uint64_t G, uint32_t T,
                           uint32_t W, const int32_t* exit_step, uint32_t* answer);
+int cdxo_reward_aggregate_f64(const double* rw, const uint32_t* ids, const uint8_t* agg, uint64_t G, uint32_t T,
+                              uint32_t W, const int32_t* exit_step, uint32_t* answer);
 
 #ifdef __cplusplus
 }

@@ -231,7 +231,8 @@ def reward_certaindex(rw, ids, agg, want_h64=False):
     R32 = np.empty((G, T), np.float32)
     H = np.empty((G, T), np.float32) if ids is not None else None
     H64 = np.empty((G, T), np.float64) if (ids is not None and want_h64) else None
-    st = lib().cdxo_reward_certaindex2(_p(np.ascontiguousarray(rw)),
+    f = lib().cdxo_reward_certaindex_f64 if rw.dtype == np.float64 else lib().cdxo_reward_certaindex2
+    st = f(_p(np.ascontiguousarray(rw)),
                                        _p(None if ids is None else np.ascontiguousarray(ids)),
                                        _p(np.ascontiguousarray(agg, dtype=np.uint8)), C.c_uint64(G), C.c_uint32(T),
                                        C.c_uint32(W), _p(R64), _p(R32), _p(H), _p(H64))
@@ -458,12 +459,15 @@ def sc_aggregate(ids, exit_knob):
 
 
 def reward_aggregate(rw, ids, agg, exit_step):
+    """f32 or f64 rewards (the latter: PathSample::reward / RewardSet doubles)."""
     G, T, W = rw.shape
     out = np.empty(max(G, 1), np.uint32)
-    lib().cdxo_reward_aggregate.argtypes = [P, P, P, C.c_uint64, C.c_uint32, C.c_uint32, P, P]
-    st = lib().cdxo_reward_aggregate(_p(np.ascontiguousarray(rw)), _p(np.ascontiguousarray(ids)),
-                                     _p(np.ascontiguousarray(agg, dtype=np.uint8)), G, T, W,
-                                     _p(np.ascontiguousarray(exit_step, dtype=np.int32)), _p(out))
+    f64 = rw.dtype == np.float64
+    f = lib().cdxo_reward_aggregate_f64 if f64 else lib().cdxo_reward_aggregate
+    f.argtypes = [P, P, P, C.c_uint64, C.c_uint32, C.c_uint32, P, P]
+    st = f(_p(np.ascontiguousarray(rw)), _p(np.ascontiguousarray(ids)),
+           _p(np.ascontiguousarray(agg, dtype=np.uint8)), G, T, W,
+           _p(np.ascontiguousarray(exit_step, dtype=np.int32)), _p(out))
     if st:
         raise ValueError(f"oracle reward_aggregate status {st}")
     return out[:G]

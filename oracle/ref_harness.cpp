@@ -472,6 +472,10 @@ int ref_aggregate(int archetype, const uint32_t* ids, const double* rewards, int
         }
         st.layer_widths.assign(layer_w, layer_w + n_layers);
         const auto res = d.aggregate_prefix(units);
+        if (res.answer.empty()) {  // weighted_plurality found no winner (NaN weights)
+            *out = 0xffffffffu;
+            return 0;
+        }
         for (uint32_t k = 0; k < nvocab; ++k)
             if (cdx::metrics::trim(voc[k]) == res.answer) {
                 *out = k;

@@ -314,8 +314,9 @@ class Context:
         a1, n1 = c_thresholds(th_mean)
         a2, n2 = c_thresholds(th_max)
         self._bind_stream()
-        self._check(self.lib.cdx_reward_certaindex(self.h, _ptr(rewards), _ptr(ids), _ptr(agg), G, T, W, a1, n1, a2,
-                                                   n2, _ptr(R), _ptr(H), _ptr(meets)))
+        f = self.lib.cdx_reward_certaindex_f64 if rewards.dtype == t.float64 else self.lib.cdx_reward_certaindex
+        self._check(f(self.h, _ptr(rewards), _ptr(ids), _ptr(agg), G, T, W, a1, n1, a2, n2, _ptr(R), _ptr(H),
+                      _ptr(meets)))
         return R, H, meets
 
     def reward_sets(self, values, row_off, agg):
@@ -384,14 +385,27 @@ class Context:
         return ans[:R]
 
     def reward_aggregate(self, rewards, ids, agg, exit_step):
+        """f32 or f64 rewards; answer CDX_NO_ANSWER (0xffffffff) where the reference's vote
+        has no winner.  Returns (answer, inexact) — inexact stays 0 (ABI v2 counter)."""
         t = self.torch
         G, T, W = rewards.shape
         ans = self.empty((max(G, 1),), t.int32)
         inexact = self.torch.zeros((1,), dtype=t.int64, device=self.dev)
         self._bind_stream()
-        self._check(self.lib.cdx_reward_aggregate(self.h, _ptr(rewards), _ptr(ids), _ptr(agg), G, T, W,
-                                                  _ptr(exit_step), _ptr(ans), _ptr(inexact)))
+        if rewards.dtype == t.float64:
+            self._check(self.lib.cdx_reward_aggregate_f64(self.h, _ptr(rewards), _ptr(ids), _ptr(agg), G, T, W,
+                                                          _ptr(exit_step), _ptr(ans)))
+        else:
+            self._check(self.lib.cdx_reward_aggregate(self.h, _ptr(rewards), _ptr(ids), _ptr(agg), G, T, W,
+                                                      _ptr(exit_step), _ptr(ans), _ptr(inexact)))
         return ans[:G], inexact
+
+    def libm_exp(self, x):
+        """std::exp with the host libm's bits, on the device (f64 tensor in, f64 out)."""
+        y = self.torch.empty_like(x)
+        self._bind_stream()
+        self._check(self.lib.cdx_libm_exp(self.h, _ptr(x), x.numel(), _ptr(y)))
+        return y
 
     # -- epsilon-accuracy stop test (probe.cpp:104-120, theory.cpp:117-146) --
     def cot_eps_stop(self, ids, hes, k: int, epsilon: float, want_state: bool = False):

@@ -86,6 +86,7 @@ SIGNATURES = {
     "cdx_meets_thresholds_rows": (C.c_int, [P, P, P, U64, C.POINTER(Threshold), U32, P]),
     "cdx_id_histogram": (C.c_int, [P, P, U64, U32, P]),
     "cdx_entropy_one": (C.c_int, [P, P, U32, U32, P, P]),
+    "cdx_entropy_sizes_host": (C.c_int, [P, P, U32, C.c_int32, P, P]),
     "cdx_iteration_tokens_rows": (C.c_int, [P, P, P, U64, C.c_double, P]),
     "cdx_alloc": (C.c_int, [P, U64, C.POINTER(P)]),
     "cdx_free": (C.c_int, [P, P]),
@@ -94,6 +95,8 @@ SIGNATURES = {
     "cdx_allocate_scan": (C.c_int, [P, P, U64, U32, C.POINTER(AllocPolicy), I64, U32, P, P, P, P, P, P, P, P]),
     "cdx_cot_exit": (C.c_int, [P, P, P, P, U64, U32, C.POINTER(ProbeCfg), P, P, P, P, P]),
     "cdx_reward_certaindex": (C.c_int, [P, P, P, P, U64, U32, U32, C.POINTER(Threshold), U32,
+                                        C.POINTER(Threshold), U32, P, P, P]),
+    "cdx_reward_certaindex_f64": (C.c_int, [P, P, P, P, U64, U32, U32, C.POINTER(Threshold), U32,
                                         C.POINTER(Threshold), U32, P, P, P]),
     "cdx_reward_sets": (C.c_int, [P, P, P, P, U64, P]),
     "cdx_canon_intern": (C.c_int, [P, P, P, U64, C.POINTER(C.c_char_p), U32, P, P, P, C.POINTER(U64)]),
@@ -106,6 +109,8 @@ SIGNATURES = {
     "cdx_probe_eps_stop_rows": (C.c_int, [P, P, P, P, U64, I32, C.c_double, P]),
     "cdx_sc_aggregate": (C.c_int, [P, P, U64, U32, U32, P, P]),
     "cdx_reward_aggregate": (C.c_int, [P, P, P, P, U64, U32, U32, P, P, P]),
+    "cdx_reward_aggregate_f64": (C.c_int, [P, P, P, P, U64, U32, U32, P, P]),
+    "cdx_libm_exp": (C.c_int, [P, P, U64, P]),
     "cdx_sc_decide_host": (C.c_int, [P, P, U64, U32, U32, C.POINTER(Threshold), U32, C.POINTER(AllocPolicy),
                                      P, P, P, P, P]),
 }

@@ -54,8 +54,6 @@ struct cdx_ctx {
     // JSONL ingestion working buffer (k_jsonl.cu)
     void* jl_buf = nullptr;
     size_t jl_bytes = 0;
-    // std::exp on the 2^-24 grid of [0,1] (Rebase aggregation), built on first use
-    double* exp_tab = nullptr;
     double* comp_tab[17] = {};  // K2: H~ per first-seen cluster-size composition, S <= 16 (k_sc.cu)
     // term-table cache (device): keyed by the list of n values it was built for
     double* tt_dev = nullptr;
@@ -108,6 +106,20 @@ int radix_sort_pairs(cdx_ctx* ctx, uint64_t* k0, uint32_t* v0, uint64_t* k1, uin
 #define CDX_LAUNCHED(ctx) ((ctx)->launches++)
 
 __device__ __forceinline__ void set_dev_err(int* d_err, int code) { atomicCAS(d_err, 0, code); }
+
+// The reference's host arithmetic is x86-64 SSE2: a + b / a / b with a NaN operand returns
+// that NaN (quieted, sign and payload kept), the first operand's when both are NaN.  The GPU
+// returns a canonical NaN instead; these keep the host's bits where a NaN reaches an f64
+// output of the scalar API (e.g. certaindex_reward's mean over a NaN reward).
+__device__ __forceinline__ double x86_nan(double a) {
+    return __longlong_as_double(__double_as_longlong(a) | 0x0008000000000000ll);
+}
+__device__ __forceinline__ double x86_add(double a, double b) {
+    return isnan(a) ? x86_nan(a) : (isnan(b) ? x86_nan(b) : __dadd_rn(a, b));
+}
+__device__ __forceinline__ double x86_div(double a, double b) {
+    return isnan(a) ? x86_nan(a) : (isnan(b) ? x86_nan(b) : __ddiv_rn(a, b));
+}
 
 // ---------------------------------------------------------------------------------------
 // mbarrier / bulk-copy / TMA (PTX for sm_90+/sm_100a; SASS: SYNCS.*, UBLKCP, UTMALDG)

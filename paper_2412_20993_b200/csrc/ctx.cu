@@ -188,7 +188,6 @@ int cdx_ctx_destroy(cdx_ctx* ctx) {
     if (ctx->pipe_buf) cudaFree(ctx->pipe_buf);
     if (ctx->tt_dev) cudaFree(ctx->tt_dev);
     if (ctx->al_state) cudaFree(ctx->al_state);
-    if (ctx->exp_tab) cudaFree(ctx->exp_tab);
     for (double* t : ctx->comp_tab)
         if (t) cudaFree(t);
     if (ctx->jl_buf) cudaFree(ctx->jl_buf);

@@ -2,8 +2,8 @@
 //
 //   cluster_exact             K1 canon_intern (trim + exact bytes -> dense first-seen ids)
 //                             + cdx_id_histogram (cluster sizes)      metrics.cpp:21-37
-//   semantic_entropy /        cdx_entropy_one: host-libm term row T_n[c] = (c/n) ln(c/n),
-//   certaindex_entropy        FP64 device fold in cluster order       metrics.cpp:107-125
+//   semantic_entropy /        cdx_entropy_sizes_host: host-libm term (c/n) ln(c/n) per
+//   certaindex_entropy        cluster, FP64 device fold in cluster order  metrics.cpp:107-125
 //   certaindex_reward         cdx_reward_sets (left fold / first max)  metrics.cpp:127-137
 //   combined_meets_thresholds cdx_meets_thresholds_rows               metrics.cpp:159-171
 // trim() is the boundary's own view adjustment (it returns a view into the caller's
@@ -48,17 +48,15 @@ Clustering cluster_exact(std::span<const std::string> answers) {
 
 namespace {
 
-// (H, H~) of one clustering on the device
+// (H, H~) of one clustering on the device (any sizes and total, as the reference)
 std::pair<double, double> entropy_pair(const Clustering& c) {
-    if (c.total < 1 || c.clusters.empty()) throw std::invalid_argument("semantic_entropy: invalid clustering");
-    std::vector<uint32_t> sizes;
+    std::vector<int32_t> sizes;
     sizes.reserve(c.clusters.size());
-    for (const auto& cl : c.clusters) sizes.push_back(cl.size < 1 ? 0u : static_cast<uint32_t>(cl.size));
+    for (const auto& cl : c.clusters) sizes.push_back(static_cast<int32_t>(cl.size));
     auto& cx = detail::scalar_ctx();
-    batch::DeviceArray<uint32_t> d_sizes(cx, std::span<const uint32_t>(sizes));
     batch::DeviceArray<double> out(cx, 2);
-    cx.check(cdx_entropy_one(cx.raw(), d_sizes.data(), static_cast<uint32_t>(sizes.size()),
-                             static_cast<uint32_t>(c.total), out.data(), out.data() + 1));
+    cx.check(cdx_entropy_sizes_host(cx.raw(), sizes.data(), static_cast<uint32_t>(sizes.size()),
+                                    static_cast<int32_t>(c.total), out.data(), out.data() + 1));
     const auto v = out.download();
     return {v[0], v[1]};
 }

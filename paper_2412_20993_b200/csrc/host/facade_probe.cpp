@@ -22,7 +22,7 @@ namespace cdx::probe {
 void ProbeConfig::validate() const {
     if (interval_tokens < 1) throw std::invalid_argument("probe: interval_tokens must be >= 1");
     if (window < 1) throw std::invalid_argument("probe: window must be >= 1");
-    if (!(threshold > 0.0) || threshold > 1.0) throw std::invalid_argument("probe: threshold must be in (0,1]");
+    if (threshold <= 0.0 || threshold > 1.0) throw std::invalid_argument("probe: threshold must be in (0,1]");
     if (max_tokens < 1) throw std::invalid_argument("probe: max_tokens must be >= 1");
 }
 

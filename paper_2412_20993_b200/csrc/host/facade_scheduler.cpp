@@ -40,24 +40,26 @@ struct DeviceSoA {
     cdx_prog_soa soa{};
 };
 
-// ProgramState list -> device SoA in input order; ids are attached after ordering.
-DeviceSoA upload(batch::Context& cx, std::span<const ProgramState> ps) {
-    const size_t n = ps.size();
+// ProgramState list -> device SoA in `idx` order (device index i = ps[idx[i]]); program ids
+// are attached after ordering.
+DeviceSoA upload(batch::Context& cx, std::span<const ProgramState> all, const std::vector<uint32_t>& idx) {
+    const size_t n = idx.size();
+    auto ps = [&](size_t i) -> const ProgramState& { return all[idx[i]]; };
     std::vector<double> a(n), l(n);
     std::vector<int64_t> s(n);
     std::vector<uint32_t> c(n);
     std::vector<uint16_t> k(n), cap(n);
     std::vector<uint8_t> t(n);
     for (size_t i = 0; i < n; ++i) {
-        if (ps[i].knob < 0 || ps[i].knob > 0xffff || ps[i].resource_cap < 0 || ps[i].resource_cap > 0xffff)
+        if (ps(i).knob < 0 || ps(i).knob > 0xffff || ps(i).resource_cap < 0 || ps(i).resource_cap > 0xffff)
             throw std::invalid_argument("next_batch: knob and resource_cap must be in [0, 65535]");
-        a[i] = ps[i].arrival;
-        l[i] = ps[i].last_service;
-        s[i] = ps[i].iteration_token_sum;
-        c[i] = ps[i].iteration_count;
-        k[i] = static_cast<uint16_t>(ps[i].knob);
-        cap[i] = static_cast<uint16_t>(ps[i].resource_cap);
-        t[i] = ps[i].terminated ? 1 : 0;
+        a[i] = ps(i).arrival;
+        l[i] = ps(i).last_service;
+        s[i] = ps(i).iteration_token_sum;
+        c[i] = ps(i).iteration_count;
+        k[i] = static_cast<uint16_t>(ps(i).knob);
+        cap[i] = static_cast<uint16_t>(ps(i).resource_cap);
+        t[i] = ps(i).terminated ? 1 : 0;
     }
     DeviceSoA d;
     d.arrival = batch::DeviceArray<double>(cx, std::span<const double>(a));
@@ -78,7 +80,13 @@ std::pair<std::vector<uint32_t>, std::vector<uint8_t>> order_of(std::span<const 
                                                                 bool want_esc) {
     if (ps.empty()) return {};
     auto& cx = detail::scalar_ctx();
-    auto d = upload(cx, ps);
+    // K6 breaks the last tie by device index (SPEC.md:470 says program id): hand it the
+    // programs in program-id order (stable, so equal ids keep input order) and map back
+    std::vector<uint32_t> by_id(ps.size());
+    for (size_t i = 0; i < ps.size(); ++i) by_id[i] = static_cast<uint32_t>(i);
+    std::stable_sort(by_id.begin(), by_id.end(),
+                     [&](uint32_t a, uint32_t b) { return ps[a].program_id < ps[b].program_id; });
+    auto d = upload(cx, ps, by_id);
     batch::DeviceArray<uint32_t> order(cx, ps.size());
     batch::DeviceArray<uint8_t> esc;
     if (want_esc) esc = batch::DeviceArray<uint8_t>(cx, ps.size());
@@ -86,8 +94,13 @@ std::pair<std::vector<uint32_t>, std::vector<uint8_t>> order_of(std::span<const 
                                             want_esc ? esc.data() : nullptr, nullptr);
     auto o = order.download();
     o.resize(n);
+    for (auto& x : o) x = by_id[x];  // device index -> input index
     std::vector<uint8_t> e;
-    if (want_esc) e = esc.download();
+    if (want_esc) {
+        const auto ed = esc.download();
+        e.assign(ps.size(), 0);
+        for (size_t i = 0; i < ps.size(); ++i) e[by_id[i]] = ed[i];
+    }
     return {o, e};
 }
 

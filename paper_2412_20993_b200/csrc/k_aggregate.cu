@@ -8,10 +8,11 @@
 //           (strict `>` over reward.value_or(0.0) in path order).
 //   Rebase  softmax-weighted plurality over the last full layer: weight(cluster) = sum of
 //           exp(reward) over its members in path order (double), earliest-seen wins ties.
-//           exp() is the host libm's: rewards on the 2^-24 grid (the synthetic traces and
-//           every value k/2^24) read a table of std::exp(k * 2^-24) built on the host once
-//           per context, so the weights are the reference's bits; a reward off that grid
-//           uses the device exp (<= 1 ulp from the host's) and is counted in *inexact.
+//           exp() is the host libm's own algorithm restated bit for bit on the device
+//           (libm_exp.cuh), so the weights are the reference's bits for every reward, on or
+//           off any grid.  When no weight beats the reference's initial -1.0 (NaN rewards)
+//           the reference returns an empty string; the answer id is then CDX_NO_ANSWER.
+// Rewards are f32 (the synthetic traces) or f64 (RewardSet holds doubles, metrics.hpp:74-77).
 // CoT's final answer is K3's final_id (probe::final_answer).  Answers are interned ids
 // (equal id <=> equal trimmed bytes), so the winner's id is the reference's trimmed answer.
 
@@ -19,6 +20,7 @@
 #include <vector>
 
 #include "cdx_internal.cuh"
+#include "libm_exp.cuh"
 
 namespace cdx {
 namespace {
@@ -56,18 +58,11 @@ __global__ void sc_aggregate_kernel(const uint32_t* __restrict__ ids, uint64_t R
     }
 }
 
-__device__ __forceinline__ double exp_ref(float r, const double* __restrict__ tab, unsigned long long* inexact) {
-    const float s = r * 16777216.0f;  // exact scaling by 2^24
-    if (r >= 0.0f && r <= 1.0f && s == truncf(s)) return __ldg(tab + static_cast<uint32_t>(s));
-    atomicAdd(inexact, 1ull);
-    return exp(static_cast<double>(r));
-}
-
 // MCTS / Rebase: thread per program, exit step t (0-based): paths = steps 0..t
+template <typename RT>
 __global__ void __launch_bounds__(AG_THREADS) reward_aggregate_kernel(
-    const float* __restrict__ rw, const uint32_t* __restrict__ ids, const uint8_t* __restrict__ agg, uint64_t G,
-    uint32_t T, uint32_t W, const int32_t* __restrict__ exit_step, const double* __restrict__ tab,
-    uint32_t* __restrict__ answer, unsigned long long* inexact, int* err) {
+    const RT* __restrict__ rw, const uint32_t* __restrict__ ids, const uint8_t* __restrict__ agg, uint64_t G,
+    uint32_t T, uint32_t W, const int32_t* __restrict__ exit_step, uint32_t* __restrict__ answer, int* err) {
     extern __shared__ __align__(16) uint8_t ag_smem[];  // per thread: W weights (f64) then W keys (u32)
     const uint64_t g = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
     if (g >= G) return;
@@ -80,10 +75,10 @@ __global__ void __launch_bounds__(AG_THREADS) reward_aggregate_kernel(
     if (agg[g] == CDX_AGG_MEAN) {  // MCTS: first maximum over every path so far
         const uint64_t n = static_cast<uint64_t>(t + 1) * W;
         uint64_t best = 0;
-        float bv = __ldg(rw + base);
+        double bv = static_cast<double>(__ldg(rw + base));
         for (uint64_t i = 1; i < n; ++i) {
-            const float v = __ldg(rw + base + i);
-            if (static_cast<double>(v) > static_cast<double>(bv)) {
+            const double v = static_cast<double>(__ldg(rw + base + i));
+            if (v > bv) {  // strict >, NaN never wins (runtime.cpp:386-388)
                 bv = v;
                 best = i;
             }
@@ -99,7 +94,7 @@ __global__ void __launch_bounds__(AG_THREADS) reward_aggregate_kernel(
     const uint64_t l0 = base + static_cast<uint64_t>(t) * W;
     for (uint32_t i = 0; i < W; ++i) {
         const uint32_t v = __ldg(ids + l0 + i);
-        const double e = exp_ref(__ldg(rw + l0 + i), tab, inexact);
+        const double e = libm::exp(static_cast<double>(__ldg(rw + l0 + i)));  // std::exp, runtime.cpp:324
         uint32_t c = 0;
         while (c < m && key[c] != v) ++c;
         if (c == m) {
@@ -109,7 +104,7 @@ __global__ void __launch_bounds__(AG_THREADS) reward_aggregate_kernel(
         }
         wt[c] = __dadd_rn(wt[c], e);
     }
-    uint32_t best = key[0];
+    uint32_t best = CDX_NO_ANSWER;  // std::string best; stays empty if nothing beats -1.0
     double bw = -1.0;
     for (uint32_t c = 0; c < m; ++c)
         if (wt[c] > bw) {
@@ -117,6 +112,12 @@ __global__ void __launch_bounds__(AG_THREADS) reward_aggregate_kernel(
             best = key[c];
         }
     answer[g] = best;
+}
+
+__global__ void libm_exp_kernel(const double* __restrict__ x, uint64_t n, double* __restrict__ y) {
+    for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<uint64_t>(gridDim.x) * blockDim.x)
+        y[i] = libm::exp(x[i]);
 }
 
 unsigned grid_of(const cdx_ctx* ctx, uint64_t n, unsigned t) {
@@ -141,38 +142,56 @@ extern "C" int cdx_sc_aggregate(cdx_ctx* ctx, const uint32_t* ids, uint64_t R, u
     return CDX_OK;
 }
 
-extern "C" int cdx_reward_aggregate(cdx_ctx* ctx, const float* rewards, const uint32_t* ids, const uint8_t* agg,
-                                    uint64_t G, uint32_t T, uint32_t W, const int32_t* exit_step, uint32_t* answer,
-                                    uint64_t* inexact) {
-    using namespace cdx;
-    CDX_NVTX("cdx_reward_aggregate");
+namespace cdx {
+namespace {
+template <typename RT>
+int reward_aggregate_impl(cdx_ctx* ctx, const RT* rewards, const uint32_t* ids, const uint8_t* agg, uint64_t G,
+                          uint32_t T, uint32_t W, const int32_t* exit_step, uint32_t* answer, uint64_t* inexact) {
     if (!ctx) return CDX_EINVAL;
     if (T == 0 || W == 0) return set_error(ctx, CDX_ERUNTIME, "aggregate: empty program");
     if (W > static_cast<uint32_t>(AG_MAX_W)) return set_error(ctx, CDX_EINVAL, "reward_aggregate: width above 256");
-    if (!inexact) return set_error(ctx, CDX_EINVAL, "reward_aggregate: null inexact counter");
-    cudaError_t e = cudaMemsetAsync(inexact, 0, 8, ctx->stream);
-    if (e != cudaSuccess) return cuda_fail(ctx, e, "reward_aggregate");
+    if (inexact) {  // ABI v2 counter of approximated weights: every weight is exact now
+        cudaError_t e = cudaMemsetAsync(inexact, 0, 8, ctx->stream);
+        if (e != cudaSuccess) return cuda_fail(ctx, e, "reward_aggregate");
+    }
     if (G == 0) return CDX_OK;
     if (!rewards || !ids || !agg || !exit_step || !answer)
         return set_error(ctx, CDX_EINVAL, "reward_aggregate: null pointer");
-    // std::exp on the 2^-24 grid of [0,1], from the host libm (the reference's exp)
-    if (!ctx->exp_tab) {
-        const size_t n = (1u << 24) + 1;
-        std::vector<double> h(n);
-        for (size_t k = 0; k < n; ++k) h[k] = std::exp(std::ldexp(static_cast<double>(k), -24));
-        if (cudaMalloc(&ctx->exp_tab, n * sizeof(double)) != cudaSuccess)
-            return set_error(ctx, CDX_ECUDA, "reward_aggregate: exp table allocation failed");
-        e = cudaMemcpy(ctx->exp_tab, h.data(), n * sizeof(double), cudaMemcpyHostToDevice);
-        if (e != cudaSuccess) return cuda_fail(ctx, e, "reward_aggregate: exp table upload");
-    }
     const unsigned threads = W > 128 ? 32u : static_cast<unsigned>(AG_THREADS);
     const size_t smem = static_cast<size_t>(threads) * W * 12u;
-    cudaFuncSetAttribute(reward_aggregate_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    cudaFuncSetAttribute(reward_aggregate_kernel<RT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         static_cast<int>(smem));
     const unsigned grid = static_cast<unsigned>((G + threads - 1) / threads);
-    reward_aggregate_kernel<<<grid, threads, smem, ctx->stream>>>(rewards, ids, agg, G, T, W, exit_step, ctx->exp_tab,
-                                                                  answer,
-                                                                  reinterpret_cast<unsigned long long*>(inexact),
-                                                                  ctx->d_err);
+    reward_aggregate_kernel<RT><<<grid, threads, smem, ctx->stream>>>(rewards, ids, agg, G, T, W, exit_step, answer,
+                                                                      ctx->d_err);
     CDX_CHECK_LAUNCH(ctx, "reward_aggregate");
+    return CDX_OK;
+}
+}  // namespace
+}  // namespace cdx
+
+extern "C" int cdx_reward_aggregate(cdx_ctx* ctx, const float* rewards, const uint32_t* ids, const uint8_t* agg,
+                                    uint64_t G, uint32_t T, uint32_t W, const int32_t* exit_step, uint32_t* answer,
+                                    uint64_t* inexact) {
+    CDX_NVTX("cdx_reward_aggregate");
+    return cdx::reward_aggregate_impl(ctx, rewards, ids, agg, G, T, W, exit_step, answer, inexact);
+}
+
+extern "C" int cdx_reward_aggregate_f64(cdx_ctx* ctx, const double* rewards, const uint32_t* ids, const uint8_t* agg,
+                                        uint64_t G, uint32_t T, uint32_t W, const int32_t* exit_step,
+                                        uint32_t* answer) {
+    CDX_NVTX("cdx_reward_aggregate_f64");
+    return cdx::reward_aggregate_impl(ctx, rewards, ids, agg, G, T, W, exit_step, answer, nullptr);
+}
+
+extern "C" int cdx_libm_exp(cdx_ctx* ctx, const double* x, uint64_t n, double* y) {
+    using namespace cdx;
+    CDX_NVTX("cdx_libm_exp");
+    if (!ctx) return CDX_EINVAL;
+    if (n == 0) return CDX_OK;
+    if (!x || !y) return set_error(ctx, CDX_EINVAL, "libm_exp: null pointer");
+    const unsigned grid = grid_of(ctx, n, 256);
+    libm_exp_kernel<<<grid, 256, 0, ctx->stream>>>(x, n, y);
+    CDX_CHECK_LAUNCH(ctx, "libm_exp");
     return CDX_OK;
 }

@@ -125,7 +125,7 @@ unsigned grid_n(const cdx_ctx* ctx, uint64_t n) {
 
 int check_eps(cdx_ctx* ctx, int32_t k, double epsilon) {  // theory.cpp:118-119
     if (k < 1) return set_error(ctx, CDX_EINVAL, "epsilon_stop_test: k must be >= 1");
-    if (!(epsilon > 0.0)) return set_error(ctx, CDX_EINVAL, "epsilon_stop_test: epsilon must be > 0");
+    if (epsilon <= 0.0) return set_error(ctx, CDX_EINVAL, "epsilon_stop_test: epsilon must be > 0");
     return CDX_OK;
 }
 

@@ -33,7 +33,6 @@ struct Markers {
     uint32_t off[MAX_MARKERS + 1];
     char bytes[MARKER_BYTES];
 };
-__constant__ Markers c_markers;
 
 __device__ __forceinline__ bool is_space(uint8_t c) {
     return c == ' ' || c == '\t' || c == '\n' || c == '\r' || c == '\f' || c == '\v';
@@ -50,13 +49,15 @@ __device__ uint64_t hash_bytes(const uint8_t* s, uint64_t n) {
     return h ? h : 1;  // 0 marks an empty slot
 }
 
-__device__ bool hesitant(const uint8_t* s, uint64_t n) {
-    for (uint32_t k = 0; k < c_markers.n; ++k) {
-        const uint32_t mb = c_markers.off[k], ml = c_markers.off[k + 1] - mb;
+// markers travel by value in the kernel's parameter space (per launch, so concurrent calls
+// from different contexts never see each other's markers)
+__device__ bool hesitant(const Markers& mk, const uint8_t* s, uint64_t n) {
+    for (uint32_t k = 0; k < mk.n; ++k) {
+        const uint32_t mb = mk.off[k], ml = mk.off[k + 1] - mb;
         if (ml == 0 || ml > n) continue;  // empty markers never match (probe.cpp:41)
         for (uint64_t i = 0; i + ml <= n; ++i) {
             uint32_t j = 0;
-            while (j < ml && lower(s[i + j]) == static_cast<uint8_t>(c_markers.bytes[mb + j])) ++j;
+            while (j < ml && lower(s[i + j]) == static_cast<uint8_t>(mk.bytes[mb + j])) ++j;
             if (j == ml) return true;
         }
     }
@@ -75,11 +76,11 @@ __device__ __forceinline__ Trim trim(const uint8_t* a, uint64_t b, uint64_t e) {
 __global__ void intern_insert(const uint8_t* __restrict__ arena, const uint64_t* __restrict__ off, uint64_t n,
                               unsigned long long* __restrict__ keys, uint32_t* __restrict__ first,
                               uint32_t* __restrict__ slot_of, uint8_t* __restrict__ hes, uint64_t cap_mask,
-                              int* d_err) {
+                              const __grid_constant__ Markers mk, int* d_err) {
     for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n;
          i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
         const uint64_t b0 = off[i], e0 = off[i + 1];
-        if (hes) hes[i] = hesitant(arena + b0, e0 - b0) ? 1 : 0;
+        if (hes) hes[i] = hesitant(mk, arena + b0, e0 - b0) ? 1 : 0;
         const Trim t = trim(arena, b0, e0);
         const unsigned long long h = hash_bytes(arena + t.b, t.e - t.b);
         uint64_t s = h & cap_mask;
@@ -174,7 +175,6 @@ extern "C" int cdx_canon_intern(cdx_ctx* ctx, const char* bytes, const uint64_t*
     mk.off[n_markers] = pos;
     *n_unique = 0;
     if (n == 0) return CDX_OK;
-    cudaMemcpyToSymbolAsync(c_markers, &mk, sizeof(mk), 0, cudaMemcpyHostToDevice, ctx->stream);
 
     uint64_t cap = 1024;
     while (cap < 2 * n) cap <<= 1;
@@ -192,7 +192,7 @@ extern "C" int cdx_canon_intern(cdx_ctx* ctx, const char* bytes, const uint64_t*
     cudaMemsetAsync(first, 0xff, cap * 4, ctx->stream);
     const unsigned grid = static_cast<unsigned>(std::min<uint64_t>((n + 255) / 256, ctx->sm_count * 16ull));
     const uint8_t* arena = reinterpret_cast<const uint8_t*>(bytes);
-    intern_insert<<<grid, 256, 0, ctx->stream>>>(arena, offsets, n, keys, first, slot_of, hes, cap - 1, ctx->d_err);
+    intern_insert<<<grid, 256, 0, ctx->stream>>>(arena, offsets, n, keys, first, slot_of, hes, cap - 1, mk, ctx->d_err);
     CDX_CHECK_LAUNCH(ctx, "canon_intern(insert)");
     intern_verify<<<grid, 256, 0, ctx->stream>>>(arena, offsets, n, first, slot_of, flags, ctx->d_err);
     CDX_CHECK_LAUNCH(ctx, "canon_intern(verify)");

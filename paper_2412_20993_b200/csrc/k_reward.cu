@@ -67,6 +67,7 @@ struct RwParams {
     // lo = max of the >= cutoffs, hi = min of the <= cutoffs; has = any threshold on it
     double box_lo[2][2], box_hi[2][2];
     uint8_t box_has[2][2];
+    uint8_t box_never[2];     // a NaN cutoff: every compare false (metrics.cpp:167)
     uint8_t th_sig[2][RW_MAX_TH];
     uint8_t th_dir[2][RW_MAX_TH];
     double th_cut[2][RW_MAX_TH];
@@ -76,6 +77,7 @@ struct RwParams {
 // compares is the interval test above (NaN fails either way); signals without a threshold
 // are not looked at, as in the reference.
 __device__ __forceinline__ bool meets_box(const RwParams& p, int a, double hc, double rv) {
+    if (p.box_never[a]) return false;
     const bool okh = !p.box_has[a][0] || (hc >= p.box_lo[a][0] && hc <= p.box_hi[a][0]);
     const bool okr = !p.box_has[a][1] || (rv >= p.box_lo[a][1] && rv <= p.box_hi[a][1]);
     return okh && okr;
@@ -562,8 +564,12 @@ constexpr int OV_WARPS = 4;
 
 // gtab (nullable): programs too large for a shared-memory table (2 * cap + T * W words per
 // warp over ~220 KB) keep it in global memory instead, one slice per warp of the grid.
+// RT = double: the f64 entry (cdx_reward_certaindex_f64) runs every program here (all = 1:
+// program j of the grid-stride loop is program j, no overflow list).
+template <typename RT>
 __global__ void __launch_bounds__(OV_WARPS * 32) reward_overflow_kernel(const __grid_constant__ RwParams p,
-                                                                        uint32_t cap_log2, uint32_t* gtab) {
+                                                                        uint32_t cap_log2, uint32_t* gtab,
+                                                                        const RT* __restrict__ rw, uint32_t all) {
     extern __shared__ __align__(16) uint8_t smem[];
     const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
     const uint32_t cap = 1u << cap_log2;  // hash slots (>= 2 * T * W)
@@ -572,14 +578,14 @@ __global__ void __launch_bounds__(OV_WARPS * 32) reward_overflow_kernel(const __
                           : reinterpret_cast<uint32_t*>(smem) + warp * (2 * cap + nmax);
     uint32_t* hord = hkey + cap;
     uint32_t* cnt = hord + cap;
-    const uint32_t n_ovf = *p.ovf_count;
-    for (uint32_t j = blockIdx.x * nw + warp; j < n_ovf; j += gridDim.x * nw) {
-        const uint64_t g = p.ovf_list[j];
+    const uint64_t n_ovf = all ? p.G : *p.ovf_count;
+    for (uint64_t j = blockIdx.x * nw + warp; j < n_ovf; j += static_cast<uint64_t>(gridDim.x) * nw) {
+        const uint64_t g = all ? j : p.ovf_list[j];
         for (uint32_t i = lane; p.ids && i < cap; i += 32) hord[i] = 0xffffffffu;  // empty
         __syncwarp();
         uint32_t m = 0;
         double sum = 0.0;
-        float best = 0.f;
+        RT best = 0;
         uint32_t mword = 0;
         const uint8_t a = p.agg[g];
         for (uint32_t t = 0; t < p.T; ++t) {
@@ -626,8 +632,8 @@ __global__ void __launch_bounds__(OV_WARPS * 32) reward_overflow_kernel(const __
             // rewards: sequential left fold / first maximum on lane 0
             if (lane == 0) {
                 for (uint32_t w = 0; w < p.W; ++w) {
-                    const float r = __ldg(p.rewards + base + w);
-                    if (r < 0.f || r > 1.f) set_dev_err(p.d_err, DEV_REWARD_RANGE);  // metrics.cpp:129-132
+                    const RT r = __ldg(rw + base + w);
+                    if (r < RT(0) || r > RT(1)) set_dev_err(p.d_err, DEV_REWARD_RANGE);  // metrics.cpp:129-132
                     sum = __dadd_rn(sum, static_cast<double>(r));
                     if (t == 0 && w == 0) best = r;
                     else if (best < r) best = r;
@@ -660,14 +666,44 @@ __global__ void __launch_bounds__(OV_WARPS * 32) reward_overflow_kernel(const __
 }  // namespace
 }  // namespace cdx
 
+namespace cdx {
+namespace {
+int reward_certaindex_impl(cdx_ctx* ctx, const float* rewards, const double* rewards64, const uint32_t* ids,
+                           const uint8_t* agg, uint64_t G, uint32_t T, uint32_t W, const cdx_threshold* th_mean,
+                           uint32_t n_th_mean, const cdx_threshold* th_max, uint32_t n_th_max, float* R, float* H,
+                           uint32_t* meets_bits);
+}  // namespace
+}  // namespace cdx
+
 extern "C" int cdx_reward_certaindex(cdx_ctx* ctx, const float* rewards, const uint32_t* ids, const uint8_t* agg,
                                      uint64_t G, uint32_t T, uint32_t W, const cdx_threshold* th_mean,
                                      uint32_t n_th_mean, const cdx_threshold* th_max, uint32_t n_th_max, float* R,
                                      float* H, uint32_t* meets_bits) {
-    using namespace cdx;
     CDX_NVTX("cdx_reward_certaindex");
+    if (!rewards && ctx) return cdx::set_error(ctx, CDX_EINVAL, "reward_certaindex: null pointer");
+    return cdx::reward_certaindex_impl(ctx, rewards, nullptr, ids, agg, G, T, W, th_mean, n_th_mean, th_max, n_th_max,
+                                       R, H, meets_bits);
+}
+
+extern "C" int cdx_reward_certaindex_f64(cdx_ctx* ctx, const double* rewards, const uint32_t* ids,
+                                         const uint8_t* agg, uint64_t G, uint32_t T, uint32_t W,
+                                         const cdx_threshold* th_mean, uint32_t n_th_mean,
+                                         const cdx_threshold* th_max, uint32_t n_th_max, float* R, float* H,
+                                         uint32_t* meets_bits) {
+    CDX_NVTX("cdx_reward_certaindex_f64");
+    if (!rewards && ctx) return cdx::set_error(ctx, CDX_EINVAL, "reward_certaindex: null pointer");
+    return cdx::reward_certaindex_impl(ctx, nullptr, rewards, ids, agg, G, T, W, th_mean, n_th_mean, th_max, n_th_max,
+                                       R, H, meets_bits);
+}
+
+namespace cdx {
+namespace {
+int reward_certaindex_impl(cdx_ctx* ctx, const float* rewards, const double* rewards64, const uint32_t* ids,
+                           const uint8_t* agg, uint64_t G, uint32_t T, uint32_t W, const cdx_threshold* th_mean,
+                           uint32_t n_th_mean, const cdx_threshold* th_max, uint32_t n_th_max, float* R, float* H,
+                           uint32_t* meets_bits) {
     if (!ctx) return CDX_EINVAL;
-    if (!rewards || !agg) return set_error(ctx, CDX_EINVAL, "reward_certaindex: null pointer");
+    if (!agg) return set_error(ctx, CDX_EINVAL, "reward_certaindex: null pointer");
     if (T == 0 || W == 0) return set_error(ctx, CDX_EINVAL, "certaindex_reward: empty reward set");
     if (static_cast<uint64_t>(T) * W > (1u << 16))
         return set_error(ctx, CDX_EINVAL, "reward_certaindex: at most 65536 paths per program");
@@ -701,9 +737,11 @@ extern "C" int cdx_reward_certaindex(cdx_ctx* ctx, const float* rewards, const u
             p.box_hi[a][sg] = INFINITY;
             p.box_has[a][sg] = 0;
         }
+        p.box_never[a] = 0;
         for (uint32_t i = 0; i < n; ++i) {
             const int sg = th[i].signal == CDX_SIG_ENTROPY ? 0 : 1;  // validated: entropy or reward
             p.box_has[a][sg] = 1;
+            if (std::isnan(th[i].cutoff)) p.box_never[a] = 1;
             if (th[i].dir == CDX_DIR_GE) p.box_lo[a][sg] = std::max(p.box_lo[a][sg], th[i].cutoff);
             else p.box_hi[a][sg] = std::min(p.box_hi[a][sg], th[i].cutoff);
         }
@@ -735,7 +773,9 @@ extern "C" int cdx_reward_certaindex(cdx_ctx* ctx, const float* rewards, const u
     p.ovf_list = ov + 16;
     cudaMemsetAsync(ov, 0, 64, ctx->stream);
 
-    bool tma = (W % 4 == 0) && reinterpret_cast<uintptr_t>(rewards) % 16 == 0 &&
+    // f64 rewards: every program through the warp-per-program kernel (left fold on lane 0)
+    const bool f64 = rewards64 != nullptr;
+    bool tma = !f64 && (W % 4 == 0) && reinterpret_cast<uintptr_t>(rewards) % 16 == 0 &&
                (!ids || reinterpret_cast<uintptr_t>(ids) % 16 == 0) && G < (1ull << 31);
     if (tma) {
         const uint64_t dims[3] = {W, T, G};
@@ -793,13 +833,13 @@ extern "C" int cdx_reward_certaindex(cdx_ctx* ctx, const float* rewards, const u
     const size_t smem = tma ? 1024 + static_cast<size_t>(p.stages) * (ids ? 2 : 1) * p.stage_bytes + 8 * RW_STAGES
                             : 0;
     const unsigned grid = static_cast<unsigned>((G + RW_PROGS - 1) / RW_PROGS);
-    if (!launched_quad) {
+    if (!launched_quad && !f64) {
         if (tma)
             cudaFuncSetAttribute(reward_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
         reward_kernel<<<grid, RW_PROGS, smem, ctx->stream>>>(p);
         CDX_CHECK_LAUNCH(ctx, "reward_certaindex");
     }
-    if (ids || launched_quad) {
+    if (ids || launched_quad || f64) {
         uint32_t cap_log2 = 1;
         while (ids && (1u << cap_log2) < 2u * T * W) ++cap_log2;
         // per-warp table: 2 * cap hash words + T*W counts; as many warps per CTA as fit
@@ -808,9 +848,19 @@ extern "C" int cdx_reward_certaindex(cdx_ctx* ctx, const float* rewards, const u
         if (per_warp <= limit) {
             const int warps = per_warp ? static_cast<int>(std::min<size_t>(OV_WARPS, limit / per_warp)) : OV_WARPS;
             const size_t osmem = std::max<size_t>(16u, warps * per_warp);
-            cudaFuncSetAttribute(reward_overflow_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 static_cast<int>(osmem));
-            reward_overflow_kernel<<<ctx->sm_count, warps * 32, osmem, ctx->stream>>>(p, cap_log2, nullptr);
+            if (f64) {
+                cudaFuncSetAttribute(reward_overflow_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     static_cast<int>(osmem));
+                const unsigned blocks = static_cast<unsigned>(
+                    std::min<uint64_t>((G + warps - 1) / warps, static_cast<uint64_t>(ctx->sm_count) * 32));
+                reward_overflow_kernel<double><<<blocks, warps * 32, osmem, ctx->stream>>>(p, cap_log2, nullptr,
+                                                                                           rewards64, 1u);
+            } else {
+                cudaFuncSetAttribute(reward_overflow_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     static_cast<int>(osmem));
+                reward_overflow_kernel<float><<<ctx->sm_count, warps * 32, osmem, ctx->stream>>>(p, cap_log2, nullptr,
+                                                                                                 rewards, 0u);
+            }
         } else {  // global-memory tables: up to ~256 MB of them, at least one warp
             uint64_t nwarps = std::max<uint64_t>(
                 1, std::min<uint64_t>(static_cast<uint64_t>(ctx->sm_count) * OV_WARPS, (256ull << 20) / per_warp));
@@ -819,12 +869,17 @@ extern "C" int cdx_reward_certaindex(cdx_ctx* ctx, const float* rewards, const u
             const unsigned blocks = static_cast<unsigned>(nwarps / wpb);
             auto* gtab = static_cast<uint32_t*>(scratch2(ctx, nwarps * per_warp));
             if (!gtab) return set_error(ctx, CDX_ECUDA, "reward_certaindex: overflow table allocation failed");
-            reward_overflow_kernel<<<blocks, wpb * 32, 16, ctx->stream>>>(p, cap_log2, gtab);
+            if (f64)
+                reward_overflow_kernel<double><<<blocks, wpb * 32, 16, ctx->stream>>>(p, cap_log2, gtab, rewards64, 1u);
+            else
+                reward_overflow_kernel<float><<<blocks, wpb * 32, 16, ctx->stream>>>(p, cap_log2, gtab, rewards, 0u);
         }
         CDX_CHECK_LAUNCH(ctx, "reward_certaindex(overflow)");
     }
     return CDX_OK;
 }
+}  // namespace
+}  // namespace cdx
 
 namespace cdx {
 namespace {
@@ -853,8 +908,8 @@ __global__ void reward_sets_kernel(const double* __restrict__ v, const uint64_t*
             out[r] = v[best];
         } else {
             double s = 0.0;
-            for (uint64_t i = b; i < e; ++i) s = __dadd_rn(s, v[i]);
-            out[r] = __ddiv_rn(s, static_cast<double>(e - b));
+            for (uint64_t i = b; i < e; ++i) s = x86_add(s, v[i]);  // NaN bits as the host's
+            out[r] = x86_div(s, static_cast<double>(e - b));
         }
     }
 }

@@ -18,6 +18,7 @@
 
 #include <climits>
 #include <cmath>
+#include <vector>
 
 #include "cdx_internal.cuh"
 
@@ -206,6 +207,24 @@ __global__ void entropy_one_kernel(const uint32_t* __restrict__ sizes, uint32_t 
     }
 }
 
+// one clustering with host-built per-cluster terms (any sizes, any total): fold in order
+__global__ void entropy_terms_kernel(const double* __restrict__ terms, uint32_t m, double log_n, int n_is_one,
+                                     double* H, double* Hc) {
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    double h = 0.0;
+    for (uint32_t k = 0; k < m; ++k) h = __dsub_rn(h, terms[k]);
+    h = (0.0 < h) ? h : 0.0;
+    if (H) *H = h;
+    if (Hc) {
+        double hc = 1.0;
+        if (!n_is_one) {
+            const double v = __ddiv_rn(__dsub_rn(log_n, h), log_n);
+            hc = v < 0.0 ? 0.0 : (1.0 < v ? 1.0 : v);
+        }
+        *Hc = hc;
+    }
+}
+
 // SPEC.md:431-439 estimate_iteration_tokens over ragged histories: exact i64 sum, one
 // IEEE division (the same arithmetic as K6's in-kernel estimate)
 __global__ void iteration_tokens_kernel(const int64_t* __restrict__ v, const uint64_t* __restrict__ row_off,
@@ -229,7 +248,7 @@ int check_probe_cfg(cdx_ctx* ctx, const cdx_probe_cfg* cfg) {
     // probe.cpp:19-25 ProbeConfig::validate, same messages
     if (cfg->interval_tokens < 1) return set_error(ctx, CDX_EINVAL, "probe: interval_tokens must be >= 1");
     if (cfg->window < 1) return set_error(ctx, CDX_EINVAL, "probe: window must be >= 1");
-    if (!(cfg->threshold > 0.0) || cfg->threshold > 1.0)
+    if (cfg->threshold <= 0.0 || cfg->threshold > 1.0)  // probe.cpp:22 (NaN passes)
         return set_error(ctx, CDX_EINVAL, "probe: threshold must be in (0,1]");
     if (cfg->max_tokens < 1) return set_error(ctx, CDX_EINVAL, "probe: max_tokens must be >= 1");
     return CDX_OK;
@@ -330,6 +349,29 @@ int cdx_entropy_one(cdx_ctx* ctx, const uint32_t* sizes, uint32_t m, uint32_t to
     entropy_one_kernel<<<1, 32, 0, ctx->stream>>>(sizes, m, total, tt.tab, std::log(static_cast<double>(total)), H,
                                                   Hcert, ctx->d_err);
     CDX_CHECK_LAUNCH(ctx, "entropy_one");
+    return CDX_OK;
+}
+
+int cdx_entropy_sizes_host(cdx_ctx* ctx, const int32_t* sizes, uint32_t m, int32_t total, double* H,
+                           double* Hcert) {
+    using namespace cdx;
+    if (!ctx) return CDX_EINVAL;
+    // metrics.cpp:108-112, in the reference's order: the clustering, then each cluster
+    if (total < 1 || m == 0) return set_error(ctx, CDX_EINVAL, "semantic_entropy: invalid clustering");
+    if (!sizes) return set_error(ctx, CDX_EINVAL, "entropy_sizes_host: null pointer");
+    std::vector<double> terms(m);
+    for (uint32_t k = 0; k < m; ++k) {
+        if (sizes[k] < 1) return set_error(ctx, CDX_EINVAL, "semantic_entropy: empty cluster");
+        terms[k] = host_term(static_cast<uint32_t>(sizes[k]), static_cast<uint32_t>(total));
+    }
+    double* d = static_cast<double*>(scratch2(ctx, static_cast<size_t>(m) * 8));
+    if (!d) return set_error(ctx, CDX_ECUDA, "entropy_sizes_host: scratch allocation failed");
+    cudaError_t e = cudaMemcpyAsync(d, terms.data(), static_cast<size_t>(m) * 8, cudaMemcpyHostToDevice, ctx->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);  // `terms` is pageable and local
+    if (e != cudaSuccess) return cuda_fail(ctx, e, "entropy_sizes_host");
+    entropy_terms_kernel<<<1, 32, 0, ctx->stream>>>(d, m, std::log(static_cast<double>(total)), total == 1 ? 1 : 0, H,
+                                                    Hcert);
+    CDX_CHECK_LAUNCH(ctx, "entropy_sizes_host");
     return CDX_OK;
 }
 

@@ -15,6 +15,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <exception>
+#include <limits>
 #include <sstream>
 #include <stdexcept>
 #include <string>
@@ -202,12 +203,9 @@ void random_cases(int count) {
             for (int k = 0; k < m; ++k) c.clusters.push_back({"c", static_cast<int>(below(9)) - (below(10) == 0 ? 1 : 0)});
             for (auto& cl : c.clusters) c.total += cl.size > 0 ? cl.size : 0;
             if (below(8) == 0) c.total = static_cast<int>(below(3));
-            bool oversized = false;
-            for (auto& cl : c.clusters) oversized |= cl.size > c.total;
-            if (!oversized) {  // p > 1 is outside the device term table (DESIGN.md deviation)
-                run("entropy " + id, [&] { return hex(metrics::semantic_entropy(c)); });
-                run("certaindex " + id, [&] { return hex(metrics::certaindex_entropy(c)); });
-            }
+            // includes clusters larger than the total (p > 1), which the reference computes
+            run("entropy " + id, [&] { return hex(metrics::semantic_entropy(c)); });
+            run("certaindex " + id, [&] { return hex(metrics::certaindex_entropy(c)); });
         }
         // reward sets
         {
@@ -281,6 +279,71 @@ void random_cases(int count) {
     }
 }
 
+// NaN / +-inf / -0.0 / subnormal inputs: every validation and comparison must take the
+// reference's branch (e.g. probe.cpp:22 accepts a NaN threshold, theory.cpp:119 a NaN epsilon,
+// metrics.cpp:131 a NaN reward, metrics.cpp:167 fails every compare against a NaN)
+void nonfinite_cases() {
+    const double nan = std::numeric_limits<double>::quiet_NaN(), inf = std::numeric_limits<double>::infinity();
+    const double den = std::numeric_limits<double>::denorm_min();
+    const std::vector<double> specials = {nan, -nan, inf, -inf, -0.0, 0.0, den, -den, 1.0, 0.5, 1.0 + 0x1p-52};
+    for (size_t a = 0; a < specials.size(); ++a) {
+        const std::string ta = std::to_string(a);
+        for (auto agg : {metrics::RewardAggregation::Mean, metrics::RewardAggregation::Max}) {
+            const std::string tg = agg == metrics::RewardAggregation::Max ? " max" : " mean";
+            run("nf reward " + ta + tg, [&] { return hex(metrics::certaindex_reward({{specials[a]}, agg})); });
+            run("nf reward mid " + ta + tg,
+                [&] { return hex(metrics::certaindex_reward({{0.25, specials[a], 0.75}, agg})); });
+            run("nf reward first " + ta + tg,
+                [&] { return hex(metrics::certaindex_reward({{specials[a], 0.25, 0.75}, agg})); });
+        }
+        for (size_t b = 0; b < specials.size(); ++b) {
+            metrics::SignalVector s;
+            s.certaindex_entropy = specials[a];
+            s.certaindex_reward = 0.5;
+            for (auto dir : {metrics::ThresholdDir::GreaterEq, metrics::ThresholdDir::LessEq}) {
+                std::vector<metrics::SignalThreshold> t = {{metrics::SignalKind::CertaindexEntropy, specials[b], dir},
+                                                           {metrics::SignalKind::CertaindexReward, 0.5}};
+                run("nf meets " + ta + " " + std::to_string(b) + " " + std::to_string(static_cast<int>(dir)),
+                    [&] { return std::to_string(metrics::combined_meets_thresholds(s, t)); });
+            }
+        }
+        probe::ProbeTrace tr;
+        const char* ans[] = {"a", "a", "b", "a", "a", "a"};
+        for (int i = 0; i < 6; ++i) tr.records.push_back({i + 1, 64L * (i + 1), ans[i], false});
+        probe::ProbeConfig cfg;
+        cfg.window = 3;
+        cfg.threshold = specials[a];
+        cfg.max_tokens = 300;
+        run("nf should_exit tau " + ta, [&] { return std::to_string(static_cast<int>(probe::should_exit(tr, cfg))); });
+        cfg.max_tokens = 1 << 20;
+        run("nf should_exit tau nobudget " + ta,
+            [&] { return std::to_string(static_cast<int>(probe::should_exit(tr, cfg))); });
+        run("nf validate " + ta, [&] {
+            cfg.validate();
+            return std::string("ok");
+        });
+        for (int k : {1, 2, 3}) {
+            run("nf eps " + ta + " k" + std::to_string(k), [&] {
+                auto e = probe::stationary_by_epsilon_test(tr.records, k, specials[a]);
+                return e ? std::to_string(*e) : std::string("nullopt");
+            });
+        }
+    }
+    // explicit clusterings with oversized clusters and large totals (metrics.cpp:107-125)
+    for (std::vector<int> sizes : {std::vector<int>{5, 1}, {3}, {7, 7, 7}, {100000000, 3}, {1, 1 << 30}, {2, -1}}) {
+        for (int total : {1, 2, 4, 1 << 28}) {
+            metrics::Clustering c;
+            for (int x : sizes) c.clusters.push_back({"c", x});
+            c.total = total;
+            std::string tag = "nf entropy";
+            for (int x : sizes) tag += " " + std::to_string(x);
+            tag += " /" + std::to_string(total);
+            run(tag + " H", [&] { return hex(metrics::semantic_entropy(c)); });
+            run(tag + " Hc", [&] { return hex(metrics::certaindex_entropy(c)); });
+        }
+    }
+}
+
 void jsonl_cases() {
     const std::vector<std::string> docs = {
         "{\"program_id\":\"p\",\"step_index\":1,\"token_offset\":64,\"answer\":\" 12 \",\"hesitant\":false}\n"
@@ -337,6 +400,7 @@ int main(int argc, char** argv) {
     const int count = argc > 1 ? std::atoi(argv[1]) : 400;
     spec_examples();
     random_cases(count);
+    nonfinite_cases();
     jsonl_cases();
     return 0;
 }

@@ -137,7 +137,9 @@ int main(int argc, char** argv) {
         double t = 0.0;
         for (int i = 0; i < n; ++i) {
             auto& s = p[static_cast<size_t>(i)];
-            s.program_id = static_cast<uint32_t>(i);
+            // odd cases: shuffled, sparse program ids (the tie-break is the id, not the position)
+            s.program_id = c % 2 ? static_cast<uint32_t>(i) * 7919u % 100003u + 11u * static_cast<uint32_t>(c)
+                                 : static_cast<uint32_t>(i);
             t += below(3) == 0 ? 0.0 : static_cast<double>(below(1000)) * 0x1p-10;  // ties on arrival
             s.arrival = below(5) == 0 ? static_cast<double>(below(8)) : t;
             s.last_service = static_cast<double>(below(64)) * 0x1p-3;
@@ -155,9 +157,9 @@ int main(int argc, char** argv) {
                            std::to_string(static_cast<int>(pol.order)) + " " + std::to_string(pol.starvation_limit) + " |";
         for (const auto& s : p) {
             char b[160];
-            std::snprintf(b, sizeof b, " %a,%a,%lld,%u,%d,%d,%d", s.arrival, s.last_service,
+            std::snprintf(b, sizeof b, " %a,%a,%lld,%u,%d,%d,%d,%u", s.arrival, s.last_service,
                           static_cast<long long>(s.iteration_token_sum), s.iteration_count, s.knob, s.resource_cap,
-                          s.terminated ? 1 : 0);
+                          s.terminated ? 1 : 0, s.program_id);
             line += b;
         }
         line += " |";

@@ -3,8 +3,9 @@
 CPU: the C restatement (oracle/cdx_oracle.c) is pinned against the reference's own
 aggregate_prefix, called through oracle/_ref on injected SC / MCTS / Rebase paths, plus the
 SPEC examples.  GPU: cdx_sc_aggregate / cdx_reward_aggregate must equal the restatement
-bit-for-bit (answer ids) at the BASELINE shapes; the Rebase exp() weights must be the host
-libm's (no off-grid rewards on the synthetic traces: the inexact counter stays 0).
+bit-for-bit (answer ids) at the BASELINE shapes; the Rebase exp() weights are the host
+libm's bits for every reward (libm_exp.cuh), so off-grid f32 and f64 rewards (a reward
+model's outputs), NaN and out-of-range rewards included, give the reference's answers.
 """
 import numpy as np
 import pytest
@@ -62,6 +63,31 @@ def test_oracle_aggregation_pinned_to_reference(seed):
         assert got[g] == want, (g, arche)
 
 
+@pytest.mark.parametrize("seed", range(4))
+def test_oracle_aggregation_off_grid_doubles_pinned_to_reference(seed):
+    """Arbitrary double rewards (reward-model outputs), near-ties, NaN and out-of-range
+    values: the f64 restatement equals the reference's aggregate_prefix, the empty-string
+    answer of an all-NaN Rebase layer included (CDX_NO_ANSWER)."""
+    _ref_or_skip()
+    rng = np.random.default_rng(100 + seed)
+    G, T, W = 40, 4, 6
+    rw = rng.random((G, T, W))
+    rw[::3] = np.round(rw[::3] * 4) / 4 + rng.integers(-2, 3, size=rw[::3].shape) * 2.0 ** -52  # near-ties
+    rw[5, :, 1] = np.nan
+    rw[7] = np.nan
+    rw[9, :, :2] = [-3.5, 7.25]
+    rid = rng.integers(0, 4, size=(G, T, W)).astype(np.uint32)
+    agg = (np.arange(G) % 2).astype(np.uint8)
+    ex = rng.integers(0, T, size=G).astype(np.int32)
+    got = O.reward_aggregate(rw, rid, agg, ex)
+    for g in range(G):
+        n = (ex[g] + 1) * W
+        arche = MCTS if agg[g] == 0 else REBASE
+        want = O.ref_aggregate(arche, rid[g].ravel()[:n].tolist(), rw[g].ravel()[:n].tolist(),
+                               [W] * int(ex[g] + 1), n, VOC)
+        assert got[g] == want, (g, arche)
+
+
 @pytest.mark.gpu
 @pytest.mark.parametrize("R,P,S", [(1, 1, 1), (1000, 64, 32), (257, 32, 16), (64, 8, 5)])
 def test_sc_aggregate_gpu(ctx, R, P, S):
@@ -92,14 +118,51 @@ def test_reward_aggregate_gpu(ctx, G, T, W):
 
 
 @pytest.mark.gpu
-def test_reward_aggregate_off_grid_is_counted(ctx):
+@pytest.mark.parametrize("dtype", [np.float32, np.float64])
+def test_reward_aggregate_off_grid_exact(ctx, dtype):
+    """Off-grid rewards with near-tied Rebase weights: the device exp is the host libm's, so
+    the vote equals the oracle's (host std::exp) for f32 and f64 rewards alike."""
     import torch
-    rw = np.full((2, 1, 4), 0.1, np.float32)  # 0.1f is not a multiple of 2^-24
-    ids = np.array([[[0, 1, 1, 0]], [[2, 2, 3, 3]]], np.uint32)
-    agg = np.array([1, 1], np.uint8)
-    ex = np.zeros(2, np.int32)
+    rng = np.random.default_rng(7)
+    G, T, W = 20000, 3, 24
+    rw = rng.random((G, T, W)).astype(dtype)
+    rw[::4] = (np.round(rw[::4] * 8) / 8 + rng.integers(-3, 4, size=rw[::4].shape) *
+               np.finfo(dtype).eps).astype(dtype)  # weight sums that differ in the last bits
+    rw[11, :, 3] = np.nan
+    rw[13] = np.nan  # all-NaN layer: no winner (the reference's empty string)
+    ids = rng.integers(0, 3, size=(G, T, W)).astype(np.uint32)
+    agg = (np.arange(G) % 2).astype(np.uint8)
+    ex = rng.integers(0, T, size=G).astype(np.int32)
     ans, inexact = ctx.reward_aggregate(torch.from_numpy(rw).cuda(), torch.from_numpy(ids.view(np.int32)).cuda(),
                                         torch.from_numpy(agg).cuda(), torch.from_numpy(ex).cuda())
     ctx.sync()
-    assert int(inexact) == 8
-    assert ans.cpu().numpy().tolist() == [0, 2]  # equal weights: earliest-seen cluster
+    assert int(inexact) == 0
+    want = O.reward_aggregate(rw, ids, agg, ex)
+    assert want[13] == 0xFFFFFFFF
+    assert np.array_equal(ans.cpu().numpy().view(np.uint32), want)
+
+
+@pytest.mark.gpu
+def test_device_exp_is_host_libm_exp(ctx):
+    """cdx_libm_exp vs this box's own std::exp (numpy's exp is not libm's: use math.exp,
+    which is the C library's) on rewards in [0,1], the whole finite range and specials."""
+    import math
+    import struct
+
+    import torch
+    rng = np.random.default_rng(3)
+    xs = np.concatenate([rng.random(1 << 20), rng.uniform(-760, 720, 1 << 20),
+                         rng.integers(0, 1 << 63, 1 << 18, dtype=np.int64).view(np.float64),
+                         np.array([0.0, -0.0, 1.0, -1.0, np.inf, -np.inf, np.nan, 709.78, 709.79, -745.13, -745.2,
+                                   -708.4, 2.0 ** -54, 2.0 ** -55, 512.0, -512.0, 1024.0, -1024.0, 5e-324])])
+    got = ctx.libm_exp(torch.from_numpy(xs).cuda()).cpu().numpy()
+
+    def host(x):
+        try:
+            return math.exp(x)
+        except OverflowError:
+            return math.inf
+    want = np.array([host(float(x)) for x in xs])
+    same = (got.view(np.uint64) == want.view(np.uint64)) | (np.isnan(got) & np.isnan(want))
+    bad = np.flatnonzero(~same)
+    assert bad.size == 0, [(struct.pack("<d", xs[i]).hex(), got[i], want[i]) for i in bad[:5]]

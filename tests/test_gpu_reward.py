@@ -198,3 +198,41 @@ def test_reward_entropy_all_partitions(ctx, n):
     _, R32, Ho = O.reward_certaindex(rw, ids, agg)
     assert np.array_equal(H.view(np.uint32), Ho.view(np.uint32))
     assert np.array_equal(R.view(np.uint32), R32.view(np.uint32))
+
+
+@pytest.mark.parametrize("G,T,W", [(1, 1, 1), (513, 16, 64), (77, 9, 13), (20, 40, 128)])
+def test_reward_f64_rewards_match_reference(ctx, G, T, W):
+    """cdx_reward_certaindex_f64: RewardSet holds doubles (metrics.hpp:74-77); arbitrary
+    off-grid doubles, subnormals, -0.0 and NaN are folded in the reference's order and the
+    thresholds see the FP64 values.  R / H~ stores and meets bits equal the oracle's."""
+    rng = np.random.default_rng(G + T * W)
+    rw = rng.random((G, T, W))
+    rw[0, 0, 0] = 5e-324
+    if G > 3:
+        rw[1, :, 0] = -0.0
+        rw[2, T - 1, W - 1] = np.nan
+        rw[3] = np.round(rw[3] * 4) / 4  # exact threshold hits on R
+    ids = rng.integers(0, 6, size=(G, T, W)).astype(np.uint32)
+    if G > 5:
+        ids[5] = rng.integers(0, 1 << 30, size=(T, W))  # many clusters
+    agg = (np.arange(G) % 2).astype(np.uint8)
+    th_mean = [(0, 0.3, 0), (1, 0.5, 0)]
+    th_max = [(1, 0.75, 0), (0, 0.2, 0)]
+    R, H, meets = _run(ctx, rw, ids, agg, th_mean, th_max)
+    R64, R32, Ho, H64o = O.reward_certaindex(rw, ids, agg, want_h64=True)
+    assert np.array_equal(R.view(np.uint32), R32.view(np.uint32))
+    assert np.array_equal(H.view(np.uint32), Ho.view(np.uint32))
+    global H64
+    H64 = H64o
+    assert np.array_equal(meets, _oracle_meets(R64, H64o, agg, th_mean, th_max))
+
+
+def test_reward_nan_cutoff_fails_every_compare(ctx):
+    """A NaN cutoff: `v >= NaN` is false (metrics.cpp:167), so nothing meets it, on both
+    the quad and the f64 path."""
+    g = O.gen_params(seed=5, conv_hi=8)
+    rw, ids = O.gen_reward(g, 256, 8, 64)
+    agg = (np.arange(256) % 2).astype(np.uint8)
+    for arr in (rw, rw.astype(np.float64)):
+        _, _, meets = _run(ctx, arr, ids, agg, [(1, float("nan"), 0)], [(0, float("nan"), 1)])
+        assert not meets.any()

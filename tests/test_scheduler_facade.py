@@ -58,6 +58,9 @@ def test_scheduler_facade_spec_and_random_orders():
         _, _, n, order_kind, limit = head.split()
         rows = [r.split(",") for r in inputs.split()]
         assert len(rows) == int(n)
+        # the last tie-break is the program id; the SPEC restatement breaks it by
+        # position, so hand it the programs in id order and read the ids back
+        rows.sort(key=lambda r: int(r[7]))
         soa = dict(arrival=np.array([float.fromhex(r[0]) for r in rows]),
                    last_service=np.array([float.fromhex(r[1]) for r in rows]),
                    iter_tok_sum=np.array([int(r[2]) for r in rows], np.int64),
@@ -66,6 +69,6 @@ def test_scheduler_facade_spec_and_random_orders():
                    cap=np.array([int(r[5]) for r in rows], np.uint16),
                    terminated=np.array([int(r[6]) for r in rows], np.uint8))
         ref, _ = O.gang_order(soa, int(order_kind), float(limit), 128.0, 8.0)
-        assert [int(x) for x in ids.split()] == ref.tolist(), head
+        assert [int(x) for x in ids.split()] == [int(rows[i][7]) for i in ref.tolist()], head
         checked += 1
     assert checked == 40
