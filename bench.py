@@ -249,8 +249,8 @@ def gang_inputs(N, seed, limit):
     last = np.maximum(last, 0.0)
     cnt = rng.integers(0, 6, N).astype(np.uint32)
     sums = (rng.integers(32, 1024, N) * cnt).astype(np.int64)
-    cap = rng.integers(4, 64, N).astype(np.uint16)
-    knob = np.minimum(cap, rng.integers(0, 64, N)).astype(np.uint16)
+    cap = rng.integers(4, 64, N).astype(np.int32)
+    knob = np.minimum(cap, rng.integers(0, 64, N)).astype(np.int32)
     arche = rng.random(N)  # 40% SC / 40% CoT / 20% MCTS: terminated by B/C/D-style exits
     term = (rng.random(N) < np.where(arche < 0.4, 0.3, np.where(arche < 0.8, 0.2, 0.1))).astype(np.uint8)
     return dict(arrival=arrival, last_service=last, iter_tok_sum=sums, iter_count=cnt, knob=knob, cap=cap,

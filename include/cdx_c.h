@@ -30,7 +30,7 @@
 extern "C" {
 #endif
 
-#define CDX_ABI_VERSION 2
+#define CDX_ABI_VERSION 3
 
 typedef enum {
     CDX_OK = 0,
@@ -106,10 +106,11 @@ typedef struct {
     const double* last_service;   /* last time the program was serviced */
     const int64_t* iter_tok_sum;  /* sum of completed iteration token counts */
     const uint32_t* iter_count;   /* number of completed iterations */
-    const uint16_t* knob;         /* units granted so far */
-    const uint16_t* cap;          /* resource cap */
+    const int32_t* knob;          /* units granted so far (ReasoningProgram::knob, int) */
+    const int32_t* cap;           /* resource cap (ReasoningProgram::resource_cap, int) */
     const uint8_t* terminated;    /* nonzero: dropped from the order */
-    uint32_t id_base;             /* program id = id_base + index */
+    const uint32_t* program_id;   /* nullable: program id = id_base + index (the last tie-break) */
+    uint32_t id_base;
     uint32_t _pad;
 } cdx_prog_soa;
 

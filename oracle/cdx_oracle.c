@@ -637,13 +637,13 @@ int cdxo_gang_order(const cdx_prog_soa* s, uint64_t N, const cdx_inter_policy* p
             /* SJF estimated remaining work = est tokens/iter x remaining knob, :425,469 */
             const double est = cdxo_estimate_iteration_tokens(s->iter_tok_sum[i], s->iter_count[i],
                                                               pol->prior_tokens);
-            const int rem = (int)s->cap[i] - (int)s->knob[i];
+            const int64_t rem = (int64_t)s->cap[i] - (int64_t)s->knob[i];
             key = est * (double)(rem > 0 ? rem : 0);
         }
         it[n].esc = esc;
         it[n].key = key;
         it[n].arrival = s->arrival[i];
-        it[n].id = s->id_base + (uint32_t)i;
+        it[n].id = s->program_id ? s->program_id[i] : s->id_base + (uint32_t)i;
         ++n;
     }
     qsort(it, n, sizeof(gang_item), gang_cmp); /* total order => unique result */

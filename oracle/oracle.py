@@ -42,7 +42,7 @@ class InterPolicy(C.Structure):
 
 class ProgSoA(C.Structure):
     _fields_ = [("arrival", P), ("last_service", P), ("iter_tok_sum", P), ("iter_count", P), ("knob", P),
-                ("cap", P), ("terminated", P), ("id_base", C.c_uint32), ("_pad", C.c_uint32)]
+                ("cap", P), ("terminated", P), ("program_id", P), ("id_base", C.c_uint32), ("_pad", C.c_uint32)]
 
 
 class GenParams(C.Structure):
@@ -246,9 +246,12 @@ def gang_order(soa, order_kind, starvation_limit, prior, now, id_base=0):
     s = ProgSoA()
     keep = {}
     for k, dt in (("arrival", np.float64), ("last_service", np.float64), ("iter_tok_sum", np.int64),
-                  ("iter_count", np.uint32), ("knob", np.uint16), ("cap", np.uint16), ("terminated", np.uint8)):
+                  ("iter_count", np.uint32), ("knob", np.int32), ("cap", np.int32), ("terminated", np.uint8)):
         keep[k] = np.ascontiguousarray(soa[k], dtype=dt)
         setattr(s, k, keep[k].ctypes.data)
+    if soa.get("program_id") is not None:
+        keep["program_id"] = np.ascontiguousarray(soa["program_id"], dtype=np.uint32)
+        s.program_id = keep["program_id"].ctypes.data
     s.id_base = id_base
     pol = InterPolicy()
     pol.gang, pol.order, pol.starvation_limit, pol.prior_tokens = 1, order_kind, starvation_limit, prior

@@ -349,6 +349,8 @@ class Context:
         s = _abi.ProgSoA()
         for k in ("arrival", "last_service", "iter_tok_sum", "iter_count", "knob", "cap", "terminated"):
             setattr(s, k, soa[k].data_ptr())
+        if soa.get("program_id") is not None:  # explicit ids (u32 stored in an int32 tensor)
+            s.program_id = soa["program_id"].data_ptr()
         s.id_base = id_base
         order = self.empty((max(N, 1),), t.int32)
         esc = self.empty((max(N, 1),), t.uint8) if want_escalated else None

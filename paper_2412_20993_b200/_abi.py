@@ -45,7 +45,8 @@ class InterPolicy(C.Structure):
 class ProgSoA(C.Structure):
     _fields_ = [("arrival", C.c_void_p), ("last_service", C.c_void_p), ("iter_tok_sum", C.c_void_p),
                 ("iter_count", C.c_void_p), ("knob", C.c_void_p), ("cap", C.c_void_p),
-                ("terminated", C.c_void_p), ("id_base", C.c_uint32), ("_pad", C.c_uint32)]
+                ("terminated", C.c_void_p), ("program_id", C.c_void_p), ("id_base", C.c_uint32),
+                ("_pad", C.c_uint32)]
 
 
 class GenParams(C.Structure):

@@ -35,58 +35,52 @@ struct DeviceSoA {
     batch::DeviceArray<double> arrival, last;
     batch::DeviceArray<int64_t> sum;
     batch::DeviceArray<uint32_t> count;
-    batch::DeviceArray<uint16_t> knob, cap;
+    batch::DeviceArray<int32_t> knob, cap;
     batch::DeviceArray<uint8_t> term;
+    batch::DeviceArray<uint32_t> id;
     cdx_prog_soa soa{};
 };
 
-// ProgramState list -> device SoA in `idx` order (device index i = ps[idx[i]]); program ids
-// are attached after ordering.
-DeviceSoA upload(batch::Context& cx, std::span<const ProgramState> all, const std::vector<uint32_t>& idx) {
-    const size_t n = idx.size();
-    auto ps = [&](size_t i) -> const ProgramState& { return all[idx[i]]; };
+// ProgramState list -> device SoA in input order, with the program ids (the last tie-break,
+// SPEC.md:470) as an explicit id array.
+DeviceSoA upload(batch::Context& cx, std::span<const ProgramState> ps) {
+    const size_t n = ps.size();
     std::vector<double> a(n), l(n);
     std::vector<int64_t> s(n);
-    std::vector<uint32_t> c(n);
-    std::vector<uint16_t> k(n), cap(n);
+    std::vector<uint32_t> c(n), id(n);
+    std::vector<int32_t> k(n), cap(n);
     std::vector<uint8_t> t(n);
     for (size_t i = 0; i < n; ++i) {
-        if (ps(i).knob < 0 || ps(i).knob > 0xffff || ps(i).resource_cap < 0 || ps(i).resource_cap > 0xffff)
-            throw std::invalid_argument("next_batch: knob and resource_cap must be in [0, 65535]");
-        a[i] = ps(i).arrival;
-        l[i] = ps(i).last_service;
-        s[i] = ps(i).iteration_token_sum;
-        c[i] = ps(i).iteration_count;
-        k[i] = static_cast<uint16_t>(ps(i).knob);
-        cap[i] = static_cast<uint16_t>(ps(i).resource_cap);
-        t[i] = ps(i).terminated ? 1 : 0;
+        a[i] = ps[i].arrival;
+        l[i] = ps[i].last_service;
+        s[i] = ps[i].iteration_token_sum;
+        c[i] = ps[i].iteration_count;
+        k[i] = ps[i].knob;
+        cap[i] = ps[i].resource_cap;
+        t[i] = ps[i].terminated ? 1 : 0;
+        id[i] = ps[i].program_id;
     }
     DeviceSoA d;
     d.arrival = batch::DeviceArray<double>(cx, std::span<const double>(a));
     d.last = batch::DeviceArray<double>(cx, std::span<const double>(l));
     d.sum = batch::DeviceArray<int64_t>(cx, std::span<const int64_t>(s));
     d.count = batch::DeviceArray<uint32_t>(cx, std::span<const uint32_t>(c));
-    d.knob = batch::DeviceArray<uint16_t>(cx, std::span<const uint16_t>(k));
-    d.cap = batch::DeviceArray<uint16_t>(cx, std::span<const uint16_t>(cap));
+    d.knob = batch::DeviceArray<int32_t>(cx, std::span<const int32_t>(k));
+    d.cap = batch::DeviceArray<int32_t>(cx, std::span<const int32_t>(cap));
     d.term = batch::DeviceArray<uint8_t>(cx, std::span<const uint8_t>(t));
+    d.id = batch::DeviceArray<uint32_t>(cx, std::span<const uint32_t>(id));
     d.soa = {d.arrival.data(), d.last.data(), d.sum.data(), d.count.data(), d.knob.data(), d.cap.data(),
-             d.term.data(), 0, 0};
+             d.term.data(), d.id.data(), 0, 0};
     return d;
 }
 
-// order (indices into ps) and escalation flags from K6
+// order (program ids) and escalation flags from K6
 std::pair<std::vector<uint32_t>, std::vector<uint8_t>> order_of(std::span<const ProgramState> ps,
                                                                 const InterSchedPolicy& pol, double now,
                                                                 bool want_esc) {
     if (ps.empty()) return {};
     auto& cx = detail::scalar_ctx();
-    // K6 breaks the last tie by device index (SPEC.md:470 says program id): hand it the
-    // programs in program-id order (stable, so equal ids keep input order) and map back
-    std::vector<uint32_t> by_id(ps.size());
-    for (size_t i = 0; i < ps.size(); ++i) by_id[i] = static_cast<uint32_t>(i);
-    std::stable_sort(by_id.begin(), by_id.end(),
-                     [&](uint32_t a, uint32_t b) { return ps[a].program_id < ps[b].program_id; });
-    auto d = upload(cx, ps, by_id);
+    auto d = upload(cx, ps);
     batch::DeviceArray<uint32_t> order(cx, ps.size());
     batch::DeviceArray<uint8_t> esc;
     if (want_esc) esc = batch::DeviceArray<uint8_t>(cx, ps.size());
@@ -94,13 +88,8 @@ std::pair<std::vector<uint32_t>, std::vector<uint8_t>> order_of(std::span<const 
                                             want_esc ? esc.data() : nullptr, nullptr);
     auto o = order.download();
     o.resize(n);
-    for (auto& x : o) x = by_id[x];  // device index -> input index
     std::vector<uint8_t> e;
-    if (want_esc) {
-        const auto ed = esc.download();
-        e.assign(ps.size(), 0);
-        for (size_t i = 0; i < ps.size(); ++i) e[by_id[i]] = ed[i];
-    }
+    if (want_esc) e = esc.download();
     return {o, e};
 }
 
@@ -200,11 +189,7 @@ std::vector<bool> escalate(std::span<const ProgramState> programs, double now, d
 
 std::vector<uint32_t> program_order(std::span<const ProgramState> programs, const InterSchedPolicy& policy,
                                     double now) {
-    auto [o, e] = order_of(programs, policy, now, false);
-    std::vector<uint32_t> ids;
-    ids.reserve(o.size());
-    for (uint32_t i : o) ids.push_back(programs[i].program_id);
-    return ids;
+    return order_of(programs, policy, now, false).first;
 }
 
 std::vector<Request> next_batch(std::span<const Request> ready, std::span<const ProgramState> programs,

@@ -41,9 +41,10 @@ struct GangParams {
     const double* last_service;
     const int64_t* iter_tok_sum;
     const uint32_t* iter_count;
-    const uint16_t* knob;
-    const uint16_t* cap;
+    const int32_t* knob;
+    const int32_t* cap;
     const uint8_t* terminated;
+    const uint32_t* program_id;  // nullable: id_base + index
     uint8_t* escalated;
     uint64_t N;
     uint32_t id_base;
@@ -161,7 +162,7 @@ __global__ void __launch_bounds__(GP_THREADS, 6) gang_prepare(const GangParams p
     const uint32_t tile = blockIdx.x;
     const uint64_t base = static_cast<uint64_t>(tile) * GP_TILE;
     uint64_t hk[GP_ITEMS], ak[GP_ITEMS];
-    uint32_t rank[GP_ITEMS];
+    uint32_t rank[GP_ITEMS], ids[GP_ITEMS];
     bool lv[GP_ITEMS];
     bool bad = false, unsorted = false;
 #pragma unroll
@@ -172,12 +173,17 @@ __global__ void __launch_bounds__(GP_THREADS, 6) gang_prepare(const GangParams p
             // every field is loaded up front (one memory round trip per item, not two)
             const double a = __ldg(p.arrival + i), ls = __ldg(p.last_service + i);
             const double an = i + 1 < p.N ? __ldg(p.arrival + i + 1) : a;
+            const uint32_t id = p.program_id ? __ldg(p.program_id + i) : p.id_base + static_cast<uint32_t>(i);
+            const uint32_t idn = p.program_id && i + 1 < p.N ? __ldg(p.program_id + i + 1) : id + 1u;
+            ids[j] = id;
             const int64_t sum = __ldg(p.iter_tok_sum + i);
             const uint32_t c = __ldg(p.iter_count + i);
-            const int rem = static_cast<int>(__ldg(p.cap + i)) - static_cast<int>(__ldg(p.knob + i));
+            const int64_t rem = static_cast<int64_t>(__ldg(p.cap + i)) - static_cast<int64_t>(__ldg(p.knob + i));
             live = __ldg(p.terminated + i) == 0;
             bad = bad || !(a >= 0.0) || !(ls >= 0.0) || isinf(a) || isinf(ls);
-            unsorted = unsorted || a > an;
+            // index order is the (arrival, id) order unless arrivals descend or, with explicit
+            // ids, an equal arrival is followed by a smaller id
+            unsorted = unsorted || a > an || (a == an && idn <= id);
             const bool esc = (p.now - ls) >= p.limit;  // inclusive escalation
             if (p.escalated) p.escalated[i] = esc ? 1 : 0;
             double key;
@@ -225,10 +231,10 @@ __global__ void __launch_bounds__(GP_THREADS, 6) gang_prepare(const GangParams p
         const uint32_t pos = s_excl + s_cnt[j * (GP_THREADS / 32) + warp] + rank[j];
         khi[pos] = hk[j];
         if (lean) {  // the sort carries the program id itself; arrival keys are not needed
-            perm[pos] = p.id_base + static_cast<uint32_t>(i);
+            perm[pos] = ids[j];
         } else {
             karr[pos] = ak[j];
-            kid[pos] = p.id_base + static_cast<uint32_t>(i);
+            kid[pos] = ids[j];
             perm[pos] = pos;
         }
     }
@@ -497,6 +503,12 @@ __global__ void __launch_bounds__(RS_THREADS, 2)
         os_tile<true, LB_WIN>(kin, vin, kout, vout, n, shift, ghist, look, tile, rs2_smem, vmap);
     else
         os_tile<false, LB_WIN>(kin, vin, kout, vout, n, shift, ghist, look, tile, rs2_smem, vmap);
+}
+
+__global__ void widen_u32(const uint32_t* __restrict__ src, uint64_t* __restrict__ dst, uint64_t n) {
+    for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<uint64_t>(gridDim.x) * blockDim.x)
+        dst[i] = src[i];
 }
 
 template <typename T>
@@ -881,7 +893,7 @@ int gang_priority_run(cdx_ctx* ctx, const cdx_prog_soa* progs, uint64_t N, const
     *redo = GANG_FAST;
     const bool full = mode == GANG_FULL;
     GangParams p{progs->arrival, progs->last_service, progs->iter_tok_sum, progs->iter_count, progs->knob,
-                 progs->cap, progs->terminated, escalated, N, progs->id_base, pol->order, now,
+                 progs->cap, progs->terminated, progs->program_id, escalated, N, progs->id_base, pol->order, now,
                  pol->starvation_limit, pol->prior_tokens};
     const uint32_t ntiles = static_cast<uint32_t>((N + RS_TILE - 1) / RS_TILE);
     const uint32_t gtiles = static_cast<uint32_t>((N + GP_TILE - 1) / GP_TILE);
@@ -966,7 +978,19 @@ int gang_priority_run(cdx_ctx* ctx, const cdx_prog_soa* progs, uint64_t N, const
     // 1) (arrival, id): programs are compacted in id order, so a stable sort on arrival
     //    bits yields the tie-break order; skipped when arrivals are non-decreasing.
     uint32_t* p1 = va;  // permutation: position -> compacted index (identity from prepare)
-    if (hm[1]) {
+    if (hm[1] && progs->program_id) {
+        // explicit ids: stable sort by id, then stably by arrival bits -> (arrival, id) order
+        widen_u32<<<L.grid(n), 256, 0, ctx->stream>>>(kid, t0, n);
+        CDX_CHECK_LAUNCH(ctx, "gang_priority(ids)");
+        int which = 0;
+        if (int st = radix_sort(ctx, t0, va, t1, vb, n, hist, &which, nullptr, nullptr, nullptr)) return st;
+        uint32_t* by_id = which ? vb : va;
+        uint32_t* other = which ? va : vb;
+        gather<uint64_t><<<L.grid(n), 256, 0, ctx->stream>>>(karr, by_id, t0, n);
+        CDX_CHECK_LAUNCH(ctx, "gang_priority(gather)");
+        if (int st = radix_sort(ctx, t0, by_id, t1, other, n, hist, &which, nullptr, nullptr, nullptr)) return st;
+        p1 = which ? other : by_id;  // va or vb; the hi sort below ping-pongs it with perm
+    } else if (hm[1]) {
         cudaMemcpyAsync(t0, karr, n * 8, cudaMemcpyDeviceToDevice, ctx->stream);
         int which = 0;
         if (int st = radix_sort(ctx, t0, va, t1, vb, n, hist, &which, nullptr, nullptr, nullptr)) return st;

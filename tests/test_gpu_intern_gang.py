@@ -64,8 +64,8 @@ def _gang_inputs(N, seed, frac_term=0.1, sorted_arrival=True):
     last = np.minimum(now, arrival + rng.exponential(0.5, N))
     cnt = rng.integers(0, 5, N).astype(np.uint32)
     sums = (rng.integers(32, 512, N) * cnt).astype(np.int64)
-    cap = rng.integers(1, 64, N).astype(np.uint16)
-    knob = np.minimum(cap, rng.integers(0, 64, N)).astype(np.uint16)
+    cap = rng.integers(1, 64, N).astype(np.int32)
+    knob = np.minimum(cap, rng.integers(0, 64, N)).astype(np.int32)
     term = (rng.random(N) < frac_term).astype(np.uint8)
     return dict(arrival=arrival, last_service=last, iter_tok_sum=sums, iter_count=cnt, knob=knob, cap=cap,
                 terminated=term), now
@@ -89,6 +89,36 @@ def test_gang_parity(ctx, N, order, limit, sorted_arrival):
                                     now, want_escalated=True)
     ctx.sync()
     ref, resc = O.gang_order(soa, order, limit, 128.0, now)
+    assert np.array_equal(esc.cpu().numpy(), resc)
+    assert np.array_equal(got.cpu().numpy().view(np.uint32), ref)
+
+
+@pytest.mark.parametrize("N,sorted_arrival,mode", [(5000, True, None), (100000, True, None), (100000, False, None),
+                                                   (70001, True, "checked"), (70001, False, "full"), (1, True, None)])
+def test_gang_explicit_program_ids(ctx, monkeypatch, N, sorted_arrival, mode):
+    """cdx_prog_soa.program_id: the last tie-break is the program id, not the
+    position.  Shuffled sparse ids with runs of equal arrivals (and identical keys) must come
+    out in (escalated, key, arrival, id) order on every path (fast, checked, full)."""
+    import torch
+    from paper_2412_20993_b200 import InterPolicy
+    if mode:
+        monkeypatch.setenv("CDX_GANG_MODE", mode)
+    soa, now = _gang_inputs(N, 77 + N, sorted_arrival=sorted_arrival)
+    rng = np.random.default_rng(N)
+    if N > 1:
+        soa["arrival"] = np.sort(soa["arrival"]) if sorted_arrival else soa["arrival"]
+        soa["arrival"][1::3] = soa["arrival"][0::3][: len(soa["arrival"][1::3])]  # equal-arrival pairs
+        if sorted_arrival:
+            soa["arrival"] = np.maximum.accumulate(soa["arrival"])
+        soa["iter_tok_sum"][::2] = 0
+        soa["iter_count"][::2] = 0  # prior estimate: many identical SJF keys
+    ids = rng.permutation(np.arange(N, dtype=np.uint64) * 7 + 3).astype(np.uint32)
+    soa["program_id"] = ids
+    dev = _to_dev(soa)
+    got, esc, _ = ctx.gang_priority(dev, InterPolicy(order=1, starvation_limit=0.5, prior_tokens=128.0), now,
+                                    want_escalated=True)
+    ctx.sync()
+    ref, resc = O.gang_order(soa, 1, 0.5, 128.0, now)
     assert np.array_equal(esc.cpu().numpy(), resc)
     assert np.array_equal(got.cpu().numpy().view(np.uint32), ref)
 

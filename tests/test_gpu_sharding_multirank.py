@@ -38,10 +38,10 @@ def _soa():
     arrival = np.cumsum(rng.exponential(1e-3, N_PROG))
     now = float(arrival.max()) + 1e-3
     cnt = rng.integers(0, 5, N_PROG).astype(np.uint32)
-    cap = rng.integers(1, 40, N_PROG).astype(np.uint16)
+    cap = rng.integers(1, 40, N_PROG).astype(np.int32)
     soa = dict(arrival=arrival, last_service=np.maximum(now - rng.exponential(0.2, N_PROG), 0.0),
                iter_tok_sum=(rng.integers(1, 500, N_PROG) * cnt).astype(np.int64), iter_count=cnt, cap=cap,
-               knob=np.minimum(cap, rng.integers(0, 40, N_PROG)).astype(np.uint16),
+               knob=np.minimum(cap, rng.integers(0, 40, N_PROG)).astype(np.int32),
                terminated=(rng.random(N_PROG) < 0.2).astype(np.uint8))
     return soa, now
 

@@ -49,8 +49,8 @@ def test_sc_decide_and_gang_order_through_nccl(ctx, nccl):
     cnt = rng.integers(0, 5, N).astype(np.uint32)
     soa = dict(arrival=arrival, last_service=np.maximum(now - rng.exponential(0.2, N), 0.0),
                iter_tok_sum=(rng.integers(1, 500, N) * cnt).astype(np.int64), iter_count=cnt,
-               cap=rng.integers(1, 30, N).astype(np.uint16), terminated=(rng.random(N) < 0.2).astype(np.uint8))
-    soa["knob"] = np.minimum(soa["cap"], rng.integers(0, 30, N)).astype(np.uint16)
+               cap=rng.integers(1, 30, N).astype(np.int32), terminated=(rng.random(N) < 0.2).astype(np.uint8))
+    soa["knob"] = np.minimum(soa["cap"], rng.integers(0, 30, N)).astype(np.int32)
     dev = {k: (torch.from_numpy(v.view(np.int16)) if v.dtype == np.uint16 else torch.from_numpy(v)).cuda()
            for k, v in soa.items()}
     order, total = sh.gang_order(dev, InterPolicy(order=1, starvation_limit=0.15, prior_tokens=128.0), now, 0, N + 5)

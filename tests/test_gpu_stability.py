@@ -27,8 +27,8 @@ def _round(ctx, i):
            "last_service": torch.zeros(n, dtype=torch.float64, device="cuda"),
            "iter_tok_sum": torch.full((n,), 640, dtype=torch.int64, device="cuda"),
            "iter_count": torch.full((n,), 5, dtype=torch.int32, device="cuda"),
-           "knob": torch.ones(n, dtype=torch.int16, device="cuda"),
-           "cap": torch.full((n,), 9, dtype=torch.int16, device="cuda"),
+           "knob": torch.ones(n, dtype=torch.int32, device="cuda"),
+           "cap": torch.full((n,), 9, dtype=torch.int32, device="cuda"),
            "terminated": torch.zeros(n, dtype=torch.uint8, device="cuda")}
     ctx.gang_priority(soa, InterPolicy(order=1, starvation_limit=0.5, prior_tokens=128.0), float(n))
     text = "\n".join(f'{{"program_id": "p{k % 7}", "step_index": {k // 7 + 1}, "token_offset": {64 * (k // 7 + 1)}, '

@@ -65,8 +65,8 @@ def test_scheduler_facade_spec_and_random_orders():
                    last_service=np.array([float.fromhex(r[1]) for r in rows]),
                    iter_tok_sum=np.array([int(r[2]) for r in rows], np.int64),
                    iter_count=np.array([int(r[3]) for r in rows], np.uint32),
-                   knob=np.array([int(r[4]) for r in rows], np.uint16),
-                   cap=np.array([int(r[5]) for r in rows], np.uint16),
+                   knob=np.array([int(r[4]) for r in rows], np.int32),
+                   cap=np.array([int(r[5]) for r in rows], np.int32),
                    terminated=np.array([int(r[6]) for r in rows], np.uint8))
         ref, _ = O.gang_order(soa, int(order_kind), float(limit), 128.0, 8.0)
         assert [int(x) for x in ids.split()] == [int(rows[i][7]) for i in ref.tolist()], head

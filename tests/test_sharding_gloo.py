@@ -79,8 +79,8 @@ def _inputs():
     cnt = rng.integers(0, 5, N_PROG).astype(np.uint32)
     soa = dict(arrival=arrival, last_service=now - rng.exponential(0.2, N_PROG),
                iter_tok_sum=(rng.integers(1, 500, N_PROG) * cnt).astype(np.int64), iter_count=cnt,
-               cap=rng.integers(1, 30, N_PROG).astype(np.uint16), terminated=(rng.random(N_PROG) < 0.2).astype(np.uint8))
-    soa["knob"] = np.minimum(soa["cap"], rng.integers(0, 30, N_PROG)).astype(np.uint16)
+               cap=rng.integers(1, 30, N_PROG).astype(np.int32), terminated=(rng.random(N_PROG) < 0.2).astype(np.uint8))
+    soa["knob"] = np.minimum(soa["cap"], rng.integers(0, 30, N_PROG)).astype(np.int32)
     soa["last_service"] = np.maximum(soa["last_service"], 0.0)
     return ids, soa, now
 
