@@ -271,6 +271,60 @@ int cdx_allocate_scan(cdx_ctx* ctx, const uint32_t* meets_bits, uint64_t R, uint
                       uint32_t* kept, uint64_t* n_kept, int64_t* tokens_saved,
                       int64_t* total_budget);
 
+/* ---- mixed-archetype batch: per-archetype certaindex + allocation at the current knob ------
+ * The batched form of ProgramDriver::update_certaindex's dispatch (runtime.cpp:264-313)
+ * followed by scheduler.allocate, for N programs of any archetypes, each at
+ * its own current knob.  Programs of one archetype group share one trace tensor; program i has
+ * archetype archetype[i] (CDX_ARCH_*) and is row slot[i] of its group's tensor (MCTS and Rebase
+ * share the reward group).  Signals per knob unit u (1-based):
+ *   SC      H~ = certaindex_entropy(cluster_exact(the S answers of probe row u-1))  (K2)
+ *   CoT     C_k = consistency(records up to probe u-1, window), 0.0 while not ready (runtime.cpp:298)
+ *   MCTS    H~ and mean reward over every path of steps 0..u-1 (cumulative, K4)
+ *   Rebase  H~ and max reward over steps 0..u-1
+ * Each archetype's thresholds (combined_meets_thresholds, metrics.cpp:159-171) and allocation
+ * policy (even | static_threshold | k_step_threshold) come from policy[CDX_ARCH_*].          */
+typedef struct {
+    const uint32_t* sc_ids;      /* u32[sc_n][sc_P][sc_S] */
+    uint64_t sc_n;
+    uint32_t sc_P, sc_S;
+    const uint32_t* cot_ids;     /* u32[cot_n][cot_P] */
+    const uint64_t* cot_hes;     /* u64[cot_n][ceil(cot_P/64)] hesitation bits */
+    uint64_t cot_n;
+    uint32_t cot_P, cot_window;
+    const float* rw_rewards;     /* f32[rw_n][rw_T][rw_W] */
+    const uint32_t* rw_ids;      /* u32[rw_n][rw_T][rw_W] (nullable: no entropy signal) */
+    uint64_t rw_n;
+    uint32_t rw_T, rw_W;
+} cdx_mixed_trace;
+
+typedef struct {
+    cdx_threshold th[4];         /* this archetype's thresholds, in order */
+    uint32_t n_th;
+    uint32_t _pad;
+    cdx_alloc_policy alloc;      /* kind, detect_at, recheck_every, resource_cap, tokens_per_unit */
+} cdx_arch_policy;
+
+/* knob i32[N]: units the program holds now (0 <= knob <= its resource_cap).  Outputs:
+ *   decision u8[N]  CDX_EXIT_CONTINUE (granted) | CDX_EXIT_CERTAIN (a test point <= knob met its
+ *                   thresholds) | CDX_EXIT_BUDGET (knob == resource_cap); nonzero = terminated,
+ *                   so it serves directly as cdx_prog_soa.terminated of the gang order
+ *   grant   i32[N]  (nullable) units granted now: up to the next decision point
+ *   cap     i32[N]  (nullable) the archetype's resource_cap (cdx_prog_soa.cap)
+ *   offsets i64[N]  (nullable) exclusive scan of grant * tokens_per_unit, program order
+ *   total_budget    (device i64, nullable) the scan's total
+ * policy: cdx_arch_policy[4] (host).  A bad archetype, slot or knob fails at cdx_sync.      */
+int cdx_mixed_allocate(cdx_ctx* ctx, const cdx_mixed_trace* trace, const uint8_t* archetype,
+                       const uint32_t* slot, const int32_t* knob, uint64_t N,
+                       const cdx_arch_policy* policy, uint8_t* decision, int32_t* grant,
+                       int32_t* cap, int64_t* offsets, int64_t* total_budget);
+
+/* The CoT signal as threshold bits: bit p of meets_bits u32[R][ceil(P/32)] =
+ * combined_meets_thresholds({C_k(p)}, th) where C_k(p) = consistency over the records up to
+ * probe p (probe.cpp:64-75), 0.0 while fewer than `window` are usable (runtime.cpp:298).
+ * ids u32[R][P], hes u64[R][ceil(P/64)]; window <= 62; thresholds on the entropy slot only. */
+int cdx_cot_meets(cdx_ctx* ctx, const uint32_t* ids, const uint64_t* hes, uint64_t R, uint32_t P,
+                  int32_t window, const cdx_threshold* th, uint32_t n_th, uint32_t* meets_bits);
+
 /* ---- K3: CoT probe-window exit ------------------------------------------------------
  * Replaces, for every prefix of each request's probe trace,
  *   probe::should_exit(trace, cfg)        probe.cpp:77-85  (consistency probe.cpp:64-75)

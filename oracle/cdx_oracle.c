@@ -860,3 +860,77 @@ int cdxo_cot_eps_stop(const uint32_t* ids, const uint64_t* hes, uint64_t R, uint
     }
     return CDX_OK;
 }
+
+/* ===================================================================================== */
+/* Mixed-archetype step (cdx_mixed_allocate): the CoT signal of update_certaindex as     */
+/* threshold bits, then scheduler.allocate at each program's current knob.              */
+/* ===================================================================================== */
+/* runtime.cpp:293-299: C = consistency(records, latest step, w).value_or(0.0) after probe p
+ * (probe.cpp:64-75), then combined_meets_thresholds({C}, th) (metrics.cpp:159-171). */
+int cdxo_cot_meets(const uint32_t* ids, const uint64_t* hes, uint64_t R, uint32_t P, int w,
+                   const cdx_threshold* th, uint32_t n_th, uint32_t* meets) {
+    if (w < 1) return CDX_EINVAL;
+    const uint32_t words = (P + 31) / 32;
+    const int present[4] = {1, 0, 0, 0};
+    for (uint64_t r = 0; r < R; ++r) {
+        for (uint32_t q = 0; q < words; ++q) meets[r * words + q] = 0;
+        for (uint32_t p = 0; p < P; ++p) {
+            const int agree = consistency_prefix(ids, hes, r, P, p + 1, w);
+            double sig[4] = {agree < 0 ? 0.0 : (double)agree / (double)w, 0.0, 0.0, 0.0};
+            const int ok = cdxo_meets_thresholds(sig, present, th, n_th);
+            if (ok < 0) return CDX_EINVAL;
+            if (ok) meets[r * words + p / 32] |= 1u << (p % 32);
+        }
+    }
+    return CDX_OK;
+}
+
+/* SPEC.md:404-412 allocate at knob k for every program, as include/cdx/scheduler.hpp's
+ * allocate: k >= cap -> terminate (resource cap); a test point t <= k (detect_at, then every
+ * recheck_every for k_step) whose bit t-1 is set -> terminate (certain); else grant up to
+ * the next decision point.  meets[g]/words[g]/n[g]: groups 0 SC, 1 CoT, 2 MCTS/Rebase. */
+int cdxo_mixed_decide(const uint8_t* arch, const uint32_t* slot, const int32_t* knob, uint64_t N,
+                      const uint32_t* const* meets, const uint32_t* words, const uint64_t* n,
+                      const cdx_arch_policy* pol, uint8_t* decision, int32_t* grant, int32_t* cap,
+                      int64_t* offsets, int64_t* total) {
+    int64_t run = 0;
+    for (uint64_t i = 0; i < N; ++i) {
+        const uint8_t a = arch[i];
+        if (a > 3) return CDX_EINVAL;
+        const int g = a == CDX_ARCH_SC ? 0 : (a == CDX_ARCH_COT ? 1 : 2);
+        const cdx_alloc_policy* q = &pol[a].alloc;
+        const int32_t k = knob[i];
+        if (slot[i] >= n[g] || k < 0 || k > q->resource_cap) return CDX_EINVAL;
+        uint8_t dec = CDX_EXIT_CONTINUE;
+        int32_t units = 0;
+        if (k >= q->resource_cap) {
+            dec = CDX_EXIT_BUDGET;
+        } else {
+            int met = 0;
+            if (q->kind != CDX_POL_EVEN) {
+                const uint32_t* row = meets[g] + (uint64_t)slot[i] * words[g];
+                const int32_t step = q->kind == CDX_POL_K_STEP_THRESHOLD ? q->recheck_every : q->resource_cap + 1;
+                for (int32_t t = q->detect_at; t <= k && !met; t += step) met = (row[(t - 1) / 32] >> ((t - 1) % 32)) & 1u;
+            }
+            if (met) {
+                dec = CDX_EXIT_CERTAIN;
+            } else {
+                int32_t next = q->resource_cap;
+                if (q->kind == CDX_POL_STATIC_THRESHOLD && k < q->detect_at) next = q->detect_at;
+                if (q->kind == CDX_POL_K_STEP_THRESHOLD) {
+                    next = q->detect_at;
+                    while (next <= k) next += q->recheck_every;
+                    if (next > q->resource_cap) next = q->resource_cap;
+                }
+                units = next - k;
+            }
+        }
+        decision[i] = dec;
+        grant[i] = units;
+        cap[i] = q->resource_cap;
+        offsets[i] = run;
+        run += (int64_t)units * q->tokens_per_unit;
+    }
+    *total = run;
+    return CDX_OK;
+}

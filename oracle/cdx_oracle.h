@@ -121,6 +121,13 @@ int cdxo_reward_aggregate(const float* rw, const uint32_t* ids, const uint8_t* a
 int cdxo_reward_aggregate_f64(const double* rw, const uint32_t* ids, const uint8_t* agg, uint64_t G, uint32_t T,
                               uint32_t W, const int32_t* exit_step, uint32_t* answer);
 
+int cdxo_cot_meets(const uint32_t* ids, const uint64_t* hes, uint64_t R, uint32_t P, int w,
+                   const cdx_threshold* th, uint32_t n_th, uint32_t* meets);
+int cdxo_mixed_decide(const uint8_t* arch, const uint32_t* slot, const int32_t* knob, uint64_t N,
+                      const uint32_t* const* meets, const uint32_t* words, const uint64_t* n,
+                      const cdx_arch_policy* pol, uint8_t* decision, int32_t* grant, int32_t* cap,
+                      int64_t* offsets, int64_t* total);
+
 #ifdef __cplusplus
 }
 #endif

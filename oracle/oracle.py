@@ -45,6 +45,10 @@ class ProgSoA(C.Structure):
                 ("cap", P), ("terminated", P), ("program_id", P), ("id_base", C.c_uint32), ("_pad", C.c_uint32)]
 
 
+class ArchPolicy(C.Structure):
+    _fields_ = [("th", Threshold * 4), ("n_th", C.c_uint32), ("_pad", C.c_uint32), ("alloc", AllocPolicy)]
+
+
 class GenParams(C.Structure):
     _fields_ = [("seed", C.c_uint64), ("groups", C.c_uint32), ("conv_lo", C.c_uint32), ("conv_hi", C.c_uint32),
                 ("_pad", C.c_uint32), ("noise_level", C.c_double), ("residual_noise", C.c_double),
@@ -538,3 +542,126 @@ def ref_parse_jsonl(text: bytes):
     praw, araw = pid.raw, ans.raw
     return [(praw[po[i]:po[i + 1]], int(step[i]), int(tok[i]), araw[ao[i]:ao[i + 1]], bool(hes[i]))
             for i in range(r)]
+
+
+# ---------------------------------------------------------------- mixed-archetype step
+def cot_meets(ids, hes, window, ths, nthreads=None):
+    """CoT signal (runtime.cpp:293-299) as threshold bits per probe (cdxo_cot_meets), run
+    over request chunks on host threads (the restatement is O(P^2) per request)."""
+    from concurrent.futures import ThreadPoolExecutor
+    R, P_ = ids.shape
+    words = (P_ + 31) // 32
+    out = np.zeros((R, words), np.uint32)
+    if R == 0:
+        return out
+    ids = np.ascontiguousarray(ids, dtype=np.uint32)
+    hes = np.ascontiguousarray(hes).view(np.uint64)
+    arr, n = thresholds(ths)
+    f = lib().cdxo_cot_meets
+    f.argtypes = [P, P, C.c_uint64, C.c_uint32, C.c_int, P, C.c_uint32, P]
+    nth = nthreads or hardware_threads()
+    chunk = max(1, -(-R // (4 * nth)))
+
+    def run(b):
+        e = min(R, b + chunk)
+        st = f(_p(ids[b:e]), _p(hes[b:e]), e - b, P_, window, C.cast(arr, P), n, _p(out[b:e]))
+        if st:
+            raise ValueError(f"oracle cot_meets status {st}")
+    with ThreadPoolExecutor(nth) as ex:
+        list(ex.map(run, range(0, R, chunk)))
+    return out
+
+
+def ref_cot_signal(ids, hes, window, groups=5, nthreads=1):
+    """The reference's own consistency(records, latest, w).value_or(0.0) after every probe
+    (runtime.cpp:293-299 through oracle/_ref), f64[R][P]."""
+    R, P_ = ids.shape
+    v, nv = _vocab_c(vocab(groups))
+    ck = np.empty((R, P_), np.float64)
+    r = ref().ref_cot_signal(_p(np.ascontiguousarray(ids)), _p(np.ascontiguousarray(hes)), C.c_uint64(R),
+                             C.c_uint32(P_), v, C.c_uint32(nv), C.c_int(window), _p(ck), C.c_int(nthreads))
+    if r < 0:
+        raise RefError(_ref_err())
+    return ck
+
+
+def arch_policy(ths, kind, detect_at, cap, recheck_every=1, tokens_per_unit=64):
+    a = ArchPolicy()
+    for i, (sig, cut, d) in enumerate(ths):
+        a.th[i].signal, a.th[i].cutoff, a.th[i].dir = sig, cut, d
+    a.n_th = len(ths)
+    a.alloc.kind, a.alloc.detect_at, a.alloc.resource_cap = kind, detect_at, cap
+    a.alloc.recheck_every, a.alloc.tokens_per_unit = recheck_every, tokens_per_unit
+    return a
+
+
+def mixed_allocate(trace, arch, slot, knob, policies, nthreads=None):
+    """The mixed step restated: per-archetype threshold bits from the restated signals (SC:
+    cdxo_sc_certaindex rows; CoT: cdxo_cot_meets; MCTS/Rebase: cdxo reward certaindex with
+    the FP64 values against each archetype's thresholds), then cdxo_mixed_decide.
+    trace: dict sc_ids[n][P][S], cot_ids[n][P], cot_hes, cot_window, rw[n][T][W], rw_ids.
+    policies: list of 4 ArchPolicy (by CDX_ARCH_*: SC, Rebase, MCTS, CoT)."""
+    SC_, REB, MCT, COT = 0, 1, 2, 3
+
+    def ths_of(a):
+        pa = policies[a]
+        return [(pa.th[i].signal, pa.th[i].cutoff, pa.th[i].dir) for i in range(pa.n_th)]
+
+    sc = trace.get("sc_ids")
+    cot = trace.get("cot_ids")
+    rw = trace.get("rw")
+    meets, words, ns = [], [], []
+    if sc is not None and len(sc):
+        _, _, m = sc_certaindex(sc, ths_of(SC_))
+    else:
+        m = np.zeros((0, 1), np.uint32)
+    meets.append(np.ascontiguousarray(m))
+    if cot is not None and len(cot):
+        m = cot_meets(cot, trace["cot_hes"], trace["cot_window"], ths_of(COT), nthreads)
+    else:
+        m = np.zeros((0, 1), np.uint32)
+    meets.append(m)
+    if rw is not None and len(rw):
+        G, T, W = rw.shape
+        agg = np.zeros(G, np.uint8)
+        a = np.asarray(arch)
+        sl = np.asarray(slot)
+        sel = (a == REB) | (a == MCT)
+        agg[sl[sel]] = (a[sel] == REB).astype(np.uint8)
+        R64, _, _, H64 = reward_certaindex(rw, trace.get("rw_ids"), agg, want_h64=True) if trace.get("rw_ids") \
+            is not None else (*reward_certaindex(rw, None, agg), None)
+        # combined_meets_thresholds on the FP64 signals, per archetype (an AND of compares)
+        ok = np.ones((G, T), bool)
+        for a_, rows in ((REB, agg == 1), (MCT, agg == 0)):
+            for sig, cut, d in ths_of(a_):
+                if sig == 0 and H64 is None or sig > 1:
+                    raise ValueError("absent signal")
+                v = (R64 if sig == 1 else H64)[rows]
+                ok[rows] &= (v >= cut) if d == 0 else (v <= cut)
+        m = np.zeros((G, (T + 31) // 32), np.uint32)
+        for t in range(T):
+            m[:, t // 32] |= ok[:, t].astype(np.uint32) << np.uint32(t % 32)
+    else:
+        m = np.zeros((0, 1), np.uint32)
+    meets.append(m)
+    for mm in meets:
+        words.append(mm.shape[1] if mm.ndim == 2 else 1)
+        ns.append(mm.shape[0])
+    N = len(arch)
+    dec = np.empty(N, np.uint8)
+    grant = np.empty(N, np.int32)
+    cap = np.empty(N, np.int32)
+    off = np.empty(N, np.int64)
+    tot = C.c_int64(0)
+    mp = (P * 3)(*[_p(mm) for mm in meets])
+    wa = (C.c_uint32 * 3)(*words)
+    na = (C.c_uint64 * 3)(*ns)
+    pa = (ArchPolicy * 4)(*policies)
+    f = lib().cdxo_mixed_decide
+    f.argtypes = [P, P, P, C.c_uint64, P, P, P, P, P, P, P, P, P]
+    st = f(_p(np.ascontiguousarray(arch, dtype=np.uint8)), _p(np.ascontiguousarray(slot, dtype=np.uint32)),
+           _p(np.ascontiguousarray(knob, dtype=np.int32)), N, C.cast(mp, P), C.cast(wa, P), C.cast(na, P),
+           C.cast(pa, P), _p(dec), _p(grant), _p(cap), _p(off), C.byref(tot))
+    if st:
+        raise ValueError(f"oracle mixed_decide status {st}")
+    return dict(decision=dec, grant=grant, cap=cap, offsets=off, total=tot.value, meets=meets)

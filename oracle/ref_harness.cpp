@@ -347,6 +347,34 @@ int ref_sc_batch(const uint32_t* ids, uint64_t R, uint32_t P, uint32_t S,
 // terminated (runtime.cpp:405-411) and final_answer taken.  ck = consistency(...).value_or(0)
 // at every prefix (runtime.cpp:293-300).  exit_step -1 = never exited (final answer then
 // from the full trace, criteria_external).
+// The CoT signal ProgramDriver::update_certaindex records after every probe
+// (runtime.cpp:293-299): consistency(records, latest step_index, window).value_or(0.0), with
+// the reference's own probe::consistency (probe.cpp:64-75), as f64 per prefix.
+int ref_cot_signal(const uint32_t* ids, const uint64_t* hes, uint64_t R, uint32_t P, const char* const* vocab,
+                   uint32_t nvocab, int window, double* ck64, int nthreads) {
+    const auto voc = make_vocab(vocab, nvocab);
+    const uint32_t hw = (P + 63) / 64;
+    std::atomic<int> fail{0};
+    parallel_for(R, nthreads, [&](uint64_t b, uint64_t e) {
+        try {
+            std::vector<pr::AnswerRecord> recs;
+            recs.reserve(P);
+            for (uint64_t r = b; r < e; ++r) {
+                recs.clear();
+                for (uint32_t p = 0; p < P; ++p) {
+                    const bool h = (hes[r * hw + p / 64] >> (p % 64)) & 1ULL;
+                    recs.push_back({static_cast<int>(p + 1), static_cast<long>(p + 1) * 64, voc[ids[r * P + p]], h});
+                    ck64[r * P + p] = pr::consistency(recs, recs.back().step_index, window).value_or(0.0);
+                }
+            }
+        } catch (const std::exception& ex) {
+            g_err = ex.what();
+            fail = 1;
+        }
+    });
+    return fail ? -1 : 0;
+}
+
 int ref_cot_batch(const uint32_t* ids, const uint64_t* hes, uint64_t R, uint32_t P,
                   const char* const* vocab, uint32_t nvocab, const CProbeCfg* cfgc,
                   int32_t* exit_step, uint8_t* reason, uint32_t* final_id, uint8_t* low_conf,

@@ -287,6 +287,51 @@ class Context:
         return dict(exit_knob=exit_knob, reason=reason, granted=granted, offsets=offsets, kept=kept,
                     scalars=scal)
 
+    # -- mixed-archetype step (update_certaindex dispatch + allocate at the current knob) --
+    def cot_meets(self, ids, hes, window: int, thresholds: Sequence[Threshold]):
+        t = self.torch
+        R, P = ids.shape
+        meets = self.empty((R, (P + 31) // 32), t.int32)
+        arr, n = c_thresholds(thresholds)
+        self._bind_stream()
+        self._check(self.lib.cdx_cot_meets(self.h, _ptr(ids), _ptr(hes), R, P, window, arr, n, _ptr(meets)))
+        return meets
+
+    def mixed_allocate(self, trace: dict, archetype, slot, knob, policies, out=None):
+        """trace: sc_ids [n][P][S], cot_ids [n][P] + cot_hes + cot_window, rw [n][T][W] (+ rw_ids);
+        archetype u8[N], slot i32[N], knob i32[N]; policies: 4 (thresholds, AllocPolicy) pairs
+        indexed by CDX_ARCH_* (SC, Rebase, MCTS, CoT).  Returns decision / grant / cap /
+        offsets tensors and the device total budget."""
+        t = self.torch
+        N = archetype.shape[0]
+        tr = _abi.MixedTrace()
+        sc, cot, rw = trace.get("sc_ids"), trace.get("cot_ids"), trace.get("rw")
+        if sc is not None:
+            tr.sc_ids, (tr.sc_n, tr.sc_P, tr.sc_S) = sc.data_ptr(), sc.shape
+        if cot is not None:
+            tr.cot_ids, tr.cot_hes = cot.data_ptr(), trace["cot_hes"].data_ptr()
+            tr.cot_n, tr.cot_P = cot.shape
+            tr.cot_window = int(trace["cot_window"])
+        if rw is not None:
+            tr.rw_rewards, (tr.rw_n, tr.rw_T, tr.rw_W) = rw.data_ptr(), rw.shape
+            tr.rw_ids = _ptr(trace.get("rw_ids"))
+        pols = (_abi.ArchPolicy * 4)()
+        for a, (ths, pol) in enumerate(policies):
+            for i, th in enumerate(ths):
+                pols[a].th[i].signal, pols[a].th[i].dir, pols[a].th[i].cutoff = th.signal, th.dir, float(th.cutoff)
+            pols[a].n_th = len(ths)
+            pols[a].alloc = c_policy(pol)
+        o = out or {}
+        dec = o.get("decision", self.empty((max(N, 1),), t.uint8))
+        grant = o.get("grant", self.empty((max(N, 1),), t.int32))
+        cap = o.get("cap", self.empty((max(N, 1),), t.int32))
+        offs = o.get("offsets", self.empty((max(N, 1),), t.int64))
+        total = o.get("total", self.empty((1,), t.int64))
+        self._bind_stream()
+        self._check(self.lib.cdx_mixed_allocate(self.h, C.byref(tr), _ptr(archetype), _ptr(slot), _ptr(knob), N,
+                                                pols, _ptr(dec), _ptr(grant), _ptr(cap), _ptr(offs), _ptr(total)))
+        return dict(decision=dec[:N], grant=grant[:N], cap=cap[:N], offsets=offs[:N], total=total)
+
     # -- K3 --
     def cot_exit(self, ids, hes, cfg: ProbeConfig, offsets=None, want_ck: bool = False, out=None):
         t = self.torch

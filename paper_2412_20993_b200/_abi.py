@@ -60,6 +60,16 @@ class GenParams(C.Structure):
 P = C.c_void_p
 U64, U32, I64, I32 = C.c_uint64, C.c_uint32, C.c_int64, C.c_int32
 
+
+class MixedTrace(C.Structure):
+    _fields_ = [("sc_ids", P), ("sc_n", U64), ("sc_P", U32), ("sc_S", U32),
+                ("cot_ids", P), ("cot_hes", P), ("cot_n", U64), ("cot_P", U32), ("cot_window", U32),
+                ("rw_rewards", P), ("rw_ids", P), ("rw_n", U64), ("rw_T", U32), ("rw_W", U32)]
+
+
+class ArchPolicy(C.Structure):
+    _fields_ = [("th", Threshold * 4), ("n_th", U32), ("_pad", U32), ("alloc", AllocPolicy)]
+
 # name -> (restype, argtypes); this table is also the export list tests check against cdx_c.h
 SIGNATURES = {
     "cdx_abi_version": (C.c_int, []),
@@ -95,6 +105,8 @@ SIGNATURES = {
     "cdx_memset": (C.c_int, [P, P, C.c_int, U64]),
     "cdx_allocate_scan": (C.c_int, [P, P, U64, U32, C.POINTER(AllocPolicy), I64, U32, P, P, P, P, P, P, P, P]),
     "cdx_cot_exit": (C.c_int, [P, P, P, P, U64, U32, C.POINTER(ProbeCfg), P, P, P, P, P]),
+    "cdx_cot_meets": (C.c_int, [P, P, P, U64, U32, I32, C.POINTER(Threshold), U32, P]),
+    "cdx_mixed_allocate": (C.c_int, [P, C.POINTER(MixedTrace), P, P, P, U64, C.POINTER(ArchPolicy), P, P, P, P, P]),
     "cdx_reward_certaindex": (C.c_int, [P, P, P, P, U64, U32, U32, C.POINTER(Threshold), U32,
                                         C.POINTER(Threshold), U32, P, P, P]),
     "cdx_reward_certaindex_f64": (C.c_int, [P, P, P, P, U64, U32, U32, C.POINTER(Threshold), U32,

@@ -43,6 +43,8 @@ struct cdx_ctx {
     size_t scratch_bytes = 0;
     void* scratch2 = nullptr;
     size_t scratch2_bytes = 0;
+    void* scratch3 = nullptr;
+    size_t scratch3_bytes = 0;
     // host-entry pipeline buffers
     void* pipe_buf = nullptr;
     size_t pipe_bytes = 0;
@@ -67,6 +69,7 @@ int set_error(cdx_ctx* ctx, int code, const std::string& msg);
 int cuda_fail(cdx_ctx* ctx, cudaError_t e, const char* what);
 void* scratch(cdx_ctx* ctx, size_t bytes);
 void* scratch2(cdx_ctx* ctx, size_t bytes);
+void* scratch3(cdx_ctx* ctx, size_t bytes);  // the mixed step's own buffers (K2/K4 use scratch, scratch2)
 // device-side validation error codes (set via atomicCAS on ctx->d_err)
 enum DevErr : int {
     DEV_OK = 0,
@@ -76,6 +79,7 @@ enum DevErr : int {
     DEV_BAD_CLUSTERING = 4,  // "semantic_entropy: invalid clustering"
     DEV_EMPTY_REWARDS = 5,   // "certaindex_reward: empty reward set"
     DEV_EMPTY_CLUSTER = 6,   // "semantic_entropy: empty cluster"
+    DEV_MIXED_PROGRAM = 7,   // "mixed_allocate: archetype, slot or knob out of range"
     DEV_ABSENT_SIGNAL = 16,  // + SignalKind: "combined_meets_thresholds: signal '<name>' absent"
 };
 const char* dev_err_message(int code);

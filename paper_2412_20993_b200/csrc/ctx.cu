@@ -38,6 +38,9 @@ void* scratch(cdx_ctx* ctx, size_t bytes) { return grow(ctx, &ctx->scratch, &ctx
 void* scratch2(cdx_ctx* ctx, size_t bytes) {
     return grow(ctx, &ctx->scratch2, &ctx->scratch2_bytes, bytes);
 }
+void* scratch3(cdx_ctx* ctx, size_t bytes) {
+    return grow(ctx, &ctx->scratch3, &ctx->scratch3_bytes, bytes);
+}
 
 const char* dev_err_message(int code) {
     switch (code) {
@@ -47,6 +50,7 @@ const char* dev_err_message(int code) {
         case DEV_BAD_CLUSTERING: return "semantic_entropy: invalid clustering";
         case DEV_EMPTY_REWARDS: return "certaindex_reward: empty reward set";
         case DEV_EMPTY_CLUSTER: return "semantic_entropy: empty cluster";
+        case DEV_MIXED_PROGRAM: return "mixed_allocate: archetype, slot or knob out of range";
         case DEV_ABSENT_SIGNAL + 0: return "combined_meets_thresholds: signal 'certaindex_entropy' absent";
         case DEV_ABSENT_SIGNAL + 1: return "combined_meets_thresholds: signal 'certaindex_reward' absent";
         case DEV_ABSENT_SIGNAL + 2: return "combined_meets_thresholds: signal 'mean_output_length' absent";
@@ -185,6 +189,7 @@ int cdx_ctx_destroy(cdx_ctx* ctx) {
     cudaStreamSynchronize(ctx->stream);
     if (ctx->scratch) cudaFree(ctx->scratch);
     if (ctx->scratch2) cudaFree(ctx->scratch2);
+    if (ctx->scratch3) cudaFree(ctx->scratch3);
     if (ctx->pipe_buf) cudaFree(ctx->pipe_buf);
     if (ctx->tt_dev) cudaFree(ctx->tt_dev);
     if (ctx->al_state) cudaFree(ctx->al_state);
@@ -231,6 +236,7 @@ int cdx_sync(cdx_ctx* ctx) {
         cudaMemset(ctx->d_err, 0, sizeof(int));
         const int st = (code == cdx::DEV_REWARD_RANGE || code == cdx::DEV_BAD_CLUSTERING ||
                         code == cdx::DEV_EMPTY_REWARDS || code == cdx::DEV_EMPTY_CLUSTER ||
+                        code == cdx::DEV_MIXED_PROGRAM ||
                         (code >= cdx::DEV_ABSENT_SIGNAL && code < cdx::DEV_ABSENT_SIGNAL + 4))
                            ? CDX_EINVAL
                            : CDX_ERUNTIME;

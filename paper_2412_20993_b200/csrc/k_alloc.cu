@@ -412,10 +412,12 @@ extern "C" int cdx_allocate_scan(cdx_ctx* ctx, const uint32_t* meets_bits, uint6
         void* args[] = {&p};
         const cudaError_t e = cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(allocate_scan_kernel),
                                                           dim3(p.ntiles), dim3(AL_THREADS), args, 0, ctx->stream);
-        if (e != cudaSuccess) return cuda_fail(ctx, e, "allocate_scan(cooperative)");
-    } else {
-        allocate_scan_kernel<<<p.ntiles, AL_THREADS, 0, ctx->stream>>>(p);
+        if (e != cudaSuccess) {  // e.g. fewer SMs than queried (MPS limits): ticketed look-back instead
+            (void)cudaGetLastError();
+            p.coop = 0;
+        }
     }
+    if (!p.coop) allocate_scan_kernel<<<p.ntiles, AL_THREADS, 0, ctx->stream>>>(p);
     CDX_CHECK_LAUNCH(ctx, "allocate_scan");
     return CDX_OK;
 }

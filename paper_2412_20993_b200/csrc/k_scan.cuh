@@ -150,8 +150,12 @@ inline int scan_excl(cdx_ctx* ctx, Load ld, uint64_t n, Out* out, bool total_slo
         const cudaError_t e = cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(scan_lb<Load, Out>),
                                                           dim3(static_cast<unsigned>(tiles)), dim3(SL_THREADS), args, 0,
                                                           ctx->stream);
-        if (e != cudaSuccess) return cuda_fail(ctx, e, "jsonl(scan, cooperative)");
-    } else {
+        if (e != cudaSuccess) {  // e.g. fewer SMs than queried (MPS limits): the look-back form below
+            (void)cudaGetLastError();
+            coop = 0;
+        }
+    }
+    if (!coop) {
         cudaMemsetAsync(rec, 0, tiles * 8 + 8, ctx->stream);
         scan_lb<Load, Out><<<static_cast<unsigned>(tiles), SL_THREADS, 0, ctx->stream>>>(ld, n, out, total_slot, rec,
                                                                                           ticket, total, 0);
