@@ -47,8 +47,12 @@ CONFIGS = {
               desc="SC entropy certaindex + token-budget allocation, 1M req x 32 samples x 64 probes"),
     "D": dict(kind="reward", G=1 << 18, T=16, W=64, conv_hi=16, detect=3,
               desc="MCTS/Rebase reward + cumulative entropy certaindex, 256K programs x 64 nodes x 16 steps"),
-    "E": dict(kind="gang", N=1 << 22, limit=0.5, prior=128.0,
-              desc="gang-scheduling priority order (escalation + SJF + tie-break), 4M mixed programs"),
+    "E": dict(kind="mixed", N=1 << 22, limit=0.5, prior=128.0, sc=(32, 16), cot=(64, 3), rw=(16, 64),
+              desc="online scheduling round over a 4M-program mixed trace (40% SC / 40% CoT / 10% MCTS / 10% "
+                   "Rebase): per-archetype certaindex at every knob unit (K2 / cot_meets / K4), allocate at each "
+                   "program's current knob + budget scan, then the gang priority order of the live programs (K6)"),
+    "G": dict(kind="gang", N=1 << 22, limit=0.5, prior=128.0,
+              desc="gang-scheduling priority order alone (escalation + SJF + tie-break), 4M programs"),
     "J": dict(kind="jsonl", lines=1 << 20, programs=1 << 14, flush_l2=True,
               desc="probe-trace JSONL ingestion (read_trace_jsonl), 1M records over 16K programs"),
 }
@@ -56,7 +60,7 @@ TH_MCTS = [(0, 0.99, 0), (1, 0.4, 0)]   # PAPER.md:963 MCTS/GSM8K thresholds
 TH_REBASE = [(0, 0.85, 0), (1, 0.99, 0)]  # PAPER.md:966 Rebase/GSM8K thresholds
 
 
-TRAFFIC_KEY = {"sc": "sc", "cot": "cot", "reward": "reward", "gang": "gang", "jsonl": "jsonl"}
+TRAFFIC_KEY = {"sc": "sc", "cot": "cot", "reward": "reward", "gang": "gang", "jsonl": "jsonl", "mixed": "mixed"}
 
 
 def load_traffic(kind):
@@ -258,14 +262,14 @@ def gang_inputs(N, seed, limit):
 
 
 def cpu_gang(cfg, nth, N, seed):
-    """SPEC restatement (no reference code exists for the scheduler): qsort with the SPEC
-    comparator, oracle/cdx_oracle.c (single thread)."""
+    """SPEC restatement (no reference code exists for the scheduler): per-thread qsort with the
+    SPEC comparator + parallel pairwise merges on `nth` host threads (cdxo_gang_order_mt)."""
     from oracle import oracle as O
     soa, now = gang_inputs(N, seed, cfg["limit"])
     t0 = time.perf_counter()
-    O.gang_order(soa, 1, cfg["limit"], cfg["prior"], now)
+    O.gang_order_mt(soa, 1, cfg["limit"], cfg["prior"], now, nth)
     dt = time.perf_counter() - t0
-    return N / dt, dt, f"{N} programs, {dt:.2f} s (SPEC restatement, 1 thread)"
+    return N / dt, dt, f"{N} programs, {dt:.2f} s (SPEC restatement, {nth} threads)"
 
 
 def jsonl_text(lines, programs, seed):
@@ -300,14 +304,94 @@ def cpu_jsonl(cfg, nth, lines, seed):
     return n / dt, dt, f"{n} records ({len(text)} bytes), {dt:.2f} s (1 thread: one sequential stream)"
 
 
-CPU = {"sc": cpu_sc, "cot": cpu_cot, "reward": cpu_reward, "gang": cpu_gang, "jsonl": cpu_jsonl}
-CPU_SAMPLE = {"A": 1024, "B": 1 << 16, "C": 1 << 18, "D": 1 << 14, "E": 1 << 20, "J": 1 << 17}
+SC_, REB_, MCT_, COT_ = 0, 1, 2, 3
+
+
+def mixed_policies(cfg):
+    """Per archetype (CDX_ARCH_*): thresholds and allocation policy of config E.  SC: H~ >= 0.7
+    at detect 5; MCTS / Rebase: the Table-3 GSM8K thresholds at step 3
+    (PAPER.md:963-966); CoT: C_k >= 0.9 re-tested every probe from the first full window."""
+    (scP, S), (cotP, w), (T, W) = cfg["sc"], cfg["cot"], cfg["rw"]
+    return {SC_: ([(0, 0.7, 0)], dict(kind=2, detect_at=5, resource_cap=scP, recheck_every=1, tokens_per_unit=64 * S)),
+            REB_: ([(0, 0.85, 0), (1, 0.99, 0)], dict(kind=2, detect_at=3, resource_cap=T, recheck_every=1,
+                                                      tokens_per_unit=W)),
+            MCT_: ([(0, 0.99, 0), (1, 0.4, 0)], dict(kind=2, detect_at=3, resource_cap=T, recheck_every=1,
+                                                     tokens_per_unit=W)),
+            COT_: ([(0, 0.9, 0)], dict(kind=4, detect_at=w, resource_cap=cotP, recheck_every=1, tokens_per_unit=64))}
+
+
+def mixed_layout(cfg, N, seed):
+    """Global program table of the mixed trace: archetype, row within the archetype's group,
+    current knob, scheduler state (paper_2412_20993_b200/synth.py)."""
+    import numpy as np
+
+    from paper_2412_20993_b200 import synth
+    (scP, _), (cotP, _), (T, _) = cfg["sc"], cfg["cot"], cfg["rw"]
+    arch, slot, sizes = synth.mixed_layout(N, seed)
+    knob = synth.mixed_knobs(arch, (scP, T, T, cotP), seed + 1)
+    state, now = synth.gang_state(N, seed + 2, cfg["limit"], knob=knob, cap=np.zeros(N, np.int32))
+    return arch, slot, sizes, knob, state, now
+
+
+def cpu_mixed(cfg, nth, n, seed):
+    """The reference's per-archetype CPU path on n programs: cluster_exact + certaindex_entropy
+    + combined_meets_thresholds per SC row, probe::consistency per CoT prefix, the cumulative
+    certaindex_reward + entropy per MCTS / Rebase step (all oracle/_ref, the reference's own
+    code), then allocate at each knob and the gang sort (SPEC restatements: no reference code
+    exists for the scheduler), on `nth` host threads."""
+    import ctypes as C
+
+    import numpy as np
+
+    from oracle import oracle as O
+    (scP, S), (cotP, w), (T, W) = cfg["sc"], cfg["cot"], cfg["rw"]
+    arch, slot, sizes, knob, state, now = mixed_layout(cfg, n, seed)
+    sc = O.gen_sc(O.gen_params(seed=seed + 3, conv_hi=scP), sizes[0], scP, S)
+    cid, ches = O.gen_cot(O.gen_params(seed=seed + 4, conv_hi=cotP, hesitation_prob=0.05), sizes[1], cotP)
+    rw, rid = O.gen_reward(O.gen_params(seed=seed + 5, conv_hi=T), sizes[2], T, W)
+    pols = mixed_policies(cfg)
+    cp = [O.arch_policy(pols[a][0], kw["kind"], kw["detect_at"], kw["resource_cap"], kw["recheck_every"],
+                        kw["tokens_per_unit"]) for a, kw in ((a, pols[a][1]) for a in range(4))]
+    agg = np.zeros(sizes[2], np.uint8)
+    sel = (arch == REB_) | (arch == MCT_)
+    agg[slot[sel]] = (arch[sel] == REB_).astype(np.uint8)
+    t0 = time.perf_counter()
+    _, m_sc = O.ref_sc_batch(sc, 5, pols[SC_][0], nthreads=nth)
+    ck = O.ref_cot_signal(cid, ches, w, nthreads=nth)
+    m_cot = np.zeros((sizes[1], (cotP + 31) // 32), np.uint32)
+    ok = ck >= pols[COT_][0][0][1]
+    for p_ in range(cotP):
+        m_cot[:, p_ // 32] |= ok[:, p_].astype(np.uint32) << np.uint32(p_ % 32)
+    R, H = O.ref_reward_batch(rw, rid, agg, nthreads=nth)
+    okr = np.where(agg[:, None] == 1, (H >= 0.85) & (R >= 0.99), (H >= 0.99) & (R >= 0.4))
+    m_rw = np.zeros((sizes[2], (T + 31) // 32), np.uint32)
+    for t in range(T):
+        m_rw[:, t // 32] |= okr[:, t].astype(np.uint32) << np.uint32(t % 32)
+    dec, grant, cap, off = np.empty(n, np.uint8), np.empty(n, np.int32), np.empty(n, np.int32), np.empty(n, np.int64)
+    tot = C.c_int64(0)
+    meets = [np.ascontiguousarray(m) for m in (m_sc, m_cot, m_rw)]
+    st = O.lib().cdxo_mixed_decide(O._p(arch), O._p(slot), O._p(knob), n,
+                                   C.cast((C.c_void_p * 3)(*[m.ctypes.data for m in meets]), C.c_void_p),
+                                   C.cast((C.c_uint32 * 3)(*[m.shape[1] for m in meets]), C.c_void_p),
+                                   C.cast((C.c_uint64 * 3)(*sizes), C.c_void_p),
+                                   C.cast((O.ArchPolicy * 4)(*cp), C.c_void_p), O._p(dec), O._p(grant), O._p(cap),
+                                   O._p(off), C.byref(tot))
+    assert st == 0
+    state = dict(state, cap=cap, terminated=dec)
+    O.gang_order_mt(state, 1, cfg["limit"], cfg["prior"], now, nth)
+    dt = time.perf_counter() - t0
+    return n / dt, dt, (f"{n} programs ({sizes[0]} SC / {sizes[1]} CoT / {sizes[2]} MCTS+Rebase), {dt:.2f} s "
+                        "(reference certaindex functions + SPEC allocate/sort ports)")
+
+
+CPU = {"sc": cpu_sc, "cot": cpu_cot, "reward": cpu_reward, "gang": cpu_gang, "jsonl": cpu_jsonl, "mixed": cpu_mixed}
+CPU_SAMPLE = {"A": 1024, "B": 1 << 16, "C": 1 << 18, "D": 1 << 14, "E": 1 << 15, "G": 1 << 20, "J": 1 << 17}
 
 
 def cpu_baseline(name, cfg, sample=None, target_s=1.0, max_reps=64):
     """The CPU path on repeated bounded samples (fresh seed each) until `target_s` seconds
     of timed CPU work have accumulated; value = total work / total timed seconds."""
-    nth = host_threads() if cfg["kind"] not in ("gang", "jsonl") else 1
+    nth = host_threads() if cfg["kind"] != "jsonl" else 1
     n = sample or CPU_SAMPLE[name]
     work = secs = 0.0
     reps = 0
@@ -328,7 +412,7 @@ def run_reference(args, cfg, rank, world):
         return
     vals = []
     n = args.ref_sample or CPU_SAMPLE[args.config]
-    nth = host_threads() if cfg["kind"] not in ("gang", "jsonl") else 1
+    nth = host_threads() if cfg["kind"] != "jsonl" else 1
     note = ""
     for i in range(args.warmup + args.steps):
         v, dt, note = CPU[cfg["kind"]](cfg, nth, n, 20993 + i)
@@ -611,7 +695,129 @@ def bench_jsonl(args, cfg, rank, world, cx, with_e2e=True):
                 extra={"text_bytes": len(text)}, e2e=None)
 
 
-BENCH = {"sc": bench_sc, "cot": bench_cot, "reward": bench_reward, "gang": bench_gang, "jsonl": bench_jsonl}
+def bench_mixed(args, cfg, rank, world, cx, with_e2e=True):
+    """Config E: one online scheduling round over the mixed trace.  Traces of each archetype
+    group are generated on the device (rows of the rank's programs only); the timed step is
+    cdx_mixed_allocate (K2 on the SC rows, cot_meets on the CoT rows, K4 on the MCTS / Rebase
+    rows, allocate at every program's knob, budget scan) followed by the gang order of the
+    live programs (K6; at N > 1 sharded with the key allgather + merge).  Programs shard
+    contiguously across ranks; the round is identical to the single-GPU one."""
+    import numpy as np
+    import torch
+    from paper_2412_20993_b200 import AllocPolicy, GenParams, InterPolicy, Threshold
+    from paper_2412_20993_b200.sharding import Sharded, max_shard, shard_range
+    N = cfg["N"]
+    (scP, S), (cotP, w), (T, W) = cfg["sc"], cfg["cot"], cfg["rw"]
+    arch, slot, sizes, knob, state, now = mixed_layout(cfg, N, 20993 + 7)
+    g0, gn = shard_range(N, rank, world)
+    group = np.where(arch == SC_, 0, np.where(arch == COT_, 1, 2))
+    a_r, s_r = arch[g0:g0 + gn], slot[g0:g0 + gn].astype(np.int64)
+    r0 = [int((group[:g0] == g).sum()) for g in range(3)]
+    n_r = [int((group[g0:g0 + gn] == g).sum()) for g in range(3)]
+    gr = group[g0:g0 + gn]
+    for g in range(3):
+        s_r[gr == g] -= r0[g]
+    trace = dict(sc_ids=cx.gen_sc(GenParams(seed=20993 + 10, conv_hi=scP), n_r[0], scP, S, r0=r0[0]),
+                 cot_window=w)
+    trace["cot_ids"], trace["cot_hes"] = cx.gen_cot(GenParams(seed=20993 + 11, conv_hi=cotP, hesitation_prob=0.05),
+                                                    n_r[1], cotP, r0=r0[1])
+    trace["rw"], trace["rw_ids"] = cx.gen_reward(GenParams(seed=20993 + 12, conv_hi=T), n_r[2], T, W, g0=r0[2])
+    dev = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda()  # noqa: E731
+    arch_d, slot_d, knob_d = dev(a_r), dev(s_r.astype(np.int32)), dev(knob[g0:g0 + gn])
+    st_d = {k: dev(v[g0:g0 + gn]) for k, v in state.items() if k not in ("cap", "knob")}
+    st_d["knob"] = knob_d
+    pols = [([Threshold(*t) for t in ths], AllocPolicy(**kw)) for ths, kw in
+            (mixed_policies(cfg)[a] for a in range(4))]
+    ipol = InterPolicy(order=1, starvation_limit=cfg["limit"], prior_tokens=cfg["prior"])
+    outbuf = {k: torch.empty((max(gn, 1),), dtype=dt, device="cuda") for k, dt in
+              (("decision", torch.uint8), ("grant", torch.int32), ("cap", torch.int32), ("offsets", torch.int64))}
+    outbuf["total"] = torch.empty((1,), dtype=torch.int64, device="cuda")
+    sh = Sharded(cx)
+    stride = max_shard(N, world)
+    res = {}
+    torch.cuda.synchronize()
+
+    def step(seg):
+        e = seg_events(seg, "mixed_allocate")
+        out = cx.mixed_allocate(trace, arch_d, slot_d, knob_d, pols, out=outbuf)
+        if e is not None:
+            e.record(torch.cuda.current_stream())
+        e = seg_events(seg, "gang_priority")
+        soa = dict(st_d, terminated=out["decision"], cap=out["cap"])
+        if world == 1:
+            res["order"] = cx.gang_priority(soa, ipol, now)[0]
+        else:
+            res["order"] = sh.gang_order(soa, ipol, now, g0, stride)[0]
+        if e is not None:
+            e.record(torch.cuda.current_stream())
+
+    l0 = cx.launches
+    ms, per, clocks = timed(args, world, step, ["mixed_allocate", "gang_priority"])
+    launches = in_timed(cx, l0, args)
+    words = lambda u: (u + 31) // 32  # noqa: E731
+    trace_b = (n_r[0] * scP * S * 4 + n_r[1] * (cotP * 4 + ((cotP + 63) // 64) * 8) + n_r[2] * T * W * 8)
+    table_b = gn * (1 + 4 + 4) + gn * (1 + 4 + 4 + 8)  # arch, slot, knob in; decision, grant, cap, offsets out
+    mixed_b = trace_b + table_b
+    gang_b = gn * (8 + 8 + 8 + 4 + 4 + 4 + 1) + int(res["order"].shape[0]) * 4
+    meets_b = 2 * 4 * (n_r[0] * words(scP) + n_r[1] * words(cotP) + n_r[2] * words(T))  # intermediate round trip
+    out = dict(value=N / (ms / 1e3), ms=ms, launches=launches, clocks=clocks,
+               kernel="mixed_allocate (K2 + cot_meets + K4 + allocate + budget scan)",
+               kernel_ms=per["mixed_allocate"], kernel_bytes=mixed_b, step_bytes=mixed_b + gang_b,
+               extra={"gang_priority_ms": per["gang_priority"], "gang_priority_bytes": gang_b,
+                      "programs": {"sc": n_r[0], "cot": n_r[1], "mcts_rebase": n_r[2]},
+                      "intermediate_meets_bytes": meets_b, "live_programs": int(res["order"].shape[0]),
+                      "probe_evals_per_step": n_r[0] * scP * S + n_r[1] * cotP + n_r[2] * T * W,
+                      "trace_bytes": trace_b},
+               scaling="strong")
+    out["e2e"] = e2e_mixed(args, cx, trace, arch_d, slot_d, knob_d, st_d, pols, ipol, now, world, N) \
+        if (with_e2e and not args.no_e2e) else None
+    return out
+
+
+def e2e_mixed(args, cx, trace, arch_d, slot_d, knob_d, st_d, pols, ipol, now, world, N):
+    """Config E through the public API from pinned host buffers: every step copies the whole
+    trace and program table host -> device, runs the mixed step and the gang order, and reads
+    the order and the decisions back (wall clock, barrier on both sides, slowest rank)."""
+    import torch
+    dev_in = dict(sc_ids=trace["sc_ids"], cot_ids=trace["cot_ids"], cot_hes=trace["cot_hes"], rw=trace["rw"],
+                  rw_ids=trace["rw_ids"], arch=arch_d, slot=slot_d, knob=knob_d, **st_d)
+    host = {k: torch.empty(v.shape, dtype=v.dtype, pin_memory=True) for k, v in dev_in.items()}
+    for k, v in dev_in.items():
+        host[k].copy_(v)
+    stage = {k: torch.empty_like(v) for k, v in dev_in.items()}
+    h2d = sum(v.numel() * v.element_size() for v in host.values())
+    res = {}
+
+    def one():
+        for k, v in host.items():
+            stage[k].copy_(v, non_blocking=True)
+        tr = dict(sc_ids=stage["sc_ids"], cot_ids=stage["cot_ids"], cot_hes=stage["cot_hes"], rw=stage["rw"],
+                  rw_ids=stage["rw_ids"], cot_window=trace["cot_window"])
+        out = cx.mixed_allocate(tr, stage["arch"], stage["slot"], stage["knob"], pols)
+        soa = {k: stage[k] for k in ("arrival", "last_service", "iter_tok_sum", "iter_count", "knob")}
+        soa.update(terminated=out["decision"], cap=out["cap"])
+        order = cx.gang_priority(soa, ipol, now)[0]
+        res["order"] = order.cpu()
+        res["decision"] = out["decision"].cpu()
+
+    for _ in range(max(1, min(args.warmup, 2))):
+        one()
+    torch.cuda.synchronize()
+    steps = max(1, min(args.steps, 3))
+    barrier(world)
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        one()
+    torch.cuda.synchronize()
+    dt = max_over_ranks((time.perf_counter() - t0) / steps, world)
+    barrier(world)
+    d2h = res["order"].numel() * 4 + res["decision"].numel()
+    return {"value": N / dt, "unit": UNIT, "h2d_bytes_per_step": h2d * world, "d2h_bytes_per_step": d2h * world,
+            "ms_per_step": dt * 1e3,
+            "api": "Context.mixed_allocate + Context.gang_priority (C-ABI) from pinned host buffers, wall clock"}
+
+
+BENCH = {"mixed": bench_mixed, "sc": bench_sc, "cot": bench_cot, "reward": bench_reward, "gang": bench_gang, "jsonl": bench_jsonl}
 
 
 def summarize(name, cfg, res, peak):
@@ -667,7 +873,7 @@ def main():
         cfg_out = {"workload": args.config, "desc": cfg["desc"],
                    **{k: v for k, v in cfg.items() if k not in ("kind", "desc", "conv_hi")},
                    "parallelism": (f"program shards x{world}, NCCL allgather of sorted key runs + merge"
-                                   if cfg["kind"] == "gang" else
+                                   if cfg["kind"] in ("gang", "mixed") else
                                    f"request shards x{world} (no data-path collective; 8 B/rank allgather "
                                    "of budget totals for global offsets)"),
                    "l2": ("L2 flushed before every timed step (512 MB write, outside the step's events)"

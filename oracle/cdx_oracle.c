@@ -934,3 +934,125 @@ int cdxo_mixed_decide(const uint8_t* arch, const uint32_t* slot, const int32_t* 
     *total = run;
     return CDX_OK;
 }
+
+/* The same order on `nthreads` host threads (the CPU baseline of the gang order): items
+ * are built and qsort-ed in per-thread chunks with the SPEC comparator, then merged in
+ * parallel pairwise rounds.  Same total order, so the same result as cdxo_gang_order. */
+typedef struct {
+    const cdx_prog_soa* s;
+    const cdx_inter_policy* pol;
+    double now;
+    uint64_t b, e;
+    gang_item* it;  /* chunk output (live items, compacted within the chunk) */
+    uint64_t n;
+} gang_chunk;
+
+static void* gang_chunk_build(void* arg) {
+    gang_chunk* c = (gang_chunk*)arg;
+    const cdx_prog_soa* s = c->s;
+    uint64_t n = 0;
+    for (uint64_t i = c->b; i < c->e; ++i) {
+        if (s->terminated[i]) continue;
+        const int esc = (c->now - s->last_service[i]) >= c->pol->starvation_limit;
+        double key;
+        if (esc || c->pol->order == CDX_ORDER_FIFO) {
+            key = s->arrival[i];
+        } else {
+            const double est = cdxo_estimate_iteration_tokens(s->iter_tok_sum[i], s->iter_count[i],
+                                                              c->pol->prior_tokens);
+            const int64_t rem = (int64_t)s->cap[i] - (int64_t)s->knob[i];
+            key = est * (double)(rem > 0 ? rem : 0);
+        }
+        c->it[n].esc = esc;
+        c->it[n].key = key;
+        c->it[n].arrival = s->arrival[i];
+        c->it[n].id = s->program_id ? s->program_id[i] : s->id_base + (uint32_t)i;
+        ++n;
+    }
+    c->n = n;
+    qsort(c->it, n, sizeof(gang_item), gang_cmp);
+    return NULL;
+}
+
+typedef struct {
+    const gang_item *a, *b;
+    uint64_t na, nb;
+    gang_item* out;
+} gang_merge_job;
+
+static void* gang_merge2(void* arg) {
+    gang_merge_job* m = (gang_merge_job*)arg;
+    uint64_t i = 0, j = 0, k = 0;
+    while (i < m->na && j < m->nb) m->out[k++] = gang_cmp(&m->b[j], &m->a[i]) < 0 ? m->b[j++] : m->a[i++];
+    while (i < m->na) m->out[k++] = m->a[i++];
+    while (j < m->nb) m->out[k++] = m->b[j++];
+    return NULL;
+}
+
+int cdxo_gang_order_mt(const cdx_prog_soa* s, uint64_t N, const cdx_inter_policy* pol, double now,
+                       uint32_t* order, uint64_t* n_out, int nthreads) {
+    if (!(pol->starvation_limit > 0.0)) return CDX_EINVAL;
+    if (pol->order != CDX_ORDER_FIFO && pol->order != CDX_ORDER_SJF) return CDX_EINVAL;
+    if (nthreads < 1) nthreads = 1;
+    if (nthreads > 256) nthreads = 256;
+    gang_item* buf = (gang_item*)malloc(sizeof(gang_item) * (N ? N : 1) * 2);
+    gang_chunk ch[256];
+    pthread_t th[256];
+    for (int t = 0; t < nthreads; ++t) {
+        ch[t].s = s;
+        ch[t].pol = pol;
+        ch[t].now = now;
+        ch[t].b = N * (uint64_t)t / (uint64_t)nthreads;
+        ch[t].e = N * (uint64_t)(t + 1) / (uint64_t)nthreads;
+        ch[t].it = buf + ch[t].b;
+        pthread_create(&th[t], NULL, gang_chunk_build, &ch[t]);
+    }
+    for (int t = 0; t < nthreads; ++t) pthread_join(th[t], NULL);
+    /* runs: (start, length) in buf; merge pairwise into the other half until one run */
+    uint64_t rs[256], rl[256];
+    int runs = nthreads;
+    for (int t = 0; t < nthreads; ++t) {
+        rs[t] = ch[t].b;
+        rl[t] = ch[t].n;
+    }
+    gang_item* src = buf;
+    gang_item* dst = buf + (N ? N : 1);
+    while (runs > 1) {
+        gang_merge_job mj[128];
+        int nm = 0;
+        uint64_t ns[256], nl[256];
+        for (int r = 0; r + 1 < runs; r += 2) {
+            mj[nm].a = src + rs[r];
+            mj[nm].na = rl[r];
+            mj[nm].b = src + rs[r + 1];
+            mj[nm].nb = rl[r + 1];
+            mj[nm].out = dst + rs[r];
+            ns[nm] = rs[r];
+            nl[nm] = rl[r] + rl[r + 1];
+            pthread_create(&th[nm], NULL, gang_merge2, &mj[nm]);
+            ++nm;
+        }
+        for (int m = 0; m < nm; ++m) pthread_join(th[m], NULL);
+        int nr = nm;
+        if (runs % 2) { /* odd run out: copy across */
+            memcpy(dst + rs[runs - 1], src + rs[runs - 1], rl[runs - 1] * sizeof(gang_item));
+            ns[nr] = rs[runs - 1];
+            nl[nr] = rl[runs - 1];
+            ++nr;
+        }
+        for (int r = 0; r < nr; ++r) {
+            rs[r] = ns[r];
+            rl[r] = nl[r];
+        }
+        runs = nr;
+        gang_item* t = src;
+        src = dst;
+        dst = t;
+    }
+    /* the merged runs are not contiguous across chunk gaps: compact while writing ids */
+    const uint64_t n = runs ? rl[0] : 0;
+    for (uint64_t i = 0; i < n; ++i) order[i] = src[rs[0] + i].id;
+    *n_out = n;
+    free(buf);
+    return CDX_OK;
+}

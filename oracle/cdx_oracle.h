@@ -128,6 +128,9 @@ int cdxo_mixed_decide(const uint8_t* arch, const uint32_t* slot, const int32_t* 
                       const cdx_arch_policy* pol, uint8_t* decision, int32_t* grant, int32_t* cap,
                       int64_t* offsets, int64_t* total);
 
+int cdxo_gang_order_mt(const cdx_prog_soa* s, uint64_t N, const cdx_inter_policy* pol, double now,
+                       uint32_t* order, uint64_t* n_out, int nthreads);
+
 #ifdef __cplusplus
 }
 #endif

@@ -245,6 +245,27 @@ def reward_certaindex(rw, ids, agg, want_h64=False):
     return (R64, R32, H, H64) if want_h64 else (R64, R32, H)
 
 
+def gang_order_mt(soa, order_kind, starvation_limit, prior, now, nthreads):
+    """cdxo_gang_order_mt: the same order from per-thread qsorts + parallel merges."""
+    N = soa["arrival"].shape[0]
+    s = ProgSoA()
+    keep = {}
+    for k, dt in (("arrival", np.float64), ("last_service", np.float64), ("iter_tok_sum", np.int64),
+                  ("iter_count", np.uint32), ("knob", np.int32), ("cap", np.int32), ("terminated", np.uint8)):
+        keep[k] = np.ascontiguousarray(soa[k], dtype=dt)
+        setattr(s, k, keep[k].ctypes.data)
+    pol = InterPolicy()
+    pol.gang, pol.order, pol.starvation_limit, pol.prior_tokens = 1, order_kind, starvation_limit, prior
+    order = np.empty(max(N, 1), np.uint32)
+    n = C.c_uint64(0)
+    lib().cdxo_gang_order_mt.argtypes = [P, C.c_uint64, P, C.c_double, P, P, C.c_int]
+    st = lib().cdxo_gang_order_mt(C.byref(s), C.c_uint64(N), C.byref(pol), C.c_double(now), _p(order), C.byref(n),
+                                  C.c_int(nthreads))
+    if st:
+        raise ValueError(f"oracle gang status {st}")
+    return order[:n.value]
+
+
 def gang_order(soa, order_kind, starvation_limit, prior, now, id_base=0):
     N = soa["arrival"].shape[0]
     s = ProgSoA()

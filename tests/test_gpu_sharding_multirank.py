@@ -103,7 +103,7 @@ def test_two_ranks_on_one_gpu_equal_single_process():
         assert np.array_equal(got[r][3], gref)
 
 
-@pytest.mark.parametrize("config", ["C", "E"])
+@pytest.mark.parametrize("config", ["C", "E", "G"])
 def test_bench_two_ranks_prints_its_line(config):
     env = dict(os.environ, CDX_BENCH_BACKEND="gloo", CDX_BENCH_SHARE_DEVICE="1")
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2", "--master-addr",
@@ -115,4 +115,4 @@ def test_bench_two_ranks_prints_its_line(config):
     assert len(lines) == 1  # rank 0 only
     d = json.loads(lines[0])
     assert d["n_gpus"] == 2 and d["value"] > 0 and d["gpu_launches"] > 0
-    assert d["scaling"] == ("strong" if config == "E" else "weak")
+    assert d["scaling"] == ("strong" if config in ("E", "G") else "weak")
