@@ -780,7 +780,7 @@ def e2e_mixed(args, cx, trace, arch_d, slot_d, knob_d, st_d, pols, ipol, now, wo
     the order and the decisions back (wall clock, barrier on both sides, slowest rank)."""
     import torch
     dev_in = dict(sc_ids=trace["sc_ids"], cot_ids=trace["cot_ids"], cot_hes=trace["cot_hes"], rw=trace["rw"],
-                  rw_ids=trace["rw_ids"], arch=arch_d, slot=slot_d, knob=knob_d, **st_d)
+                  rw_ids=trace["rw_ids"], arch=arch_d, slot=slot_d, **st_d)  # st_d holds the knob
     host = {k: torch.empty(v.shape, dtype=v.dtype, pin_memory=True) for k, v in dev_in.items()}
     for k, v in dev_in.items():
         host[k].copy_(v)

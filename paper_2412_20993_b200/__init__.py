@@ -272,12 +272,14 @@ class Context:
                       out=None):
         t = self.torch
         o = out or {}
-        exit_knob = o.get("exit_knob", self.empty((R,), t.int32))
-        reason = o.get("reason", self.empty((R,), t.uint8))
-        granted = o.get("granted", self.empty((R,), t.int32))
-        offsets = o.get("offsets", self.empty((R,), t.int64))
-        kept = o.get("kept", self.empty((max(R, 1),), t.int32))
-        scal = o.get("scalars", self.torch.zeros((3,), dtype=t.int64, device=self.dev))
+        # defaults allocated only when missing (a dict.get default would be evaluated, and a
+        # torch.zeros default launched, on every call)
+        exit_knob = o["exit_knob"] if "exit_knob" in o else self.empty((R,), t.int32)
+        reason = o["reason"] if "reason" in o else self.empty((R,), t.uint8)
+        granted = o["granted"] if "granted" in o else self.empty((R,), t.int32)
+        offsets = o["offsets"] if "offsets" in o else self.empty((R,), t.int64)
+        kept = o["kept"] if "kept" in o else self.empty((max(R, 1),), t.int32)
+        scal = o["scalars"] if "scalars" in o else self.empty((3,), t.int64)  # written by the kernel
         pol = c_policy(policy)
         self._bind_stream()
         self._check(self.lib.cdx_allocate_scan(self.h, _ptr(meets), R, P, C.byref(pol), base_offset, kept_base,
@@ -322,11 +324,11 @@ class Context:
             pols[a].n_th = len(ths)
             pols[a].alloc = c_policy(pol)
         o = out or {}
-        dec = o.get("decision", self.empty((max(N, 1),), t.uint8))
-        grant = o.get("grant", self.empty((max(N, 1),), t.int32))
-        cap = o.get("cap", self.empty((max(N, 1),), t.int32))
-        offs = o.get("offsets", self.empty((max(N, 1),), t.int64))
-        total = o.get("total", self.empty((1,), t.int64))
+        dec = o["decision"] if "decision" in o else self.empty((max(N, 1),), t.uint8)
+        grant = o["grant"] if "grant" in o else self.empty((max(N, 1),), t.int32)
+        cap = o["cap"] if "cap" in o else self.empty((max(N, 1),), t.int32)
+        offs = o["offsets"] if "offsets" in o else self.empty((max(N, 1),), t.int64)
+        total = o["total"] if "total" in o else self.empty((1,), t.int64)
         self._bind_stream()
         self._check(self.lib.cdx_mixed_allocate(self.h, C.byref(tr), _ptr(archetype), _ptr(slot), _ptr(knob), N,
                                                 pols, _ptr(dec), _ptr(grant), _ptr(cap), _ptr(offs), _ptr(total)))
@@ -337,10 +339,10 @@ class Context:
         t = self.torch
         R, P = ids.shape
         o = out or {}
-        ex = o.get("exit_step", self.empty((R,), t.int32))
-        reason = o.get("reason", self.empty((R,), t.uint8))
-        fid = o.get("final_id", self.empty((R,), t.int32))
-        low = o.get("low_conf", self.empty((R,), t.uint8))
+        ex = o["exit_step"] if "exit_step" in o else self.empty((R,), t.int32)
+        reason = o["reason"] if "reason" in o else self.empty((R,), t.uint8)
+        fid = o["final_id"] if "final_id" in o else self.empty((R,), t.int32)
+        low = o["low_conf"] if "low_conf" in o else self.empty((R,), t.uint8)
         ck = self.empty((R, P), t.float32) if want_ck else None
         c = c_probe(cfg)
         self._bind_stream()

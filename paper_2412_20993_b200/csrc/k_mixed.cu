@@ -15,6 +15,7 @@
 // decision point.  The token budgets of the grants are scanned into offsets (K5's scan) and the
 // decision byte doubles as the `terminated` flag of the gang order (K6, cdx_prog_soa).
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 
@@ -108,6 +109,81 @@ __global__ void __launch_bounds__(CM_WARPS * 32) cot_meets_kernel(const uint32_t
     }
 }
 
+// Lean form: P = 4 * NC probes (NC <= 32, P <= 128) and a compile-time window W.  Each
+// thread reads its staged row as uint4 (4 probes per LDS.128, conflict-free with the +4 word
+// row stride), the hesitation bits as up to two 64-bit words, and walks the probes fully
+// unrolled and branch-free: a usable probe shifts the register window, the outcome bit of
+// the newest window is a table lookup, a hesitant probe repeats the previous outcome.
+template <int W, int NC>
+__global__ void __launch_bounds__(CM_WARPS * 32) cot_meets_lean(const uint32_t* __restrict__ ids,
+                                                                const uint64_t* __restrict__ hes, uint64_t R,
+                                                                uint32_t stride, uint64_t lut, uint32_t notready,
+                                                                uint32_t* __restrict__ meets) {
+    constexpr uint32_t P = 4 * NC, HW = (P + 63) / 64, WORDS = (P + 31) / 32;
+    extern __shared__ __align__(16) uint32_t cm_smem[];
+    const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
+    uint32_t* rows = cm_smem + static_cast<size_t>(warp) * 32u * stride;
+    const uint64_t nwarps = static_cast<uint64_t>(gridDim.x) * CM_WARPS;
+    for (uint64_t r0 = (static_cast<uint64_t>(blockIdx.x) * CM_WARPS + warp) * 32u; r0 < R; r0 += nwarps * 32u) {
+        const uint32_t nr = static_cast<uint32_t>(R - r0 < 32u ? R - r0 : 32u);
+        const uint4* src = reinterpret_cast<const uint4*>(ids + r0 * P);
+        if (nr == 32) {  // 32 rows = 32 * NC uint4, NC per lane, coalesced
+#pragma unroll
+            for (int j = 0; j < NC; ++j) {
+                const uint32_t q = static_cast<uint32_t>(j) * 32u + lane;
+                const uint4 v = __ldg(src + q);
+                const uint32_t rr = q / NC, cc = (q - rr * NC) * 4u;
+                *reinterpret_cast<uint4*>(rows + rr * stride + cc) = v;
+            }
+        } else {
+            for (uint32_t q = lane; q < nr * NC; q += 32u) {
+                const uint32_t rr = q / NC, cc = (q - rr * NC) * 4u;
+                *reinterpret_cast<uint4*>(rows + rr * stride + cc) = __ldg(src + q);
+            }
+        }
+        uint64_t hb[HW];
+        if (lane < nr) {
+#pragma unroll
+            for (uint32_t k = 0; k < HW; ++k) hb[k] = __ldg(hes + (r0 + lane) * HW + k);
+        }
+        __syncwarp();
+        if (lane < nr) {
+            const uint4* row = reinterpret_cast<const uint4*>(rows + lane * stride);
+            uint32_t win[W];
+#pragma unroll
+            for (int j = 0; j < W; ++j) win[j] = 0;
+            int32_t used = 0;
+            uint32_t bit = notready, out[WORDS];
+#pragma unroll
+            for (uint32_t k = 0; k < WORDS; ++k) out[k] = 0;
+#pragma unroll
+            for (int c = 0; c < NC; ++c) {
+                const uint4 q4 = row[c];
+                const uint32_t qv[4] = {q4.x, q4.y, q4.z, q4.w};
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    const uint32_t p = 4u * c + j;
+                    const bool u = !((hb[p / 64] >> (p % 64)) & 1ull);
+                    if (u) {
+#pragma unroll
+                        for (int t = W - 1; t > 0; --t) win[t] = win[t - 1];
+                        win[0] = qv[j];
+                        ++used;
+                        int32_t a = 0;
+#pragma unroll
+                        for (int t = 0; t < W; ++t) a += win[t] == qv[j] ? 1 : 0;
+                        bit = used >= W ? static_cast<uint32_t>((lut >> a) & 1ull) : notready;
+                    }
+                    out[p / 32] |= bit << (p % 32);
+                }
+            }
+#pragma unroll
+            for (uint32_t k = 0; k < WORDS; ++k) meets[(r0 + lane) * WORDS + k] = out[k];
+        }
+        __syncwarp();
+    }
+}
+
 // ---- Rebase vs MCTS: the aggregation of each reward row, from its program's archetype -----
 __global__ void mixed_agg_kernel(const uint8_t* __restrict__ arch, const uint32_t* __restrict__ slot, uint64_t N,
                                  uint64_t rw_n, uint8_t* __restrict__ agg) {
@@ -145,62 +221,84 @@ __device__ __forceinline__ int group_of(uint8_t a) {
     return a == CDX_ARCH_SC ? 0 : (a == CDX_ARCH_COT ? 1 : 2);
 }
 
-__global__ void mixed_decide_kernel(const __grid_constant__ DecideParams p) {
-    for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < p.N;
-         i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
-        const uint8_t a = p.arch[i];
-        uint8_t dec = CDX_EXIT_CONTINUE;
-        int32_t g_units = 0, cap = 0;
-        if (a > 3) {
-            set_dev_err(p.d_err, DEV_MIXED_PROGRAM);
-        } else {
-            const ArchPol& q = p.pol[a];
-            const int g = group_of(a);
-            const uint32_t s = p.slot[i];
-            const int32_t k = p.knob[i];
-            cap = q.cap;
-            if (s >= p.n[g] || k < 0 || k > q.cap) {
-                set_dev_err(p.d_err, DEV_MIXED_PROGRAM);
-            } else if (k >= q.cap) {  // "always terminate at resource_cap"
-                dec = CDX_EXIT_BUDGET;
-            } else {
-                bool met = false;
-                if (q.kind != CDX_POL_EVEN) {
-                    const uint32_t* row = p.meets[g] + static_cast<uint64_t>(s) * p.words[g];
-                    const int32_t step = q.kind == CDX_POL_K_STEP_THRESHOLD ? q.recheck : q.cap + 1;
-                    for (int32_t t = q.detect; t <= k && !met; t += step)
-                        met = (__ldg(row + (t - 1) / 32) >> ((t - 1) % 32)) & 1u;
-                }
-                if (met) {
-                    dec = CDX_EXIT_CERTAIN;
-                } else {  // grant up to the next decision point
-                    int32_t next = q.cap;
-                    if (q.kind == CDX_POL_STATIC_THRESHOLD && k < q.detect) next = q.detect;
-                    if (q.kind == CDX_POL_K_STEP_THRESHOLD) {
-                        next = q.detect;
-                        if (next <= k) next += ((k - next) / q.recheck + 1) * q.recheck;
-                        next = next < q.cap ? next : q.cap;
-                    }
-                    g_units = next - k;
-                }
-            }
-        }
-        p.decision[i] = dec;
-        if (p.grant) p.grant[i] = g_units;
-        if (p.cap) p.cap[i] = cap;
+// any bit of row[] in the knob-unit range [lo, hi] (1-based, inclusive)
+__device__ __forceinline__ bool any_bits(const uint32_t* __restrict__ row, int32_t lo, int32_t hi) {
+    bool met = false;
+    for (int32_t w = (lo - 1) / 32; w <= (hi - 1) / 32 && !met; ++w) {
+        const int32_t b0 = w * 32 + 1;  // knob unit of bit 0 of word w
+        uint32_t m = 0xffffffffu;
+        if (lo > b0) m &= 0xffffffffu << (lo - b0);
+        if (hi < b0 + 31) m &= 0xffffffffu >> (b0 + 31 - hi);
+        met = (__ldg(row + w) & m) != 0u;
     }
+    return met;
 }
 
-// token budget of program i's grant, the scan's input (u32: cap * tokens_per_unit < 2^32)
-struct LoadBudget {
-    const uint8_t* arch;
-    const int32_t* grant;
-    uint32_t tpu[4];
-    __device__ uint32_t operator()(uint64_t i) const {
-        const uint8_t a = arch[i];
-        return a < 4 ? static_cast<uint32_t>(grant[i]) * tpu[a] : 0u;
+// scheduler.allocate at the current knob for program i (as
+// facade_scheduler.cpp): writes decision / grant / cap, returns the grant's token budget
+__device__ __forceinline__ uint32_t decide_one(const DecideParams& p, uint64_t i) {
+    const uint8_t a = __ldg(p.arch + i);
+    uint8_t dec = CDX_EXIT_CONTINUE;
+    int32_t g_units = 0, cap = 0;
+    uint32_t budget = 0;
+    if (a > 3) {
+        set_dev_err(p.d_err, DEV_MIXED_PROGRAM);
+    } else {
+        const ArchPol& q = p.pol[a];
+        const int g = group_of(a);
+        const uint32_t s = __ldg(p.slot + i);
+        const int32_t k = __ldg(p.knob + i);
+        cap = q.cap;
+        if (s >= p.n[g] || k < 0 || k > q.cap) {
+            set_dev_err(p.d_err, DEV_MIXED_PROGRAM);
+        } else if (k >= q.cap) {  // "always terminate at resource_cap"
+            dec = CDX_EXIT_BUDGET;
+        } else {
+            bool met = false;
+            if (q.kind != CDX_POL_EVEN && q.detect <= k) {
+                const uint32_t* row = p.meets[g] + static_cast<uint64_t>(s) * p.words[g];
+                if (q.kind == CDX_POL_STATIC_THRESHOLD) {
+                    met = (__ldg(row + (q.detect - 1) / 32) >> ((q.detect - 1) % 32)) & 1u;
+                } else if (q.recheck == 1) {  // every unit from detect_at to k
+                    met = any_bits(row, q.detect, k);
+                } else {
+                    for (int32_t t = q.detect; t <= k && !met; t += q.recheck)
+                        met = (__ldg(row + (t - 1) / 32) >> ((t - 1) % 32)) & 1u;
+                }
+            }
+            if (met) {
+                dec = CDX_EXIT_CERTAIN;
+            } else {  // grant up to the next decision point
+                int32_t next = q.cap;
+                if (q.kind == CDX_POL_STATIC_THRESHOLD && k < q.detect) next = q.detect;
+                if (q.kind == CDX_POL_K_STEP_THRESHOLD) {
+                    next = q.detect;
+                    if (next <= k) next += ((k - next) / q.recheck + 1) * q.recheck;
+                    next = next < q.cap ? next : q.cap;
+                }
+                g_units = next - k;
+                budget = static_cast<uint32_t>(g_units) * q.tpu;
+            }
+        }
     }
+    p.decision[i] = dec;
+    if (p.grant) p.grant[i] = g_units;
+    if (p.cap) p.cap[i] = cap;
+    return budget;
+}
+
+// The decision is the budget scan's loader: one pass decides every program and scans the
+// token budgets of the grants (each index is loaded exactly once by the scan)
+struct DecideLoad {
+    DecideParams p;
+    __device__ uint32_t operator()(uint64_t i) const { return decide_one(p, i); }
 };
+
+__global__ void mixed_decide_kernel(const __grid_constant__ DecideParams p) {
+    for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < p.N;
+         i += static_cast<uint64_t>(gridDim.x) * blockDim.x)
+        (void)decide_one(p, i);
+}
 
 unsigned grid_for(const cdx_ctx* ctx, uint64_t n, unsigned t) {
     const uint64_t want = (n + t - 1) / t;
@@ -256,6 +354,25 @@ extern "C" int cdx_cot_meets(cdx_ctx* ctx, const uint32_t* ids, const uint64_t* 
     if (smem > 200u * 1024u) return set_error(ctx, CDX_EINVAL, "cot_meets: rows too long for shared memory");
     const uint64_t want = (R + CM_WARPS * 32 - 1) / (CM_WARPS * 32);
     const unsigned grid = static_cast<unsigned>(std::min<uint64_t>(want, static_cast<uint64_t>(ctx->sm_count) * 8));
+    // lean kernel: P in {32, 64, 96, 128}, window 1..8, 16-byte aligned rows
+    if (P % 32 == 0 && P <= 128 && window <= 8 && (reinterpret_cast<uintptr_t>(ids) & 15u) == 0 &&
+        !getenv("CDX_COTM_GENERIC")) {
+        void (*k)(const uint32_t*, const uint64_t*, uint64_t, uint32_t, uint64_t, uint32_t, uint32_t*) = nullptr;
+#define CDX_COTM_W(Wv)                                                                               \
+    case Wv:                                                                                         \
+        k = P == 32 ? cot_meets_lean<Wv, 8> : P == 64 ? cot_meets_lean<Wv, 16>                       \
+                                           : P == 96 ? cot_meets_lean<Wv, 24> : cot_meets_lean<Wv, 32>; \
+        break;
+        switch (window) {
+            CDX_COTM_W(1) CDX_COTM_W(2) CDX_COTM_W(3) CDX_COTM_W(4)
+            CDX_COTM_W(5) CDX_COTM_W(6) CDX_COTM_W(7) CDX_COTM_W(8)
+        }
+#undef CDX_COTM_W
+        cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+        k<<<grid, CM_WARPS * 32, smem, ctx->stream>>>(ids, hes, R, stride, lut, notready, meets_bits);
+        CDX_CHECK_LAUNCH(ctx, "cot_meets(lean)");
+        return CDX_OK;
+    }
     auto launch = [&](auto kern) {
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
         kern<<<grid, CM_WARPS * 32, smem, ctx->stream>>>(ids, hes, R, P, stride, window, lut, notready, meets_bits);
@@ -317,9 +434,7 @@ extern "C" int cdx_mixed_allocate(cdx_ctx* ctx, const cdx_mixed_trace* tr, const
     const uint64_t tiles = (N + scan::SL_TILE - 1) / scan::SL_TILE;
     const size_t rec_off = bytes;
     bytes += (tiles + 2) * 8 + 16;
-    const size_t grant_off = bytes;  // grants (when the caller wants none) and offsets (ditto)
-    bytes += (N * 4 + 255) / 256 * 256;
-    const size_t offs_off = bytes;
+    const size_t offs_off = bytes;  // offsets when the caller wants only the total
     bytes += N * 8 + 64;
     uint8_t* s = static_cast<uint8_t*>(scratch3(ctx, bytes));
     if (!s) return set_error(ctx, CDX_ECUDA, "mixed_allocate: scratch allocation failed");
@@ -368,18 +483,13 @@ extern "C" int cdx_mixed_allocate(cdx_ctx* ctx, const cdx_mixed_trace* tr, const
     p.cap = cap;
     p.N = N;
     p.d_err = ctx->d_err;
-    int32_t* g_units = grant;
-    if (!g_units && (offsets || total_budget)) {  // the scan needs the grants: keep them in scratch
-        g_units = reinterpret_cast<int32_t*>(s + grant_off);
-        p.grant = g_units;
-    }
-    mixed_decide_kernel<<<grid_for(ctx, N, 256), 256, 0, ctx->stream>>>(p);
-    CDX_CHECK_LAUNCH(ctx, "mixed_allocate(decide)");
-    if (offsets || total_budget) {
-        LoadBudget ld{archetype, g_units, {p.pol[0].tpu, p.pol[1].tpu, p.pol[2].tpu, p.pol[3].tpu}};
+    if (offsets || total_budget) {  // decisions + budget scan in one single-pass kernel
         uint64_t* out = offsets ? reinterpret_cast<uint64_t*>(offsets) : reinterpret_cast<uint64_t*>(s + offs_off);
-        if (int st = scan::scan_excl(ctx, ld, N, out, false, rec, reinterpret_cast<uint64_t*>(total_budget)))
+        if (int st = scan::scan_excl(ctx, DecideLoad{p}, N, out, false, rec, reinterpret_cast<uint64_t*>(total_budget)))
             return st;
+    } else {
+        mixed_decide_kernel<<<grid_for(ctx, N, 256), 256, 0, ctx->stream>>>(p);
+        CDX_CHECK_LAUNCH(ctx, "mixed_allocate(decide)");
     }
     return CDX_OK;
 }
