@@ -287,17 +287,13 @@ __device__ __forceinline__ uint32_t decide_one(const DecideParams& p, uint64_t i
     return budget;
 }
 
-// The decision is the budget scan's loader: one pass decides every program and scans the
-// token budgets of the grants (each index is loaded exactly once by the scan)
-struct DecideLoad {
-    DecideParams p;
-    __device__ uint32_t operator()(uint64_t i) const { return decide_one(p, i); }
-};
-
-__global__ void mixed_decide_kernel(const __grid_constant__ DecideParams p) {
+// thread per program, coalesced; budget (nullable) = the grant's tokens, the scan's input
+__global__ void mixed_decide_kernel(const __grid_constant__ DecideParams p, uint32_t* __restrict__ budget) {
     for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < p.N;
-         i += static_cast<uint64_t>(gridDim.x) * blockDim.x)
-        (void)decide_one(p, i);
+         i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+        const uint32_t b = decide_one(p, i);
+        if (budget) budget[i] = b;
+    }
 }
 
 unsigned grid_for(const cdx_ctx* ctx, uint64_t n, unsigned t) {
@@ -434,6 +430,8 @@ extern "C" int cdx_mixed_allocate(cdx_ctx* ctx, const cdx_mixed_trace* tr, const
     const uint64_t tiles = (N + scan::SL_TILE - 1) / scan::SL_TILE;
     const size_t rec_off = bytes;
     bytes += (tiles + 2) * 8 + 16;
+    const size_t bud_off = bytes;  // per-program token budgets (the scan's input)
+    bytes += (N * 4 + 255) / 256 * 256;
     const size_t offs_off = bytes;  // offsets when the caller wants only the total
     bytes += N * 8 + 64;
     uint8_t* s = static_cast<uint8_t*>(scratch3(ctx, bytes));
@@ -483,13 +481,15 @@ extern "C" int cdx_mixed_allocate(cdx_ctx* ctx, const cdx_mixed_trace* tr, const
     p.cap = cap;
     p.N = N;
     p.d_err = ctx->d_err;
-    if (offsets || total_budget) {  // decisions + budget scan in one single-pass kernel
+    const bool scan_b = offsets || total_budget;
+    uint32_t* budget = scan_b ? reinterpret_cast<uint32_t*>(s + bud_off) : nullptr;
+    mixed_decide_kernel<<<grid_for(ctx, N, 256), 256, 0, ctx->stream>>>(p, budget);
+    CDX_CHECK_LAUNCH(ctx, "mixed_allocate(decide)");
+    if (scan_b) {  // exclusive scan of the grants' token budgets (K5's single-pass scan)
         uint64_t* out = offsets ? reinterpret_cast<uint64_t*>(offsets) : reinterpret_cast<uint64_t*>(s + offs_off);
-        if (int st = scan::scan_excl(ctx, DecideLoad{p}, N, out, false, rec, reinterpret_cast<uint64_t*>(total_budget)))
+        if (int st = scan::scan_excl(ctx, scan::LoadU32{budget}, N, out, false, rec,
+                                     reinterpret_cast<uint64_t*>(total_budget)))
             return st;
-    } else {
-        mixed_decide_kernel<<<grid_for(ctx, N, 256), 256, 0, ctx->stream>>>(p);
-        CDX_CHECK_LAUNCH(ctx, "mixed_allocate(decide)");
     }
     return CDX_OK;
 }
