@@ -604,8 +604,37 @@ def bench_cot(args, cfg, rank, world, cx, with_e2e=True):
     l0 = cx.launches
     ms, per, clocks = timed(args, world, step, ["cot_exit"])
     b = R * P * 4 + R * ((P + 63) // 64) * 8 + R * (4 + 1 + 4 + 1)
-    return dict(value=R * P * world / (ms / 1e3), ms=ms, launches=in_timed(cx, l0, args), clocks=clocks,
-                kernel="cot_exit", kernel_ms=per["cot_exit"], kernel_bytes=b, step_bytes=b, extra={}, e2e=None)
+    launches = in_timed(cx, l0, args)
+    e2e = None
+    if with_e2e and not args.no_e2e:
+        host = dict(ids=torch.empty((R, P), dtype=torch.int32, pin_memory=True),
+                    hes=torch.empty(hes.shape, dtype=torch.int64, pin_memory=True))
+        host["ids"].copy_(ids)
+        host["hes"].copy_(hes)
+        outs = {k: torch.empty((R,), dtype=dt, pin_memory=True) for k, dt in
+                (("exit_step", torch.int32), ("reason", torch.uint8), ("final_id", torch.int32),
+                 ("low_conf", torch.uint8))}
+        e2e = e2e_host(args, world, lambda: cx.cot_decide_host(host["ids"], host["hes"], pc, out=outs),
+                       R * P * world, R * P * 4 + hes.numel() * 8, R * 10,
+                       "cdx_cot_decide_host (C-ABI, pinned host buffers, wall clock)")
+    return dict(value=R * P * world / (ms / 1e3), ms=ms, launches=launches, clocks=clocks,
+                kernel="cot_exit", kernel_ms=per["cot_exit"], kernel_bytes=b, step_bytes=b, extra={}, e2e=e2e)
+
+
+def e2e_host(args, world, one, units, h2d, d2h, api):
+    """Time `one()` (a host-buffer entry: H2D + kernels + D2H, returns with results on the host)
+    on the wall clock; barrier on both sides, the slowest rank, whole-job throughput."""
+    for _ in range(max(1, min(args.warmup, 3))):
+        one()
+    steps = max(1, min(args.steps, 5))
+    barrier(world)
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        one()
+    dt = max_over_ranks((time.perf_counter() - t0) / steps, world)
+    barrier(world)
+    return {"value": units / dt, "unit": UNIT, "h2d_bytes_per_step": h2d * world, "d2h_bytes_per_step": d2h * world,
+            "ms_per_step": dt * 1e3, "api": api}
 
 
 def bench_reward(args, cfg, rank, world, cx, with_e2e=True):
@@ -632,9 +661,25 @@ def bench_reward(args, cfg, rank, world, cx, with_e2e=True):
     l0 = cx.launches
     ms, per, clocks = timed(args, world, step, ["reward_certaindex", "allocate_scan"])
     b = G * T * W * 8 + G * T * 8 + G * ((T + 31) // 32) * 4
-    return dict(value=G * T * W * world / (ms / 1e3), ms=ms, launches=in_timed(cx, l0, args),
+    launches = in_timed(cx, l0, args)
+    e2e = None
+    if with_e2e and not args.no_e2e:
+        host = dict(rw=torch.empty((G, T, W), dtype=torch.float32, pin_memory=True),
+                    ids=torch.empty((G, T, W), dtype=torch.int32, pin_memory=True),
+                    agg=torch.empty((G,), dtype=torch.uint8, pin_memory=True))
+        host["rw"].copy_(rw)
+        host["ids"].copy_(ids)
+        host["agg"].copy_(agg)
+        outs = {k: torch.empty(shape, dtype=dt, pin_memory=True) for k, shape, dt in
+                (("exit_knob", (G,), torch.int32), ("reason", (G,), torch.uint8), ("offsets", (G,), torch.int64),
+                 ("R", (G, T), torch.float32))}
+        e2e = e2e_host(args, world, lambda: cx.reward_decide_host(host["rw"], host["ids"], host["agg"], thm, thx, pol,
+                                                                  out=outs),
+                       G * T * W * world, G * T * W * 8 + G, G * (4 + 1 + 8 + T * 4),
+                       "cdx_reward_decide_host (C-ABI, pinned host buffers, wall clock)")
+    return dict(value=G * T * W * world / (ms / 1e3), ms=ms, launches=launches,
                 clocks=clocks, kernel="reward_certaindex", kernel_ms=per["reward_certaindex"], kernel_bytes=b,
-                step_bytes=b + G * 21, extra={"allocate_scan_ms": per["allocate_scan"]}, e2e=None)
+                step_bytes=b + G * 21, extra={"allocate_scan_ms": per["allocate_scan"]}, e2e=e2e)
 
 
 def bench_gang(args, cfg, rank, world, cx, with_e2e=True):
@@ -665,10 +710,27 @@ def bench_gang(args, cfg, rank, world, cx, with_e2e=True):
 
     l0 = cx.launches
     ms, per, clocks = timed(args, world, step, ["gang_priority"])
-    b = gn * (8 + 8 + 8 + 4 + 2 + 2 + 1) + gn * 4
-    return dict(value=N / (ms / 1e3), ms=ms, launches=in_timed(cx, l0, args), clocks=clocks,
+    b = gn * (8 + 8 + 8 + 4 + 4 + 4 + 1) + gn * 4
+    launches = in_timed(cx, l0, args)
+    e2e = None
+    if with_e2e and not args.no_e2e:
+        host = {k: torch.empty(v.shape, dtype=v.dtype, pin_memory=True) for k, v in dev.items()}
+        for k, v in dev.items():
+            host[k].copy_(v)
+        stage = {k: torch.empty_like(v) for k, v in dev.items()}
+        res = {}
+
+        def one():
+            for k, v in host.items():
+                stage[k].copy_(v, non_blocking=True)
+            order = cx.gang_priority(stage, pol, now)[0] if world == 1 else \
+                sh.gang_order(stage, pol, now, g0, stride)[0]
+            res["order"] = order.cpu()
+        e2e = e2e_host(args, world, one, N, sum(v.numel() * v.element_size() for v in host.values()), gn * 4,
+                       "Context.gang_priority (C-ABI) from pinned host buffers, order read back, wall clock")
+    return dict(value=N / (ms / 1e3), ms=ms, launches=launches, clocks=clocks,
                 kernel="gang_priority (radix sort, all passes)" + (" + allgather + merge" if world > 1 else ""),
-                kernel_ms=per["gang_priority"], kernel_bytes=b, step_bytes=b, extra={}, e2e=None,
+                kernel_ms=per["gang_priority"], kernel_bytes=b, step_bytes=b, extra={}, e2e=e2e,
                 scaling="strong")
 
 
@@ -688,11 +750,24 @@ def bench_jsonl(args, cfg, rank, world, cx, with_e2e=True):
 
     l0 = cx.launches
     ms, per, clocks = timed(args, world, step, ["jsonl_parse"], cfg.get("flush_l2", False))
+    launches = in_timed(cx, l0, args)
     n = out["n_records"]
     b = len(text) + n * (4 + 4 + 8 + 1 + 8 + 8) + n * 8
-    return dict(value=n * world / (ms / 1e3), ms=ms, launches=in_timed(cx, l0, args), clocks=clocks,
+    e2e = None
+    if with_e2e and not args.no_e2e:
+        host_text = torch.frombuffer(bytearray(text), dtype=torch.uint8).pin_memory()
+        stage = torch.empty_like(dev)
+        keep = {}
+
+        def one():
+            stage.copy_(host_text, non_blocking=True)
+            o = cx.jsonl_parse(stage, cap)
+            keep.update({k: o[k][:o["n_records"]].cpu() for k in ("program", "step_index", "token_offset", "hesitant")})
+        e2e = e2e_host(args, world, one, n * world, len(text), n * 17,
+                       "Context.jsonl_parse (C-ABI) from a pinned host text buffer, records read back, wall clock")
+    return dict(value=n * world / (ms / 1e3), ms=ms, launches=launches, clocks=clocks,
                 kernel="jsonl_parse (all passes)", kernel_ms=per["jsonl_parse"], kernel_bytes=b, step_bytes=b,
-                extra={"text_bytes": len(text)}, e2e=None)
+                extra={"text_bytes": len(text)}, e2e=e2e)
 
 
 def bench_mixed(args, cfg, rank, world, cx, with_e2e=True):
@@ -822,7 +897,8 @@ BENCH = {"mixed": bench_mixed, "sc": bench_sc, "cot": bench_cot, "reward": bench
 
 def summarize(name, cfg, res, peak):
     ach = res["kernel_bytes"] / (res["kernel_ms"] / 1e3) / 1e9
-    return {"value": res["value"], "unit": UNIT, "ms_per_step": res["ms"], "desc": cfg["desc"],
+    return {"value": res["value"], "unit": UNIT, "ms_per_step": res["ms"], "desc": cfg["desc"], "e2e": res.get("e2e"),
+            "gpu_launches": res["launches"], "clocks": res["clocks"],
             "kernel": res["kernel"], "kernel_ms": res["kernel_ms"], "achieved_gbs": ach, "frac": ach / peak,
             "frac_nominal": ach / NOMINAL_HBM_GBS,
             "l2": "flushed before every timed step" if cfg.get("flush_l2") else "inputs > L2", **res["extra"]}
@@ -860,7 +936,7 @@ def main():
         for name, c in CONFIGS.items():
             if name == args.config:
                 continue
-            r = BENCH[c["kind"]](sub, c, 0, 1, cx, with_e2e=False)
+            r = BENCH[c["kind"]](sub, c, 0, 1, cx, with_e2e=True)
             others[name] = summarize(name, c, r, peak)
             if not args.no_cpu_baseline:
                 others[name]["cpu_baseline"] = cpu_baseline(name, c)

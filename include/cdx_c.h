@@ -469,6 +469,26 @@ int cdx_sc_decide_host(cdx_ctx* ctx, const uint32_t* ids_host, uint64_t R, uint3
                        uint8_t* reason_host, int64_t* offsets_host, float* hcert_host,
                        int64_t* tokens_saved_host);
 
+/* probe::should_exit at every prefix + final_answer (as cdx_cot_exit) from HOST buffers:
+ * ids u32[R][P], hes u64[R][ceil(P/64)], offsets i64[R][P] (nullable: (p+1)*interval).
+ * Outputs to host: exit_step i32[R], reason u8[R], final_id u32[R] (nullable), low_conf u8[R]
+ * (nullable).  Chunked and double buffered like cdx_sc_decide_host.                        */
+int cdx_cot_decide_host(cdx_ctx* ctx, const uint32_t* ids_host, const uint64_t* hes_host,
+                        const int64_t* offsets_host, uint64_t R, uint32_t P, const cdx_probe_cfg* cfg,
+                        int32_t* exit_step_host, uint8_t* reason_host, uint32_t* final_id_host,
+                        uint8_t* low_conf_host);
+
+/* MCTS/Rebase certaindex (as cdx_reward_certaindex) + allocate (as cdx_allocate_scan, knob
+ * unit = step) from HOST buffers: rewards f32[G][T][W], ids u32[G][T][W] (nullable), agg
+ * u8[G].  Outputs to host: exit_knob i32[G], reason u8[G], offsets i64[G] (global across
+ * chunks), R f32[G][T] (nullable), *tokens_saved_host (nullable).                          */
+int cdx_reward_decide_host(cdx_ctx* ctx, const float* rewards_host, const uint32_t* ids_host,
+                           const uint8_t* agg_host, uint64_t G, uint32_t T, uint32_t W,
+                           const cdx_threshold* th_mean, uint32_t n_th_mean,
+                           const cdx_threshold* th_max, uint32_t n_th_max, const cdx_alloc_policy* pol,
+                           int32_t* exit_knob_host, uint8_t* reason_host, int64_t* offsets_host,
+                           float* R_host, int64_t* tokens_saved_host);
+
 #ifdef __cplusplus
 }
 #endif

@@ -334,6 +334,76 @@ class Context:
                                                 pols, _ptr(dec), _ptr(grant), _ptr(cap), _ptr(offs), _ptr(total)))
         return dict(decision=dec[:N], grant=grant[:N], cap=cap[:N], offsets=offs[:N], total=total)
 
+    # -- end-to-end entries from HOST buffers (chunked H2D / kernels / D2H, double buffered) --
+    @staticmethod
+    def _host(a):
+        """(pointer, keep-alive) of a host array: numpy array or CPU torch tensor."""
+        if a is None:
+            return None, None
+        if hasattr(a, "data_ptr"):
+            assert not a.is_cuda, "host entry points take host buffers"
+            return a.data_ptr(), a
+        import numpy as np
+        a = np.ascontiguousarray(a)
+        return a.ctypes.data, a
+
+    def sc_decide_host(self, ids, thresholds, policy: AllocPolicy, want_hcert: bool = False):
+        import numpy as np
+        R, P, S = ids.shape
+        out = dict(exit_knob=np.empty(R, np.int32), reason=np.empty(R, np.uint8), offsets=np.empty(R, np.int64),
+                   hcert=np.empty((R, P), np.float32) if want_hcert else None)
+        p_ids, keep = self._host(ids)
+        arr, n = c_thresholds(thresholds)
+        pol = c_policy(policy)
+        saved = C.c_int64(0)
+        self._check(self.lib.cdx_sc_decide_host(self.h, p_ids, R, P, S, arr, n, C.byref(pol),
+                                                out["exit_knob"].ctypes.data, out["reason"].ctypes.data,
+                                                out["offsets"].ctypes.data,
+                                                out["hcert"].ctypes.data if want_hcert else None, C.byref(saved)))
+        out["tokens_saved"] = saved.value
+        del keep
+        return out
+
+    def cot_decide_host(self, ids, hes, cfg: ProbeConfig, offsets=None, out=None):
+        import numpy as np
+        R, P = ids.shape
+        o = out or {}
+        res = {k: o[k] if k in o else np.empty(R, dt) for k, dt in (("exit_step", np.int32), ("reason", np.uint8),
+                                                                     ("final_id", np.uint32), ("low_conf", np.uint8))}
+        p_ids, k1 = self._host(ids)
+        p_hes, k2 = self._host(hes)
+        p_off, k3 = self._host(offsets)
+        c = c_probe(cfg)
+        ptr = lambda a: a.ctypes.data if hasattr(a, "ctypes") else a.data_ptr()  # noqa: E731
+        self._check(self.lib.cdx_cot_decide_host(self.h, p_ids, p_hes, p_off, R, P, C.byref(c),
+                                                 *[ptr(res[k]) for k in ("exit_step", "reason", "final_id",
+                                                                         "low_conf")]))
+        del k1, k2, k3
+        return res
+
+    def reward_decide_host(self, rewards, ids, agg, th_mean, th_max, policy: AllocPolicy, want_R: bool = False,
+                           out=None):
+        import numpy as np
+        G, T, W = rewards.shape
+        o = out or {}
+        res = {k: o[k] if k in o else np.empty(G, dt) for k, dt in (("exit_knob", np.int32), ("reason", np.uint8),
+                                                                     ("offsets", np.int64))}
+        res["R"] = o.get("R") if "R" in o else (np.empty((G, T), np.float32) if want_R else None)
+        p_rw, k1 = self._host(rewards)
+        p_ids, k2 = self._host(ids)
+        p_agg, k3 = self._host(agg)
+        a1, n1 = c_thresholds(th_mean)
+        a2, n2 = c_thresholds(th_max)
+        pol = c_policy(policy)
+        saved = C.c_int64(0)
+        ptr = lambda a: None if a is None else (a.ctypes.data if hasattr(a, "ctypes") else a.data_ptr())  # noqa
+        self._check(self.lib.cdx_reward_decide_host(self.h, p_rw, p_ids, p_agg, G, T, W, a1, n1, a2, n2, C.byref(pol),
+                                                    ptr(res["exit_knob"]), ptr(res["reason"]), ptr(res["offsets"]),
+                                                    ptr(res["R"]), C.byref(saved)))
+        res["tokens_saved"] = saved.value
+        del k1, k2, k3
+        return res
+
     # -- K3 --
     def cot_exit(self, ids, hes, cfg: ProbeConfig, offsets=None, want_ck: bool = False, out=None):
         t = self.torch

@@ -126,6 +126,9 @@ SIGNATURES = {
     "cdx_libm_exp": (C.c_int, [P, P, U64, P]),
     "cdx_sc_decide_host": (C.c_int, [P, P, U64, U32, U32, C.POINTER(Threshold), U32, C.POINTER(AllocPolicy),
                                      P, P, P, P, P]),
+    "cdx_cot_decide_host": (C.c_int, [P, P, P, P, U64, U32, C.POINTER(ProbeCfg), P, P, P, P]),
+    "cdx_reward_decide_host": (C.c_int, [P, P, P, P, U64, U32, U32, C.POINTER(Threshold), U32, C.POINTER(Threshold),
+                                         U32, C.POINTER(AllocPolicy), P, P, P, P, P]),
 }
 
 _lib = None

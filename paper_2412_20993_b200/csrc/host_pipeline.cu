@@ -1,12 +1,19 @@
-// host_pipeline.cu — end-to-end entry from HOST buffers: cdx_sc_decide_host.
+// host_pipeline.cu — end-to-end entries from HOST buffers (the reference-facing calls a serving
+// loop makes with traces that live in host memory):
 //
-// The reference-facing call a serving loop makes with answers that live in host memory:
-// ids stream through the device in chunks of whole requests on a copy stream, double
-// buffered against K2 (sc_certaindex) + K5 (allocate_scan) on the compute stream; budget
-// offsets are made global across chunks on the device; results come back with one D2H per
-// chunk.  Returns when every result is in the caller's host buffers.
+//   cdx_sc_decide_host      K2 sc_certaindex + K5 allocate_scan   (configs A, C)
+//   cdx_cot_decide_host     K3 cot_exit                           (config B)
+//   cdx_reward_decide_host  K4 reward_certaindex + K5             (config D)
+//
+// All three share one pipeline: the inputs stream through the device in chunks of whole
+// requests / programs on a copy stream, double buffered against the kernels on the compute
+// stream; results come back with one D2H per output per chunk; token-budget offsets are made
+// global across chunks on the device.  Each call returns when every result is in the
+// caller's host buffers (pinned buffers give full PCIe bandwidth; pageable ones work too).
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
+#include <vector>
 
 #include "cdx_internal.cuh"
 
@@ -25,31 +32,31 @@ __global__ void accumulate(const int64_t* __restrict__ scal, int64_t* __restrict
     acc[1] += scal[1];
 }
 
-}  // namespace
-}  // namespace cdx
+// one host array streamed per chunk: `unit` bytes per request / program
+struct Stream {
+    const void* in;  // host input (nullptr: an output)
+    void* out;       // host output
+    uint64_t unit;
+};
 
-extern "C" int cdx_sc_decide_host(cdx_ctx* ctx, const uint32_t* ids_host, uint64_t R, uint32_t P, uint32_t S,
-                                  const cdx_threshold* th, uint32_t n_th, const cdx_alloc_policy* pol,
-                                  int32_t* exit_knob_host, uint8_t* reason_host, int64_t* offsets_host,
-                                  float* hcert_host, int64_t* tokens_saved_host) {
-    using namespace cdx;
-    if (!ctx) return CDX_EINVAL;
-    if (!ids_host || !pol || !exit_knob_host || !reason_host || !offsets_host)
-        return set_error(ctx, CDX_EINVAL, "sc_decide_host: null pointer");
-    if (P == 0 || S == 0) return set_error(ctx, CDX_EINVAL, "sc_decide_host: empty shape");
-    if (R == 0) {
-        if (tokens_saved_host) *tokens_saved_host = 0;
-        return CDX_OK;
-    }
-    const uint64_t req_bytes = static_cast<uint64_t>(P) * S * 4u;
-    uint64_t chunk = std::max<uint64_t>(1, (256ull << 20) / req_bytes);  // ~256 MB of ids per chunk
-    chunk = std::min<uint64_t>(chunk, R);
-    const uint32_t words = (P + 31) / 32;
-    // per buffer: ids | hcert | meets | exit | reason | granted | offsets | kept | scalars
+// Chunked, double-buffered host pipeline.  `arrays` lists every host input and output with
+// its bytes per unit; `scratch_unit` is per-unit device scratch the kernels may use (not
+// copied).  compute(r0, nr, dev, scratch, acc) enqueues the kernels of one chunk on
+// ctx->stream (the compute stream) reading dev[k] for inputs and writing dev[k] for outputs;
+// acc is 16 bytes of device state carried across chunks (zeroed once).
+template <class F>
+int pipeline(cdx_ctx* ctx, const char* name, uint64_t n, const std::vector<Stream>& arrays, uint64_t scratch_unit,
+             int64_t* acc_out, F compute) {
+    uint64_t in_unit = 0;
+    for (const auto& a : arrays) in_unit += a.in ? a.unit : 0;
+    // ~256 MB of inputs per chunk (CDX_PIPE_CHUNK_KB overrides: tests of the chunk seams)
+    uint64_t chunk_bytes = 256ull << 20;
+    if (const char* e = getenv("CDX_PIPE_CHUNK_KB")) chunk_bytes = std::max<uint64_t>(1, strtoull(e, nullptr, 10)) << 10;
+    uint64_t chunk = std::max<uint64_t>(1, chunk_bytes / std::max<uint64_t>(1, in_unit));
+    chunk = std::min<uint64_t>(chunk, n);
     auto al = [](uint64_t b) { return (b + 255) / 256 * 256; };
-    const uint64_t b_ids = al(chunk * req_bytes), b_h = al(chunk * P * 4), b_m = al(chunk * words * 4);
-    const uint64_t b_e = al(chunk * 4), b_r = al(chunk), b_g = al(chunk * 4), b_o = al(chunk * 8), b_k = al(chunk * 4);
-    const uint64_t per = b_ids + b_h + b_m + b_e + b_r + b_g + b_o + b_k + 256;
+    uint64_t per = al(chunk * scratch_unit) + 256;
+    for (const auto& a : arrays) per += al(chunk * a.unit);
     const uint64_t need = 2 * per + 256;
     if (ctx->pipe_bytes < need) {
         if (ctx->pipe_buf) {
@@ -58,41 +65,21 @@ extern "C" int cdx_sc_decide_host(cdx_ctx* ctx, const uint32_t* ids_host, uint64
         }
         ctx->pipe_buf = nullptr;
         ctx->pipe_bytes = 0;
-        if (cudaMalloc(&ctx->pipe_buf, need) != cudaSuccess) return set_error(ctx, CDX_ECUDA, "sc_decide_host: alloc");
+        if (cudaMalloc(&ctx->pipe_buf, need) != cudaSuccess)
+            return set_error(ctx, CDX_ECUDA, std::string(name) + ": pipeline buffer allocation failed");
         ctx->pipe_bytes = need;
     }
     uint8_t* base = static_cast<uint8_t*>(ctx->pipe_buf);
     int64_t* acc = reinterpret_cast<int64_t*>(base + 2 * per);
-    struct Buf {
-        uint32_t* ids;
-        float* h;
-        uint32_t* meets;
-        int32_t* exit;
-        uint8_t* reason;
-        int32_t* granted;
-        int64_t* off;
-        uint32_t* kept;
-        int64_t* scal;
-    } buf[2];
+    std::vector<void*> dev[2];
+    void* scr[2];
     for (int i = 0; i < 2; ++i) {
         uint8_t* q = base + i * per;
-        buf[i].ids = reinterpret_cast<uint32_t*>(q);
-        q += b_ids;
-        buf[i].h = reinterpret_cast<float*>(q);
-        q += b_h;
-        buf[i].meets = reinterpret_cast<uint32_t*>(q);
-        q += b_m;
-        buf[i].exit = reinterpret_cast<int32_t*>(q);
-        q += b_e;
-        buf[i].reason = q;
-        q += b_r;
-        buf[i].granted = reinterpret_cast<int32_t*>(q);
-        q += b_g;
-        buf[i].off = reinterpret_cast<int64_t*>(q);
-        q += b_o;
-        buf[i].kept = reinterpret_cast<uint32_t*>(q);
-        q += b_k;
-        buf[i].scal = reinterpret_cast<int64_t*>(q);
+        for (const auto& a : arrays) {
+            dev[i].push_back(q);
+            q += al(chunk * a.unit);
+        }
+        scr[i] = q;
     }
     cudaStream_t user = ctx->stream;
     cudaStream_t comp = ctx->own_stream, copy = ctx->copy_stream;
@@ -104,40 +91,35 @@ extern "C" int cdx_sc_decide_host(cdx_ctx* ctx, const uint32_t* ids_host, uint64
     cudaMemsetAsync(acc, 0, 16, comp);
     int st = CDX_OK;
     ctx->stream = comp;
-    const uint64_t nchunks = (R + chunk - 1) / chunk;
+    const uint64_t nchunks = (n + chunk - 1) / chunk;
     auto upload = [&](uint64_t c) {
-        const uint64_t r0 = c * chunk, nr = std::min(chunk, R - r0);
+        const uint64_t r0 = c * chunk, nr = std::min(chunk, n - r0);
         cudaStreamWaitEvent(copy, consumed[c & 1], 0);
-        cudaMemcpyAsync(buf[c & 1].ids, ids_host + r0 * P * S, nr * req_bytes, cudaMemcpyHostToDevice, copy);
+        for (size_t k = 0; k < arrays.size(); ++k)
+            if (arrays[k].in)
+                cudaMemcpyAsync(dev[c & 1][k], static_cast<const uint8_t*>(arrays[k].in) + r0 * arrays[k].unit,
+                                nr * arrays[k].unit, cudaMemcpyHostToDevice, copy);
         cudaEventRecord(loaded[c & 1], copy);
     };
     for (int i = 0; i < 2; ++i) cudaEventRecord(consumed[i], comp);
     upload(0);
     for (uint64_t c = 0; c < nchunks && st == CDX_OK; ++c) {
         if (c + 1 < nchunks) upload(c + 1);
-        const uint64_t r0 = c * chunk, nr = std::min(chunk, R - r0);
-        Buf& b = buf[c & 1];
+        const uint64_t r0 = c * chunk, nr = std::min(chunk, n - r0);
         cudaStreamWaitEvent(comp, loaded[c & 1], 0);
-        st = cdx_sc_certaindex(ctx, b.ids, nr, P, S, th, n_th, hcert_host ? b.h : nullptr, b.meets);
+        st = compute(r0, nr, dev[c & 1], scr[c & 1], acc);
         if (st) break;
-        cudaEventRecord(consumed[c & 1], comp);  // ids buffer free once K2 has read it
-        st = cdx_allocate_scan(ctx, b.meets, nr, P, pol, 0, static_cast<uint32_t>(r0), b.exit, b.reason, b.granted,
-                               b.off, b.kept, reinterpret_cast<uint64_t*>(b.scal), b.scal + 1, b.scal + 2);
-        if (st) break;
-        add_base<<<static_cast<unsigned>(std::min<uint64_t>((nr + 255) / 256, 1184)), 256, 0, comp>>>(b.off, nr, acc);
-        CDX_CHECK_LAUNCH(ctx, "sc_decide_host(offsets)");
-        accumulate<<<1, 1, 0, comp>>>(b.scal, acc);
-        CDX_CHECK_LAUNCH(ctx, "sc_decide_host(totals)");
-        cudaMemcpyAsync(exit_knob_host + r0, b.exit, nr * 4, cudaMemcpyDeviceToHost, comp);
-        cudaMemcpyAsync(reason_host + r0, b.reason, nr, cudaMemcpyDeviceToHost, comp);
-        cudaMemcpyAsync(offsets_host + r0, b.off, nr * 8, cudaMemcpyDeviceToHost, comp);
-        if (hcert_host) cudaMemcpyAsync(hcert_host + r0 * P, b.h, nr * P * 4, cudaMemcpyDeviceToHost, comp);
+        cudaEventRecord(consumed[c & 1], comp);
+        for (size_t k = 0; k < arrays.size(); ++k)
+            if (arrays[k].out)
+                cudaMemcpyAsync(static_cast<uint8_t*>(arrays[k].out) + r0 * arrays[k].unit, dev[c & 1][k],
+                                nr * arrays[k].unit, cudaMemcpyDeviceToHost, comp);
     }
     int64_t hacc[2] = {0, 0};
     if (st == CDX_OK) {
         cudaMemcpyAsync(hacc, acc, 16, cudaMemcpyDeviceToHost, comp);
         cudaError_t e = cudaStreamSynchronize(comp);
-        if (e != cudaSuccess) st = cuda_fail(ctx, e, "sc_decide_host");
+        if (e != cudaSuccess) st = cuda_fail(ctx, e, name);
     } else {
         cudaStreamSynchronize(comp);
     }
@@ -147,6 +129,143 @@ extern "C" int cdx_sc_decide_host(cdx_ctx* ctx, const uint32_t* ids_host, uint64
         cudaEventDestroy(consumed[i]);
     }
     ctx->stream = user;
-    if (st == CDX_OK && tokens_saved_host) *tokens_saved_host = hacc[1];
+    if (st == CDX_OK && acc_out) {
+        acc_out[0] = hacc[0];
+        acc_out[1] = hacc[1];
+    }
+    if (st == CDX_OK) st = cdx_sync(ctx);  // device-side validation errors of the whole call
+    return st;
+}
+
+// K5 on a chunk's meets bits, offsets made global with the running base in acc[0]
+int allocate_chunk(cdx_ctx* ctx, const char* name, const uint32_t* meets, uint64_t nr, uint32_t P,
+                   const cdx_alloc_policy* pol, uint64_t r0, int32_t* exit, uint8_t* reason, int64_t* off,
+                   uint8_t* scr, int64_t* acc) {
+    int32_t* granted = reinterpret_cast<int32_t*>(scr);
+    uint32_t* kept = reinterpret_cast<uint32_t*>(scr + (nr * 4 + 255) / 256 * 256);
+    int64_t* scal = reinterpret_cast<int64_t*>(scr + 2 * ((nr * 4 + 255) / 256 * 256));
+    if (int st = cdx_allocate_scan(ctx, meets, nr, P, pol, 0, static_cast<uint32_t>(r0), exit, reason, granted, off,
+                                   kept, reinterpret_cast<uint64_t*>(scal), scal + 1, scal + 2))
+        return st;
+    add_base<<<static_cast<unsigned>(std::min<uint64_t>((nr + 255) / 256, 1184)), 256, 0, ctx->stream>>>(off, nr, acc);
+    CDX_CHECK_LAUNCH(ctx, name);
+    accumulate<<<1, 1, 0, ctx->stream>>>(scal, acc);
+    CDX_CHECK_LAUNCH(ctx, name);
+    return CDX_OK;
+}
+constexpr uint64_t ALLOC_SCRATCH_UNIT = 8 + 64;  // granted + kept per unit (+ alignment slack)
+
+}  // namespace
+}  // namespace cdx
+
+extern "C" int cdx_sc_decide_host(cdx_ctx* ctx, const uint32_t* ids_host, uint64_t R, uint32_t P, uint32_t S,
+                                  const cdx_threshold* th, uint32_t n_th, const cdx_alloc_policy* pol,
+                                  int32_t* exit_knob_host, uint8_t* reason_host, int64_t* offsets_host,
+                                  float* hcert_host, int64_t* tokens_saved_host) {
+    using namespace cdx;
+    CDX_NVTX("cdx_sc_decide_host");
+    if (!ctx) return CDX_EINVAL;
+    if (!ids_host || !pol || !exit_knob_host || !reason_host || !offsets_host)
+        return set_error(ctx, CDX_EINVAL, "sc_decide_host: null pointer");
+    if (P == 0 || S == 0) return set_error(ctx, CDX_EINVAL, "sc_decide_host: empty shape");
+    if (R == 0) {
+        if (tokens_saved_host) *tokens_saved_host = 0;
+        return CDX_OK;
+    }
+    const uint32_t words = (P + 31) / 32;
+    // arrays: ids in | meets (device only) | exit | reason | offsets | hcert
+    std::vector<Stream> arr = {{ids_host, nullptr, static_cast<uint64_t>(P) * S * 4},
+                               {nullptr, nullptr, static_cast<uint64_t>(words) * 4},
+                               {nullptr, exit_knob_host, 4},
+                               {nullptr, reason_host, 1},
+                               {nullptr, offsets_host, 8},
+                               {nullptr, hcert_host, hcert_host ? static_cast<uint64_t>(P) * 4 : 0}};
+    int64_t acc[2];
+    const int st = pipeline(ctx, "sc_decide_host", R, arr, ALLOC_SCRATCH_UNIT, acc,
+                            [&](uint64_t r0, uint64_t nr, std::vector<void*>& d, void* scr, int64_t* dacc) {
+                                auto* meets = static_cast<uint32_t*>(d[1]);
+                                if (int s = cdx_sc_certaindex(ctx, static_cast<const uint32_t*>(d[0]), nr, P, S, th, n_th,
+                                                              hcert_host ? static_cast<float*>(d[5]) : nullptr, meets))
+                                    return s;
+                                return allocate_chunk(ctx, "sc_decide_host", meets, nr, P, pol, r0,
+                                                      static_cast<int32_t*>(d[2]), static_cast<uint8_t*>(d[3]),
+                                                      static_cast<int64_t*>(d[4]), static_cast<uint8_t*>(scr), dacc);
+                            });
+    if (st == CDX_OK && tokens_saved_host) *tokens_saved_host = acc[1];
+    return st;
+}
+
+extern "C" int cdx_cot_decide_host(cdx_ctx* ctx, const uint32_t* ids_host, const uint64_t* hes_host,
+                                   const int64_t* offsets_host, uint64_t R, uint32_t P, const cdx_probe_cfg* cfg,
+                                   int32_t* exit_step_host, uint8_t* reason_host, uint32_t* final_id_host,
+                                   uint8_t* low_conf_host) {
+    using namespace cdx;
+    CDX_NVTX("cdx_cot_decide_host");
+    if (!ctx) return CDX_EINVAL;
+    if (!ids_host || !hes_host || !cfg || !exit_step_host || !reason_host)
+        return set_error(ctx, CDX_EINVAL, "cot_decide_host: null pointer");
+    if (P == 0) return set_error(ctx, CDX_EINVAL, "final_answer: empty trace");
+    if (R == 0) return CDX_OK;
+    const uint32_t hw = (P + 63) / 64;
+    // arrays: ids | hes | offsets | exit | reason | final | low
+    std::vector<Stream> arr = {{ids_host, nullptr, static_cast<uint64_t>(P) * 4},
+                               {hes_host, nullptr, static_cast<uint64_t>(hw) * 8},
+                               {offsets_host, nullptr, offsets_host ? static_cast<uint64_t>(P) * 8 : 0},
+                               {nullptr, exit_step_host, 4},
+                               {nullptr, reason_host, 1},
+                               {nullptr, final_id_host, final_id_host ? 4u : 0u},
+                               {nullptr, low_conf_host, low_conf_host ? 1u : 0u}};
+    return pipeline(ctx, "cot_decide_host", R, arr, 0, nullptr,
+                    [&](uint64_t, uint64_t nr, std::vector<void*>& d, void*, int64_t*) {
+                        return cdx_cot_exit(ctx, static_cast<const uint32_t*>(d[0]), static_cast<const uint64_t*>(d[1]),
+                                            offsets_host ? static_cast<const int64_t*>(d[2]) : nullptr, nr, P, cfg,
+                                            static_cast<int32_t*>(d[3]), static_cast<uint8_t*>(d[4]),
+                                            final_id_host ? static_cast<uint32_t*>(d[5]) : nullptr,
+                                            low_conf_host ? static_cast<uint8_t*>(d[6]) : nullptr, nullptr);
+                    });
+}
+
+extern "C" int cdx_reward_decide_host(cdx_ctx* ctx, const float* rewards_host, const uint32_t* ids_host,
+                                      const uint8_t* agg_host, uint64_t G, uint32_t T, uint32_t W,
+                                      const cdx_threshold* th_mean, uint32_t n_th_mean, const cdx_threshold* th_max,
+                                      uint32_t n_th_max, const cdx_alloc_policy* pol, int32_t* exit_knob_host,
+                                      uint8_t* reason_host, int64_t* offsets_host, float* R_host,
+                                      int64_t* tokens_saved_host) {
+    using namespace cdx;
+    CDX_NVTX("cdx_reward_decide_host");
+    if (!ctx) return CDX_EINVAL;
+    if (!rewards_host || !agg_host || !pol || !exit_knob_host || !reason_host || !offsets_host)
+        return set_error(ctx, CDX_EINVAL, "reward_decide_host: null pointer");
+    if (T == 0 || W == 0) return set_error(ctx, CDX_EINVAL, "certaindex_reward: empty reward set");
+    if (G == 0) {
+        if (tokens_saved_host) *tokens_saved_host = 0;
+        return CDX_OK;
+    }
+    const uint64_t node = static_cast<uint64_t>(T) * W;
+    const uint32_t words = (T + 31) / 32;
+    // arrays: rewards | ids | agg | meets (device) | exit | reason | offsets | R
+    std::vector<Stream> arr = {{rewards_host, nullptr, node * 4},
+                               {ids_host, nullptr, ids_host ? node * 4 : 0},
+                               {agg_host, nullptr, 1},
+                               {nullptr, nullptr, static_cast<uint64_t>(words) * 4},
+                               {nullptr, exit_knob_host, 4},
+                               {nullptr, reason_host, 1},
+                               {nullptr, offsets_host, 8},
+                               {nullptr, R_host, R_host ? static_cast<uint64_t>(T) * 4 : 0}};
+    int64_t acc[2];
+    const int st = pipeline(ctx, "reward_decide_host", G, arr, ALLOC_SCRATCH_UNIT, acc,
+                            [&](uint64_t r0, uint64_t nr, std::vector<void*>& d, void* scr, int64_t* dacc) {
+                                auto* meets = static_cast<uint32_t*>(d[3]);
+                                if (int s = cdx_reward_certaindex(
+                                        ctx, static_cast<const float*>(d[0]),
+                                        ids_host ? static_cast<const uint32_t*>(d[1]) : nullptr,
+                                        static_cast<const uint8_t*>(d[2]), nr, T, W, th_mean, n_th_mean, th_max,
+                                        n_th_max, R_host ? static_cast<float*>(d[7]) : nullptr, nullptr, meets))
+                                    return s;
+                                return allocate_chunk(ctx, "reward_decide_host", meets, nr, T, pol, r0,
+                                                      static_cast<int32_t*>(d[4]), static_cast<uint8_t*>(d[5]),
+                                                      static_cast<int64_t*>(d[6]), static_cast<uint8_t*>(scr), dacc);
+                            });
+    if (st == CDX_OK && tokens_saved_host) *tokens_saved_host = acc[1];
     return st;
 }
