@@ -109,6 +109,18 @@ struct ScShape {
 void sc_certaindex(Context& cx, const uint32_t* ids, const ScShape& shape,
                    std::span<const metrics::SignalThreshold> thresholds, float* hcert, uint32_t* meets);
 
+// Majority-fraction certaindex (largest cluster / S: the share of the plurality answer,
+// runtime.cpp:317-334) thresholds, ANDed with the entropy thresholds above.
+struct MajorityThreshold {
+    double cutoff = 0.5;
+    metrics::ThresholdDir direction = metrics::ThresholdDir::GreaterEq;
+};
+// The same plus majority f32[R][P] (nullable) and majority thresholds.
+void sc_certaindex(Context& cx, const uint32_t* ids, const ScShape& shape,
+                   std::span<const metrics::SignalThreshold> thresholds,
+                   std::span<const MajorityThreshold> majority_thresholds, float* hcert, float* majority,
+                   uint32_t* meets);
+
 struct AllocationOutputs {
     int32_t* exit_knob = nullptr;  // i32[R]
     uint8_t* reason = nullptr;     // u8[R]  CDX_EXIT_CERTAIN | CDX_EXIT_BUDGET

@@ -44,6 +44,11 @@ typedef enum {
 
 /* metrics.hpp:85 SignalKind (same ordinals) */
 enum { CDX_SIG_ENTROPY = 0, CDX_SIG_REWARD = 1, CDX_SIG_MEAN_LEN = 2, CDX_SIG_LOGPROB = 3 };
+/* Batched-API extension (no SignalKind ordinal in the reference): the majority-fraction
+ * certaindex of Self-Consistency = size of the plurality cluster / n, the share of the answer
+ * weighted_plurality returns (runtime.cpp:317-334, unweighted).  Only cdx_sc_certaindex(_ex)
+ * and the SC archetype of cdx_mixed_allocate accept thresholds on it.                       */
+enum { CDX_SIG_MAJORITY = 4 };
 /* metrics.hpp:105 ThresholdDir */
 enum { CDX_DIR_GE = 0, CDX_DIR_LE = 1 };
 /* metrics.hpp:72 RewardAggregation */
@@ -176,6 +181,13 @@ int cdx_gen_reward(cdx_ctx* ctx, const cdx_gen_params* g, uint64_t g0, uint64_t 
  * Decisions are taken on the FP64 certaindex; hcert is its fp32 rounding.               */
 int cdx_sc_certaindex(cdx_ctx* ctx, const uint32_t* ids, uint64_t R, uint32_t P, uint32_t S,
                       const cdx_threshold* th, uint32_t n_th, float* hcert, uint32_t* meets_bits);
+/* The same plus the majority-fraction certaindex (north_star (2)): majority f32[R][P]
+ * (nullable) = largest cluster size / S of each row, the fp32 rounding of the double
+ * (double)max_size / S on which CDX_SIG_MAJORITY thresholds are decided.  Thresholds may mix
+ * CDX_SIG_ENTROPY and CDX_SIG_MAJORITY (an AND, metrics.cpp:159-171).                      */
+int cdx_sc_certaindex_ex(cdx_ctx* ctx, const uint32_t* ids, uint64_t R, uint32_t P, uint32_t S,
+                         const cdx_threshold* th, uint32_t n_th, float* hcert, float* majority,
+                         uint32_t* meets_bits);
 
 /* Per-row clusters in first-seen order (the full metrics::Clustering of every row), 1 <= S <= 4096:
  * n_clusters u32[rows], leader u32[rows][S] (sample index of the cluster's first answer,

@@ -269,15 +269,33 @@ int cdxo_meets_thresholds(const double* signals, const int* present, const cdx_t
 /* ===================================================================================== */
 /* K2 restated: SC certaindex per (r,p) row (runtime.cpp:266-271 applied per probe row)  */
 /* ===================================================================================== */
+/* Majority-fraction certaindex of one clustering: the weight of the answer the reference's
+ * plurality vote returns, over n.  runtime.cpp:317-334 weighted_plurality (softmax off): every
+ * path weighs 1.0, clusters are visited in first-seen order and a later cluster wins only with
+ * a strictly larger weight, so the winner is the first largest cluster; its weight is its size
+ * (an exact double sum of 1.0s).                                                              */
+double cdxo_majority_fraction(const int* sizes, int m, int n) {
+    double best_w = -1.0;
+    for (int k = 0; k < m; ++k)
+        if ((double)sizes[k] > best_w) best_w = (double)sizes[k];
+    return best_w / (double)n;
+}
+
 int cdxo_sc_certaindex(const uint32_t* ids, uint64_t R, uint32_t P, uint32_t S,
                        const cdx_threshold* th, uint32_t n_th, double* hcert64, float* hcert,
                        uint32_t* meets_bits) {
+    return cdxo_sc_certaindex_ex(ids, R, P, S, th, n_th, hcert64, hcert, NULL, NULL, meets_bits);
+}
+
+int cdxo_sc_certaindex_ex(const uint32_t* ids, uint64_t R, uint32_t P, uint32_t S,
+                          const cdx_threshold* th, uint32_t n_th, double* hcert64, float* hcert,
+                          double* maj64, float* maj, uint32_t* meets_bits) {
     if (S == 0) return CDX_EINVAL;
     int* sizes = (int*)malloc(sizeof(int) * S);
     int* leaders = (int*)malloc(sizeof(int) * S);
     const uint32_t words = (P + 31) / 32;
-    double sig[4] = {0, 0, 0, 0};
-    int present[4] = {1, 0, 0, 0};
+    double sig[5] = {0, 0, 0, 0, 0};
+    int present[5] = {1, 0, 0, 0, 1};
     int st = CDX_OK;
     for (uint64_t r = 0; r < R && st == CDX_OK; ++r) {
         if (meets_bits)
@@ -286,9 +304,13 @@ int cdxo_sc_certaindex(const uint32_t* ids, uint64_t R, uint32_t P, uint32_t S,
             const uint64_t row = r * P + p;
             const int m = cdxo_cluster_exact_ids(ids + row * S, (int)S, sizes, leaders);
             const double hc = cdxo_certaindex_entropy(sizes, m, (int)S);
+            const double mf = cdxo_majority_fraction(sizes, m, (int)S);
             if (hcert64) hcert64[row] = hc;
             if (hcert) hcert[row] = (float)hc;
+            if (maj64) maj64[row] = mf;
+            if (maj) maj[row] = (float)mf;
             sig[CDX_SIG_ENTROPY] = hc;
+            sig[CDX_SIG_MAJORITY] = mf;
             const int ok = cdxo_meets_thresholds(sig, present, th, n_th);
             if (ok < 0) {
                 st = CDX_EINVAL;

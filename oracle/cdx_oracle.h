@@ -65,6 +65,11 @@ int cdxo_meets_thresholds(const double* signals, const int* present, const cdx_t
 int cdxo_sc_certaindex(const uint32_t* ids, uint64_t R, uint32_t P, uint32_t S,
                        const cdx_threshold* th, uint32_t n_th, double* hcert64, float* hcert,
                        uint32_t* meets_bits);
+/* ... plus the majority fraction (largest cluster / S, runtime.cpp:317-334's plurality) */
+double cdxo_majority_fraction(const int* sizes, int m, int n);
+int cdxo_sc_certaindex_ex(const uint32_t* ids, uint64_t R, uint32_t P, uint32_t S,
+                          const cdx_threshold* th, uint32_t n_th, double* hcert64, float* hcert,
+                          double* maj64, float* maj, uint32_t* meets_bits);
 
 /* ---- SPEC allocate + exclusive scan + stable compaction (K5), SPEC.md:404-412 ------- */
 int cdxo_allocate_scan(const uint32_t* meets_bits, uint64_t R, uint32_t P,

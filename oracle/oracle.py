@@ -185,6 +185,30 @@ def sc_certaindex(ids, ths):
     return h64, h32, meets
 
 
+def sc_certaindex_ex(ids, ths):
+    """K2 restated with the majority fraction: (h64, h32, maj64, maj32, meets)."""
+    R, P_, S = ids.shape
+    h64 = np.empty((R, P_), np.float64)
+    h32 = np.empty((R, P_), np.float32)
+    m64 = np.empty((R, P_), np.float64)
+    m32 = np.empty((R, P_), np.float32)
+    meets = np.empty((R, (P_ + 31) // 32), np.uint32)
+    arr, n = thresholds(ths)
+    st = lib().cdxo_sc_certaindex_ex(_p(np.ascontiguousarray(ids)), C.c_uint64(R), C.c_uint32(P_), C.c_uint32(S),
+                                     arr, C.c_uint32(n), _p(h64), _p(h32), _p(m64), _p(m32), _p(meets))
+    if st:
+        raise ValueError(f"oracle sc_certaindex_ex status {st}")
+    return h64, h32, m64, m32, meets
+
+
+def majority_fraction(sizes):
+    a = (C.c_int * len(sizes))(*[int(x) for x in sizes])
+    f = lib().cdxo_majority_fraction
+    f.restype = C.c_double
+    f.argtypes = [P, C.c_int, C.c_int]
+    return f(C.cast(a, P), len(sizes), int(sum(sizes)))
+
+
 def allocate_scan(meets, R, P_, kind, detect_at, cap, recheck_every=1, tokens_per_unit=64, base_offset=0):
     pol = AllocPolicy()
     pol.kind, pol.detect_at, pol.resource_cap = kind, detect_at, cap

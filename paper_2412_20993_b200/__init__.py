@@ -247,6 +247,20 @@ class Context:
                                                _ptr(hcert) if want_hcert else None, _ptr(meets)))
         return hcert, meets
 
+    def sc_certaindex_ex(self, ids, thresholds: Sequence[Threshold] = (), want_hcert: bool = True,
+                         want_majority: bool = True):
+        """K2 with the majority-fraction certaindex (largest cluster / S, SIG_MAJORITY)."""
+        t = self.torch
+        R, P, S = ids.shape
+        hcert = self.empty((R, P), t.float32) if want_hcert else None
+        maj = self.empty((R, P), t.float32) if want_majority else None
+        meets = self.empty((R, (P + 31) // 32), t.int32)
+        arr, n = c_thresholds(thresholds)
+        self._bind_stream()
+        self._check(self.lib.cdx_sc_certaindex_ex(self.h, _ptr(ids), R, P, S, arr, n, _ptr(hcert), _ptr(maj),
+                                                  _ptr(meets)))
+        return hcert, maj, meets
+
     def cluster_rows(self, ids2d):
         t = self.torch
         rows, S = ids2d.shape

@@ -89,6 +89,7 @@ SIGNATURES = {
     "cdx_gen_cot": (C.c_int, [P, C.POINTER(GenParams), U64, U64, U32, P, P]),
     "cdx_gen_reward": (C.c_int, [P, C.POINTER(GenParams), U64, U64, U32, U32, P, P]),
     "cdx_sc_certaindex": (C.c_int, [P, P, U64, U32, U32, C.POINTER(Threshold), U32, P, P]),
+    "cdx_sc_certaindex_ex": (C.c_int, [P, P, U64, U32, U32, C.POINTER(Threshold), U32, P, P, P]),
     "cdx_cluster_rows": (C.c_int, [P, P, U64, U32, P, P, P]),
     "cdx_entropy_from_sizes": (C.c_int, [P, P, P, P, U64, U32, U32, P, P]),
     "cdx_probe_consistency": (C.c_int, [P, P, P, P, P, P, U64, I32, P, P]),

@@ -70,6 +70,22 @@ void sc_certaindex(Context& cx, const uint32_t* ids, const ScShape& s,
     cx.check(cdx_sc_certaindex(cx.raw(), ids, s.requests, s.probes, s.samples, th.data(), th.size(), hcert, meets));
 }
 
+void sc_certaindex(Context& cx, const uint32_t* ids, const ScShape& s,
+                   std::span<const metrics::SignalThreshold> thresholds,
+                   std::span<const MajorityThreshold> majority_thresholds, float* hcert, float* majority,
+                   uint32_t* meets) {
+    CThresholds th(thresholds);
+    for (const auto& m : majority_thresholds) {
+        cdx_threshold c{};
+        c.signal = CDX_SIG_MAJORITY;
+        c.dir = m.direction == metrics::ThresholdDir::GreaterEq ? CDX_DIR_GE : CDX_DIR_LE;
+        c.cutoff = m.cutoff;
+        th.v.push_back(c);
+    }
+    cx.check(cdx_sc_certaindex_ex(cx.raw(), ids, s.requests, s.probes, s.samples, th.data(), th.size(), hcert,
+                                  majority, meets));
+}
+
 void allocate_scan(Context& cx, const uint32_t* meets, uint64_t R, uint32_t P,
                    const scheduler::AllocationPolicy& pol, int64_t tokens_per_unit, int64_t base_offset,
                    uint32_t kept_base, const AllocationOutputs& o) {

@@ -326,7 +326,7 @@ extern "C" int cdx_cot_meets(cdx_ctx* ctx, const uint32_t* ids, const uint64_t* 
     CDX_NVTX("cdx_cot_meets");
     if (!ctx) return CDX_EINVAL;
     if (window < 1) return set_error(ctx, CDX_EINVAL, "consistency: window must be >= 1");
-    const bool present[4] = {true, false, false, false};  // CoT's SignalVector: C_k in the entropy slot
+    const bool present[5] = {true, false, false, false, false};  // CoT's SignalVector: C_k in the entropy slot
     if (int st = check_thresholds(ctx, th, n_th, present)) return st;
     if (window > 62) return set_error(ctx, CDX_EINVAL, "cot_meets: window must be <= 62");
     if (P == 0 || P > 4096) return set_error(ctx, CDX_EINVAL, "cot_meets: probes must be in [1, 4096]");

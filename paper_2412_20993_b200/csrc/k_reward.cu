@@ -707,7 +707,7 @@ int reward_certaindex_impl(cdx_ctx* ctx, const float* rewards, const double* rew
     if (T == 0 || W == 0) return set_error(ctx, CDX_EINVAL, "certaindex_reward: empty reward set");
     if (static_cast<uint64_t>(T) * W > (1u << 16))
         return set_error(ctx, CDX_EINVAL, "reward_certaindex: at most 65536 paths per program");
-    const bool present[4] = {ids != nullptr, true, false, false};
+    const bool present[5] = {ids != nullptr, true, false, false, false};
     if (int st = check_thresholds(ctx, th_mean, n_th_mean, present)) return st;
     if (int st = check_thresholds(ctx, th_max, n_th_max, present)) return st;
     if (G == 0) return CDX_OK;

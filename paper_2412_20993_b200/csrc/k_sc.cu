@@ -53,7 +53,7 @@ __device__ __forceinline__ uint32_t eq_mask_rt(const uint32_t (&x)[SB], uint32_t
 template <int SB>
 __device__ __forceinline__ double alu_row_rt(const uint32_t* __restrict__ row, uint32_t S,
                                              const double* __restrict__ term, double logn,
-                                             const double* __restrict__ comp, bool* more) {
+                                             const double* __restrict__ comp, bool* more, uint32_t& maxc) {
     uint32_t x[SB];
     if ((S & 3u) == 0) {  // 16-byte rows: vector loads (rows of a group are 16B-aligned)
 #pragma unroll
@@ -71,10 +71,11 @@ __device__ __forceinline__ double alu_row_rt(const uint32_t* __restrict__ row, u
     const uint32_t valid = S >= 32 ? 0xffffffffu : ((1u << S) - 1u);
     uint32_t eq = eq_mask_rt<SB>(x, x[0]) & valid;
     uint32_t un = valid & ~eq;
+    maxc = __popc(eq);  // largest cluster so far (majority fraction = maxc / S)
     if (un == 0) return 1.0;  // one cluster holds every answer: H~ = 1 exactly
     uint32_t peeled = 1;
     if (comp) {  // S <= 16: composition code -> table
-        uint32_t cum = __popc(eq), code = 1u << (cum - 1);
+        uint32_t cum = maxc, code = 1u << (cum - 1);
         while (un) {
             if (peeled == RT_PEEL_MAX) {
                 *more = true;
@@ -83,12 +84,14 @@ __device__ __forceinline__ double alu_row_rt(const uint32_t* __restrict__ row, u
             ++peeled;
             eq = eq_mask_rt<SB>(x, row[__ffs(un) - 1]) & valid;
             un &= ~eq;
-            cum += __popc(eq);
+            const uint32_t c = __popc(eq);
+            maxc = max(maxc, c);
+            cum += c;
             code |= 1u << (cum - 1);
         }
         return __ldg(comp + (code & ((1u << (S - 1)) - 1u)));
     }
-    double h = __dsub_rn(0.0, term[__popc(eq)]);
+    double h = __dsub_rn(0.0, term[maxc]);
     while (un) {
         if (peeled == RT_PEEL_MAX) {
             *more = true;
@@ -97,7 +100,9 @@ __device__ __forceinline__ double alu_row_rt(const uint32_t* __restrict__ row, u
         ++peeled;
         eq = eq_mask_rt<SB>(x, row[__ffs(un) - 1]) & valid;
         un &= ~eq;
-        h = __dsub_rn(h, term[__popc(eq)]);  // h -= p*log(p), first-seen order
+        const uint32_t c = __popc(eq);
+        maxc = max(maxc, c);
+        h = __dsub_rn(h, term[c]);  // h -= p*log(p), first-seen order
     }
     h = (0.0 < h) ? h : 0.0;
     const double v = __ddiv_rn(__dsub_rn(logn, h), logn);
@@ -127,18 +132,20 @@ __device__ __forceinline__ void sc_group(const ScParams& p, const uint32_t* __re
     if (SCT == 0) {  // runtime S: the ALU engine first, the match engine only for its overflow
         bool more = false;
         double hc = 1.0;
+        uint32_t maxc = S;
         if (lane < rows) {
             const uint32_t* rowp = base + lane * S;
-            if (S <= 8) hc = alu_row_rt<8>(rowp, S, term, p.logn, p.comp, &more);
-            else if (S <= 16) hc = alu_row_rt<16>(rowp, S, term, p.logn, p.comp, &more);
-            else if (S <= 24) hc = alu_row_rt<24>(rowp, S, term, p.logn, p.comp, &more);
-            else hc = alu_row_rt<32>(rowp, S, term, p.logn, p.comp, &more);
+            if (S <= 8) hc = alu_row_rt<8>(rowp, S, term, p.logn, p.comp, &more, maxc);
+            else if (S <= 16) hc = alu_row_rt<16>(rowp, S, term, p.logn, p.comp, &more, maxc);
+            else if (S <= 24) hc = alu_row_rt<24>(rowp, S, term, p.logn, p.comp, &more, maxc);
+            else hc = alu_row_rt<32>(rowp, S, term, p.logn, p.comp, &more, maxc);
         }
         if (!__any_sync(0xffffffffu, more)) {
             bool meets = false;
             if (lane < rows) {
-                meets = sc_meets(p, hc);
+                meets = sc_meets(p, hc, maxc);
                 if (p.hcert) p.hcert[req * p.P + row0 + lane] = static_cast<float>(hc);
+                if (p.maj) p.maj[req * p.P + row0 + lane] = p.maj_tab[maxc];
             }
             const uint32_t mw = __ballot_sync(0xffffffffu, meets);
             if (lane == 0 && p.meets) p.meets[req * p.words + g] = mw;
@@ -169,12 +176,22 @@ __device__ __forceinline__ void sc_group(const ScParams& p, const uint32_t* __re
     bool meets = false;
     if (lane < rows) {
         double hc = 1.0;  // metrics.cpp:121: a single path is fully certain
+        uint32_t maxc = S;
         const uint4* rowp = reinterpret_cast<const uint4*>(cntw + lane * 32u);
         const uint4 a = rowp[0];
         // one cluster holding every answer: H = -(1*log 1) = 0 exactly, so H~ = 1 exactly
         if (S > 1 && (a.x & 0xffu) != S) {
             const uint4 b = S > 16 ? rowp[1] : make_uint4(0, 0, 0, 0);
             const uint32_t wv[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+            maxc = 0;  // largest size byte among the row's S slots (the rest are stale)
+#pragma unroll
+            for (uint32_t k = 0; k < 8; ++k) {
+                if (k * 4u >= S) break;
+                const uint32_t keep = S >= k * 4u + 4u ? 0xffffffffu : ((1u << ((S - k * 4u) * 8u)) - 1u);
+                maxc = __vmaxu4(maxc, wv[k] & keep);
+            }
+            maxc = __vmaxu4(maxc, maxc >> 16);
+            maxc = __vmaxu4(maxc, maxc >> 8) & 0xffu;
             double h = 0.0;
             if (SCT != 0) {
                 // Branch-free fold over every sample slot in order: term[0] = +0.0 and h >= 0,
@@ -208,12 +225,9 @@ __device__ __forceinline__ void sc_group(const ScParams& p, const uint32_t* __re
             const double v = __ddiv_rn(__dsub_rn(p.logn, h), p.logn);
             hc = v < 0.0 ? 0.0 : (1.0 < v ? 1.0 : v);  // std::clamp
         }
-        meets = true;
-        for (int t = 0; t < p.n_th; ++t) {
-            const bool ok = p.th_dir[t] == CDX_DIR_GE ? hc >= p.th_cut[t] : hc <= p.th_cut[t];
-            meets = meets && ok;
-        }
+        meets = sc_meets(p, hc, maxc);
         if (p.hcert) p.hcert[req * p.P + row0 + lane] = static_cast<float>(hc);
+        if (p.maj) p.maj[req * p.P + row0 + lane] = p.maj_tab[maxc];
     }
     const uint32_t mw = __ballot_sync(0xffffffffu, meets);
     if (lane == 0 && p.meets) p.meets[req * p.words + g] = mw;
@@ -387,19 +401,35 @@ __global__ void entropy_sizes_kernel(const uint32_t* __restrict__ sizes, const u
     }
 }
 
-int check_thresholds(cdx_ctx* ctx, const cdx_threshold* th, uint32_t n_th, const bool present[4]) {
-    static const char* names[4] = {"certaindex_entropy", "certaindex_reward", "mean_output_length",
-                                   "mean_norm_logprob"};
+int check_thresholds(cdx_ctx* ctx, const cdx_threshold* th, uint32_t n_th, const bool present[5]) {
+    static const char* names[5] = {"certaindex_entropy", "certaindex_reward", "mean_output_length",
+                                   "mean_norm_logprob", "majority_fraction"};
     if (n_th > MAX_TH) return set_error(ctx, CDX_EINVAL, "thresholds: at most 8 per call");
     if (n_th && !th) return set_error(ctx, CDX_EINVAL, "thresholds: null array");
     for (uint32_t i = 0; i < n_th; ++i) {
-        if (th[i].signal > 3 || th[i].dir > 1) return set_error(ctx, CDX_EINVAL, "thresholds: bad enum");
+        if (th[i].signal > CDX_SIG_MAJORITY || th[i].dir > 1) return set_error(ctx, CDX_EINVAL, "thresholds: bad enum");
         if (!present[th[i].signal])
             return set_error(ctx, CDX_EINVAL,
                              std::string("combined_meets_thresholds: signal '") + names[th[i].signal] +
                                  "' absent");
     }
     return CDX_OK;
+}
+
+void majority_interval(const cdx_threshold* th, uint32_t n_th, uint32_t S, uint32_t* lo, uint32_t* hi) {
+    *lo = S + 1;
+    *hi = 0;
+    for (uint32_t c = 0; c <= S; ++c) {
+        const double v = static_cast<double>(c) / static_cast<double>(S);
+        bool ok = true;
+        for (uint32_t i = 0; i < n_th; ++i)
+            if (th[i].signal == CDX_SIG_MAJORITY)
+                ok = ok && (th[i].dir == CDX_DIR_GE ? v >= th[i].cutoff : v <= th[i].cutoff);
+        if (ok) {  // v is monotone in c and each compare is a half-line: the set is an interval
+            *lo = std::min(*lo, c);
+            *hi = c;
+        }
+    }
 }
 
 template <int SCT>
@@ -428,12 +458,16 @@ constexpr uint32_t SC_WIDE_WARPS = 4;
 struct WideParams {
     const uint32_t* ids;
     float* hcert;
+    float* maj;         // majority fraction f32 (nullable)
+    uint32_t maj_lo, maj_hi;
+    int maj_th;
     uint32_t* meets;
     const double* tab;  // T_S[0..S]
     double logn;
     uint64_t rows;      // R * P
     uint32_t P, S, words, cap_log2;
     int n_th;
+    uint8_t th_sig[MAX_TH];
     uint8_t th_dir[MAX_TH];
     double th_cut[MAX_TH];
 };
@@ -498,19 +532,27 @@ __global__ void __launch_bounds__(SC_WIDE_WARPS * 32) sc_wide_kernel(const __gri
         const uint32_t m = wide_cluster(p.ids + row * p.S, p.S, p.cap_log2, hkey, hord, cnt, nullptr, lane);
         if (lane == 0) {
             double hc = 1.0;  // one cluster holds every answer: H~ = 1 exactly
+            uint32_t maxc = p.S;
             if (m > 1) {
                 double h = 0.0;
-                for (uint32_t k = 0; k < m; ++k) h = __dsub_rn(h, __ldg(p.tab + cnt[k]));  // first-seen order
+                maxc = 0;
+                for (uint32_t k = 0; k < m; ++k) {
+                    h = __dsub_rn(h, __ldg(p.tab + cnt[k]));  // first-seen order
+                    maxc = max(maxc, cnt[k]);
+                }
                 h = (0.0 < h) ? h : 0.0;
                 const double v = __ddiv_rn(__dsub_rn(p.logn, h), p.logn);
                 hc = v < 0.0 ? 0.0 : (1.0 < v ? 1.0 : v);
             }
             bool meets = true;
             for (int t = 0; t < p.n_th; ++t) {
+                if (p.th_sig[t] == CDX_SIG_MAJORITY) continue;  // the integer interval below
                 const bool ok = p.th_dir[t] == CDX_DIR_GE ? hc >= p.th_cut[t] : hc <= p.th_cut[t];
                 meets = meets && ok;
             }
+            if (p.maj_th) meets = meets && maxc >= p.maj_lo && maxc <= p.maj_hi;
             if (p.hcert) p.hcert[row] = static_cast<float>(hc);
+            if (p.maj) p.maj[row] = static_cast<float>(__ddiv_rn(static_cast<double>(maxc), static_cast<double>(p.S)));
             if (p.meets && meets) {
                 const uint64_t r = row / p.P;
                 const uint32_t pp = static_cast<uint32_t>(row - r * p.P);
@@ -592,6 +634,12 @@ extern "C" {
 
 int cdx_sc_certaindex(cdx_ctx* ctx, const uint32_t* ids, uint64_t R, uint32_t P, uint32_t S,
                       const cdx_threshold* th, uint32_t n_th, float* hcert, uint32_t* meets_bits) {
+    return cdx_sc_certaindex_ex(ctx, ids, R, P, S, th, n_th, hcert, nullptr, meets_bits);
+}
+
+int cdx_sc_certaindex_ex(cdx_ctx* ctx, const uint32_t* ids, uint64_t R, uint32_t P, uint32_t S,
+                         const cdx_threshold* th, uint32_t n_th, float* hcert, float* majority,
+                         uint32_t* meets_bits) {
     using namespace cdx;
     CDX_NVTX("cdx_sc_certaindex");
     if (!ctx) return CDX_EINVAL;
@@ -599,13 +647,21 @@ int cdx_sc_certaindex(cdx_ctx* ctx, const uint32_t* ids, uint64_t R, uint32_t P,
     if (S > SC_WIDE_MAX) return set_error(ctx, CDX_EINVAL, "sc_certaindex: at most 4096 samples per row");
     if (P == 0) return set_error(ctx, CDX_EINVAL, "sc_certaindex: probes must be >= 1");
     if (!ids) return set_error(ctx, CDX_EINVAL, "sc_certaindex: null ids");
-    const bool present[4] = {true, false, false, false};
+    const bool present[5] = {true, false, false, false, true};
     if (int st = check_thresholds(ctx, th, n_th, present)) return st;
     if (R == 0) return CDX_OK;
+    uint32_t maj_lo = 0, maj_hi = 0;
+    int maj_th = 0;
+    for (uint32_t i = 0; i < n_th; ++i) maj_th |= th[i].signal == CDX_SIG_MAJORITY;
+    if (maj_th) majority_interval(th, n_th, S, &maj_lo, &maj_hi);
     if (S > 32) {  // wide rows: a warp per row, shared-memory hash of first-seen ordinals
         WideParams w{};
         w.ids = ids;
         w.hcert = hcert;
+        w.maj = majority;
+        w.maj_th = maj_th;
+        w.maj_lo = maj_lo;
+        w.maj_hi = maj_hi;
         w.meets = meets_bits;
         w.rows = R * P;
         w.P = P;
@@ -615,6 +671,7 @@ int cdx_sc_certaindex(cdx_ctx* ctx, const uint32_t* ids, uint64_t R, uint32_t P,
         while ((1u << w.cap_log2) < 2u * S) ++w.cap_log2;
         w.n_th = static_cast<int>(n_th);
         for (uint32_t i = 0; i < n_th; ++i) {
+            w.th_sig[i] = th[i].signal;
             w.th_dir[i] = th[i].dir;
             w.th_cut[i] = th[i].cutoff;
         }
@@ -640,6 +697,12 @@ int cdx_sc_certaindex(cdx_ctx* ctx, const uint32_t* ids, uint64_t R, uint32_t P,
     ScParams p{};
     p.ids = ids;
     p.hcert = hcert;
+    p.maj = majority;
+    p.maj_th = maj_th;
+    p.maj_lo = maj_lo;
+    p.maj_hi = maj_hi;
+    for (uint32_t c = 0; c <= S; ++c)
+        p.maj_tab[c] = static_cast<float>(static_cast<double>(c) / static_cast<double>(S));
     p.meets = meets_bits;
     p.R = R;
     p.P = P;
@@ -660,6 +723,7 @@ int cdx_sc_certaindex(cdx_ctx* ctx, const uint32_t* ids, uint64_t R, uint32_t P,
     for (uint32_t i = 0; i < n_th; ++i) {
         p.th_dir[i] = th[i].dir;
         p.th_cut[i] = th[i].cutoff;
+        if (th[i].signal == CDX_SIG_MAJORITY) continue;  // the integer interval [maj_lo, maj_hi]
         if (std::isnan(th[i].cutoff)) p.box_never = 1;
         else if (th[i].dir == CDX_DIR_GE) p.box_lo = std::max(p.box_lo, th[i].cutoff);
         else p.box_hi = std::min(p.box_hi, th[i].cutoff);

@@ -30,12 +30,26 @@ struct ScParams {
     // box_never: a NaN cutoff (every compare false)
     double box_lo, box_hi;
     int box_never;
+    // majority fraction (CDX_SIG_MAJORITY): largest cluster size / S.  maj: f32[R][P]
+    // output (nullable), maj_tab[c] = fp32 of (double)c / S.  Its thresholds reduce to an
+    // integer interval of the largest cluster size [maj_lo, maj_hi] (empty: never met),
+    // evaluated on the host with the same double compare, as a_min is for CoT.
+    float* maj;
+    int maj_th;  // any threshold on the majority signal
+    uint32_t maj_lo, maj_hi;
+    float maj_tab[33];
 };
 
-// meets for an SC certaindex value (finite, in [0, 1]): the interval form of the AND
-__device__ __forceinline__ bool sc_meets(const ScParams& p, double hc) {
-    return p.n_th == 0 || (!p.box_never && hc >= p.box_lo && hc <= p.box_hi);
+// meets for an SC certaindex value (finite, in [0, 1]) and the row's largest cluster size:
+// the interval form of the AND (metrics.cpp:159-171) on each signal
+__device__ __forceinline__ bool sc_meets(const ScParams& p, double hc, uint32_t maxc) {
+    return p.n_th == 0 || (!p.box_never && hc >= p.box_lo && hc <= p.box_hi &&
+                           (!p.maj_th || (maxc >= p.maj_lo && maxc <= p.maj_hi)));
 }
+
+// [lo, hi] = {c in 0..S : every majority threshold holds for (double)c / S} (lo > hi: none).
+// metrics.cpp:167's inclusive compares, evaluated on the host exactly as the oracle does.
+void majority_interval(const cdx_threshold* th, uint32_t n_th, uint32_t S, uint32_t* lo, uint32_t* hi);
 
 // The TMA fast path (S in {4,8,16,32}, P % 32 == 0, 16B-aligned ids).  Returns true when
 // it launched; false when the shape needs the generic warp-match kernel.
@@ -43,6 +57,6 @@ bool launch_sc_fast(cdx_ctx* ctx, const ScParams& p);
 
 // Validate a threshold list against the signals an entry point produces (present[kind]);
 // an absent signal fails with the reference's message (metrics.cpp:163-166).
-int check_thresholds(cdx_ctx* ctx, const cdx_threshold* th, uint32_t n_th, const bool present[4]);
+int check_thresholds(cdx_ctx* ctx, const cdx_threshold* th, uint32_t n_th, const bool present[5]);
 
 }  // namespace cdx

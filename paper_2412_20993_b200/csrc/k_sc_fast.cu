@@ -20,7 +20,8 @@
 //     clusters is redone here (warp vote), and CDX_SCF_MATCH=k dedicates k warps of a CTA
 //     to it (the pipes are independent; both engines pull from the same counter).
 //
-// Both produce, per row, the first-seen-ordered cluster sizes folded in FP64 exactly as
+// Both produce, per row, the largest cluster size (the majority fraction maxc / S, the
+// plurality rule of runtime.cpp:317-334) and the first-seen-ordered cluster sizes folded in FP64 exactly as
 // metrics.cpp:107-125 (h -= term[size], term[c] = (c/S)*log(c/S) from the host libm;
 // max(0,h); clamp((log n - h)/log n)), thresholds on the FP64 value (metrics.cpp:159-171),
 // an fp32 store and one meets word per group.
@@ -75,7 +76,7 @@ constexpr uint32_t PEEL_MAX = 8;
 template <int S>
 __device__ __forceinline__ double alu_row(const uint8_t* __restrict__ buf, const double* __restrict__ term,
                                           uint32_t lane, double logn, bool* more,
-                                          const double* __restrict__ comp) {
+                                          const double* __restrict__ comp, uint32_t& maxc) {
     uint32_t x[S];
 #pragma unroll
     for (uint32_t j = 0; j < S / 4; ++j) {
@@ -89,9 +90,10 @@ __device__ __forceinline__ double alu_row(const uint8_t* __restrict__ buf, const
     // first cluster: its leader is sample 0
     uint32_t eq = eq_mask<S>(x, x[0]);
     un &= ~eq;
+    maxc = __popc(eq);  // largest cluster so far (majority fraction = maxc / S)
     if (un == 0) return 1.0;  // one cluster holds every answer: H = 0, H~ = 1 exactly
     if (S <= 16 && comp) {  // composition code: a cut bit after every cluster but the last
-        uint32_t cum = __popc(eq), code = 1u << (cum - 1);
+        uint32_t cum = maxc, code = 1u << (cum - 1);
         uint32_t peeled = 1;
         while (un) {
             if (peeled == PEEL_MAX) {
@@ -103,12 +105,14 @@ __device__ __forceinline__ double alu_row(const uint8_t* __restrict__ buf, const
             const uint32_t v = *reinterpret_cast<const uint32_t*>(buf + elem_addr(lane * S + l));
             eq = eq_mask<S>(x, v);
             un &= ~eq;
-            cum += __popc(eq);
+            const uint32_t c = __popc(eq);
+            maxc = max(maxc, c);
+            cum += c;
             code |= 1u << (cum - 1);
         }
         return __ldg(comp + (code & ((1u << (S - 1)) - 1u)));
     }
-    double h = __dsub_rn(0.0, term[__popc(eq)]);
+    double h = __dsub_rn(0.0, term[maxc]);
     uint32_t peeled = 1;
     while (un) {
         if (peeled == PEEL_MAX) {
@@ -120,16 +124,28 @@ __device__ __forceinline__ double alu_row(const uint8_t* __restrict__ buf, const
         const uint32_t v = *reinterpret_cast<const uint32_t*>(buf + elem_addr(lane * S + l));
         eq = eq_mask<S>(x, v);
         un &= ~eq;
-        h = __dsub_rn(h, term[__popc(eq)]);  // h -= p*log(p), first-seen order
+        const uint32_t c = __popc(eq);
+        maxc = max(maxc, c);
+        h = __dsub_rn(h, term[c]);  // h -= p*log(p), first-seen order
     }
     return finish_entropy(h, logn);
+}
+
+// largest byte of a row's size slots (the largest cluster), S/4 words of 4 bytes
+__device__ __forceinline__ uint32_t max_byte(const uint32_t* wv, uint32_t nwords) {
+    uint32_t m = 0;
+    for (uint32_t k = 0; k < nwords; ++k) m = __vmaxu4(m, wv[k]);
+    m = __vmaxu4(m, m >> 16);
+    m = __vmaxu4(m, m >> 8);
+    return m & 0xffu;
 }
 
 // warp-match engine: lane = sample of the rows of one match iteration; the fold runs on
 // the row's owner lane over the [row][32]-byte size table (0 = not a leader).
 template <int S>
 __device__ __forceinline__ double match_rows(const uint8_t* __restrict__ buf, uint8_t* __restrict__ cntw,
-                                             const double* __restrict__ term, uint32_t lane, double logn) {
+                                             const double* __restrict__ term, uint32_t lane, double logn,
+                                             uint32_t& maxc) {
     constexpr uint32_t rpi = 32u / S;
     constexpr uint32_t smask = S >= 32 ? 0xffffffffu : ((1u << S) - 1u);
     const uint32_t sub = lane / S, s = lane - sub * S;
@@ -145,9 +161,13 @@ __device__ __forceinline__ double match_rows(const uint8_t* __restrict__ buf, ui
     __syncwarp();
     const uint4* rowp = reinterpret_cast<const uint4*>(cntw + lane * 32u);
     const uint4 a = rowp[0];
-    if ((a.x & 0xffu) == S) return 1.0;  // sample 0's cluster holds every answer
+    if ((a.x & 0xffu) == S) {  // sample 0's cluster holds every answer
+        maxc = S;
+        return 1.0;
+    }
     const uint4 b = S > 16 ? rowp[1] : make_uint4(0, 0, 0, 0);
     const uint32_t wv[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+    maxc = max_byte(wv, S / 4);
     // branch-free fold over every slot in sample order: term[0] = +0.0 and h >= 0, so a
     // non-leader slot leaves h bit-identical
     double h = 0.0;
@@ -219,19 +239,22 @@ __global__ void __launch_bounds__(FAST_WARPS * 32) sc_fast_kernel(const __grid_c
         mbar_wait(&bar[stage], parity);
         const uint8_t* buf = wbase + stage * GS;
         bool more = false;
-        double hc = use_match ? 0.0 : alu_row<S>(buf, term, lane, p.logn, &more, p.comp);
-        if (use_match || __any_sync(0xffffffffu, more)) hc = match_rows<S>(buf, cntw, term, lane, p.logn);
+        uint32_t maxc = 0;
+        double hc = use_match ? 0.0 : alu_row<S>(buf, term, lane, p.logn, &more, p.comp, maxc);
+        if (use_match || __any_sync(0xffffffffu, more)) hc = match_rows<S>(buf, cntw, term, lane, p.logn, maxc);
         __syncwarp();  // every lane is done with this stage (and with cntw)
         if (lane == 0) claim_issue(stage);
-        const bool meets = sc_meets(p, hc);
+        const bool meets = sc_meets(p, hc, maxc);
         const uint64_t row = G * 32u + lane;  // flat row r * P + p
         if (p.P % 32u == 0) {  // a group is 32 probes of one request: one meets word
             if (p.hcert) p.hcert[row] = static_cast<float>(hc);
+            if (p.maj) p.maj[row] = p.maj_tab[maxc];
             const uint32_t mw = __ballot_sync(0xffffffffu, meets);
             if (lane == 0 && p.meets) p.meets[G] = mw;
         } else {  // flat groups straddle requests: OR each word's bits in (meets zeroed first)
             const bool valid = row < p.R * p.P;
             if (p.hcert && valid) p.hcert[row] = static_cast<float>(hc);
+            if (p.maj && valid) p.maj[row] = p.maj_tab[maxc];
             const uint64_t r = row / p.P;
             const uint32_t pp = static_cast<uint32_t>(row - r * p.P);
             const uint64_t word = valid ? r * p.words + (pp >> 5) : ~0ull;

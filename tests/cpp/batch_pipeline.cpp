@@ -96,6 +96,13 @@ int main(int argc, char** argv) {
             cx.sync();
             dump("sc_exit_graph", ek.download());
             dump("sc_answer_graph", ans.download());
+            // majority-fraction certaindex ANDed with the entropy threshold
+            batch::DeviceArray<float> mj(cx, R * P);
+            const batch::MajorityThreshold mt{0.6, metrics::ThresholdDir::GreaterEq};
+            batch::sc_certaindex(cx, ids.data(), {R, P, S}, {&th, 1}, {&mt, 1}, nullptr, mj.data(), meets.data());
+            cx.sync();
+            dump("sc_majority", mj.download());
+            dump("sc_meets_majority", meets.download());
         }
         // ---- CoT: 8192 requests x 64 probes, w = 3, tau = 0.9, budget at the last probe
         {

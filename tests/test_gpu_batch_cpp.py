@@ -53,6 +53,9 @@ def test_batch_pipeline_matches_oracle():
         assert ld("sc_scalars", np.int64)[0] == ref["n_kept"]
         assert np.array_equal(ld("sc_exit_graph", np.int32), ref["exit_knob"])
         assert np.array_equal(ld("sc_answer_graph", np.uint32), ans)
+        _, _, _, m32, mmeets = O.sc_certaindex_ex(ids, [(0, 0.7, 0), (4, 0.6, 0)])
+        assert np.array_equal(ld("sc_majority", np.uint32), m32.view(np.uint32).ravel())
+        assert np.array_equal(ld("sc_meets_majority", np.uint32), mmeets.ravel())
         # CoT
         cids, hes = O.gen_cot(_gp(32, 64, 0.05), 8192, 64)
         cref = O.cot_exit(cids, hes, O.probe_cfg(64, 3, 0.9, 4096))
