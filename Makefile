@@ -20,7 +20,8 @@ HHDRS   := $(wildcard $(PKG)/csrc/host/*.hpp) include/cdx_c.h $(wildcard include
 HOSTCXX := g++
 CXXFLAGS_HOST := -std=c++20 -O2 -fPIC -Wall -Wextra -Iinclude
 
-DROPIN  := tests/cpp/bin/dropin_ours tests/cpp/bin/scheduler_cases tests/cpp/bin/batch_pipeline tests/cpp/bin/sim_cases
+DROPIN  := tests/cpp/bin/dropin_ours tests/cpp/bin/scheduler_cases tests/cpp/bin/batch_pipeline tests/cpp/bin/sim_cases \
+           tests/cpp/bin/shard_world2
 
 all: lib oracle dropin
 
@@ -43,7 +44,7 @@ build/obj/%.cpp.o: $(PKG)/csrc/%.cpp $(HDRS)
 
 $(LIB): $(OBJS)
 	@mkdir -p $(PKG)/lib
-	$(NVCC) $(ARCH) -shared -o $@ $(OBJS) -lpthread
+	$(NVCC) $(ARCH) -shared -o $@ $(OBJS) -lpthread -ldl
 
 oracle:
 	$(MAKE) -C oracle
@@ -55,6 +56,11 @@ CPPTEST = @mkdir -p tests/cpp/bin && $(HOSTCXX) -std=c++20 -O2 -Wall -Iinclude -
           -Wl,-rpath,'$$ORIGIN/../../../$(PKG)/lib'
 tests/cpp/bin/dropin_ours: tests/cpp/dropin_cases.cpp $(HOSTLIB) $(HHDRS)
 	$(CPPTEST)
+# multi-rank C-ABI test: W host threads, one context each, host-staged communicator callbacks
+tests/cpp/bin/shard_world2: tests/cpp/shard_world2.cpp $(LIB) include/cdx_c.h
+	@mkdir -p tests/cpp/bin && $(HOSTCXX) -std=c++20 -O2 -Wall -Iinclude -I/usr/local/cuda/include -o $@ $< \
+	  -L$(PKG)/lib -lcdx -L/usr/local/cuda/lib64 -lcudart -lpthread \
+	  -Wl,-rpath,'$$ORIGIN/../../../$(PKG)/lib' -Wl,-rpath,/usr/local/cuda/lib64
 tests/cpp/bin/%: tests/cpp/%.cpp $(HOSTLIB) $(HHDRS)
 	$(CPPTEST)
 

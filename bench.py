@@ -514,12 +514,16 @@ def bench_sc(args, cfg, rank, world, cx, with_e2e=True):
         if e is not None:
             e.record(torch.cuda.current_stream())
         e = seg_events(seg, "allocate_scan")
-        cx.allocate_scan(meets, R, P, pol, kept_base=rank * R, out=out)
-        if e is not None:
-            e.record(torch.cuda.current_stream())
-        if world > 1:  # global token offsets: allgather of shard budget totals (8 B/rank) + rebase
+        if world == 1:
+            cx.allocate_scan(meets, R, P, pol, kept_base=rank * R, out=out)
+        elif sh.native:  # global offsets / kept / totals: one 32-B-per-rank allgather inside
+            cx.allocate_scan_sharded(meets, R, P, pol, out=out)
+        else:
+            cx.allocate_scan(meets, R, P, pol, kept_base=rank * R, out=out)
             totals = sh.allgather(out["scalars"][2:3])
             cx.offsets_rebase(out["offsets"], totals, rank)
+        if e is not None:
+            e.record(torch.cuda.current_stream())
 
     if cfg.get("graph") and world == 1:
         # launch-bound size: capture K2 + K5 once, replay the graph (one launch per step)
@@ -683,13 +687,14 @@ def bench_reward(args, cfg, rank, world, cx, with_e2e=True):
 
 
 def bench_gang(args, cfg, rank, world, cx, with_e2e=True):
-    """Config E.  N=1: one radix-sorted order of all programs.  N>1: the 4M programs are
-    sharded (strong scaling of the fixed trace), each rank sorts its shard, the sorted key
-    runs are allgathered over NCCL and merged on every rank (sharding.Sharded.gang_order)."""
+    """Config G.  N=1: one radix-sorted order of all programs.  N>1: the 4M programs are
+    sharded (strong scaling of the fixed trace), each rank sorts its shard and the global
+    order comes from the distributed sample sort (cdx_gang_priority_sharded: samples
+    allgather, keys alltoallv to their bucket's rank, merge, ids allgather)."""
     import numpy as np
     import torch
     from paper_2412_20993_b200 import InterPolicy
-    from paper_2412_20993_b200.sharding import Sharded, max_shard, shard_range
+    from paper_2412_20993_b200.sharding import Sharded, shard_range
     N = cfg["N"]
     soa, now = gang_inputs(N, 20993 + 5, cfg["limit"])
     g0, gn = shard_range(N, rank, world)
@@ -697,14 +702,16 @@ def bench_gang(args, cfg, rank, world, cx, with_e2e=True):
                else torch.from_numpy(np.ascontiguousarray(v[g0:g0 + gn]))).cuda() for k, v in soa.items()}
     pol = InterPolicy(order=1, starvation_limit=cfg["limit"], prior_tokens=cfg["prior"])
     sh = Sharded(cx)
-    stride = max_shard(N, world)
+    gorder = torch.empty((N,), dtype=torch.int32, device="cuda")
 
     def step(seg):
         e = seg_events(seg, "gang_priority")
         if world == 1:
             cx.gang_priority(dev, pol, now)
+        elif sh.native:
+            cx.gang_priority_sharded(dev, pol, now, id_base=g0, capacity=N, out=gorder)
         else:
-            sh.gang_order(dev, pol, now, g0, stride)
+            sh.gang_order(dev, pol, now, g0, capacity=N)
         if e is not None:
             e.record(torch.cuda.current_stream())
 
@@ -724,12 +731,12 @@ def bench_gang(args, cfg, rank, world, cx, with_e2e=True):
             for k, v in host.items():
                 stage[k].copy_(v, non_blocking=True)
             order = cx.gang_priority(stage, pol, now)[0] if world == 1 else \
-                sh.gang_order(stage, pol, now, g0, stride)[0]
+                sh.gang_order(stage, pol, now, g0, capacity=N)
             res["order"] = order.cpu()
         e2e = e2e_host(args, world, one, N, sum(v.numel() * v.element_size() for v in host.values()), gn * 4,
                        "Context.gang_priority (C-ABI) from pinned host buffers, order read back, wall clock")
     return dict(value=N / (ms / 1e3), ms=ms, launches=launches, clocks=clocks,
-                kernel="gang_priority (radix sort, all passes)" + (" + allgather + merge" if world > 1 else ""),
+                kernel="gang_priority (radix sort, all passes)" + (" + sample-sort exchange" if world > 1 else ""),
                 kernel_ms=per["gang_priority"], kernel_bytes=b, step_bytes=b, extra={}, e2e=e2e,
                 scaling="strong")
 
@@ -780,7 +787,7 @@ def bench_mixed(args, cfg, rank, world, cx, with_e2e=True):
     import numpy as np
     import torch
     from paper_2412_20993_b200 import AllocPolicy, GenParams, InterPolicy, Threshold
-    from paper_2412_20993_b200.sharding import Sharded, max_shard, shard_range
+    from paper_2412_20993_b200.sharding import Sharded, shard_range
     N = cfg["N"]
     (scP, S), (cotP, w), (T, W) = cfg["sc"], cfg["cot"], cfg["rw"]
     arch, slot, sizes, knob, state, now = mixed_layout(cfg, N, 20993 + 7)
@@ -808,21 +815,26 @@ def bench_mixed(args, cfg, rank, world, cx, with_e2e=True):
               (("decision", torch.uint8), ("grant", torch.int32), ("cap", torch.int32), ("offsets", torch.int64))}
     outbuf["total"] = torch.empty((1,), dtype=torch.int64, device="cuda")
     sh = Sharded(cx)
-    stride = max_shard(N, world)
+    gorder = torch.empty((N,), dtype=torch.int32, device="cuda")
     res = {}
     torch.cuda.synchronize()
 
     def step(seg):
         e = seg_events(seg, "mixed_allocate")
         out = cx.mixed_allocate(trace, arch_d, slot_d, knob_d, pols, out=outbuf)
+        if world > 1:  # global budget offsets: allgather of the shard totals + device rebase
+            totals = sh.allgather(out["total"])
+            cx.offsets_rebase(out["offsets"], totals, rank)
         if e is not None:
             e.record(torch.cuda.current_stream())
         e = seg_events(seg, "gang_priority")
         soa = dict(st_d, terminated=out["decision"], cap=out["cap"])
         if world == 1:
             res["order"] = cx.gang_priority(soa, ipol, now)[0]
+        elif sh.native:
+            res["order"] = cx.gang_priority_sharded(soa, ipol, now, id_base=g0, capacity=N, out=gorder)
         else:
-            res["order"] = sh.gang_order(soa, ipol, now, g0, stride)[0]
+            res["order"] = sh.gang_order(soa, ipol, now, g0, capacity=N)
         if e is not None:
             e.record(torch.cuda.current_stream())
 
@@ -844,12 +856,18 @@ def bench_mixed(args, cfg, rank, world, cx, with_e2e=True):
                       "probe_evals_per_step": n_r[0] * scP * S + n_r[1] * cotP + n_r[2] * T * W,
                       "trace_bytes": trace_b},
                scaling="strong")
-    out["e2e"] = e2e_mixed(args, cx, trace, arch_d, slot_d, knob_d, st_d, pols, ipol, now, world, N) \
+    def gang(soa):  # the global order at N > 1, as in the device-timed step
+        if world == 1:
+            return cx.gang_priority(soa, ipol, now)[0]
+        if sh.native:
+            return cx.gang_priority_sharded(soa, ipol, now, id_base=g0, capacity=N, out=gorder)
+        return sh.gang_order(soa, ipol, now, g0, capacity=N)
+    out["e2e"] = e2e_mixed(args, cx, trace, arch_d, slot_d, knob_d, st_d, pols, gang, world, N) \
         if (with_e2e and not args.no_e2e) else None
     return out
 
 
-def e2e_mixed(args, cx, trace, arch_d, slot_d, knob_d, st_d, pols, ipol, now, world, N):
+def e2e_mixed(args, cx, trace, arch_d, slot_d, knob_d, st_d, pols, gang, world, N):
     """Config E through the public API from pinned host buffers: every step copies the whole
     trace and program table host -> device, runs the mixed step and the gang order, and reads
     the order and the decisions back (wall clock, barrier on both sides, slowest rank)."""
@@ -871,8 +889,7 @@ def e2e_mixed(args, cx, trace, arch_d, slot_d, knob_d, st_d, pols, ipol, now, wo
         out = cx.mixed_allocate(tr, stage["arch"], stage["slot"], stage["knob"], pols)
         soa = {k: stage[k] for k in ("arrival", "last_service", "iter_tok_sum", "iter_count", "knob")}
         soa.update(terminated=out["decision"], cap=out["cap"])
-        order = cx.gang_priority(soa, ipol, now)[0]
-        res["order"] = order.cpu()
+        res["order"] = gang(soa).cpu()
         res["decision"] = out["decision"].cpu()
 
     for _ in range(max(1, min(args.warmup, 2))):
@@ -926,7 +943,12 @@ def main():
         return
 
     from paper_2412_20993_b200 import Context
-    cx = Context(local)
+    if world > 1 and os.environ.get("CDX_BENCH_BACKEND", "nccl") == "nccl":
+        # the context owns an NCCL communicator spanning the job (cdx_ctx_create_comm): the
+        # exchange steps run through the C-ABI sharded entries, as a C++ caller would
+        cx = Context.for_process_group(local)
+    else:
+        cx = Context(local)
     peak, peak_src = load_peaks()
     res = BENCH[cfg["kind"]](args, cfg, rank, world, cx)
     others = {}

@@ -15,6 +15,8 @@
 //   cot_eps_stop       the epsilon-accuracy stop rule at every CoT prefix (probe.cpp:104-120)
 //   jsonl_parse        probe-trace JSONL ingestion (probe.cpp:126-165)
 //   Graph              capture / replay of a call sequence (launch-bound small batches)
+//   allocate_scan_sharded / gang_priority_sharded   K5 / K6 with global results across the
+//                      ranks of a multi-GPU job (Context(device, comm))
 
 #include <cstddef>
 #include <cstdint>
@@ -36,6 +38,10 @@ namespace cdx::batch {
 class Context {
 public:
     explicit Context(int device = 0);
+    // A rank of a multi-GPU job: the context owns the communicator (NCCL from comm.nccl_id,
+    // or the caller's allgather / alltoallv callbacks); the *_sharded calls below exchange
+    // through it.  Collective with NCCL.
+    Context(int device, const cdx_comm& comm);
     ~Context();
     Context(const Context&) = delete;
     Context& operator=(const Context&) = delete;
@@ -137,6 +143,12 @@ void allocate_scan(Context& cx, const uint32_t* meets, uint64_t requests, uint32
                    const scheduler::AllocationPolicy& policy, int64_t tokens_per_unit, int64_t base_offset,
                    uint32_t kept_base, const AllocationOutputs& out);
 
+// The same over this rank's request shard with GLOBAL offsets, kept indices and totals
+// (cdx_allocate_scan_sharded); n_kept is this rank's kept count.
+void allocate_scan_sharded(Context& cx, const uint32_t* meets, uint64_t requests, uint32_t probes,
+                           const scheduler::AllocationPolicy& policy, int64_t tokens_per_unit,
+                           const AllocationOutputs& out, uint64_t* shard_info = nullptr);
+
 // ---- K3: CoT probe window --------------------------------------------------------------
 
 struct CotOutputs {
@@ -173,6 +185,11 @@ uint64_t canon_intern(Context& cx, const char* arena, const uint64_t* offsets, u
 uint64_t gang_priority(Context& cx, const cdx_prog_soa& progs, uint64_t n,
                        const scheduler::InterSchedPolicy& policy, double now, uint32_t* order,
                        uint8_t* escalated, uint64_t* keys);
+
+// The GLOBAL order of every rank's live programs (program ids must be global), on every rank
+// (cdx_gang_priority_sharded); returns its length.
+uint64_t gang_priority_sharded(Context& cx, const cdx_prog_soa& progs, uint64_t n,
+                               const scheduler::InterSchedPolicy& policy, double now, uint32_t* order);
 
 // ---- aggregation (runtime.cpp:316-403) ---------------------------------------------------
 

@@ -30,7 +30,7 @@
 extern "C" {
 #endif
 
-#define CDX_ABI_VERSION 3
+#define CDX_ABI_VERSION 4
 
 typedef enum {
     CDX_OK = 0,
@@ -405,6 +405,81 @@ int cdx_gang_priority(cdx_ctx* ctx, const cdx_prog_soa* progs, uint64_t N,
  * total (device u64, nullable) their count.  Used after the NCCL allgather (K6).        */
 int cdx_gang_merge(cdx_ctx* ctx, const uint64_t* keys, const uint64_t* run_len, uint32_t runs,
                    uint64_t stride, uint32_t* order_out, uint64_t* total);
+
+/* ---- multi-GPU: a context that owns its communicator -------------
+ * One process (or host thread) per rank, one context per rank.  Requests / programs shard
+ * into contiguous per-rank slices with no data-path exchange; the sharded entry points below
+ * run the only two exchange steps (global token offsets, the global gang order) through the
+ * context's communicator.  The transport is either
+ *   - NCCL: nccl_id (128 bytes = ncclUniqueId, made once by cdx_nccl_unique_id on one rank and
+ *     broadcast by the caller).  The context creates and owns an NCCL communicator over
+ *     libnccl.so.2, loaded at run time (NVLink / NVSwitch on one box); or
+ *   - caller callbacks (any transport: an NCCL communicator the caller owns, MPI, host
+ *     staging between threads).  Buffers are DEVICE pointers; a callback must order its
+ *     transfers after the work already queued on `stream` (a cudaStream_t) and complete them
+ *     (or queue them on `stream`) before returning; nonzero return = failure (CDX_ENCCL).
+ * The reference is single-process (proj/src/CMakeLists.txt:11-12), so these have no
+ * reference counterpart: concatenating the ranks' outputs reproduces the 1-GPU result.    */
+typedef struct {
+    uint32_t rank, world;
+    const uint8_t* nccl_id; /* non-null: NCCL transport (callbacks ignored) */
+    void* user;             /* callbacks' first argument */
+    /* recv[q*bytes .. (q+1)*bytes) <- rank q's send[0 .. bytes) */
+    int (*allgather)(void* user, const void* send, void* recv, uint64_t bytes, void* stream);
+    /* send[send_off[q] .. + send_bytes[q]) -> rank q; recv[recv_off[q] .. + recv_bytes[q]) <- rank q.
+     * counts and offsets are HOST arrays of `world` entries (bytes) */
+    int (*alltoallv)(void* user, const void* send, const uint64_t* send_bytes, const uint64_t* send_off,
+                     void* recv, const uint64_t* recv_bytes, const uint64_t* recv_off, void* stream);
+} cdx_comm;
+
+/* A 128-byte NCCL unique id for cdx_comm.nccl_id (CDX_ENCCL when libnccl.so.2 is absent). */
+int cdx_nccl_unique_id(uint8_t id[128]);
+/* cdx_ctx_create plus a communicator (comm nullable = world 1, no exchange).  Collective:
+ * with NCCL every rank must call it. */
+int cdx_ctx_create_comm(int device, const cdx_comm* comm, cdx_ctx** out);
+int cdx_ctx_comm_info(const cdx_ctx* ctx, uint32_t* rank, uint32_t* world);
+/* recv[q*bytes ..] <- rank q's send (DEVICE), on the context stream. */
+int cdx_allgather(cdx_ctx* ctx, const void* send, void* recv, uint64_t bytes);
+
+/* K5 over this rank's request shard with GLOBAL results (SPEC.md:404-412 over the whole
+ * batch): as cdx_allocate_scan, but offsets are the exclusive scan over all ranks' requests in
+ * rank order, kept holds GLOBAL request indices (rank q's first request is the sum of the
+ * requests of ranks < q), *n_kept (device) this rank's kept count, *tokens_saved and
+ * *total_budget (device, nullable) the sums over all ranks.  shard_info (device u64[world][4],
+ * nullable) receives every rank's {requests, budget total, kept, tokens saved}.  Collective.  */
+int cdx_allocate_scan_sharded(cdx_ctx* ctx, const uint32_t* meets_bits, uint64_t R, uint32_t P,
+                              const cdx_alloc_policy* pol, int32_t* exit_knob, uint8_t* reason,
+                              int32_t* granted, int64_t* offsets, uint32_t* kept, uint64_t* n_kept,
+                              int64_t* tokens_saved, int64_t* total_budget, uint64_t* shard_info);
+
+/* K6 over this rank's programs (GLOBAL program ids via progs->program_id / id_base) with the
+ * GLOBAL order on every rank: a distributed sample sort.  Each rank sorts its keys (as
+ * cdx_gang_priority), allgathers cdx_shard_samples of its run, derives the same splitters
+ * (cdx_shard_splitters), sends each key to the rank owning its bucket (alltoallv, about
+ * 24 B x N_local x (world-1)/world per rank), merges the runs it received and the buckets'
+ * program ids are allgathered in bucket order (4 B per program).  order: DEVICE u32 with room
+ * for every rank's live programs; *n_out (host) = their count.  Identical to the 1-GPU order
+ * (the composite key is a total order).  Collective.                                        */
+int cdx_gang_priority_sharded(cdx_ctx* ctx, const cdx_prog_soa* progs, uint64_t N_local,
+                              const cdx_inter_policy* pol, double now, uint32_t* order, uint64_t* n_out);
+
+/* Building blocks of the sample sort (also used by torch.distributed hosts, sharding.py).
+ * cdx_shard_samples: s keys of a sorted run keys u64[n][3] (DEVICE) at the midpoints of s
+ * equal ranges -> samples u64[s][3] (DEVICE); all-ones sentinels when n == 0.
+ * cdx_shard_splitters (HOST only, no device): samples u64[world][s][3] and counts u64[world]
+ * (every rank's run length) -> world-1 splitters u64[world-1][3]: bucket b holds the keys k
+ * with splitter[b-1] <= k < splitter[b]; each sample stands for counts[q]/s keys and
+ * splitter b is the first sample at which the weight before it reaches b * total / world.
+ * cdx_shard_bounds: bucket boundaries of a sorted run -> bounds u64[world+1] (DEVICE).
+ * cdx_gang_merge_runs: merge sorted runs keys[run_off[q] .. run_off[q+1]) (run_off DEVICE
+ * u64[runs+1]) -> program ids order_out u32[run_off[runs]].                                */
+int cdx_shard_samples(cdx_ctx* ctx, const uint64_t* keys, uint64_t n, uint32_t s, uint64_t* samples);
+int cdx_shard_splitters(const uint64_t* samples, const uint64_t* counts, uint32_t world, uint32_t s,
+                        uint64_t* splitters);
+int cdx_shard_bounds(cdx_ctx* ctx, const uint64_t* keys, uint64_t n, const uint64_t* splitters,
+                     uint32_t world, uint64_t* bounds);
+int cdx_gang_merge_runs(cdx_ctx* ctx, const uint64_t* keys, const uint64_t* run_off, uint32_t runs,
+                        uint32_t* order_out);
 
 /* Global token offsets across request shards (K5 multi-GPU): offsets[i] += sum of
  * shard_totals[q] for q < rank.  shard_totals i64[world] is the allgathered vector of

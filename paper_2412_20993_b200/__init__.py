@@ -158,21 +158,68 @@ def _ptr(t) -> Optional[int]:
     return None if t is None else t.data_ptr()
 
 
+def nccl_unique_id() -> bytes:
+    """128-byte NCCL unique id for Context.with_nccl (host only)."""
+    buf = (C.c_uint8 * 128)()
+    st = _abi.load().cdx_nccl_unique_id(C.cast(buf, C.c_void_p))
+    if st != _abi.CDX_OK:
+        raise CdxNcclError("cdx_nccl_unique_id failed (libnccl.so.2 not loadable)")
+    return bytes(buf)
+
+
+def shard_splitters(samples, counts, world: int, s: int):
+    """Host-only planning step of the sharded gang order (cdx_shard_splitters): samples
+    u64[world][s][3], counts u64[world] (numpy) -> splitters u64[world-1][3]."""
+    import numpy as np
+    smp = np.ascontiguousarray(samples, dtype=np.uint64).reshape(world, s, 3)
+    cnt = np.ascontiguousarray(counts, dtype=np.uint64).reshape(world)
+    out = np.zeros((max(world - 1, 1), 3), np.uint64)
+    st = _abi.load().cdx_shard_splitters(smp.ctypes.data, cnt.ctypes.data, world, s, out.ctypes.data)
+    if st != _abi.CDX_OK:
+        raise CdxInvalidArgument("shard_splitters: bad arguments")
+    return out[: world - 1]
+
+
 class Context:
     """One cdx_ctx bound to a CUDA device; calls run on torch's current stream."""
 
-    def __init__(self, device: int = 0):
+    def __init__(self, device: int = 0, comm: Optional["_abi.Comm"] = None):
         import torch
         self.torch = torch
         self.lib = _abi.load()
         self.device = device
         h = C.c_void_p()
-        st = self.lib.cdx_ctx_create(device, C.byref(h))
+        self._comm = comm  # keeps the callbacks / id buffer alive as long as the context
+        if comm is None:
+            st = self.lib.cdx_ctx_create(device, C.byref(h))
+        else:
+            st = self.lib.cdx_ctx_create_comm(device, C.byref(comm), C.byref(h))
         if st != _abi.CDX_OK:
             raise _ERR.get(st, CdxError)(f"cdx_ctx_create(device={device}) failed with status {st}"
                                          " (a B200 / sm_100 device is required; there is no CPU fallback)")
         self.h = h
         self.dev = torch.device("cuda", device)
+        self.rank = comm.rank if comm is not None else 0
+        self.world = comm.world if comm is not None else 1
+
+    @classmethod
+    def with_nccl(cls, device: int, rank: int, world: int, nccl_id: bytes) -> "Context":
+        """A context owning an NCCL communicator (collective: every rank calls it with the
+        same 128-byte id from nccl_unique_id())."""
+        buf = (C.c_uint8 * 128).from_buffer_copy(nccl_id)
+        comm = _abi.Comm(rank=rank, world=world, nccl_id=C.cast(buf, C.c_void_p))
+        comm._id_buf = buf
+        return cls(device, comm)
+
+    @classmethod
+    def for_process_group(cls, device: int, group=None) -> "Context":
+        """A context whose NCCL communicator spans torch.distributed's `group` (rank 0 makes
+        the id, torch broadcasts it; torch's own communicator is not used by the kernels)."""
+        import torch.distributed as dist
+        rank, world = dist.get_rank(group), dist.get_world_size(group)
+        obj = [nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=dist.get_global_rank(group, 0) if group is not None else 0, group=group)
+        return cls.with_nccl(device, rank, world, obj[0])
 
     def close(self):
         if getattr(self, "h", None):
@@ -503,6 +550,68 @@ class Context:
         self._check(self.lib.cdx_gang_merge(self.h, _ptr(keys), _ptr(run_len), runs, stride, _ptr(out),
                                             _ptr(total)))
         return out
+
+    # -- multi-GPU: the context's communicator (shard.cu) --
+    def allocate_scan_sharded(self, meets, R: int, P: int, policy: AllocPolicy, out=None):
+        """K5 over this rank's requests with global offsets / kept indices / totals."""
+        t = self.torch
+        o = out or {}
+        exit_knob = o["exit_knob"] if "exit_knob" in o else self.empty((max(R, 1),), t.int32)
+        reason = o["reason"] if "reason" in o else self.empty((max(R, 1),), t.uint8)
+        granted = o["granted"] if "granted" in o else self.empty((max(R, 1),), t.int32)
+        offsets = o["offsets"] if "offsets" in o else self.empty((max(R, 1),), t.int64)
+        kept = o["kept"] if "kept" in o else self.empty((max(R, 1),), t.int32)
+        scal = o["scalars"] if "scalars" in o else self.empty((3,), t.int64)
+        info = o["shard_info"] if "shard_info" in o else self.empty((self.world, 4), t.int64)
+        pol = c_policy(policy)
+        self._bind_stream()
+        self._check(self.lib.cdx_allocate_scan_sharded(self.h, _ptr(meets), R, P, C.byref(pol), _ptr(exit_knob),
+                                                       _ptr(reason), _ptr(granted), _ptr(offsets), _ptr(kept),
+                                                       scal.data_ptr(), scal.data_ptr() + 8, scal.data_ptr() + 16,
+                                                       _ptr(info)))
+        return dict(exit_knob=exit_knob[:R], reason=reason[:R], granted=granted[:R], offsets=offsets[:R],
+                    kept=kept, scalars=scal, shard_info=info)
+
+    def gang_priority_sharded(self, soa: dict, policy: InterPolicy, now: float, id_base: int = 0,
+                              capacity: Optional[int] = None, out=None):
+        """The global gang order on every rank (distributed sample sort); `capacity` bounds
+        the global live count (default: world x this rank's programs)."""
+        t = self.torch
+        N = soa["arrival"].shape[0]
+        s = _abi.ProgSoA()
+        for k in ("arrival", "last_service", "iter_tok_sum", "iter_count", "knob", "cap", "terminated"):
+            setattr(s, k, soa[k].data_ptr())
+        if soa.get("program_id") is not None:
+            s.program_id = soa["program_id"].data_ptr()
+        s.id_base = id_base
+        cap = capacity if capacity is not None else self.world * max(N, 1)
+        order = out if out is not None else self.empty((max(cap, 1),), t.int32)
+        n_out = C.c_uint64(0)
+        pol = c_inter(policy)
+        self._bind_stream()
+        self._check(self.lib.cdx_gang_priority_sharded(self.h, C.byref(s), N, C.byref(pol), float(now), _ptr(order),
+                                                       C.byref(n_out)))
+        return order[: n_out.value]
+
+    def shard_samples(self, keys, s: int):
+        out = self.empty((s, 3), self.torch.int64)
+        self._bind_stream()
+        self._check(self.lib.cdx_shard_samples(self.h, _ptr(keys), keys.shape[0], s, _ptr(out)))
+        return out
+
+    def shard_bounds(self, keys, splitters, world: int):
+        out = self.empty((world + 1,), self.torch.int64)
+        self._bind_stream()
+        self._check(self.lib.cdx_shard_bounds(self.h, _ptr(keys), keys.shape[0], _ptr(splitters), world, _ptr(out)))
+        return out
+
+    def gang_merge_runs(self, keys, run_off):
+        """keys i64[n][3] holding sorted runs at run_off (device i64[runs+1]) -> program ids."""
+        n = keys.shape[0]
+        out = self.empty((max(n, 1),), self.torch.int32)
+        self._bind_stream()
+        self._check(self.lib.cdx_gang_merge_runs(self.h, _ptr(keys), _ptr(run_off), run_off.shape[0] - 1, _ptr(out)))
+        return out[:n]
 
     def offsets_rebase(self, offsets, shard_totals, rank: int):
         self._bind_stream()

@@ -70,6 +70,17 @@ class MixedTrace(C.Structure):
 class ArchPolicy(C.Structure):
     _fields_ = [("th", Threshold * 4), ("n_th", U32), ("_pad", U32), ("alloc", AllocPolicy)]
 
+ALLGATHER_FN = C.CFUNCTYPE(C.c_int, P, P, P, U64, P)
+ALLTOALLV_FN = C.CFUNCTYPE(C.c_int, P, P, C.POINTER(U64), C.POINTER(U64), P, C.POINTER(U64), C.POINTER(U64), P)
+
+
+class Comm(C.Structure):
+    _fields_ = [("rank", U32), ("world", U32), ("nccl_id", P), ("user", P), ("allgather", ALLGATHER_FN),
+                ("alltoallv", ALLTOALLV_FN)]
+
+
+SIG_MAJORITY = 4
+
 # name -> (restype, argtypes); this table is also the export list tests check against cdx_c.h
 SIGNATURES = {
     "cdx_abi_version": (C.c_int, []),
@@ -118,6 +129,17 @@ SIGNATURES = {
                                     C.POINTER(U64), P, P]),
     "cdx_gang_merge": (C.c_int, [P, P, P, U32, U64, P, P]),
     "cdx_offsets_rebase": (C.c_int, [P, P, U64, P, U32]),
+    "cdx_nccl_unique_id": (C.c_int, [P]),
+    "cdx_ctx_create_comm": (C.c_int, [C.c_int, C.POINTER(Comm), C.POINTER(P)]),
+    "cdx_ctx_comm_info": (C.c_int, [P, C.POINTER(U32), C.POINTER(U32)]),
+    "cdx_allgather": (C.c_int, [P, P, P, U64]),
+    "cdx_allocate_scan_sharded": (C.c_int, [P, P, U64, U32, C.POINTER(AllocPolicy), P, P, P, P, P, P, P, P, P]),
+    "cdx_gang_priority_sharded": (C.c_int, [P, C.POINTER(ProgSoA), U64, C.POINTER(InterPolicy), C.c_double, P,
+                                            C.POINTER(U64)]),
+    "cdx_shard_samples": (C.c_int, [P, P, U64, U32, P]),
+    "cdx_shard_splitters": (C.c_int, [P, P, U32, U32, P]),
+    "cdx_shard_bounds": (C.c_int, [P, P, U64, P, U32, P]),
+    "cdx_gang_merge_runs": (C.c_int, [P, P, P, U32, P]),
     "cdx_jsonl_parse": (C.c_int, [P, P, U64, U64, P, P, P, P, P, P, P, P, P, C.POINTER(U64), C.POINTER(U64)]),
     "cdx_cot_eps_stop": (C.c_int, [P, P, P, U64, U32, I32, C.c_double, P, P]),
     "cdx_probe_eps_stop_rows": (C.c_int, [P, P, P, P, U64, I32, C.c_double, P]),

@@ -61,6 +61,16 @@ struct cdx_ctx {
     double* tt_dev = nullptr;
     size_t tt_bytes = 0;
     std::string tt_key;
+    // communicator (shard.cu): rank / world, the caller's callbacks or an owned NCCL comm
+    uint32_t rank = 0, world = 1;
+    cdx_comm comm{};
+    void* nccl = nullptr;  // ncclComm_t
+    // sharded paths' buffers (shard.cu)
+    void* sh_buf = nullptr;
+    size_t sh_bytes = 0;
+    void* sh_buf2 = nullptr;
+    size_t sh_bytes2 = 0;
+    uint64_t* sh_host = nullptr;  // pinned host staging (counts, bounds)
 };
 
 namespace cdx {
@@ -70,6 +80,8 @@ int cuda_fail(cdx_ctx* ctx, cudaError_t e, const char* what);
 void* scratch(cdx_ctx* ctx, size_t bytes);
 void* scratch2(cdx_ctx* ctx, size_t bytes);
 void* scratch3(cdx_ctx* ctx, size_t bytes);  // the mixed step's own buffers (K2/K4 use scratch, scratch2)
+void* grow_buffer(cdx_ctx* ctx, void** buf, size_t* have, size_t bytes);
+void comm_destroy(cdx_ctx* ctx);  // shard.cu
 // device-side validation error codes (set via atomicCAS on ctx->d_err)
 enum DevErr : int {
     DEV_OK = 0,

@@ -34,6 +34,8 @@ static void* grow(cdx_ctx* ctx, void** buf, size_t* have, size_t bytes) {
     return *buf;
 }
 
+void* grow_buffer(cdx_ctx* ctx, void** buf, size_t* have, size_t bytes) { return grow(ctx, buf, have, bytes); }
+
 void* scratch(cdx_ctx* ctx, size_t bytes) { return grow(ctx, &ctx->scratch, &ctx->scratch_bytes, bytes); }
 void* scratch2(cdx_ctx* ctx, size_t bytes) {
     return grow(ctx, &ctx->scratch2, &ctx->scratch2_bytes, bytes);
@@ -196,6 +198,10 @@ int cdx_ctx_destroy(cdx_ctx* ctx) {
     for (double* t : ctx->comp_tab)
         if (t) cudaFree(t);
     if (ctx->jl_buf) cudaFree(ctx->jl_buf);
+    cdx::comm_destroy(ctx);
+    if (ctx->sh_buf) cudaFree(ctx->sh_buf);
+    if (ctx->sh_buf2) cudaFree(ctx->sh_buf2);
+    if (ctx->sh_host) cudaFreeHost(ctx->sh_host);
     if (ctx->d_err) cudaFree(ctx->d_err);
     if (ctx->h_err) cudaFreeHost(ctx->h_err);
     if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);

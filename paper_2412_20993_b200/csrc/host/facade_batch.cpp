@@ -28,6 +28,14 @@ Context::Context(int device) {
                   .c_str());
 }
 
+Context::Context(int device, const cdx_comm& comm) {
+    const int st = cdx_ctx_create_comm(device, &comm, &h_);
+    if (st == CDX_ENCCL) raise(CDX_ERUNTIME, "cdx: NCCL communicator could not be created (libnccl.so.2)");
+    if (st != CDX_OK)
+        raise(st == CDX_EINVAL ? CDX_EINVAL : CDX_ERUNTIME,
+              ("cdx: no usable sm_100 device " + std::to_string(device) + " or a bad communicator").c_str());
+}
+
 Context::~Context() {
     if (h_) cdx_ctx_destroy(h_);
 }
@@ -99,6 +107,19 @@ void allocate_scan(Context& cx, const uint32_t* meets, uint64_t R, uint32_t P,
                                o.offsets, o.kept, o.n_kept, o.tokens_saved, o.total_budget));
 }
 
+void allocate_scan_sharded(Context& cx, const uint32_t* meets, uint64_t R, uint32_t P,
+                           const scheduler::AllocationPolicy& pol, int64_t tokens_per_unit, const AllocationOutputs& o,
+                           uint64_t* shard_info) {
+    cdx_alloc_policy p{};
+    p.kind = policy_kind(pol.kind);
+    p.detect_at = pol.detect_at_knob;
+    p.recheck_every = pol.recheck_every;
+    p.resource_cap = pol.resource_cap;
+    p.tokens_per_unit = tokens_per_unit;
+    cx.check(cdx_allocate_scan_sharded(cx.raw(), meets, R, P, &p, o.exit_knob, o.reason, o.granted, o.offsets, o.kept,
+                                       o.n_kept, o.tokens_saved, o.total_budget, shard_info));
+}
+
 void cot_exit(Context& cx, const uint32_t* ids, const uint64_t* hes, const int64_t* offsets, uint64_t R, uint32_t P,
               const probe::ProbeConfig& cfg, const CotOutputs& o) {
     cfg.validate();
@@ -128,8 +149,8 @@ uint64_t canon_intern(Context& cx, const char* arena, const uint64_t* offsets, u
     return nu;
 }
 
-uint64_t gang_priority(Context& cx, const cdx_prog_soa& progs, uint64_t n, const scheduler::InterSchedPolicy& pol,
-                       double now, uint32_t* order, uint8_t* escalated, uint64_t* keys) {
+namespace {
+cdx_inter_policy inter_policy(const scheduler::InterSchedPolicy& pol) {
     cdx_inter_policy p{};
     p.gang = pol.gang ? 1 : 0;
     switch (pol.order) {
@@ -139,8 +160,23 @@ uint64_t gang_priority(Context& cx, const cdx_prog_soa& progs, uint64_t n, const
     }
     p.starvation_limit = pol.starvation_limit;
     p.prior_tokens = pol.prior_tokens;
+    return p;
+}
+}  // namespace
+
+uint64_t gang_priority(Context& cx, const cdx_prog_soa& progs, uint64_t n, const scheduler::InterSchedPolicy& pol,
+                       double now, uint32_t* order, uint8_t* escalated, uint64_t* keys) {
+    const cdx_inter_policy p = inter_policy(pol);
     uint64_t n_out = 0;
     cx.check(cdx_gang_priority(cx.raw(), &progs, n, &p, now, order, &n_out, escalated, keys));
+    return n_out;
+}
+
+uint64_t gang_priority_sharded(Context& cx, const cdx_prog_soa& progs, uint64_t n,
+                               const scheduler::InterSchedPolicy& pol, double now, uint32_t* order) {
+    const cdx_inter_policy p = inter_policy(pol);
+    uint64_t n_out = 0;
+    cx.check(cdx_gang_priority_sharded(cx.raw(), &progs, n, &p, now, order, &n_out));
     return n_out;
 }
 

@@ -38,7 +38,7 @@ def test_binding_table_covers_header():
 
 
 def test_abi_version(lib):
-    assert lib.cdx_abi_version() == 3
+    assert lib.cdx_abi_version() == 4
 
 
 def test_no_cpu_fallback():

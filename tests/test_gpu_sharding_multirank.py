@@ -53,7 +53,7 @@ def _worker(rank, world, port, q):
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
         from paper_2412_20993_b200 import AllocPolicy, Context, GenParams, InterPolicy, Threshold
-        from paper_2412_20993_b200.sharding import Sharded, max_shard, shard_range
+        from paper_2412_20993_b200.sharding import Sharded, shard_range
         cx = Context(0)
         sh = Sharded(cx)
         assert not sh.nccl and sh.world == world
@@ -66,12 +66,11 @@ def _worker(rank, world, port, q):
         part = {k: (torch.from_numpy(np.ascontiguousarray(v[g0:g0 + gn])) if v.dtype != np.uint16 else
                     torch.from_numpy(np.ascontiguousarray(v[g0:g0 + gn]).view(np.int16))).cuda()
                 for k, v in soa.items()}
-        order, total = sh.gang_order(part, InterPolicy(order=1, starvation_limit=0.15, prior_tokens=128.0), now,
-                                     g0, max_shard(N_PROG, world))
+        order = sh.gang_order(part, InterPolicy(order=1, starvation_limit=0.15, prior_tokens=128.0), now, g0)
         cx.sync()
         nk = int(res["scalars"][0])
         q.put((rank, res["offsets"].cpu().numpy(), res["kept"][:nk].cpu().numpy().view(np.uint32),
-               res["exit_knob"].cpu().numpy(), order[: int(total)].cpu().numpy().view(np.uint32)))
+               res["exit_knob"].cpu().numpy(), order.cpu().numpy().view(np.uint32)))
     finally:
         dist.destroy_process_group()
 

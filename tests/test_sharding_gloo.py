@@ -59,6 +59,27 @@ class CheckerOps:
         k = torch.from_numpy(keys.view(np.int64))
         return torch.from_numpy(ref.view(np.int32)), None, k
 
+    # device building blocks of the sample sort (shard.cu), restated on the host
+    def shard_samples(self, keys, s):
+        k = keys.numpy().view(np.uint64)
+        n = k.shape[0]
+        if n == 0:
+            return torch.full((s, 3), -1, dtype=torch.int64)
+        idx = ((2 * np.arange(s, dtype=np.uint64) + 1) * n) // (2 * s)
+        return torch.from_numpy(np.ascontiguousarray(k[idx]).view(np.int64))
+
+    def shard_bounds(self, keys, split, world):
+        k = [tuple(r) for r in keys.numpy().view(np.uint64).tolist()]
+        sp = [tuple(r) for r in split.numpy().view(np.uint64).tolist()]
+        import bisect
+        b = [0] + [bisect.bisect_left(k, x) for x in sp] + [len(k)]
+        return torch.tensor(b, dtype=torch.int64)
+
+    def gang_merge_runs(self, keys, run_off):
+        rows = keys.numpy().view(np.uint64)
+        rows = rows[np.lexsort((rows[:, 2], rows[:, 1], rows[:, 0]))]
+        return torch.from_numpy(rows[:, 2].astype(np.uint32).view(np.int32))
+
     def gang_merge(self, recv, lens, stride, total=None):
         keys = recv.numpy().view(np.uint64)
         rows = np.concatenate([keys[q * stride: q * stride + int(lens[q])] for q in range(len(lens))])
@@ -97,10 +118,9 @@ def _worker(rank, world, port, q):
         res = sh.sc_decide(torch.from_numpy(ids[r0:r0 + n].view(np.int32)), [Threshold(0, 0.7, 0)], pol, r0)
         g0, gn = shard_range(N_PROG, rank, world)
         part = {k: torch.from_numpy(np.ascontiguousarray(v[g0:g0 + gn])) for k, v in soa.items()}
-        order, total = sh.gang_order(part, InterPolicy(order=1, starvation_limit=0.15, prior_tokens=128.0), now,
-                                     g0, max_shard(N_PROG, world))
+        order = sh.gang_order(part, InterPolicy(order=1, starvation_limit=0.15, prior_tokens=128.0), now, g0)
         q.put((rank, res["offsets"].numpy(), res["kept"].numpy(), res["shard_totals"].numpy(),
-               order[: int(total)].numpy().view(np.uint32)))
+               order.numpy().view(np.uint32)))
     finally:
         dist.destroy_process_group()
 
@@ -113,7 +133,7 @@ def _free_port():
     return p
 
 
-@pytest.mark.parametrize("world", [2])
+@pytest.mark.parametrize("world", [2, 3])
 def test_sharded_equals_single_process(world):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
@@ -135,7 +155,8 @@ def test_sharded_equals_single_process(world):
     kept = np.concatenate([got[r][1] for r in range(world)])
     assert np.array_equal(offsets, ref["offsets"])
     assert np.array_equal(kept, ref["kept"].astype(np.int64))
-    assert np.array_equal(got[0][2], got[1][2])
+    for r in range(1, world):
+        assert np.array_equal(got[0][2], got[r][2])
     gref, _ = O.gang_order(soa, 1, 0.15, 128.0, now)
     for r in range(world):
         assert np.array_equal(got[r][3], gref)
@@ -148,3 +169,40 @@ def test_shard_range_covers():
             assert spans[0][0] == 0 and sum(c for _, c in spans) == n
             assert all(spans[i][0] + spans[i][1] == spans[i + 1][0] for i in range(w - 1))
             assert max_shard(n, w) == max(c for _, c in spans)
+
+
+@pytest.mark.parametrize("world,seed", [(2, 0), (3, 1), (8, 2), (8, 3), (5, 4)])
+def test_shard_splitters_partition_the_global_order(world, seed):
+    """The product's host planning step (libcdx cdx_shard_splitters, no device): buckets cut
+    by its splitters are contiguous ranges of the global order, every key lands in exactly
+    one bucket, and buckets are balanced to within the sampling error."""
+    from paper_2412_20993_b200 import shard_splitters
+    from paper_2412_20993_b200.sharding import SHARD_SAMPLES as s
+    rng = np.random.default_rng(seed)
+    sizes = rng.integers(0, 3000, world)
+    sizes[rng.integers(0, world)] = 0  # an empty rank
+    runs = []
+    for q in range(world):
+        k = np.stack([rng.integers(0, 50, sizes[q]).astype(np.uint64) << np.uint64(40),
+                      rng.integers(0, 4, sizes[q]).astype(np.uint64),
+                      rng.permutation(100000)[: sizes[q]].astype(np.uint64) * world + q], 1)
+        runs.append(k[np.lexsort((k[:, 2], k[:, 1], k[:, 0]))])
+    samples = np.full((world, s, 3), np.iinfo(np.uint64).max, np.uint64)
+    for q in range(world):
+        n = len(runs[q])
+        if n:
+            samples[q] = runs[q][((2 * np.arange(s, dtype=np.uint64) + 1) * n) // (2 * s)]
+    split = shard_splitters(samples, sizes.astype(np.uint64), world, s)
+    assert split.shape == (world - 1, 3)
+    allk = np.concatenate(runs)
+    allk = allk[np.lexsort((allk[:, 2], allk[:, 1], allk[:, 0]))]
+    tup = [tuple(r) for r in allk.tolist()]
+    import bisect
+    cuts = [0] + [bisect.bisect_left(tup, tuple(x)) for x in split.tolist()] + [len(tup)]
+    assert all(a <= b for a, b in zip(cuts, cuts[1:]))
+    total = len(tup)
+    # each run contributes s samples standing for n/s keys: a bucket deviates by at most
+    # about world runs x 2 sample weights from total/world
+    slack = sum(2 * int(sz) // s + 2 for sz in sizes)
+    for b in range(world):
+        assert abs((cuts[b + 1] - cuts[b]) - total / world) <= slack, (b, cuts, total)
