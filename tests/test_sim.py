@@ -44,4 +44,52 @@ def test_sim_host_arithmetic_and_loud_failure():
 
 @pytest.mark.gpu
 def test_sim_spec_examples():
-    assert _run() == SPEC
+    got = _run()
+    assert {k: got[k] for k in SPEC} == SPEC
+
+
+def _poisson_restated(n, rate, seed):
+    """SimConfig::arrival_rate restated: gaps -log1p(-u)/rate, u = 53-bit uniform of the
+    reference's derive_seed(seed, i, 0) (rng.hpp:25-34, through the oracle's copy)."""
+    import math
+    from oracle import oracle as O
+    t, out = 0.0, []
+    for i in range(n):
+        u = (O.lib().cdxo_derive_seed(seed, i, 0) >> 11) * 2.0 ** -53
+        t += -math.log1p(-u) / rate
+        out.append(t)
+    return out
+
+
+@pytest.mark.gpu
+def test_sim_knob_programs_poisson_and_allocate():
+    """Knob-unit SC programs (signals from the reference API on the B200) under Poisson
+    arrivals, allocate at detect / recheck points.  SPEC properties: safety
+    (knob <= cap), determinism, throughput ceiling, early-exit savings at equal accuracy on a
+    zero-residual-noise workload, threshold monotonicity, the
+    token-to-accuracy curve."""
+    got = _run()
+    want = _poisson_restated(6, 250.0, 99)
+    assert [float(x) for x in got["poisson"].split()] == pytest.approx(want, rel=1e-8, abs=0)
+
+    def parse(k):
+        v = got[k].split()
+        return dict(tokens=float(v[0]), acc=float(v[1]), units=int(v[2]), dec=int(v[3]), cert=int(v[4]),
+                    maxknob=int(v[5]), lat=float(v[6]), makespan=float(v[7]), tput=float(v[8]), trunc=int(v[9]))
+    even, static, kstep, k07 = (parse(k) for k in ("knob even", "knob static", "knob kstep", "knob kstep tau0.7"))
+    NP, CAP, S = 48, 16, 8
+    for r in (even, static, kstep, k07):
+        assert r["maxknob"] <= CAP and r["trunc"] == 0                  # safety
+        assert r["tput"] <= 16 * 64000.0 * (1 + 1e-12)                   # throughput ceiling
+        assert r["tokens"] == r["units"] * S * 64                        # every unit issues S requests
+    assert got["knob kstep repeat"] == got["knob kstep"]                 # determinism
+    assert even["units"] == NP * CAP and even["cert"] == 0 and even["dec"] == NP
+    # tau = 1: stop only on a unanimous row; residual noise 0 -> every converged row is unanimous "S"
+    assert kstep["acc"] == even["acc"] and static["acc"] == even["acc"]
+    assert kstep["tokens"] < static["tokens"] < even["tokens"]
+    assert kstep["cert"] > 0 and kstep["lat"] < even["lat"]
+    assert k07["tokens"] <= kstep["tokens"]
+    assert got["knob monotone"] == "0"
+    pts = [tuple(map(float, p.split(":"))) for p in got["curve"].split()]
+    assert len(pts) == 2 and pts[0][0] < pts[1][0]
+    assert pts[1][0] == 2 * pts[0][0]                                     # even allocation: cap 16 = 2 x cap 8
