@@ -53,6 +53,9 @@ CONFIGS = {
                    "program's current knob + budget scan, then the gang priority order of the live programs (K6)"),
     "G": dict(kind="gang", N=1 << 22, limit=0.5, prior=128.0,
               desc="gang-scheduling priority order alone (escalation + SJF + tie-break), 4M programs"),
+    "K": dict(kind="intern", n=1 << 27, width=12, S=32,
+              desc="answer canonicalisation + interning (trim, hash, byte-verify, dense first-seen ids) + "
+                   "hesitation flags over 2^27 whitespace-padded answers (1.6 GB arena, K1)"),
     "J": dict(kind="jsonl", lines=1 << 20, programs=1 << 14, flush_l2=True,
               desc="probe-trace JSONL ingestion (read_trace_jsonl), 1M records over 16K programs"),
 }
@@ -60,7 +63,8 @@ TH_MCTS = [(0, 0.99, 0), (1, 0.4, 0)]   # PAPER.md:963 MCTS/GSM8K thresholds
 TH_REBASE = [(0, 0.85, 0), (1, 0.99, 0)]  # PAPER.md:966 Rebase/GSM8K thresholds
 
 
-TRAFFIC_KEY = {"sc": "sc", "cot": "cot", "reward": "reward", "gang": "gang", "jsonl": "jsonl", "mixed": "mixed"}
+TRAFFIC_KEY = {"sc": "sc", "cot": "cot", "reward": "reward", "gang": "gang", "jsonl": "jsonl", "mixed": "mixed",
+               "intern": "intern"}
 
 
 def load_traffic(kind):
@@ -384,8 +388,26 @@ def cpu_mixed(cfg, nth, n, seed):
                         "(reference certaindex functions + SPEC allocate/sort ports)")
 
 
-CPU = {"sc": cpu_sc, "cot": cpu_cot, "reward": cpu_reward, "gang": cpu_gang, "jsonl": cpu_jsonl, "mixed": cpu_mixed}
-CPU_SAMPLE = {"A": 1024, "B": 1 << 16, "C": 1 << 18, "D": 1 << 14, "E": 1 << 15, "G": 1 << 20, "J": 1 << 17}
+def cpu_intern(cfg, nth, n, seed):
+    """The reference's K1 work (oracle/_ref): rows of S answers materialised as std::string,
+    metrics::cluster_exact (trim + string_view map) + probe::flag_hesitation per answer."""
+    import numpy as np
+
+    from oracle import oracle as O
+    from paper_2412_20993_b200 import synth
+    ids = O.gen_sc(O.gen_params(seed=seed, conv_hi=64), max(1, n // (64 * cfg["S"])), 64, cfg["S"]).reshape(-1)[:n]
+    arena, off = synth.answer_arena_np(ids, cfg["width"])
+    O.ref_intern_batch(arena, off[: 1 + max(1, n // 64)], cfg["S"], nthreads=nth)  # warm
+    t0 = time.perf_counter()
+    O.ref_intern_batch(arena, off, cfg["S"], nthreads=nth, want=False)
+    dt = time.perf_counter() - t0
+    return n / dt, dt, f"{n} answers in rows of {cfg['S']}, {dt:.2f} s"
+
+
+CPU = {"sc": cpu_sc, "cot": cpu_cot, "reward": cpu_reward, "gang": cpu_gang, "jsonl": cpu_jsonl, "mixed": cpu_mixed,
+       "intern": cpu_intern}
+CPU_SAMPLE = {"A": 1024, "B": 1 << 16, "C": 1 << 18, "D": 1 << 14, "E": 1 << 15, "G": 1 << 20, "J": 1 << 17,
+              "K": 1 << 22}
 
 
 def cpu_baseline(name, cfg, sample=None, target_s=1.0, max_reps=64):
@@ -777,6 +799,51 @@ def bench_jsonl(args, cfg, rank, world, cx, with_e2e=True):
                 extra={"text_bytes": len(text)}, e2e=e2e)
 
 
+def bench_intern(args, cfg, rank, world, cx, with_e2e=True):
+    """Config K: K1 over a device-resident answer arena (trim, hash, insert, byte-verify,
+    dense first-seen ids, hesitation flags).  Answers shard by rank (weak scaling)."""
+    import torch
+    from paper_2412_20993_b200 import GenParams, synth
+    n, S, wd = cfg["n"], cfg["S"], cfg["width"]
+    R = n // (64 * S)
+    ids = cx.gen_sc(GenParams(seed=20993 + 8, conv_hi=64), R, 64, S, r0=rank * R).view(-1)
+    arena, off = synth.answer_arena_torch(ids, wd)
+    del ids
+    torch.cuda.synchronize()
+    out = {}
+
+    def step(seg):
+        e = seg_events(seg, "canon_intern")
+        out["r"] = cx.canon_intern(arena, off)
+        if e is not None:
+            e.record(torch.cuda.current_stream())
+
+    l0 = cx.launches
+    ms, per, clocks = timed(args, world, step, ["canon_intern"])
+    launches = in_timed(cx, l0, args)
+    b = n * wd + (n + 1) * 8 + n * 4 + n
+    e2e = None
+    if with_e2e and not args.no_e2e:
+        h_arena = torch.empty(arena.shape, dtype=torch.uint8, pin_memory=True)
+        h_off = torch.empty(off.shape, dtype=torch.int64, pin_memory=True)
+        h_arena.copy_(arena)
+        h_off.copy_(off)
+        s_arena, s_off = torch.empty_like(arena), torch.empty_like(off)
+        keep = {}
+
+        def one():
+            s_arena.copy_(h_arena, non_blocking=True)
+            s_off.copy_(h_off, non_blocking=True)
+            r = cx.canon_intern(s_arena, s_off)
+            keep["ids"], keep["hes"] = r[0].cpu(), r[1].cpu()
+        e2e = e2e_host(args, world, one, n * world, (arena.numel() + off.numel() * 8), n * 5,
+                       "Context.canon_intern (C-ABI) from pinned host arena + offsets, ids and flags read back, "
+                       "wall clock")
+    return dict(value=n * world / (ms / 1e3), ms=ms, launches=launches, clocks=clocks,
+                kernel="canon_intern (all passes)", kernel_ms=per["canon_intern"], kernel_bytes=b, step_bytes=b,
+                extra={"unique_answers": int(out["r"][3]), "arena_bytes": n * wd}, e2e=e2e)
+
+
 def bench_mixed(args, cfg, rank, world, cx, with_e2e=True):
     """Config E: one online scheduling round over the mixed trace.  Traces of each archetype
     group are generated on the device (rows of the rank's programs only); the timed step is
@@ -909,7 +976,8 @@ def e2e_mixed(args, cx, trace, arch_d, slot_d, knob_d, st_d, pols, gang, world, 
             "api": "Context.mixed_allocate + Context.gang_priority (C-ABI) from pinned host buffers, wall clock"}
 
 
-BENCH = {"mixed": bench_mixed, "sc": bench_sc, "cot": bench_cot, "reward": bench_reward, "gang": bench_gang, "jsonl": bench_jsonl}
+BENCH = {"mixed": bench_mixed, "sc": bench_sc, "cot": bench_cot, "reward": bench_reward, "gang": bench_gang,
+         "jsonl": bench_jsonl, "intern": bench_intern}
 
 
 def summarize(name, cfg, res, peak):
@@ -970,7 +1038,8 @@ def main():
         ach = res["kernel_bytes"] / (res["kernel_ms"] / 1e3) / 1e9
         cfg_out = {"workload": args.config, "desc": cfg["desc"],
                    **{k: v for k, v in cfg.items() if k not in ("kind", "desc", "conv_hi")},
-                   "parallelism": (f"program shards x{world}, NCCL allgather of sorted key runs + merge"
+                   "parallelism": (f"program shards x{world}, distributed sample sort (samples allgather, "
+                                   "keys alltoallv, merge, ids allgather)"
                                    if cfg["kind"] in ("gang", "mixed") else
                                    f"request shards x{world} (no data-path collective; 8 B/rank allgather "
                                    "of budget totals for global offsets)"),

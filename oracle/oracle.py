@@ -460,6 +460,22 @@ def ref_sc_batch(ids, groups, ths, nthreads=1, mode=0, want=True):
     return h, meets
 
 
+def ref_intern_batch(arena, offsets, S, markers=("wait", "hmm"), nthreads=1, want=True):
+    """The reference's cluster_exact over rows of S answers + flag_hesitation per answer."""
+    n = len(offsets) - 1
+    rows = (n + S - 1) // S
+    ncl = np.empty(max(rows, 1), np.uint32) if want else None
+    hes = np.empty(max(n, 1), np.uint8) if want else None
+    mk = (C.c_char_p * max(1, len(markers)))(*[m.encode() for m in markers])
+    f = ref().ref_intern_batch
+    f.argtypes = [P, P, C.c_uint64, C.c_uint32, P, C.c_uint32, P, P, C.c_int]
+    a = np.ascontiguousarray(arena, dtype=np.uint8)
+    o = np.ascontiguousarray(offsets, dtype=np.uint64)
+    if f(_p(a), _p(o), n, S, C.cast(mk, P), len(markers), _p(ncl), _p(hes), nthreads) < 0:
+        raise RefError(_ref_err())
+    return (ncl[:rows], hes[:n]) if want else (None, None)
+
+
 def ref_cot_batch(ids, hes, groups, interval_tokens=64, window=3, threshold=0.9, max_tokens=1 << 20, nthreads=1,
                   want_ck=True):
     R, P_ = ids.shape

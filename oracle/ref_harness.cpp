@@ -342,6 +342,39 @@ int ref_sc_batch(const uint32_t* ids, uint64_t R, uint32_t P, uint32_t S,
     return fail ? -1 : 0;
 }
 
+// K1's reference work over a string arena (answers arena[off[i] .. off[i+1])), rows of S
+// consecutive answers: each row is materialised as the std::string answers the reference
+// consumes, clustered by metrics::cluster_exact (trim + unordered_map<string_view> key,
+// metrics.cpp:12-37) and each answer flagged by probe::flag_hesitation (probe.cpp:36-44).
+// ncl[row] = cluster count, hes[i] = flag (both nullable).
+int ref_intern_batch(const char* arena, const uint64_t* off, uint64_t n, uint32_t S, const char* const* markers,
+                     uint32_t n_markers, uint32_t* ncl, uint8_t* hes, int nthreads) {
+    std::vector<std::string> mk;
+    for (uint32_t k = 0; k < n_markers; ++k) mk.emplace_back(markers[k]);
+    const uint64_t rows = (n + S - 1) / S;
+    std::atomic<int> fail{0};
+    parallel_for(rows, nthreads, [&](uint64_t b, uint64_t e) {
+        std::vector<std::string> row;
+        try {
+            for (uint64_t r = b; r < e; ++r) {
+                const uint64_t i0 = r * S, i1 = std::min<uint64_t>(n, i0 + S);
+                row.clear();
+                for (uint64_t i = i0; i < i1; ++i) row.emplace_back(arena + off[i], off[i + 1] - off[i]);
+                const auto c = m::cluster_exact(row);
+                if (ncl) ncl[r] = static_cast<uint32_t>(c.group_count());
+                for (uint64_t i = i0; i < i1; ++i) {
+                    const bool h = pr::flag_hesitation(row[i - i0], mk);
+                    if (hes) hes[i] = h ? 1 : 0;
+                }
+            }
+        } catch (const std::exception& ex) {
+            g_err = ex.what();
+            fail = 1;
+        }
+    });
+    return fail ? -1 : 0;
+}
+
 // CoT: ids[R][P] (vocab), hes bits [R][ceil(P/64)], implicit offsets (p+1)*interval.
 // Every prefix: should_exit(trace, cfg) (probe.cpp:77-85); on the first exit the trace is
 // terminated (runtime.cpp:405-411) and final_answer taken.  ck = consistency(...).value_or(0)

@@ -71,6 +71,7 @@ struct cdx_ctx {
     void* sh_buf2 = nullptr;
     size_t sh_bytes2 = 0;
     uint64_t* sh_host = nullptr;  // pinned host staging (counts, bounds)
+    uint64_t it_cap = 0;          // K1 global table capacity of the last call (k_intern.cu)
 };
 
 namespace cdx {

@@ -54,6 +54,67 @@ def test_intern_spec_examples(ctx):
     assert hes.tolist() == [0, 0]
 
 
+def test_intern_synthetic_arena_scale(ctx):
+    """The bench config K arena (synth.answer_arena_*: vocabulary answers, hesitant forms,
+    whitespace pads) at 2^20 answers: device and host builders agree and K1 equals the oracle."""
+    import torch
+    from paper_2412_20993_b200 import synth
+    n = 1 << 20
+    ids = np.random.default_rng(7).integers(0, 5, n).astype(np.uint32)
+    arena, off = synth.answer_arena_np(ids)
+    ta, to = synth.answer_arena_torch(torch.from_numpy(ids.astype(np.int64)).cuda())
+    assert np.array_equal(ta.cpu().numpy(), arena)
+    got, hes, first, nu = ctx.canon_intern(ta, to)
+    ctx.sync()
+    strings = [bytes(arena[12 * i: 12 * i + 12]) for i in range(n)]
+    oid, ohes, onu = O.canon_intern(strings)
+    assert nu == onu == 10
+    assert np.array_equal(got.cpu().numpy().view(np.uint32), oid)
+    assert np.array_equal(hes.cpu().numpy(), ohes)
+
+
+@pytest.mark.parametrize("case", ["all_distinct", "long_answers", "unaligned", "long_markers", "tile_edges"])
+def test_intern_paths(ctx, case):
+    """All-distinct answers past the first table's capacity (the retry with room for every
+    answer), answers longer than a staged tile (read in place), an unaligned arena (offsets
+    staged by hand), markers longer than 8 bytes, and counts around the 1024-answer tile."""
+    import torch
+    rng = np.random.default_rng(11)
+    markers = ("wait", "hmm")
+    if case == "all_distinct":
+        strings = [f" u{i} " for i in range(700000)] + [" u5", "u7 "]
+    elif case == "long_answers":
+        strings = [("  x" * int(rng.integers(1, 3000))) + (" WAIT " if i % 3 == 0 else "") for i in range(700)]
+    elif case == "unaligned":
+        strings = [f"\t{k}\n" for k in rng.integers(0, 50, 20000)]
+    elif case == "long_markers":
+        strings = ["I think, wait a second, maybe 7", "WAIT A SECOND", "wait a secon", "x" * 40 + "wait a second"]
+        markers = ("wait a second", "")
+    else:
+        strings = [f"a{k}" for k in rng.integers(0, 3, 1024 * 3 + 1)]
+    arena, offs = _arena(strings)
+    if case == "unaligned":
+        pad = np.zeros(len(arena) + 3, np.uint8)
+        pad[3:] = arena
+        tbuf = torch.from_numpy(pad).cuda()
+        ta = tbuf[3:]
+        obuf = torch.zeros(len(offs) + 1, dtype=torch.int64).cuda()
+        obuf[1:] = torch.from_numpy(offs.view(np.int64))
+        to = obuf[1:]
+    else:
+        ta = torch.from_numpy(arena).cuda()
+        to = torch.from_numpy(offs.view(np.int64)).cuda()
+    ids, hes, first, nu = ctx.canon_intern(ta, to, markers)
+    ctx.sync()
+    oid, ohes, onu = O.canon_intern(strings, markers) if case == "long_markers" else O.canon_intern(strings)
+    assert nu == onu
+    assert np.array_equal(ids.cpu().numpy().view(np.uint32), oid)
+    assert np.array_equal(hes.cpu().numpy(), ohes)
+    f = first.cpu().numpy()
+    for d in range(min(nu, 100)):
+        assert oid[f[d]] == d and (oid[: f[d]] != d).all()
+
+
 def _gang_inputs(N, seed, frac_term=0.1, sorted_arrival=True):
     rng = np.random.default_rng(seed)
     gaps = rng.exponential(1e-3, N)
