@@ -336,6 +336,27 @@ def canon_intern(strings, markers=("wait", "hmm")):
     return ids[:len(bs)], hes[:len(bs)], nu.value
 
 
+def canon_intern_arena(arena, offs, markers=("wait", "hmm")):
+    """canon_intern over a byte arena u8[] + offsets u64[n+1] (no Python strings)."""
+    arena = np.ascontiguousarray(arena, np.uint8)
+    offs = np.ascontiguousarray(offs, np.uint64)
+    n = len(offs) - 1
+    mk = b"".join(m.encode() for m in markers)
+    moff = np.zeros(len(markers) + 1, np.uint32)
+    if markers:
+        np.cumsum([len(m.encode()) for m in markers], out=moff[1:])
+    ids = np.empty(max(n, 1), np.uint32)
+    hes = np.empty(max(n, 1), np.uint8)
+    nu = C.c_uint64(0)
+    ab = np.concatenate([arena, np.zeros(1, np.uint8)])
+    mb = C.create_string_buffer(mk, len(mk) + 1)
+    st = lib().cdxo_canon_intern(ab.ctypes.data_as(C.c_char_p), _p(offs), C.c_uint64(n), mb, _p(moff),
+                                 C.c_uint32(len(markers)), _p(ids), _p(hes), C.byref(nu))
+    if st:
+        raise ValueError("oracle intern failed")
+    return ids[:n], hes[:n], nu.value
+
+
 # ---------------------------------------------------------------- the reference itself
 class RefError(Exception):
     pass

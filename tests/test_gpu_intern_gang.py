@@ -115,6 +115,63 @@ def test_intern_paths(ctx, case):
         assert oid[f[d]] == d and (oid[: f[d]] != d).all()
 
 
+def _grow_arena(n, vocab, seed, lead_ws=True):
+    """Answers whose vocabulary grows along the arena (key k first appears near k * n / vocab),
+    with whitespace pads and hesitant forms: new keys keep arriving in every round of tiles."""
+    rng = np.random.default_rng(seed)
+    i = np.arange(n)
+    top = np.maximum(1, (i * vocab) // n + 1)
+    key = (rng.random(n) * top).astype(np.int64)
+    lpad = rng.integers(0, 3, n) if lead_ws else np.zeros(n, np.int64)
+    rpad = rng.integers(0, 3, n)
+    hes = rng.random(n) < 0.05
+    names = [b"k%d" % k for k in range(vocab)]
+    wsb = [bytes([c]) for c in b" \t\n\r\f\v"]
+    w = rng.integers(0, 6, (n, 4))
+    parts = [b"".join(wsb[w[a, q]] for q in range(lpad[a])) + (b"wait, " if hes[a] else b"") + names[key[a]] +
+             b"".join(wsb[w[a, 2 + q]] for q in range(rpad[a])) for a in range(n)]
+    lens = np.fromiter((len(x) for x in parts), np.int64, n)
+    offs = np.zeros(n + 1, np.uint64)
+    offs[1:] = np.cumsum(lens)
+    return np.frombuffer(b"".join(parts), np.uint8).copy(), offs
+
+
+@pytest.mark.parametrize("n,vocab", [(1 << 18, 3000), (1 << 21, 100), (1 << 21, 60000)])
+def test_intern_growing_vocabulary(ctx, n, vocab):
+    """Keys first seen in late rounds of tiles: dense ids come from the round counts (final
+    slices) or the flagged-slice remap; both must equal the oracle's first-seen order."""
+    import torch
+    arena, offs = _grow_arena(n, vocab, seed=n + vocab)
+    ta = torch.from_numpy(arena).cuda()
+    to = torch.from_numpy(offs.view(np.int64)).cuda()
+    ids, hes, first, nu = ctx.canon_intern(ta, to, ("wait", "hmm"))
+    ctx.sync()
+    oid, ohes, onu = O.canon_intern_arena(arena, offs, ("wait", "hmm"))
+    assert nu == onu
+    assert np.array_equal(ids.cpu().numpy().view(np.uint32), oid)
+    assert np.array_equal(hes.cpu().numpy(), ohes)
+    f = first.cpu().numpy()[:nu]
+    first_seen = np.full(nu, -1, np.int64)
+    _, idx = np.unique(oid, return_index=True)
+    first_seen[:] = idx
+    assert np.array_equal(f.astype(np.int64), first_seen)
+
+
+def test_intern_synthetic_arena_large(ctx):
+    """Config K's arena at 2^24 answers (16K tiles, ~110 rounds): every id and flag."""
+    import torch
+    from paper_2412_20993_b200 import GenParams, synth
+    n = 1 << 24
+    sid = ctx.gen_sc(GenParams(seed=20993 + 8, conv_hi=64), n // (64 * 32), 64, 32).view(-1)
+    ta, to = synth.answer_arena_torch(sid, 12)
+    got, hes, first, nu = ctx.canon_intern(ta, to)
+    ctx.sync()
+    oid, ohes, onu = O.canon_intern_arena(ta.cpu().numpy(), to.cpu().numpy().view(np.uint64))
+    assert nu == onu
+    assert np.array_equal(got.cpu().numpy().view(np.uint32), oid)
+    assert np.array_equal(hes.cpu().numpy(), ohes)
+
+
 def _gang_inputs(N, seed, frac_term=0.1, sorted_arrival=True):
     rng = np.random.default_rng(seed)
     gaps = rng.exponential(1e-3, N)
