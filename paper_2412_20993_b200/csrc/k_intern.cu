@@ -323,11 +323,13 @@ __device__ __forceinline__ uint32_t rc_set(uint32_t h) { return (h >> 23) * 4u; 
 __device__ __forceinline__ uint32_t rc_tag_of(uint32_t h) { return (h | 1u) & 0x7fffffffu; }
 static_assert(WS_RC == 2048, "rc_set takes the top 9 bits");
 
-// the first 12 bytes at sa as three words, masked to the answer's length: four aligned
-// 4-byte loads (conflict-free for odd word strides) and three funnel shifts
-__device__ __forceinline__ void load_words(const uint8_t* sa, const uint4& m, uint32_t& w0, uint32_t& w1, uint32_t& w2) {
-    const uint32_t* a4 = reinterpret_cast<const uint32_t*>(reinterpret_cast<uintptr_t>(sa) & ~static_cast<uintptr_t>(3));
-    const uint32_t sh = static_cast<uint32_t>(reinterpret_cast<uintptr_t>(sa) & 3u) * 8u;
+// the 12 bytes at base + rel as three words, masked to the answer's length: four aligned
+// 4-byte loads (conflict-free for odd word strides) and three funnel shifts.  base is a
+// 16-byte aligned shared-memory pointer (pointer arithmetic only, so the loads stay LDS).
+__device__ __forceinline__ void load_words(const uint8_t* base, uint32_t rel, const uint4& m, uint32_t& w0, uint32_t& w1,
+                                           uint32_t& w2) {
+    const uint32_t* a4 = reinterpret_cast<const uint32_t*>(base + (rel & ~3u));
+    const uint32_t sh = (rel & 3u) * 8u;
     const uint32_t x0 = a4[0], x1 = a4[1], x2 = a4[2], x3 = a4[3];
     w0 = __funnelshift_r(x0, x1, sh) & m.x;
     w1 = __funnelshift_r(x1, x2, sh) & m.y;
@@ -539,8 +541,7 @@ __device__ __noinline__ MissOut chunk_misses(const WsParams& p, const Markers& m
         const bool cacheable = abase != INPLACE && len <= WS_RAWMAX;
         uint32_t w0 = 0, w1 = 0, w2 = 0, rh = 0;
         if (cacheable) {
-            load_words(sbuf + WS_OFFB + (static_cast<uint32_t>(b0) - static_cast<uint32_t>(abase)), S.lenmask[len], w0, w1,
-                       w2);
+            load_words(sbuf + WS_OFFB, static_cast<uint32_t>(b0) - static_cast<uint32_t>(abase), S.lenmask[len], w0, w1, w2);
             rh = raw_hash(w0, w1, w2, static_cast<uint32_t>(len));
         }
         const uint8_t* src = abase != INPLACE ? sbuf + WS_OFFB + (static_cast<int64_t>(b0) - abase) : p.arena + b0;
@@ -792,7 +793,7 @@ __global__ void __launch_bounds__(32 * (WS_MAXW + 2), 1) intern_ws(const __grid_
 #pragma unroll
         for (uint32_t k = 0; k < 4; ++k) {
             const uint32_t rel = cach[k] ? static_cast<uint32_t>(b0[k]) - static_cast<uint32_t>(abase) : 0u;
-            load_words(sbuf + WS_OFFB + rel, S.lenmask[ln[k]], w0[k], w1[k], w2[k]);
+            load_words(sbuf + WS_OFFB, rel, S.lenmask[ln[k]], w0[k], w1[k], w2[k]);
             rh[k] = raw_hash(w0[k], w1[k], w2[k], ln[k]);
         }
         uint4 tg[4], ce[4];
