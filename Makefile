@@ -20,7 +20,7 @@ HHDRS   := $(wildcard $(PKG)/csrc/host/*.hpp) include/cdx_c.h $(wildcard include
 HOSTCXX := g++
 CXXFLAGS_HOST := -std=c++20 -O2 -fPIC -Wall -Wextra -Iinclude
 
-DROPIN  := tests/cpp/bin/dropin_ours tests/cpp/bin/scheduler_cases tests/cpp/bin/batch_pipeline tests/cpp/bin/sim_cases \
+DROPIN  := tests/cpp/bin/dropin_ours tests/cpp/bin/facade_latency_ours tests/cpp/bin/scheduler_cases tests/cpp/bin/batch_pipeline tests/cpp/bin/sim_cases \
            tests/cpp/bin/shard_world2
 
 all: lib oracle dropin
@@ -55,6 +55,8 @@ dropin: $(DROPIN)
 CPPTEST = @mkdir -p tests/cpp/bin && $(HOSTCXX) -std=c++20 -O2 -Wall -Iinclude -o $@ $< -L$(PKG)/lib -lcdxhost -lcdx \
           -Wl,-rpath,'$$ORIGIN/../../../$(PKG)/lib'
 tests/cpp/bin/dropin_ours: tests/cpp/dropin_cases.cpp $(HOSTLIB) $(HHDRS)
+	$(CPPTEST)
+tests/cpp/bin/facade_latency_ours: tests/cpp/facade_latency.cpp $(HOSTLIB) $(HHDRS)
 	$(CPPTEST)
 # multi-rank C-ABI test: W host threads, one context each, host-staged communicator callbacks
 tests/cpp/bin/shard_world2: tests/cpp/shard_world2.cpp $(LIB) include/cdx_c.h

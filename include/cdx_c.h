@@ -576,6 +576,38 @@ int cdx_reward_decide_host(cdx_ctx* ctx, const float* rewards_host, const uint32
                            int32_t* exit_knob_host, uint8_t* reason_host, int64_t* offsets_host,
                            float* R_host, int64_t* tokens_saved_host);
 
+/* ---- one-round-trip scalar entries (k_scalar.cu) -------------------------------------
+ * Host buffers in and out: ONE pinned host->device copy of every input, one launch, one
+ * device->host copy of the outputs, one synchronisation.  They back the reference's scalar
+ * C++ API (include/cdx/metrics.hpp, probe.hpp) for the per-program call sizes of
+ * runtime.cpp:264-313; the batched entries above are the throughput path.  Answers are a
+ * byte arena + offsets[n+1] (1..2048 answers, at most 1 MiB of text). */
+/* metrics::cluster_exact (metrics.cpp:21-37) + probe::flag_hesitation (probe.cpp:36-44):
+ * dense first-seen ids of the trimmed bytes, per cluster its first index and size; hes
+ * (nullable) = the marker test on the raw answers.  Any output but n_unique may be NULL. */
+int cdx_cluster_host(cdx_ctx* ctx, const char* bytes, const uint64_t* offsets, uint32_t n, const char* const* markers,
+                     uint32_t n_markers, uint32_t* ids, uint8_t* hes, uint32_t* first_index, uint32_t* sizes,
+                     uint32_t* n_unique);
+/* probe::consistency(records, k, w) (probe.cpp:64-75): *ready = 0 for nullopt */
+int cdx_consistency_host(cdx_ctx* ctx, const char* bytes, const uint64_t* offsets, uint32_t n, const uint8_t* hes,
+                         const int32_t* step_index, int32_t k, int32_t w, double* C, uint8_t* ready);
+/* probe::should_exit(trace, cfg) (probe.cpp:77-85): decision = cdx_exit_decision */
+int cdx_should_exit_host(cdx_ctx* ctx, const char* bytes, const uint64_t* offsets, uint32_t n, const uint8_t* hes,
+                         const int32_t* step_index, const int64_t* token_offset, const cdx_probe_cfg* cfg,
+                         uint8_t* decision);
+/* probe::final_answer(trace) (probe.cpp:87-102): record index + low-confidence flag;
+ * terminated_at = INT32_MIN for nullopt, termination_reason = TerminationReason ordinal */
+int cdx_final_answer_host(cdx_ctx* ctx, const uint8_t* hes, const int32_t* step_index, uint32_t n,
+                          int32_t terminated_at, uint8_t termination_reason, uint64_t* pos, uint8_t* low_conf);
+/* semantic_entropy / certaindex_entropy of one clustering (metrics.cpp:107-125), host outputs */
+int cdx_entropy_host(cdx_ctx* ctx, const int32_t* sizes, uint32_t m, int32_t total, double* H, double* Hcert);
+/* certaindex_reward (metrics.cpp:127-137): aggregation CDX_AGG_MEAN / CDX_AGG_MAX */
+int cdx_reward_host(cdx_ctx* ctx, const double* rewards, uint64_t n, uint8_t aggregation, double* out);
+/* combined_meets_thresholds (metrics.cpp:159-171): signals4 in SignalKind order, present
+ * bit k = signal k present, at most 8 thresholds */
+int cdx_meets_host(cdx_ctx* ctx, const double* signals4, uint8_t present, const cdx_threshold* th, uint32_t n_th,
+                   uint8_t* meets);
+
 #ifdef __cplusplus
 }
 #endif

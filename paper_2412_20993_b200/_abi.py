@@ -109,6 +109,13 @@ SIGNATURES = {
     "cdx_meets_thresholds_rows": (C.c_int, [P, P, P, U64, C.POINTER(Threshold), U32, P]),
     "cdx_id_histogram": (C.c_int, [P, P, U64, U32, P]),
     "cdx_entropy_one": (C.c_int, [P, P, U32, U32, P, P]),
+    "cdx_cluster_host": (C.c_int, [P, P, P, U32, P, U32, P, P, P, P, P]),
+    "cdx_consistency_host": (C.c_int, [P, P, P, U32, P, P, C.c_int32, C.c_int32, P, P]),
+    "cdx_should_exit_host": (C.c_int, [P, P, P, U32, P, P, P, P, P]),
+    "cdx_final_answer_host": (C.c_int, [P, P, P, U32, C.c_int32, C.c_uint8, P, P]),
+    "cdx_entropy_host": (C.c_int, [P, P, U32, C.c_int32, P, P]),
+    "cdx_reward_host": (C.c_int, [P, P, U64, C.c_uint8, P]),
+    "cdx_meets_host": (C.c_int, [P, P, C.c_uint8, P, U32, P]),
     "cdx_entropy_sizes_host": (C.c_int, [P, P, U32, C.c_int32, P, P]),
     "cdx_iteration_tokens_rows": (C.c_int, [P, P, P, U64, C.c_double, P]),
     "cdx_alloc": (C.c_int, [P, U64, C.POINTER(P)]),

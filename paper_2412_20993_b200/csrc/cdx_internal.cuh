@@ -72,6 +72,10 @@ struct cdx_ctx {
     size_t sh_bytes2 = 0;
     uint64_t* sh_host = nullptr;  // pinned host staging (counts, bounds)
     uint64_t it_cap = 0;          // K1 global table capacity of the last call (k_intern.cu)
+    // one-round-trip scalar calls (k_scalar.cu): pinned host / device staging pair
+    uint8_t* sc_h = nullptr;
+    uint8_t* sc_d = nullptr;
+    size_t sc_cap = 0;
 };
 
 namespace cdx {
@@ -96,6 +100,13 @@ enum DevErr : int {
     DEV_ABSENT_SIGNAL = 16,  // + SignalKind: "combined_meets_thresholds: signal '<name>' absent"
 };
 const char* dev_err_message(int code);
+// the device error word already copied to *ctx->h_err (stream synchronised): CDX_OK, or the
+// mapped status with the message (the word is cleared for the next call)
+int take_dev_err(cdx_ctx* ctx);
+// k_rows.cu helpers shared with the one-round-trip entries (k_scalar.cu)
+int check_probe_cfg_c(cdx_ctx* ctx, const cdx_probe_cfg* cfg);
+int entropy_terms_launch(cdx_ctx* ctx, const double* terms, uint32_t m, double log_n, bool n_is_one, double* H,
+                         double* Hc);
 // cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda needed)
 bool encode_tmap_2d(CUtensorMap* map, const void* base, uint64_t inner, uint64_t outer,
                     uint64_t row_stride_bytes, uint32_t box_inner, uint32_t box_outer,

@@ -13,6 +13,18 @@ int set_error(cdx_ctx* ctx, int code, const std::string& msg) {
     return code;
 }
 
+int take_dev_err(cdx_ctx* ctx) {
+    const int code = *ctx->h_err;
+    if (code == 0) return CDX_OK;
+    cudaMemsetAsync(ctx->d_err, 0, sizeof(int), ctx->stream);
+    const int st = (code == DEV_REWARD_RANGE || code == DEV_BAD_CLUSTERING || code == DEV_EMPTY_REWARDS ||
+                    code == DEV_EMPTY_CLUSTER || code == DEV_MIXED_PROGRAM ||
+                    (code >= DEV_ABSENT_SIGNAL && code < DEV_ABSENT_SIGNAL + 4))
+                       ? CDX_EINVAL
+                       : CDX_ERUNTIME;
+    return set_error(ctx, st, dev_err_message(code));
+}
+
 int cuda_fail(cdx_ctx* ctx, cudaError_t e, const char* what) {
     return set_error(ctx, CDX_ECUDA, std::string(what) + ": " + cudaGetErrorString(e));
 }
@@ -204,6 +216,8 @@ int cdx_ctx_destroy(cdx_ctx* ctx) {
     if (ctx->sh_host) cudaFreeHost(ctx->sh_host);
     if (ctx->d_err) cudaFree(ctx->d_err);
     if (ctx->h_err) cudaFreeHost(ctx->h_err);
+    if (ctx->sc_d) cudaFree(ctx->sc_d);
+    if (ctx->sc_h) cudaFreeHost(ctx->sc_h);
     if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
     if (ctx->copy_stream) cudaStreamDestroy(ctx->copy_stream);
     delete ctx;
@@ -237,18 +251,7 @@ int cdx_sync(cdx_ctx* ctx) {
     if (e != cudaSuccess) return cdx::cuda_fail(ctx, e, "cdx_sync");
     e = cudaMemcpy(ctx->h_err, ctx->d_err, sizeof(int), cudaMemcpyDeviceToHost);
     if (e != cudaSuccess) return cdx::cuda_fail(ctx, e, "cdx_sync");
-    const int code = *ctx->h_err;
-    if (code != 0) {
-        cudaMemset(ctx->d_err, 0, sizeof(int));
-        const int st = (code == cdx::DEV_REWARD_RANGE || code == cdx::DEV_BAD_CLUSTERING ||
-                        code == cdx::DEV_EMPTY_REWARDS || code == cdx::DEV_EMPTY_CLUSTER ||
-                        code == cdx::DEV_MIXED_PROGRAM ||
-                        (code >= cdx::DEV_ABSENT_SIGNAL && code < cdx::DEV_ABSENT_SIGNAL + 4))
-                           ? CDX_EINVAL
-                           : CDX_ERUNTIME;
-        return cdx::set_error(ctx, st, cdx::dev_err_message(code));
-    }
-    return CDX_OK;
+    return cdx::take_dev_err(ctx);
 }
 
 }  // extern "C"

@@ -31,4 +31,25 @@ Interned intern(batch::Context& cx, std::span<const std::string_view> strs, std:
 
 cdx_threshold to_c(const metrics::SignalThreshold& t);
 
+// Answers as one byte arena + offsets[n+1] for the one-round-trip entries (cdx_*_host);
+// fits = within their limits (1..2048 answers, at most 1 MiB), else the batched kernels.
+struct HostArena {
+    std::string bytes;
+    std::vector<uint64_t> off;
+    bool fits = false;
+};
+template <class It, class Get>
+HostArena host_arena(It begin, It end, Get get) {
+    HostArena a;
+    a.off.push_back(0);
+    for (It it = begin; it != end; ++it) {
+        const std::string_view s = get(*it);
+        a.bytes.append(s.data(), s.size());
+        a.off.push_back(a.bytes.size());
+    }
+    const size_t n = a.off.size() - 1;
+    a.fits = n >= 1 && n <= 2048 && a.bytes.size() <= (1u << 20);
+    return a;
+}
+
 }  // namespace cdx::detail

@@ -32,6 +32,20 @@ std::string_view trim(std::string_view s) {
 Clustering cluster_exact(std::span<const std::string> answers) {
     if (answers.empty()) throw std::invalid_argument("cluster_exact: empty answer set");
     auto& cx = detail::scalar_ctx();
+    const auto ar = detail::host_arena(answers.begin(), answers.end(), [](const std::string& s) { return std::string_view(s); });
+    if (ar.fits) {  // one round trip (k_scalar.cu)
+        const uint32_t n = static_cast<uint32_t>(answers.size());
+        std::vector<uint32_t> first(n), sizes(n);
+        uint32_t nu = 0;
+        cx.check(cdx_cluster_host(cx.raw(), ar.bytes.data(), ar.off.data(), n, nullptr, 0, nullptr, nullptr, first.data(),
+                                  sizes.data(), &nu));
+        Clustering out;
+        out.total = static_cast<int>(n);
+        out.clusters.reserve(nu);
+        for (uint32_t c = 0; c < nu; ++c)
+            out.clusters.push_back({std::string(trim(answers[first[c]])), static_cast<int>(sizes[c])});
+        return out;
+    }
     std::vector<std::string_view> views(answers.begin(), answers.end());
     auto in = detail::intern(cx, views, {}, false, true);
     batch::DeviceArray<uint32_t> counts(cx, in.n_unique);
@@ -54,11 +68,10 @@ std::pair<double, double> entropy_pair(const Clustering& c) {
     sizes.reserve(c.clusters.size());
     for (const auto& cl : c.clusters) sizes.push_back(static_cast<int32_t>(cl.size));
     auto& cx = detail::scalar_ctx();
-    batch::DeviceArray<double> out(cx, 2);
-    cx.check(cdx_entropy_sizes_host(cx.raw(), sizes.data(), static_cast<uint32_t>(sizes.size()),
-                                    static_cast<int32_t>(c.total), out.data(), out.data() + 1));
-    const auto v = out.download();
-    return {v[0], v[1]};
+    double h = 0.0, hc = 0.0;
+    cx.check(cdx_entropy_host(cx.raw(), sizes.data(), static_cast<uint32_t>(sizes.size()), static_cast<int32_t>(c.total),
+                              &h, &hc));
+    return {h, hc};
 }
 
 }  // namespace
@@ -73,14 +86,10 @@ double certaindex_entropy(const Clustering& c) {
 double certaindex_reward(const RewardSet& r) {
     if (r.rewards.empty()) throw std::invalid_argument("certaindex_reward: empty reward set");
     auto& cx = detail::scalar_ctx();
-    const uint64_t off[2] = {0, r.rewards.size()};
     const uint8_t agg = r.aggregation == RewardAggregation::Max ? CDX_AGG_MAX : CDX_AGG_MEAN;
-    batch::DeviceArray<double> d_v(cx, std::span<const double>(r.rewards));
-    batch::DeviceArray<uint64_t> d_off(cx, std::span<const uint64_t>(off, 2));
-    batch::DeviceArray<uint8_t> d_agg(cx, std::span<const uint8_t>(&agg, 1));
-    batch::DeviceArray<double> out(cx, 1);
-    cx.check(cdx_reward_sets(cx.raw(), d_v.data(), d_off.data(), d_agg.data(), 1, out.data()));
-    return out.download()[0];
+    double out = 0.0;
+    cx.check(cdx_reward_host(cx.raw(), r.rewards.data(), r.rewards.size(), agg, &out));
+    return out;
 }
 
 const char* signal_name(SignalKind kind) {
@@ -114,17 +123,14 @@ bool combined_meets_thresholds(const SignalVector& s, std::span<const SignalThre
             present |= static_cast<uint8_t>(1u << k);
         }
     }
-    batch::DeviceArray<double> d_sig(cx, std::span<const double>(sig, 4));
-    batch::DeviceArray<uint8_t> d_present(cx, std::span<const uint8_t>(&present, 1));
-    batch::DeviceArray<uint8_t> d_out(cx, 1);
     // the device evaluates up to 8 thresholds per call, in order; longer lists continue
     // only while every threshold so far has held (the reference's early return)
     for (size_t i = 0; i < thresholds.size(); i += 8) {
         std::vector<cdx_threshold> th;
         for (size_t j = i; j < std::min(thresholds.size(), i + 8); ++j) th.push_back(detail::to_c(thresholds[j]));
-        cx.check(cdx_meets_thresholds_rows(cx.raw(), d_sig.data(), d_present.data(), 1, th.data(),
-                                           static_cast<uint32_t>(th.size()), d_out.data()));
-        if (!d_out.download()[0]) return false;
+        uint8_t ok = 0;
+        cx.check(cdx_meets_host(cx.raw(), sig, present, th.data(), static_cast<uint32_t>(th.size()), &ok));
+        if (!ok) return false;
     }
     return true;
 }

@@ -37,6 +37,16 @@ const char* termination_reason_name(TerminationReason r) {
 
 bool flag_hesitation(std::string_view answer, std::span<const std::string> markers) {
     auto& cx = detail::scalar_ctx();
+    if (answer.size() <= (1u << 20) && markers.size() <= 16) {  // one round trip (k_scalar.cu)
+        std::vector<const char*> mk;
+        for (const auto& m : markers) mk.push_back(m.c_str());
+        const uint64_t off[2] = {0, answer.size()};
+        uint8_t h = 0;
+        uint32_t nu = 0;
+        cx.check(cdx_cluster_host(cx.raw(), answer.data(), off, 1, mk.data(), static_cast<uint32_t>(mk.size()), nullptr, &h,
+                                  nullptr, nullptr, &nu));
+        return h != 0;
+    }
     const std::string_view one[1] = {answer};
     auto in = detail::intern(cx, one, markers, true, false);
     return in.hes.download()[0] != 0;
@@ -82,6 +92,21 @@ std::optional<double> consistency(std::span<const AnswerRecord> records, int k, 
     if (w < 1) throw std::invalid_argument("consistency: window must be >= 1");
     if (records.empty()) return std::nullopt;  // no usable record can fill a window of w >= 1
     auto& cx = detail::scalar_ctx();
+    const auto ar = detail::host_arena(records.begin(), records.end(), [](const AnswerRecord& r) { return std::string_view(r.answer); });
+    if (ar.fits) {  // one round trip (k_scalar.cu)
+        std::vector<uint8_t> hes;
+        std::vector<int32_t> step;
+        for (const auto& r : records) {
+            hes.push_back(r.hesitant ? 1 : 0);
+            step.push_back(r.step_index);
+        }
+        double c = 0.0;
+        uint8_t ready = 0;
+        cx.check(cdx_consistency_host(cx.raw(), ar.bytes.data(), ar.off.data(), static_cast<uint32_t>(records.size()),
+                                      hes.data(), step.data(), k, w, &c, &ready));
+        if (!ready) return std::nullopt;
+        return c;
+    }
     auto t = upload(cx, records, true, false);
     batch::DeviceArray<int32_t> d_k(cx, std::span<const int32_t>(&k, 1));
     batch::DeviceArray<double> C(cx, 1);
@@ -97,16 +122,33 @@ ExitDecision should_exit(const ProbeTrace& trace, const ProbeConfig& cfg) {
     cfg.validate();
     if (trace.records.empty()) return ExitDecision::Continue;
     auto& cx = detail::scalar_ctx();
-    auto t = upload(cx, trace.records, true, true);
     cdx_probe_cfg c{};
     c.interval_tokens = cfg.interval_tokens;
     c.window = cfg.window;
     c.threshold = cfg.threshold;
     c.max_tokens = cfg.max_tokens;
-    batch::DeviceArray<uint8_t> d(cx, 1);
-    cx.check(cdx_probe_should_exit(cx.raw(), t.in.ids.data(), t.hes.data(), t.step.data(), t.tok.data(),
-                                   t.row_off.data(), 1, &c, d.data()));
-    switch (d.download()[0]) {
+    uint8_t dec = 0;
+    const auto& recs = trace.records;
+    const auto ar = detail::host_arena(recs.begin(), recs.end(), [](const AnswerRecord& r) { return std::string_view(r.answer); });
+    if (ar.fits) {  // one round trip (k_scalar.cu)
+        std::vector<uint8_t> hes;
+        std::vector<int32_t> step;
+        std::vector<int64_t> tok;
+        for (const auto& r : recs) {
+            hes.push_back(r.hesitant ? 1 : 0);
+            step.push_back(r.step_index);
+            tok.push_back(r.token_offset);
+        }
+        cx.check(cdx_should_exit_host(cx.raw(), ar.bytes.data(), ar.off.data(), static_cast<uint32_t>(recs.size()),
+                                      hes.data(), step.data(), tok.data(), &c, &dec));
+    } else {
+        auto t = upload(cx, trace.records, true, true);
+        batch::DeviceArray<uint8_t> d(cx, 1);
+        cx.check(cdx_probe_should_exit(cx.raw(), t.in.ids.data(), t.hes.data(), t.step.data(), t.tok.data(),
+                                       t.row_off.data(), 1, &c, d.data()));
+        dec = d.download()[0];
+    }
+    switch (dec) {
         case CDX_EXIT_CERTAIN: return ExitDecision::ExitCertain;
         case CDX_EXIT_BUDGET: return ExitDecision::ExitBudget;
         default: return ExitDecision::Continue;
@@ -116,9 +158,22 @@ ExitDecision should_exit(const ProbeTrace& trace, const ProbeConfig& cfg) {
 FinalAnswer final_answer(const ProbeTrace& trace) {
     if (trace.records.empty()) throw std::invalid_argument("final_answer: empty trace");
     auto& cx = detail::scalar_ctx();
-    auto t = upload(cx, trace.records, false, false);
     const int32_t term = trace.terminated_at ? *trace.terminated_at : INT_MIN;
     const uint8_t why = static_cast<uint8_t>(trace.termination_reason);
+    if (trace.records.size() <= 0xffffffffull) {  // one round trip (k_scalar.cu)
+        std::vector<uint8_t> hes;
+        std::vector<int32_t> step;
+        for (const auto& r : trace.records) {
+            hes.push_back(r.hesitant ? 1 : 0);
+            step.push_back(r.step_index);
+        }
+        uint64_t p = 0;
+        uint8_t low = 0;
+        cx.check(cdx_final_answer_host(cx.raw(), hes.data(), step.data(), static_cast<uint32_t>(trace.records.size()), term,
+                                       why, &p, &low));
+        return {std::string(metrics::trim(trace.records[p].answer)), low != 0};
+    }
+    auto t = upload(cx, trace.records, false, false);
     batch::DeviceArray<int32_t> d_term(cx, std::span<const int32_t>(&term, 1));
     batch::DeviceArray<uint8_t> d_why(cx, std::span<const uint8_t>(&why, 1));
     batch::DeviceArray<uint64_t> pos(cx, 1);

@@ -255,6 +255,16 @@ int check_probe_cfg(cdx_ctx* ctx, const cdx_probe_cfg* cfg) {
 }
 
 }  // namespace
+
+int check_probe_cfg_c(cdx_ctx* ctx, const cdx_probe_cfg* cfg) { return check_probe_cfg(ctx, cfg); }
+
+int entropy_terms_launch(cdx_ctx* ctx, const double* terms, uint32_t m, double log_n, bool n_is_one, double* H,
+                         double* Hc) {
+    entropy_terms_kernel<<<1, 32, 0, ctx->stream>>>(terms, m, log_n, n_is_one ? 1 : 0, H, Hc);
+    CDX_CHECK_LAUNCH(ctx, "entropy_terms");
+    return CDX_OK;
+}
+
 }  // namespace cdx
 
 extern "C" {

@@ -396,11 +396,42 @@ void jsonl_cases() {
 
 }  // namespace
 
+// Sizes on both sides of the one-round-trip limit of this repo's scalar entries (2048
+// answers / records): the results must not depend on which path took the call.
+void size_edge_cases() {
+    for (int n : {1, 2047, 2048, 2049, 5000}) {
+        std::vector<std::string> a;
+        for (int i = 0; i < n; ++i) a.push_back(random_answer() + (i % 97 == 5 ? std::to_string(i % 13) : ""));
+        run("size cluster_exact " + std::to_string(n), [&] {
+            const auto c = metrics::cluster_exact(a);
+            return show(c) + " " + hex(metrics::certaindex_entropy(c));
+        });
+        auto recs = random_records(n, true);
+        run("size consistency " + std::to_string(n), [&] {
+            const auto v = probe::consistency(recs, recs.back().step_index - 1, 3);
+            return v ? hex(*v) : std::string("nullopt");
+        });
+        probe::ProbeTrace t;
+        t.records = recs;
+        probe::ProbeConfig cfg;
+        cfg.max_tokens = 1000000;
+        run("size should_exit " + std::to_string(n), [&] { return std::to_string(static_cast<int>(probe::should_exit(t, cfg))); });
+        run("size final_answer " + std::to_string(n), [&] {
+            const auto f = probe::final_answer(t);
+            return esc(f.answer) + (f.low_confidence ? " low" : "");
+        });
+    }
+    std::string big(1 << 21, 'x');  // one answer above the byte limit
+    run("size flag_hesitation big", [&] { return std::to_string(probe::flag_hesitation(big + " WAIT", std::vector<std::string>{"wait"})); });
+    run("size cluster_exact big", [&] { return show(metrics::cluster_exact(std::vector<std::string>{big, " " + big})).substr(0, 40); });
+}
+
 int main(int argc, char** argv) {
     const int count = argc > 1 ? std::atoi(argv[1]) : 400;
     spec_examples();
     random_cases(count);
     nonfinite_cases();
     jsonl_cases();
+    size_edge_cases();
     return 0;
 }

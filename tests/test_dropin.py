@@ -105,3 +105,20 @@ def test_reference_runtime_fails_loudly_without_device():
         pytest.skip("a CUDA device is present")
     lines = _run_plain(RT_OURS)
     assert any("no usable sm_100 device" in l for l in lines)
+
+
+LAT_REF = os.path.join(ROOT, "oracle", "_ref", "facade_latency_ref")
+LAT_OURS = os.path.join(ROOT, "tests", "cpp", "bin", "facade_latency_ours")
+
+
+@pytest.mark.gpu
+def test_scalar_calls_one_round_trip_match_reference():
+    """tests/cpp/facade_latency.cpp against both builds: the same checksums per call (the
+    one-round-trip entries of k_scalar.cu behind the C++ API), and every call of ours well
+    under the multi-launch cost it replaced (profiles/r3_facade_latency.txt: 34-214 us)."""
+    ref = [ln.split() for ln in _run(LAT_REF, 20)]
+    ours = [ln.split() for ln in _run(LAT_OURS, 20)]
+    assert [r[0] for r in ref] == [o[0] for o in ours]
+    assert [r[2] for r in ref] == [o[2] for o in ours], "results differ from the reference"
+    slow = [(o[0], float(o[1])) for o in ours if o[0] != "sc_update[32]" and float(o[1]) > 80.0]
+    assert not slow, f"scalar calls slower than one round trip should be: {slow}"
