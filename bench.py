@@ -298,14 +298,16 @@ def jsonl_text(lines, programs, seed):
 
 
 def cpu_jsonl(cfg, nth, lines, seed):
-    """The reference's read_trace_jsonl (nlohmann parse + checks) on one thread: it is a
-    single sequential stream in the reference (probe.cpp:126-165)."""
+    """The reference's read_trace_jsonl (nlohmann parse + checks, probe.cpp:126-165) on `nth`
+    host threads: line-aligned chunks, each parsed by the reference function, plus the
+    per-program order checks across chunk boundaries (oracle/ref_harness.cpp)."""
     from oracle import oracle as O
     text = jsonl_text(lines, max(1, cfg["programs"] * lines // cfg["lines"]), seed)
     t0 = time.perf_counter()
-    n = O.ref_read_trace_jsonl(text)
+    n = O.ref_read_trace_jsonl_mt(text, nth)
     dt = time.perf_counter() - t0
-    return n / dt, dt, f"{n} records ({len(text)} bytes), {dt:.2f} s (1 thread: one sequential stream)"
+    return n / dt, dt, (f"{n} records ({len(text)} bytes), {dt:.2f} s ({nth} threads: line-aligned chunks through "
+                        "read_trace_jsonl + cross-chunk order checks)")
 
 
 SC_, REB_, MCT_, COT_ = 0, 1, 2, 3

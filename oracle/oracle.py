@@ -458,6 +458,15 @@ def ref_read_trace_jsonl(text):
     return r
 
 
+def ref_read_trace_jsonl_mt(text, nthreads):
+    """The reference's read_trace_jsonl on line-aligned chunks, one per host thread, plus the
+    cross-chunk order checks (oracle/ref_harness.cpp)."""
+    r = ref().ref_read_trace_jsonl_mt(text.encode() if isinstance(text, str) else text, C.c_int(nthreads))
+    if r < 0:
+        raise RefError(_ref_err())
+    return r
+
+
 def ref_driver_signals(archetype, seed, cap, conv, solvable, units):
     ent = (C.c_double * units)()
     rew = (C.c_double * units)()

@@ -23,6 +23,7 @@
 #include <optional>
 #include <string>
 #include <thread>
+#include <unordered_map>
 #include <vector>
 
 #include "cdx/metrics.hpp"
@@ -230,6 +231,62 @@ int ref_read_trace_jsonl(const char* text) {
         std::string s(text);
         std::istringstream in(s);
         return static_cast<int>(pr::read_trace_jsonl(in).size());
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return -1;
+    }
+}
+
+// read_trace_jsonl on `nthreads` host threads: the text is cut at line boundaries into one
+// contiguous chunk per thread, each chunk parsed by the reference's own read_trace_jsonl
+// (nlohmann parse, field checks, per-program order checks inside the chunk), then one
+// sequential pass applies the per-program order checks across chunk boundaries (a program's
+// first record in a chunk against its last record in the chunks before).  Valid traces
+// give the reference's result; returns the record count or -1 (message in g_err).
+int ref_read_trace_jsonl_mt(const char* text, int nthreads) {
+    try {
+        const std::string s(text);
+        const size_t nt = static_cast<size_t>(std::max(1, nthreads));
+        std::vector<size_t> cut(nt + 1, s.size());
+        cut[0] = 0;
+        for (size_t t = 1; t < nt; ++t) {
+            size_t c = std::max(cut[t - 1], s.size() * t / nt);
+            while (c < s.size() && c > 0 && s[c - 1] != '\n') ++c;
+            cut[t] = c;
+        }
+        std::vector<std::vector<pr::TraceLine>> part(nt);
+        std::vector<std::string> err(nt);
+        std::vector<std::thread> pool;
+        for (size_t t = 0; t < nt; ++t)
+            pool.emplace_back([&, t] {
+                try {
+                    std::istringstream in(s.substr(cut[t], cut[t + 1] - cut[t]));
+                    part[t] = pr::read_trace_jsonl(in);
+                } catch (const std::exception& e) {
+                    err[t] = e.what();
+                }
+            });
+        for (auto& th : pool) th.join();
+        for (size_t t = 0; t < nt; ++t)
+            if (!err[t].empty()) throw std::runtime_error(err[t] + " (chunk " + std::to_string(t) + ")");
+        std::unordered_map<std::string, std::pair<long, int>> last;  // program -> (offset, step)
+        size_t n = 0;
+        for (size_t t = 0; t < nt; ++t) {
+            std::unordered_map<std::string, bool> seen_here;
+            for (const auto& l : part[t]) {
+                if (!seen_here.count(l.program_id)) {
+                    seen_here[l.program_id] = true;
+                    auto it = last.find(l.program_id);
+                    if (it != last.end()) {
+                        if (l.record.token_offset <= it->second.first) throw std::runtime_error("token_offset does not increase");
+                        if (l.record.step_index <= it->second.second) throw std::runtime_error("step_index does not increase");
+                    }
+                }
+                last[l.program_id] = {l.record.token_offset, l.record.step_index};
+            }
+            n += part[t].size();
+        }
+        return static_cast<int>(n);
     } catch (const std::exception& e) {
         g_err = e.what();
         return -1;
