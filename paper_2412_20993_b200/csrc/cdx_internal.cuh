@@ -73,6 +73,7 @@ struct cdx_ctx {
     uint64_t* sh_host = nullptr;  // pinned host staging (counts, bounds)
     uint64_t it_cap = 0;          // K1 global table capacity of the last call (k_intern.cu)
     // one-round-trip scalar calls (k_scalar.cu): pinned host / device staging pair
+    void* sc_counter = nullptr;   // K2 fast path: group claims + CTAs done (k_sc_fast.cu)
     uint8_t* sc_h = nullptr;
     uint8_t* sc_d = nullptr;
     size_t sc_cap = 0;

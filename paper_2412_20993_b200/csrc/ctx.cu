@@ -191,6 +191,11 @@ int cdx_ctx_create(int device, cdx_ctx** out) {
         return CDX_ECUDA;
     }
     cudaMemset(c->d_err, 0, sizeof(int));
+    // K2's group-claim counters (k_sc_fast.cu): zeroed once here, rewound by the kernel
+    if (cudaMalloc(&c->sc_counter, 2 * sizeof(unsigned long long)) == cudaSuccess)
+        cudaMemset(c->sc_counter, 0, 2 * sizeof(unsigned long long));
+    else
+        c->sc_counter = nullptr;
     cudaDeviceSynchronize();
     c->stream = c->own_stream;
     *out = c;
@@ -217,6 +222,7 @@ int cdx_ctx_destroy(cdx_ctx* ctx) {
     if (ctx->d_err) cudaFree(ctx->d_err);
     if (ctx->h_err) cudaFreeHost(ctx->h_err);
     if (ctx->sc_d) cudaFree(ctx->sc_d);
+    if (ctx->sc_counter) cudaFree(ctx->sc_counter);
     if (ctx->sc_h) cudaFreeHost(ctx->sc_h);
     if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
     if (ctx->copy_stream) cudaStreamDestroy(ctx->copy_stream);

@@ -268,6 +268,17 @@ __global__ void __launch_bounds__(FAST_WARPS * 32) sc_fast_kernel(const __grid_c
             parity ^= 1u;
         }
     }
+    // the last CTA out rewinds the claim counter for the next call (no memset launch): every
+    // other CTA has left its loop, so no claim can follow the reset
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        if (atomicAdd(counter + 1, 1ull) == gridDim.x - 1) {
+            counter[0] = 0;
+            counter[1] = 0;
+            __threadfence();
+        }
+    }
 }
 
 template <int S>
@@ -353,9 +364,9 @@ bool launch_sc_fast(cdx_ctx* ctx, const ScParams& p0) {
     if (impl && std::string(impl) == "matchonly") mw = 64;
     wpc = std::max<uint32_t>(1, std::min<uint32_t>(FAST_WARPS, wpc));
     p.stages = std::max<uint32_t>(1, std::min<uint32_t>(SC_MAX_STAGES, stages));
-    auto* counter = static_cast<unsigned long long*>(scratch2(ctx, 256));
-    if (!counter) return false;
-    cudaMemsetAsync(counter, 0, sizeof(unsigned long long), ctx->stream);
+    // claim counter + CTAs-done counter: the context's own (ctx.cu), zeroed once, rewound in-kernel
+    if (!ctx->sc_counter) return false;
+    auto* counter = static_cast<unsigned long long*>(ctx->sc_counter);
     switch (S) {
         case 32: launch_fast<32>(ctx, tmap, p, wpc, mw, counter); break;
         case 16: launch_fast<16>(ctx, tmap, p, wpc, mw, counter); break;
