@@ -415,7 +415,7 @@ CPU_SAMPLE = {"A": 1024, "B": 1 << 16, "C": 1 << 18, "D": 1 << 14, "E": 1 << 15,
 def cpu_baseline(name, cfg, sample=None, target_s=1.0, max_reps=64):
     """The CPU path on repeated bounded samples (fresh seed each) until `target_s` seconds
     of timed CPU work have accumulated; value = total work / total timed seconds."""
-    nth = host_threads() if cfg["kind"] != "jsonl" else 1
+    nth = host_threads()
     n = sample or CPU_SAMPLE[name]
     work = secs = 0.0
     reps = 0
@@ -436,7 +436,7 @@ def run_reference(args, cfg, rank, world):
         return
     vals = []
     n = args.ref_sample or CPU_SAMPLE[args.config]
-    nth = host_threads() if cfg["kind"] != "jsonl" else 1
+    nth = host_threads()
     note = ""
     for i in range(args.warmup + args.steps):
         v, dt, note = CPU[cfg["kind"]](cfg, nth, n, 20993 + i)

@@ -720,8 +720,13 @@ __global__ void __launch_bounds__(32 * (WS_MAXW + 2), 1) intern_ws(const __grid_
                 pre_q += k;
                 if (k) progress = true;
             }
-            if (ld_volatile(&S.ranked) < ld_volatile(&S.lt_fill)) {
-                for (uint32_t base = 0; base < WS_LT; base += 32) {
+            // dense ids pay off for a small vocabulary (its answers hit the caches); with many
+            // keys most answers take the global path and are remapped anyway, so the helper
+            // stops ranking there (each rank walks up to a round of bitmap words)
+            const uint32_t fill = ld_volatile(&S.lt_fill);
+            uint32_t budget = 4;  // ranks per pass: the round counts above keep flowing
+            if (fill <= 64 && ld_volatile(&S.ranked) < fill) {
+                for (uint32_t base = 0; base < WS_LT && budget; base += 32) {
                     const uint32_t e = base + lane;
                     const uint32_t ready = ld_volatile(&S.lt_info[e].w), gs = ld_volatile(&S.lt_info[e].x);
                     const uint32_t rk = ld_volatile(&S.lt_info[e].y);
@@ -732,9 +737,10 @@ __global__ void __launch_bounds__(32 * (WS_MAXW + 2), 1) intern_ws(const __grid_
                     uint32_t m = __ballot_sync(0xffffffffu, cand);
                     if (!m) continue;
                     fence_acq_rel_gpu();
-                    while (m) {
+                    while (m && budget && ld_volatile(&S.cons_done) < NW) {
                         const int src = __ffs(m) - 1;
                         m &= m - 1;
+                        --budget;
                         const uint32_t ff = __shfl_sync(0xffffffffu, f, src);
                         const uint32_t gsl = __shfl_sync(0xffffffffu, gs, src);
                         if (__ldcg(p.first + gsl) != ff) continue;  // lowered meanwhile: next time

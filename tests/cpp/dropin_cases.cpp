@@ -421,6 +421,15 @@ void size_edge_cases() {
             return esc(f.answer) + (f.low_confidence ? " low" : "");
         });
     }
+    // hand-built clusterings the reference still evaluates: a cluster larger than the total,
+    // a total past 2^26
+    for (auto [sz, tot] : {std::pair<int, int>{5, 4}, {3, 2}, {1 << 27, (1 << 27) + 3}, {7, 100000000}}) {
+        metrics::Clustering c;
+        c.total = tot;
+        c.clusters = {{"a", sz}, {"b", 1}};
+        run("size entropy " + std::to_string(sz) + "/" + std::to_string(tot),
+            [&] { return hex(metrics::semantic_entropy(c)) + " " + hex(metrics::certaindex_entropy(c)); });
+    }
     std::string big(1 << 21, 'x');  // one answer above the byte limit
     run("size flag_hesitation big", [&] { return std::to_string(probe::flag_hesitation(big + " WAIT", std::vector<std::string>{"wait"})); });
     run("size cluster_exact big", [&] { return show(metrics::cluster_exact(std::vector<std::string>{big, " " + big})).substr(0, 40); });
