@@ -235,7 +235,9 @@ class Context:
     # -- plumbing --
     def _bind_stream(self):
         s = self.torch.cuda.current_stream(self.dev).cuda_stream
-        self.lib.cdx_ctx_set_stream(self.h, C.c_void_p(s))
+        if s != self.__dict__.get("_bound_stream"):  # only this method sets the context's stream
+            self.lib.cdx_ctx_set_stream(self.h, C.c_void_p(s))
+            self._bound_stream = s
 
     def _check(self, st: int):
         if st != _abi.CDX_OK:
@@ -520,23 +522,42 @@ class Context:
         return ids[:n], (hes[:n] if hes is not None else None), first[:nu.value], nu.value
 
     # -- K6 --
+    _SOA_FIELDS = ("arrival", "last_service", "iter_tok_sum", "iter_count", "knob", "cap", "terminated")
+
+    def _prog_soa(self, soa: dict, id_base: int):
+        """cdx_prog_soa for these tensors; the ctypes struct is reused while the same storage
+        is passed again (a scheduling loop calls the order on the same state every round)."""
+        pid = soa.get("program_id")
+        key = tuple(soa[k].data_ptr() for k in self._SOA_FIELDS) + (pid.data_ptr() if pid is not None else 0,
+                                                                     id_base)
+        cache = self.__dict__.setdefault("_soa_cache", {})
+        s = cache.get(key)
+        if s is None:
+            s = _abi.ProgSoA()
+            for k, p in zip(self._SOA_FIELDS, key):
+                setattr(s, k, p)
+            if pid is not None:  # explicit ids (u32 stored in an int32 tensor)
+                s.program_id = key[7]
+            s.id_base = id_base
+            if len(cache) > 64:
+                cache.clear()
+            cache[key] = s
+        return s
+
     def gang_priority(self, soa: dict, policy: InterPolicy, now: float, id_base: int = 0, want_keys: bool = False,
-                      want_escalated: bool = False):
+                      want_escalated: bool = False, out=None):
+        """Program order of the live programs (cdx_gang_priority).  `out` (int32[>= N], device)
+        receives the order instead of a fresh tensor."""
         t = self.torch
         N = soa["arrival"].shape[0]
-        s = _abi.ProgSoA()
-        for k in ("arrival", "last_service", "iter_tok_sum", "iter_count", "knob", "cap", "terminated"):
-            setattr(s, k, soa[k].data_ptr())
-        if soa.get("program_id") is not None:  # explicit ids (u32 stored in an int32 tensor)
-            s.program_id = soa["program_id"].data_ptr()
-        s.id_base = id_base
-        order = self.empty((max(N, 1),), t.int32)
+        s = self._prog_soa(soa, id_base)
+        order = out if out is not None else self.empty((max(N, 1),), t.int32)
         esc = self.empty((max(N, 1),), t.uint8) if want_escalated else None
         keys = self.empty((max(N, 1), 3), t.int64) if want_keys else None
         n_out = C.c_uint64(0)
         pol = c_inter(policy)
         self._bind_stream()
-        self._check(self.lib.cdx_gang_priority(self.h, C.byref(s), N, C.byref(pol), float(now), _ptr(order),
+        self._check(self.lib.cdx_gang_priority(self.h, C.byref(s), N, C.byref(pol), float(now), order.data_ptr(),
                                                C.byref(n_out), _ptr(esc), _ptr(keys)))
         n = n_out.value
         return order[:n], (esc[:N] if esc is not None else None), (keys[:n] if keys is not None else None)

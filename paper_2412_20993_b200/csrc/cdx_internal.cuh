@@ -36,7 +36,8 @@ struct cdx_ctx {
     uint64_t graph_mark = 0;  // launches before the current graph capture
     // device error word: 0 ok, else a CDX_E* code set by a kernel (validated on sync)
     int* d_err = nullptr;
-    int* h_err = nullptr;  // pinned mirror
+    int* h_err = nullptr;  // pinned mirror (a 64-word pinned block)
+    uint32_t* h_small = nullptr;  // pinned staging for small results read back by a call (h_err + 16, 48 words)
     std::string pending_err_msg[8];
     // growable scratch (look-back tile state, counters, tables)
     void* scratch = nullptr;

@@ -186,11 +186,12 @@ int cdx_ctx_create(int device, cdx_ctx** out) {
     if (cudaStreamCreateWithFlags(&c->own_stream, cudaStreamNonBlocking) != cudaSuccess ||
         cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking) != cudaSuccess ||
         cudaMalloc(&c->d_err, sizeof(int)) != cudaSuccess ||
-        cudaMallocHost(&c->h_err, sizeof(int)) != cudaSuccess) {
+        cudaMallocHost(&c->h_err, 64 * sizeof(int)) != cudaSuccess) {
         delete c;
         return CDX_ECUDA;
     }
     cudaMemset(c->d_err, 0, sizeof(int));
+    c->h_small = reinterpret_cast<uint32_t*>(c->h_err) + 16;
     // K2's group-claim counters (k_sc_fast.cu): zeroed once here, rewound by the kernel
     if (cudaMalloc(&c->sc_counter, 2 * sizeof(unsigned long long)) == cudaSuccess)
         cudaMemset(c->sc_counter, 0, 2 * sizeof(unsigned long long));

@@ -22,9 +22,13 @@
 // shared memory, resolve their offsets by windowed decoupled look-back and write digit
 // runs; the last pass writes program ids directly.
 #include <algorithm>
+#include <atomic>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <vector>
+
+#include <cooperative_groups.h>
 
 #include "cdx_internal.cuh"
 
@@ -792,6 +796,643 @@ __global__ void gang_fix_b(uint64_t* __restrict__ k, uint32_t* __restrict__ v, c
     }
 }
 
+// ---- persistent gang order: key build, radix passes and the run fix-up in ONE launch -------
+// The lean fast path (no key output, arrivals assumed non-decreasing) as a cooperative kernel
+// with one 1024-thread CTA per SM.  The sort moves 4-byte upper halves and 4-byte program
+// indices (the low halves stay in lo[program], read only by the fix-up), and every pass is
+// reduce-then-scan across the grid instead of a look-back chain:
+//   phase 0   CTA c builds the keys of programs [c*Q0, (c+1)*Q0) (as
+//             gang_prepare), writes lo[i] and the upper half (PG_DEAD when terminated),
+//             counts all 4 digits of its live upper halves and ORs / ANDs the live keys'
+//             halves;                                                           grid barrier
+//   plan      digits on which every live key agrees are skipped (the OR / AND of all CTAs);
+//   pass      every CTA reads the digit's counts of all CTAs (G x 256, L2) and derives its
+//             exclusive base per digit value; then, tile by tile over its input range (the
+//             first pass: its programs, dead ones dropped; later passes: positions
+//             [c*Q, (c+1)*Q) of the previous output), ranks stably (ballot digit match + a
+//             shared atomic per group of equal digits), sorts the tile by digit in shared
+//             memory and writes whole digit runs;                                grid barrier
+//             then counts the next digit over its next input range;             grid barrier
+//   fix-up    only when the low halves differ at all: runs of equal upper halves whose low
+//             halves descend are listed (gang_fix_a's rule) and insertion-sorted by the low
+//             half (gang_fix_b's rule);                                         grid barrier
+// On this path arrivals are non-decreasing and ids increase with the index (the flag that
+// says otherwise sends the call to the checked path), so the (arrival, id) tie-break IS the
+// index order, which every pass keeps.  An escalated program's key is its arrival, so the
+// escalated programs' order is the index order too: their key is canonicalised to 0 (they
+// still precede every other program, whose key has bit 63 set); under FIFO the others' keys
+// are arrivals as well and become the constant 1 << 63.  The order is unchanged, and digits
+// that no longer vary are skipped (FIFO sorts nothing: one compaction pass).
+// No ticket counters, no look-back records, nothing cleared before the launch: flags and
+// bit masks are per-CTA records reduced after the first barrier; the run counter is zeroed
+// in phase 0.
+constexpr int PG_THREADS = 1024, PG_WARPS = PG_THREADS / 32, PG_ITEMS = 8, PG_TILE = PG_THREADS * PG_ITEMS;
+constexpr uint32_t PG_DEAD = 0xffffffffu;
+constexpr int PG_FEW = 24;  // never a live upper half: a finite key's exponent is <= 0x7fe
+// dynamic shared memory: sk, sv, stk, stv [PG_TILE] (phase 0: the program-field ring) | wcnt
+// [PG_WARPS][256] | s_q [4][256] | s_red [4][256] | s_base, s_gb, s_toff [256] | s_ws [32] |
+// scalars [16] | mbarriers [4]
+// Phase 0 ring: PG_NST stages of PG_CH programs, every SoA field bulk-copied (arrival, last
+// service, token sum: 8 B; count, knob, cap, id: 4 B; terminated: 1 B)
+constexpr int PG_CH = 1024, PG_NST = 3;
+constexpr int PG_ST_ARR = 0, PG_ST_LS = PG_CH * 8, PG_ST_SUM = PG_CH * 16, PG_ST_CNT = PG_CH * 24,
+              PG_ST_KNOB = PG_CH * 28, PG_ST_CAP = PG_CH * 32, PG_ST_TERM = PG_CH * 36, PG_ST_PID = PG_CH * 37,
+              PG_ST_BYTES = PG_CH * 41;
+static_assert(PG_NST * PG_ST_BYTES <= PG_TILE * 16, "the phase-0 ring lives in the tile buffers");
+constexpr int PG_SMEM = PG_TILE * 16 + PG_WARPS * 256 * 4 + 2 * 4 * 256 * 4 + 3 * 256 * 4 + 32 * 4 + 16 * 4 + 32;
+
+struct PgArgs {
+    GangParams p;
+    uint32_t* lo;                  // [N] low half of program i's key
+    uint32_t *ka, *va, *kb, *vb;   // [N] ping-pong (kb holds phase 0's per-program upper halves)
+    uint32_t* hist;                // [4 digits][G][256] counts of each CTA's input range
+    uint32_t* crec;                // [G][8] phase-0 record per CTA: flags, OR / AND of upper and low halves
+    uint32_t* misc;                // [0] live count [1] unsorted [2] bad [3] fix-up fallback [4] listed runs
+    uint32_t* order;
+    unsigned long long* prof;      // nullable: per-CTA %globaltimer stamps at each phase end (CDX_GANG_PS_PROF)
+    int bulk0;                     // every SoA pointer 16-byte aligned: phase 0 streams them by bulk copies
+};
+
+__device__ __forceinline__ void pg_stamp(const PgArgs& a, uint32_t slot) {
+    if (a.prof && threadIdx.x == 0) {
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        a.prof[blockIdx.x * 16 + slot] = t;
+    }
+}
+__device__ __forceinline__ uint64_t umin64(uint64_t x, uint64_t y) { return x < y ? x : y; }
+__device__ __forceinline__ uint64_t policy_evict_last() {
+    uint64_t q;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(q));
+    return q;
+}
+__device__ __forceinline__ void fence_proxy_async_all() { asm volatile("fence.proxy.async;" ::: "memory"); }
+__device__ __forceinline__ uint32_t warp_incl_scan(uint32_t x, uint32_t lane) {
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= static_cast<uint32_t>(o)) x += y;
+    }
+    return x;
+}
+// Lanes holding the same 8-bit digit: one vote when the warp agrees, else MATCH.ANY or 8
+// ballots (one per bit).  MATCH.ANY's cost grows with the number of distinct values (1.6 to
+// 12.7 cycles per warp per SM on this part, tools/mb_match.cu) while the ballots cost the
+// same for any digit, so a pass whose digit takes few values (skewed exponent bytes, integer
+// mantissas) matches and the others vote.  An invalid lane matches only itself.
+__device__ __forceinline__ uint32_t match_digit(uint32_t d, bool ok, uint32_t lane, bool few) {
+    const uint32_t vm = __ballot_sync(0xffffffffu, ok);
+    const uint32_t d0 = __shfl_sync(0xffffffffu, d, vm ? __ffs(vm) - 1 : 0);
+    uint32_t m = vm;
+    if (!__all_sync(0xffffffffu, !ok || d == d0)) {
+        if (few) {
+            m = __match_any_sync(0xffffffffu, ok ? d : 256u + lane);
+        } else {
+#pragma unroll
+            for (int b = 0; b < 8; ++b) {
+                const bool bit = (d >> b) & 1u;
+                const uint32_t bb = __ballot_sync(0xffffffffu, bit);
+                m &= bit ? bb : ~bb;
+            }
+        }
+    }
+    return ok ? m : (1u << lane);
+}
+// digit count: one atomic when the warp's valid lanes agree, else one per lane (distinct
+// digits rarely collide within a warp)
+__device__ __forceinline__ void cnt_add(uint32_t* h, uint32_t d, bool ok, uint32_t lane) {
+    const uint32_t vm = __ballot_sync(0xffffffffu, ok);
+    if (!vm) return;
+    const int src = __ffs(vm) - 1;
+    const uint32_t d0 = __shfl_sync(0xffffffffu, d, src);
+    if (__all_sync(0xffffffffu, !ok || d == d0)) {
+        if (lane == static_cast<uint32_t>(src)) atomicAdd(h + d0, static_cast<uint32_t>(__popc(vm)));
+    } else if (ok) {
+        atomicAdd(h + d, 1u);
+    }
+}
+
+__global__ void __launch_bounds__(PG_THREADS, 1) gang_order_persistent(const PgArgs a) {
+    namespace cg = cooperative_groups;
+    cg::grid_group grid = cg::this_grid();
+    extern __shared__ __align__(16) uint8_t pg_smem[];
+    uint32_t* sk = reinterpret_cast<uint32_t*>(pg_smem);
+    uint32_t* sv = sk + PG_TILE;
+    uint32_t* stk = sv + PG_TILE;    // staging: the next tile's keys / values, bulk-copied while the
+    uint32_t* stv = stk + PG_TILE;   // current tile is scanned, sorted and written
+    uint32_t(*wcnt)[256] = reinterpret_cast<uint32_t(*)[256]>(stv + PG_TILE);
+    uint32_t(*s_q)[256] = reinterpret_cast<uint32_t(*)[256]>(&wcnt[PG_WARPS][0]);
+    uint32_t(*s_red)[256] = s_q + 4;
+    uint32_t* s_base = &s_red[4][0];
+    uint32_t* s_gb = s_base + 256;
+    uint32_t* s_toff = s_gb + 256;
+    uint32_t* s_ws = s_toff + 256;
+    uint32_t* s_sc = s_ws + 32;  // [0] live count, [1] tile live count, [2..6] reduced phase-0 record
+    uint64_t* bars = reinterpret_cast<uint64_t*>(s_sc + 16);  // [0..2] phase-0 ring, [3] tile staging
+    uint64_t* bar = bars + 3;
+    const GangParams& p = a.p;
+    const uint32_t G = gridDim.x, c = blockIdx.x, tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
+    const uint32_t lt = (1u << lane) - 1u;
+    const uint64_t N = p.N;
+    // ranges start on 16-byte boundaries (bulk copies of every field); buffers are padded past N
+    const uint64_t Q0 = ((N + G - 1) / G + 15) & ~15ull;
+    const uint64_t b0 = umin64(N, static_cast<uint64_t>(c) * Q0), e0 = umin64(N, b0 + Q0);
+
+    pg_stamp(a, 0);
+    // ---- phase 0: keys of programs [b0, e0); digit counts and bit masks of the live ones
+    wcnt[tid >> 8][tid & 255u] = 0;  // rows 0..3: the 4 digit counts
+    if (c == 0 && tid == 0) {
+        a.misc[3] = 0;
+        a.misc[4] = 0;
+    }
+    if (tid == 0) {
+        for (int q = 0; q < 4; ++q) mbar_init(bars + q, 1);
+        fence_mbar_init();
+    }
+    __syncthreads();
+    bool bad = false, unsorted = false;
+    uint32_t oh = 0, ah = ~0u, ol = 0, al = ~0u;
+    // one program: key, flags, masks, digit-0 count (every thread calls it the same number of
+    // times: the count uses warp votes)
+    auto program = [&](uint64_t i, bool has, double a_, double ls, double an, uint32_t id, uint32_t idn,
+                       int64_t sum, uint32_t cntv, int64_t rem, bool live) {
+        uint32_t k32 = PG_DEAD;
+        if (has) {
+            bad = bad || !(a_ >= 0.0) || !(ls >= 0.0) || isinf(a_) || isinf(ls);
+            unsorted = unsorted || a_ > an || (a_ == an && idn <= id);
+            const bool esc = (p.now - ls) >= p.limit;  // inclusive escalation
+            if (p.escalated) p.escalated[i] = esc ? 1 : 0;
+            uint64_t hk = 0;  // escalated: arrival order == index order here
+            if (!esc) {
+                hk = 1ull << 63;  // fifo: arrival order == index order here
+                if (p.order != CDX_ORDER_FIFO) {
+                    const double est =
+                        cntv ? __ddiv_rn(static_cast<double>(sum), static_cast<double>(cntv)) : p.prior;
+                    const double key = __dmul_rn(est, static_cast<double>(rem > 0 ? rem : 0));
+                    bad = bad || !(key >= 0.0) || isinf(key);
+                    hk |= dbits(key);
+                }
+            }
+            const uint32_t h32 = static_cast<uint32_t>(hk >> 32), l32 = static_cast<uint32_t>(hk);
+            a.lo[i] = l32;
+            if (live) {
+                k32 = h32;
+                oh |= h32;
+                ah &= h32;
+                ol |= l32;
+                al &= l32;
+            }
+            a.kb[i] = k32;
+        }
+        cnt_add(wcnt[0], k32 & 0xffu, has && k32 != PG_DEAD, lane);  // digit 0 (see the plan)
+    };
+    uint64_t dstart = b0;  // programs from here on take the direct-load loop
+    if (a.bulk0) {
+        // whole chunks of PG_CH programs through a PG_NST-stage ring of bulk copies (thread 0
+        // refills a stage once every thread has read it); the partial last chunk loads directly
+        uint8_t* ring = reinterpret_cast<uint8_t*>(pg_smem);
+        const uint32_t nfull = static_cast<uint32_t>((e0 - b0) / PG_CH);
+        const uint64_t pol0 = policy_evict_first();
+        auto issue0 = [&](uint32_t j) {
+            uint8_t* st = ring + (j % PG_NST) * PG_ST_BYTES;
+            uint64_t* br = bars + (j % PG_NST);
+            const uint64_t i = b0 + static_cast<uint64_t>(j) * PG_CH;
+            mbar_expect_tx(br, PG_CH * (8 * 3 + 4 * 3 + 1) + (p.program_id ? PG_CH * 4 : 0));
+            bulk_g2s(st + PG_ST_ARR, p.arrival + i, PG_CH * 8, br, pol0);
+            bulk_g2s(st + PG_ST_LS, p.last_service + i, PG_CH * 8, br, pol0);
+            bulk_g2s(st + PG_ST_SUM, p.iter_tok_sum + i, PG_CH * 8, br, pol0);
+            bulk_g2s(st + PG_ST_CNT, p.iter_count + i, PG_CH * 4, br, pol0);
+            bulk_g2s(st + PG_ST_KNOB, p.knob + i, PG_CH * 4, br, pol0);
+            bulk_g2s(st + PG_ST_CAP, p.cap + i, PG_CH * 4, br, pol0);
+            bulk_g2s(st + PG_ST_TERM, p.terminated + i, PG_CH, br, pol0);
+            if (p.program_id) bulk_g2s(st + PG_ST_PID, p.program_id + i, PG_CH * 4, br, pol0);
+        };
+        if (tid == 0)
+            for (uint32_t j = 0; j < nfull && j < static_cast<uint32_t>(PG_NST); ++j) issue0(j);
+        for (uint32_t j = 0; j < nfull; ++j) {
+            const uint8_t* st = ring + (j % PG_NST) * PG_ST_BYTES;
+            mbar_wait(bars + (j % PG_NST), (j / PG_NST) & 1u);
+            const uint64_t i = b0 + static_cast<uint64_t>(j) * PG_CH + tid;
+            const double* sa = reinterpret_cast<const double*>(st + PG_ST_ARR);
+            const uint32_t* sp = reinterpret_cast<const uint32_t*>(st + PG_ST_PID);
+            const double a_ = sa[tid];
+            const double an = tid + 1 < PG_CH ? sa[tid + 1] : (i + 1 < N ? __ldg(p.arrival + i + 1) : a_);
+            const uint32_t id = p.program_id ? sp[tid] : p.id_base + static_cast<uint32_t>(i);
+            const uint32_t idn = !p.program_id ? id + 1u
+                                 : tid + 1 < PG_CH ? sp[tid + 1]
+                                 : (i + 1 < N ? __ldg(p.program_id + i + 1) : id + 1u);
+            const int64_t rem = static_cast<int64_t>(reinterpret_cast<const int32_t*>(st + PG_ST_CAP)[tid]) -
+                                static_cast<int64_t>(reinterpret_cast<const int32_t*>(st + PG_ST_KNOB)[tid]);
+            program(i, true, a_, reinterpret_cast<const double*>(st + PG_ST_LS)[tid], an, id, idn,
+                    reinterpret_cast<const int64_t*>(st + PG_ST_SUM)[tid],
+                    reinterpret_cast<const uint32_t*>(st + PG_ST_CNT)[tid], rem, (st + PG_ST_TERM)[tid] == 0);
+            __syncthreads();  // the stage is read: refill it
+            if (tid == 0 && j + PG_NST < nfull) {
+                fence_proxy_async();
+                issue0(j + PG_NST);
+            }
+        }
+        dstart = b0 + static_cast<uint64_t>(nfull) * PG_CH;
+    }
+    // every thread runs the same trip count (the digit counts use warp votes)
+    const uint64_t span0 = (e0 - dstart + 2 * PG_THREADS - 1) / (2 * PG_THREADS) * (2 * PG_THREADS);
+    for (uint64_t i0 = dstart + tid; i0 < dstart + span0; i0 += 2 * PG_THREADS) {
+        double av[2], lsv[2], anv[2];
+        uint32_t idv[2], idnv[2], cntv[2];
+        int64_t sumv[2], remv[2];
+        bool has[2], live[2];
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {  // every field of both items loaded before any is used
+            const uint64_t i = i0 + static_cast<uint64_t>(u) * PG_THREADS;
+            has[u] = i < e0;
+            const uint64_t k = has[u] ? i : dstart;
+            av[u] = __ldg(p.arrival + k);
+            lsv[u] = __ldg(p.last_service + k);
+            anv[u] = k + 1 < N ? __ldg(p.arrival + k + 1) : av[u];
+            idv[u] = p.program_id ? __ldg(p.program_id + k) : p.id_base + static_cast<uint32_t>(k);
+            idnv[u] = p.program_id && k + 1 < N ? __ldg(p.program_id + k + 1) : idv[u] + 1u;
+            sumv[u] = __ldg(p.iter_tok_sum + k);
+            cntv[u] = __ldg(p.iter_count + k);
+            remv[u] = static_cast<int64_t>(__ldg(p.cap + k)) - static_cast<int64_t>(__ldg(p.knob + k));
+            live[u] = __ldg(p.terminated + k) == 0;
+        }
+#pragma unroll
+        for (int u = 0; u < 2; ++u)
+            program(i0 + static_cast<uint64_t>(u) * PG_THREADS, has[u], av[u], lsv[u], anv[u], idv[u], idnv[u],
+                    sumv[u], cntv[u], remv[u], live[u]);
+    }
+    {  // this CTA's record: flags and the live keys' bit masks
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            oh |= __shfl_xor_sync(0xffffffffu, oh, o);
+            ah &= __shfl_xor_sync(0xffffffffu, ah, o);
+            ol |= __shfl_xor_sync(0xffffffffu, ol, o);
+            al &= __shfl_xor_sync(0xffffffffu, al, o);
+        }
+        uint32_t* rec = &s_red[0][0];  // [PG_WARPS][4]
+        if (lane == 0) {
+            rec[warp * 4 + 0] = oh;
+            rec[warp * 4 + 1] = ah;
+            rec[warp * 4 + 2] = ol;
+            rec[warp * 4 + 3] = al;
+        }
+        const int fl = (__syncthreads_or(unsorted) ? 1 : 0) | (__syncthreads_or(bad) ? 2 : 0);
+        if (warp == 0) {
+            oh = rec[lane * 4 + 0];
+            ah = rec[lane * 4 + 1];
+            ol = rec[lane * 4 + 2];
+            al = rec[lane * 4 + 3];
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+                oh |= __shfl_xor_sync(0xffffffffu, oh, o);
+                ah &= __shfl_xor_sync(0xffffffffu, ah, o);
+                ol |= __shfl_xor_sync(0xffffffffu, ol, o);
+                al &= __shfl_xor_sync(0xffffffffu, al, o);
+            }
+            if (lane == 0) {
+                uint32_t* r = a.crec + static_cast<uint64_t>(c) * 8;
+                r[0] = static_cast<uint32_t>(fl);
+                r[1] = oh;
+                r[2] = ah;
+                r[3] = ol;
+                r[4] = al;
+            }
+        }
+    }
+    if (tid < 256) a.hist[static_cast<uint64_t>(c) * 256 + tid] = wcnt[0][tid];
+    pg_stamp(a, 1);
+    grid.sync();
+    if (warp == 0) {  // every CTA's record, reduced (each CTA plans the same passes)
+        uint32_t f = 0;
+        oh = 0, ah = ~0u, ol = 0, al = ~0u;
+        for (uint32_t q = lane; q < G; q += 32) {
+            const uint32_t* r = a.crec + static_cast<uint64_t>(q) * 8;
+            f |= __ldcg(r);
+            oh |= __ldcg(r + 1);
+            ah &= __ldcg(r + 2);
+            ol |= __ldcg(r + 3);
+            al &= __ldcg(r + 4);
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            f |= __shfl_xor_sync(0xffffffffu, f, o);
+            oh |= __shfl_xor_sync(0xffffffffu, oh, o);
+            ah &= __shfl_xor_sync(0xffffffffu, ah, o);
+            ol |= __shfl_xor_sync(0xffffffffu, ol, o);
+            al &= __shfl_xor_sync(0xffffffffu, al, o);
+        }
+        if (lane == 0) {
+            s_sc[2] = f;
+            s_sc[3] = oh ^ ah;  // varying bits of the upper halves (0 when no key is live)
+            s_sc[4] = ol ^ al;  // ... and of the low halves
+            if (c == 0) {
+                a.misc[1] = f & 1u;
+                a.misc[2] = (f >> 1) & 1u;
+            }
+        }
+    }
+    __syncthreads();
+    const uint32_t vary_hi = s_sc[3], vary_lo = s_sc[4];
+    uint32_t dlist = 0, np = 0;  // digits to sort, 4 bits each in pass order
+#pragma unroll
+    for (uint32_t d = 0; d < 4; ++d)
+        if ((vary_hi >> (8 * d)) & 0xffu) dlist |= d << (4 * np++);
+    if (np == 0) np = 1;  // every live key equal: one pass is the stable compaction
+    if ((dlist & 0xfu) != 0) {  // the first pass is not digit 0: count its digit over the programs
+        const uint32_t d0 = dlist & 0xfu;
+        __syncthreads();
+        if (tid < 256) wcnt[0][tid] = 0;
+        __syncthreads();
+        const uint64_t span = (e0 - b0 + PG_THREADS - 1) / PG_THREADS * PG_THREADS;
+        for (uint64_t i = b0 + tid; i < b0 + span; i += PG_THREADS) {
+            const uint32_t key = i < e0 ? __ldcg(a.kb + i) : PG_DEAD;
+            cnt_add(wcnt[0], (key >> (8 * d0)) & 0xffu, key != PG_DEAD, lane);
+        }
+        __syncthreads();
+        if (tid < 256) a.hist[(static_cast<uint64_t>(d0) * G + c) * 256 + tid] = wcnt[0][tid];
+        grid.sync();
+    }
+
+    uint32_t n = 0;  // live programs (known after the first pass's offsets)
+    uint32_t phase = 0;
+    bool few = false;  // this pass's digit takes at most PG_FEW values: rank by MATCH.ANY
+    const uint64_t pol = policy_evict_last();
+    for (uint32_t k = 0; k < np; ++k) {
+        const uint32_t dg = (dlist >> (4 * k)) & 0xfu;
+        const int shift = 8 * static_cast<int>(dg);
+        const uint32_t* hp = a.hist + static_cast<uint64_t>(dg) * G * 256;
+        // this pass's input range (the first pass: this CTA's programs)
+        const uint32_t* kin = (k & 1) ? a.ka : a.kb;
+        const uint32_t* vin = (k & 1) ? a.va : a.vb;
+        uint32_t* kout = (k & 1) ? a.kb : a.ka;
+        uint32_t* vout = (k & 1) ? a.vb : a.va;
+        const bool last = k + 1 == np;
+        // thread 0 bulk-copies tile tb of the range into the staging buffers (keys; values
+        // after the first pass), completion on `bar`; whole 16-byte chunks (padding past the
+        // range is never read)
+        auto issue = [&](uint64_t tb, uint64_t re_) {
+            const uint32_t cnt = static_cast<uint32_t>(umin64(PG_TILE, re_ - tb));
+            const uint32_t bytes = (cnt * 4 + 15) & ~15u;
+            fence_proxy_async_all();  // generic writes of earlier passes -> async-proxy reads
+            mbar_expect_tx(bar, k ? 2 * bytes : bytes);
+            bulk_g2s(stk, kin + tb, bytes, bar, pol);
+            if (k) bulk_g2s(stv, vin + tb, bytes, bar, pol);
+        };
+        // the first pass reads this CTA's programs; later ones positions [c*Q, (c+1)*Q) of the
+        // previous output (n is known from the first pass on)
+        const uint64_t Q = ((static_cast<uint64_t>(n) + G - 1) / G + 3) & ~3ull;
+        const uint64_t rb = k == 0 ? b0 : umin64(n, c * Q);
+        const uint64_t re = k == 0 ? e0 : umin64(n, rb + Q);
+        if (tid == 0 && rb < re) issue(rb, re);  // overlaps the offsets below
+        // ---- this CTA's exclusive base per digit: all CTAs' counts before it + smaller digits
+        {  // thread: 4 digits (one 16-byte load) of every 16th CTA's row; partial sums in wcnt
+            const uint32_t rg = tid >> 6, cc = tid & 63u;
+            uint4 all4 = make_uint4(0, 0, 0, 0), bef4 = make_uint4(0, 0, 0, 0);
+#pragma unroll 4
+            for (uint32_t q = rg; q < G; q += 16) {
+                const uint4 x = __ldcg(reinterpret_cast<const uint4*>(hp + static_cast<uint64_t>(q) * 256) + cc);
+                all4.x += x.x, all4.y += x.y, all4.z += x.z, all4.w += x.w;
+                if (q < c) bef4.x += x.x, bef4.y += x.y, bef4.z += x.z, bef4.w += x.w;
+            }
+            reinterpret_cast<uint4*>(wcnt[rg])[cc] = all4;
+            reinterpret_cast<uint4*>(wcnt[16 + rg])[cc] = bef4;
+        }
+        __syncthreads();
+        {
+            uint32_t all = 0, before = 0;
+            if (tid < 256) {
+#pragma unroll
+                for (int q = 0; q < 16; ++q) {
+                    all += wcnt[q][tid];
+                    before += wcnt[16 + q][tid];
+                }
+            }
+            const uint32_t incl = warp_incl_scan(all, lane);
+            if (lane == 31 && warp < 8) s_ws[warp] = incl;
+            few = __syncthreads_count(all != 0) <= PG_FEW;  // values the digit takes over all keys
+            if (tid < 256) {
+                uint32_t wpre = 0;
+                for (uint32_t w = 0; w < warp; ++w) wpre += s_ws[w];
+                s_base[tid] = wpre + incl - all + before;
+                if (tid == 255) s_sc[0] = wpre + incl;  // every live key counted once
+            }
+            __syncthreads();
+        }
+        pg_stamp(a, 2 + 3 * k);
+        if (k == 0) {
+            n = s_sc[0];
+            if (c == 0 && tid == 0) a.misc[0] = n;
+        }
+        // ---- rank, sort by digit in shared memory, write digit runs; tile by tile in order
+#pragma unroll
+        for (int w = 0; w < PG_WARPS; w += 4) wcnt[w + (tid >> 8)][tid & 255u] = 0;
+        __syncthreads();
+        for (uint64_t tb = rb; tb < re; tb += PG_TILE) {
+            const uint32_t tile_n = static_cast<uint32_t>(umin64(PG_TILE, re - tb));
+            mbar_wait(bar, phase);
+            phase ^= 1u;
+            uint32_t kk[PG_ITEMS], v[PG_ITEMS], rank[PG_ITEMS];
+            const uint32_t wofs = warp * 32 * PG_ITEMS + lane;  // item j: tile index wofs + 32 j
+#pragma unroll
+            for (int j = 0; j < PG_ITEMS; ++j) {
+                const uint32_t li = wofs + 32 * j;
+                const bool ok = li < tile_n;
+                kk[j] = ok ? stk[li] : PG_DEAD;
+                v[j] = k == 0 ? static_cast<uint32_t>(tb + li) : stv[li];
+            }
+#pragma unroll
+            for (int j = 0; j < PG_ITEMS; ++j) {
+                const bool ok = kk[j] != PG_DEAD;  // out of range or terminated (first pass)
+                const uint32_t d = (kk[j] >> shift) & 0xffu;
+                const uint32_t peers = match_digit(d, ok, lane, few);
+                const uint32_t below = peers & lt;
+                // the row is this warp's own and the group leaders hold distinct digits: a plain
+                // read-modify-write, ordered against the next item by the warp barrier
+                uint32_t old = 0;
+                if (ok && below == 0) {
+                    old = wcnt[warp][d];
+                    wcnt[warp][d] = old + static_cast<uint32_t>(__popc(peers));
+                }
+                rank[j] = __shfl_sync(0xffffffffu, old, __ffs(peers) - 1) + __popc(below);
+                __syncwarp();
+            }
+            __syncthreads();  // the staging buffers are consumed: fetch the next tile behind this one
+            if (tid == 0 && tb + PG_TILE < re) issue(tb + PG_TILE, re);
+            {  // quarter sums over warps
+                const uint32_t d = tid & 255u, q = tid >> 8;
+                uint32_t sq = 0;
+#pragma unroll
+                for (int w = 0; w < PG_WARPS / 4; ++w) sq += wcnt[q * (PG_WARPS / 4) + w][d];
+                s_q[q][d] = sq;
+            }
+            __syncthreads();
+            uint32_t cnt = 0;
+            if (tid < 256) cnt = s_q[0][tid] + s_q[1][tid] + s_q[2][tid] + s_q[3][tid];
+            const uint32_t incl = warp_incl_scan(cnt, lane);
+            if (lane == 31 && warp < 8) s_ws[warp] = incl;
+            __syncthreads();
+            if (tid < 256) {
+                uint32_t wpre = 0;
+                for (uint32_t w = 0; w < warp; ++w) wpre += s_ws[w];
+                const uint32_t toff = wpre + incl - cnt;
+                s_toff[tid] = toff;
+                s_gb[tid] = s_base[tid] - toff;  // global position = s_gb[digit] + tile-sorted index
+                s_base[tid] += cnt;
+                if (tid == 255) s_sc[1] = wpre + incl;
+            }
+            __syncthreads();
+            {  // wcnt[w][d] = first tile-sorted index of warp w's digit-d keys
+                const uint32_t d = tid & 255u, q = tid >> 8;
+                uint32_t run = s_toff[d];
+                for (uint32_t qq = 0; qq < q; ++qq) run += s_q[qq][d];
+#pragma unroll
+                for (int w = 0; w < PG_WARPS / 4; ++w) {
+                    const uint32_t x = wcnt[q * (PG_WARPS / 4) + w][d];
+                    wcnt[q * (PG_WARPS / 4) + w][d] = run;
+                    run += x;
+                }
+            }
+            __syncthreads();
+#pragma unroll
+            for (int j = 0; j < PG_ITEMS; ++j) {
+                if (kk[j] == PG_DEAD) continue;
+                const uint32_t lp = wcnt[warp][(kk[j] >> shift) & 0xffu] + rank[j];
+                sk[lp] = kk[j];
+                sv[lp] = v[j];
+            }
+            __syncthreads();
+#pragma unroll
+            for (int w = 0; w < PG_WARPS; w += 4) wcnt[w + (tid >> 8)][tid & 255u] = 0;  // next tile's counts
+            const uint32_t tl = s_sc[1];
+            for (uint32_t li = tid; li < tl; li += PG_THREADS) {
+                const uint32_t key = sk[li], val = sv[li];
+                const uint32_t pos = s_gb[(key >> shift) & 0xffu] + li;
+                kout[pos] = key;
+                vout[pos] = val;
+                if (last) a.order[pos] = p.program_id ? __ldg(p.program_id + val) : p.id_base + val;
+            }
+            __syncthreads();  // sk / sv / wcnt / s_gb / s_sc are reused by the next tile
+        }
+        pg_stamp(a, 3 + 3 * k);
+        grid.sync();
+        if (last) break;
+        // ---- next digit's counts over this CTA's next input range (positions [c*Q, (c+1)*Q))
+        if (tid < 256) wcnt[0][tid] = 0;
+        __syncthreads();
+        {
+            const uint32_t dn = (dlist >> (4 * (k + 1))) & 0xfu;
+            const int nshift = 8 * static_cast<int>(dn);
+            const uint64_t Qn = ((static_cast<uint64_t>(n) + G - 1) / G + 3) & ~3ull;  // n is known now
+            const uint64_t nb = umin64(n, c * Qn), ne = umin64(n, nb + Qn);  // the next pass's range
+            constexpr int U = 8;  // keys in flight per thread per round trip
+            const uint64_t span = (ne - nb + U * PG_THREADS - 1) / (U * PG_THREADS) * (U * PG_THREADS);
+            for (uint64_t i0 = nb + tid; i0 < nb + span; i0 += U * PG_THREADS) {
+                uint32_t key[U];
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    const uint64_t i = i0 + static_cast<uint64_t>(u) * PG_THREADS;
+                    key[u] = i < ne ? __ldcg(kout + i) : 0u;
+                }
+#pragma unroll
+                for (int u = 0; u < U; ++u)
+                    cnt_add(wcnt[0], (key[u] >> nshift) & 0xffu, i0 + static_cast<uint64_t>(u) * PG_THREADS < ne, lane);
+            }
+            __syncthreads();
+            if (tid < 256) a.hist[(static_cast<uint64_t>(dn) * G + c) * 256 + tid] = wcnt[0][tid];
+        }
+        pg_stamp(a, 4 + 3 * k);
+        grid.sync();
+    }
+    if (vary_lo == 0) {  // every live low half equal: the upper halves decide alone
+        pg_stamp(a, 15);
+        return;
+    }
+
+    // ---- fix-up: runs of equal upper halves whose low halves descend
+    const bool odd = ((np - 1) & 1u) != 0;  // the last pass wrote kb / vb when odd, ka / va when even
+    const uint32_t* kf = odd ? a.kb : a.ka;
+    const uint32_t* vf = odd ? a.vb : a.va;
+    uint32_t* runs = odd ? a.va : a.vb;  // free after the last pass
+    {
+        const uint64_t Q = ((static_cast<uint64_t>(n) + G - 1) / G + 3) & ~3ull;
+        const uint64_t nb = umin64(n, c * Q), ne = umin64(n, nb + Q);
+        constexpr int U = 8;  // positions per thread per round: the key / value / low-half loads
+                              // of all U are in flight together
+        for (uint64_t i0 = nb + tid; i0 < ne; i0 += U * PG_THREADS) {
+            uint32_t hk[U], hq[U], vi[U], vp[U], li[U], lp[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const uint64_t i = i0 + static_cast<uint64_t>(u) * PG_THREADS;
+                const bool in = i < ne && i > 0;
+                hk[u] = in ? __ldcg(kf + i) : 0u;
+                hq[u] = in ? __ldcg(kf + i - 1) : 1u;
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const uint64_t i = i0 + static_cast<uint64_t>(u) * PG_THREADS;
+                const bool eq = hk[u] == hq[u];
+                vi[u] = eq ? __ldcg(vf + i) : 0u;
+                vp[u] = eq ? __ldcg(vf + i - 1) : 0u;
+            }
+            uint32_t desc = 0;  // bit u: a descent at position i0 + u * PG_THREADS
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const bool eq = hk[u] == hq[u];
+                li[u] = eq ? __ldcg(a.lo + vi[u]) : 1u;
+                lp[u] = eq ? __ldcg(a.lo + vp[u]) : 0u;
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u) desc |= (li[u] < lp[u] ? 1u : 0u) << u;
+            while (desc) {  // a descent inside a run: the first one of its run lists the run start
+                const int u = __ffs(desc) - 1;
+                desc &= desc - 1;
+                const uint64_t i = i0 + static_cast<uint64_t>(u) * PG_THREADS;
+                const uint32_t h = __ldcg(kf + i);
+                uint64_t j = i - 1;
+                bool first = true;
+                while (j > 0 && __ldcg(kf + j - 1) == h) {
+                    if (i - j >= FIX_RUN) break;
+                    first = first && !(__ldcg(a.lo + __ldcg(vf + j)) < __ldcg(a.lo + __ldcg(vf + j - 1)));
+                    --j;
+                }
+                const bool reach = j == 0 || __ldcg(kf + j - 1) != h;
+                if (!reach) {
+                    atomicOr(a.misc + 3, 1u);  // the run is longer than the fix-up handles
+                } else if (first) {
+                    uint64_t e = i + 1;  // the run must also end within reach
+                    while (e < n && e - j <= FIX_RUN && __ldcg(kf + e) == h) ++e;
+                    if (e - j > FIX_RUN) atomicOr(a.misc + 3, 1u);
+                    else runs[atomicAdd(a.misc + 4, 1u)] = static_cast<uint32_t>(j);  // at most n/2 runs
+                }
+            }
+        }
+    }
+    pg_stamp(a, 14);
+    grid.sync();
+    if (__ldcg(a.misc + 3)) return;  // the caller re-sorts all 8 digits
+    const uint32_t cnt = __ldcg(a.misc + 4);
+    for (uint32_t t = c * PG_THREADS + tid; t < cnt; t += G * PG_THREADS) {
+        const uint64_t i = __ldcg(runs + t);
+        const uint32_t h = __ldcg(kf + i);
+        uint32_t rv[FIX_RUN], rl[FIX_RUN];
+        uint32_t m = 0;
+        for (uint64_t e = i; e < n && m < FIX_RUN && __ldcg(kf + e) == h; ++e, ++m) {
+            const uint32_t val = __ldcg(vf + e), l = __ldcg(a.lo + val);
+            uint32_t b = m;  // stable insertion by the low half
+            while (b > 0 && rl[b - 1] > l) {
+                rl[b] = rl[b - 1];
+                rv[b] = rv[b - 1];
+                --b;
+            }
+            rl[b] = l;
+            rv[b] = val;
+        }
+        for (uint32_t q = 0; q < m; ++q)
+            a.order[i + q] = p.program_id ? __ldg(p.program_id + rv[q]) : p.id_base + rv[q];
+    }
+    pg_stamp(a, 15);
+}
+
 // Digits [dlo, 8) with the key count on the device (n_dev; nmax bounds it): the caller has
 // histogrammed the keys into lb[0, 2048) already.  No host round trip: every digit gets a
 // pass (trivial ones copy), so the result lands in k0/v0 for an even pass count.
@@ -883,11 +1524,93 @@ int radix_sort_pairs(cdx_ctx* ctx, uint64_t* k0, uint32_t* v0, uint64_t* k1, uin
 
 namespace cdx {
 namespace {
+enum GangMode { GANG_FAST = 0, GANG_CHECKED = 1, GANG_FULL = 2 };
+// The persistent one-launch order (gang_order_persistent).  *used = false when this device
+// cannot host the cooperative grid (no cooperative launch, an SM limit leaving no room), or
+// CDX_GANG_PS=0 asks for the multi-launch path; the caller then takes that path.
+int gang_persistent(cdx_ctx* ctx, const GangParams& p, uint64_t N, uint32_t* order, uint64_t* n_out, int* redo,
+                    bool* used) {
+    *used = false;
+    const char* env = getenv("CDX_GANG_PS");
+    if (env && env[0] == '0') return CDX_OK;
+    // resident CTAs per SM, queried once per device (-1: not yet, 0: no cooperative launch)
+    static std::atomic<int> occ_cache[64];
+    static std::atomic<int> occ_set[64];
+    const int dev = ctx->device & 63;
+    int occ = 0;
+    if (occ_set[dev].load(std::memory_order_acquire)) {
+        occ = occ_cache[dev].load(std::memory_order_relaxed);
+    } else {
+        int coop = 0;
+        cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, ctx->device);
+        cudaError_t e = cudaFuncSetAttribute(gang_order_persistent, cudaFuncAttributeMaxDynamicSharedMemorySize, PG_SMEM);
+        if (e == cudaSuccess && coop)
+            e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, gang_order_persistent, PG_THREADS, PG_SMEM);
+        if (e != cudaSuccess || !coop) {
+            cudaGetLastError();
+            occ = 0;
+        }
+        occ_cache[dev].store(occ, std::memory_order_relaxed);
+        occ_set[dev].store(1, std::memory_order_release);
+    }
+    if (occ < 1) return CDX_OK;
+    const uint64_t want = std::max<uint64_t>(1, (N + PG_TILE - 1) / PG_TILE);
+    const uint32_t G = static_cast<uint32_t>(std::min<uint64_t>(want, static_cast<uint64_t>(ctx->sm_count) * occ));
+    // scratch: lo ka va kb vb [NP] | hist [4][G][256] | crec [G][8] | misc [16]; NP pads N to whole
+    // 16-byte chunks plus one (the bulk copies read whole chunks)
+    const size_t NP = ((N + 3) & ~3ull) + 4;
+    const size_t words = NP * 5 + static_cast<size_t>(4) * G * 256 + static_cast<size_t>(G) * 8 + 16;
+    uint32_t* s = static_cast<uint32_t*>(scratch(ctx, words * 4));
+    if (!s) return set_error(ctx, CDX_ECUDA, "gang_priority: scratch allocation failed");
+    PgArgs a{p, s, s + NP, s + 2 * NP, s + 3 * NP, s + 4 * NP, s + 5 * NP, nullptr, nullptr, order, nullptr, 0};
+    auto al16 = [](const void* q) { return (reinterpret_cast<uintptr_t>(q) & 15) == 0; };
+    a.bulk0 = al16(p.arrival) && al16(p.last_service) && al16(p.iter_tok_sum) && al16(p.iter_count) &&
+              al16(p.knob) && al16(p.cap) && al16(p.terminated) && al16(p.program_id);
+    a.crec = a.hist + static_cast<size_t>(4) * G * 256;
+    a.misc = a.crec + static_cast<size_t>(G) * 8;
+    const bool prof = getenv("CDX_GANG_PS_PROF") != nullptr;  // phase timings to stderr (tuning only)
+    if (prof) {
+        a.prof = static_cast<unsigned long long*>(scratch2(ctx, static_cast<size_t>(G) * 16 * 8));
+        cudaMemsetAsync(a.prof, 0, static_cast<size_t>(G) * 16 * 8, ctx->stream);
+    }
+    void* args[] = {&a};
+    cudaError_t e = cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(gang_order_persistent), dim3(G),
+                                                dim3(PG_THREADS), args, PG_SMEM, ctx->stream);
+    if (e == cudaErrorCooperativeLaunchTooLarge) {  // e.g. an MPS SM limit below the occupancy query
+        cudaGetLastError();
+        return CDX_OK;
+    }
+    if (e != cudaSuccess) return cuda_fail(ctx, e, "gang_priority(persistent)");
+    CDX_LAUNCHED(ctx);
+    *used = true;
+    uint32_t* hm = ctx->h_small;  // pinned: an asynchronous copy, then one stream sync
+    e = cudaMemcpyAsync(hm, a.misc, 5 * 4, cudaMemcpyDeviceToHost, ctx->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
+    if (e != cudaSuccess) return cuda_fail(ctx, e, "gang_priority");
+    if (prof) {  // per phase: the latest CTA's stamp minus the earliest start
+        std::vector<unsigned long long> t(static_cast<size_t>(G) * 16);
+        cudaMemcpy(t.data(), a.prof, t.size() * 8, cudaMemcpyDeviceToHost);
+        unsigned long long t0 = ~0ull, mx[16] = {};
+        for (uint32_t c = 0; c < G; ++c) {
+            t0 = std::min(t0, t[c * 16]);
+            for (int k = 0; k < 16; ++k) mx[k] = std::max(mx[k], t[c * 16 + k]);
+        }
+        fprintf(stderr, "gang_ps G=%u N=%llu:", G, static_cast<unsigned long long>(N));
+        for (int k = 1; k < 16; ++k) fprintf(stderr, " %d:%.1f", k, mx[k] >= t0 ? (mx[k] - t0) / 1e3 : -1.0);
+        fprintf(stderr, " us  (runs %u fallback %u)\n", hm[4], hm[3]);
+    }
+    if (hm[2]) return set_error(ctx, CDX_EINVAL, "gang_priority: times and keys must be finite and >= 0");
+    *n_out = hm[0];
+    if (hm[0] == 0) return CDX_OK;
+    if (hm[1]) *redo = GANG_CHECKED;
+    else if (hm[3]) *redo = GANG_FULL;
+    return CDX_OK;
+}
+
 // One evaluation.  GANG_FAST: no pre-sort, device-side count, one sync (see below).
 // GANG_CHECKED: host-driven, with the (arrival, id) pre-sort when arrivals are unsorted and
 // the upper-half sort + run fix-up.  GANG_FULL: all 8 digits.  *redo names the path the
 // caller must run instead when this one could not finish (unsorted arrivals, a long run).
-enum GangMode { GANG_FAST = 0, GANG_CHECKED = 1, GANG_FULL = 2 };
 int gang_priority_run(cdx_ctx* ctx, const cdx_prog_soa* progs, uint64_t N, const cdx_inter_policy* pol, double now,
                       uint32_t* order, uint64_t* n_out, uint8_t* escalated, uint64_t* keys, int mode, int* redo) {
     *redo = GANG_FAST;
@@ -895,6 +1618,11 @@ int gang_priority_run(cdx_ctx* ctx, const cdx_prog_soa* progs, uint64_t N, const
     GangParams p{progs->arrival, progs->last_service, progs->iter_tok_sum, progs->iter_count, progs->knob,
                  progs->cap, progs->terminated, progs->program_id, escalated, N, progs->id_base, pol->order, now,
                  pol->starvation_limit, pol->prior_tokens};
+    if (mode == GANG_FAST && !keys) {
+        bool used = false;
+        if (int st = gang_persistent(ctx, p, N, order, n_out, redo, &used)) return st;
+        if (used) return CDX_OK;
+    }
     const uint32_t ntiles = static_cast<uint32_t>((N + RS_TILE - 1) / RS_TILE);
     const uint32_t gtiles = static_cast<uint32_t>((N + GP_TILE - 1) / GP_TILE);
     const uint64_t nh = static_cast<uint64_t>(8) * 256 * ntiles + 8 * 256 + 16;  // radix look-back scratch

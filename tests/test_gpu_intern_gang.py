@@ -261,11 +261,14 @@ def test_gang_flag_bytes_and_alignment(ctx, N, off):
     assert np.array_equal(got.cpu().numpy().view(np.uint32), ref)
 
 
+@pytest.mark.parametrize("ps", ["1", "0"])
 @pytest.mark.parametrize("case", ["identical", "all_escalated", "one_digit", "upper_half_ties", "short_runs"])
-def test_gang_degenerate_keys(ctx, case):
+def test_gang_degenerate_keys(ctx, case, ps, monkeypatch):
     """Keys that agree on most or all radix digits (skipped passes, single-digit sorts,
-    ties resolved purely by arrival then program id)."""
+    ties resolved purely by arrival then program id), on the one-launch persistent order
+    (CDX_GANG_PS=1, the default) and on the multi-launch onesweep path (CDX_GANG_PS=0)."""
     from paper_2412_20993_b200 import InterPolicy
+    monkeypatch.setenv("CDX_GANG_PS", ps)
     N = 20000
     soa, now = _gang_inputs(N, 3, frac_term=0.0)
     if case == "identical":
@@ -306,6 +309,26 @@ def test_gang_degenerate_keys(ctx, case):
     got, _, _ = ctx.gang_priority(_to_dev(soa), pol, now)
     ctx.sync()
     ref, _ = O.gang_order(soa, 1, 1.0, 128.0, now)
+    assert np.array_equal(got.cpu().numpy().view(np.uint32), ref)
+
+
+@pytest.mark.parametrize("ps", ["1", "0"])
+@pytest.mark.parametrize("N,frac_term,sorted_arrival", [(2, 0.0, True), (33, 0.5, True), (8192, 0.1, True),
+                                                        (8193, 0.0, True), (50000, 1.0, True), (1212121, 0.3, True),
+                                                        (3000001, 0.1, True), (30000, 0.2, False)])
+def test_gang_one_launch_and_multi_launch(ctx, monkeypatch, ps, N, frac_term, sorted_arrival):
+    """The persistent one-launch order (key build, 4 radix passes with grid-wide digit
+    offsets, run fix-up: gang_order_persistent) and the multi-launch onesweep path it
+    replaces, on tile and CTA-range boundaries, all-terminated traces, several tiles per CTA
+    and unsorted arrivals (which send both to the host-checked path)."""
+    from paper_2412_20993_b200 import InterPolicy
+    monkeypatch.setenv("CDX_GANG_PS", ps)
+    soa, now = _gang_inputs(N, 4242 + N, frac_term=frac_term, sorted_arrival=sorted_arrival)
+    got, esc, _ = ctx.gang_priority(_to_dev(soa), InterPolicy(order=1, starvation_limit=0.5, prior_tokens=128.0),
+                                    now, want_escalated=True)
+    ctx.sync()
+    ref, resc = O.gang_order(soa, 1, 0.5, 128.0, now)
+    assert np.array_equal(esc.cpu().numpy(), resc)
     assert np.array_equal(got.cpu().numpy().view(np.uint32), ref)
 
 
