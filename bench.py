@@ -731,7 +731,7 @@ def bench_gang(args, cfg, rank, world, cx, with_e2e=True):
     def step(seg):
         e = seg_events(seg, "gang_priority")
         if world == 1:
-            cx.gang_priority(dev, pol, now)
+            cx.gang_priority(dev, pol, now, out=gorder)
         elif sh.native:
             cx.gang_priority_sharded(dev, pol, now, id_base=g0, capacity=N, out=gorder)
         else:
@@ -899,7 +899,7 @@ def bench_mixed(args, cfg, rank, world, cx, with_e2e=True):
         e = seg_events(seg, "gang_priority")
         soa = dict(st_d, terminated=out["decision"], cap=out["cap"])
         if world == 1:
-            res["order"] = cx.gang_priority(soa, ipol, now)[0]
+            res["order"] = cx.gang_priority(soa, ipol, now, out=gorder)[0]
         elif sh.native:
             res["order"] = cx.gang_priority_sharded(soa, ipol, now, id_base=g0, capacity=N, out=gorder)
         else:
