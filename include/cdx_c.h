@@ -283,6 +283,17 @@ int cdx_allocate_scan(cdx_ctx* ctx, const uint32_t* meets_bits, uint64_t R, uint
                       uint32_t* kept, uint64_t* n_kept, int64_t* tokens_saved,
                       int64_t* total_budget);
 
+/* K2 + K5 in one call: cdx_sc_certaindex (meets_bits required, hcert nullable) followed by
+ * cdx_allocate_scan over its meets bits, with the same arguments and results as those two
+ * calls (the SC update_certaindex + scheduler.allocate of runtime.cpp:264-313 /
+ * SPEC.md:404-412 for a whole batch).  The policy is validated before anything launches.
+ * Two launches back to back: running K5's tiles inside K2's tail was measured slower on the
+ * B200 (the per-tile release of K2's finished meets words costs more than K5's launch). */
+int cdx_sc_decide(cdx_ctx* ctx, const uint32_t* ids, uint64_t R, uint32_t P, uint32_t S, const cdx_threshold* th,
+                  uint32_t n_th, float* hcert, uint32_t* meets_bits, const cdx_alloc_policy* pol, int64_t base_offset,
+                  uint32_t kept_base, int32_t* exit_knob, uint8_t* reason, int32_t* granted, int64_t* offsets,
+                  uint32_t* kept, uint64_t* n_kept, int64_t* tokens_saved, int64_t* total_budget);
+
 /* ---- mixed-archetype batch: per-archetype certaindex + allocation at the current knob ------
  * The batched form of ProgramDriver::update_certaindex's dispatch (runtime.cpp:264-313)
  * followed by scheduler.allocate, for N programs of any archetypes, each at

@@ -352,6 +352,31 @@ class Context:
         return dict(exit_knob=exit_knob, reason=reason, granted=granted, offsets=offsets, kept=kept,
                     scalars=scal)
 
+    def sc_decide(self, ids, thresholds: Sequence[Threshold], policy: AllocPolicy, hcert=None, meets=None,
+                  base_offset: int = 0, kept_base: int = 0, out=None):
+        """K2 + K5 in one call (cdx_sc_decide: one launch on the fast path).  Returns
+        (hcert or None, meets, the allocate_scan output dict)."""
+        t = self.torch
+        R, P, S = ids.shape
+        if meets is None:
+            meets = self.empty((R, (P + 31) // 32), t.int32)
+        o = out or {}
+        exit_knob = o["exit_knob"] if "exit_knob" in o else self.empty((R,), t.int32)
+        reason = o["reason"] if "reason" in o else self.empty((R,), t.uint8)
+        granted = o["granted"] if "granted" in o else self.empty((R,), t.int32)
+        offsets = o["offsets"] if "offsets" in o else self.empty((R,), t.int64)
+        kept = o["kept"] if "kept" in o else self.empty((max(R, 1),), t.int32)
+        scal = o["scalars"] if "scalars" in o else self.empty((3,), t.int64)
+        arr, n = c_thresholds(thresholds)
+        pol = c_policy(policy)
+        self._bind_stream()
+        self._check(self.lib.cdx_sc_decide(self.h, _ptr(ids), R, P, S, arr, n, _ptr(hcert), _ptr(meets),
+                                           C.byref(pol), base_offset, kept_base, _ptr(exit_knob), _ptr(reason),
+                                           _ptr(granted), _ptr(offsets), _ptr(kept), scal.data_ptr(),
+                                           scal.data_ptr() + 8, scal.data_ptr() + 16))
+        return hcert, meets, dict(exit_knob=exit_knob, reason=reason, granted=granted, offsets=offsets, kept=kept,
+                                  scalars=scal)
+
     # -- mixed-archetype step (update_certaindex dispatch + allocate at the current knob) --
     def cot_meets(self, ids, hes, window: int, thresholds: Sequence[Threshold]):
         t = self.torch

@@ -123,6 +123,8 @@ SIGNATURES = {
     "cdx_memcpy": (C.c_int, [P, P, P, U64]),
     "cdx_memset": (C.c_int, [P, P, C.c_int, U64]),
     "cdx_allocate_scan": (C.c_int, [P, P, U64, U32, C.POINTER(AllocPolicy), I64, U32, P, P, P, P, P, P, P, P]),
+    "cdx_sc_decide": (C.c_int, [P, P, U64, U32, U32, C.POINTER(Threshold), U32, P, P, C.POINTER(AllocPolicy), I64,
+                                U32, P, P, P, P, P, P, P, P]),
     "cdx_cot_exit": (C.c_int, [P, P, P, P, U64, U32, C.POINTER(ProbeCfg), P, P, P, P, P]),
     "cdx_cot_meets": (C.c_int, [P, P, P, U64, U32, I32, C.POINTER(Threshold), U32, P]),
     "cdx_mixed_allocate": (C.c_int, [P, C.POINTER(MixedTrace), P, P, P, U64, C.POINTER(ArchPolicy), P, P, P, P, P]),

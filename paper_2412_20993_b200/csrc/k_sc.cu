@@ -21,6 +21,7 @@
 #include <cstdlib>
 #include <vector>
 
+#include "k_alloc.cuh"
 #include "k_sc.cuh"
 
 namespace cdx {
@@ -637,12 +638,13 @@ int cdx_sc_certaindex(cdx_ctx* ctx, const uint32_t* ids, uint64_t R, uint32_t P,
     return cdx_sc_certaindex_ex(ctx, ids, R, P, S, th, n_th, hcert, nullptr, meets_bits);
 }
 
-int cdx_sc_certaindex_ex(cdx_ctx* ctx, const uint32_t* ids, uint64_t R, uint32_t P, uint32_t S,
-                         const cdx_threshold* th, uint32_t n_th, float* hcert, float* majority,
-                         uint32_t* meets_bits) {
-    using namespace cdx;
-    CDX_NVTX("cdx_sc_certaindex");
-    if (!ctx) return CDX_EINVAL;
+}  // extern "C"
+
+namespace cdx {
+namespace {
+// cdx_sc_certaindex_ex's body
+int sc_impl(cdx_ctx* ctx, const uint32_t* ids, uint64_t R, uint32_t P, uint32_t S, const cdx_threshold* th,
+            uint32_t n_th, float* hcert, float* majority, uint32_t* meets_bits) {
     if (S == 0) return set_error(ctx, CDX_EINVAL, "cluster_exact: empty answer set");
     if (S > SC_WIDE_MAX) return set_error(ctx, CDX_EINVAL, "sc_certaindex: at most 4096 samples per row");
     if (P == 0) return set_error(ctx, CDX_EINVAL, "sc_certaindex: probes must be >= 1");
@@ -753,6 +755,39 @@ int cdx_sc_certaindex_ex(cdx_ctx* ctx, const uint32_t* ids, uint64_t R, uint32_t
     }
     CDX_CHECK_LAUNCH(ctx, "sc_certaindex");
     return CDX_OK;
+}
+}  // namespace
+}  // namespace cdx
+
+extern "C" {
+
+int cdx_sc_certaindex_ex(cdx_ctx* ctx, const uint32_t* ids, uint64_t R, uint32_t P, uint32_t S,
+                         const cdx_threshold* th, uint32_t n_th, float* hcert, float* majority,
+                         uint32_t* meets_bits) {
+    using namespace cdx;
+    CDX_NVTX("cdx_sc_certaindex");
+    if (!ctx) return CDX_EINVAL;
+    return sc_impl(ctx, ids, R, P, S, th, n_th, hcert, majority, meets_bits);
+}
+
+int cdx_sc_decide(cdx_ctx* ctx, const uint32_t* ids, uint64_t R, uint32_t P, uint32_t S, const cdx_threshold* th,
+                  uint32_t n_th, float* hcert, uint32_t* meets_bits, const cdx_alloc_policy* pol, int64_t base_offset,
+                  uint32_t kept_base, int32_t* exit_knob, uint8_t* reason, int32_t* granted, int64_t* offsets,
+                  uint32_t* kept, uint64_t* n_kept, int64_t* tokens_saved, int64_t* total_budget) {
+    using namespace cdx;
+    CDX_NVTX("cdx_sc_decide");
+    if (!ctx) return CDX_EINVAL;
+    if (!meets_bits) return set_error(ctx, CDX_EINVAL, "sc_decide: null meets bits");
+    // the policy is validated before anything is launched (the two calls' errors, in order)
+    al::AllocParams ap;
+    bool empty = false;
+    if (int st = alloc_prepare(ctx, meets_bits, R, P, pol, base_offset, kept_base, exit_knob, reason, granted, offsets,
+                               kept, n_kept, tokens_saved, total_budget, &ap, &empty))
+        return st;
+    if (int st = sc_impl(ctx, ids, R, P, S, th, n_th, hcert, nullptr, meets_bits)) return st;
+    if (empty) return CDX_OK;
+    return cdx_allocate_scan(ctx, meets_bits, R, P, pol, base_offset, kept_base, exit_knob, reason, granted, offsets,
+                             kept, n_kept, tokens_saved, total_budget);
 }
 
 int cdx_cluster_rows(cdx_ctx* ctx, const uint32_t* ids, uint64_t rows, uint32_t S, uint32_t* n_clusters,
