@@ -644,7 +644,8 @@ namespace cdx {
 namespace {
 // cdx_sc_certaindex_ex's body
 int sc_impl(cdx_ctx* ctx, const uint32_t* ids, uint64_t R, uint32_t P, uint32_t S, const cdx_threshold* th,
-            uint32_t n_th, float* hcert, float* majority, uint32_t* meets_bits) {
+            uint32_t n_th, float* hcert, float* majority, uint32_t* meets_bits, const al::AllocParams* tail = nullptr,
+            bool* tail_done = nullptr) {
     if (S == 0) return set_error(ctx, CDX_EINVAL, "cluster_exact: empty answer set");
     if (S > SC_WIDE_MAX) return set_error(ctx, CDX_EINVAL, "sc_certaindex: at most 4096 samples per row");
     if (P == 0) return set_error(ctx, CDX_EINVAL, "sc_certaindex: probes must be >= 1");
@@ -740,7 +741,7 @@ int sc_impl(cdx_ctx* ctx, const uint32_t* ids, uint64_t R, uint32_t P, uint32_t 
         p.comp = ctx->comp_tab[S];
     }
     // fast path: TMA-staged groups, warp-match + ALU-peel engines side by side (k_sc_fast.cu)
-    if (launch_sc_fast(ctx, p)) {
+    if (launch_sc_fast(ctx, p, tail, tail_done)) {
         CDX_CHECK_LAUNCH(ctx, "sc_certaindex(fast)");
         return CDX_OK;
     }
@@ -784,8 +785,11 @@ int cdx_sc_decide(cdx_ctx* ctx, const uint32_t* ids, uint64_t R, uint32_t P, uin
     if (int st = alloc_prepare(ctx, meets_bits, R, P, pol, base_offset, kept_base, exit_knob, reason, granted, offsets,
                                kept, n_kept, tokens_saved, total_budget, &ap, &empty))
         return st;
-    if (int st = sc_impl(ctx, ids, R, P, S, th, n_th, hcert, nullptr, meets_bits)) return st;
-    if (empty) return CDX_OK;
+    // a batch of one K5 tile runs K5 in K2's last CTA (one launch); larger ones launch K5
+    bool tail_done = false;
+    if (int st = sc_impl(ctx, ids, R, P, S, th, n_th, hcert, nullptr, meets_bits, empty ? nullptr : &ap, &tail_done))
+        return st;
+    if (empty || tail_done) return CDX_OK;
     return cdx_allocate_scan(ctx, meets_bits, R, P, pol, base_offset, kept_base, exit_knob, reason, granted, offsets,
                              kept, n_kept, tokens_saved, total_budget);
 }

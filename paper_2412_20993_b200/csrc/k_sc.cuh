@@ -51,9 +51,14 @@ __device__ __forceinline__ bool sc_meets(const ScParams& p, double hc, uint32_t 
 // metrics.cpp:167's inclusive compares, evaluated on the host exactly as the oracle does.
 void majority_interval(const cdx_threshold* th, uint32_t n_th, uint32_t S, uint32_t* lo, uint32_t* hi);
 
+namespace al {
+struct AllocParams;
+}
 // The TMA fast path (S in {4,8,16,32}, P % 32 == 0, 16B-aligned ids).  Returns true when
-// it launched; false when the shape needs the generic warp-match kernel.
-bool launch_sc_fast(cdx_ctx* ctx, const ScParams& p);
+// it launched; false when the shape needs the generic warp-match kernel.  tail (nullable):
+// K5's parameters; *tail_done = true when K5 ran in the same launch (one K5 tile: at most 2048
+// requests), else the caller launches it.
+bool launch_sc_fast(cdx_ctx* ctx, const ScParams& p, const al::AllocParams* tail = nullptr, bool* tail_done = nullptr);
 
 // Validate a threshold list against the signals an entry point produces (present[kind]);
 // an absent signal fails with the reference's message (metrics.cpp:163-166).

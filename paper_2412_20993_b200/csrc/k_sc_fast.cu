@@ -34,6 +34,7 @@
 #include <cstdlib>
 #include <string>
 
+#include "k_alloc.cuh"
 #include "k_sc.cuh"
 
 namespace cdx {
@@ -183,12 +184,17 @@ __device__ __forceinline__ double match_rows(const uint8_t* __restrict__ buf, ui
     return finish_entropy(h, logn);
 }
 
-template <int S>
+// TAIL: a batch of at most one K5 tile (2048 requests, P % 32 == 0): the last CTA out runs
+// K5 on it (al::alloc_tile) in the same launch.  Every CTA publishes its meets words with the
+// fence before its arrival on the CTAs-done counter, and the last arrival fences again before
+// its CTA reads them: one launch for the whole SC decision of a small batch (config A).
+template <int S, bool TAIL>
 __global__ void __launch_bounds__(FAST_WARPS * 32) sc_fast_kernel(const __grid_constant__ CUtensorMap tmap,
                                                                   const __grid_constant__ ScParams p,
                                                                   unsigned long long* __restrict__ counter,
                                                                   uint32_t match_warps, uint32_t claim,
-                                                                  uint64_t nchunks, uint64_t stride) {
+                                                                  uint64_t nchunks, uint64_t stride,
+                                                                  const __grid_constant__ al::AllocParams ap) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     // 128B-swizzled TMA destinations need 1024-byte alignment (offset the shared array, do
     // not cast through an integer, so every access stays an LDS)
@@ -285,20 +291,28 @@ __global__ void __launch_bounds__(FAST_WARPS * 32) sc_fast_kernel(const __grid_c
     }
     // the last CTA out rewinds the claim counter for the next call (no memset launch): every
     // other CTA has left its loop, so no claim can follow the reset
+    __shared__ uint32_t s_last;
+    if (TAIL) __threadfence();  // each lane 0's meets words before this CTA's arrival
     __syncthreads();
     if (threadIdx.x == 0) {
         __threadfence();
-        if (atomicAdd(counter + 1, 1ull) == gridDim.x - 1) {
+        const bool last = atomicAdd(counter + 1, 1ull) == gridDim.x - 1;
+        if (last) {
             counter[0] = 0;
             counter[1] = 0;
             __threadfence();
         }
+        s_last = last ? 1u : 0u;
+    }
+    if (TAIL) {
+        __syncthreads();
+        if (s_last) al::alloc_tile(ap, 0, 0, true, false);  // every meets word is written
     }
 }
 
-template <int S>
+template <int S, bool TAIL>
 void launch_fast(cdx_ctx* ctx, const CUtensorMap& tmap, const ScParams& p, uint32_t wpc, uint32_t match_warps,
-                 unsigned long long* counter) {
+                 unsigned long long* counter, const al::AllocParams& ap) {
     const size_t smem = 1024 + static_cast<size_t>(wpc) * (p.stages * std::max(32u * S * 4u, 1024u) + 1024u) + 34 * 8 +
                         FAST_WARPS * SC_MAX_STAGES * 16;
     // attribute + occupancy once per (device, CTA shape): host work per call stays one launch
@@ -308,13 +322,13 @@ void launch_fast(cdx_ctx* ctx, const CUtensorMap& tmap, const ScParams& p, uint3
         size_t smem = 0;
         int per_sm = 0;
     };
-    static thread_local Occ oc;  // one per S
+    static thread_local Occ oc;  // one per (S, TAIL)
     int per_sm = 0;
     if (oc.dev == ctx->device && oc.wpc == wpc && oc.smem == smem) {
         per_sm = oc.per_sm;
     } else {
-        cudaFuncSetAttribute(sc_fast_kernel<S>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sc_fast_kernel<S>, wpc * 32, smem);
+        cudaFuncSetAttribute(sc_fast_kernel<S, TAIL>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sc_fast_kernel<S, TAIL>, wpc * 32, smem);
         oc = Occ{ctx->device, wpc, smem, per_sm};
     }
     if (per_sm < 1) per_sm = 1;
@@ -338,13 +352,14 @@ void launch_fast(cdx_ctx* ctx, const CUtensorMap& tmap, const ScParams& p, uint3
         auto gcd = [](uint64_t a, uint64_t b) { while (b) { const uint64_t t = a % b; a = b; b = t; } return a; };
         while (gcd(stride, nchunks) != 1) stride += 2;
     }
-    sc_fast_kernel<S><<<static_cast<unsigned>(grid), wpc * 32, smem, ctx->stream>>>(tmap, p, counter, match_warps,
-                                                                                    claim, nchunks, stride);
+    sc_fast_kernel<S, TAIL><<<static_cast<unsigned>(grid), wpc * 32, smem, ctx->stream>>>(
+        tmap, p, counter, match_warps, claim, nchunks, stride, ap);
 }
 
 }  // namespace
 
-bool launch_sc_fast(cdx_ctx* ctx, const ScParams& p0) {
+bool launch_sc_fast(cdx_ctx* ctx, const ScParams& p0, const al::AllocParams* tail, bool* tail_done) {
+    if (tail_done) *tail_done = false;
     const uint32_t S = p0.S;
     // Groups are 32 consecutive rows of the flat [R*P] row sequence.  With P % 32 == 0 a
     // group is 32 probes of one request; otherwise it may straddle requests and each row's
@@ -396,11 +411,25 @@ bool launch_sc_fast(cdx_ctx* ctx, const ScParams& p0) {
     // claim counter + CTAs-done counter: the context's own (ctx.cu), zeroed once, rewound in-kernel
     if (!ctx->sc_counter) return false;
     auto* counter = static_cast<unsigned long long*>(ctx->sc_counter);
+    // one K5 tile, one meets word per group, a CTA of K5's 256 threads: K5 in K2's last CTA
+    const bool tl = tail && tail_done && tail->ntiles == 1 && p.P % 32u == 0 && p.meets &&
+                    wpc * 32 == static_cast<uint32_t>(al::AL_THREADS);
+    static const al::AllocParams none{};
+    if (tl) {
+        *tail_done = true;
+        switch (S) {
+            case 32: launch_fast<32, true>(ctx, tmap, p, wpc, mw, counter, *tail); break;
+            case 16: launch_fast<16, true>(ctx, tmap, p, wpc, mw, counter, *tail); break;
+            case 8: launch_fast<8, true>(ctx, tmap, p, wpc, mw, counter, *tail); break;
+            default: launch_fast<4, true>(ctx, tmap, p, wpc, mw, counter, *tail); break;
+        }
+        return true;
+    }
     switch (S) {
-        case 32: launch_fast<32>(ctx, tmap, p, wpc, mw, counter); break;
-        case 16: launch_fast<16>(ctx, tmap, p, wpc, mw, counter); break;
-        case 8: launch_fast<8>(ctx, tmap, p, wpc, mw, counter); break;
-        default: launch_fast<4>(ctx, tmap, p, wpc, mw, counter); break;
+        case 32: launch_fast<32, false>(ctx, tmap, p, wpc, mw, counter, none); break;
+        case 16: launch_fast<16, false>(ctx, tmap, p, wpc, mw, counter, none); break;
+        case 8: launch_fast<8, false>(ctx, tmap, p, wpc, mw, counter, none); break;
+        default: launch_fast<4, false>(ctx, tmap, p, wpc, mw, counter, none); break;
     }
     return true;
 }
