@@ -127,6 +127,10 @@ struct TermTables {
 };
 int build_term_tables(cdx_ctx* ctx, const uint32_t* ns, uint32_t count, TermTables* out);
 double host_term(uint32_t c, uint32_t n);
+// K1 for inputs with many distinct keys (k_intern.cu): dense first-seen ids of the trimmed
+// bytes with one thread per answer against one global table; no markers / hesitation
+int canon_intern_direct(cdx_ctx* ctx, const char* bytes, const uint64_t* offsets, uint64_t n, uint32_t* ids,
+                        uint64_t* first_index, uint64_t* n_unique);
 // stable LSD radix sort of (u64 key, u32 value) (k_gang.cu); lb = radix_scratch_words(n)
 // u32 of device scratch; *which = 1 when the result is in (k1, v1)
 size_t radix_scratch_words(uint64_t n);

@@ -961,6 +961,98 @@ __global__ void intern_remap(uint32_t* __restrict__ ids, uint64_t n, const uint3
     }
 }
 
+// ---- direct interning: one thread per answer against one global table ------------------
+// For inputs whose distinct keys are many (JSONL program ids: one id per ~P records), the
+// CTA-local tables and raw-answer caches of intern_ws fill and every answer takes the global
+// path anyway; this form goes there directly: pass 1 trims, hashes (8-byte words) and inserts
+// (CAS on the hash, atomicMin of the first index), pass 2 byte-verifies every answer against
+// its key's first occurrence (collisions reported, never merged) and flags first
+// occurrences, an exclusive scan of the flags gives the dense first-seen ids, pass 3 writes
+// them.  No markers, no hesitation flags.
+__device__ __forceinline__ uint64_t dload8(const uint8_t* __restrict__ a, uint64_t pos, uint64_t end) {
+    const uintptr_t base = reinterpret_cast<uintptr_t>(a);
+    const uintptr_t addr = base + pos, al = addr & ~static_cast<uintptr_t>(7);
+    if (al >= base && al + 16 <= base + end && pos + 8 <= end) {  // one aligned 16-byte window
+        const uint64_t w0 = *reinterpret_cast<const uint64_t*>(al);
+        const uint64_t w1 = *reinterpret_cast<const uint64_t*>(al + 8);
+        const uint32_t sh = static_cast<uint32_t>(addr & 7) * 8;
+        return sh ? (w0 >> sh) | (w1 << (64 - sh)) : w0;
+    }
+    uint64_t v = 0;
+    for (uint32_t k = 0; k < 8 && pos + k < end; ++k) v |= static_cast<uint64_t>(a[pos + k]) << (8 * k);
+    return v;
+}
+__device__ __forceinline__ void dtrim(const uint8_t* a, uint64_t& b, uint64_t& e) {
+    while (b < e && is_space(a[b])) ++b;
+    while (e > b && is_space(a[e - 1])) --e;
+}
+
+__global__ void intern_direct_insert(const uint8_t* __restrict__ arena, const uint64_t* __restrict__ off, uint64_t n,
+                                     unsigned long long* __restrict__ keys, uint32_t* __restrict__ first,
+                                     uint32_t* __restrict__ slot_of, uint64_t cap_mask, int* d_err) {
+    const uint64_t end = off[n];
+    for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+        uint64_t b = off[i], e = off[i + 1];
+        dtrim(arena, b, e);
+        const uint64_t len = e - b;
+        uint64_t h = 0xcbf29ce484222325ull ^ (len * 0x9E3779B97F4A7C15ull);
+        for (uint64_t q = 0; q < len; q += 8) {
+            const uint64_t m = len - q >= 8 ? ~0ull : (1ull << (8 * (len - q))) - 1ull;
+            h = mix(h, dload8(arena, b + q, end) & m);
+        }
+        h = fmix(h);
+        uint64_t sl = h & cap_mask;
+        for (uint64_t probes = 0;; ++probes) {
+            unsigned long long prev = __ldcg(keys + sl);  // most keys exist: no atomic to find them
+            if (prev == 0ull) prev = atomicCAS(keys + sl, 0ull, h);
+            if (prev == 0ull || prev == h) break;
+            sl = (sl + 1) & cap_mask;
+            if (probes > cap_mask) {
+                set_dev_err(d_err, DEV_INTERN_FULL);
+                break;
+            }
+        }
+        atomicMin(first + sl, static_cast<uint32_t>(i));
+        slot_of[i] = static_cast<uint32_t>(sl);
+    }
+}
+
+__global__ void intern_direct_verify(const uint8_t* __restrict__ arena, const uint64_t* __restrict__ off, uint64_t n,
+                                     const uint32_t* __restrict__ first, const uint32_t* __restrict__ slot_of,
+                                     uint32_t* __restrict__ is_first, int* d_err) {
+    const uint64_t end = off[n];
+    for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+        const uint32_t rep = first[slot_of[i]];
+        is_first[i] = rep == i ? 1u : 0u;
+        if (rep != i) {
+            uint64_t ab = off[i], ae = off[i + 1], bb = off[rep], be = off[rep + 1];
+            dtrim(arena, ab, ae);
+            dtrim(arena, bb, be);
+            const uint64_t len = ae - ab;
+            bool same = len == be - bb;
+            for (uint64_t k = 0; same && k < len; k += 8) {  // 8 bytes per compare
+                const uint64_t m = len - k >= 8 ? ~0ull : (1ull << (8 * (len - k))) - 1ull;
+                same = ((dload8(arena, ab + k, end) ^ dload8(arena, bb + k, end)) & m) == 0;
+            }
+            if (!same) set_dev_err(d_err, DEV_INTERN_COLLISION);
+        }
+    }
+}
+
+__global__ void intern_direct_finish(uint64_t n, const uint32_t* __restrict__ excl, const uint32_t* __restrict__ first,
+                                     const uint32_t* __restrict__ slot_of, uint32_t* __restrict__ ids,
+                                     unsigned long long* __restrict__ first_index) {
+    for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+        const uint32_t rep = first[slot_of[i]];
+        const uint32_t dense = excl[rep];  // first occurrences before rep = its dense id
+        ids[i] = dense;
+        if (rep == i && first_index) first_index[dense] = i;
+    }
+}
+
 }  // namespace
 }  // namespace cdx
 
@@ -1119,3 +1211,46 @@ extern "C" int cdx_canon_intern(cdx_ctx* ctx, const char* bytes, const uint64_t*
     }
     return set_error(ctx, CDX_ERUNTIME, "canon_intern: intern table full");
 }
+
+namespace cdx {
+int canon_intern_direct(cdx_ctx* ctx, const char* bytes, const uint64_t* offsets, uint64_t n, uint32_t* ids,
+                        uint64_t* first_index, uint64_t* n_unique) {
+    CDX_NVTX("canon_intern_direct");
+    if (!offsets || !ids || !n_unique) return set_error(ctx, CDX_EINVAL, "canon_intern: null pointer");
+    if (n >= 0xffffffffull) return set_error(ctx, CDX_EINVAL, "canon_intern: at most 2^32-2 answers per call");
+    *n_unique = 0;
+    if (n == 0) return CDX_OK;
+    if (!bytes) return set_error(ctx, CDX_EINVAL, "canon_intern: null pointer");
+    uint64_t cap = 1024;
+    while (cap < 2 * n) cap <<= 1;
+    const uint64_t nrec = (n + scan::SL_TILE - 1) / scan::SL_TILE + 2;  // scan tile records + ticket
+    const size_t bytes_need = cap * 8 + cap * 4 + n * 4 * 2 + 16 + nrec * 8 + 16;
+    uint8_t* s = static_cast<uint8_t*>(scratch(ctx, bytes_need));
+    if (!s) return set_error(ctx, CDX_ECUDA, "canon_intern: scratch allocation failed");
+    auto* keys = reinterpret_cast<unsigned long long*>(s);
+    auto* first = reinterpret_cast<uint32_t*>(s + cap * 8);
+    auto* slot_of = first + cap;
+    auto* flags = slot_of + n;
+    auto* rec = reinterpret_cast<uint64_t*>(reinterpret_cast<uintptr_t>(flags + n + 3) & ~static_cast<uintptr_t>(7));
+    auto* total = rec + nrec;
+    cudaMemsetAsync(keys, 0, cap * 8, ctx->stream);
+    cudaMemsetAsync(first, 0xff, cap * 4, ctx->stream);
+    const unsigned grid = static_cast<unsigned>(std::min<uint64_t>((n + 255) / 256, ctx->sm_count * 16ull));
+    const uint8_t* arena = reinterpret_cast<const uint8_t*>(bytes);
+    intern_direct_insert<<<grid, 256, 0, ctx->stream>>>(arena, offsets, n, keys, first, slot_of, cap - 1, ctx->d_err);
+    CDX_CHECK_LAUNCH(ctx, "canon_intern(direct insert)");
+    intern_direct_verify<<<grid, 256, 0, ctx->stream>>>(arena, offsets, n, first, slot_of, flags, ctx->d_err);
+    CDX_CHECK_LAUNCH(ctx, "canon_intern(direct verify)");
+    // first-occurrence flags -> exclusive prefix in place = dense first-seen ids
+    if (int st = scan::scan_excl(ctx, scan::LoadU32{flags}, n, flags, false, rec, total)) return st;
+    intern_direct_finish<<<grid, 256, 0, ctx->stream>>>(n, flags, first, slot_of, ids,
+                                                         reinterpret_cast<unsigned long long*>(first_index));
+    CDX_CHECK_LAUNCH(ctx, "canon_intern(direct finish)");
+    uint64_t* h_total = reinterpret_cast<uint64_t*>(ctx->h_small);
+    cudaError_t e = cudaMemcpyAsync(h_total, total, 8, cudaMemcpyDeviceToHost, ctx->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
+    if (e != cudaSuccess) return cuda_fail(ctx, e, "canon_intern");
+    *n_unique = *h_total;
+    return CDX_OK;
+}
+}  // namespace cdx

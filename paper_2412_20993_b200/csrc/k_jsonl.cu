@@ -24,6 +24,7 @@
 // in those fields is rejected ("unsupported number"), a documented restriction.
 
 #include <algorithm>
+#include <cstring>
 #include <climits>
 #include <string>
 #include <vector>
@@ -940,10 +941,17 @@ extern "C" int cdx_jsonl_parse(cdx_ctx* ctx, const char* text, uint64_t nbytes, 
         write_strings<<<gridn(ctx, n_lines), 128, 0, ctx->stream>>>(text, nbytes, o.st, pos, n_lines, o, pid_off, pid_arena,
                                                                     answer_off, answer_arena);
         CDX_CHECK_LAUNCH(ctx, "jsonl(strings)");
-        // exact program interning (sentinel-wrapped: trimming cannot merge ids)
+        // exact program interning (sentinel-wrapped: trimming cannot merge ids).  A trace holds
+        // one program id per ~P records, so most keys are distinct within any tile: the direct
+        // one-thread-per-record form (CDX_JSONL_INTERN=ws: K1's tiled serving kernel)
         uint64_t np = 0;
-        if (int st = cdx_canon_intern(ctx, pid_arena, pid_off, nr, nullptr, 0, program, nullptr, program_first, &np))
+        const char* iv = getenv("CDX_JSONL_INTERN");
+        if (iv && std::strcmp(iv, "ws") == 0) {
+            if (int st = cdx_canon_intern(ctx, pid_arena, pid_off, nr, nullptr, 0, program, nullptr, program_first, &np))
+                return st;
+        } else if (int st = canon_intern_direct(ctx, pid_arena, pid_off, nr, program, program_first, &np)) {
             return st;
+        }
         *n_programs = np;
         if (program_off && program_arena) {
             unwrap_pids<<<gridn(ctx, nr + 1), 256, 0, ctx->stream>>>(pid_off, pid_arena, nr, program_off, program_arena);

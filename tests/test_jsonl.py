@@ -65,9 +65,11 @@ def _category(msg):
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("intern", ["direct", "ws"])  # program-id interning: one thread per record | K1's tiled kernel
 @pytest.mark.parametrize("n,progs,seed", [(1, 1, 0), (200, 5, 1), (5000, 300, 2), (50000, 4000, 3),
                                            (1 << 20, 1 << 14, 5)])  # the last: config J's size
-def test_jsonl_matches_reference(ctx, n, progs, seed):
+def test_jsonl_matches_reference(ctx, monkeypatch, n, progs, seed, intern):
+    monkeypatch.setenv("CDX_JSONL_INTERN", intern)
     text = _gen_trace(n, progs, seed)
     ref = O.ref_parse_jsonl(text)
     got, pid, npg = _parse_gpu(ctx, text)
