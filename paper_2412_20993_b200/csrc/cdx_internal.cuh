@@ -78,6 +78,10 @@ struct cdx_ctx {
     uint8_t* sc_h = nullptr;
     uint8_t* sc_d = nullptr;
     size_t sc_cap = 0;
+    // the mixed step's side streams (k_mixed.cu): the archetype engines run concurrently
+    cudaStream_t aux[2] = {nullptr, nullptr};
+    cudaEvent_t ev_fork = nullptr, ev_join[2] = {nullptr, nullptr};
+    uint32_t sc_ctas_per_sm = 0;  // K2 fast path: resident CTAs per SM cap while sharing the GPU (0: none)
 };
 
 namespace cdx {

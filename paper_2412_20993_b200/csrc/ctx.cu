@@ -225,6 +225,11 @@ int cdx_ctx_destroy(cdx_ctx* ctx) {
     if (ctx->sc_d) cudaFree(ctx->sc_d);
     if (ctx->sc_counter) cudaFree(ctx->sc_counter);
     if (ctx->sc_h) cudaFreeHost(ctx->sc_h);
+    for (int q = 0; q < 2; ++q) {
+        if (ctx->aux[q]) cudaStreamDestroy(ctx->aux[q]);
+        if (ctx->ev_join[q]) cudaEventDestroy(ctx->ev_join[q]);
+    }
+    if (ctx->ev_fork) cudaEventDestroy(ctx->ev_fork);
     if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
     if (ctx->copy_stream) cudaStreamDestroy(ctx->copy_stream);
     delete ctx;

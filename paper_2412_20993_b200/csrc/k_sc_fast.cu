@@ -332,6 +332,7 @@ void launch_fast(cdx_ctx* ctx, const CUtensorMap& tmap, const ScParams& p, uint3
         oc = Occ{ctx->device, wpc, smem, per_sm};
     }
     if (per_sm < 1) per_sm = 1;
+    if (ctx->sc_ctas_per_sm && per_sm > static_cast<int>(ctx->sc_ctas_per_sm)) per_sm = static_cast<int>(ctx->sc_ctas_per_sm);
     const uint64_t want = (p.ngroups + wpc - 1) / wpc;
     const uint64_t grid = std::min<uint64_t>(want, static_cast<uint64_t>(ctx->sm_count) * per_sm);
     // claim 16 groups per atomic on large batches; fewer when that would leave warps idle

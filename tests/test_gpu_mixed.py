@@ -133,3 +133,46 @@ def test_mixed_then_gang_order(ctx):
     assert np.array_equal(order.cpu().numpy().view(np.uint32), ref)
     assert len(ref) == int((want["decision"] == 0).sum())
     del torch
+
+
+@pytest.mark.parametrize("serial", ["0", "1"])
+def test_mixed_concurrent_engines_and_graph(ctx, monkeypatch, serial):
+    """The archetype engines forked onto side streams (SC and reward rows present) and the
+    serial form (CDX_MIXED_SERIAL=1) give the oracle's decisions; the forked step captured as
+    a CUDA graph replays bit-identically (the fork / join are stream events)."""
+    import torch
+    from paper_2412_20993_b200 import AllocPolicy, Threshold
+    monkeypatch.setenv("CDX_MIXED_SERIAL", serial)
+    caps = (32, 16, 16, 64)
+    pols_o = [O.arch_policy(TH[a], (STATIC, KSTEP, STATIC, KSTEP)[a], (5, 3, 3, 4)[a], caps[a], (2, 1, 3, 1)[a],
+                            64 * (a + 1)) for a in range(4)]
+    arch, slot, host = _trace(30000, 21)
+    knob = synth.mixed_knobs(arch, caps, 21)
+    want = O.mixed_allocate(host, arch, slot, knob, pols_o)
+    got = _run(ctx, arch, slot, knob, host, pols_o)
+    for k in ("decision", "grant", "cap", "offsets"):
+        assert np.array_equal(got[k], want[k]), k
+    dev = {k: (_dev(v) if isinstance(v, np.ndarray) else v) for k, v in host.items() if v is not None}
+    pols = []
+    for a in range(4):
+        p = pols_o[a]
+        q = p.alloc
+        pols.append(([Threshold(p.th[i].signal, p.th[i].cutoff, p.th[i].dir) for i in range(p.n_th)],
+                     AllocPolicy(kind=q.kind, detect_at=q.detect_at, resource_cap=q.resource_cap,
+                                 recheck_every=q.recheck_every, tokens_per_unit=q.tokens_per_unit)))
+    a_d, s_d, k_d = _dev(arch), _dev(slot), _dev(knob)
+    n = arch.shape[0]
+    out = {k: torch.empty((n,), dtype=dt, device="cuda") for k, dt in
+           (("decision", torch.uint8), ("grant", torch.int32), ("cap", torch.int32), ("offsets", torch.int64))}
+    out["total"] = torch.empty((1,), dtype=torch.int64, device="cuda")
+    ctx.mixed_allocate(dev, a_d, s_d, k_d, pols, out=out)  # warm (tables, occupancy caches)
+    ctx.sync()
+    graph = ctx.graph_capture(lambda: ctx.mixed_allocate(dev, a_d, s_d, k_d, pols, out=out))
+    for _ in range(2):
+        for v in out.values():
+            v.fill_(-1) if v.dtype != torch.uint8 else v.fill_(255)
+        graph()
+        ctx.sync()
+        for k in ("decision", "grant", "cap", "offsets"):
+            assert np.array_equal(out[k].cpu().numpy(), want[k]), k
+        assert int(out["total"][0]) == want["total"]
