@@ -379,12 +379,17 @@ constexpr size_t WS_SMEM = WS_ST * WS_STAGE + sizeof(WsShared);
 
 // A local entry found under creation is published by a thread of this CTA within a global
 // round trip: wait for it (bounded) rather than repeat its global insert.
+// A true return is followed by a CTA fence: the entry's fields (written before its creator's
+// fence and flag store) are read after the flag was seen.
 __device__ __forceinline__ bool entry_ready(WsShared& S, int e) {
-    for (int spin = 0; spin < 64; ++spin) {
-        if (ld_volatile(&S.lt_info[e].w)) return true;
-        __nanosleep(128);
+    bool ready = false;
+    for (int spin = 0; spin < 64 && !ready; ++spin) {
+        ready = ld_volatile(&S.lt_info[e].w) != 0u;
+        if (!ready) __nanosleep(128);
     }
-    return ld_volatile(&S.lt_info[e].w) != 0u;
+    ready = ready || ld_volatile(&S.lt_info[e].w) != 0u;
+    if (ready) __threadfence_block();
+    return ready;
 }
 
 // The miss path of one answer: trim, hash, hesitation, local/global key, verify, cache.
