@@ -1258,16 +1258,13 @@ __global__ void __launch_bounds__(PG_THREADS, 1) gang_order_persistent(const PgA
             }
             __syncthreads();  // the staging buffers are consumed: fetch the next tile behind this one
             if (tid == 0 && tb + PG_TILE < re) issue(tb + PG_TILE, re);
-            {  // quarter sums over warps
-                const uint32_t d = tid & 255u, q = tid >> 8;
-                uint32_t sq = 0;
-#pragma unroll
-                for (int w = 0; w < PG_WARPS / 4; ++w) sq += wcnt[q * (PG_WARPS / 4) + w][d];
-                s_q[q][d] = sq;
-            }
-            __syncthreads();
+            // thread d < 256: the tile's count of digit d over the warps, the digit scan, then the
+            // warps' first tile-sorted index per digit (two CTA barriers)
             uint32_t cnt = 0;
-            if (tid < 256) cnt = s_q[0][tid] + s_q[1][tid] + s_q[2][tid] + s_q[3][tid];
+            if (tid < 256) {
+#pragma unroll 8
+                for (int w = 0; w < PG_WARPS; ++w) cnt += wcnt[w][tid];
+            }
             const uint32_t incl = warp_incl_scan(cnt, lane);
             if (lane == 31 && warp < 8) s_ws[warp] = incl;
             __syncthreads();
@@ -1275,20 +1272,14 @@ __global__ void __launch_bounds__(PG_THREADS, 1) gang_order_persistent(const PgA
                 uint32_t wpre = 0;
                 for (uint32_t w = 0; w < warp; ++w) wpre += s_ws[w];
                 const uint32_t toff = wpre + incl - cnt;
-                s_toff[tid] = toff;
                 s_gb[tid] = s_base[tid] - toff;  // global position = s_gb[digit] + tile-sorted index
                 s_base[tid] += cnt;
                 if (tid == 255) s_sc[1] = wpre + incl;
-            }
-            __syncthreads();
-            {  // wcnt[w][d] = first tile-sorted index of warp w's digit-d keys
-                const uint32_t d = tid & 255u, q = tid >> 8;
-                uint32_t run = s_toff[d];
-                for (uint32_t qq = 0; qq < q; ++qq) run += s_q[qq][d];
-#pragma unroll
-                for (int w = 0; w < PG_WARPS / 4; ++w) {
-                    const uint32_t x = wcnt[q * (PG_WARPS / 4) + w][d];
-                    wcnt[q * (PG_WARPS / 4) + w][d] = run;
+                uint32_t run = toff;  // wcnt[w][d] = first tile-sorted index of warp w's digit-d keys
+#pragma unroll 8
+                for (int w = 0; w < PG_WARPS; ++w) {
+                    const uint32_t x = wcnt[w][tid];
+                    wcnt[w][tid] = run;
                     run += x;
                 }
             }
