@@ -393,3 +393,40 @@ def test_gang_errors(ctx):
     soa["arrival"][3] = -1.0
     with pytest.raises(CdxInvalidArgument, match="finite and >= 0"):
         ctx.gang_priority(_to_dev(soa), InterPolicy(order=1, starvation_limit=1.0), now)
+
+
+@pytest.mark.parametrize("trial", range(24))
+def test_gang_persistent_fuzz(ctx, trial):
+    """Randomised traces through the one-launch order: sizes around tile (8192) and CTA-range
+    boundaries, real-valued estimates (low halves differ: the run fix-up), integer-valued ones
+    (low halves equal: fix-up skipped), FIFO and SJF, few to all escalated, duplicate keys,
+    explicit program ids; every result against the oracle."""
+    from paper_2412_20993_b200 import InterPolicy
+    rng = np.random.default_rng(1000 + trial)
+    N = int(rng.choice([1, 2, 7, 8191, 8192, 8193, 20000, 148 * 8192 + 5, 300001, 1 << 20]))
+    order = int(rng.integers(0, 2))
+    limit = float(rng.choice([0.05, 0.5, 5.0, 1e9]))
+    arrival = np.cumsum(rng.exponential(1e-3, N))
+    if rng.random() < 0.3:
+        arrival = np.round(arrival, 2)  # runs of equal arrivals: the id decides
+    now = float(arrival[-1]) + float(rng.uniform(0.0, 2.0))
+    last = np.minimum(now, arrival + rng.exponential(limit, N))
+    cnt = rng.integers(0, 6, N).astype(np.uint32)
+    if rng.random() < 0.5:
+        sums = (rng.integers(1, 2000, N) * cnt).astype(np.int64)  # integer means
+    else:
+        sums = (rng.integers(0, 5000, N) * (cnt + (rng.random(N) < 0.5))).astype(np.int64)  # real means
+    cap = rng.integers(1, 64, N).astype(np.int32)
+    knob = np.minimum(cap, rng.integers(0, 64, N)).astype(np.int32)
+    term = (rng.random(N) < float(rng.choice([0.0, 0.2, 0.9]))).astype(np.uint8)
+    soa = dict(arrival=arrival, last_service=last, iter_tok_sum=sums, iter_count=cnt, knob=knob, cap=cap,
+               terminated=term)
+    if rng.random() < 0.3 and N > 1:
+        soa["program_id"] = (np.arange(N, dtype=np.uint64) * 3 + 11).astype(np.uint32)  # increasing ids
+    prior = float(rng.choice([128.0, 1.5, 1e6]))
+    got, esc, _ = ctx.gang_priority(_to_dev(soa), InterPolicy(order=order, starvation_limit=limit, prior_tokens=prior),
+                                    now, want_escalated=True)
+    ctx.sync()
+    ref, resc = O.gang_order(soa, order, limit, prior, now)
+    assert np.array_equal(esc.cpu().numpy(), resc)
+    assert np.array_equal(got.cpu().numpy().view(np.uint32), ref)
