@@ -831,15 +831,16 @@ constexpr uint32_t PG_DEAD = 0xffffffffu;
 constexpr int PG_FEW = 24;  // never a live upper half: a finite key's exponent is <= 0x7fe
 // dynamic shared memory: sk, sv, stk, stv [PG_TILE] (phase 0: the program-field ring) | wcnt
 // [PG_WARPS][256] | s_q [4][256] | s_red [4][256] | s_base, s_gb, s_toff [256] | s_ws [32] |
-// scalars [16] | mbarriers [4]
+// scalars [16] | mbarriers [PG_NST + 1]
 // Phase 0 ring: PG_NST stages of PG_CH programs, every SoA field bulk-copied (arrival, last
 // service, token sum: 8 B; count, knob, cap, id: 4 B; terminated: 1 B)
-constexpr int PG_CH = 1024, PG_NST = 3;
+constexpr int PG_CH = 1024, PG_NST = 3;  // (6 x 512 with two chunks per step measured slower: 40 -> 52 us)
 constexpr int PG_ST_ARR = 0, PG_ST_LS = PG_CH * 8, PG_ST_SUM = PG_CH * 16, PG_ST_CNT = PG_CH * 24,
               PG_ST_KNOB = PG_CH * 28, PG_ST_CAP = PG_CH * 32, PG_ST_TERM = PG_CH * 36, PG_ST_PID = PG_CH * 37,
               PG_ST_BYTES = PG_CH * 41;
 static_assert(PG_NST * PG_ST_BYTES <= PG_TILE * 16, "the phase-0 ring lives in the tile buffers");
-constexpr int PG_SMEM = PG_TILE * 16 + PG_WARPS * 256 * 4 + 2 * 4 * 256 * 4 + 3 * 256 * 4 + 32 * 4 + 16 * 4 + 32;
+constexpr int PG_SMEM = PG_TILE * 16 + PG_WARPS * 256 * 4 + 2 * 4 * 256 * 4 + 3 * 256 * 4 + 32 * 4 + 16 * 4 +
+                        8 * (PG_NST + 1);  // + the mbarriers
 
 struct PgArgs {
     GangParams p;
@@ -928,8 +929,8 @@ __global__ void __launch_bounds__(PG_THREADS, 1) gang_order_persistent(const PgA
     uint32_t* s_toff = s_gb + 256;
     uint32_t* s_ws = s_toff + 256;
     uint32_t* s_sc = s_ws + 32;  // [0] live count, [1] tile live count, [2..6] reduced phase-0 record
-    uint64_t* bars = reinterpret_cast<uint64_t*>(s_sc + 16);  // [0..2] phase-0 ring, [3] tile staging
-    uint64_t* bar = bars + 3;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(s_sc + 16);  // [0, PG_NST) phase-0 ring, [PG_NST] tile staging
+    uint64_t* bar = bars + PG_NST;
     const GangParams& p = a.p;
     const uint32_t G = gridDim.x, c = blockIdx.x, tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
     const uint32_t lt = (1u << lane) - 1u;
@@ -946,7 +947,7 @@ __global__ void __launch_bounds__(PG_THREADS, 1) gang_order_persistent(const PgA
         a.misc[4] = 0;
     }
     if (tid == 0) {
-        for (int q = 0; q < 4; ++q) mbar_init(bars + q, 1);
+        for (int q = 0; q <= PG_NST; ++q) mbar_init(bars + q, 1);
         fence_mbar_init();
     }
     __syncthreads();
